@@ -1,0 +1,254 @@
+/*
+ * lc_b200.h -- C ABI of the B200-native Logits-Cache re-sampling path.
+ *
+ * This is the drop-in boundary for the reference's logits-cache interface
+ * (reference: /root/reference/pkg/src/agentserve).  The
+ * reference exposes that interface as in-process Python (no FFI); the entry
+ * points below are what a binding of that interface needs, each one citing
+ * the reference function it replaces.  INTEGRATION.md shows the ctypes
+ * binding the reference side would add.
+ *
+ * Conventions
+ *   - every function returns an int status (lc_status); nothing throws across
+ *     the ABI; lc_last_error() describes the last failure on this thread;
+ *   - pointers named d_* are DEVICE pointers on the handle's device; h_* are
+ *     host pointers;
+ *   - `stream` is a cudaStream_t passed as void* (NULL = legacy default
+ *     stream); calls are asynchronous on that stream unless documented as
+ *     synchronising;
+ *   - a cache handle is single-threaded: the caller serialises calls (the
+ *     reference serialises every cache access under InferenceEngine._lock,
+ *     engine.py:113, 267-268).
+ */
+#ifndef LC_B200_H
+#define LC_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define LC_ABI_VERSION 1
+
+typedef enum lc_status {
+  LC_OK = 0,
+  LC_E_CONFIG = 1,    /* -> agentserve.errors.ConfigError (errors.py:6) */
+  LC_E_ZERO_MASS = 2, /* -> RuntimeError (sampling.py:101-102) */
+  LC_E_CAPACITY = 3,  /* slab pages or entry slots exhausted */
+  LC_E_CUDA = 4,      /* CUDA runtime failure (lc_last_error has the text) */
+  LC_E_ARG = 5        /* bad argument (null pointer, negative size ...) */
+} lc_status;
+
+typedef enum lc_dtype { LC_F32 = 0, LC_BF16 = 1 } lc_dtype;
+
+/* per-draw flags written by the resample entry points */
+#define LC_DRAW_PRECISE 1u    /* decided by the fp64 precise pass (fast path uncertain) */
+#define LC_DRAW_UNRESOLVED 2u /* even the precise pass could not certify the decision */
+#define LC_DRAW_BAD_ROW 4u    /* non-finite maximum / NaN logits: token = -1 */
+
+int lc_abi_version(void);
+const char* lc_status_string(int status);
+const char* lc_last_error(void);
+
+/* ------------------------------------------------------------------ mixing
+ * Bit-exact integer primitives (determinism.md:14-92).                    */
+
+/* Rolling prefix hash, one digest per prompt: digest[i] = hash_tokens(
+ * tokens[offsets[i] .. offsets[i+1]), start = parent ? parent[i] : EMPTY_HASH).
+ * Replaces StateKey.of (logits_cache.py:31-32) -> hash_tokens (mixing.py:68-73)
+ * and its O(1) prefix extension (fold_token, mixing.py:63-65).               */
+int lc_hash_prefix(const int32_t* d_tokens, const int64_t* d_offsets, const uint64_t* d_parent,
+                   int64_t n_prompts, uint64_t* d_out, void* stream);
+
+/* u[i] = RngStream(seeds[i]).next_float() at draw index index[i]
+ * (mixing.py:81-98).                                                          */
+int lc_uniforms(const uint64_t* d_seeds, const int64_t* d_index, int64_t n, double* d_out, void* stream);
+
+/* Synthetic logits producer (reference model.py:67-83 / kernels.py:47-71 /
+ * _mixcore.pyx:27-40): row r = fill_logits(states[r], vocab, conc, range),
+ * written as dtype (bf16 = RNE of the fp32 value) at d_out + r*row_stride.   */
+int lc_fill_logits(const uint64_t* d_states, int64_t n_rows, int64_t vocab, double concentration,
+                   double logit_range, int dtype, void* d_out, int64_t row_stride, void* stream);
+
+/* ---------------------------------------------------------------- resample
+ * One task = one logits row + sampling parameters + a range of draws that
+ * share the row (Best-of-N siblings at the same position share it).  Token
+ * decision per draw = sample(truncate(softmax(z, T), top_k, top_p), u)
+ * (sampling.py:57-109), bit-exact given the same u.                          */
+typedef struct lc_task {
+  int64_t row;        /* row index into `rows` (row_stride elements apart); -1 = cache (slot,pos) */
+  int32_t slot;       /* cache entry slot (lc_cache_resample only) */
+  int32_t pos;        /* position inside the cached trajectory */
+  double temperature; /* SamplingConfig.temperature (>= 0) */
+  int32_t top_k;      /* <= 0: none (SamplingConfig.top_k None) */
+  int32_t vocab;      /* <= 0: the row width passed to the call */
+  double top_p;       /* (0, 1] */
+  int64_t draw_begin; /* draws [draw_begin, draw_end) of this task */
+  int64_t draw_end;
+  int64_t seed_base;  /* seed mode: draw d uses d_seed[seed_base + d - draw_begin] */
+  int64_t u_index;    /* seed mode: RngStream draw number (< 0: use pos, the step-wise index) */
+} lc_task;
+
+/* Draw source, one of:
+ *   d_u != NULL                 u = d_u[draw]                       (FixedUniform)
+ *   d_u == NULL, d_index != 0   u = RngStream(d_seed[draw]) draw number d_index[draw]
+ *   d_u == NULL, d_index == 0   u = RngStream(d_seed[task.seed_base + draw - draw_begin])
+ *                               draw number task.u_index (or task.pos)
+ * RngStream values are computed on the device bit-exactly (mixing.py:91-98). */
+typedef struct lc_draws {
+  const double* d_u;
+  const uint64_t* d_seed;
+  const int64_t* d_index;
+  int32_t* d_token; /* out */
+  uint8_t* d_flags; /* out, LC_DRAW_* (may be NULL) */
+} lc_draws;
+
+/* Bytes of scratch the resample entry points need for n_tasks tasks. */
+int64_t lc_resample_workspace_bytes(int64_t n_tasks, int64_t vocab);
+
+/* Resample rows of a plain device array.  d_counters (may be NULL) receives
+ * int64 {tasks sent to the precise pass, unresolved draws, bad rows}
+ * accumulated (atomicAdd) on the device.                                      */
+int lc_resample(const void* d_rows, int dtype, int64_t vocab, int64_t row_stride, const lc_task* d_tasks,
+                int64_t n_tasks, lc_draws draws, void* d_workspace, int64_t workspace_bytes,
+                int64_t* d_counters, void* stream);
+
+/* Inverse-CDF draw over explicit fp64 probability rows (sampling.py:97-109):
+ * token[r] for row r with uniform u[r]; zero mass -> token -1 and flag. */
+int lc_draw_probs(const double* d_probs, int64_t vocab, int64_t n_rows, int64_t row_stride, const double* d_u,
+                  int32_t* d_token, uint8_t* d_flags, void* stream);
+
+/* truncate() on explicit fp64 probability rows (sampling.py:71-94): top-k
+ * (k <= 0: none) then nucleus on the untruncated mass, renormalised, written
+ * to d_out (zeros outside the kept set).  d_scratch: n_rows*vocab*12 + 256
+ * bytes.  top_k <= 0 and top_p == 1 is the identity (the caller may skip). */
+int lc_truncate_probs(const double* d_probs, int64_t vocab, int64_t n_rows, int64_t row_stride, int32_t top_k,
+                      double top_p, double* d_out, void* d_scratch, void* stream);
+
+/* softmax at temperature T (sampling.py:57-68) into fp64 probabilities, with
+ * the reference's operation order (f64 divide, subtract max, exp, divide by
+ * numpy's pairwise sum).                                                      */
+int lc_softmax(const void* d_rows, int dtype, int64_t vocab, int64_t row_stride, int64_t n_rows,
+               const double* d_temperature, double* d_out, void* stream);
+
+/* Per-row entropy (nats) and max probability of softmax(z, T), the hotspot
+ * scores' inputs (sampling.py:112-126).                                       */
+int lc_row_entropy(const void* d_rows, int dtype, int64_t vocab, int64_t row_stride, int64_t n_rows,
+                   double temperature, double* d_entropy, double* d_pmax, void* stream);
+
+/* ------------------------------------------------------------------- cache
+ * HBM-resident replacement of LogitsCache (logits_cache.py:73-183):
+ * an open-addressing digest -> slot index, a slab of [pages x page_rows x
+ * vocab] rows (fp32 or bf16), the reference's LRU-by-last-hit eviction over
+ * accounted bytes n*V*4 + 8*n (logits_cache.py:54-56, 128-140) and pins.     */
+typedef struct lc_cache lc_cache;
+
+typedef struct lc_cache_config {
+  int64_t vocab;          /* slab row width (entries may be narrower) */
+  int32_t dtype;          /* lc_dtype of the slab */
+  int32_t page_rows;      /* rows per page (>= 1) */
+  int64_t key_capacity;   /* max live entries */
+  int64_t page_capacity;  /* pages in the slab */
+  int32_t max_pages;      /* max pages per entry (bounds trajectory length) */
+  int32_t device;         /* CUDA device ordinal */
+  int64_t budget_bytes;   /* accounted-byte budget (LogitsCache(budget_bytes)) */
+} lc_cache_config;
+
+typedef struct lc_cache_stats {
+  int64_t entries;      /* len(cache) */
+  int64_t total_bytes;  /* accounted, logits_cache.py:78 */
+  int64_t budget_bytes;
+  int64_t lookups;      /* logits_cache.py:82 */
+  int64_t hits;
+  int64_t inserts;
+  int64_t evictions;
+  int64_t clock;        /* _hit_clock, logits_cache.py:79 */
+  int64_t free_pages;
+  int64_t free_slots;
+  int64_t error;        /* latched lc_status from inside insert batches (cleared on read) */
+} lc_cache_stats;
+
+int lc_cache_create(const lc_cache_config* cfg, lc_cache** out);
+int lc_cache_destroy(lc_cache* cache);
+
+/* LogitsCache.lookup for a batch (logits_cache.py:87-94) in index order:
+ * out_slot = -1 on a miss; hits tick the clock in index order.  out_len,
+ * out_vocab, out_gen describe the hit entry (may be NULL).                    */
+int lc_cache_lookup(lc_cache* cache, const uint64_t* d_digests, int64_t n, int32_t* d_slot, uint32_t* d_gen,
+                    int32_t* d_len, int32_t* d_vocab, void* stream);
+
+/* LogitsCache.update for a batch (logits_cache.py:96-140), applied in index
+ * order: entry i has d_lengths[i] rows, row t being d_rows[(d_row_offsets[i] +
+ * t) * rows_stride ...] (rows_dtype, first d_vocabs[i] columns; converted to
+ * the slab dtype with round-to-nearest-even) and token d_tokens[d_row_offsets[i]
+ * + t].  Accounted bytes are n*V*4 + 8*n whatever the slab dtype
+ * (logits_cache.py:54-56).  max_len (host) = max(d_lengths) sizes the copy grid.
+ * d_slot/d_gen receive the (slot, generation) of the entry each insert created;
+ * a later insert or an eviction in the same batch may already have replaced it.
+ * Errors inside the batch (entry wider than the slab: LC_E_CONFIG, exhausted
+ * slots/pages: LC_E_CAPACITY) are latched and reported by lc_cache_stats_get. */
+int lc_cache_insert(lc_cache* cache, const uint64_t* d_digests, const int32_t* d_lengths, const int32_t* d_vocabs,
+                    int64_t n, const void* d_rows, int32_t rows_dtype, int64_t rows_stride,
+                    const int64_t* d_row_offsets, const int32_t* d_tokens, int32_t max_len, int32_t* d_slot,
+                    uint32_t* d_gen, void* stream);
+
+/* pin/unpin (logits_cache.py:145-149) by (slot, generation) handles; a
+ * handle whose entry was overwritten or evicted is ignored (the reference
+ * pins the old entry object).  delta = +1 pin, -1 unpin.                     */
+int lc_cache_pin(lc_cache* cache, const int32_t* d_slot, const uint32_t* d_gen, int64_t n, int32_t delta,
+                 void* stream);
+
+/* Copy cached rows (slot, pos) out as out_dtype (entry.logits_seq[pos]). */
+int lc_cache_gather(lc_cache* cache, const int32_t* d_slot, const int32_t* d_pos, int64_t n, void* d_out,
+                    int32_t out_dtype, int64_t out_stride, void* stream);
+/* Cached tokens (entry.token_seq[pos]). */
+int lc_cache_tokens(lc_cache* cache, const int32_t* d_slot, const int32_t* d_pos, int64_t n, int32_t* d_out,
+                    void* stream);
+
+/* Resample cached rows: tasks use (slot, pos) with row = -1. */
+int lc_cache_resample(lc_cache* cache, const lc_task* d_tasks, int64_t n_tasks, lc_draws draws, void* d_workspace,
+                      int64_t workspace_bytes, int64_t* d_counters, void* stream);
+
+/* Fused replay helpers (engine.py:296-331 for a batch of requests x branches).
+ * lc_replay_tasks: request r (slot d_slot[r] from lc_cache_lookup, -1 = miss,
+ * trajectory length d_len[r]) replays positions t < min(d_len[r], max_pos);
+ * task r*max_pos + t resamples cached row (slot, t) for the request's n_branch
+ * branches with draws [(r*max_pos + t)*n_branch, +n_branch), branch b using
+ * seed d_seeds[r*n_branch + b] at draw number t (step-wise: one draw per
+ * position, engine.py:301-310).  Positions past the limit get empty draw
+ * ranges.  d_temperature/d_top_k/d_top_p are per request.                    */
+int lc_replay_tasks(const int32_t* d_slot, const int32_t* d_len, int64_t n_req, int32_t max_pos, int32_t n_branch,
+                    const double* d_temperature, const int32_t* d_top_k, const double* d_top_p, lc_task* d_tasks,
+                    void* stream);
+/* Step-wise acceptance: for request r, branch b, the replay keeps positions up
+ * to and including the first sampled token that differs from the cached one
+ * (engine.py:305-310).  d_tokens is the draw-indexed output of the resample;
+ * d_cached[r*max_pos + t] the cached tokens (lc_cache_tokens).  Writes
+ * replayed_len and diverged_at (-1 = none) per (r, b).                        */
+int lc_replay_accept(const int32_t* d_tokens, const int32_t* d_cached, const int32_t* d_len, int64_t n_req,
+                     int32_t max_pos, int32_t n_branch, int32_t* d_replayed, int32_t* d_diverged, void* stream);
+
+/* Test probe: the FAST tier's exponential e(z) ~ exp((z - m)/T) for given z,
+ * so tests can measure its error bound against fp64 (not on the hot path). */
+int lc_probe_fast_exp(const float* d_z, int64_t n, float m, double temperature, float* d_out, void* stream);
+
+/* Synchronising: copy the counters out. */
+int lc_cache_stats_get(lc_cache* cache, lc_cache_stats* h_out, void* stream);
+
+/* Slab geometry (for callers that resample slab rows through lc_resample). */
+int lc_cache_slab(lc_cache* cache, void** d_base, int64_t* row_stride, int32_t* dtype);
+/* Copy per-slot entry metadata out (any pointer may be NULL):
+ * digest u64, last_hit u64, generation u32, pins i32, rows i32, vocab i32,
+ * alive u8 -- arrays of key_capacity elements.  Used by tests (slot parity with
+ * the oracle) and by CachedTrajectory's lazy fields.                          */
+int lc_cache_snapshot(lc_cache* cache, uint64_t* d_digest, unsigned long long* d_last_hit, uint32_t* d_gen,
+                      int32_t* d_pins, int32_t* d_nrows, int32_t* d_vocab, uint8_t* d_alive, void* stream);
+/* Page table [key_capacity][max_pages] (-1 = unused), for fused consumers. */
+int lc_cache_page_table(lc_cache* cache, const int32_t** d_pages, int32_t* max_pages, int32_t* page_rows);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* LC_B200_H */

@@ -1,0 +1,755 @@
+// K3 (digest -> slot index) + K4 (HBM slab) + the reference's eviction policy.
+//
+// Reference: pkg/src/agentserve/logits_cache.py
+//   lookup            :87-94   lookups += 1; hit -> clock += 1, last_hit = clock, hits += 1
+//   update            :96-126  overwrite subtracts old bytes, NEW entry (pins reset),
+//                              clock += 1, last_hit = clock, bytes += n*V*4 + 8n
+//   _evict_over_budget:128-140 while total > budget and len > 1: evict the unpinned
+//                              entry with min (last_hit, digest); stop if all pinned
+//   pin / unpin       :145-149
+//
+// Design:
+//   * index: open addressing, linear probing, 2x over-provisioned, probed by
+//     tiles of 8 lanes reading 8 consecutive buckets per round; deletion by
+//     backward shift (no tombstones);
+//   * last_hit values are unique clock ticks, so min (last_hit, digest) is the
+//     entry with the oldest tick.  Every tick appends (clock, slot) to an event
+//     ring; the ring tail is the LRU end.  An event is live iff the slot is
+//     alive and its last_hit still equals the event's clock (lazy deletion).
+//     Pinned events met at the tail move to a side list (they are older than
+//     everything left in the ring and are re-checked first);
+//   * a batch of inserts is applied in index order by one sequential "policy"
+//     thread (the semantics are sequential); row copies into the slab run in
+//     parallel afterwards, only for entries still alive at the end of the batch;
+//   * slots and pages come from LIFO free stacks -- the discipline restated in
+//     oracle/cache_ref.py, so slot and page indices are bit-exact vs the oracle.
+#include <cub/cub.cuh>
+#include <new>
+#include <vector>
+
+#include "lc_common.cuh"
+#include "lc_resample.cuh"
+
+namespace lcb {
+
+struct Ctl {
+  long long total_bytes;
+  long long budget;
+  long long clock;
+  long long lookups;
+  long long hits;
+  long long inserts;
+  long long evictions;
+  long long ring_head;  // positions grow monotonically; index = pos % R
+  long long ring_tail;
+  int alive;
+  int free_slot_top;
+  int free_page_top;
+  int side_count;
+  int error;  // first lc_status raised inside a kernel (sticky until read)
+};
+
+struct CacheDev {
+  Ctl* ctl;
+  uint64_t* hkeys;
+  int32_t* hvals;  // slot, -1 empty
+  uint32_t hmask;
+  uint64_t* digest;
+  unsigned long long* last_hit;
+  uint32_t* gen;
+  int32_t* pins;
+  int32_t* nrows;
+  int32_t* vocab;
+  uint8_t* alive;
+  long long* nbytes;
+  int32_t* pages;       // [E][maxp]
+  int32_t* free_slots;  // stack
+  int32_t* free_pages;  // stack
+  int32_t* tokens;      // [P * page_rows]
+  char* slab;           // [P * page_rows * V] of dtype
+  unsigned long long* ring_clock;
+  int32_t* ring_slot;
+  long long R;
+  unsigned long long* side_clock;
+  int32_t* side_slot;
+  int side_cap;
+  int E, P, maxp, page_rows, V, dtype;
+};
+
+__device__ __forceinline__ uint32_t home_bucket(uint64_t d, uint32_t mask) {
+  return (uint32_t)((d ^ (d >> 29) ^ (d >> 47)) & mask);
+}
+
+// ---- lookup ----------------------------------------------------------------------------------
+
+// 8-lane tiles, one key per tile; each round a tile reads 8 consecutive buckets.
+__global__ void lookup_probe_kernel(CacheDev c, const uint64_t* __restrict__ dig, int64_t n, int32_t* __restrict__ out) {
+  const int64_t key = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 3;
+  const int sub = threadIdx.x & 7;
+  const int lane = threadIdx.x & 31;
+  const unsigned tile_bits = 0xffu << (lane & 24);
+  const bool active = key < n;
+  const uint64_t d = active ? dig[key] : 0ull;
+  const uint32_t start = home_bucket(d, c.hmask);
+  int result = -1;
+  bool done = !active;
+  for (uint32_t round = 0; __any_sync(0xffffffffu, !done); ++round) {
+    bool match = false, empty = false;
+    if (!done) {
+      uint32_t b = (start + round * 8u + sub) & c.hmask;
+      int32_t v = c.hvals[b];
+      match = v >= 0 && c.hkeys[b] == d;
+      empty = v < 0;
+      if (match) result = v;
+      if (round * 8u > c.hmask) empty = true;  // table full safety
+    }
+    unsigned mm = __ballot_sync(0xffffffffu, match) & tile_bits;
+    unsigned em = __ballot_sync(0xffffffffu, empty) & tile_bits;
+    if (!done) {
+      if (mm) {
+        result = __shfl_sync(tile_bits, result, __ffs(mm) - 1, 32);
+        done = true;
+      } else if (em) {
+        // linear probing: the key cannot lie past the first empty bucket --
+        // unless a match sits before it inside this round (handled above)
+        result = -1;
+        done = true;
+      }
+    }
+  }
+  if (active && sub == 0) out[key] = result;
+}
+
+// In-order commit of a lookup batch: hit ranks -> clock ticks, last_hit, ring events.
+__global__ void __launch_bounds__(1024) lookup_commit_kernel(CacheDev c, const int32_t* __restrict__ slot, int64_t n,
+                                                             uint32_t* gen_out, int32_t* len_out, int32_t* vocab_out,
+                                                             int32_t* slot_out) {
+  typedef cub::BlockScan<int, 1024> Scan;
+  __shared__ typename Scan::TempStorage tmp;
+  __shared__ long long s_clock, s_head;
+  if (threadIdx.x == 0) {
+    s_clock = c.ctl->clock;
+    s_head = c.ctl->ring_head;
+  }
+  __syncthreads();
+  for (int64_t b0 = 0; b0 < n; b0 += 1024) {
+    const int64_t i = b0 + threadIdx.x;
+    const int s = i < n ? slot[i] : -1;
+    const int hit = s >= 0;
+    int rank, total;
+    Scan(tmp).ExclusiveSum(hit, rank, total);
+    if (hit) {
+      const unsigned long long ck = (unsigned long long)(s_clock + rank + 1);
+      atomicMax(&c.last_hit[s], ck);
+      const long long pos = (s_head + rank) % c.R;
+      c.ring_clock[pos] = ck;
+      c.ring_slot[pos] = s;
+    }
+    if (i < n) {
+      if (slot_out) slot_out[i] = s;
+      if (gen_out) gen_out[i] = hit ? c.gen[s] : 0u;
+      if (len_out) len_out[i] = hit ? c.nrows[s] : 0;
+      if (vocab_out) vocab_out[i] = hit ? c.vocab[s] : 0;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      s_clock += total;
+      s_head += total;
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    c.ctl->lookups += n;
+    c.ctl->hits += s_clock - c.ctl->clock;
+    c.ctl->clock = s_clock;
+    c.ctl->ring_head = s_head;
+  }
+}
+
+// ---- sequential policy thread helpers ------------------------------------------------------
+
+__device__ int table_find(const CacheDev& c, uint64_t d) {
+  uint32_t b = home_bucket(d, c.hmask);
+  for (uint32_t k = 0; k <= c.hmask; ++k, b = (b + 1) & c.hmask) {
+    int v = c.hvals[b];
+    if (v < 0) return -1;
+    if (c.hkeys[b] == d) return v;
+  }
+  return -1;
+}
+
+__device__ void table_insert(const CacheDev& c, uint64_t d, int s) {
+  uint32_t b = home_bucket(d, c.hmask);
+  while (c.hvals[b] >= 0) b = (b + 1) & c.hmask;
+  c.hkeys[b] = d;
+  c.hvals[b] = s;
+}
+
+__device__ void table_delete(const CacheDev& c, uint64_t d) {
+  uint32_t i = home_bucket(d, c.hmask);
+  for (;;) {
+    int v = c.hvals[i];
+    if (v < 0) return;
+    if (c.hkeys[i] == d) break;
+    i = (i + 1) & c.hmask;
+  }
+  uint32_t j = i;
+  for (;;) {
+    j = (j + 1) & c.hmask;
+    if (c.hvals[j] < 0) break;
+    uint32_t k = home_bucket(c.hkeys[j], c.hmask);
+    bool stays = (i <= j) ? (i < k && k <= j) : (i < k || k <= j);
+    if (stays) continue;
+    c.hkeys[i] = c.hkeys[j];
+    c.hvals[i] = c.hvals[j];
+    i = j;
+  }
+  c.hvals[i] = -1;
+}
+
+__device__ __forceinline__ bool event_live(const CacheDev& c, int s, unsigned long long ck) {
+  return c.alive[s] && c.last_hit[s] == ck;
+}
+
+// Oldest live unpinned entry, consuming it from the side list or the ring tail.
+__device__ int next_victim(const CacheDev& c) {
+  Ctl* ctl = c.ctl;
+  // side list (already in clock order): drop stale entries, take the first unpinned
+  int w = 0, found = -1;
+  for (int j = 0; j < ctl->side_count; ++j) {
+    int s = c.side_slot[j];
+    unsigned long long ck = c.side_clock[j];
+    if (!event_live(c, s, ck)) continue;
+    if (found < 0 && c.pins[s] == 0) {
+      found = s;
+      continue;
+    }
+    c.side_slot[w] = s;
+    c.side_clock[w] = ck;
+    ++w;
+  }
+  ctl->side_count = w;
+  if (found >= 0) return found;
+  while (ctl->ring_tail < ctl->ring_head) {
+    long long pos = ctl->ring_tail % c.R;
+    int s = c.ring_slot[pos];
+    unsigned long long ck = c.ring_clock[pos];
+    ctl->ring_tail++;
+    if (!event_live(c, s, ck)) continue;
+    if (c.pins[s] > 0) {
+      if (ctl->side_count < c.side_cap) {
+        c.side_slot[ctl->side_count] = s;
+        c.side_clock[ctl->side_count] = ck;
+        ctl->side_count++;
+      } else {
+        ctl->error = LC_E_CAPACITY;  // too many pinned entries to track
+      }
+      continue;
+    }
+    return s;
+  }
+  return -1;
+}
+
+__device__ void push_pages(const CacheDev& c, int s) {
+  Ctl* ctl = c.ctl;
+  for (int k = 0; k < c.maxp; ++k) {
+    int pg = c.pages[(int64_t)s * c.maxp + k];
+    if (pg < 0) break;
+    c.free_pages[ctl->free_page_top++] = pg;
+    c.pages[(int64_t)s * c.maxp + k] = -1;
+  }
+}
+
+__device__ void evict_entry(const CacheDev& c, int s) {
+  Ctl* ctl = c.ctl;
+  table_delete(c, c.digest[s]);
+  ctl->total_bytes -= c.nbytes[s];
+  push_pages(c, s);
+  c.free_slots[ctl->free_slot_top++] = s;
+  c.gen[s] += 1u;
+  c.alive[s] = 0;
+  ctl->alive -= 1;
+  ctl->evictions += 1;
+}
+
+// One thread applies the batch in index order (logits_cache.py:96-140).
+__global__ void insert_policy_kernel(CacheDev c, const uint64_t* __restrict__ dig, const int32_t* __restrict__ lens,
+                                     const int32_t* __restrict__ vocabs, int64_t n, int32_t* out_slot,
+                                     uint32_t* out_gen) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  Ctl* ctl = c.ctl;
+  for (int64_t i = 0; i < n; ++i) {
+    const uint64_t d = dig[i];
+    const int nr = lens[i];
+    const int vv = vocabs[i];
+    const int np = (nr + c.page_rows - 1) / c.page_rows;
+    out_slot[i] = -1;
+    out_gen[i] = 0;
+    if (nr < 0 || vv < 1 || vv > c.V || np > c.maxp) {
+      if (!ctl->error) ctl->error = LC_E_CONFIG;
+      continue;
+    }
+    const long long bytes = (long long)nr * vv * 4 + 8ll * nr;  // logits_cache.py:54-56
+    int s = table_find(c, d);
+    if (s >= 0) {  // overwrite: the key keeps its slot, the entry is new
+      ctl->total_bytes -= c.nbytes[s];
+      push_pages(c, s);
+      c.gen[s] += 1u;
+    } else {
+      if (ctl->free_slot_top == 0) {
+        if (!ctl->error) ctl->error = LC_E_CAPACITY;
+        continue;
+      }
+      s = c.free_slots[--ctl->free_slot_top];
+      table_insert(c, d, s);
+      c.alive[s] = 1;
+      ctl->alive += 1;
+    }
+    if (ctl->free_page_top < np) {
+      if (!ctl->error) ctl->error = LC_E_CAPACITY;
+      // keep the index consistent: an entry without rows cannot be replayed
+      c.nrows[s] = 0;
+      c.nbytes[s] = 0;
+      continue;
+    }
+    for (int k = 0; k < np; ++k) c.pages[(int64_t)s * c.maxp + k] = c.free_pages[--ctl->free_page_top];
+    ctl->clock += 1;
+    c.last_hit[s] = (unsigned long long)ctl->clock;
+    c.pins[s] = 0;
+    c.nrows[s] = nr;
+    c.vocab[s] = vv;
+    c.nbytes[s] = bytes;
+    c.digest[s] = d;
+    {
+      long long pos = ctl->ring_head % c.R;
+      c.ring_clock[pos] = (unsigned long long)ctl->clock;
+      c.ring_slot[pos] = s;
+      ctl->ring_head++;
+    }
+    ctl->total_bytes += bytes;
+    ctl->inserts += 1;
+    out_slot[i] = s;
+    out_gen[i] = c.gen[s];
+    while (ctl->total_bytes > ctl->budget && ctl->alive > 1) {
+      int v = next_victim(c);
+      if (v < 0) break;
+      evict_entry(c, v);
+    }
+  }
+}
+
+// Copy the rows/tokens of inserts whose entry is still alive at the end of the batch.
+template <typename SrcT, typename DstT>
+__global__ void insert_copy_kernel(CacheDev c, const int32_t* __restrict__ lens, const int32_t* __restrict__ vocabs,
+                                   const char* __restrict__ src, int64_t src_stride, const int64_t* __restrict__ offs,
+                                   const int32_t* __restrict__ toks, const int32_t* __restrict__ out_slot,
+                                   const uint32_t* __restrict__ out_gen, int64_t i0) {
+  const int64_t i = i0 + blockIdx.y;
+  const int s = out_slot[i];
+  if (s < 0 || !c.alive[s] || c.gen[s] != out_gen[i]) return;
+  const int nr = lens[i], vv = vocabs[i];
+  for (int t = blockIdx.x; t < nr; t += gridDim.x) {
+    const int pg = c.pages[(int64_t)s * c.maxp + t / c.page_rows];
+    const int64_t slab_row = (int64_t)pg * c.page_rows + t % c.page_rows;
+    const SrcT* srow = reinterpret_cast<const SrcT*>(src) + (offs[i] + t) * src_stride;
+    DstT* drow = reinterpret_cast<DstT*>(c.slab) + slab_row * (int64_t)c.V;
+    if (threadIdx.x == 0) c.tokens[slab_row] = toks ? toks[offs[i] + t] : 0;
+    const bool same = sizeof(SrcT) == sizeof(DstT);
+    const bool al = ((reinterpret_cast<uintptr_t>(srow) | reinterpret_cast<uintptr_t>(drow)) & 15) == 0;
+    if (same && al) {
+      const int per = 16 / sizeof(DstT);
+      const int nv = vv / per;
+      for (int k = threadIdx.x; k < nv; k += blockDim.x)
+        reinterpret_cast<uint4*>(drow)[k] = __ldg(reinterpret_cast<const uint4*>(srow) + k);
+      for (int k = nv * per + threadIdx.x; k < vv; k += blockDim.x) drow[k] = reinterpret_cast<const DstT*>(srow)[k];
+    } else {
+      for (int k = threadIdx.x; k < vv; k += blockDim.x) {
+        float f;
+        if (sizeof(SrcT) == 4) f = reinterpret_cast<const float*>(srow)[k];
+        else f = bf16_bits_to_f32(reinterpret_cast<const uint16_t*>(srow)[k]);
+        if (sizeof(DstT) == 4) reinterpret_cast<float*>(drow)[k] = f;
+        else reinterpret_cast<uint16_t*>(drow)[k] = f32_to_bf16_bits(f);
+      }
+    }
+  }
+}
+
+__global__ void pin_kernel(CacheDev c, const int32_t* __restrict__ slot, const uint32_t* __restrict__ gen, int64_t n,
+                           int delta) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  int s = slot[i];
+  if (s < 0 || s >= c.E) return;
+  if (c.alive[s] && c.gen[s] == gen[i]) atomicAdd(&c.pins[s], delta);
+}
+
+template <typename DstT>
+__global__ void gather_kernel(CacheDev c, const int32_t* __restrict__ slot, const int32_t* __restrict__ pos, int64_t n,
+                              DstT* out, int64_t out_stride) {
+  const int64_t i = blockIdx.x;
+  if (i >= n) return;
+  const int s = slot[i], t = pos[i];
+  DstT* o = out + i * out_stride;
+  bool ok = s >= 0 && s < c.E && c.alive[s] && t >= 0 && t < c.nrows[s];
+  const int vv = ok ? c.vocab[s] : 0;
+  const int64_t slab_row =
+      ok ? (int64_t)c.pages[(int64_t)s * c.maxp + t / c.page_rows] * c.page_rows + t % c.page_rows : 0;
+  for (int k = threadIdx.x; k < out_stride; k += blockDim.x) {
+    float f = 0.0f;
+    if (ok && k < vv) {
+      if (c.dtype == LC_F32) f = reinterpret_cast<const float*>(c.slab)[slab_row * c.V + k];
+      else f = bf16_bits_to_f32(reinterpret_cast<const uint16_t*>(c.slab)[slab_row * c.V + k]);
+    }
+    if (sizeof(DstT) == 4) reinterpret_cast<float*>(o)[k] = f;
+    else reinterpret_cast<uint16_t*>(o)[k] = f32_to_bf16_bits(f);
+  }
+}
+
+__global__ void tokens_kernel(CacheDev c, const int32_t* __restrict__ slot, const int32_t* __restrict__ pos, int64_t n,
+                              int32_t* out) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  int s = slot[i], t = pos[i];
+  if (s < 0 || s >= c.E || !c.alive[s] || t < 0 || t >= c.nrows[s]) {
+    out[i] = -1;
+    return;
+  }
+  int64_t slab_row = (int64_t)c.pages[(int64_t)s * c.maxp + t / c.page_rows] * c.page_rows + t % c.page_rows;
+  out[i] = c.tokens[slab_row];
+}
+
+// Ring compaction: rebuild the ring from live entries sorted by last_hit.
+__global__ void compact_keys_kernel(CacheDev c, unsigned long long* keys, int32_t* vals) {
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= c.E) return;
+  keys[i] = c.alive[i] ? c.last_hit[i] : ~0ull;
+  vals[i] = i;
+}
+
+__global__ void compact_write_kernel(CacheDev c, const unsigned long long* keys, const int32_t* vals) {
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  int alive = c.ctl->alive;
+  if (i < alive) {
+    c.ring_clock[i] = keys[i];
+    c.ring_slot[i] = vals[i];
+  }
+  if (i == 0) {
+    c.ctl->ring_tail = 0;
+    c.ctl->ring_head = alive;
+    c.ctl->side_count = 0;
+  }
+}
+
+__global__ void init_kernel(CacheDev c) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t k = i; k <= (int64_t)c.hmask; k += stride) c.hvals[k] = -1;
+  for (int64_t k = i; k < c.E; k += stride) {
+    c.free_slots[k] = c.E - 1 - (int)k;  // pop order 0, 1, 2, ... (oracle/cache_ref.py)
+    c.alive[k] = 0;
+    c.gen[k] = 0;
+    c.pins[k] = 0;
+    c.nrows[k] = 0;
+    c.last_hit[k] = 0;
+  }
+  for (int64_t k = i; k < (int64_t)c.E * c.maxp; k += stride) c.pages[k] = -1;
+  for (int64_t k = i; k < c.P; k += stride) c.free_pages[k] = c.P - 1 - (int)k;
+}
+
+}  // namespace lcb
+
+using namespace lcb;
+
+struct lc_cache {
+  lc_cache_config cfg;
+  CacheDev dev;
+  Ctl* d_ctl;
+  void* sort_tmp;
+  size_t sort_tmp_bytes;
+  unsigned long long* sort_keys[2];
+  int32_t* sort_vals[2];
+  int32_t* d_probe;  // lookup probe results
+  int64_t probe_cap;
+  long long ring_bound;  // host upper bound of ring occupancy
+  std::vector<void*> allocs;
+};
+
+static int cache_alloc(lc_cache* c, void** p, size_t bytes) {
+  cudaError_t e = cudaMalloc(p, bytes ? bytes : 16);
+  if (e != cudaSuccess) {
+    lcb_set_last_error(cudaGetErrorString(e), __FILE__, __LINE__);
+    return LC_E_CUDA;
+  }
+  c->allocs.push_back(*p);
+  return LC_OK;
+}
+
+extern "C" int lc_cache_destroy(lc_cache* c) {
+  if (!c) return LC_OK;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  cudaSetDevice(c->cfg.device);
+  cudaDeviceSynchronize();
+  for (void* p : c->allocs) cudaFree(p);
+  cudaSetDevice(dev);
+  delete c;
+  return LC_OK;
+}
+
+extern "C" int lc_cache_create(const lc_cache_config* cfg, lc_cache** out) {
+  if (!cfg || !out) return LC_E_ARG;
+  *out = nullptr;
+  if (cfg->vocab < 1 || cfg->vocab > (1 << 28) || (cfg->dtype != LC_F32 && cfg->dtype != LC_BF16) ||
+      cfg->page_rows < 1 || cfg->key_capacity < 1 || cfg->key_capacity > (1 << 30) || cfg->page_capacity < 1 ||
+      cfg->page_capacity > (1ll << 31) - 1 || cfg->max_pages < 1 || cfg->budget_bytes < 0)
+    return LC_E_CONFIG;
+  LCB_CUDA_TRY(cudaSetDevice(cfg->device));
+  lc_cache* c = new (std::nothrow) lc_cache();
+  if (!c) return LC_E_CAPACITY;
+  c->cfg = *cfg;
+  CacheDev& d = c->dev;
+  d.E = (int)cfg->key_capacity;
+  d.P = (int)cfg->page_capacity;
+  d.maxp = cfg->max_pages;
+  d.page_rows = cfg->page_rows;
+  d.V = (int)cfg->vocab;
+  d.dtype = cfg->dtype;
+  uint32_t H = 16;
+  while (H < 2u * (uint32_t)d.E) H <<= 1;
+  d.hmask = H - 1;
+  d.R = 4ll * d.E + 4096;
+  d.side_cap = d.E < 65536 ? d.E : 65536;
+  const size_t esz = cfg->dtype == LC_F32 ? 4 : 2;
+  int rc = 0;
+#define ALLOC(ptr, n)                                                     \
+  do {                                                                    \
+    rc = cache_alloc(c, (void**)&(ptr), (size_t)(n) * sizeof(*(ptr)));    \
+    if (rc) {                                                             \
+      lc_cache_destroy(c);                                                \
+      return rc;                                                          \
+    }                                                                     \
+  } while (0)
+  ALLOC(c->d_ctl, 1);
+  d.ctl = c->d_ctl;
+  ALLOC(d.hkeys, H);
+  ALLOC(d.hvals, H);
+  ALLOC(d.digest, d.E);
+  ALLOC(d.last_hit, d.E);
+  ALLOC(d.gen, d.E);
+  ALLOC(d.pins, d.E);
+  ALLOC(d.nrows, d.E);
+  ALLOC(d.vocab, d.E);
+  ALLOC(d.alive, d.E);
+  ALLOC(d.nbytes, d.E);
+  ALLOC(d.pages, (int64_t)d.E * d.maxp);
+  ALLOC(d.free_slots, d.E);
+  ALLOC(d.free_pages, d.P);
+  ALLOC(d.tokens, (int64_t)d.P * d.page_rows);
+  rc = cache_alloc(c, (void**)&d.slab, (size_t)d.P * d.page_rows * d.V * esz);
+  if (rc) {
+    lc_cache_destroy(c);
+    return LC_E_CAPACITY;
+  }
+  ALLOC(d.ring_clock, d.R);
+  ALLOC(d.ring_slot, d.R);
+  ALLOC(d.side_clock, d.side_cap);
+  ALLOC(d.side_slot, d.side_cap);
+  for (int k = 0; k < 2; ++k) {
+    ALLOC(c->sort_keys[k], d.E);
+    ALLOC(c->sort_vals[k], d.E);
+  }
+  c->sort_tmp_bytes = 0;
+  cub::DeviceRadixSort::SortPairs(nullptr, c->sort_tmp_bytes, c->sort_keys[0], c->sort_keys[1], c->sort_vals[0],
+                                  c->sort_vals[1], d.E);
+  rc = cache_alloc(c, &c->sort_tmp, c->sort_tmp_bytes);
+  if (rc) {
+    lc_cache_destroy(c);
+    return rc;
+  }
+  c->probe_cap = 0;
+  c->d_probe = nullptr;
+#undef ALLOC
+  Ctl h{};
+  h.budget = cfg->budget_bytes;
+  h.free_slot_top = d.E;
+  h.free_page_top = d.P;
+  LCB_CUDA_TRY(cudaMemcpy(c->d_ctl, &h, sizeof(Ctl), cudaMemcpyHostToDevice));
+  init_kernel<<<1024, 256>>>(d);
+  LCB_CUDA_TRY(cudaGetLastError());
+  LCB_CUDA_TRY(cudaDeviceSynchronize());
+  c->ring_bound = 0;
+  *out = c;
+  return LC_OK;
+}
+
+static int ensure_ring(lc_cache* c, int64_t incoming, cudaStream_t st) {
+  if (c->ring_bound + incoming <= c->dev.R) return LC_OK;
+  CacheDev& d = c->dev;
+  compact_keys_kernel<<<ceil_div(d.E, 256), 256, 0, st>>>(d, c->sort_keys[0], c->sort_vals[0]);
+  LCB_CUDA_TRY(cudaGetLastError());
+  size_t tb = c->sort_tmp_bytes;
+  LCB_CUDA_TRY(cub::DeviceRadixSort::SortPairs(c->sort_tmp, tb, c->sort_keys[0], c->sort_keys[1], c->sort_vals[0],
+                                               c->sort_vals[1], d.E, 0, 64, st));
+  compact_write_kernel<<<ceil_div(d.E, 256), 256, 0, st>>>(d, c->sort_keys[1], c->sort_vals[1]);
+  LCB_CUDA_TRY(cudaGetLastError());
+  c->ring_bound = d.E;
+  if (c->ring_bound + incoming > d.R) return LC_E_CAPACITY;  // batch larger than the ring
+  return LC_OK;
+}
+
+extern "C" int lc_cache_lookup(lc_cache* c, const uint64_t* d_digests, int64_t n, int32_t* d_slot, uint32_t* d_gen,
+                               int32_t* d_len, int32_t* d_vocab, void* stream) {
+  if (!c || n < 0 || (n > 0 && (!d_digests || !d_slot))) return LC_E_ARG;
+  if (n == 0) return LC_OK;
+  cudaStream_t st = (cudaStream_t)stream;
+  int rc = ensure_ring(c, n, st);
+  if (rc) return rc;
+  const int threads = 256;
+  lookup_probe_kernel<<<ceil_div(n * 8, threads), threads, 0, st>>>(c->dev, d_digests, n, d_slot);
+  LCB_CUDA_TRY(cudaGetLastError());
+  lookup_commit_kernel<<<1, 1024, 0, st>>>(c->dev, d_slot, n, d_gen, d_len, d_vocab, nullptr);
+  LCB_CUDA_TRY(cudaGetLastError());
+  c->ring_bound += n;
+  return LC_OK;
+}
+
+extern "C" int lc_cache_insert(lc_cache* c, const uint64_t* d_digests, const int32_t* d_lengths,
+                               const int32_t* d_vocabs, int64_t n, const void* d_rows, int32_t rows_dtype,
+                               int64_t rows_stride, const int64_t* d_row_offsets, const int32_t* d_tokens,
+                               int32_t max_len, int32_t* d_slot, uint32_t* d_gen, void* stream) {
+  if (!c || n < 0) return LC_E_ARG;
+  if (n == 0) return LC_OK;
+  if (!d_digests || !d_lengths || !d_vocabs || !d_slot || !d_gen || !d_row_offsets) return LC_E_ARG;
+  if (max_len > 0 && !d_rows) return LC_E_ARG;
+  if (rows_dtype != LC_F32 && rows_dtype != LC_BF16) return LC_E_ARG;
+  cudaStream_t st = (cudaStream_t)stream;
+  int rc = ensure_ring(c, n, st);
+  if (rc) return rc;
+  insert_policy_kernel<<<1, 32, 0, st>>>(c->dev, d_digests, d_lengths, d_vocabs, n, d_slot, d_gen);
+  LCB_CUDA_TRY(cudaGetLastError());
+  c->ring_bound += n;
+  if (max_len > 0) {
+    const int bx = max_len < 64 ? max_len : 64;
+    for (int64_t i0 = 0; i0 < n; i0 += 65535) {
+      const int ny = (int)((n - i0) < 65535 ? (n - i0) : 65535);
+      dim3 grid(bx, ny);
+      const char* src = (const char*)d_rows;
+      if (rows_dtype == LC_F32 && c->cfg.dtype == LC_F32)
+        insert_copy_kernel<float, float><<<grid, 256, 0, st>>>(c->dev, d_lengths, d_vocabs, src, rows_stride,
+                                                               d_row_offsets, d_tokens, d_slot, d_gen, i0);
+      else if (rows_dtype == LC_F32)
+        insert_copy_kernel<float, uint16_t><<<grid, 256, 0, st>>>(c->dev, d_lengths, d_vocabs, src, rows_stride,
+                                                                  d_row_offsets, d_tokens, d_slot, d_gen, i0);
+      else if (c->cfg.dtype == LC_BF16)
+        insert_copy_kernel<uint16_t, uint16_t><<<grid, 256, 0, st>>>(c->dev, d_lengths, d_vocabs, src, rows_stride,
+                                                                     d_row_offsets, d_tokens, d_slot, d_gen, i0);
+      else
+        insert_copy_kernel<uint16_t, float><<<grid, 256, 0, st>>>(c->dev, d_lengths, d_vocabs, src, rows_stride,
+                                                                  d_row_offsets, d_tokens, d_slot, d_gen, i0);
+      LCB_CUDA_TRY(cudaGetLastError());
+    }
+  }
+  return LC_OK;
+}
+
+extern "C" int lc_cache_pin(lc_cache* c, const int32_t* d_slot, const uint32_t* d_gen, int64_t n, int32_t delta,
+                            void* stream) {
+  if (!c || n < 0 || (n > 0 && (!d_slot || !d_gen))) return LC_E_ARG;
+  if (n == 0) return LC_OK;
+  pin_kernel<<<ceil_div(n, 256), 256, 0, (cudaStream_t)stream>>>(c->dev, d_slot, d_gen, n, delta);
+  LCB_CUDA_TRY(cudaGetLastError());
+  return LC_OK;
+}
+
+extern "C" int lc_cache_gather(lc_cache* c, const int32_t* d_slot, const int32_t* d_pos, int64_t n, void* d_out,
+                               int32_t out_dtype, int64_t out_stride, void* stream) {
+  if (!c || n < 0 || (n > 0 && (!d_slot || !d_pos || !d_out)) || out_stride < 1) return LC_E_ARG;
+  if (n == 0) return LC_OK;
+  cudaStream_t st = (cudaStream_t)stream;
+  for (int64_t i0 = 0; i0 < n; i0 += (1 << 30)) {
+    int64_t nn = n - i0 < (1 << 30) ? n - i0 : (1 << 30);
+    if (out_dtype == LC_F32)
+      gather_kernel<float><<<(unsigned)nn, 256, 0, st>>>(c->dev, d_slot + i0, d_pos + i0, nn,
+                                                         (float*)d_out + i0 * out_stride, out_stride);
+    else
+      gather_kernel<uint16_t><<<(unsigned)nn, 256, 0, st>>>(c->dev, d_slot + i0, d_pos + i0, nn,
+                                                            (uint16_t*)d_out + i0 * out_stride, out_stride);
+    LCB_CUDA_TRY(cudaGetLastError());
+  }
+  return LC_OK;
+}
+
+extern "C" int lc_cache_tokens(lc_cache* c, const int32_t* d_slot, const int32_t* d_pos, int64_t n, int32_t* d_out,
+                               void* stream) {
+  if (!c || n < 0 || (n > 0 && (!d_slot || !d_pos || !d_out))) return LC_E_ARG;
+  if (n == 0) return LC_OK;
+  tokens_kernel<<<ceil_div(n, 256), 256, 0, (cudaStream_t)stream>>>(c->dev, d_slot, d_pos, n, d_out);
+  LCB_CUDA_TRY(cudaGetLastError());
+  return LC_OK;
+}
+
+extern "C" int lc_cache_resample(lc_cache* c, const lc_task* d_tasks, int64_t n_tasks, lc_draws draws,
+                                 void* d_workspace, int64_t workspace_bytes, int64_t* d_counters, void* stream) {
+  if (!c) return LC_E_ARG;
+  return lcb::resample_launch(c->dev.slab, c->dev.dtype, c->dev.V, c->dev.V, d_tasks, n_tasks, draws, c->dev.pages,
+                              c->dev.maxp, c->dev.page_rows, d_workspace, workspace_bytes, d_counters,
+                              (cudaStream_t)stream);
+}
+
+extern "C" int lc_cache_stats_get(lc_cache* c, lc_cache_stats* out, void* stream) {
+  if (!c || !out) return LC_E_ARG;
+  Ctl h;
+  cudaStream_t st = (cudaStream_t)stream;
+  LCB_CUDA_TRY(cudaMemcpyAsync(&h, c->d_ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, st));
+  LCB_CUDA_TRY(cudaStreamSynchronize(st));
+  out->entries = h.alive;
+  out->total_bytes = h.total_bytes;
+  out->budget_bytes = h.budget;
+  out->lookups = h.lookups;
+  out->hits = h.hits;
+  out->inserts = h.inserts;
+  out->evictions = h.evictions;
+  out->clock = h.clock;
+  out->free_pages = h.free_page_top;
+  out->free_slots = h.free_slot_top;
+  out->error = h.error;
+  if (h.error) {
+    int zero = 0;
+    LCB_CUDA_TRY(cudaMemcpyAsync(&c->d_ctl->error, &zero, sizeof(int), cudaMemcpyHostToDevice, st));
+    LCB_CUDA_TRY(cudaStreamSynchronize(st));
+  }
+  return LC_OK;
+}
+
+extern "C" int lc_cache_slab(lc_cache* c, void** d_base, int64_t* row_stride, int32_t* dtype) {
+  if (!c) return LC_E_ARG;
+  if (d_base) *d_base = c->dev.slab;
+  if (row_stride) *row_stride = c->dev.V;
+  if (dtype) *dtype = c->dev.dtype;
+  return LC_OK;
+}
+
+extern "C" int lc_cache_page_table(lc_cache* c, const int32_t** d_pages, int32_t* max_pages, int32_t* page_rows) {
+  if (!c) return LC_E_ARG;
+  if (d_pages) *d_pages = c->dev.pages;
+  if (max_pages) *max_pages = c->dev.maxp;
+  if (page_rows) *page_rows = c->dev.page_rows;
+  return LC_OK;
+}
+
+extern "C" int lc_cache_snapshot(lc_cache* c, uint64_t* d_digest, unsigned long long* d_last_hit, uint32_t* d_gen,
+                                 int32_t* d_pins, int32_t* d_nrows, int32_t* d_vocab, uint8_t* d_alive,
+                                 void* stream) {
+  if (!c) return LC_E_ARG;
+  cudaStream_t st = (cudaStream_t)stream;
+  const size_t E = (size_t)c->dev.E;
+  if (d_digest) LCB_CUDA_TRY(cudaMemcpyAsync(d_digest, c->dev.digest, E * 8, cudaMemcpyDeviceToDevice, st));
+  if (d_last_hit) LCB_CUDA_TRY(cudaMemcpyAsync(d_last_hit, c->dev.last_hit, E * 8, cudaMemcpyDeviceToDevice, st));
+  if (d_gen) LCB_CUDA_TRY(cudaMemcpyAsync(d_gen, c->dev.gen, E * 4, cudaMemcpyDeviceToDevice, st));
+  if (d_pins) LCB_CUDA_TRY(cudaMemcpyAsync(d_pins, c->dev.pins, E * 4, cudaMemcpyDeviceToDevice, st));
+  if (d_nrows) LCB_CUDA_TRY(cudaMemcpyAsync(d_nrows, c->dev.nrows, E * 4, cudaMemcpyDeviceToDevice, st));
+  if (d_vocab) LCB_CUDA_TRY(cudaMemcpyAsync(d_vocab, c->dev.vocab, E * 4, cudaMemcpyDeviceToDevice, st));
+  if (d_alive) LCB_CUDA_TRY(cudaMemcpyAsync(d_alive, c->dev.alive, E, cudaMemcpyDeviceToDevice, st));
+  return LC_OK;
+}

@@ -1,0 +1,108 @@
+// Shared device primitives for the B200 logits-cache re-sampling path.
+//
+// Bit-exact 64-bit mixing follows the reference contract
+// (pkg/docs/determinism.md:14-92, pkg/src/agentserve/mixing.py:43-105).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <cuda_bf16.h>
+#include <stdint.h>
+
+#include "../../include/lc_b200.h"
+
+namespace lcb {
+
+constexpr uint64_t kGolden = 0x9E3779B97F4A7C15ull;   // mixing.py:29
+constexpr uint64_t kMult1 = 0xBF58476D1CE4E5B9ull;    // mixing.py:30
+constexpr uint64_t kMult2 = 0x94D049BB133111EBull;    // mixing.py:31
+constexpr uint64_t kEmptyHash = 0xA0761D6478BD642Full; // mixing.py:34
+constexpr uint64_t kPeakSalt = 0x8BB84B93962EACC9ull;  // mixing.py:36
+constexpr uint64_t kSamplerSalt = 0x2545F4914F6CDD1Dull; // mixing.py:38
+
+__host__ __device__ __forceinline__ uint64_t avalanche64(uint64_t z) {
+  z ^= z >> 30;
+  z *= kMult1;
+  z ^= z >> 27;
+  z *= kMult2;
+  z ^= z >> 31;
+  return z;
+}
+
+__host__ __device__ __forceinline__ uint64_t stream_u64(uint64_t state, uint64_t i) {
+  return avalanche64(state + (i + 1) * kGolden);
+}
+
+__host__ __device__ __forceinline__ double unit_float(uint64_t u) {
+  return (double)(u >> 11) * 0x1.0p-53;  // exact: 53-bit integer times 2^-53
+}
+
+__host__ __device__ __forceinline__ uint64_t fold_token(uint64_t h, int64_t t) {
+  return avalanche64(h ^ (uint64_t)(t + 1));
+}
+
+// RngStream(seed)'s i-th next_float() (mixing.py:91-98).
+__host__ __device__ __forceinline__ double request_uniform(uint64_t seed, uint64_t i) {
+  return unit_float(stream_u64(avalanche64(seed ^ kSamplerSalt), i));
+}
+
+// ---- small utilities -------------------------------------------------------------
+
+__device__ __forceinline__ float bf16_bits_to_f32(uint16_t b) {
+  return __uint_as_float(((uint32_t)b) << 16);
+}
+
+// fp32 -> bf16 round-to-nearest-even (NaN kept quiet).
+__device__ __forceinline__ uint16_t f32_to_bf16_bits(float f) {
+  uint32_t u = __float_as_uint(f);
+  if ((u & 0x7fffffffu) > 0x7f800000u) return (uint16_t)((u >> 16) | 0x40);
+  u += 0x7fffu + ((u >> 16) & 1u);
+  return (uint16_t)(u >> 16);
+}
+
+// Monotone map float -> uint32 (larger float -> larger key; -0 < +0 handled as
+// equal magnitude ordering is irrelevant because -0 == +0 never both matter).
+__device__ __forceinline__ uint32_t f32_order_key(float f) {
+  uint32_t u = __float_as_uint(f);
+  return (u & 0x80000000u) ? ~u : (u | 0x80000000u);
+}
+
+template <typename T>
+__device__ __forceinline__ T warp_sum(T v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+__device__ __forceinline__ float warp_max(float v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+
+__device__ __forceinline__ int warp_min_int(int v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = min(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+
+// ex2.approx.ftz.f32 -- the MUFU exponential (SFU pipe).
+__device__ __forceinline__ float ex2_approx(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
+inline int ceil_div(int64_t a, int64_t b) { return (int)((a + b - 1) / b); }
+
+}  // namespace lcb
+
+#define LCB_CUDA_TRY(expr)                                   \
+  do {                                                       \
+    cudaError_t _e = (expr);                                 \
+    if (_e != cudaSuccess) {                                 \
+      lcb_set_last_error(cudaGetErrorString(_e), __FILE__, __LINE__); \
+      return LC_E_CUDA;                                      \
+    }                                                        \
+  } while (0)
+
+void lcb_set_last_error(const char* msg, const char* file, int line);

@@ -1,0 +1,260 @@
+// Probability-level entry points of the reference sampler API
+// (sampling.py:57-126): softmax into fp64 probabilities, the inverse-CDF draw
+// on an explicit probability vector, and the per-row entropy / max-prob used by
+// hotspot scoring.  These serve the drop-in Python functions
+// (paper_2604_17353_b200.sampling); the hot path is the fused lc_resample.
+#include <math.h>
+
+#include "lc_common.cuh"
+#include "lc_numpy.cuh"
+
+namespace lcb {
+
+constexpr int PB_THREADS = 256;
+
+template <int DT>
+__device__ __forceinline__ float ld(const char* row, int64_t i) {
+  if (DT == LC_BF16) return bf16_bits_to_f32(reinterpret_cast<const uint16_t*>(row)[i]);
+  return reinterpret_cast<const float*>(row)[i];
+}
+
+__device__ float block_max(float v, float* red) {
+  v = warp_max(v);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
+  __syncthreads();
+  float r = -INFINITY;
+  for (int w = 0; w < PB_THREADS / 32; ++w) r = fmaxf(r, red[w]);
+  __syncthreads();
+  return r;
+}
+
+__device__ double block_sum(double v, double* red) {
+  v = warp_sum(v);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
+  __syncthreads();
+  double r = 0.0;
+  for (int w = 0; w < PB_THREADS / 32; ++w) r += red[w];
+  __syncthreads();
+  return r;
+}
+
+// softmax: s = f64(z)/T - max (sampling.py:65-66), e = exp(s), p = e / pairwise_sum(e)
+template <int DT>
+__global__ void __launch_bounds__(PB_THREADS)
+softmax_kernel(const char* rows, int64_t row_bytes, int64_t V, const double* temps, double* out) {
+  __shared__ float fred[PB_THREADS / 32];
+  __shared__ double s_S;
+  const char* row = rows + blockIdx.x * row_bytes;
+  double* o = out + blockIdx.x * V;
+  const double T = temps[blockIdx.x];
+  float m = -INFINITY;
+  for (int64_t i = threadIdx.x; i < V; i += PB_THREADS) m = fmaxf(m, ld<DT>(row, i));
+  m = block_max(m, fred);
+  if (T == 0.0) {  // one-hot at the first argmax (sampling.py:61-64)
+    __shared__ int s_arg;
+    if (threadIdx.x == 0) {
+      int a = 0;
+      while (ld<DT>(row, a) != m) ++a;
+      s_arg = a;
+    }
+    __syncthreads();
+    for (int64_t i = threadIdx.x; i < V; i += PB_THREADS) o[i] = (i == s_arg) ? 1.0 : 0.0;
+    return;
+  }
+  const double mT = __ddiv_rn((double)m, T);
+  for (int64_t i = threadIdx.x; i < V; i += PB_THREADS) o[i] = exp(__dsub_rn(__ddiv_rn((double)ld<DT>(row, i), T), mT));
+  __syncthreads();
+  if (threadIdx.x == 0) s_S = pairwise_seq(o, V);
+  __syncthreads();
+  const double S = s_S;
+  for (int64_t i = threadIdx.x; i < V; i += PB_THREADS) o[i] = __ddiv_rn(o[i], S);
+}
+
+// sample(): total = pairwise_sum(q); cdf = sequential cumsum; first index with
+// cdf > u*total; clamp to V-1; back off over zeros (sampling.py:97-109).
+__global__ void draw_probs_kernel(const double* probs, int64_t V, int64_t stride, const double* u, int32_t* tok,
+                                  uint8_t* flags) {
+  if (threadIdx.x != 0) return;
+  const double* q = probs + blockIdx.x * stride;
+  const double total = pairwise_seq(q, V);
+  if (!(total > 0.0)) {
+    tok[blockIdx.x] = -1;
+    if (flags) flags[blockIdx.x] = LC_DRAW_BAD_ROW;
+    return;
+  }
+  const double t = u[blockIdx.x] * total;
+  double c = 0.0;
+  int64_t i = 0;
+  for (; i < V; ++i) {
+    c += q[i];
+    if (c > t) break;
+  }
+  if (i >= V) i = V - 1;
+  while (i > 0 && q[i] == 0.0) --i;
+  tok[blockIdx.x] = (int32_t)i;
+  if (flags) flags[blockIdx.x] = 0;
+}
+
+// H = -sum p ln p = ln S - sum(e*s)/S with s <= 0 the shifted scaled logits;
+// pmax = max p = 1/S (sampling.py:112-126).
+template <int DT>
+__global__ void __launch_bounds__(PB_THREADS)
+entropy_kernel(const char* rows, int64_t row_bytes, int64_t V, double T, double* H, double* pmax) {
+  __shared__ float fred[PB_THREADS / 32];
+  __shared__ double dred[PB_THREADS / 32];
+  const char* row = rows + blockIdx.x * row_bytes;
+  float m = -INFINITY;
+  for (int64_t i = threadIdx.x; i < V; i += PB_THREADS) m = fmaxf(m, ld<DT>(row, i));
+  m = block_max(m, fred);
+  if (T == 0.0) {
+    if (threadIdx.x == 0) {
+      H[blockIdx.x] = 0.0;
+      pmax[blockIdx.x] = 1.0;
+    }
+    return;
+  }
+  const double mT = __ddiv_rn((double)m, T);
+  double se = 0.0, ses = 0.0;
+  for (int64_t i = threadIdx.x; i < V; i += PB_THREADS) {
+    double s = __dsub_rn(__ddiv_rn((double)ld<DT>(row, i), T), mT);
+    double e = exp(s);
+    se += e;
+    if (e > 0.0) ses += e * s;
+  }
+  se = block_sum(se, dred);
+  ses = block_sum(ses, dred);
+  if (threadIdx.x == 0) {
+    H[blockIdx.x] = log(se) - ses / se;
+    pmax[blockIdx.x] = 1.0 / se;
+  }
+}
+
+}  // namespace lcb
+
+using namespace lcb;
+
+extern "C" int lc_softmax(const void* d_rows, int dtype, int64_t vocab, int64_t row_stride, int64_t n_rows,
+                          const double* d_temperature, double* d_out, void* stream) {
+  if (n_rows < 0 || vocab < 1 || (n_rows > 0 && (!d_rows || !d_temperature || !d_out))) return LC_E_ARG;
+  if (n_rows == 0) return LC_OK;
+  cudaStream_t st = (cudaStream_t)stream;
+  if (dtype == LC_F32)
+    softmax_kernel<LC_F32><<<(unsigned)n_rows, PB_THREADS, 0, st>>>((const char*)d_rows, row_stride * 4, vocab,
+                                                                    d_temperature, d_out);
+  else if (dtype == LC_BF16)
+    softmax_kernel<LC_BF16><<<(unsigned)n_rows, PB_THREADS, 0, st>>>((const char*)d_rows, row_stride * 2, vocab,
+                                                                     d_temperature, d_out);
+  else
+    return LC_E_ARG;
+  LCB_CUDA_TRY(cudaGetLastError());
+  return LC_OK;
+}
+
+extern "C" int lc_draw_probs(const double* d_probs, int64_t vocab, int64_t n_rows, int64_t row_stride,
+                             const double* d_u, int32_t* d_token, uint8_t* d_flags, void* stream) {
+  if (n_rows < 0 || vocab < 1 || (n_rows > 0 && (!d_probs || !d_u || !d_token))) return LC_E_ARG;
+  if (n_rows == 0) return LC_OK;
+  draw_probs_kernel<<<(unsigned)n_rows, 32, 0, (cudaStream_t)stream>>>(d_probs, vocab, row_stride, d_u, d_token,
+                                                                       d_flags);
+  LCB_CUDA_TRY(cudaGetLastError());
+  return LC_OK;
+}
+
+extern "C" int lc_row_entropy(const void* d_rows, int dtype, int64_t vocab, int64_t row_stride, int64_t n_rows,
+                              double temperature, double* d_entropy, double* d_pmax, void* stream) {
+  if (n_rows < 0 || vocab < 1 || (n_rows > 0 && (!d_rows || !d_entropy || !d_pmax))) return LC_E_ARG;
+  if (n_rows == 0) return LC_OK;
+  cudaStream_t st = (cudaStream_t)stream;
+  if (dtype == LC_F32)
+    entropy_kernel<LC_F32><<<(unsigned)n_rows, PB_THREADS, 0, st>>>((const char*)d_rows, row_stride * 4, vocab,
+                                                                    temperature, d_entropy, d_pmax);
+  else if (dtype == LC_BF16)
+    entropy_kernel<LC_BF16><<<(unsigned)n_rows, PB_THREADS, 0, st>>>((const char*)d_rows, row_stride * 2, vocab,
+                                                                     temperature, d_entropy, d_pmax);
+  else
+    return LC_E_ARG;
+  LCB_CUDA_TRY(cudaGetLastError());
+  return LC_OK;
+}
+
+// truncate() on explicit probabilities (sampling.py:71-94): kept prefix of the
+// (p desc, id asc) order by block-wide argmax steps, sequential csum against
+// top_p ('left' cut, inclusive), renormalised by numpy's pairwise sum of the
+// kept values in sorted order.  O(V * kept) -- an API-parity path, not the hot
+// path (the fused lc_resample never materialises truncated probabilities).
+namespace lcb {
+__global__ void __launch_bounds__(PB_THREADS)
+truncate_probs_kernel(const double* probs, int64_t V, int64_t stride, int topk, double topp, double* out,
+                      int32_t* ord_scr, double* val_scr) {
+  __shared__ double s_bp[PB_THREADS];
+  __shared__ int64_t s_bi[PB_THREADS];
+  const double* p = probs + blockIdx.x * stride;
+  double* o = out + blockIdx.x * stride;
+  int32_t* ord = ord_scr + blockIdx.x * V;
+  double* val = val_scr + blockIdx.x * V;
+  const int64_t lim = (topk > 0 && topk < V) ? topk : V;
+  double last_p = INFINITY;
+  int64_t last_id = -1, n = 0;
+  double c = 0.0;
+  while (n < lim) {
+    double bp = -INFINITY;
+    int64_t bi = INT64_MAX;
+    for (int64_t i = threadIdx.x; i < V; i += PB_THREADS) {
+      double pi = p[i];
+      bool after = (pi < last_p) || (pi == last_p && i > last_id);
+      if (after && (pi > bp || (pi == bp && i < bi))) {
+        bp = pi;
+        bi = i;
+      }
+    }
+    s_bp[threadIdx.x] = bp;
+    s_bi[threadIdx.x] = bi;
+    __syncthreads();
+    for (int s = PB_THREADS / 2; s > 0; s >>= 1) {
+      if (threadIdx.x < s) {
+        double op = s_bp[threadIdx.x + s];
+        int64_t oi = s_bi[threadIdx.x + s];
+        if (op > s_bp[threadIdx.x] || (op == s_bp[threadIdx.x] && oi < s_bi[threadIdx.x])) {
+          s_bp[threadIdx.x] = op;
+          s_bi[threadIdx.x] = oi;
+        }
+      }
+      __syncthreads();
+    }
+    bp = s_bp[0];
+    bi = s_bi[0];
+    __syncthreads();
+    if (bi == INT64_MAX) break;
+    if (threadIdx.x == 0) {
+      ord[n] = (int32_t)bi;
+      val[n] = bp;
+    }
+    ++n;
+    last_p = bp;
+    last_id = bi;
+    if (topp < 1.0) {
+      c += bp;
+      if (c >= topp) break;
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double ks = pairwise_seq(val, n);
+    for (int64_t i = 0; i < V; ++i) o[i] = 0.0;
+    for (int64_t i = 0; i < n; ++i) o[ord[i]] = __ddiv_rn(val[i], ks);
+  }
+}
+}  // namespace lcb
+
+extern "C" int lc_truncate_probs(const double* d_probs, int64_t vocab, int64_t n_rows, int64_t row_stride,
+                                 int32_t top_k, double top_p, double* d_out, void* d_scratch, void* stream) {
+  if (n_rows < 0 || vocab < 1 || (n_rows > 0 && (!d_probs || !d_out || !d_scratch))) return LC_E_ARG;
+  if (!(top_p > 0.0 && top_p <= 1.0)) return LC_E_CONFIG;
+  if (n_rows == 0) return LC_OK;
+  int32_t* ord = (int32_t*)d_scratch;
+  double* val = (double*)((char*)d_scratch + ((n_rows * vocab * 4 + 255) & ~255ll));
+  lcb::truncate_probs_kernel<<<(unsigned)n_rows, lcb::PB_THREADS, 0, (cudaStream_t)stream>>>(
+      d_probs, vocab, row_stride, top_k, top_p, d_out, ord, val);
+  LCB_CUDA_TRY(cudaGetLastError());
+  return LC_OK;
+}

@@ -1,0 +1,82 @@
+// Fused replay plumbing: device-side task construction from lookup results
+// and step-wise acceptance (engine.py:296-331), so that lookup -> resample ->
+// accept runs as one stream-ordered sequence with no host synchronisation.
+#include "lc_common.cuh"
+
+namespace lcb {
+
+__global__ void replay_tasks_kernel(const int32_t* __restrict__ slot, const int32_t* __restrict__ len, int64_t n_req,
+                                    int max_pos, int nb, const double* __restrict__ temp,
+                                    const int32_t* __restrict__ topk, const double* __restrict__ topp,
+                                    lc_task* __restrict__ tasks) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n_req * (int64_t)max_pos) return;
+  const int64_t r = i / max_pos;
+  const int t = (int)(i % max_pos);
+  const int s = slot[r];
+  const int lim = s >= 0 ? min(len[r], max_pos) : 0;
+  lc_task tk;
+  tk.row = -1;
+  tk.slot = s;
+  tk.pos = t;
+  tk.temperature = temp[r];
+  tk.top_k = topk[r];
+  tk.vocab = 0;
+  tk.top_p = topp[r];
+  tk.draw_begin = i * nb;
+  tk.draw_end = t < lim ? i * nb + nb : i * nb;
+  tk.seed_base = r * nb;
+  tk.u_index = t;
+  tasks[i] = tk;
+}
+
+// one thread per (request, branch): first position whose draw differs from the
+// cached token ends the replay; that divergent token is kept (engine.py:305-310)
+__global__ void replay_accept_kernel(const int32_t* __restrict__ tok, const int32_t* __restrict__ cached,
+                                     const int32_t* __restrict__ len, int64_t n_req, int max_pos, int nb,
+                                     int32_t* __restrict__ replayed, int32_t* __restrict__ diverged) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n_req * (int64_t)nb) return;
+  const int64_t r = i / nb;
+  const int b = (int)(i % nb);
+  const int lim = min(len[r], max_pos);
+  int rep = 0, div = -1;
+  for (int t = 0; t < lim; ++t) {
+    const int y = tok[((r * max_pos) + t) * (int64_t)nb + b];
+    rep = t + 1;
+    if (y != cached[r * max_pos + t]) {
+      div = t;
+      break;
+    }
+  }
+  replayed[i] = rep;
+  if (diverged) diverged[i] = div;
+}
+
+}  // namespace lcb
+
+extern "C" int lc_replay_tasks(const int32_t* d_slot, const int32_t* d_len, int64_t n_req, int32_t max_pos,
+                               int32_t n_branch, const double* d_temperature, const int32_t* d_top_k,
+                               const double* d_top_p, lc_task* d_tasks, void* stream) {
+  if (n_req < 0 || max_pos < 0 || n_branch < 0) return LC_E_ARG;
+  const int64_t n = n_req * (int64_t)max_pos;
+  if (n == 0) return LC_OK;
+  if (!d_slot || !d_len || !d_temperature || !d_top_k || !d_top_p || !d_tasks) return LC_E_ARG;
+  lcb::replay_tasks_kernel<<<lcb::ceil_div(n, 256), 256, 0, (cudaStream_t)stream>>>(
+      d_slot, d_len, n_req, max_pos, n_branch, d_temperature, d_top_k, d_top_p, d_tasks);
+  LCB_CUDA_TRY(cudaGetLastError());
+  return LC_OK;
+}
+
+extern "C" int lc_replay_accept(const int32_t* d_tokens, const int32_t* d_cached, const int32_t* d_len, int64_t n_req,
+                                int32_t max_pos, int32_t n_branch, int32_t* d_replayed, int32_t* d_diverged,
+                                void* stream) {
+  if (n_req < 0 || max_pos < 0 || n_branch < 0) return LC_E_ARG;
+  const int64_t n = n_req * (int64_t)n_branch;
+  if (n == 0) return LC_OK;
+  if (!d_tokens || !d_cached || !d_len || !d_replayed) return LC_E_ARG;
+  lcb::replay_accept_kernel<<<lcb::ceil_div(n, 256), 256, 0, (cudaStream_t)stream>>>(
+      d_tokens, d_cached, d_len, n_req, max_pos, n_branch, d_replayed, d_diverged);
+  LCB_CUDA_TRY(cudaGetLastError());
+  return LC_OK;
+}

@@ -1,0 +1,1220 @@
+// K1: fused temperature -> softmax -> top-k/top-p -> inverse-CDF draw.
+//
+// Reference semantics (bit-exact token decisions given the same uniform):
+//   softmax   sampling.py:57-68   s = f64(z)/T - max, e = exp(s), p = e / pairwise_sum(e)
+//   truncate  sampling.py:71-94   order (p desc, id asc); top-k if k < V; nucleus on the
+//                                 UNtruncated mass: cut = first csum >= top_p ('left');
+//                                 renormalise by the kept sum
+//   sample    sampling.py:97-109  t = u * pairwise_sum(q); first id with cumsum(q) > t
+//                                 ('right'), clamp to V-1, back off over q == 0
+//
+// Three tiers:
+//   FAST    fp32 MUFU exponentials with an exactly-carried argument and a
+//           rigorous per-row error bound; every decision (nucleus cut, draw) is
+//           certified against the bound, otherwise the task goes to REFINE.
+//   REFINE  the same algorithm with fp64 e = exp(fl(fl(z/T) - fl(m/T))) -- the
+//           reference's own argument -- and bounds of ~V*2^-52.  Uncertified
+//           decisions go to EXACT.
+//   EXACT   emulation of numpy's operation order (pairwise sums, sequential
+//           cumsum, lexsort order) by one CTA per task.  Only the libm exp can
+//           differ from numpy's (<= 1 ulp); a draw whose margin is within that
+//           is flagged LC_DRAW_UNRESOLVED.
+//
+// Layout: one CTA (512 threads) per task, persistent over tasks.  Warp w owns
+// the contiguous id range [w*C, (w+1)*C) of the row (C a multiple of 8); a
+// lane reads 8 consecutive elements per 16 B (bf16) / 32 B (fp32) vector, so a
+// warp instruction covers 256 consecutive ids (coalesced) and the warp ranges
+// are in id order -- which is what the inverse-CDF search needs.
+#include <float.h>
+#include <limits.h>
+#include <math.h>
+
+#include "lc_common.cuh"
+#include "lc_numpy.cuh"
+#include "lc_resample.cuh"
+
+namespace lcb {
+
+constexpr int RS_THREADS = 512;
+constexpr int RS_WARPS = RS_THREADS / 32;
+constexpr int CAND_CAP = 2048;        // candidate list (top-k / small nucleus / bracket) in smem
+constexpr int NBINS = 256;            // nucleus histogram bins
+constexpr float BINS_PER_OCT = 4.0f;  // 64 octaves of dynamic range
+constexpr int K0_SPEC = 64;           // speculative candidate count for top-p without top-k
+constexpr int SCR_PER_WARP = 1024;    // large-nucleus kept elements per warp (global scratch)
+constexpr int SCR_PER_CTA = SCR_PER_WARP * RS_WARPS;
+
+// ---- error model ----------------------------------------------
+// ex2.approx.ftz.f32 relative error bound (PTX ISA: ~2 ulp).  The GPU test
+// tests/test_gpu_numerics.py::test_fast_exp_error_bound measures fast_exp over
+// dense argument grids and fails if this constant is ever exceeded.
+constexpr double kEx2RelErr = 4.0e-7;
+constexpr double kCorrErr = 1.0e-10;                         // 2nd-order term of the argument correction
+constexpr double kSum8Err = 3.0 * 5.9604644775390625e-08;    // fp32 pairwise sum of 8 (3 roundings)
+constexpr double kRefExpErr = 8.881784197001252e-16;         // libm / numpy exp vs exact: 4 ulp
+constexpr double kEps64 = 1.1102230246251565e-16;            // 2^-53
+
+// ---- loading --------------------------------------------------------------------------------
+
+// 8 consecutive logits starting at id e0; ids >= V (the caller's limit) read as -inf.
+template <int DT>
+__device__ __forceinline__ void load8(const char* row, int e0, int V, bool vec, float v[8]) {
+  if (e0 >= V) {
+#pragma unroll
+    for (int j = 0; j < 8; ++j) v[j] = -INFINITY;
+    return;
+  }
+  if (DT == LC_BF16) {
+    const uint16_t* r = reinterpret_cast<const uint16_t*>(row);
+    if (vec && e0 + 8 <= V) {
+      uint4 q = __ldg(reinterpret_cast<const uint4*>(r + e0));
+      uint32_t w[4] = {q.x, q.y, q.z, q.w};
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        v[2 * j] = __uint_as_float(w[j] << 16);
+        v[2 * j + 1] = __uint_as_float(w[j] & 0xffff0000u);
+      }
+    } else {
+#pragma unroll
+      for (int j = 0; j < 8; ++j) v[j] = (e0 + j < V) ? bf16_bits_to_f32(__ldg(r + e0 + j)) : -INFINITY;
+    }
+  } else {
+    const float* r = reinterpret_cast<const float*>(row);
+    if (vec && e0 + 8 <= V) {
+      float4 a = __ldg(reinterpret_cast<const float4*>(r + e0));
+      float4 b = __ldg(reinterpret_cast<const float4*>(r + e0 + 4));
+      v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w;
+      v[4] = b.x; v[5] = b.y; v[6] = b.z; v[7] = b.w;
+    } else {
+#pragma unroll
+      for (int j = 0; j < 8; ++j) v[j] = (e0 + j < V) ? __ldg(r + e0 + j) : -INFINITY;
+    }
+  }
+}
+
+// Warp-uniform pass over the warp's id range [cb, ce): UNR vectors per lane are
+// loaded before any is consumed (memory-level parallelism); f(e0, v) sees ids
+// e0..e0+7 with ids >= ce read as -inf (callers mask with e0 + j < ce).
+template <int DT, int UNR, typename F>
+__device__ __forceinline__ void warp_pass(const char* row, int cb, int ce, bool vec, int lane, F&& f) {
+  for (int base = cb; base < ce; base += 256 * UNR) {
+    float v[UNR][8];
+#pragma unroll
+    for (int u = 0; u < UNR; ++u) load8<DT>(row, base + 256 * u + 8 * lane, ce, vec, v[u]);
+#pragma unroll
+    for (int u = 0; u < UNR; ++u) f(base + 256 * u + 8 * lane, v[u]);
+  }
+}
+
+template <int DT>
+__device__ __forceinline__ float load1(const char* row, int i) {
+  if (DT == LC_BF16) return bf16_bits_to_f32(__ldg(reinterpret_cast<const uint16_t*>(row) + i));
+  return __ldg(reinterpret_cast<const float*>(row) + i);
+}
+
+// ---- exponentials ------------------------------------------------------------------------------
+
+struct ExpCtx {
+  float m;         // row max (exact)
+  float Lhi, Llo;  // log2(e)/T split, Lhi + Llo = log2e/T to ~2^-48
+  double T;
+  double mT;       // fl(m / T): the reference's scaled max (sampling.py:65-66)
+};
+
+// FAST: e ~ 2^((z - m) * log2e / T).  z - m is carried exactly (TwoSum), the
+// product error and the constant's low part go into alo, and ex2's input
+// rounding is removed by the first-order correction e*(1 + alo*ln2).
+// Relative error <= kEx2RelErr + kCorrErr; 0 for z = -inf; e(m) == 1 exactly.
+__device__ __forceinline__ float fast_exp(const ExpCtx& c, float z) {
+  float s = z - c.m;
+  float bb = s - z;
+  float err = (z - (s - bb)) + (-c.m - bb);
+  float ahi = s * c.Lhi;
+  float alo = fmaf(s, c.Lhi, -ahi) + fmaf(err, c.Lhi, s * c.Llo);
+  float e = ex2_approx(ahi);
+  return (e > 0.0f) ? fmaf(e, alo * 0.69314718055994531f, e) : 0.0f;
+}
+
+// REFINE / EXACT: the reference's own argument s = fl(fl(z/T) - fl(m/T)), then
+// the fp64 exponential (<= 1 ulp).
+__device__ __forceinline__ double ref_exp(const ExpCtx& c, float z) {
+  double s = __dsub_rn(__ddiv_rn((double)z, c.T), c.mT);
+  return exp(s);
+}
+
+template <bool REFINE>
+__device__ __forceinline__ double elem_exp(const ExpCtx& c, float z) {
+  if (REFINE) return ref_exp(c, z);
+  return (double)fast_exp(c, z);
+}
+
+// log2-distance bin of z below the max (monotone non-increasing in z)
+__device__ __forceinline__ int nbin(const ExpCtx& c, float z) {
+  float a = (z - c.m) * c.Lhi;
+  return max((int)fminf(-a * BINS_PER_OCT, (float)(NBINS - 1)), 0);
+}
+
+// ---- keys ----------------------------------------------------------------------------------
+
+// (z desc, id asc) == numeric descending order of this key
+__device__ __forceinline__ unsigned long long cand_key(float z, int id) {
+  return ((unsigned long long)f32_order_key(z) << 32) | (unsigned long long)(0xffffffffu - (uint32_t)id);
+}
+__device__ __forceinline__ int cand_id(unsigned long long k) { return (int)(0xffffffffu - (uint32_t)(k & 0xffffffffu)); }
+__device__ __forceinline__ float cand_z(unsigned long long k) {
+  uint32_t o = (uint32_t)(k >> 32);
+  uint32_t u = (o & 0x80000000u) ? (o & 0x7fffffffu) : ~o;
+  return __uint_as_float(u);
+}
+
+// ---- shared memory ----------------------------------------------------------------------------
+
+struct __align__(16) Smem {
+  unsigned long long cand[CAND_CAP];  // candidate keys
+  double ce[CAND_CAP];                // precise e of sorted candidates
+  int sl_id[CAND_CAP];                // kept small list, id order
+  double sl_e[CAND_CAP];              // its e, later its inclusive prefix
+  uint32_t hist[RS_WARPS][NBINS];     // per-warp fixed-point nucleus histogram
+  unsigned long long tk64[RS_THREADS];
+  double wsum[RS_WARPS];
+  double werr[RS_WARPS];
+  double wpre[RS_WARPS + 1];
+  float wmax[RS_WARPS];
+  int warg[RS_WARPS];
+  int wcount[RS_WARPS];
+  int wsl[RS_WARPS + 1];
+  double dsc[4];
+  int isc[8];
+};
+// isc: 0 cand count, 1 bad row, 2 overflow, 3 kept count, 4 uncertain, 5 blo, 6 bhi, 7 need-next-tier
+
+// Descending bitonic sort of n (power of two) 64-bit keys in smem.
+__device__ void bitonic_desc(unsigned long long* a, int n) {
+  for (int k = 2; k <= n; k <<= 1) {
+    for (int j = k >> 1; j > 0; j >>= 1) {
+      for (int i = threadIdx.x; i < n; i += RS_THREADS) {
+        int p = i ^ j;
+        if (p > i) {
+          unsigned long long x = a[i], y = a[p];
+          bool desc = ((i & k) == 0);
+          if (desc ? (x < y) : (x > y)) {
+            a[i] = y;
+            a[p] = x;
+          }
+        }
+      }
+      __syncthreads();
+    }
+  }
+}
+
+__device__ __forceinline__ int pow2_at_least(int n) {
+  int p = 1;
+  while (p < n) p <<= 1;
+  return p;
+}
+
+// warp-aggregated append to sm.cand
+__device__ __forceinline__ void push_cand(Smem& sm, bool pred, float z, int id, int& overflow) {
+  unsigned mask = __ballot_sync(0xffffffffu, pred);
+  if (mask == 0) return;
+  int lane = threadIdx.x & 31;
+  int leader = __ffs(mask) - 1;
+  int base = 0;
+  if (lane == leader) base = atomicAdd(&sm.isc[0], __popc(mask));
+  base = __shfl_sync(0xffffffffu, base, leader);
+  if (pred) {
+    int pos = base + __popc(mask & ((1u << lane) - 1u));
+    if (pos < CAND_CAP) sm.cand[pos] = cand_key(z, id);
+    else overflow = 1;
+  }
+}
+
+// ---- task plumbing ------------------------------------------------------------------------------
+
+struct TaskView {
+  const char* row;
+  int V;
+  double T;
+  int topk;  // effective top-k (0 = none / k >= V)
+  double topp;
+  bool trunc;
+  int64_t d0, d1;
+  int64_t seed_base;
+  int64_t u_index;
+};
+
+struct CacheMap {
+  const int32_t* pages;  // [slots][max_pages], -1 = unused
+  int max_pages;
+  int page_rows;
+};
+
+struct DrawIO {
+  const double* u;
+  const uint64_t* seed;
+  const int64_t* index;
+  int32_t* token;
+  uint8_t* flags;
+};
+
+struct Workspace {
+  int* q_refine;  // [0] = count, [1..] task ids
+  int* q_exact;
+  int* scr_id;    // [grid][2][SCR_PER_CTA]
+  double* scr_e;  // [grid][2][SCR_PER_CTA]
+};
+
+
+__device__ __forceinline__ double draw_u(const DrawIO& io, int64_t d, const TaskView& tv) {
+  if (io.u) return io.u[d];
+  if (io.index) return request_uniform(io.seed[d], (uint64_t)io.index[d]);
+  return request_uniform(io.seed[tv.seed_base + (d - tv.d0)], (uint64_t)tv.u_index);
+}
+
+__device__ __forceinline__ bool resolve_task(const lc_task& tk, const char* rows, int64_t row_bytes, int Vdef,
+                                             const CacheMap& cm, TaskView& tv) {
+  tv.d0 = tk.draw_begin;
+  tv.d1 = tk.draw_end;
+  tv.seed_base = tk.seed_base;
+  tv.u_index = tk.u_index >= 0 ? tk.u_index : tk.pos;
+  tv.V = tk.vocab > 0 ? tk.vocab : Vdef;
+  tv.T = tk.temperature;
+  tv.topk = (tk.top_k > 0 && tk.top_k < tv.V) ? tk.top_k : 0;
+  tv.topp = tk.top_p;
+  tv.trunc = !(tk.top_k <= 0 && tk.top_p == 1.0);
+  tv.row = nullptr;
+  if (tv.V < 1 || tv.V > Vdef || !(tv.T >= 0.0) || !(tv.topp > 0.0 && tv.topp <= 1.0)) return false;
+  int64_t r = tk.row;
+  if (r < 0) {
+    if (!cm.pages || tk.slot < 0 || tk.pos < 0) return false;
+    int pg = tk.pos / cm.page_rows;
+    if (pg >= cm.max_pages) return false;
+    int page = cm.pages[(int64_t)tk.slot * cm.max_pages + pg];
+    if (page < 0) return false;
+    r = (int64_t)page * cm.page_rows + tk.pos % cm.page_rows;
+  }
+  tv.row = rows + r * row_bytes;
+  return true;
+}
+
+__device__ __forceinline__ void write_all(const TaskView& tv, const DrawIO& io, int tok, uint8_t flag) {
+  for (int64_t d = tv.d0 + threadIdx.x; d < tv.d1; d += RS_THREADS) {
+    io.token[d] = tok;
+    if (io.flags) io.flags[d] = flag;
+  }
+}
+
+// ============================== FAST / REFINE kernel ==============================
+
+template <int DT, bool REFINE>
+__global__ void __launch_bounds__(RS_THREADS, 1)
+resample_kernel(const char* __restrict__ rows, int64_t row_bytes, int Vdef, const lc_task* __restrict__ tasks,
+                int n_tasks, const int* __restrict__ task_list, CacheMap cm, DrawIO io, Workspace ws,
+                unsigned long long* counters) {
+  extern __shared__ __align__(16) unsigned char smraw[];
+  Smem& sm = *reinterpret_cast<Smem*>(smraw);
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int ntask = task_list ? task_list[0] : n_tasks;
+  int* scrA_id = ws.scr_id + (int64_t)blockIdx.x * 2 * SCR_PER_CTA;
+  double* scrA_e = ws.scr_e + (int64_t)blockIdx.x * 2 * SCR_PER_CTA;
+  int* scrM_id = scrA_id + SCR_PER_CTA;
+  double* scrM_e = scrA_e + SCR_PER_CTA;
+  const uint8_t tier_flag = REFINE ? LC_DRAW_PRECISE : 0;
+
+  for (int ti = blockIdx.x; ti < ntask; ti += gridDim.x) {
+    const int task_id = task_list ? task_list[1 + ti] : ti;
+    TaskView tv;
+    const lc_task tk = tasks[task_id];
+    if (tk.draw_end <= tk.draw_begin) continue;  // nothing to draw (uniform across the CTA)
+    if (!resolve_task(tk, rows, row_bytes, Vdef, cm, tv)) {
+      write_all(tv, io, -1, LC_DRAW_BAD_ROW);
+      if (tid == 0) atomicAdd(&counters[2], 1ull);
+      __syncthreads();
+      continue;
+    }
+    const int V = tv.V;
+    const bool vec = ((reinterpret_cast<uintptr_t>(tv.row) & 15) == 0);
+    const int C = ((V + RS_WARPS - 1) / RS_WARPS + 7) & ~7;
+    const int cb = min(V, warp * C);
+    const int ce = min(V, cb + C);
+    if (tid == 0) {
+      for (int i = 0; i < 8; ++i) sm.isc[i] = 0;
+    }
+
+    // ---------------- phase A: max, first argmax, thread maxima, NaN check
+    float tmax = -INFINITY;
+    int targ = INT_MAX;
+    bool bad = false;
+    warp_pass<DT, 4>(tv.row, cb, ce, vec, lane, [&](int e0, const float* v) {
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        bad |= (v[j] != v[j]);
+        if (v[j] > tmax) {
+          tmax = v[j];
+          targ = e0 + j;
+        }
+      }
+    });
+    __syncthreads();  // isc reset visible
+    {
+      float wm = warp_max(tmax);
+      int wa = warp_min_int(tmax == wm ? targ : INT_MAX);
+      bool wbad = __any_sync(0xffffffffu, bad);
+      if (lane == 0) {
+        sm.wmax[warp] = wm;
+        sm.warg[warp] = wa;
+        if (wbad) sm.isc[1] = 1;
+      }
+      sm.tk64[tid] = ((unsigned long long)f32_order_key(tmax) << 32) | (uint32_t)tid;
+    }
+    __syncthreads();
+    float m = -INFINITY;
+    int amax = INT_MAX;
+    for (int w = 0; w < RS_WARPS; ++w) {
+      if (sm.wmax[w] > m) {
+        m = sm.wmax[w];
+        amax = sm.warg[w];
+      }
+    }
+    const bool rowbad = sm.isc[1] || !(m > -INFINITY) || !(m < INFINITY);
+    if (rowbad) {
+      write_all(tv, io, -1, LC_DRAW_BAD_ROW);
+      if (tid == 0) atomicAdd(&counters[2], 1ull);
+      __syncthreads();
+      continue;
+    }
+    if (tv.T == 0.0) {  // greedy: one-hot at the first argmax, still one draw (sampling.py:61-64)
+      write_all(tv, io, amax, tier_flag);
+      __syncthreads();
+      continue;
+    }
+    ExpCtx ec;
+    ec.m = m;
+    ec.T = tv.T;
+    ec.mT = __ddiv_rn((double)m, tv.T);
+    {
+      double Ld = 1.4426950408889634 / tv.T;
+      ec.Lhi = (float)Ld;
+      ec.Llo = (float)(Ld - (double)ec.Lhi);
+    }
+    // temperatures whose scaled logits leave the fp32 range go straight to REFINE
+    bool fail = !REFINE && !(ec.Lhi < 1e20f && ec.Lhi > 1e-20f && fabsf(m) * ec.Lhi < 1e30f);
+
+    // ---------------- candidate threshold (top-k, or speculative small nucleus)
+    int kc = 0;
+    if (tv.topk > 0) kc = tv.topk;
+    else if (tv.trunc && tv.topp < 1.0) kc = K0_SPEC;
+    float theta = INFINITY;
+    if (kc > 0 && kc <= RS_THREADS) {
+      // the kc-th largest thread maximum lower-bounds the kc-th largest logit
+      bitonic_desc(sm.tk64, RS_THREADS);
+      theta = cand_z((sm.tk64[kc - 1] & 0xffffffff00000000ull) | 0xffffffffull);
+    } else if (kc > RS_THREADS) {
+      theta = -INFINITY;  // collect all; overflow -> next tier
+    }
+
+    // ---------------- phase B: mass, per-warp sums, candidates
+    double S_part = 0.0;
+    int overflow = 0;
+    warp_pass<DT, 2>(tv.row, cb, ce, vec, lane, [&](int e0, const float* v) {
+      if (REFINE) {
+        double s8 = 0.0;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) s8 += ref_exp(ec, v[j]);  // ids >= ce are -inf -> 0
+        S_part += s8;
+      } else {
+        float e[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) e[j] = fast_exp(ec, v[j]);
+        float s8 = ((e[0] + e[1]) + (e[2] + e[3])) + ((e[4] + e[5]) + (e[6] + e[7]));
+        S_part += (double)s8;
+      }
+      if (kc > 0) {
+#pragma unroll
+        for (int j = 0; j < 8; ++j) push_cand(sm, (e0 + j < ce) && v[j] >= theta, v[j], e0 + j, overflow);
+      }
+    });
+    {
+      double wsm = warp_sum(S_part);
+      int wo = __any_sync(0xffffffffu, overflow);
+      if (lane == 0) {
+        sm.wsum[warp] = wsm;
+        if (wo) sm.isc[2] = 1;
+      }
+    }
+    __syncthreads();
+    double S = 0.0;
+    for (int w = 0; w < RS_WARPS; ++w) S += sm.wsum[w];
+    // relative error of our e's and sums vs the reference's e's (exact-arithmetic sums)
+    const double relE = REFINE ? (2.0 * kRefExpErr + (double)(V + 16) * kEps64)
+                               : (kEx2RelErr + kCorrErr + kSum8Err + kRefExpErr + (double)(V + 16) * kEps64);
+    const double E_S = S * relE + (REFINE ? 0.0 : (double)V * 2.4e-38);  // + flushed subnormals
+    // the reference's own rounding in p = e/S, csum, sum(q), cumsum (relative)
+    const double relRef = (double)(2 * V + 64) * kEps64;
+    const int ncand = min(sm.isc[0], CAND_CAP);
+    const bool cand_overflow = sm.isc[2] != 0;
+    __syncthreads();
+    if (tid == 0) {
+      sm.isc[2] = 0;
+      sm.isc[7] = 0;
+    }
+
+    // Kept-set representation for the draw:
+    //   mode 0 -- untruncated: all ids, e recomputed by the owning warp;
+    //   mode 1 -- small list sl_id/sl_e (id order) of length L;
+    //   mode 2 -- per-warp merged lists in global scratch (scrM), counts wcount[].
+    int mode = 0;
+    int L = 0;
+
+    if (!fail && tv.trunc) {
+      const double P = tv.topp * S;  // nucleus target in e-space
+      bool done = false;
+      if (kc > 0 && !cand_overflow && ncand >= kc) {
+        const int n2 = pow2_at_least(ncand);
+        for (int i = ncand + tid; i < n2; i += RS_THREADS) sm.cand[i] = 0ull;
+        __syncthreads();
+        bitonic_desc(sm.cand, n2);
+        const int klim = tv.topk > 0 ? tv.topk : ncand;
+        for (int i = tid; i < klim; i += RS_THREADS) sm.ce[i] = ref_exp(ec, cand_z(sm.cand[i]));
+        __syncthreads();
+        if (tid == 0) {
+          int cut = -1;
+          bool unc = false;
+          if (tv.topp < 1.0) {
+            double c = 0.0;
+            for (int i = 0; i < klim; ++i) {
+              double prev = c;
+              c += sm.ce[i];
+              double tol = tv.topp * E_S + c * relRef;
+              if (c >= P - tol) {
+                cut = i;
+                if (!(c - P > tol && P - prev > tol)) unc = true;
+                break;
+              }
+            }
+          }
+          int Lk = cut >= 0 ? cut + 1 : (tv.topk > 0 ? klim : -1);
+          if (Lk > 0) {
+            // distinct logits that the reference might round to equal p: ordering unsafe
+            int lim = min(Lk + 1, ncand);
+            for (int i = 1; i < lim; ++i) {
+              float za = cand_z(sm.cand[i - 1]), zb = cand_z(sm.cand[i]);
+              if (za != zb) {
+                double da = __ddiv_rn((double)za, tv.T), db = __ddiv_rn((double)zb, tv.T);
+                if (da - db <= fmax(fabs(da), fabs(ec.mT)) * 8.0 * kEps64) unc = true;
+              }
+            }
+          }
+          sm.isc[3] = Lk;
+          sm.isc[4] = unc;
+        }
+        __syncthreads();
+        if (sm.isc[4]) fail = true;
+        if (!fail && sm.isc[3] > 0) {
+          done = true;
+          mode = 1;
+          L = sm.isc[3];
+        }
+      } else if (tv.topk > 0) {
+        fail = true;  // top-k candidates overflowed (heavy ties / k > 512) -> next tier
+      }
+
+      if (!fail && !done) {
+        // -------- large nucleus: top-p without top-k, nucleus beyond the speculative list
+        __syncthreads();
+        for (int i = tid; i < RS_WARPS * NBINS; i += RS_THREADS) (&sm.hist[0][0])[i] = 0u;
+        __syncthreads();
+        const int lgC = 32 - __clz(C + 1);
+        const float qscale = ldexpf(1.0f, 31 - lgC);
+        warp_pass<DT, 2>(tv.row, cb, ce, vec, lane, [&](int e0, const float* v) {
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            if (e0 + j < ce) {
+              float e = REFINE ? (float)ref_exp(ec, v[j]) : fast_exp(ec, v[j]);
+              atomicAdd(&sm.hist[warp][nbin(ec, v[j])], __float2uint_rn(e * qscale));
+            }
+          }
+        });
+        __syncthreads();
+        if (tid < 32) {
+          const double inv = 1.0 / (double)qscale;
+          const double qerr = (double)V * 0.5 * inv + 2.0 * E_S + P * relRef;
+          double cum = 0.0;
+          int blo = NBINS - 1, bhi = NBINS - 1;
+          bool got_lo = false;
+          for (int b0 = 0; b0 < NBINS; b0 += 32) {
+            unsigned long long hs = 0;
+            for (int w = 0; w < RS_WARPS; ++w) hs += sm.hist[w][b0 + lane];
+            double x = (double)hs * inv;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+              double y = __shfl_up_sync(0xffffffffu, x, o);
+              if (lane >= o) x += y;
+            }
+            double incl = cum + x;
+            unsigned lo_m = __ballot_sync(0xffffffffu, incl >= P - qerr);
+            unsigned hi_m = __ballot_sync(0xffffffffu, incl >= P + qerr);
+            if (!got_lo && lo_m) {
+              blo = b0 + __ffs(lo_m) - 1;
+              got_lo = true;
+            }
+            if (hi_m) {
+              bhi = b0 + __ffs(hi_m) - 1;
+              break;
+            }
+            cum = __shfl_sync(0xffffffffu, incl, 31);
+          }
+          if (lane == 0) {
+            sm.isc[5] = blo;
+            sm.isc[6] = bhi;
+            sm.isc[0] = 0;
+            sm.isc[2] = 0;
+          }
+        }
+        __syncthreads();
+        const int blo = sm.isc[5], bhi = sm.isc[6];
+        // B3: order-preserving per-warp compaction of bins < blo (certainly kept) to
+        // scratch A; bracket bins [blo, bhi] to the smem candidate list.
+        int wn = 0, ovf = 0;
+        warp_pass<DT, 2>(tv.row, cb, ce, vec, lane, [&](int e0, const float* v) {
+          int b[8];
+#pragma unroll
+          for (int j = 0; j < 8; ++j) b[j] = (e0 + j < ce) ? nbin(ec, v[j]) : NBINS;
+          // lane-major order inside a 256-id step: lane l's 8 ids precede lane l+1's
+          int mine = 0;
+#pragma unroll
+          for (int j = 0; j < 8; ++j) mine += (b[j] < blo);
+          int x = mine;
+#pragma unroll
+          for (int o = 1; o < 32; o <<= 1) {
+            int y = __shfl_up_sync(0xffffffffu, x, o);
+            if (lane >= o) x += y;
+          }
+          int pos = wn + x - mine;
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            if (b[j] < blo) {
+              if (pos < SCR_PER_WARP) scrA_id[warp * SCR_PER_WARP + pos] = e0 + j;
+              else ovf = 1;
+              ++pos;
+            }
+          }
+          wn += __shfl_sync(0xffffffffu, x, 31);
+#pragma unroll
+          for (int j = 0; j < 8; ++j) push_cand(sm, b[j] >= blo && b[j] <= bhi, v[j], e0 + j, ovf);
+        });
+        ovf = __any_sync(0xffffffffu, ovf);
+        if (lane == 0) {
+          sm.wcount[warp] = min(wn, SCR_PER_WARP);
+          if (ovf || wn > SCR_PER_WARP) sm.isc[2] = 1;
+        }
+        __syncthreads();
+        if (sm.isc[2]) {
+          fail = true;
+        } else {
+          // precise e of the certainly-kept elements (dense, per warp)
+          const int nw = sm.wcount[warp];
+          double acc = 0.0;
+          for (int i = lane; i < nw; i += 32) {
+            double e = ref_exp(ec, load1<DT>(tv.row, scrA_id[warp * SCR_PER_WARP + i]));
+            scrA_e[warp * SCR_PER_WARP + i] = e;
+            acc += e;
+          }
+          acc = warp_sum(acc);
+          if (lane == 0) sm.wsum[warp] = acc;
+          const int nb = min(sm.isc[0], CAND_CAP);
+          const int n2 = pow2_at_least(max(nb, 1));
+          for (int i = nb + tid; i < n2; i += RS_THREADS) sm.cand[i] = 0ull;
+          __syncthreads();
+          bitonic_desc(sm.cand, n2);
+          for (int i = tid; i < nb; i += RS_THREADS) sm.ce[i] = ref_exp(ec, cand_z(sm.cand[i]));
+          __syncthreads();
+          if (tid == 0) {
+            double Mabove = 0.0;
+            for (int w = 0; w < RS_WARPS; ++w) Mabove += sm.wsum[w];
+            int cut = -1;
+            bool unc = false;
+            double c = Mabove;
+            const double tolS = tv.topp * E_S;
+            if (c >= P - tolS - c * relRef) unc = true;  // the cut would lie above the bracket
+            for (int i = 0; i < nb && !unc; ++i) {
+              double prev = c;
+              c += sm.ce[i];
+              double tol = tolS + c * relRef;
+              if (c >= P - tol) {
+                cut = i;
+                if (!(c - P > tol && P - prev > tol)) unc = true;
+                break;
+              }
+            }
+            if (cut < 0) unc = true;
+            if (!unc) {
+              for (int i = max(cut, 1); i <= min(cut + 1, nb - 1); ++i) {
+                float za = cand_z(sm.cand[i - 1]), zb = cand_z(sm.cand[i]);
+                if (za != zb) {
+                  double da = __ddiv_rn((double)za, tv.T), db = __ddiv_rn((double)zb, tv.T);
+                  if (da - db <= fmax(fabs(da), fabs(ec.mT)) * 8.0 * kEps64) unc = true;
+                }
+              }
+            }
+            sm.isc[3] = cut + 1;
+            sm.isc[4] = unc;
+          }
+          __syncthreads();
+          if (sm.isc[4]) {
+            fail = true;
+          } else {
+            mode = 2;
+            L = sm.isc[3];  // first L bracket candidates are kept
+          }
+        }
+      }
+    }
+
+    if (fail) {
+      if (tid == 0) {
+        int* q = REFINE ? ws.q_exact : ws.q_refine;
+        int pos = atomicAdd(q, 1);
+        q[1 + pos] = task_id;
+        atomicAdd(&counters[0], 1ull);
+      }
+      __syncthreads();
+      continue;
+    }
+
+    // ---------------- kept small list in id order (modes 1 and 2)
+    if (mode != 0) {
+      // key: id ascending == descending (~id); payload: index into cand/ce
+      // rank sort by id (ids are distinct; L is small: top-k, nucleus or bracket members)
+      for (int i = tid; i < L; i += RS_THREADS) {
+        int id = cand_id(sm.cand[i]);
+        int rank = 0;
+        for (int j = 0; j < L; ++j) rank += (cand_id(sm.cand[j]) < id);
+        sm.sl_id[rank] = id;
+        sm.sl_e[rank] = sm.ce[i];
+      }
+      __syncthreads();
+    }
+
+    if (mode == 1) {
+      // inclusive prefix (sequential, exact order) on thread 0; L <= 2048
+      if (tid == 0) {
+        double c = 0.0;
+        for (int i = 0; i < L; ++i) {
+          c += sm.sl_e[i];
+          sm.sl_e[i] = c;
+        }
+        sm.dsc[0] = c;
+      }
+      __syncthreads();
+      const double K = sm.dsc[0];
+      // kept e's are precise: only the reference's rounding and ours remain
+      const double tolK = K * ((double)(V + L + 64) * 4.0 * kEps64 + 4.0 * kRefExpErr);
+      int need = 0;
+      for (int64_t d = tv.d0 + tid; d < tv.d1; d += RS_THREADS) {
+        const double u = draw_u(io, d, tv);
+        const double t = u * K;
+        int lo = 0, hi = L;
+        while (lo < hi) {
+          int mid = (lo + hi) >> 1;
+          if (sm.sl_e[mid] > t) hi = mid;
+          else lo = mid + 1;
+        }
+        bool ok = lo < L && (lo == 0 || t - sm.sl_e[lo - 1] > tolK) && (sm.sl_e[lo] - t > tolK);
+        int i = min(lo, L - 1);
+        io.token[d] = sm.sl_id[i];
+        if (io.flags) io.flags[d] = tier_flag;
+        need |= !ok;
+      }
+      need = __syncthreads_or(need);
+      if (need && tid == 0) sm.isc[7] = 1;
+    } else {
+      // ---------------- modes 0 and 2: per-warp masses, owner warp searches its range
+      if (mode == 2) {
+        // merge the warp's scratch list A with its kept bracket members into scratch M
+        // (both id-ordered): new position = own index + #other-list ids below.
+        if (tid <= RS_WARPS) {
+          // sl segment of warp w: ids in [w*C, (w+1)*C)
+          int w = tid, bound = min(V, w * C), lo = 0, hi = L;
+          while (lo < hi) {
+            int mid = (lo + hi) >> 1;
+            if (sm.sl_id[mid] < bound) lo = mid + 1;
+            else hi = mid;
+          }
+          sm.wsl[w] = (w == RS_WARPS) ? L : lo;
+        }
+        __syncthreads();
+        const int na = sm.wcount[warp];
+        const int s0 = sm.wsl[warp], s1 = sm.wsl[warp + 1];
+        const int nbw = s1 - s0;
+        if (na + nbw > SCR_PER_WARP) {
+          if (lane == 0) sm.isc[2] = 1;
+        } else {
+          for (int i = lane; i < na; i += 32) {
+            int id = scrA_id[warp * SCR_PER_WARP + i];
+            int lo = s0, hi = s1;
+            while (lo < hi) {
+              int mid = (lo + hi) >> 1;
+              if (sm.sl_id[mid] < id) lo = mid + 1;
+              else hi = mid;
+            }
+            int pos = i + (lo - s0);
+            scrM_id[warp * SCR_PER_WARP + pos] = id;
+            scrM_e[warp * SCR_PER_WARP + pos] = scrA_e[warp * SCR_PER_WARP + i];
+          }
+          double add = 0.0;
+          for (int b = s0 + lane; b < s1; b += 32) {
+            int id = sm.sl_id[b];
+            int lo = 0, hi = na;
+            while (lo < hi) {
+              int mid = (lo + hi) >> 1;
+              if (scrA_id[warp * SCR_PER_WARP + mid] < id) lo = mid + 1;
+              else hi = mid;
+            }
+            int pos = (b - s0) + lo;
+            scrM_id[warp * SCR_PER_WARP + pos] = id;
+            scrM_e[warp * SCR_PER_WARP + pos] = sm.sl_e[b];
+            add += sm.sl_e[b];
+          }
+          add = warp_sum(add);
+          if (lane == 0) {
+            sm.wsum[warp] += add;
+            sm.wcount[warp] = na + nbw;
+          }
+        }
+        __syncthreads();
+        if (sm.isc[2]) {
+          if (tid == 0) {
+            int pos = atomicAdd(REFINE ? ws.q_exact : ws.q_refine, 1);
+            (REFINE ? ws.q_exact : ws.q_refine)[1 + pos] = task_id;
+            atomicAdd(&counters[0], 1ull);
+          }
+          __syncthreads();
+          continue;
+        }
+        __threadfence_block();
+      } else {
+        if (lane == 0) sm.werr[warp] = sm.wsum[warp] * relE;
+      }
+      if (tid == 0) {
+        double c = 0.0;
+        for (int w = 0; w < RS_WARPS; ++w) {
+          sm.wpre[w] = c;
+          c += sm.wsum[w];
+        }
+        sm.wpre[RS_WARPS] = c;
+      }
+      __syncthreads();
+      const double K = sm.wpre[RS_WARPS];
+      // absolute error bounds: total mass, and prefix masses through warp w
+      const double EK = (mode == 0) ? E_S : K * ((double)(V + 64) * 4.0 * kEps64 + 4.0 * kRefExpErr);
+      double Epre = 0.0;
+      if (mode == 0) {
+        for (int w = 0; w <= warp; ++w) Epre += sm.werr[w];
+      } else {
+        Epre = EK;
+      }
+      int need = 0;
+      for (int64_t dbase = tv.d0; dbase < tv.d1; dbase += 32) {
+        const int64_t d = dbase + lane;
+        double t = 0.0, u = 0.0;
+        bool mine = false;
+        if (d < tv.d1) {
+          u = draw_u(io, d, tv);
+          t = u * K;
+          if (!(t < K)) {
+            if (warp == 0) need = 1;  // clamp region: let the next tier emulate it
+          } else {
+            mine = (t >= sm.wpre[warp]) && (t < sm.wpre[warp + 1]);
+          }
+        }
+        unsigned own = __ballot_sync(0xffffffffu, mine);
+        while (own) {
+          const int src = __ffs(own) - 1;
+          own &= own - 1;
+          const double tt = __shfl_sync(0xffffffffu, t, src);
+          const double uu = __shfl_sync(0xffffffffu, u, src);
+          int found = -1;
+          double flo = 0.0, fhi = 0.0;
+          double off = sm.wpre[warp];
+          if (mode == 0) {
+            for (int e0 = cb; e0 < ce; e0 += 256) {
+              const int my0 = e0 + 8 * lane;
+              float v[8];
+              load8<DT>(tv.row, my0, ce, vec, v);
+              double ev[8];
+              double ls = 0.0;
+#pragma unroll
+              for (int j = 0; j < 8; ++j) {
+                ev[j] = (my0 + j < ce) ? elem_exp<REFINE>(ec, v[j]) : 0.0;
+                ls += ev[j];
+              }
+              double x = ls;
+#pragma unroll
+              for (int o = 1; o < 32; o <<= 1) {
+                double y = __shfl_up_sync(0xffffffffu, x, o);
+                if (lane >= o) x += y;
+              }
+              const double excl = off + (x - ls);
+              const bool hit = (ls > 0.0) && (tt < off + x);
+              const unsigned hm = __ballot_sync(0xffffffffu, hit);
+              if (hm) {
+                const int hl = __ffs(hm) - 1;
+                if (lane == hl) {
+                  double c = excl;
+                  for (int j = 0; j < 8; ++j) {
+                    double nc = c + ev[j];
+                    if (ev[j] > 0.0 && tt < nc) {
+                      found = my0 + j;
+                      flo = c;
+                      fhi = nc;
+                      break;
+                    }
+                    c = nc;
+                  }
+                }
+                found = __shfl_sync(0xffffffffu, found, hl);
+                flo = __shfl_sync(0xffffffffu, flo, hl);
+                fhi = __shfl_sync(0xffffffffu, fhi, hl);
+                break;
+              }
+              off = __shfl_sync(0xffffffffu, off + x, 31);
+            }
+          } else {
+            const int n = sm.wcount[warp];
+            for (int i0 = 0; i0 < n; i0 += 32) {
+              const int i = i0 + lane;
+              double e = 0.0;
+              int id = -1;
+              if (i < n) {
+                e = scrM_e[warp * SCR_PER_WARP + i];
+                id = scrM_id[warp * SCR_PER_WARP + i];
+              }
+              double x = e;
+#pragma unroll
+              for (int o = 1; o < 32; o <<= 1) {
+                double y = __shfl_up_sync(0xffffffffu, x, o);
+                if (lane >= o) x += y;
+              }
+              const bool hit = (i < n) && (e > 0.0) && (tt < off + x);
+              const unsigned hm = __ballot_sync(0xffffffffu, hit);
+              if (hm) {
+                const int hl = __ffs(hm) - 1;
+                found = __shfl_sync(0xffffffffu, id, hl);
+                flo = __shfl_sync(0xffffffffu, off + x - e, hl);
+                fhi = __shfl_sync(0xffffffffu, off + x, hl);
+                break;
+              }
+              off = __shfl_sync(0xffffffffu, off + x, 31);
+            }
+          }
+          if (lane == 0) {
+            const double tol = uu * EK + Epre + tt * relRef * 4.0;
+            // flo == 0 with precise e's: nothing precedes the element, so t >= 0 lies on its
+            // right exactly.  FAST flushes e < 2^-126 to zero, so it must certify the margin.
+            bool ok = found >= 0 && (tt - flo > tol || ((REFINE || mode == 2) && flo == 0.0)) && (fhi - tt > tol);
+            io.token[dbase + src] = found;
+            if (io.flags) io.flags[dbase + src] = tier_flag;
+            need |= !ok;
+          }
+        }
+      }
+      need = __syncthreads_or(need);
+      if (need && tid == 0) sm.isc[7] = 1;
+    }
+    __syncthreads();
+    if (sm.isc[7] && tid == 0) {
+      int* q = REFINE ? ws.q_exact : ws.q_refine;
+      int pos = atomicAdd(q, 1);
+      q[1 + pos] = task_id;
+      atomicAdd(&counters[0], 1ull);
+    }
+    __syncthreads();
+  }
+}
+
+// ============================== EXACT kernel ==============================
+// numpy emulation (pairwise_seq in lc_numpy.cuh).
+
+constexpr int EX_THREADS = 256;
+
+template <int DT>
+__global__ void __launch_bounds__(EX_THREADS)
+exact_kernel(const char* __restrict__ rows, int64_t row_bytes, int Vdef, const lc_task* __restrict__ tasks,
+             const int* __restrict__ task_list, CacheMap cm, DrawIO io, double* scratch, int32_t* iscratch,
+             int64_t scr_stride, unsigned long long* counters) {
+  const int ntask = task_list[0];
+  double* p = scratch + (int64_t)blockIdx.x * scr_stride * 3;  // probabilities
+  double* q = p + scr_stride;                                   // truncated, renormalised
+  double* tmp = q + scr_stride;                                 // kept values in sorted order
+  int32_t* ord = iscratch + (int64_t)blockIdx.x * scr_stride;   // kept ids in sorted order
+  __shared__ float s_m;
+  __shared__ double s_S;
+  __shared__ int s_L;
+  __shared__ double s_bp[EX_THREADS];
+  __shared__ int s_bi[EX_THREADS];
+  __shared__ int s_stop;
+  const int tid = threadIdx.x;
+  for (int ti = blockIdx.x; ti < ntask; ti += gridDim.x) {
+    const int task_id = task_list[1 + ti];
+    TaskView tv;
+    if (!resolve_task(tasks[task_id], rows, row_bytes, Vdef, cm, tv)) continue;
+    const int V = tv.V;
+    // max (fp32 exact)
+    float mloc = -INFINITY;
+    for (int i = tid; i < V; i += EX_THREADS) mloc = fmaxf(mloc, load1<DT>(tv.row, i));
+    mloc = warp_max(mloc);
+    s_bp[tid] = (double)mloc;
+    __syncthreads();
+    if (tid == 0) {
+      float m = -INFINITY;
+      for (int w = 0; w < EX_THREADS; w += 32) m = fmaxf(m, (float)s_bp[w]);
+      s_m = m;
+    }
+    __syncthreads();
+    ExpCtx ec;
+    ec.m = s_m;
+    ec.T = tv.T;
+    ec.mT = __ddiv_rn((double)s_m, tv.T);
+    for (int i = tid; i < V; i += EX_THREADS) p[i] = ref_exp(ec, load1<DT>(tv.row, i));
+    __syncthreads();
+    if (tid == 0) s_S = pairwise_seq(p, V);
+    __syncthreads();
+    for (int i = tid; i < V; i += EX_THREADS) p[i] = __ddiv_rn(p[i], s_S);
+    __syncthreads();
+    int L = V;
+    if (tv.trunc) {
+      // kept prefix of the (p desc, id asc) order, one element per block-wide argmax
+      const int lim = tv.topk > 0 ? tv.topk : V;
+      double last_p = INFINITY;
+      int last_id = -1;
+      double c = 0.0;
+      int n = 0;
+      if (tid == 0) s_stop = 0;
+      __syncthreads();
+      while (n < lim) {
+        double bp = -1.0;
+        int bi = INT_MAX;
+        for (int i = tid; i < V; i += EX_THREADS) {
+          double pi = p[i];
+          bool after = (pi < last_p) || (pi == last_p && i > last_id);
+          if (after && (pi > bp || (pi == bp && i < bi))) {
+            bp = pi;
+            bi = i;
+          }
+        }
+        s_bp[tid] = bp;
+        s_bi[tid] = bi;
+        __syncthreads();
+        for (int s = EX_THREADS / 2; s > 0; s >>= 1) {
+          if (tid < s) {
+            double op = s_bp[tid + s];
+            int oi = s_bi[tid + s];
+            if (op > s_bp[tid] || (op == s_bp[tid] && oi < s_bi[tid])) {
+              s_bp[tid] = op;
+              s_bi[tid] = oi;
+            }
+          }
+          __syncthreads();
+        }
+        bp = s_bp[0];
+        bi = s_bi[0];
+        __syncthreads();
+        if (bi == INT_MAX) break;
+        if (tid == 0) ord[n] = bi;
+        ++n;
+        last_p = bp;
+        last_id = bi;
+        if (tv.topp < 1.0) {
+          c += bp;  // sequential cumsum in sorted order (all threads track it identically)
+          if (c >= tv.topp) break;
+        }
+      }
+      L = n;
+      __syncthreads();
+      if (tid == 0) {
+        for (int i = 0; i < L; ++i) tmp[i] = p[ord[i]];
+        double ks = pairwise_seq(tmp, L);
+        for (int i = 0; i < V; ++i) q[i] = 0.0;
+        for (int i = 0; i < L; ++i) q[ord[i]] = __ddiv_rn(tmp[i], ks);
+      }
+    } else {
+      for (int i = tid; i < V; i += EX_THREADS) q[i] = p[i];
+    }
+    __syncthreads();
+    if (tid == 0) {
+      s_L = L;
+      s_S = pairwise_seq(q, V);  // total = q.sum()
+    }
+    __syncthreads();
+    const double Q = s_S;
+    for (int64_t d = tv.d0 + tid; d < tv.d1; d += EX_THREADS) {
+      const double u = draw_u(io, d, tv);
+      const double t = u * Q;
+      int tok;
+      uint8_t fl = LC_DRAW_PRECISE;
+      if (!(Q > 0.0)) {
+        tok = -1;
+        fl |= LC_DRAW_BAD_ROW;
+      } else {
+        double c = 0.0, prev = 0.0;
+        int i = 0;
+        for (; i < V; ++i) {
+          prev = c;
+          c += q[i];
+          if (c > t) break;
+        }
+        double margin = (i < V) ? fmin(t - prev, c - t) : t - c;
+        if (i >= V) i = V - 1;
+        while (i > 0 && q[i] == 0.0) --i;
+        tok = i;
+        // exp may differ from numpy's by an ulp: flag razor-thin margins
+        if (margin <= fmax(t, 1e-300) * 64.0 * kEps64) {
+          fl |= LC_DRAW_UNRESOLVED;
+          atomicAdd(&counters[1], 1ull);
+        }
+      }
+      io.token[d] = tok;
+      if (io.flags) io.flags[d] = fl;
+    }
+    __syncthreads();
+  }
+}
+
+// ============================== host launcher ==============================
+
+static int g_num_sms = 0;
+
+static int num_sms() {
+  if (g_num_sms == 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || g_num_sms <= 0)
+      g_num_sms = 148;
+  }
+  return g_num_sms;
+}
+
+constexpr int kExactCtas = 32;
+
+int64_t workspace_bytes(int64_t n_tasks, int64_t vocab) {
+  const int64_t grid = num_sms();
+  int64_t b = 0;
+  b += 2 * (((n_tasks + 1) * 4 + 255) & ~255ll);
+  b += ((grid * 2 * SCR_PER_CTA * 4) + 255) & ~255ll;
+  b += ((grid * 2 * SCR_PER_CTA * 8) + 255) & ~255ll;
+  b += ((kExactCtas * vocab * 3 * 8) + 255) & ~255ll;
+  b += ((kExactCtas * vocab * 4) + 255) & ~255ll;
+  b += 256;
+  return b;
+}
+
+template <int DT>
+static int launch_all(const char* rows, int64_t row_bytes, int V, const lc_task* tasks, int64_t n_tasks, CacheMap cm,
+                      DrawIO io, void* d_ws, int64_t ws_bytes, int64_t* d_counters, cudaStream_t st) {
+  if (n_tasks > INT32_MAX - 2) return LC_E_ARG;
+  const int grid = num_sms();
+  char* p = (char*)d_ws;
+  auto take = [&](int64_t n) {
+    char* r = p;
+    p += (n + 255) & ~255ll;
+    return r;
+  };
+  Workspace ws;
+  ws.q_refine = (int*)take((n_tasks + 1) * 4);
+  ws.q_exact = (int*)take((n_tasks + 1) * 4);
+  ws.scr_id = (int*)take((int64_t)grid * 2 * SCR_PER_CTA * 4);
+  ws.scr_e = (double*)take((int64_t)grid * 2 * SCR_PER_CTA * 8);
+  const int64_t scr_stride = V;
+  double* ex_scr = (double*)take(kExactCtas * scr_stride * 3 * 8);
+  int32_t* ex_iscr = (int32_t*)take(kExactCtas * scr_stride * 4);
+  unsigned long long* cnt = (unsigned long long*)take(64);
+  if (!d_ws || p - (char*)d_ws > ws_bytes) {
+    lcb_set_last_error("resample workspace too small (see lc_resample_workspace_bytes)", __FILE__, __LINE__);
+    return LC_E_ARG;
+  }
+  LCB_CUDA_TRY(cudaMemsetAsync(ws.q_refine, 0, 4, st));
+  LCB_CUDA_TRY(cudaMemsetAsync(ws.q_exact, 0, 4, st));
+  unsigned long long* counters = d_counters ? (unsigned long long*)d_counters : cnt;
+  if (!d_counters) LCB_CUDA_TRY(cudaMemsetAsync(cnt, 0, 64, st));
+
+  const size_t smem = sizeof(Smem);
+  static bool attr_set[2] = {false, false};
+  if (!attr_set[DT]) {
+    LCB_CUDA_TRY(cudaFuncSetAttribute(resample_kernel<DT, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      (int)smem));
+    LCB_CUDA_TRY(cudaFuncSetAttribute(resample_kernel<DT, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      (int)smem));
+    attr_set[DT] = true;
+  }
+  const int g1 = (int)(n_tasks < grid ? n_tasks : grid);
+  resample_kernel<DT, false><<<g1, RS_THREADS, smem, st>>>(rows, row_bytes, V, tasks, (int)n_tasks, nullptr, cm, io,
+                                                            ws, counters);
+  LCB_CUDA_TRY(cudaGetLastError());
+  resample_kernel<DT, true><<<grid, RS_THREADS, smem, st>>>(rows, row_bytes, V, tasks, (int)n_tasks, ws.q_refine, cm,
+                                                            io, ws, counters);
+  LCB_CUDA_TRY(cudaGetLastError());
+  exact_kernel<DT><<<kExactCtas, EX_THREADS, 0, st>>>(rows, row_bytes, V, tasks, ws.q_exact, cm, io, ex_scr, ex_iscr,
+                                                      scr_stride, counters);
+  LCB_CUDA_TRY(cudaGetLastError());
+  return LC_OK;
+}
+
+int resample_launch(const void* rows, int dtype, int64_t vocab, int64_t row_stride, const lc_task* tasks,
+                    int64_t n_tasks, lc_draws draws, const int32_t* pages, int max_pages, int page_rows, void* ws,
+                    int64_t ws_bytes, int64_t* counters, cudaStream_t st) {
+  if (n_tasks < 0 || vocab < 1 || vocab > (1 << 28) || !draws.d_token) return LC_E_ARG;
+  if (!draws.d_u && !draws.d_seed) return LC_E_ARG;
+  if (n_tasks == 0) return LC_OK;
+  DrawIO io{draws.d_u, draws.d_seed, draws.d_index, draws.d_token, draws.d_flags};
+  CacheMap cm{pages, max_pages, page_rows};
+  const int64_t esz = dtype == LC_BF16 ? 2 : 4;
+  if (dtype == LC_BF16)
+    return launch_all<LC_BF16>((const char*)rows, row_stride * esz, (int)vocab, tasks, n_tasks, cm, io, ws, ws_bytes,
+                               counters, st);
+  if (dtype == LC_F32)
+    return launch_all<LC_F32>((const char*)rows, row_stride * esz, (int)vocab, tasks, n_tasks, cm, io, ws, ws_bytes,
+                              counters, st);
+  return LC_E_ARG;
+}
+
+}  // namespace lcb
+
+extern "C" int64_t lc_resample_workspace_bytes(int64_t n_tasks, int64_t vocab) {
+  return lcb::workspace_bytes(n_tasks, vocab);
+}
+
+extern "C" int lc_resample(const void* d_rows, int dtype, int64_t vocab, int64_t row_stride, const lc_task* d_tasks,
+                           int64_t n_tasks, lc_draws draws, void* d_workspace, int64_t workspace_bytes,
+                           int64_t* d_counters, void* stream) {
+  if (n_tasks == 0) return LC_OK;
+  if (!d_rows || !d_tasks) return LC_E_ARG;
+  return lcb::resample_launch(d_rows, dtype, vocab, row_stride, d_tasks, n_tasks, draws, nullptr, 0, 1, d_workspace,
+                              workspace_bytes, d_counters, (cudaStream_t)stream);
+}
+
+// Test probe: the FAST tier's exponential, so the GPU tests can measure its
+// error against an fp64 reference and pin kEx2RelErr.
+namespace lcb {
+__global__ void probe_fast_exp_kernel(const float* z, int64_t n, float m, double T, float* out) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  ExpCtx c;
+  c.m = m;
+  c.T = T;
+  c.mT = __ddiv_rn((double)m, T);
+  double Ld = 1.4426950408889634 / T;
+  c.Lhi = (float)Ld;
+  c.Llo = (float)(Ld - (double)c.Lhi);
+  out[i] = fast_exp(c, z[i]);
+}
+}  // namespace lcb
+
+extern "C" int lc_probe_fast_exp(const float* d_z, int64_t n, float m, double temperature, float* d_out,
+                                 void* stream) {
+  if (n <= 0) return n == 0 ? LC_OK : LC_E_ARG;
+  lcb::probe_fast_exp_kernel<<<lcb::ceil_div(n, 256), 256, 0, (cudaStream_t)stream>>>(d_z, n, m, temperature, d_out);
+  LCB_CUDA_TRY(cudaGetLastError());
+  return LC_OK;
+}

@@ -1,0 +1,345 @@
+"""GPU parity: the CUDA path (through the C ABI) vs the CPU oracle and the
+reference's golden vectors.  Bit-exact for tokens, kept sets, hashes,
+uniforms, hit/miss and slots; probabilities within 1e-5 relative (fp32) --
+the tolerance BASELINE.json's north star states.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import cache_ref, mixing_ref, sampling_ref
+from tests.golden_io import load_json, sampling_cases
+
+pytestmark = pytest.mark.gpu
+
+lcb = pytest.importorskip("paper_2604_17353_b200")
+from paper_2604_17353_b200 import _capi  # noqa: E402
+
+DEV = torch.device("cuda", 0)
+
+
+def _resample_rows(rows: np.ndarray, T, k, p, u_lists, dtype=torch.float32):
+    """One task per row; row i draws u_lists[i]."""
+    z = torch.from_numpy(np.ascontiguousarray(rows, dtype=np.float32)).to(DEV).to(dtype)
+    n = len(rows)
+    counts = np.array([len(x) for x in u_lists])
+    begin = np.concatenate([[0], np.cumsum(counts)[:-1]])
+    tasks = lcb.make_tasks(row=np.arange(n), temperature=T, top_k=k, top_p=p, draw_begin=begin,
+                           draw_end=begin + counts)
+    u = torch.tensor(np.concatenate(u_lists), dtype=torch.float64, device=DEV)
+    cnt = torch.zeros(8, dtype=torch.int64, device=DEV)
+    tok, fl = lcb.resample(z, tasks, u=u, counters=cnt)
+    return tok.cpu().numpy(), fl.cpu().numpy(), cnt.cpu().numpy()
+
+
+# -- mixing ----------------------------------------------------------------------------
+
+
+def test_hash_prefix_golden():
+    g = load_json("mixing.json")
+    seqs = [s for s, _ in g["hash"]]
+    got = lcb.mixing.hash_prompts(seqs)
+    assert [int(x) for x in got.cpu().numpy().view(np.uint64)] == [h for _, h in g["hash"]]
+    # prefix extension from a parent digest
+    toks = list(range(1, 300))
+    par = lcb.mixing.hash_prompts([toks[:100]])
+    ext = lcb.mixing.hash_prompts([toks[100:]], parents=par.cpu().numpy().view(np.uint64))
+    assert int(ext.cpu().numpy().view(np.uint64)[0]) == mixing_ref.hash_tokens(toks)
+
+
+def test_uniforms_golden():
+    g = load_json("mixing.json")
+    for seed, us in g["uniform"]:
+        got = lcb.uniforms([seed] * len(us), np.arange(len(us))).cpu().numpy()
+        assert got.tolist() == us
+
+
+def test_fill_logits_matches_reference_producer():
+    g = load_json("mixing.json")
+    for vocab, state, conc, rng, want in g["fill"]:
+        st = lcb._dev.u64_tensor([state], DEV)
+        out = torch.empty(vocab, dtype=torch.float32, device=DEV)
+        _capi.check(_capi.lib.lc_fill_logits(st.data_ptr(), 1, vocab, conc, rng, _capi.LC_F32, out.data_ptr(), vocab,
+                                             None))
+        bits = out.cpu().numpy().view(np.uint32)
+        if vocab <= 1000:
+            assert bits.tolist() == want
+        else:
+            assert int(bits.sum(dtype=np.uint64)) == want[0] and bits[:4].tolist() == want[1]
+        outb = torch.empty(vocab, dtype=torch.bfloat16, device=DEV)
+        _capi.check(_capi.lib.lc_fill_logits(st.data_ptr(), 1, vocab, conc, rng, _capi.LC_BF16, outb.data_ptr(),
+                                             vocab, None))
+        ref = mixing_ref.bf16_round(mixing_ref.fill_logits_np(state, vocab, conc, rng))
+        assert np.array_equal(outb.float().cpu().numpy(), ref)
+
+
+# -- fast-tier error model ------------------------------------------------------------------
+
+
+def test_fast_exp_error_bound():
+    """kEx2RelErr (lc_resample.cu) must bound the FAST exponential's relative error."""
+    rng = np.random.default_rng(0)
+    worst = 0.0
+    for T in (0.01, 0.1, 0.6, 1.0, 1.3, 7.0):
+        m = np.float32(rng.normal() * 4)
+        z = (m - rng.random(1 << 20) * 60 * T).astype(np.float32)
+        z[:1024] = np.nextafter(m, np.float32(-np.inf), dtype=np.float32) - np.arange(1024, dtype=np.float32) * 1e-6
+        zt = torch.from_numpy(z).to(DEV)
+        out = torch.empty_like(zt)
+        _capi.check(_capi.lib.lc_probe_fast_exp(zt.data_ptr(), z.size, float(m), T, out.data_ptr(), None))
+        got = out.cpu().numpy().astype(np.float64)
+        exact = np.exp((z.astype(np.float64) - np.float64(m)) / T)
+        ok = exact > 1e-37
+        rel = np.abs(got[ok] - exact[ok]) / exact[ok]
+        worst = max(worst, float(rel.max()))
+    assert worst < 4.0e-7, worst
+
+
+# -- resample vs golden (reference) ----------------------------------------------------------
+
+
+@pytest.mark.parametrize("as_bf16", [False, True])
+def test_resample_golden_cases(as_bf16):
+    cases = sampling_cases()
+    if as_bf16:  # rows that are exactly bf16-representable can go through the bf16 kernels
+        cases = [c for c in cases if c.name.startswith("bf16_")]
+    n_checked = 0
+    for c in cases:
+        tok, fl, _ = _resample_rows(c.z[None, :], c.T, c.top_k, c.top_p, [c.u],
+                                    dtype=torch.bfloat16 if as_bf16 else torch.float32)
+        assert tok.tolist() == c.tokens.tolist(), (c.name, c.T, c.top_k, c.top_p)
+        assert not np.any(fl & _capi.LC_DRAW_UNRESOLVED)
+        n_checked += len(c.u)
+    assert n_checked > (500 if as_bf16 else 4000)
+
+
+def _oracle_tokens(rows, T, k, p, ulists):
+    out = []
+    for z, us in zip(rows, ulists):
+        q = sampling_ref.truncate(sampling_ref.softmax(z, T), k, p)
+        out += [sampling_ref.draw(q, float(u)) for u in us]
+    return out
+
+
+@pytest.mark.parametrize("V,conc,T,k,p,bf16", [
+    (32000, 2.5, 0.6, None, 1.0, False),   # config 1 shape (fp32, untruncated)
+    (32000, 2.5, 0.6, None, 0.9, True),    # config 2 shape (bf16, top-p 0.9)
+    (32000, 0.0, 0.6, None, 0.9, True),    # flat worst case: large nucleus
+    (32000, 0.0, 1.0, None, 1.0, False),
+    (151936, 2.5, 0.6, 50, 0.95, True),    # configs 3/5 shape
+    (128256, 2.5, 0.6, None, 1.0, True),
+    (4099, 1.0, 0.25, 3, 0.999, False),
+])
+def test_resample_matches_oracle(V, conc, T, k, p, bf16):
+    rng = np.random.default_rng(V + int(conc * 10) + int(T * 100))
+    nrows = 24 if V > 100000 else 64
+    states = [mixing_ref.mix2(7, 10_000 + i) for i in range(nrows)]
+    rows = mixing_ref.fill_rows_np(states, V, conc)
+    if bf16:
+        rows = mixing_ref.bf16_round(rows)
+    ulists = [rng.random(8).tolist() + [0.0] for _ in range(nrows)]
+    tok, fl, cnt = _resample_rows(rows, T, k, p, ulists, dtype=torch.bfloat16 if bf16 else torch.float32)
+    want = _oracle_tokens(rows, T, k, p, ulists)
+    assert tok.tolist() == want
+    assert not np.any(fl & _capi.LC_DRAW_UNRESOLVED)
+
+
+def test_seed_mode_uniforms_equal_explicit_u():
+    V = 1000
+    rows = mixing_ref.fill_rows_np([mixing_ref.mix2(3, i) for i in range(16)], V, 1.0)
+    seeds = [mixing_ref.mix2(1, b) for b in range(4)]
+    # task t (row t, position pos=t) draws 4 branches with u = uniform(seed_b, t)
+    tasks = lcb.make_tasks(row=np.arange(16), pos=np.arange(16), temperature=0.8, top_p=0.9,
+                           draw_begin=np.arange(16) * 4, draw_end=np.arange(16) * 4 + 4, seed_base=0)
+    z = torch.from_numpy(rows).to(DEV)
+    sd = lcb._dev.u64_tensor(seeds, DEV)
+    tok, _ = lcb.resample(z, tasks, seeds=sd, n_draws=64)
+    want = []
+    for t in range(16):
+        for b in range(4):
+            want += _oracle_tokens(rows[t:t + 1], 0.8, None, 0.9, [[mixing_ref.uniform(seeds[b], t)]])
+    assert tok.cpu().tolist() == want
+
+
+def test_edge_rows():
+    # NaN row is flagged; -inf entries are zero-probability; T == 0 is greedy
+    z = np.array([[1.0, np.nan, 0.0, 2.0], [-np.inf, 3.0, -np.inf, 3.0], [5.0, 5.0, 1.0, -1.0]], dtype=np.float32)
+    tok, fl, _ = _resample_rows(z, 1.0, None, 1.0, [[0.5], [0.1, 0.9], [0.3]])
+    assert tok[0] == -1 and fl[0] & _capi.LC_DRAW_BAD_ROW
+    want = _oracle_tokens(z[1:], 1.0, None, 1.0, [[0.1, 0.9], [0.3]])
+    assert tok[1:].tolist() == want
+    tok0, _, _ = _resample_rows(z[2:], 0.0, 2, 0.5, [[0.0, 0.99]])
+    assert tok0.tolist() == [0, 0]
+
+
+def test_many_draws_per_row_shared():
+    """Best-of-N sharing: 64 draws per row in one task == oracle."""
+    V = 32000
+    rows = mixing_ref.bf16_round(mixing_ref.fill_rows_np([mixing_ref.mix2(9, i) for i in range(8)], V, 2.5))
+    rng = np.random.default_rng(5)
+    ulists = [rng.random(64).tolist() for _ in range(8)]
+    tok, _, _ = _resample_rows(rows, 0.6, None, 0.9, ulists, dtype=torch.bfloat16)
+    assert tok.tolist() == _oracle_tokens(rows, 0.6, None, 0.9, ulists)
+
+
+# -- probability-level API -------------------------------------------------------------------
+
+
+def test_probs_api_golden():
+    g = load_json("probs.json")
+    for case in g["cases"]:
+        p = np.array(case["p"])
+        q = lcb.truncate(p, case["top_k"], case["top_p"])
+        assert np.asarray(q).tolist() == case["q"]
+        for u, tok in case["draws"]:
+            class U:
+                def next_float(self, u=u):
+                    return u
+            assert lcb.sample(np.asarray(q), U()) == tok
+    with pytest.raises(RuntimeError):
+        lcb.sample(np.zeros(2), lcb.RngStream(1))
+
+
+def test_softmax_matches_oracle():
+    for V, T in ((3, 1.0), (64, 0.6), (32000, 0.6), (1000, 0.0)):
+        z = mixing_ref.fill_logits_np(mixing_ref.mix2(2, V), V, 2.5, 5.0)
+        got = lcb.softmax(z, T)
+        want = sampling_ref.softmax(z, T)
+        assert np.allclose(got, want, rtol=1e-12, atol=0)
+
+
+def test_hotspots_golden():
+    for case in load_json("hotspots.json"):
+        rows = np.array(case["rows"], dtype=np.uint32).view(np.float32)
+        cfg = lcb.SamplingConfig(temperature=case["T"], max_tokens=1)
+        hp = lcb.HotspotParams(decay=case["decay"], threshold=case["threshold"], max_hotspots=case["max_hotspots"])
+        assert list(lcb.identify_hotspots(list(rows), cfg, hp)) == case["hotspots"]
+
+
+# -- cache ---------------------------------------------------------------------------------------
+
+
+def test_cache_replays_reference_traces():
+    for tr in load_json("cache_traces.json"):
+        cache = lcb.LogitsCache(tr["budget"], vocab=16, key_capacity=64, max_rows=8)
+        pinned = {}
+        for op in tr["ops"]:
+            kind, digest, state = op[0], op[1], op[-1]
+            if kind == "lookup":
+                e = cache.lookup(lcb.StateKey(digest))
+                assert (e is not None) == op[2]
+            elif kind == "update":
+                n, v = op[2], op[3]
+                cache.update(lcb.StateKey(digest), np.zeros((n, v), np.float32), list(range(n)))
+            elif kind == "pin":
+                e = cache.entries[digest]
+                cache.pin(e)
+            elif kind == "unpin":
+                e = cache.entries[digest]
+                cache.unpin(e)
+            assert sorted(cache.entries) == state["present"], kind
+            assert cache.total_bytes == state["total"]
+            assert cache.hits == state["hits"] and cache.lookups == state["lookups"]
+
+
+def test_cache_slots_match_oracle_under_batches():
+    """Batched inserts/lookups: hit/miss, slots and victims bit-exact vs the oracle allocator."""
+    rng = np.random.default_rng(42)
+    V, page_rows = 64, 4
+    one = 6 * V * 4 + 6 * 8
+    budget = one * 20
+    cache = lcb.LogitsCache(budget, vocab=V, key_capacity=128, page_rows=page_rows, max_rows=8, page_capacity=256)
+    orc = cache_ref.CacheOracle(budget, 128, 256, page_rows)
+    keys = [mixing_ref.hash_tokens([i, 77]) for i in range(60)]
+    for step in range(40):
+        nb = int(rng.integers(1, 24))
+        batch = [keys[int(i)] for i in rng.integers(0, len(keys), nb)]
+        if rng.random() < 0.5:
+            dg = lcb._dev.u64_tensor(batch, DEV)
+            slot, gen, ln, vv = cache.lookup_batch(dg)
+            want = []
+            for d in batch:
+                e = orc.lookup(d)
+                want.append(-1 if e is None else e.slot)
+            assert slot.cpu().tolist() == want
+        else:
+            lens = rng.integers(0, 8, nb).astype(np.int32)
+            offs = np.concatenate([[0], np.cumsum(lens)[:-1]]).astype(np.int64)
+            tot = int(lens.sum()) or 1
+            rows = torch.randn(tot, V, device=DEV)
+            toks = torch.arange(tot, dtype=torch.int32, device=DEV)
+            slot, gen = cache.insert_batch(lcb._dev.u64_tensor(batch, DEV), torch.from_numpy(lens).to(DEV),
+                                           torch.full((nb,), V, dtype=torch.int32, device=DEV), rows,
+                                           torch.from_numpy(offs).to(DEV), toks, int(lens.max()))
+            want = [orc.insert(d, int(n), V)[0].slot for d, n in zip(batch, lens)]
+            assert slot.cpu().tolist() == want
+        st = cache._stats()
+        assert st.entries == len(orc.entries)
+        assert st.total_bytes == orc.total
+        assert st.hits == orc.hits and st.lookups == orc.lookups
+        snap = cache._snapshot()
+        live = {int(snap["digest"][s]): int(s) for s in np.flatnonzero(snap["alive"])}
+        assert live == {d: e.slot for d, e in orc.entries.items()}
+
+
+def test_cache_update_shape_errors_and_accounting():
+    cache = lcb.LogitsCache()
+    with pytest.raises(lcb.ConfigError):
+        cache.update(lcb.StateKey.of([1]), np.zeros((5, 8), np.float32), [1, 2, 3])
+    z = np.random.default_rng(0).normal(size=(500, 256)).astype(np.float32)
+    e = cache.update(lcb.StateKey.of([1]), z, list(range(500)))
+    assert e.nbytes == 500 * 256 * 4 + 500 * lcb.TOKEN_OVERHEAD_BYTES
+    assert cache.total_bytes == e.nbytes
+    got = cache.lookup(lcb.StateKey.of([1]))
+    assert got.logits_seq.shape == (500, 256) and got.token_seq == list(range(500))
+    assert np.array_equal(got.logits_seq, z)
+
+
+def test_cache_narrow_then_wide_entries():
+    cache = lcb.LogitsCache()
+    cache.update(lcb.StateKey.of([1, 2]), np.ones((5, 32), np.float32), [0, 1, 2, 3, 4])
+    cache.update(lcb.StateKey.of([3]), np.ones((2, 64), np.float32), [0, 1])
+    a = cache.lookup(lcb.StateKey.of([1, 2]))
+    assert a.vocab_size == 32 and a.logits_seq.shape == (5, 32) and np.all(a.logits_seq == 1)
+    assert len(cache) == 2
+
+
+def test_replay_stepwise_matches_oracle():
+    """Fused lookup -> speculative step-wise resample -> acceptance vs the oracle."""
+    V, n_req, L, nb = 2048, 6, 40, 5
+    cache = lcb.LogitsCache(1 << 30, vocab=V, dtype="bfloat16", max_rows=64)
+    prompts = [[r, 3, 5] for r in range(n_req)]
+    keys = [mixing_ref.hash_tokens(p) for p in prompts]
+    rows = mixing_ref.bf16_round(mixing_ref.fill_rows_np([mixing_ref.mix2(5, i) for i in range(n_req * L)], V, 2.5))
+    cached_tok = np.random.default_rng(1).integers(0, V, n_req * L).astype(np.int32)
+    # make early positions agree with the likely sample so replays run for a while
+    cached_tok = np.where(np.arange(n_req * L) % L < 10, rows.argmax(1), cached_tok).astype(np.int32)
+    lens = np.full(n_req, L, np.int32)
+    lens[1] = 17
+    offs = (np.arange(n_req) * L).astype(np.int64)
+    cache.insert_batch(lcb._dev.u64_tensor(keys, DEV), torch.from_numpy(lens).to(DEV),
+                       torch.full((n_req,), V, dtype=torch.int32, device=DEV),
+                       torch.from_numpy(rows).to(DEV).to(torch.bfloat16), torch.from_numpy(offs).to(DEV),
+                       torch.from_numpy(cached_tok).to(DEV), L)
+    digests = lcb._dev.u64_tensor(keys + [12345], DEV)  # last request misses
+    seeds = [mixing_ref.mix2(1, b) for b in range((n_req + 1) * nb)]
+    T = torch.full((n_req + 1,), 0.6, dtype=torch.float64, device=DEV)
+    K = torch.zeros(n_req + 1, dtype=torch.int32, device=DEV)
+    Pp = torch.full((n_req + 1,), 0.9, dtype=torch.float64, device=DEV)
+    tok, rep, div, slot, ln = cache.replay_stepwise(digests, 32, nb, lcb._dev.u64_tensor(seeds, DEV), T, K, Pp)
+    rep = rep.cpu().numpy().reshape(n_req + 1, nb)
+    for r in range(n_req):
+        lim = min(int(lens[r]), 32)
+        for b in range(nb):
+            want_rep = 0
+            for t in range(lim):
+                u = mixing_ref.uniform(seeds[r * nb + b], t)
+                y = _oracle_tokens(rows[r * L + t: r * L + t + 1], 0.6, None, 0.9, [[u]])[0]
+                want_rep = t + 1
+                if y != cached_tok[r * L + t]:
+                    break
+            assert rep[r, b] == want_rep, (r, b)
+    assert np.all(rep[n_req] == 0)
