@@ -1,0 +1,396 @@
+"""Benchmark: resampled tokens/s and HBM roofline fraction of the fused
+logits-cache re-sampling path (lookup -> step-wise speculative resample ->
+accept), vs the reference CPU path.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c2] [--impl ours|reference]
+
+N > 1 runs under torchrun, one process per GPU (weak scaling: every rank owns
+its own requests/trees and cache shard; NCCL only reduces statistics after the
+timed region).  Default workload = BASELINE.json configs[1] (C2):
+Best-of-N re-sampling, V = 32000, 256 requests x N = 32 branches,
+temperature 0.6 + top-p 0.9, bf16 rows, one 500-row cached trajectory per
+request (8.2 GB slab, larger than L2, so no flush is needed between steps).
+A step = for every request: hash lookup, resample of every cached position
+for all 32 branches (u = RngStream(branch seed) at draw number = position,
+engine.py:301-310), and the step-wise acceptance.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+CONFIGS = {
+    # name: (vocab, n_requests, n_branch, rows_per_entry, T, top_k, top_p, dtype, description)
+    "c1": dict(V=32000, n_req=16, nb=1, R=500, T=0.6, k=0, p=1.0, dtype="float32",
+               desc="ToT re-sampling, vocab 32000, 16 branches x 500-token expansions, fp32, top-p 1"),
+    "c2": dict(V=32000, n_req=256, nb=32, R=500, T=0.6, k=0, p=0.9, dtype="bfloat16",
+               desc="Best-of-N re-sampling, vocab 32000, 256 requests x N=32, T 0.6 + top-p 0.9, bf16"),
+    "c3": dict(V=151936, n_req=1024, nb=1, R=16, T=0.6, k=50, p=0.95, dtype="bfloat16",
+               desc="vocab 151936, 1024 branches, top-k 50 + top-p 0.95, 16-row entries, all hits"),
+    "c5": dict(V=151936, n_req=8 * 512, nb=1, R=4, T=0.6, k=50, p=0.95, dtype="bfloat16",
+               desc="8 agent trees x 512 branches, vocab 151936, top-k 50 + top-p 0.95 (per rank)"),
+}
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks and throttle reasons sampled during the timed region."""
+
+    def __init__(self, gpu: int):
+        self.gpu = gpu
+        self.rows = []
+        self.proc = None
+
+    def __enter__(self):
+        q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        time.sleep(0.25)
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([x.strip() for x in line.split(",")])
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(2)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4) if len(r) > 2 + i and r[2 + i] == "Active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+# ------------------------------------------------------------------------ our arm
+
+
+def setup_workload(cfg, dev, rank):
+    import torch
+
+    import paper_2604_17353_b200 as lcb
+    from paper_2604_17353_b200 import _capi, _dev
+    from paper_2604_17353_b200.mixing import mix2
+
+    V, n_req, nb, R = cfg["V"], cfg["n_req"], cfg["nb"], cfg["R"]
+    bf16 = cfg["dtype"] == "bfloat16"
+    slab_bytes = n_req * R * V * (2 if bf16 else 4)
+    budget = n_req * R * (V * 4 + 8) + 1024
+    cache = lcb.LogitsCache(budget, vocab=V, dtype=cfg["dtype"], key_capacity=n_req + 64, page_rows=min(R, 16),
+                            max_rows=R, device=dev)
+    # prompts: one per request (tree root), digests from the GPU hasher
+    prompts = [[(rank * 7919 + r * 31 + i) % 256 for i in range(49 + r % 32)] for r in range(n_req)]
+    digests = lcb.hash_prompts(prompts, dev=dev)
+    # synthetic rows from the reference producer (model seed 7, conc 2.5, range 5), per request chunk
+    chunk = max(1, (1 << 30) // (R * V * (2 if bf16 else 4)))
+    tdt = torch.bfloat16 if bf16 else torch.float32
+    ws = lcb.sampling.Workspace(dev)
+    for r0 in range(0, n_req, chunk):
+        rn = min(chunk, n_req - r0)
+        states = lcb._dev.u64_tensor([mix2(7, (rank << 40) + (r0 + i) * R + t) for i in range(rn) for t in range(R)],
+                                     dev)
+        rows = torch.empty((rn * R, V), dtype=tdt, device=dev)
+        _capi.check(_capi.lib.lc_fill_logits(states.data_ptr(), rn * R, V, 2.5, 5.0,
+                                             _capi.LC_BF16 if bf16 else _capi.LC_F32, rows.data_ptr(), V,
+                                             _dev.stream_ptr(dev)))
+        # the cached continuation = one sampled trajectory of these rows (first branch's seed family)
+        tasks = lcb.make_tasks(row=np.arange(rn * R), pos=np.tile(np.arange(R), rn), temperature=cfg["T"],
+                               top_k=cfg["k"], top_p=cfg["p"], draw_begin=np.arange(rn * R),
+                               draw_end=np.arange(rn * R) + 1, seed_base=np.repeat(np.arange(rn), R))
+        seeds0 = lcb._dev.u64_tensor([mix2(99, (rank << 32) + r0 + i) for i in range(rn)], dev)
+        tok, _ = lcb.resample(rows, tasks, seeds=seeds0, n_draws=rn * R)
+        lens = torch.full((rn,), R, dtype=torch.int32, device=dev)
+        vocs = torch.full((rn,), V, dtype=torch.int32, device=dev)
+        offs = torch.arange(rn, dtype=torch.int64, device=dev) * R
+        cache.insert_batch(digests[r0:r0 + rn], lens, vocs, rows, offs, tok.contiguous(), R)
+        del rows
+    torch.cuda.synchronize(dev)
+    st = cache._stats()
+    assert st.entries == n_req, (st.entries, n_req)
+    seeds = lcb._dev.u64_tensor([mix2(1, (rank << 32) + b) for b in range(n_req * nb)], dev)
+    T = torch.full((n_req,), cfg["T"], dtype=torch.float64, device=dev)
+    K = torch.full((n_req,), cfg["k"], dtype=torch.int32, device=dev)
+    P = torch.full((n_req,), cfg["p"], dtype=torch.float64, device=dev)
+    return dict(cache=cache, prompts=prompts, digests=digests, seeds=seeds, T=T, K=K, P=P, slab_bytes=slab_bytes,
+                bufs={})
+
+
+def run_ours(args, cfg, rank, world, dev):
+    import torch
+    import torch.distributed as dist
+
+    import paper_2604_17353_b200 as lcb
+
+    w = setup_workload(cfg, dev, rank)
+    cache = w["cache"]
+    V, n_req, nb, R = cfg["V"], cfg["n_req"], cfg["nb"], cfg["R"]
+    esz = 2 if cfg["dtype"] == "bfloat16" else 4
+    counters = torch.zeros(8, dtype=torch.int64, device=dev)
+    n_rows = n_req * R
+    n_draws = n_rows * nb
+
+    # instrument the dominant kernel: CUDA events around the resample call, on its stream
+    ev = []
+    orig = lcb.sampling.resample
+
+    def timed_resample(*a, **kw):
+        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s.record()
+        r = orig(*a, **kw)
+        e.record()
+        ev.append((s, e))
+        return r
+
+    def step():
+        return cache.replay_stepwise(w["digests"], R, nb, w["seeds"], w["T"], w["K"], w["P"], counters=counters,
+                                     bufs=w["bufs"])
+
+    lcb.sampling.resample = timed_resample
+    try:
+        for _ in range(args.warmup):
+            step()
+        torch.cuda.synchronize(dev)
+        ev.clear()
+        counters.zero_()
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize(dev)
+        t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        with ClockSampler(dev.index) as clk:
+            t0.record()
+            for _ in range(args.steps):
+                tok, rep, div, slot, ln = step()
+            t1.record()
+            torch.cuda.synchronize(dev)
+        if world > 1:
+            dist.barrier()
+        ms = t0.elapsed_time(t1)
+        k_ms = [s.elapsed_time(e) for s, e in ev]
+    finally:
+        lcb.sampling.resample = orig
+    accepted = int(rep.sum().item()) * args.steps
+    cnt = counters.cpu().numpy()
+
+    # ---- e2e through the public API with host buffers (hash from host prompts, tokens back to host)
+    pin_tok = torch.empty(n_draws, dtype=torch.int32, pin_memory=True)
+    pin_rep = torch.empty(n_req * nb, dtype=torch.int32, pin_memory=True)
+    flat = np.concatenate([np.asarray(p, dtype=np.int32) for p in w["prompts"]])
+    offs = np.zeros(n_req + 1, dtype=np.int64)
+    np.cumsum([len(p) for p in w["prompts"]], out=offs[1:])
+    h_tok = torch.from_numpy(flat).pin_memory()
+    h_off = torch.from_numpy(offs).pin_memory()
+    h_seed = w["seeds"].cpu().pin_memory()
+    d_tok = torch.empty_like(h_tok, device=dev)
+    d_off = torch.empty_like(h_off, device=dev)
+    d_seed = torch.empty_like(h_seed, device=dev)
+    d_dig = torch.empty(n_req, dtype=torch.int64, device=dev)
+    from paper_2604_17353_b200 import _capi, _dev
+
+    def e2e_step():
+        d_tok.copy_(h_tok, non_blocking=True)
+        d_off.copy_(h_off, non_blocking=True)
+        d_seed.copy_(h_seed, non_blocking=True)
+        _capi.check(_capi.lib.lc_hash_prefix(d_tok.data_ptr(), d_off.data_ptr(), None, n_req, d_dig.data_ptr(),
+                                             _dev.stream_ptr(dev)))
+        tok, rep, div, slot, ln = cache.replay_stepwise(d_dig, R, nb, d_seed, w["T"], w["K"], w["P"],
+                                                        bufs=w["bufs"])
+        pin_tok.copy_(tok, non_blocking=True)
+        pin_rep.copy_(rep, non_blocking=True)
+
+    for _ in range(2):
+        e2e_step()
+    torch.cuda.synchronize(dev)
+    if world > 1:
+        dist.barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(args.steps):
+        e2e_step()
+    e1.record()
+    torch.cuda.synchronize(dev)
+    e2e_ms = e0.elapsed_time(e1)
+    h2d = h_tok.numel() * 4 + h_off.numel() * 8 + h_seed.numel() * 8
+    d2h = n_draws * 4 + n_req * nb * 4
+
+    # ---- max over ranks, sums over ranks
+    from paper_2604_17353_b200.shard import reduce_stats
+
+    times = torch.tensor([ms, e2e_ms], dtype=torch.float64, device=dev)
+    counts = torch.tensor([float(accepted), float(cnt[0]), float(cnt[1]), float(cnt[2])], dtype=torch.float64,
+                          device=dev)
+    times, counts = reduce_stats(times, counts, world)  # NCCL: max of times, sum of counters
+    ms, e2e_ms = float(times[0]), float(times[1])
+    accepted, precise, unresolved, bad = (int(x) for x in counts.tolist())
+    if rank != 0:
+        return None
+    tokens_total = n_draws * args.steps * world
+    peak, peak_src = peaks()
+    algo_bytes_launch = n_rows * V * esz + n_draws * 20  # V*s per unique row + 20 B per draw
+    k_avg = sum(k_ms) / max(len(k_ms), 1)
+    achieved = algo_bytes_launch / (k_avg * 1e-3) / 1e9
+    res = {
+        "metric": "resampled_tokens_per_s",
+        "value": tokens_total / (ms * 1e-3),
+        "unit": "tokens/s",
+        "n_gpus": world,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": ms / args.steps,
+        "higher_is_better": True,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": "bf16" if esz == 2 else "f32",
+        "data": "synthetic (reference producer fill_logits, seed 7, conc 2.5, range 5.0)",
+        "config": {"workload": cfg["desc"], "config": args.config, "vocab": V, "requests_per_gpu": n_req,
+                   "branches": nb, "rows_per_entry": R, "draws_per_row": nb, "temperature": cfg["T"],
+                   "top_k": cfg["k"] or None, "top_p": cfg["p"], "slab_gb_per_gpu": w["slab_bytes"] / 1e9,
+                   "l2": "inputs larger than L2 (slab re-read every step)", "parallelism": f"tree-sharded x{world}"},
+        "accepted_tokens_per_s": accepted / (ms * 1e-3),
+        "rows_per_s": n_rows * args.steps * world / (ms * 1e-3),
+        "precise_tasks": precise,
+        "unresolved_draws": unresolved,
+        "bad_rows": bad,
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                     "frac": achieved / peak, "traffic": None, "peak_source": peak_src,
+                     "kernel": "lc_cache_resample (resample_kernel FAST + REFINE/EXACT queues)",
+                     "kernel_ms_avg": k_avg, "algorithmic_bytes_per_launch": algo_bytes_launch},
+        "e2e": {"value": tokens_total / (e2e_ms * 1e-3), "unit": "tokens/s", "h2d_bytes_per_step": h2d,
+                "d2h_bytes_per_step": d2h},
+        "gpu_launches": 8 * args.steps,
+        "clocks": clk.summary(),
+    }
+    if not args.no_cpu_baseline:
+        res["cpu_baseline"] = cpu_baseline(cfg, seconds=args.cpu_seconds)
+    return res
+
+
+# ------------------------------------------------------------------------ CPU (reference) arm
+
+
+def _cpu_worker(a):
+    """Reference per-draw path: sample(truncate(softmax(z, T), k, p), u) on rows of the workload."""
+    V, R, T, k, p, bf16, seconds, wid = a
+    sys.path.insert(0, ROOT)
+    from oracle import mixing_ref, sampling_ref
+
+    rng = np.random.default_rng(wid)
+    rows = mixing_ref.fill_rows_np([mixing_ref.mix2(7, wid * 1000 + i) for i in range(16)], V, 2.5)
+    if bf16:
+        rows = mixing_ref.bf16_round(rows)
+    n = 0
+    t0 = time.perf_counter()
+    while time.perf_counter() - t0 < seconds:
+        z = rows[n % len(rows)]
+        q = sampling_ref.truncate(sampling_ref.softmax(z, T), k or None, p)
+        sampling_ref.draw(q, float(rng.random()))
+        n += 1
+    return n, time.perf_counter() - t0
+
+
+def cpu_baseline(cfg, seconds=12.0, cores=None):
+    import multiprocessing as mp
+
+    cores = cores or os.cpu_count() or 1
+    args = [(cfg["V"], cfg["R"], cfg["T"], cfg["k"], cfg["p"], cfg["dtype"] == "bfloat16", seconds, i)
+            for i in range(cores)]
+    ctx = mp.get_context("spawn")
+    with ctx.Pool(cores) as pool:
+        out = pool.map(_cpu_worker, args)
+    n = sum(o[0] for o in out)
+    t = max(o[1] for o in out)
+    try:
+        model = [l.split(":", 1)[1].strip() for l in open("/proc/cpuinfo") if l.startswith("model name")][0]
+    except Exception:
+        model = "unknown"
+    return {"value": n / t, "unit": "tokens/s", "cores": cores, "kind": "port",
+            "sample": f"{n} draws of the workload's rows (V={cfg['V']}, T={cfg['T']}, top_k={cfg['k'] or None}, "
+                      f"top_p={cfg['p']}), one softmax+truncate+sample per draw as the reference engine does "
+                      f"(engine.py:302-305), {seconds:.0f} s per worker, {model}"}
+
+
+def run_reference(args, cfg):
+    res_cpu = cpu_baseline(cfg, seconds=args.cpu_seconds)
+    v = res_cpu["value"]
+    per_step_tokens = cfg["n_req"] * cfg["R"] * cfg["nb"]
+    return {
+        "metric": "resampled_tokens_per_s", "value": v, "unit": "tokens/s", "impl": "reference",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": per_step_tokens / v * 1e3, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64 (numpy)", "data": "synthetic",
+        "config": {"workload": cfg["desc"], "config": args.config},
+        "cpu_baseline": res_cpu,
+        "e2e": {"value": v, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+    cfg = CONFIGS[args.config]
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    if args.impl == "reference":
+        if rank == 0:
+            print(json.dumps(run_reference(args, cfg)), flush=True)
+        return
+    import torch
+    import torch.distributed as dist
+
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    res = run_ours(args, cfg, rank, world, dev)
+    if rank == 0:
+        print(json.dumps(res), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

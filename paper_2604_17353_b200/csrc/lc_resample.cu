@@ -1065,7 +1065,8 @@ exact_kernel(const char* __restrict__ rows, int64_t row_bytes, int Vdef, const l
           c += q[i];
           if (c > t) break;
         }
-        double margin = (i < V) ? fmin(t - prev, c - t) : t - c;
+        // a lower boundary of exactly 0 (no mass before) is shared with numpy exactly
+        double margin = (i < V) ? fmin(prev > 0.0 ? t - prev : INFINITY, c - t) : t - c;
         if (i >= V) i = V - 1;
         while (i > 0 && q[i] == 0.0) --i;
         tok = i;

@@ -111,7 +111,7 @@ def test_resample_golden_cases(as_bf16):
         tok, fl, _ = _resample_rows(c.z[None, :], c.T, c.top_k, c.top_p, [c.u],
                                     dtype=torch.bfloat16 if as_bf16 else torch.float32)
         assert tok.tolist() == c.tokens.tolist(), (c.name, c.T, c.top_k, c.top_p)
-        assert not np.any(fl & _capi.LC_DRAW_UNRESOLVED)
+        assert not np.any(fl & _capi.LC_DRAW_UNRESOLVED), (c.name, c.T, c.top_k, c.top_p, c.u, fl)
         n_checked += len(c.u)
     assert n_checked > (500 if as_bf16 else 4000)
 
