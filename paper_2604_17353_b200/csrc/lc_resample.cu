@@ -508,6 +508,7 @@ resample_kernel(const char* __restrict__ rows, int64_t row_bytes, int Vdef, cons
           }
           sm.isc[3] = Lk;
           sm.isc[4] = unc;
+          if (unc) atomicAdd(&counters[3], 1ull);
         }
         __syncthreads();
         if (sm.isc[4]) fail = true;
@@ -518,6 +519,7 @@ resample_kernel(const char* __restrict__ rows, int64_t row_bytes, int Vdef, cons
         }
       } else if (tv.topk > 0) {
         fail = true;  // top-k candidates overflowed (heavy ties / k > 512) -> next tier
+        if (tid == 0) atomicAdd(&counters[7], 1ull);
       }
 
       if (!fail && !done) {
@@ -612,6 +614,7 @@ resample_kernel(const char* __restrict__ rows, int64_t row_bytes, int Vdef, cons
         __syncthreads();
         if (sm.isc[2]) {
           fail = true;
+          if (tid == 0) atomicAdd(&counters[7], 1ull);
         } else {
           // precise e of the certainly-kept elements (dense, per warp)
           const int nw = sm.wcount[warp];
@@ -660,6 +663,7 @@ resample_kernel(const char* __restrict__ rows, int64_t row_bytes, int Vdef, cons
             }
             sm.isc[3] = cut + 1;
             sm.isc[4] = unc;
+            if (unc) atomicAdd(&counters[4], 1ull);
           }
           __syncthreads();
           if (sm.isc[4]) {
@@ -924,6 +928,7 @@ resample_kernel(const char* __restrict__ rows, int64_t row_bytes, int Vdef, cons
       if (need && tid == 0) sm.isc[7] = 1;
     }
     __syncthreads();
+    if (sm.isc[7] && tid == 0) atomicAdd(&counters[5], 1ull);
     if (sm.isc[7] && tid == 0) {
       int* q = REFINE ? ws.q_exact : ws.q_refine;
       int pos = atomicAdd(q, 1);
