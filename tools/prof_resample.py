@@ -1,0 +1,63 @@
+"""Standalone driver for profiling the resample kernel (ncu target).
+
+python tools/prof_resample.py --V 32000 --rows 4096 --draws 32 --top-p 0.9 --bf16 --iters 3
+Prints per-call CUDA-event times and the tier/reason counters
+(0 requeued tasks, 1 unresolved draws, 2 bad rows, 3 small-cut uncertain,
+4 large-nucleus uncertain, 5 draw uncertain, 7 candidate/scratch overflow).
+"""
+
+from __future__ import annotations
+
+import argparse
+import os
+import sys
+
+import numpy as np
+import torch
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import paper_2604_17353_b200 as lcb  # noqa: E402
+from paper_2604_17353_b200 import _capi, _dev  # noqa: E402
+from paper_2604_17353_b200.mixing import mix2  # noqa: E402
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--V", type=int, default=32000)
+    ap.add_argument("--rows", type=int, default=4096)
+    ap.add_argument("--draws", type=int, default=32)
+    ap.add_argument("--T", type=float, default=0.6)
+    ap.add_argument("--top-k", type=int, default=0)
+    ap.add_argument("--top-p", type=float, default=0.9)
+    ap.add_argument("--conc", type=float, default=2.5)
+    ap.add_argument("--bf16", action="store_true")
+    ap.add_argument("--iters", type=int, default=3)
+    a = ap.parse_args()
+    dev = torch.device("cuda", 0)
+    dt = torch.bfloat16 if a.bf16 else torch.float32
+    states = _dev.u64_tensor([mix2(7, i) for i in range(a.rows)], dev)
+    rows = torch.empty((a.rows, a.V), dtype=dt, device=dev)
+    _capi.check(_capi.lib.lc_fill_logits(states.data_ptr(), a.rows, a.V, a.conc, 5.0,
+                                         _capi.LC_BF16 if a.bf16 else _capi.LC_F32, rows.data_ptr(), a.V, None))
+    n = a.rows
+    tasks = lcb.make_tasks(row=np.arange(n), pos=np.arange(n) % 500, temperature=a.T, top_k=a.top_k, top_p=a.top_p,
+                           draw_begin=np.arange(n) * a.draws, draw_end=np.arange(n) * a.draws + a.draws,
+                           seed_base=np.arange(n) % 256 * a.draws)
+    tt = torch.from_numpy(tasks.view(np.uint8).copy()).to(dev)
+    seeds = _dev.u64_tensor([mix2(1, b) for b in range(256 * a.draws)], dev)
+    cnt = torch.zeros(8, dtype=torch.int64, device=dev)
+    for i in range(a.iters):
+        cnt.zero_()
+        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s.record()
+        lcb.resample(rows, tt, seeds=seeds, n_draws=n * a.draws, counters=cnt)
+        e.record()
+        torch.cuda.synchronize()
+        ms = s.elapsed_time(e)
+        gb = n * a.V * rows.element_size() / 1e9
+        print(f"iter {i}: {ms:.3f} ms  {n / ms / 1e3:.2f} M rows/s  {gb / ms * 1e3:.1f} GB/s  "
+              f"counters {cnt.cpu().tolist()}", flush=True)
+
+
+if __name__ == "__main__":
+    main()
