@@ -8,23 +8,24 @@
 //   sample    sampling.py:97-109  t = u * pairwise_sum(q); first id with cumsum(q) > t
 //                                 ('right'), clamp to V-1, back off over q == 0
 //
-// Three tiers:
-//   FAST    fp32 MUFU exponentials with an exactly-carried argument and a
-//           rigorous per-row error bound; every decision (nucleus cut, draw) is
-//           certified against the bound, otherwise the task goes to REFINE.
-//   REFINE  the same algorithm with fp64 e = exp(fl(fl(z/T) - fl(m/T))) -- the
-//           reference's own argument -- and bounds of ~V*2^-52.  Uncertified
-//           decisions go to EXACT.
-//   EXACT   emulation of numpy's operation order (pairwise sums, sequential
-//           cumsum, lexsort order) by one CTA per task.  Only the libm exp can
-//           differ from numpy's (<= 1 ulp); a draw whose margin is within that
-//           is flagged LC_DRAW_UNRESOLVED.
+// Tiers:
+//   FAST     fp32 MUFU exponentials with an exactly-carried argument and a
+//            rigorous per-row error bound; every decision (nucleus cut, draw) is
+//            certified against the bound.
+//   PRECISE  (same CTA, same task, second pass) only when a FAST decision is
+//            uncertain: the row mass is recomputed with a table-driven fp64
+//            exponential (~12 fp64 ops, relative error <= 3e-13) and the
+//            decisions are re-run with bounds of ~V*2^-52.
+//   EXACT    (separate kernel, queued) emulation of numpy's operation order
+//            (pairwise sums, sequential cumsum, lexsort order).  Only the libm
+//            exp can differ from numpy's (<= 1 ulp); a draw whose margin is
+//            within that is flagged LC_DRAW_UNRESOLVED.
 //
-// Layout: one CTA (512 threads) per task, persistent over tasks.  Warp w owns
-// the contiguous id range [w*C, (w+1)*C) of the row (C a multiple of 8); a
-// lane reads 8 consecutive elements per 16 B (bf16) / 32 B (fp32) vector, so a
-// warp instruction covers 256 consecutive ids (coalesced) and the warp ranges
-// are in id order -- which is what the inverse-CDF search needs.
+// Layout: one CTA (256 threads, 2 CTAs per SM) per task, persistent over
+// tasks.  Warp w owns the contiguous id range [w*C, (w+1)*C) of the row (C a
+// multiple of 8); a lane reads 8 consecutive elements per 16 B (bf16) / 32 B
+// (fp32) vector, so a warp instruction covers 256 consecutive ids (coalesced)
+// and warp ranges are in id order -- what the inverse-CDF search needs.
 #include <float.h>
 #include <limits.h>
 #include <math.h>
@@ -35,38 +36,40 @@
 
 namespace lcb {
 
-constexpr int RS_THREADS = 512;
+constexpr int RS_THREADS = 256;
 constexpr int RS_WARPS = RS_THREADS / 32;
-constexpr int CAND_CAP = 2048;        // candidate list (top-k / small nucleus / bracket) in smem
+constexpr int RS_MIN_BLOCKS = 2;      // CTAs per SM (registers <= 128/thread)
+constexpr int CAND_CAP = 1024;        // candidate list (top-k / small nucleus / bracket) in smem
 constexpr int NBINS = 256;            // nucleus histogram bins
 constexpr float BINS_PER_OCT = 4.0f;  // 64 octaves of dynamic range
 constexpr int K0_SPEC = 64;           // speculative candidate count for top-p without top-k
-constexpr int SCR_PER_WARP = 1024;    // large-nucleus kept elements per warp (global scratch)
+constexpr int SCR_PER_WARP = 2048;    // large-nucleus kept elements per warp (global scratch)
 constexpr int SCR_PER_CTA = SCR_PER_WARP * RS_WARPS;
 
 // ---- error model ----------------------------------------------
 // ex2.approx.ftz.f32 relative error bound (PTX ISA: ~2 ulp).  The GPU test
-// tests/test_gpu_numerics.py::test_fast_exp_error_bound measures fast_exp over
+// tests/test_gpu_parity.py::test_fast_exp_error_bound measures fast_exp over
 // dense argument grids and fails if this constant is ever exceeded.
 constexpr double kEx2RelErr = 4.0e-7;
-constexpr double kCorrErr = 1.0e-10;                         // 2nd-order term of the argument correction
-constexpr double kSum8Err = 3.0 * 5.9604644775390625e-08;    // fp32 pairwise sum of 8 (3 roundings)
-constexpr double kRefExpErr = 8.881784197001252e-16;         // libm / numpy exp vs exact: 4 ulp
-constexpr double kEps64 = 1.1102230246251565e-16;            // 2^-53
+constexpr double kCorrErr = 1.0e-10;                       // 2nd-order term of the argument correction
+constexpr double kSum8Err = 3.0 * 5.9604644775390625e-08;  // fp32 pairwise sum of 8 (3 roundings)
+constexpr double kRefExpErr = 8.881784197001252e-16;       // libm / numpy exp vs exact: 4 ulp
+constexpr double kLiteErr = 3.0e-13;                       // lite_exp incl. its argument (|a| <= 1100)
+constexpr double kEps64 = 1.1102230246251565e-16;          // 2^-53
 
 // ---- loading --------------------------------------------------------------------------------
 
-// 8 consecutive logits starting at id e0; ids >= V (the caller's limit) read as -inf.
+// 8 consecutive logits starting at id e0; ids >= lim read as -inf.
 template <int DT>
-__device__ __forceinline__ void load8(const char* row, int e0, int V, bool vec, float v[8]) {
-  if (e0 >= V) {
+__device__ __forceinline__ void load8(const char* row, int e0, int lim, bool vec, float v[8]) {
+  if (e0 >= lim) {
 #pragma unroll
     for (int j = 0; j < 8; ++j) v[j] = -INFINITY;
     return;
   }
   if (DT == LC_BF16) {
     const uint16_t* r = reinterpret_cast<const uint16_t*>(row);
-    if (vec && e0 + 8 <= V) {
+    if (vec && e0 + 8 <= lim) {
       uint4 q = __ldg(reinterpret_cast<const uint4*>(r + e0));
       uint32_t w[4] = {q.x, q.y, q.z, q.w};
 #pragma unroll
@@ -76,25 +79,25 @@ __device__ __forceinline__ void load8(const char* row, int e0, int V, bool vec, 
       }
     } else {
 #pragma unroll
-      for (int j = 0; j < 8; ++j) v[j] = (e0 + j < V) ? bf16_bits_to_f32(__ldg(r + e0 + j)) : -INFINITY;
+      for (int j = 0; j < 8; ++j) v[j] = (e0 + j < lim) ? bf16_bits_to_f32(__ldg(r + e0 + j)) : -INFINITY;
     }
   } else {
     const float* r = reinterpret_cast<const float*>(row);
-    if (vec && e0 + 8 <= V) {
+    if (vec && e0 + 8 <= lim) {
       float4 a = __ldg(reinterpret_cast<const float4*>(r + e0));
       float4 b = __ldg(reinterpret_cast<const float4*>(r + e0 + 4));
       v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w;
       v[4] = b.x; v[5] = b.y; v[6] = b.z; v[7] = b.w;
     } else {
 #pragma unroll
-      for (int j = 0; j < 8; ++j) v[j] = (e0 + j < V) ? __ldg(r + e0 + j) : -INFINITY;
+      for (int j = 0; j < 8; ++j) v[j] = (e0 + j < lim) ? __ldg(r + e0 + j) : -INFINITY;
     }
   }
 }
 
 // Warp-uniform pass over the warp's id range [cb, ce): UNR vectors per lane are
 // loaded before any is consumed (memory-level parallelism); f(e0, v) sees ids
-// e0..e0+7 with ids >= ce read as -inf (callers mask with e0 + j < ce).
+// e0..e0+7, ids >= ce read as -inf (callers mask with e0 + j < ce).
 template <int DT, int UNR, typename F>
 __device__ __forceinline__ void warp_pass(const char* row, int cb, int ce, bool vec, int lane, F&& f) {
   for (int base = cb; base < ce; base += 256 * UNR) {
@@ -119,9 +122,11 @@ struct ExpCtx {
   float Lhi, Llo;  // log2(e)/T split, Lhi + Llo = log2e/T to ~2^-48
   double T;
   double mT;       // fl(m / T): the reference's scaled max (sampling.py:65-66)
+  double md;       // (double) m
+  double L16;      // 16 * log2(e) / T
 };
 
-// FAST: e ~ 2^((z - m) * log2e / T).  z - m is carried exactly (TwoSum), the
+// FAST: e ~ 2^((z-m) * log2e / T).  z - m is carried exactly (TwoSum), the
 // product error and the constant's low part go into alo, and ex2's input
 // rounding is removed by the first-order correction e*(1 + alo*ln2).
 // Relative error <= kEx2RelErr + kCorrErr; 0 for z = -inf; e(m) == 1 exactly.
@@ -135,17 +140,34 @@ __device__ __forceinline__ float fast_exp(const ExpCtx& c, float z) {
   return (e > 0.0f) ? fmaf(e, alo * 0.69314718055994531f, e) : 0.0f;
 }
 
-// REFINE / EXACT: the reference's own argument s = fl(fl(z/T) - fl(m/T)), then
-// the fp64 exponential (<= 1 ulp).
+// PRECISE: table-driven fp64 exp of (z - m)/T.  b = 16*log2e*(z-m)/T,
+// n = rint(b), x = b - n in [-1/2, 1/2]; 2^(b/16) = 2^(n>>4) * 2^((n&15)/16) *
+// exp(x*ln2/16) with a degree-6 Taylor polynomial (|x ln2/16| <= 0.0217,
+// truncation 5e-16).  Relative error <= kLiteErr for |b/16| <= 1100.
+__device__ __forceinline__ double lite_exp(const ExpCtx& c, float z, const double* t16) {
+  const double b = ((double)z - c.md) * c.L16;
+  if (!(b > -17000.0)) return 0.0;
+  const double t = b + 6755399441055744.0;  // 1.5 * 2^52: round to nearest
+  const int n16 = __double2loint(t);
+  const double x = b - (t - 6755399441055744.0);
+  double p = 9.181219573844438764e-12;
+  p = fma(x, p, 1.271587195055813162e-9);
+  p = fma(x, p, 1.467610032291942926e-7);
+  p = fma(x, p, 1.355080777949745604e-5);
+  p = fma(x, p, 9.383847928089871576e-4);
+  p = fma(x, p, 4.332169878499658184e-2);
+  p = fma(x, p, 1.0);
+  const double r = t16[n16 & 15] * p;
+  const int e2 = n16 >> 4;
+  if (e2 >= -1021) return __hiloint2double(__double2hiint(r) + (e2 << 20), __double2loint(r));
+  return (r * __hiloint2double((e2 + 1023 + 600) << 20, 0)) * 0x1p-600;
+}
+
+// REFINE-grade exp for candidate values: the reference's own argument
+// s = fl(fl(z/T) - fl(m/T)), then the fp64 libm exponential (<= 1 ulp).
 __device__ __forceinline__ double ref_exp(const ExpCtx& c, float z) {
   double s = __dsub_rn(__ddiv_rn((double)z, c.T), c.mT);
   return exp(s);
-}
-
-template <bool REFINE>
-__device__ __forceinline__ double elem_exp(const ExpCtx& c, float z) {
-  if (REFINE) return ref_exp(c, z);
-  return (double)fast_exp(c, z);
 }
 
 // log2-distance bin of z below the max (monotone non-increasing in z)
@@ -175,18 +197,21 @@ struct __align__(16) Smem {
   int sl_id[CAND_CAP];                // kept small list, id order
   double sl_e[CAND_CAP];              // its e, later its inclusive prefix
   uint32_t hist[RS_WARPS][NBINS];     // per-warp fixed-point nucleus histogram
-  unsigned long long tk64[RS_THREADS];
+  unsigned long long tmp64[RS_THREADS];
+  double t16[16];                     // 2^(j/16) for lite_exp
   double wsum[RS_WARPS];
   double werr[RS_WARPS];
   double wpre[RS_WARPS + 1];
   float wmax[RS_WARPS];
+  float wmin[RS_WARPS];
+  float wtheta[RS_WARPS];
   int warg[RS_WARPS];
   int wcount[RS_WARPS];
   int wsl[RS_WARPS + 1];
   double dsc[4];
   int isc[8];
 };
-// isc: 0 cand count, 1 bad row, 2 overflow, 3 kept count, 4 uncertain, 5 blo, 6 bhi, 7 need-next-tier
+// isc: 0 candidate count, 1 bad row, 2 overflow, 3 kept count, 4 uncertain, 5 blo, 6 bhi, 7 draw uncertain
 
 // Descending bitonic sort of n (power of two) 64-bit keys in smem.
 __device__ void bitonic_desc(unsigned long long* a, int n) {
@@ -208,10 +233,44 @@ __device__ void bitonic_desc(unsigned long long* a, int n) {
   }
 }
 
-__device__ __forceinline__ int pow2_at_least(int n) {
-  int p = 1;
-  while (p < n) p <<= 1;
-  return p;
+// r-th largest (1-based) of the 32 lane values, via a warp bitonic sort.
+__device__ __forceinline__ float warp_rth_largest(float v, int r) {
+  const int lane = threadIdx.x & 31;
+#pragma unroll
+  for (int k = 2; k <= 32; k <<= 1) {
+#pragma unroll
+    for (int j = k >> 1; j > 0; j >>= 1) {
+      float o = __shfl_xor_sync(0xffffffffu, v, j);
+      bool desc = (lane & k) == 0 || k == 32;
+      bool lower = (lane & j) == 0;
+      v = (lower == desc) ? fmaxf(v, o) : fminf(v, o);
+    }
+  }
+  return __shfl_sync(0xffffffffu, v, r - 1);
+}
+
+// Sort n distinct keys descending (n <= CAND_CAP): rank by counting for
+// n <= RS_THREADS, bitonic otherwise.
+__device__ void sort_desc(unsigned long long* a, int n, unsigned long long* tmp) {
+  if (n <= RS_THREADS) {
+    unsigned long long k = 0;
+    int rank = 0;
+    if ((int)threadIdx.x < n) {
+      k = a[threadIdx.x];
+      for (int j = 0; j < n; ++j) rank += (a[j] > k);
+    }
+    __syncthreads();
+    if ((int)threadIdx.x < n) tmp[rank] = k;
+    __syncthreads();
+    if ((int)threadIdx.x < n) a[threadIdx.x] = tmp[threadIdx.x];
+    __syncthreads();
+    return;
+  }
+  int n2 = 1;
+  while (n2 < n) n2 <<= 1;
+  for (int i = n + threadIdx.x; i < n2; i += RS_THREADS) a[i] = 0ull;
+  __syncthreads();
+  bitonic_desc(a, n2);
 }
 
 // warp-aggregated append to sm.cand
@@ -228,6 +287,17 @@ __device__ __forceinline__ void push_cand(Smem& sm, bool pred, float z, int id, 
     if (pos < CAND_CAP) sm.cand[pos] = cand_key(z, id);
     else overflow = 1;
   }
+}
+
+// inclusive warp scan (fp64)
+__device__ __forceinline__ double warp_incl_scan(double x) {
+  const int lane = threadIdx.x & 31;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    double y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += y;
+  }
+  return x;
 }
 
 // ---- task plumbing ------------------------------------------------------------------------------
@@ -259,12 +329,10 @@ struct DrawIO {
 };
 
 struct Workspace {
-  int* q_refine;  // [0] = count, [1..] task ids
-  int* q_exact;
+  int* q_exact;   // [0] = count, [1..] task ids
   int* scr_id;    // [grid][2][SCR_PER_CTA]
   double* scr_e;  // [grid][2][SCR_PER_CTA]
 };
-
 
 __device__ __forceinline__ double draw_u(const DrawIO& io, int64_t d, const TaskView& tv) {
   if (io.u) return io.u[d];
@@ -305,32 +373,33 @@ __device__ __forceinline__ void write_all(const TaskView& tv, const DrawIO& io, 
   }
 }
 
-// ============================== FAST / REFINE kernel ==============================
+// counters: 0 tasks that needed the PRECISE pass, 1 unresolved draws (EXACT),
+// 2 bad rows, 3 tasks sent to EXACT, 4 uncertain cut (FAST), 5 uncertain draw
+// (FAST), 6 uncertain after PRECISE, 7 candidate/scratch overflow.
 
-template <int DT, bool REFINE>
-__global__ void __launch_bounds__(RS_THREADS, 1)
+// ============================== FAST + PRECISE kernel ==============================
+
+template <int DT>
+__global__ void __launch_bounds__(RS_THREADS, RS_MIN_BLOCKS)
 resample_kernel(const char* __restrict__ rows, int64_t row_bytes, int Vdef, const lc_task* __restrict__ tasks,
-                int n_tasks, const int* __restrict__ task_list, CacheMap cm, DrawIO io, Workspace ws,
-                unsigned long long* counters) {
+                int n_tasks, CacheMap cm, DrawIO io, Workspace ws, unsigned long long* counters) {
   extern __shared__ __align__(16) unsigned char smraw[];
   Smem& sm = *reinterpret_cast<Smem*>(smraw);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int ntask = task_list ? task_list[0] : n_tasks;
   int* scrA_id = ws.scr_id + (int64_t)blockIdx.x * 2 * SCR_PER_CTA;
   double* scrA_e = ws.scr_e + (int64_t)blockIdx.x * 2 * SCR_PER_CTA;
   int* scrM_id = scrA_id + SCR_PER_CTA;
   double* scrM_e = scrA_e + SCR_PER_CTA;
-  const uint8_t tier_flag = REFINE ? LC_DRAW_PRECISE : 0;
+  if (tid < 16) sm.t16[tid] = exp2((double)tid / 16.0);
 
-  for (int ti = blockIdx.x; ti < ntask; ti += gridDim.x) {
-    const int task_id = task_list ? task_list[1 + ti] : ti;
-    TaskView tv;
+  for (int task_id = blockIdx.x; task_id < n_tasks; task_id += gridDim.x) {
     const lc_task tk = tasks[task_id];
     if (tk.draw_end <= tk.draw_begin) continue;  // nothing to draw (uniform across the CTA)
+    TaskView tv;
+    __syncthreads();  // previous task's smem readers are done
     if (!resolve_task(tk, rows, row_bytes, Vdef, cm, tv)) {
       write_all(tv, io, -1, LC_DRAW_BAD_ROW);
       if (tid == 0) atomicAdd(&counters[2], 1ull);
-      __syncthreads();
       continue;
     }
     const int V = tv.V;
@@ -338,12 +407,10 @@ resample_kernel(const char* __restrict__ rows, int64_t row_bytes, int Vdef, cons
     const int C = ((V + RS_WARPS - 1) / RS_WARPS + 7) & ~7;
     const int cb = min(V, warp * C);
     const int ce = min(V, cb + C);
-    if (tid == 0) {
-      for (int i = 0; i < 8; ++i) sm.isc[i] = 0;
-    }
+    if (tid < 8) sm.isc[tid] = 0;
 
-    // ---------------- phase A: max, first argmax, thread maxima, NaN check
-    float tmax = -INFINITY;
+    // ---------------- phase A: max, first argmax, |z| range, thread maxima, NaN check
+    float tmax = -INFINITY, tmin = INFINITY;
     int targ = INT_MAX;
     bool bad = false;
     warp_pass<DT, 4>(tv.row, cb, ce, vec, lane, [&](int e0, const float* v) {
@@ -354,85 +421,93 @@ resample_kernel(const char* __restrict__ rows, int64_t row_bytes, int Vdef, cons
           tmax = v[j];
           targ = e0 + j;
         }
+        if (e0 + j < ce) tmin = fminf(tmin, v[j]);
       }
     });
     __syncthreads();  // isc reset visible
     {
       float wm = warp_max(tmax);
+      float wn = -warp_max(-tmin);
       int wa = warp_min_int(tmax == wm ? targ : INT_MAX);
       bool wbad = __any_sync(0xffffffffu, bad);
       if (lane == 0) {
         sm.wmax[warp] = wm;
+        sm.wmin[warp] = wn;
         sm.warg[warp] = wa;
         if (wbad) sm.isc[1] = 1;
       }
-      sm.tk64[tid] = ((unsigned long long)f32_order_key(tmax) << 32) | (uint32_t)tid;
     }
     __syncthreads();
-    float m = -INFINITY;
+    float m = -INFINITY, zmin = INFINITY;
     int amax = INT_MAX;
     for (int w = 0; w < RS_WARPS; ++w) {
       if (sm.wmax[w] > m) {
         m = sm.wmax[w];
         amax = sm.warg[w];
       }
+      zmin = fminf(zmin, sm.wmin[w]);
     }
-    const bool rowbad = sm.isc[1] || !(m > -INFINITY) || !(m < INFINITY);
-    if (rowbad) {
+    const uint8_t base_flag = 0;
+    if (sm.isc[1] || !(m > -INFINITY) || !(m < INFINITY)) {
       write_all(tv, io, -1, LC_DRAW_BAD_ROW);
       if (tid == 0) atomicAdd(&counters[2], 1ull);
-      __syncthreads();
       continue;
     }
     if (tv.T == 0.0) {  // greedy: one-hot at the first argmax, still one draw (sampling.py:61-64)
-      write_all(tv, io, amax, tier_flag);
-      __syncthreads();
+      write_all(tv, io, amax, base_flag);
       continue;
     }
     ExpCtx ec;
     ec.m = m;
     ec.T = tv.T;
     ec.mT = __ddiv_rn((double)m, tv.T);
+    ec.md = (double)m;
     {
       double Ld = 1.4426950408889634 / tv.T;
       ec.Lhi = (float)Ld;
       ec.Llo = (float)(Ld - (double)ec.Lhi);
+      ec.L16 = 16.0 * Ld;
     }
-    // temperatures whose scaled logits leave the fp32 range go straight to REFINE
-    bool fail = !REFINE && !(ec.Lhi < 1e20f && ec.Lhi > 1e-20f && fabsf(m) * ec.Lhi < 1e30f);
+    // temperatures whose scaled logits leave the fp32 / table range go to EXACT
+    const double zabs = fmax(fabs((double)m), isfinite(zmin) ? fabs((double)zmin) : fabs((double)m));
+    const bool sane = ec.Lhi < 1e20f && ec.Lhi > 1e-20f && fabsf(m) * ec.Lhi < 1e30f && zabs / tv.T < 1e15;
+    // reference argument rounding: |s_ref - s| <= 2^-51 (|z| + |m|) / T  (relative error of e)
+    const double relArg = 4.440892098500626e-16 * 2.0 * zabs / tv.T;
+    const double relRef = (double)(2 * V + 64) * kEps64;  // reference's rounding of p, csum, sum(q), cumsum
 
     // ---------------- candidate threshold (top-k, or speculative small nucleus)
     int kc = 0;
     if (tv.topk > 0) kc = tv.topk;
     else if (tv.trunc && tv.topp < 1.0) kc = K0_SPEC;
     float theta = INFINITY;
-    if (kc > 0 && kc <= RS_THREADS) {
-      // the kc-th largest thread maximum lower-bounds the kc-th largest logit
-      bitonic_desc(sm.tk64, RS_THREADS);
-      theta = cand_z((sm.tk64[kc - 1] & 0xffffffff00000000ull) | 0xffffffffull);
-    } else if (kc > RS_THREADS) {
-      theta = -INFINITY;  // collect all; overflow -> next tier
+    if (kc > 0 && kc <= 32 * RS_WARPS) {
+      // every warp has r = ceil(kc/WARPS) thread maxima >= its r-th largest, so
+      // the minimum over warps lower-bounds the kc-th largest logit
+      const int r = (kc + RS_WARPS - 1) / RS_WARPS;
+      float tw = warp_rth_largest(tmax, r);
+      if (lane == 0) sm.wtheta[warp] = tw;
+      __syncthreads();
+      for (int w = 0; w < RS_WARPS; ++w) theta = fminf(theta, sm.wtheta[w]);
+    } else if (kc > 0) {
+      theta = -INFINITY;  // collect all; overflow -> EXACT
     }
 
-    // ---------------- phase B: mass, per-warp sums, candidates
+    // ---------------- phase B: fast mass per warp, candidates
     double S_part = 0.0;
     int overflow = 0;
     warp_pass<DT, 2>(tv.row, cb, ce, vec, lane, [&](int e0, const float* v) {
-      if (REFINE) {
-        double s8 = 0.0;
+      float e[8];
 #pragma unroll
-        for (int j = 0; j < 8; ++j) s8 += ref_exp(ec, v[j]);  // ids >= ce are -inf -> 0
-        S_part += s8;
-      } else {
-        float e[8];
-#pragma unroll
-        for (int j = 0; j < 8; ++j) e[j] = fast_exp(ec, v[j]);
-        float s8 = ((e[0] + e[1]) + (e[2] + e[3])) + ((e[4] + e[5]) + (e[6] + e[7]));
-        S_part += (double)s8;
-      }
+      for (int j = 0; j < 8; ++j) e[j] = fast_exp(ec, v[j]);  // ids >= ce are -inf -> 0
+      S_part += (double)(((e[0] + e[1]) + (e[2] + e[3])) + ((e[4] + e[5]) + (e[6] + e[7])));
       if (kc > 0) {
+        unsigned m8 = 0;
 #pragma unroll
-        for (int j = 0; j < 8; ++j) push_cand(sm, (e0 + j < ce) && v[j] >= theta, v[j], e0 + j, overflow);
+        for (int j = 0; j < 8; ++j) m8 |= (unsigned)((e0 + j < ce) && v[j] >= theta) << j;
+        if (__any_sync(0xffffffffu, m8 != 0)) {
+#pragma unroll
+          for (int j = 0; j < 8; ++j) push_cand(sm, (m8 >> j) & 1u, v[j], e0 + j, overflow);
+        }
       }
     });
     {
@@ -444,305 +519,354 @@ resample_kernel(const char* __restrict__ rows, int64_t row_bytes, int Vdef, cons
       }
     }
     __syncthreads();
-    double S = 0.0;
-    for (int w = 0; w < RS_WARPS; ++w) S += sm.wsum[w];
-    // relative error of our e's and sums vs the reference's e's (exact-arithmetic sums)
-    const double relE = REFINE ? (2.0 * kRefExpErr + (double)(V + 16) * kEps64)
-                               : (kEx2RelErr + kCorrErr + kSum8Err + kRefExpErr + (double)(V + 16) * kEps64);
-    const double E_S = S * relE + (REFINE ? 0.0 : (double)V * 2.4e-38);  // + flushed subnormals
-    // the reference's own rounding in p = e/S, csum, sum(q), cumsum (relative)
-    const double relRef = (double)(2 * V + 64) * kEps64;
     const int ncand = min(sm.isc[0], CAND_CAP);
-    const bool cand_overflow = sm.isc[2] != 0;
+    const bool cand_ok = (sm.isc[2] == 0) && kc > 0 && ncand >= kc;
     __syncthreads();
-    if (tid == 0) {
-      sm.isc[2] = 0;
-      sm.isc[7] = 0;
-    }
 
-    // Kept-set representation for the draw:
-    //   mode 0 -- untruncated: all ids, e recomputed by the owning warp;
-    //   mode 1 -- small list sl_id/sl_e (id order) of length L;
-    //   mode 2 -- per-warp merged lists in global scratch (scrM), counts wcount[].
-    int mode = 0;
-    int L = 0;
+    // per-row state kept across the FAST and PRECISE decision passes
+    bool cands_sorted = false;   // small list sorted + ce computed
+    int large_state = 0;         // 0 not built, 1 built, -1 failed
+    bool to_exact = !sane;
+    bool done = false;
 
-    if (!fail && tv.trunc) {
-      const double P = tv.topp * S;  // nucleus target in e-space
-      bool done = false;
-      if (kc > 0 && !cand_overflow && ncand >= kc) {
-        const int n2 = pow2_at_least(ncand);
-        for (int i = ncand + tid; i < n2; i += RS_THREADS) sm.cand[i] = 0ull;
+    for (int pass = 0; pass < 2 && !done && !to_exact; ++pass) {
+      const bool precise = pass == 1;
+      const uint8_t tier_flag = precise ? LC_DRAW_PRECISE : 0;
+      if (precise) {
+        // ---- PRECISE: recompute per-warp masses with lite_exp (fp64)
+        if (tid == 0) atomicAdd(&counters[0], 1ull);
+        double acc = 0.0;
+        warp_pass<DT, 2>(tv.row, cb, ce, vec, lane, [&](int e0, const float* v) {
+#pragma unroll
+          for (int j = 0; j < 8; ++j) acc += lite_exp(ec, v[j], sm.t16);
+        });
+        acc = warp_sum(acc);
         __syncthreads();
-        bitonic_desc(sm.cand, n2);
-        const int klim = tv.topk > 0 ? tv.topk : ncand;
-        for (int i = tid; i < klim; i += RS_THREADS) sm.ce[i] = ref_exp(ec, cand_z(sm.cand[i]));
+        if (lane == 0) sm.wsum[warp] = acc;
         __syncthreads();
-        if (tid == 0) {
-          int cut = -1;
-          bool unc = false;
-          if (tv.topp < 1.0) {
-            double c = 0.0;
-            for (int i = 0; i < klim; ++i) {
-              double prev = c;
-              c += sm.ce[i];
-              double tol = tv.topp * E_S + c * relRef;
-              if (c >= P - tol) {
-                cut = i;
-                if (!(c - P > tol && P - prev > tol)) unc = true;
-                break;
-              }
-            }
-          }
-          int Lk = cut >= 0 ? cut + 1 : (tv.topk > 0 ? klim : -1);
-          if (Lk > 0) {
-            // distinct logits that the reference might round to equal p: ordering unsafe
-            int lim = min(Lk + 1, ncand);
-            for (int i = 1; i < lim; ++i) {
-              float za = cand_z(sm.cand[i - 1]), zb = cand_z(sm.cand[i]);
-              if (za != zb) {
-                double da = __ddiv_rn((double)za, tv.T), db = __ddiv_rn((double)zb, tv.T);
-                if (da - db <= fmax(fabs(da), fabs(ec.mT)) * 8.0 * kEps64) unc = true;
-              }
-            }
-          }
-          sm.isc[3] = Lk;
-          sm.isc[4] = unc;
-          if (unc) atomicAdd(&counters[3], 1ull);
-        }
-        __syncthreads();
-        if (sm.isc[4]) fail = true;
-        if (!fail && sm.isc[3] > 0) {
+      }
+      double S = 0.0;
+      for (int w = 0; w < RS_WARPS; ++w) S += sm.wsum[w];
+      const double relE = precise ? (kLiteErr + 2.0 * kRefExpErr + relArg + (double)(V + 16) * kEps64)
+                                  : (kEx2RelErr + kCorrErr + kSum8Err + kRefExpErr + relArg +
+                                     (double)(V + 16) * kEps64);
+      const double absE = precise ? (double)V * 1e-300 : (double)V * 2.4e-38;  // flushed / subnormal mass
+      const double E_S = S * relE + absE;
+      bool unc = false;
+
+      // Kept-set representation for the draw:
+      //   mode 0 -- untruncated: all ids, e recomputed by the owning warp;
+      //   mode 1 -- small list sl_id/sl_e (id order) of length L;
+      //   mode 2 -- per-warp merged lists in global scratch (scrM), counts wcount[].
+      int mode = 0;
+      int L = 0;
+
+      if (tv.trunc && tv.topp < 1.0) {
+        // p(first argmax) = 1/S (its e is exactly 1 in both implementations); if it
+        // certainly reaches top_p the nucleus is {argmax} and every draw returns it
+        const double pmax_lo = (1.0 / (S + E_S)) * (1.0 - relRef);
+        if (pmax_lo > tv.topp) {
+          write_all(tv, io, amax, tier_flag);
           done = true;
-          mode = 1;
-          L = sm.isc[3];
+          break;
         }
-      } else if (tv.topk > 0) {
-        fail = true;  // top-k candidates overflowed (heavy ties / k > 512) -> next tier
-        if (tid == 0) atomicAdd(&counters[7], 1ull);
       }
 
-      if (!fail && !done) {
-        // -------- large nucleus: top-p without top-k, nucleus beyond the speculative list
-        __syncthreads();
-        for (int i = tid; i < RS_WARPS * NBINS; i += RS_THREADS) (&sm.hist[0][0])[i] = 0u;
-        __syncthreads();
-        const int lgC = 32 - __clz(C + 1);
-        const float qscale = ldexpf(1.0f, 31 - lgC);
-        warp_pass<DT, 2>(tv.row, cb, ce, vec, lane, [&](int e0, const float* v) {
-#pragma unroll
-          for (int j = 0; j < 8; ++j) {
-            if (e0 + j < ce) {
-              float e = REFINE ? (float)ref_exp(ec, v[j]) : fast_exp(ec, v[j]);
-              atomicAdd(&sm.hist[warp][nbin(ec, v[j])], __float2uint_rn(e * qscale));
-            }
+      if (tv.trunc) {
+        const double P = tv.topp * S;  // nucleus target in e-space
+        bool small_done = false;
+        if (cand_ok && large_state == 0) {
+          if (!cands_sorted) {
+            sort_desc(sm.cand, ncand, sm.tmp64);
+            const int klim0 = tv.topk > 0 ? tv.topk : ncand;
+            for (int i = tid; i < klim0; i += RS_THREADS) sm.ce[i] = ref_exp(ec, cand_z(sm.cand[i]));
+            __syncthreads();
+            cands_sorted = true;
           }
-        });
-        __syncthreads();
-        if (tid < 32) {
-          const double inv = 1.0 / (double)qscale;
-          const double qerr = (double)V * 0.5 * inv + 2.0 * E_S + P * relRef;
-          double cum = 0.0;
-          int blo = NBINS - 1, bhi = NBINS - 1;
-          bool got_lo = false;
-          for (int b0 = 0; b0 < NBINS; b0 += 32) {
-            unsigned long long hs = 0;
-            for (int w = 0; w < RS_WARPS; ++w) hs += sm.hist[w][b0 + lane];
-            double x = (double)hs * inv;
-#pragma unroll
-            for (int o = 1; o < 32; o <<= 1) {
-              double y = __shfl_up_sync(0xffffffffu, x, o);
-              if (lane >= o) x += y;
-            }
-            double incl = cum + x;
-            unsigned lo_m = __ballot_sync(0xffffffffu, incl >= P - qerr);
-            unsigned hi_m = __ballot_sync(0xffffffffu, incl >= P + qerr);
-            if (!got_lo && lo_m) {
-              blo = b0 + __ffs(lo_m) - 1;
-              got_lo = true;
-            }
-            if (hi_m) {
-              bhi = b0 + __ffs(hi_m) - 1;
-              break;
-            }
-            cum = __shfl_sync(0xffffffffu, incl, 31);
-          }
-          if (lane == 0) {
-            sm.isc[5] = blo;
-            sm.isc[6] = bhi;
-            sm.isc[0] = 0;
-            sm.isc[2] = 0;
-          }
-        }
-        __syncthreads();
-        const int blo = sm.isc[5], bhi = sm.isc[6];
-        // B3: order-preserving per-warp compaction of bins < blo (certainly kept) to
-        // scratch A; bracket bins [blo, bhi] to the smem candidate list.
-        int wn = 0, ovf = 0;
-        warp_pass<DT, 2>(tv.row, cb, ce, vec, lane, [&](int e0, const float* v) {
-          int b[8];
-#pragma unroll
-          for (int j = 0; j < 8; ++j) b[j] = (e0 + j < ce) ? nbin(ec, v[j]) : NBINS;
-          // lane-major order inside a 256-id step: lane l's 8 ids precede lane l+1's
-          int mine = 0;
-#pragma unroll
-          for (int j = 0; j < 8; ++j) mine += (b[j] < blo);
-          int x = mine;
-#pragma unroll
-          for (int o = 1; o < 32; o <<= 1) {
-            int y = __shfl_up_sync(0xffffffffu, x, o);
-            if (lane >= o) x += y;
-          }
-          int pos = wn + x - mine;
-#pragma unroll
-          for (int j = 0; j < 8; ++j) {
-            if (b[j] < blo) {
-              if (pos < SCR_PER_WARP) scrA_id[warp * SCR_PER_WARP + pos] = e0 + j;
-              else ovf = 1;
-              ++pos;
-            }
-          }
-          wn += __shfl_sync(0xffffffffu, x, 31);
-#pragma unroll
-          for (int j = 0; j < 8; ++j) push_cand(sm, b[j] >= blo && b[j] <= bhi, v[j], e0 + j, ovf);
-        });
-        ovf = __any_sync(0xffffffffu, ovf);
-        if (lane == 0) {
-          sm.wcount[warp] = min(wn, SCR_PER_WARP);
-          if (ovf || wn > SCR_PER_WARP) sm.isc[2] = 1;
-        }
-        __syncthreads();
-        if (sm.isc[2]) {
-          fail = true;
-          if (tid == 0) atomicAdd(&counters[7], 1ull);
-        } else {
-          // precise e of the certainly-kept elements (dense, per warp)
-          const int nw = sm.wcount[warp];
-          double acc = 0.0;
-          for (int i = lane; i < nw; i += 32) {
-            double e = ref_exp(ec, load1<DT>(tv.row, scrA_id[warp * SCR_PER_WARP + i]));
-            scrA_e[warp * SCR_PER_WARP + i] = e;
-            acc += e;
-          }
-          acc = warp_sum(acc);
-          if (lane == 0) sm.wsum[warp] = acc;
-          const int nb = min(sm.isc[0], CAND_CAP);
-          const int n2 = pow2_at_least(max(nb, 1));
-          for (int i = nb + tid; i < n2; i += RS_THREADS) sm.cand[i] = 0ull;
-          __syncthreads();
-          bitonic_desc(sm.cand, n2);
-          for (int i = tid; i < nb; i += RS_THREADS) sm.ce[i] = ref_exp(ec, cand_z(sm.cand[i]));
-          __syncthreads();
-          if (tid == 0) {
-            double Mabove = 0.0;
-            for (int w = 0; w < RS_WARPS; ++w) Mabove += sm.wsum[w];
+          const int klim = tv.topk > 0 ? tv.topk : ncand;
+          if (warp == 0) {
+            // inclusive scan of the sorted candidates' e; first crossing of P
             int cut = -1;
-            bool unc = false;
-            double c = Mabove;
-            const double tolS = tv.topp * E_S;
-            if (c >= P - tolS - c * relRef) unc = true;  // the cut would lie above the bracket
-            for (int i = 0; i < nb && !unc; ++i) {
-              double prev = c;
-              c += sm.ce[i];
-              double tol = tolS + c * relRef;
-              if (c >= P - tol) {
-                cut = i;
-                if (!(c - P > tol && P - prev > tol)) unc = true;
-                break;
+            bool u_ = false;
+            if (tv.topp < 1.0) {
+              double off = 0.0;
+              for (int i0 = 0; i0 < klim; i0 += 32) {
+                const int i = i0 + lane;
+                const double e = i < klim ? sm.ce[i] : 0.0;
+                const double c = off + warp_incl_scan(e), prev = c - e;
+                const double tol = tv.topp * E_S + c * relRef;
+                const unsigned hm = __ballot_sync(0xffffffffu, i < klim && c >= P - tol);
+                if (hm) {
+                  const int hl = __ffs(hm) - 1;
+                  cut = i0 + hl;
+                  const bool ok = (c - P > tol && P - prev > tol);
+                  u_ = !__shfl_sync(0xffffffffu, ok, hl);
+                  break;
+                }
+                off = __shfl_sync(0xffffffffu, c, 31);
               }
             }
-            if (cut < 0) unc = true;
-            if (!unc) {
-              for (int i = max(cut, 1); i <= min(cut + 1, nb - 1); ++i) {
+            int Lk = cut >= 0 ? cut + 1 : (tv.topk > 0 ? klim : -1);
+            if (Lk > 0) {
+              // distinct logits that the reference might round to equal p: ordering unsafe
+              const int lim = min(Lk + 1, ncand);
+              bool bad_order = false;
+              for (int i = 1 + lane; i < lim; i += 32) {
                 float za = cand_z(sm.cand[i - 1]), zb = cand_z(sm.cand[i]);
                 if (za != zb) {
                   double da = __ddiv_rn((double)za, tv.T), db = __ddiv_rn((double)zb, tv.T);
-                  if (da - db <= fmax(fabs(da), fabs(ec.mT)) * 8.0 * kEps64) unc = true;
+                  if (da - db <= fmax(fabs(da), fabs(ec.mT)) * 8.0 * kEps64) bad_order = true;
                 }
               }
+              u_ |= __any_sync(0xffffffffu, bad_order);
             }
-            sm.isc[3] = cut + 1;
-            sm.isc[4] = unc;
-            if (unc) atomicAdd(&counters[4], 1ull);
+            if (lane == 0) {
+              sm.isc[3] = Lk;
+              sm.isc[4] = u_;
+            }
+          }
+          __syncthreads();
+          const int Lk = sm.isc[3];
+          if (sm.isc[4]) unc = true;
+          else if (Lk > 0) {
+            small_done = true;
+            mode = 1;
+            L = Lk;
+          }
+          __syncthreads();
+        } else if (tv.topk > 0) {
+          to_exact = true;  // top-k candidates overflowed (heavy ties / k > 256) -> EXACT
+          if (tid == 0) atomicAdd(&counters[7], 1ull);
+          break;
+        }
+
+        if (!unc && !small_done) {
+          // -------- large nucleus: top-p without top-k, nucleus beyond the speculative list
+          if (large_state == 0) {
+            for (int i = tid; i < RS_WARPS * NBINS; i += RS_THREADS) (&sm.hist[0][0])[i] = 0u;
+            __syncthreads();
+            const int lgC = 32 - __clz(C + 1);
+            const float qscale = ldexpf(1.0f, 31 - lgC);
+            warp_pass<DT, 2>(tv.row, cb, ce, vec, lane, [&](int e0, const float* v) {
+#pragma unroll
+              for (int j = 0; j < 8; ++j)
+                if (e0 + j < ce) atomicAdd(&sm.hist[warp][nbin(ec, v[j])], __float2uint_rn(fast_exp(ec, v[j]) * qscale));
+            });
+            __syncthreads();
+            if (warp == 0) {
+              // bracket [blo, bhi] of bins that can hold the cut (fast mass + quantisation error)
+              const double inv = 1.0 / (double)qscale;
+              const double qerr = (double)V * 0.5 * inv + 2.0 * E_S + P * relRef + S * 2e-6;
+              double cum = 0.0;
+              int blo = NBINS - 1, bhi = NBINS - 1;
+              bool got_lo = false;
+              for (int b0 = 0; b0 < NBINS; b0 += 32) {
+                unsigned long long hs = 0;
+                for (int w = 0; w < RS_WARPS; ++w) hs += sm.hist[w][b0 + lane];
+                const double incl = cum + warp_incl_scan((double)hs * inv);
+                const unsigned lo_m = __ballot_sync(0xffffffffu, incl >= P - qerr);
+                const unsigned hi_m = __ballot_sync(0xffffffffu, incl >= P + qerr);
+                if (!got_lo && lo_m) {
+                  blo = b0 + __ffs(lo_m) - 1;
+                  got_lo = true;
+                }
+                if (hi_m) {
+                  bhi = b0 + __ffs(hi_m) - 1;
+                  break;
+                }
+                cum = __shfl_sync(0xffffffffu, incl, 31);
+              }
+              if (lane == 0) {
+                sm.isc[5] = blo;
+                sm.isc[6] = bhi;
+                sm.isc[0] = 0;
+                sm.isc[2] = 0;
+              }
+            }
+            __syncthreads();
+            const int blo = sm.isc[5], bhi = sm.isc[6];
+            // order-preserving per-warp compaction of bins < blo (certainly kept) to
+            // scratch A; bracket bins [blo, bhi] to the smem candidate list
+            int wn = 0, ovf = 0;
+            warp_pass<DT, 2>(tv.row, cb, ce, vec, lane, [&](int e0, const float* v) {
+              int b[8];
+              int mine = 0;
+#pragma unroll
+              for (int j = 0; j < 8; ++j) {
+                b[j] = (e0 + j < ce) ? nbin(ec, v[j]) : NBINS;
+                mine += (b[j] < blo);
+              }
+              const int x = (int)warp_incl_scan((double)mine);
+              int pos = wn + x - mine;
+#pragma unroll
+              for (int j = 0; j < 8; ++j) {
+                if (b[j] < blo) {
+                  if (pos < SCR_PER_WARP) scrA_id[warp * SCR_PER_WARP + pos] = e0 + j;
+                  else ovf = 1;
+                  ++pos;
+                }
+              }
+              wn += __shfl_sync(0xffffffffu, x, 31);
+              unsigned m8 = 0;
+#pragma unroll
+              for (int j = 0; j < 8; ++j) m8 |= (unsigned)(b[j] >= blo && b[j] <= bhi) << j;
+              if (__any_sync(0xffffffffu, m8 != 0)) {
+#pragma unroll
+                for (int j = 0; j < 8; ++j) push_cand(sm, (m8 >> j) & 1u, v[j], e0 + j, ovf);
+              }
+            });
+            ovf = __any_sync(0xffffffffu, ovf);
+            if (lane == 0) {
+              sm.wcount[warp] = min(wn, SCR_PER_WARP);
+              if (ovf || wn > SCR_PER_WARP) sm.isc[2] = 1;
+            }
+            __syncthreads();
+            if (sm.isc[2]) {
+              large_state = -1;
+            } else {
+              // precise e of the certainly-kept elements (dense, per warp)
+              const int nw = sm.wcount[warp];
+              double acc = 0.0;
+              for (int i = lane; i < nw; i += 32) {
+                double e = ref_exp(ec, load1<DT>(tv.row, scrA_id[warp * SCR_PER_WARP + i]));
+                scrA_e[warp * SCR_PER_WARP + i] = e;
+                acc += e;
+              }
+              acc = warp_sum(acc);
+              if (lane == 0) sm.werr[warp] = acc;  // kept mass above the bracket, per warp
+              sort_desc(sm.cand, min(sm.isc[0], CAND_CAP), sm.tmp64);
+              const int nb = min(sm.isc[0], CAND_CAP);
+              for (int i = tid; i < nb; i += RS_THREADS) sm.ce[i] = ref_exp(ec, cand_z(sm.cand[i]));
+              __syncthreads();
+              double Mab = 0.0;
+              for (int w = 0; w < RS_WARPS; ++w) Mab += sm.werr[w];
+              if (tid == 0) sm.dsc[1] = Mab;
+              large_state = 1;
+            }
+            __syncthreads();
+          }
+          if (large_state < 0) {
+            to_exact = true;
+            if (tid == 0) atomicAdd(&counters[7], 1ull);
+            break;
+          }
+          const int nb = min(sm.isc[0], CAND_CAP);
+          if (warp == 0) {
+            const double Mabove = sm.dsc[1];
+            const double tolS = tv.topp * E_S;
+            int cut = -1;
+            bool u_ = Mabove >= P - tolS - Mabove * relRef;  // the cut would lie above the bracket
+            double off = Mabove;
+            for (int i0 = 0; i0 < nb && !u_; i0 += 32) {
+              const int i = i0 + lane;
+              const double e = i < nb ? sm.ce[i] : 0.0;
+              const double c = off + warp_incl_scan(e), prev = c - e;
+              const double tol = tolS + c * relRef;
+              const unsigned hm = __ballot_sync(0xffffffffu, i < nb && c >= P - tol);
+              if (hm) {
+                const int hl = __ffs(hm) - 1;
+                cut = i0 + hl;
+                const bool ok = (c - P > tol && P - prev > tol);
+                u_ = !__shfl_sync(0xffffffffu, ok, hl);
+                break;
+              }
+              off = __shfl_sync(0xffffffffu, c, 31);
+            }
+            if (cut < 0) u_ = true;
+            if (!u_) {
+              bool bad_order = false;
+              for (int i = max(cut, 1) + lane; i <= min(cut + 1, nb - 1); i += 32) {
+                float za = cand_z(sm.cand[i - 1]), zb = cand_z(sm.cand[i]);
+                if (za != zb) {
+                  double da = __ddiv_rn((double)za, tv.T), db = __ddiv_rn((double)zb, tv.T);
+                  if (da - db <= fmax(fabs(da), fabs(ec.mT)) * 8.0 * kEps64) bad_order = true;
+                }
+              }
+              u_ |= __any_sync(0xffffffffu, bad_order);
+            }
+            if (lane == 0) {
+              sm.isc[3] = cut + 1;
+              sm.isc[4] = u_;
+            }
           }
           __syncthreads();
           if (sm.isc[4]) {
-            fail = true;
+            unc = true;
           } else {
             mode = 2;
-            L = sm.isc[3];  // first L bracket candidates are kept
+            L = sm.isc[3];  // the first L bracket candidates are kept
           }
+          __syncthreads();
+        }
+        if (unc) {
+          if (tid == 0 && !precise) atomicAdd(&counters[4], 1ull);
+          continue;  // -> PRECISE pass (or EXACT after it)
         }
       }
-    }
 
-    if (fail) {
-      if (tid == 0) {
-        int* q = REFINE ? ws.q_exact : ws.q_refine;
-        int pos = atomicAdd(q, 1);
-        q[1 + pos] = task_id;
-        atomicAdd(&counters[0], 1ull);
-      }
-      __syncthreads();
-      continue;
-    }
-
-    // ---------------- kept small list in id order (modes 1 and 2)
-    if (mode != 0) {
-      // key: id ascending == descending (~id); payload: index into cand/ce
-      // rank sort by id (ids are distinct; L is small: top-k, nucleus or bracket members)
-      for (int i = tid; i < L; i += RS_THREADS) {
-        int id = cand_id(sm.cand[i]);
-        int rank = 0;
-        for (int j = 0; j < L; ++j) rank += (cand_id(sm.cand[j]) < id);
-        sm.sl_id[rank] = id;
-        sm.sl_e[rank] = sm.ce[i];
-      }
-      __syncthreads();
-    }
-
-    if (mode == 1) {
-      // inclusive prefix (sequential, exact order) on thread 0; L <= 2048
-      if (tid == 0) {
-        double c = 0.0;
-        for (int i = 0; i < L; ++i) {
-          c += sm.sl_e[i];
-          sm.sl_e[i] = c;
+      // ---------------- kept small list in id order (modes 1 and 2)
+      if (mode != 0) {
+        // ids are distinct: rank by counting (L is a top-k, a small nucleus or a bracket prefix)
+        for (int i = tid; i < L; i += RS_THREADS) {
+          const int id = cand_id(sm.cand[i]);
+          int rank = 0;
+          for (int j = 0; j < L; ++j) rank += (cand_id(sm.cand[j]) < id);
+          sm.sl_id[rank] = id;
+          sm.sl_e[rank] = sm.ce[i];
         }
-        sm.dsc[0] = c;
+        __syncthreads();
       }
-      __syncthreads();
-      const double K = sm.dsc[0];
-      // kept e's are precise: only the reference's rounding and ours remain
-      const double tolK = K * ((double)(V + L + 64) * 4.0 * kEps64 + 4.0 * kRefExpErr);
-      int need = 0;
-      for (int64_t d = tv.d0 + tid; d < tv.d1; d += RS_THREADS) {
-        const double u = draw_u(io, d, tv);
-        const double t = u * K;
-        int lo = 0, hi = L;
-        while (lo < hi) {
-          int mid = (lo + hi) >> 1;
-          if (sm.sl_e[mid] > t) hi = mid;
-          else lo = mid + 1;
+
+      if (mode == 1) {
+        if (warp == 0) {  // inclusive prefix of the kept e's in id order
+          double off = 0.0;
+          for (int i0 = 0; i0 < L; i0 += 32) {
+            const int i = i0 + lane;
+            const double e = i < L ? sm.sl_e[i] : 0.0;
+            const double c = off + warp_incl_scan(e);
+            if (i < L) sm.sl_e[i] = c;
+            off = __shfl_sync(0xffffffffu, c, 31);
+          }
+          if (lane == 0) sm.dsc[0] = off;
         }
-        bool ok = lo < L && (lo == 0 || t - sm.sl_e[lo - 1] > tolK) && (sm.sl_e[lo] - t > tolK);
-        int i = min(lo, L - 1);
-        io.token[d] = sm.sl_id[i];
-        if (io.flags) io.flags[d] = tier_flag;
-        need |= !ok;
+        __syncthreads();
+        const double K = sm.dsc[0];
+        // kept e's are precise: only the reference's rounding and ours remain
+        const double tolK = K * ((double)(V + L + 64) * 4.0 * kEps64 + 4.0 * kRefExpErr + 2.0 * relArg);
+        int need = 0;
+        for (int64_t d = tv.d0 + tid; d < tv.d1; d += RS_THREADS) {
+          const double u = draw_u(io, d, tv);
+          const double t = u * K;
+          int lo = 0, hi = L;
+          while (lo < hi) {
+            const int mid = (lo + hi) >> 1;
+            if (sm.sl_e[mid] > t) hi = mid;
+            else lo = mid + 1;
+          }
+          // lower boundary 0 (nothing kept before) is exact in both implementations
+          const bool ok = lo < L && (lo == 0 || t - sm.sl_e[lo - 1] > tolK) && (sm.sl_e[lo] - t > tolK);
+          io.token[d] = sm.sl_id[min(lo, L - 1)];
+          if (io.flags) io.flags[d] = tier_flag;
+          need |= !ok;
+        }
+        need = __syncthreads_or(need);
+        if (!need) {
+          done = true;
+        } else if (tid == 0 && !precise) {
+          atomicAdd(&counters[5], 1ull);
+        }
+        continue;
       }
-      need = __syncthreads_or(need);
-      if (need && tid == 0) sm.isc[7] = 1;
-    } else {
-      // ---------------- modes 0 and 2: per-warp masses, owner warp searches its range
+
+      // ---------------- modes 0 and 2: per-warp masses, the owner warp searches its range
       if (mode == 2) {
         // merge the warp's scratch list A with its kept bracket members into scratch M
         // (both id-ordered): new position = own index + #other-list ids below.
         if (tid <= RS_WARPS) {
-          // sl segment of warp w: ids in [w*C, (w+1)*C)
-          int w = tid, bound = min(V, w * C), lo = 0, hi = L;
+          const int w = tid, bound = min(V, w * C);
+          int lo = 0, hi = L;
           while (lo < hi) {
-            int mid = (lo + hi) >> 1;
+            const int mid = (lo + hi) >> 1;
             if (sm.sl_id[mid] < bound) lo = mid + 1;
             else hi = mid;
           }
@@ -751,55 +875,45 @@ resample_kernel(const char* __restrict__ rows, int64_t row_bytes, int Vdef, cons
         __syncthreads();
         const int na = sm.wcount[warp];
         const int s0 = sm.wsl[warp], s1 = sm.wsl[warp + 1];
-        const int nbw = s1 - s0;
-        if (na + nbw > SCR_PER_WARP) {
+        if (na + (s1 - s0) > SCR_PER_WARP) {
           if (lane == 0) sm.isc[2] = 1;
         } else {
           for (int i = lane; i < na; i += 32) {
-            int id = scrA_id[warp * SCR_PER_WARP + i];
+            const int id = scrA_id[warp * SCR_PER_WARP + i];
             int lo = s0, hi = s1;
             while (lo < hi) {
-              int mid = (lo + hi) >> 1;
+              const int mid = (lo + hi) >> 1;
               if (sm.sl_id[mid] < id) lo = mid + 1;
               else hi = mid;
             }
-            int pos = i + (lo - s0);
-            scrM_id[warp * SCR_PER_WARP + pos] = id;
-            scrM_e[warp * SCR_PER_WARP + pos] = scrA_e[warp * SCR_PER_WARP + i];
+            scrM_id[warp * SCR_PER_WARP + i + (lo - s0)] = id;
+            scrM_e[warp * SCR_PER_WARP + i + (lo - s0)] = scrA_e[warp * SCR_PER_WARP + i];
           }
           double add = 0.0;
           for (int b = s0 + lane; b < s1; b += 32) {
-            int id = sm.sl_id[b];
+            const int id = sm.sl_id[b];
             int lo = 0, hi = na;
             while (lo < hi) {
-              int mid = (lo + hi) >> 1;
+              const int mid = (lo + hi) >> 1;
               if (scrA_id[warp * SCR_PER_WARP + mid] < id) lo = mid + 1;
               else hi = mid;
             }
-            int pos = (b - s0) + lo;
-            scrM_id[warp * SCR_PER_WARP + pos] = id;
-            scrM_e[warp * SCR_PER_WARP + pos] = sm.sl_e[b];
+            scrM_id[warp * SCR_PER_WARP + (b - s0) + lo] = id;
+            scrM_e[warp * SCR_PER_WARP + (b - s0) + lo] = sm.sl_e[b];
             add += sm.sl_e[b];
           }
           add = warp_sum(add);
           if (lane == 0) {
-            sm.wsum[warp] += add;
-            sm.wcount[warp] = na + nbw;
+            sm.wsum[warp] = sm.werr[warp] + add;  // kept mass of this warp's range (precise e's)
+            sm.wcount[warp] = na + (s1 - s0);
           }
         }
         __syncthreads();
         if (sm.isc[2]) {
-          if (tid == 0) {
-            int pos = atomicAdd(REFINE ? ws.q_exact : ws.q_refine, 1);
-            (REFINE ? ws.q_exact : ws.q_refine)[1 + pos] = task_id;
-            atomicAdd(&counters[0], 1ull);
-          }
-          __syncthreads();
-          continue;
+          to_exact = true;
+          if (tid == 0) atomicAdd(&counters[7], 1ull);
+          break;
         }
-        __threadfence_block();
-      } else {
-        if (lane == 0) sm.werr[warp] = sm.wsum[warp] * relE;
       }
       if (tid == 0) {
         double c = 0.0;
@@ -811,14 +925,11 @@ resample_kernel(const char* __restrict__ rows, int64_t row_bytes, int Vdef, cons
       }
       __syncthreads();
       const double K = sm.wpre[RS_WARPS];
-      // absolute error bounds: total mass, and prefix masses through warp w
-      const double EK = (mode == 0) ? E_S : K * ((double)(V + 64) * 4.0 * kEps64 + 4.0 * kRefExpErr);
-      double Epre = 0.0;
-      if (mode == 0) {
-        for (int w = 0; w <= warp; ++w) Epre += sm.werr[w];
-      } else {
-        Epre = EK;
-      }
+      // mode 0: per-element relative bound relE on every partial sum (fast or precise e's);
+      // mode 2: kept e's are precise
+      const double relD = (mode == 0) ? relE : ((double)(V + 64) * 4.0 * kEps64 + 4.0 * kRefExpErr + 2.0 * relArg);
+      const double absD = (mode == 0) ? absE : 0.0;
+      const bool exact_zero_left = precise || mode == 2;  // no flushed mass can precede
       int need = 0;
       for (int64_t dbase = tv.d0; dbase < tv.d1; dbase += 32) {
         const int64_t d = dbase + lane;
@@ -828,7 +939,7 @@ resample_kernel(const char* __restrict__ rows, int64_t row_bytes, int Vdef, cons
           u = draw_u(io, d, tv);
           t = u * K;
           if (!(t < K)) {
-            if (warp == 0) need = 1;  // clamp region: let the next tier emulate it
+            if (warp == 0) need = 1;  // clamp region: let EXACT emulate it
           } else {
             mine = (t >= sm.wpre[warp]) && (t < sm.wpre[warp + 1]);
           }
@@ -851,24 +962,17 @@ resample_kernel(const char* __restrict__ rows, int64_t row_bytes, int Vdef, cons
               double ls = 0.0;
 #pragma unroll
               for (int j = 0; j < 8; ++j) {
-                ev[j] = (my0 + j < ce) ? elem_exp<REFINE>(ec, v[j]) : 0.0;
+                ev[j] = precise ? lite_exp(ec, v[j], sm.t16) : (double)fast_exp(ec, v[j]);
                 ls += ev[j];
               }
-              double x = ls;
-#pragma unroll
-              for (int o = 1; o < 32; o <<= 1) {
-                double y = __shfl_up_sync(0xffffffffu, x, o);
-                if (lane >= o) x += y;
-              }
-              const double excl = off + (x - ls);
-              const bool hit = (ls > 0.0) && (tt < off + x);
-              const unsigned hm = __ballot_sync(0xffffffffu, hit);
+              const double x = warp_incl_scan(ls);
+              const unsigned hm = __ballot_sync(0xffffffffu, (ls > 0.0) && (tt < off + x));
               if (hm) {
                 const int hl = __ffs(hm) - 1;
                 if (lane == hl) {
-                  double c = excl;
+                  double c = off + (x - ls);
                   for (int j = 0; j < 8; ++j) {
-                    double nc = c + ev[j];
+                    const double nc = c + ev[j];
                     if (ev[j] > 0.0 && tt < nc) {
                       found = my0 + j;
                       flo = c;
@@ -895,14 +999,8 @@ resample_kernel(const char* __restrict__ rows, int64_t row_bytes, int Vdef, cons
                 e = scrM_e[warp * SCR_PER_WARP + i];
                 id = scrM_id[warp * SCR_PER_WARP + i];
               }
-              double x = e;
-#pragma unroll
-              for (int o = 1; o < 32; o <<= 1) {
-                double y = __shfl_up_sync(0xffffffffu, x, o);
-                if (lane >= o) x += y;
-              }
-              const bool hit = (i < n) && (e > 0.0) && (tt < off + x);
-              const unsigned hm = __ballot_sync(0xffffffffu, hit);
+              const double x = warp_incl_scan(e);
+              const unsigned hm = __ballot_sync(0xffffffffu, (i < n) && (e > 0.0) && (tt < off + x));
               if (hm) {
                 const int hl = __ffs(hm) - 1;
                 found = __shfl_sync(0xffffffffu, id, hl);
@@ -914,10 +1012,10 @@ resample_kernel(const char* __restrict__ rows, int64_t row_bytes, int Vdef, cons
             }
           }
           if (lane == 0) {
-            const double tol = uu * EK + Epre + tt * relRef * 4.0;
-            // flo == 0 with precise e's: nothing precedes the element, so t >= 0 lies on its
-            // right exactly.  FAST flushes e < 2^-126 to zero, so it must certify the margin.
-            bool ok = found >= 0 && (tt - flo > tol || ((REFINE || mode == 2) && flo == 0.0)) && (fhi - tt > tol);
+            // correlated bound: err(u*K - A) <= rel * ((1-u)*A + u*(K - A)) + abs
+            const double tlo = relD * ((1.0 - uu) * flo + uu * (K - flo)) + absD + tt * relRef * 4.0;
+            const double thi = relD * ((1.0 - uu) * fhi + uu * (K - fhi)) + absD + tt * relRef * 4.0;
+            const bool ok = found >= 0 && (tt - flo > tlo || (exact_zero_left && flo == 0.0)) && (fhi - tt > thi);
             io.token[dbase + src] = found;
             if (io.flags) io.flags[dbase + src] = tier_flag;
             need |= !ok;
@@ -925,17 +1023,21 @@ resample_kernel(const char* __restrict__ rows, int64_t row_bytes, int Vdef, cons
         }
       }
       need = __syncthreads_or(need);
-      if (need && tid == 0) sm.isc[7] = 1;
+      if (!need) {
+        done = true;
+      } else if (tid == 0 && !precise) {
+        atomicAdd(&counters[5], 1ull);
+      }
     }
-    __syncthreads();
-    if (sm.isc[7] && tid == 0) atomicAdd(&counters[5], 1ull);
-    if (sm.isc[7] && tid == 0) {
-      int* q = REFINE ? ws.q_exact : ws.q_refine;
-      int pos = atomicAdd(q, 1);
-      q[1 + pos] = task_id;
-      atomicAdd(&counters[0], 1ull);
+
+    if (!done) {
+      // FAST and PRECISE could not certify (or row too extreme): numpy emulation
+      if (tid == 0) {
+        int pos = atomicAdd(ws.q_exact, 1);
+        ws.q_exact[1 + pos] = task_id;
+        atomicAdd(&counters[3], 1ull);
+      }
     }
-    __syncthreads();
   }
 }
 
@@ -964,6 +1066,7 @@ exact_kernel(const char* __restrict__ rows, int64_t row_bytes, int Vdef, const l
   for (int ti = blockIdx.x; ti < ntask; ti += gridDim.x) {
     const int task_id = task_list[1 + ti];
     TaskView tv;
+    if (tasks[task_id].draw_end <= tasks[task_id].draw_begin) continue;
     if (!resolve_task(tasks[task_id], rows, row_bytes, Vdef, cm, tv)) continue;
     const int V = tv.V;
     // max (fp32 exact)
@@ -1104,10 +1207,12 @@ static int num_sms() {
 
 constexpr int kExactCtas = 32;
 
+static int grid_ctas() { return num_sms() * RS_MIN_BLOCKS; }
+
 int64_t workspace_bytes(int64_t n_tasks, int64_t vocab) {
-  const int64_t grid = num_sms();
+  const int64_t grid = grid_ctas();
   int64_t b = 0;
-  b += 2 * (((n_tasks + 1) * 4 + 255) & ~255ll);
+  b += ((n_tasks + 1) * 4 + 255) & ~255ll;
   b += ((grid * 2 * SCR_PER_CTA * 4) + 255) & ~255ll;
   b += ((grid * 2 * SCR_PER_CTA * 8) + 255) & ~255ll;
   b += ((kExactCtas * vocab * 3 * 8) + 255) & ~255ll;
@@ -1120,7 +1225,7 @@ template <int DT>
 static int launch_all(const char* rows, int64_t row_bytes, int V, const lc_task* tasks, int64_t n_tasks, CacheMap cm,
                       DrawIO io, void* d_ws, int64_t ws_bytes, int64_t* d_counters, cudaStream_t st) {
   if (n_tasks > INT32_MAX - 2) return LC_E_ARG;
-  const int grid = num_sms();
+  const int grid = grid_ctas();
   char* p = (char*)d_ws;
   auto take = [&](int64_t n) {
     char* r = p;
@@ -1128,7 +1233,6 @@ static int launch_all(const char* rows, int64_t row_bytes, int V, const lc_task*
     return r;
   };
   Workspace ws;
-  ws.q_refine = (int*)take((n_tasks + 1) * 4);
   ws.q_exact = (int*)take((n_tasks + 1) * 4);
   ws.scr_id = (int*)take((int64_t)grid * 2 * SCR_PER_CTA * 4);
   ws.scr_e = (double*)take((int64_t)grid * 2 * SCR_PER_CTA * 8);
@@ -1140,7 +1244,6 @@ static int launch_all(const char* rows, int64_t row_bytes, int V, const lc_task*
     lcb_set_last_error("resample workspace too small (see lc_resample_workspace_bytes)", __FILE__, __LINE__);
     return LC_E_ARG;
   }
-  LCB_CUDA_TRY(cudaMemsetAsync(ws.q_refine, 0, 4, st));
   LCB_CUDA_TRY(cudaMemsetAsync(ws.q_exact, 0, 4, st));
   unsigned long long* counters = d_counters ? (unsigned long long*)d_counters : cnt;
   if (!d_counters) LCB_CUDA_TRY(cudaMemsetAsync(cnt, 0, 64, st));
@@ -1148,18 +1251,11 @@ static int launch_all(const char* rows, int64_t row_bytes, int V, const lc_task*
   const size_t smem = sizeof(Smem);
   static bool attr_set[2] = {false, false};
   if (!attr_set[DT]) {
-    LCB_CUDA_TRY(cudaFuncSetAttribute(resample_kernel<DT, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      (int)smem));
-    LCB_CUDA_TRY(cudaFuncSetAttribute(resample_kernel<DT, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      (int)smem));
+    LCB_CUDA_TRY(cudaFuncSetAttribute(resample_kernel<DT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     attr_set[DT] = true;
   }
   const int g1 = (int)(n_tasks < grid ? n_tasks : grid);
-  resample_kernel<DT, false><<<g1, RS_THREADS, smem, st>>>(rows, row_bytes, V, tasks, (int)n_tasks, nullptr, cm, io,
-                                                            ws, counters);
-  LCB_CUDA_TRY(cudaGetLastError());
-  resample_kernel<DT, true><<<grid, RS_THREADS, smem, st>>>(rows, row_bytes, V, tasks, (int)n_tasks, ws.q_refine, cm,
-                                                            io, ws, counters);
+  resample_kernel<DT><<<g1, RS_THREADS, smem, st>>>(rows, row_bytes, V, tasks, (int)n_tasks, cm, io, ws, counters);
   LCB_CUDA_TRY(cudaGetLastError());
   exact_kernel<DT><<<kExactCtas, EX_THREADS, 0, st>>>(rows, row_bytes, V, tasks, ws.q_exact, cm, io, ex_scr, ex_iscr,
                                                       scr_stride, counters);
@@ -1213,6 +1309,8 @@ __global__ void probe_fast_exp_kernel(const float* z, int64_t n, float m, double
   double Ld = 1.4426950408889634 / T;
   c.Lhi = (float)Ld;
   c.Llo = (float)(Ld - (double)c.Lhi);
+  c.md = (double)m;
+  c.L16 = 16.0 * Ld;
   out[i] = fast_exp(c, z[i]);
 }
 }  // namespace lcb
