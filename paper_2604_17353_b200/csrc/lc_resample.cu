@@ -170,6 +170,13 @@ __device__ __forceinline__ double ref_exp(const ExpCtx& c, float z) {
   return exp(s);
 }
 
+// 2^(b/4) (fp32, relative error <= 2^-24)
+__device__ __forceinline__ float bin_scale(int b) {
+  const float frac = (b & 3) == 0 ? 1.0f : (b & 3) == 1 ? 1.18920711500272f : (b & 3) == 2 ? 1.41421356237310f
+                                                                                            : 1.68179283050743f;
+  return __int_as_float(((b >> 2) + 127) << 23) * frac;
+}
+
 // log2-distance bin of z below the max (monotone non-increasing in z)
 __device__ __forceinline__ int nbin(const ExpCtx& c, float z) {
   float a = (z - c.m) * c.Lhi;
@@ -645,25 +652,33 @@ resample_kernel(const char* __restrict__ rows, int64_t row_bytes, int Vdef, cons
           if (large_state == 0) {
             for (int i = tid; i < RS_WARPS * NBINS; i += RS_THREADS) (&sm.hist[0][0])[i] = 0u;
             __syncthreads();
+            // per-bin relative fixed point: bin b holds e in (2^-(b+1)/4, 2^-b/4] (up to the
+            // approximate binning argument), so q = e * 2^(b/4) * qscale is < 2^31/C per element
+            // and the bin mass carries a relative error <= 2^-(31-lgC)/0.8 + fast_exp's.
             const int lgC = 32 - __clz(C + 1);
-            const float qscale = ldexpf(1.0f, 31 - lgC);
+            const float qscale = ldexpf(1.0f, 30 - lgC);
             warp_pass<DT, 2>(tv.row, cb, ce, vec, lane, [&](int e0, const float* v) {
 #pragma unroll
               for (int j = 0; j < 8; ++j)
-                if (e0 + j < ce) atomicAdd(&sm.hist[warp][nbin(ec, v[j])], __float2uint_rn(fast_exp(ec, v[j]) * qscale));
+                if (e0 + j < ce) {
+                  const int b = nbin(ec, v[j]);
+                  const float q = fast_exp(ec, v[j]) * bin_scale(b) * qscale;
+                  atomicAdd(&sm.hist[warp][b], __float2uint_rn(fminf(q, 2.0f * qscale)));
+                }
             });
             __syncthreads();
             if (warp == 0) {
               // bracket [blo, bhi] of bins that can hold the cut (fast mass + quantisation error)
               const double inv = 1.0 / (double)qscale;
-              const double qerr = (double)V * 0.5 * inv + 2.0 * E_S + P * relRef + S * 2e-6;
+              const double qrel = ldexp(1.0, lgC - 30) * 1.25 + kEx2RelErr * 2.0 + 1e-6;
+              const double qerr = qrel * S + 2.0 * E_S + P * relRef;
               double cum = 0.0;
               int blo = NBINS - 1, bhi = NBINS - 1;
               bool got_lo = false;
               for (int b0 = 0; b0 < NBINS; b0 += 32) {
                 unsigned long long hs = 0;
                 for (int w = 0; w < RS_WARPS; ++w) hs += sm.hist[w][b0 + lane];
-                const double incl = cum + warp_incl_scan((double)hs * inv);
+                const double incl = cum + warp_incl_scan((double)hs * inv * exp2(-0.25 * (double)(b0 + lane)));
                 const unsigned lo_m = __ballot_sync(0xffffffffu, incl >= P - qerr);
                 const unsigned hi_m = __ballot_sync(0xffffffffu, incl >= P + qerr);
                 if (!got_lo && lo_m) {
@@ -944,36 +959,75 @@ resample_kernel(const char* __restrict__ rows, int64_t row_bytes, int Vdef, cons
             mine = (t >= sm.wpre[warp]) && (t < sm.wpre[warp + 1]);
           }
         }
-        unsigned own = __ballot_sync(0xffffffffu, mine);
-        while (own) {
-          const int src = __ffs(own) - 1;
-          own &= own - 1;
-          const double tt = __shfl_sync(0xffffffffu, t, src);
-          const double uu = __shfl_sync(0xffffffffu, u, src);
-          int found = -1;
-          double flo = 0.0, fhi = 0.0;
-          double off = sm.wpre[warp];
-          if (mode == 0) {
-            for (int e0 = cb; e0 < ce; e0 += 256) {
-              const int my0 = e0 + 8 * lane;
-              float v[8];
-              load8<DT>(tv.row, my0, ce, vec, v);
-              double ev[8];
-              double ls = 0.0;
+        const unsigned own = __ballot_sync(0xffffffffu, mine);
+        if (!own) continue;
+        // the warp's targets, sorted ascending (warp bitonic on (t, lane)), searched in ONE
+        // pass over its id range
+        const int nown = __popc(own);
+        double st = mine ? t : INFINITY;
+        int ssrc = lane;
 #pragma unroll
-              for (int j = 0; j < 8; ++j) {
-                ev[j] = precise ? lite_exp(ec, v[j], sm.t16) : (double)fast_exp(ec, v[j]);
-                ls += ev[j];
-              }
-              const double x = warp_incl_scan(ls);
-              const unsigned hm = __ballot_sync(0xffffffffu, (ls > 0.0) && (tt < off + x));
+        for (int k2 = 2; k2 <= 32; k2 <<= 1) {
+#pragma unroll
+          for (int j2 = k2 >> 1; j2 > 0; j2 >>= 1) {
+            const double ot = __shfl_xor_sync(0xffffffffu, st, j2);
+            const int os = __shfl_xor_sync(0xffffffffu, ssrc, j2);
+            const bool asc = (lane & k2) == 0 || k2 == 32;
+            const bool lower = (lane & j2) == 0;
+            const bool take_other = (lower == asc) ? (ot < st || (ot == st && os < ssrc))
+                                                   : (ot > st || (ot == st && os > ssrc));
+            if (take_other) {
+              st = ot;
+              ssrc = os;
+            }
+          }
+        }
+        const double su = __shfl_sync(0xffffffffu, u, ssrc);  // u of the target held by this lane
+        int k = 0;
+        double off = sm.wpre[warp];
+        // certify + write target k (found/flo/fhi broadcast to all lanes)
+        auto finish = [&](int found, double flo, double fhi) {
+          const double tt = __shfl_sync(0xffffffffu, st, k);
+          const double uu = __shfl_sync(0xffffffffu, su, k);
+          const int src = __shfl_sync(0xffffffffu, ssrc, k);
+          if (lane == 0) {
+            // correlated bound: err(u*K - A) <= rel * ((1-u)*A + u*(K - A)) + abs
+            const double tlo = relD * ((1.0 - uu) * flo + uu * (K - flo)) + absD + tt * relRef * 4.0;
+            const double thi = relD * ((1.0 - uu) * fhi + uu * (K - fhi)) + absD + tt * relRef * 4.0;
+            const bool ok = found >= 0 && (tt - flo > tlo || (exact_zero_left && flo == 0.0)) && (fhi - tt > thi);
+            io.token[dbase + src] = found;
+            if (io.flags) io.flags[dbase + src] = tier_flag;
+            need |= !ok;
+          }
+          ++k;
+        };
+        if (mode == 0) {
+          for (int e0 = cb; e0 < ce && k < nown; e0 += 256) {
+            const int my0 = e0 + 8 * lane;
+            float v[8];
+            load8<DT>(tv.row, my0, ce, vec, v);
+            double ev[8];
+            double ls = 0.0;
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+              ev[j] = precise ? lite_exp(ec, v[j], sm.t16) : (double)fast_exp(ec, v[j]);
+              ls += ev[j];
+            }
+            const double x = warp_incl_scan(ls);
+            const double tot = __shfl_sync(0xffffffffu, x, 31);
+            while (k < nown) {
+              const double tk = __shfl_sync(0xffffffffu, st, k);
+              if (!(tk < off + tot)) break;
+              const unsigned hm = __ballot_sync(0xffffffffu, (ls > 0.0) && (tk < off + x));
+              int found = -1;
+              double flo = 0.0, fhi = 0.0;
               if (hm) {
                 const int hl = __ffs(hm) - 1;
                 if (lane == hl) {
                   double c = off + (x - ls);
                   for (int j = 0; j < 8; ++j) {
                     const double nc = c + ev[j];
-                    if (ev[j] > 0.0 && tt < nc) {
+                    if (ev[j] > 0.0 && tk < nc) {
                       found = my0 + j;
                       flo = c;
                       fhi = nc;
@@ -985,42 +1039,41 @@ resample_kernel(const char* __restrict__ rows, int64_t row_bytes, int Vdef, cons
                 found = __shfl_sync(0xffffffffu, found, hl);
                 flo = __shfl_sync(0xffffffffu, flo, hl);
                 fhi = __shfl_sync(0xffffffffu, fhi, hl);
-                break;
               }
-              off = __shfl_sync(0xffffffffu, off + x, 31);
+              finish(found, flo, fhi);
             }
-          } else {
-            const int n = sm.wcount[warp];
-            for (int i0 = 0; i0 < n; i0 += 32) {
-              const int i = i0 + lane;
-              double e = 0.0;
-              int id = -1;
-              if (i < n) {
-                e = scrM_e[warp * SCR_PER_WARP + i];
-                id = scrM_id[warp * SCR_PER_WARP + i];
-              }
-              const double x = warp_incl_scan(e);
-              const unsigned hm = __ballot_sync(0xffffffffu, (i < n) && (e > 0.0) && (tt < off + x));
+            off += tot;
+          }
+        } else {
+          const int n = sm.wcount[warp];
+          for (int i0 = 0; i0 < n && k < nown; i0 += 32) {
+            const int i = i0 + lane;
+            double e = 0.0;
+            int id = -1;
+            if (i < n) {
+              e = scrM_e[warp * SCR_PER_WARP + i];
+              id = scrM_id[warp * SCR_PER_WARP + i];
+            }
+            const double x = warp_incl_scan(e);
+            const double tot = __shfl_sync(0xffffffffu, x, 31);
+            while (k < nown) {
+              const double tk = __shfl_sync(0xffffffffu, st, k);
+              if (!(tk < off + tot)) break;
+              const unsigned hm = __ballot_sync(0xffffffffu, (i < n) && (e > 0.0) && (tk < off + x));
+              int found = -1;
+              double flo = 0.0, fhi = 0.0;
               if (hm) {
                 const int hl = __ffs(hm) - 1;
                 found = __shfl_sync(0xffffffffu, id, hl);
                 flo = __shfl_sync(0xffffffffu, off + x - e, hl);
                 fhi = __shfl_sync(0xffffffffu, off + x, hl);
-                break;
               }
-              off = __shfl_sync(0xffffffffu, off + x, 31);
+              finish(found, flo, fhi);
             }
-          }
-          if (lane == 0) {
-            // correlated bound: err(u*K - A) <= rel * ((1-u)*A + u*(K - A)) + abs
-            const double tlo = relD * ((1.0 - uu) * flo + uu * (K - flo)) + absD + tt * relRef * 4.0;
-            const double thi = relD * ((1.0 - uu) * fhi + uu * (K - fhi)) + absD + tt * relRef * 4.0;
-            const bool ok = found >= 0 && (tt - flo > tlo || (exact_zero_left && flo == 0.0)) && (fhi - tt > thi);
-            io.token[dbase + src] = found;
-            if (io.flags) io.flags[dbase + src] = tier_flag;
-            need |= !ok;
+            off += tot;
           }
         }
+        while (k < nown) finish(-1, 0.0, 0.0);  // rounding left a target past the range end
       }
       need = __syncthreads_or(need);
       if (!need) {
