@@ -229,9 +229,10 @@ int lc_replay_tasks(const int32_t* d_slot, const int32_t* d_len, int64_t n_req, 
 int lc_replay_accept(const int32_t* d_tokens, const int32_t* d_cached, const int32_t* d_len, int64_t n_req,
                      int32_t max_pos, int32_t n_branch, int32_t* d_replayed, int32_t* d_diverged, void* stream);
 
-/* Test probe: the FAST tier's exponential e(z) ~ exp((z - m)/T) for given z,
- * so tests can measure its error bound against fp64 (not on the hot path). */
-int lc_probe_fast_exp(const float* d_z, int64_t n, float m, double temperature, float* d_out, void* stream);
+/* Test probe: the resample tiers' exponentials e(z) ~ exp((z - m)/T) for given
+ * z (mode 0 FAST corrected, 1 FAST cheap, 2 PRECISE table fp64), so tests can
+ * pin their error bounds against fp64 (not on the hot path).                  */
+int lc_probe_exp(const float* d_z, int64_t n, float m, double temperature, int mode, double* d_out, void* stream);
 
 /* Synchronising: copy the counters out. */
 int lc_cache_stats_get(lc_cache* cache, lc_cache_stats* h_out, void* stream);

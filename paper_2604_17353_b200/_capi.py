@@ -100,7 +100,7 @@ _SIGS = {
     "lc_cache_slab": (C.c_int, [P, C.POINTER(P), C.POINTER(I64), C.POINTER(I32)]),
     "lc_cache_page_table": (C.c_int, [P, C.POINTER(P), C.POINTER(I32), C.POINTER(I32)]),
     "lc_cache_snapshot": (C.c_int, [P, P, P, P, P, P, P, P, P]),
-    "lc_probe_fast_exp": (C.c_int, [P, I64, C.c_float, D, P, P]),
+    "lc_probe_exp": (C.c_int, [P, I64, C.c_float, D, C.c_int, P, P]),
     "lc_replay_tasks": (C.c_int, [P, P, I64, I32, I32, P, P, P, P, P]),
     "lc_replay_accept": (C.c_int, [P, P, P, I64, I32, I32, P, P, P]),
 }

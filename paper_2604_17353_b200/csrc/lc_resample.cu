@@ -50,7 +50,9 @@ constexpr int SCR_PER_CTA = SCR_PER_WARP * RS_WARPS;
 // ex2.approx.ftz.f32 relative error bound (PTX ISA: ~2 ulp).  The GPU test
 // tests/test_gpu_parity.py::test_fast_exp_error_bound measures fast_exp over
 // dense argument grids and fails if this constant is ever exceeded.
-constexpr double kEx2RelErr = 4.0e-7;
+constexpr double kEx2RelErr = 4.0e-7;    // fast_exp (corrected) incl. margin
+constexpr double kEx2Raw = 2.5e-7;       // ex2.approx.ftz.f32 alone (cheap_exp), measured bound + margin
+constexpr double kArgRel = 3.0 * 5.9604644775390625e-08 * 0.6931471805599453 * 1.01;  // cheap_exp: per |a|
 constexpr double kCorrErr = 1.0e-10;                       // 2nd-order term of the argument correction
 constexpr double kSum8Err = 3.0 * 5.9604644775390625e-08;  // fp32 pairwise sum of 8 (3 roundings)
 constexpr double kRefExpErr = 8.881784197001252e-16;       // libm / numpy exp vs exact: 4 ulp
@@ -138,6 +140,75 @@ __device__ __forceinline__ float fast_exp(const ExpCtx& c, float z) {
   float alo = fmaf(s, c.Lhi, -ahi) + fmaf(err, c.Lhi, s * c.Llo);
   float e = ex2_approx(ahi);
   return (e > 0.0f) ? fmaf(e, alo * 0.69314718055994531f, e) : 0.0f;
+}
+
+// CHEAP (truncated modes, where only the row mass and bracketing use it):
+// e = ex2(fl(fl(z - m) * Lhi)).  Relative error <= kEx2Raw + kArgRel * |a|
+// (three fp32 roundings carried into the argument); a is clamped at -200 so
+// -inf inputs give e = 0 and e*a = 0.
+__device__ __forceinline__ float cheap_exp(const ExpCtx& c, float z, float& a) {
+  a = fmaxf((z - c.m) * c.Lhi, -200.0f);
+  return ex2_approx(a);
+}
+
+__device__ __forceinline__ float max_nan(float a, float b) {
+  float r;
+  asm("max.NaN.f32 %0, %1, %2;" : "=f"(r) : "f"(a), "f"(b));
+  return r;
+}
+__device__ __forceinline__ float min_nan(float a, float b) {
+  float r;
+  asm("min.NaN.f32 %0, %1, %2;" : "=f"(r) : "f"(a), "f"(b));
+  return r;
+}
+
+// Phase A: per-thread max and min over the warp's id range, NaN-propagating,
+// packed bf16x2 for bf16 rows (one HMNMX2 per two elements).
+template <int DT>
+__device__ __forceinline__ void phase_a(const char* row, int cb, int ce, bool vec, int lane, float& tmax, float& tmin) {
+  if (DT == LC_BF16 && vec) {
+    const uint16_t* r = reinterpret_cast<const uint16_t*>(row);
+    __nv_bfloat162 mx = __float2bfloat162_rn(-INFINITY), mn = __float2bfloat162_rn(INFINITY);
+    for (int base = cb; base < ce; base += 256 * 4) {
+      uint4 q[4];
+      bool full[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int e0 = base + 256 * u + 8 * lane;
+        full[u] = e0 + 8 <= ce;
+        if (full[u]) q[u] = __ldg(reinterpret_cast<const uint4*>(r + e0));
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int e0 = base + 256 * u + 8 * lane;
+        if (full[u]) {
+          const uint32_t w[4] = {q[u].x, q[u].y, q[u].z, q[u].w};
+#pragma unroll
+          for (int k = 0; k < 4; ++k) {
+            const __nv_bfloat162 x = *reinterpret_cast<const __nv_bfloat162*>(&w[k]);
+            mx = __hmax2_nan(mx, x);
+            mn = __hmin2_nan(mn, x);
+          }
+        } else {
+          for (int j = 0; j < 8 && e0 + j < ce; ++j) {
+            const float f = bf16_bits_to_f32(r[e0 + j]);
+            tmax = max_nan(tmax, f);
+            tmin = min_nan(tmin, f);
+          }
+        }
+      }
+    }
+    tmax = max_nan(tmax, max_nan(__low2float(mx), __high2float(mx)));
+    tmin = min_nan(tmin, min_nan(__low2float(mn), __high2float(mn)));
+  } else {
+    warp_pass<DT, 4>(row, cb, ce, vec, lane, [&](int e0, const float* v) {
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        tmax = max_nan(tmax, v[j]);
+        if (e0 + j < ce) tmin = min_nan(tmin, v[j]);
+      }
+    });
+  }
 }
 
 // PRECISE: table-driven fp64 exp of (z - m)/T.  b = 16*log2e*(z-m)/T,
@@ -418,40 +489,24 @@ resample_kernel(const char* __restrict__ rows, int64_t row_bytes, int Vdef, cons
 
     // ---------------- phase A: max, first argmax, |z| range, thread maxima, NaN check
     float tmax = -INFINITY, tmin = INFINITY;
-    int targ = INT_MAX;
-    bool bad = false;
-    warp_pass<DT, 4>(tv.row, cb, ce, vec, lane, [&](int e0, const float* v) {
-#pragma unroll
-      for (int j = 0; j < 8; ++j) {
-        bad |= (v[j] != v[j]);
-        if (v[j] > tmax) {
-          tmax = v[j];
-          targ = e0 + j;
-        }
-        if (e0 + j < ce) tmin = fminf(tmin, v[j]);
-      }
-    });
+    phase_a<DT>(tv.row, cb, ce, vec, lane, tmax, tmin);
+    const bool bad = (tmax != tmax) || (tmin != tmin);
+    if (bad) tmax = -INFINITY;
     __syncthreads();  // isc reset visible
     {
       float wm = warp_max(tmax);
       float wn = -warp_max(-tmin);
-      int wa = warp_min_int(tmax == wm ? targ : INT_MAX);
       bool wbad = __any_sync(0xffffffffu, bad);
       if (lane == 0) {
         sm.wmax[warp] = wm;
         sm.wmin[warp] = wn;
-        sm.warg[warp] = wa;
         if (wbad) sm.isc[1] = 1;
       }
     }
     __syncthreads();
     float m = -INFINITY, zmin = INFINITY;
-    int amax = INT_MAX;
     for (int w = 0; w < RS_WARPS; ++w) {
-      if (sm.wmax[w] > m) {
-        m = sm.wmax[w];
-        amax = sm.warg[w];
-      }
+      m = fmaxf(m, sm.wmax[w]);
       zmin = fminf(zmin, sm.wmin[w]);
     }
     const uint8_t base_flag = 0;
@@ -460,7 +515,24 @@ resample_kernel(const char* __restrict__ rows, int64_t row_bytes, int Vdef, cons
       if (tid == 0) atomicAdd(&counters[2], 1ull);
       continue;
     }
+    // first argmax (lowest id with z == m), computed lazily: greedy rows need it now
+    auto first_argmax = [&]() -> int {
+      int best = INT_MAX;
+      warp_pass<DT, 2>(tv.row, cb, ce, vec, lane, [&](int e0, const float* v) {
+#pragma unroll
+        for (int j = 0; j < 8; ++j)
+          if (v[j] == m && e0 + j < best) best = e0 + j;
+      });
+      best = warp_min_int(best);
+      __syncthreads();
+      if (lane == 0) sm.warg[warp] = best;
+      __syncthreads();
+      int a = INT_MAX;
+      for (int w = 0; w < RS_WARPS; ++w) a = min(a, sm.warg[w]);
+      return a;
+    };
     if (tv.T == 0.0) {  // greedy: one-hot at the first argmax, still one draw (sampling.py:61-64)
+      const int amax = first_argmax();
       write_all(tv, io, amax, base_flag);
       continue;
     }
@@ -500,34 +572,87 @@ resample_kernel(const char* __restrict__ rows, int64_t row_bytes, int Vdef, cons
     }
 
     // ---------------- phase B: fast mass per warp, candidates
+    // truncated rows only need the mass for the nucleus target (bound via W);
+    // untruncated rows need tight per-element errors for the draw itself
+    const bool accurate = !tv.trunc;
     double S_part = 0.0;
+    float W_part = 0.0f;
     int overflow = 0;
-    warp_pass<DT, 2>(tv.row, cb, ce, vec, lane, [&](int e0, const float* v) {
-      float e[8];
+    auto push_lane = [&](unsigned m8, int e0, const float* v) {
+      const int cnt = __popc(m8);
+      if (__any_sync(0xffffffffu, cnt != 0)) {
+        int incl = cnt;
 #pragma unroll
-      for (int j = 0; j < 8; ++j) e[j] = fast_exp(ec, v[j]);  // ids >= ce are -inf -> 0
-      S_part += (double)(((e[0] + e[1]) + (e[2] + e[3])) + ((e[4] + e[5]) + (e[6] + e[7])));
-      if (kc > 0) {
-        unsigned m8 = 0;
+        for (int o = 1; o < 32; o <<= 1) {
+          const int y = __shfl_up_sync(0xffffffffu, incl, o);
+          if (lane >= o) incl += y;
+        }
+        int base = 0;
+        if (lane == 31) base = atomicAdd(&sm.isc[0], incl);
+        base = __shfl_sync(0xffffffffu, base, 31);
+        int pos = base + incl - cnt;
 #pragma unroll
-        for (int j = 0; j < 8; ++j) m8 |= (unsigned)((e0 + j < ce) && v[j] >= theta) << j;
-        if (__any_sync(0xffffffffu, m8 != 0)) {
-#pragma unroll
-          for (int j = 0; j < 8; ++j) push_cand(sm, (m8 >> j) & 1u, v[j], e0 + j, overflow);
+        for (int j = 0; j < 8; ++j) {
+          if ((m8 >> j) & 1u) {
+            if (pos < CAND_CAP) sm.cand[pos] = cand_key(v[j], e0 + j);
+            else overflow = 1;
+            ++pos;
+          }
         }
       }
-    });
+    };
+    if (accurate) {
+      warp_pass<DT, 2>(tv.row, cb, ce, vec, lane, [&](int e0, const float* v) {
+        float e[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) e[j] = fast_exp(ec, v[j]);  // ids >= ce are -inf -> 0
+        S_part += (double)(((e[0] + e[1]) + (e[2] + e[3])) + ((e[4] + e[5]) + (e[6] + e[7])));
+      });
+    } else {
+      warp_pass<DT, 2>(tv.row, cb, ce, vec, lane, [&](int e0, const float* v) {
+        float e[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          float a;
+          e[j] = cheap_exp(ec, v[j], a);
+          W_part = fmaf(e[j], -a, W_part);
+        }
+        S_part += (double)(((e[0] + e[1]) + (e[2] + e[3])) + ((e[4] + e[5]) + (e[6] + e[7])));
+        if (kc > 0) {
+          unsigned m8 = 0;
+#pragma unroll
+          for (int j = 0; j < 8; ++j) m8 |= (unsigned)((e0 + j < ce) && v[j] >= theta) << j;
+          push_lane(m8, e0, v);
+        }
+      });
+    }
     {
       double wsm = warp_sum(S_part);
+      double wW = warp_sum((double)W_part);
       int wo = __any_sync(0xffffffffu, overflow);
       if (lane == 0) {
         sm.wsum[warp] = wsm;
+        sm.werr[warp] = wW;
         if (wo) sm.isc[2] = 1;
       }
     }
     __syncthreads();
     const int ncand = min(sm.isc[0], CAND_CAP);
     const bool cand_ok = (sm.isc[2] == 0) && kc > 0 && ncand >= kc;
+    double Wrow = 0.0;
+    for (int w = 0; w < RS_WARPS; ++w) Wrow += sm.werr[w];
+    Wrow *= 1.001;  // fp32 accumulation of a bound quantity
+    // first argmax: lowest id among candidates with z == m (the candidates hold every z >= theta <= m)
+    int amax = INT_MAX;
+    if (cand_ok) {
+      int best = INT_MAX;
+      for (int i = tid; i < ncand; i += RS_THREADS)
+        if (cand_z(sm.cand[i]) == m) best = min(best, cand_id(sm.cand[i]));
+      best = warp_min_int(best);
+      if (lane == 0) sm.warg[warp] = best;
+      __syncthreads();
+      for (int w = 0; w < RS_WARPS; ++w) amax = min(amax, sm.warg[w]);
+    }
     __syncthreads();
 
     // per-row state kept across the FAST and PRECISE decision passes
@@ -554,11 +679,12 @@ resample_kernel(const char* __restrict__ rows, int64_t row_bytes, int Vdef, cons
       }
       double S = 0.0;
       for (int w = 0; w < RS_WARPS; ++w) S += sm.wsum[w];
-      const double relE = precise ? (kLiteErr + 2.0 * kRefExpErr + relArg + (double)(V + 16) * kEps64)
-                                  : (kEx2RelErr + kCorrErr + kSum8Err + kRefExpErr + relArg +
-                                     (double)(V + 16) * kEps64);
+      const double relE = precise    ? (kLiteErr + 2.0 * kRefExpErr + relArg + (double)(V + 16) * kEps64)
+                          : accurate ? (kEx2RelErr + kCorrErr + kSum8Err + kRefExpErr + relArg +
+                                        (double)(V + 16) * kEps64)
+                                     : (kEx2Raw + kSum8Err + kRefExpErr + relArg + (double)(V + 16) * kEps64);
       const double absE = precise ? (double)V * 1e-300 : (double)V * 2.4e-38;  // flushed / subnormal mass
-      const double E_S = S * relE + absE;
+      const double E_S = S * relE + absE + ((!precise && !accurate) ? kArgRel * Wrow : 0.0);
       bool unc = false;
 
       // Kept-set representation for the draw:
@@ -573,6 +699,7 @@ resample_kernel(const char* __restrict__ rows, int64_t row_bytes, int Vdef, cons
         // certainly reaches top_p the nucleus is {argmax} and every draw returns it
         const double pmax_lo = (1.0 / (S + E_S)) * (1.0 - relRef);
         if (pmax_lo > tv.topp) {
+          if (amax == INT_MAX) amax = first_argmax();
           write_all(tv, io, amax, tier_flag);
           done = true;
           break;
@@ -662,7 +789,8 @@ resample_kernel(const char* __restrict__ rows, int64_t row_bytes, int Vdef, cons
               for (int j = 0; j < 8; ++j)
                 if (e0 + j < ce) {
                   const int b = nbin(ec, v[j]);
-                  const float q = fast_exp(ec, v[j]) * bin_scale(b) * qscale;
+                  float a;
+                  const float q = cheap_exp(ec, v[j], a) * bin_scale(b) * qscale;
                   atomicAdd(&sm.hist[warp][b], __float2uint_rn(fminf(q, 2.0f * qscale)));
                 }
             });
@@ -670,7 +798,8 @@ resample_kernel(const char* __restrict__ rows, int64_t row_bytes, int Vdef, cons
             if (warp == 0) {
               // bracket [blo, bhi] of bins that can hold the cut (fast mass + quantisation error)
               const double inv = 1.0 / (double)qscale;
-              const double qrel = ldexp(1.0, lgC - 30) * 1.25 + kEx2RelErr * 2.0 + 1e-6;
+              // quantisation + cheap_exp (|a| <= 64 below the catch-all bin) + bin_scale rounding
+              const double qrel = ldexp(1.0, lgC - 30) * 1.25 + kEx2Raw + kArgRel * 64.0 + 1e-7;
               const double qerr = qrel * S + 2.0 * E_S + P * relRef;
               double cum = 0.0;
               int blo = NBINS - 1, bhi = NBINS - 1;
@@ -743,7 +872,7 @@ resample_kernel(const char* __restrict__ rows, int64_t row_bytes, int Vdef, cons
               const int nw = sm.wcount[warp];
               double acc = 0.0;
               for (int i = lane; i < nw; i += 32) {
-                double e = ref_exp(ec, load1<DT>(tv.row, scrA_id[warp * SCR_PER_WARP + i]));
+                double e = lite_exp(ec, load1<DT>(tv.row, scrA_id[warp * SCR_PER_WARP + i]), sm.t16);
                 scrA_e[warp * SCR_PER_WARP + i] = e;
                 acc += e;
               }
@@ -768,7 +897,7 @@ resample_kernel(const char* __restrict__ rows, int64_t row_bytes, int Vdef, cons
           const int nb = min(sm.isc[0], CAND_CAP);
           if (warp == 0) {
             const double Mabove = sm.dsc[1];
-            const double tolS = tv.topp * E_S;
+            const double tolS = tv.topp * E_S + Mabove * (kLiteErr + relArg + 2.0 * kRefExpErr);
             int cut = -1;
             bool u_ = Mabove >= P - tolS - Mabove * relRef;  // the cut would lie above the bracket
             double off = Mabove;
@@ -942,7 +1071,8 @@ resample_kernel(const char* __restrict__ rows, int64_t row_bytes, int Vdef, cons
       const double K = sm.wpre[RS_WARPS];
       // mode 0: per-element relative bound relE on every partial sum (fast or precise e's);
       // mode 2: kept e's are precise
-      const double relD = (mode == 0) ? relE : ((double)(V + 64) * 4.0 * kEps64 + 4.0 * kRefExpErr + 2.0 * relArg);
+      const double relD = (mode == 0) ? relE
+                                      : ((double)(V + 64) * 4.0 * kEps64 + 4.0 * kRefExpErr + 2.0 * relArg + kLiteErr);
       const double absD = (mode == 0) ? absE : 0.0;
       const bool exact_zero_left = precise || mode == 2;  // no flushed mass can precede
       int need = 0;
@@ -1349,10 +1479,14 @@ extern "C" int lc_resample(const void* d_rows, int dtype, int64_t vocab, int64_t
                               workspace_bytes, d_counters, (cudaStream_t)stream);
 }
 
-// Test probe: the FAST tier's exponential, so the GPU tests can measure its
-// error against an fp64 reference and pin kEx2RelErr.
+// Test probe: the exponentials of the FAST / PRECISE tiers, so the GPU tests
+// can measure their error against fp64 and pin kEx2RelErr / kEx2Raw / kLiteErr
+// (DESIGN.md "Certification").  mode 0 fast_exp, 1 cheap_exp, 2 lite_exp.
 namespace lcb {
-__global__ void probe_fast_exp_kernel(const float* z, int64_t n, float m, double T, float* out) {
+__global__ void probe_exp_kernel(const float* z, int64_t n, float m, double T, int mode, double* out) {
+  __shared__ double t16[16];
+  if (threadIdx.x < 16) t16[threadIdx.x] = exp2((double)threadIdx.x / 16.0);
+  __syncthreads();
   int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
   ExpCtx c;
@@ -1364,14 +1498,15 @@ __global__ void probe_fast_exp_kernel(const float* z, int64_t n, float m, double
   c.Llo = (float)(Ld - (double)c.Lhi);
   c.md = (double)m;
   c.L16 = 16.0 * Ld;
-  out[i] = fast_exp(c, z[i]);
+  float a;
+  out[i] = mode == 0 ? (double)fast_exp(c, z[i]) : mode == 1 ? (double)cheap_exp(c, z[i], a) : lite_exp(c, z[i], t16);
 }
 }  // namespace lcb
 
-extern "C" int lc_probe_fast_exp(const float* d_z, int64_t n, float m, double temperature, float* d_out,
-                                 void* stream) {
+extern "C" int lc_probe_exp(const float* d_z, int64_t n, float m, double temperature, int mode, double* d_out,
+                            void* stream) {
   if (n <= 0) return n == 0 ? LC_OK : LC_E_ARG;
-  lcb::probe_fast_exp_kernel<<<lcb::ceil_div(n, 256), 256, 0, (cudaStream_t)stream>>>(d_z, n, m, temperature, d_out);
+  lcb::probe_exp_kernel<<<lcb::ceil_div(n, 256), 256, 0, (cudaStream_t)stream>>>(d_z, n, m, temperature, mode, d_out);
   LCB_CUDA_TRY(cudaGetLastError());
   return LC_OK;
 }

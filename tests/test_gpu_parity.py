@@ -79,23 +79,52 @@ def test_fill_logits_matches_reference_producer():
 # -- fast-tier error model ------------------------------------------------------------------
 
 
-def test_fast_exp_error_bound():
-    """kEx2RelErr (lc_resample.cu) must bound the FAST exponential's relative error."""
-    rng = np.random.default_rng(0)
+def _probe(z, m, T, mode):
+    zt = torch.from_numpy(z).to(DEV)
+    out = torch.empty(z.size, dtype=torch.float64, device=DEV)
+    _capi.check(_capi.lib.lc_probe_exp(zt.data_ptr(), z.size, float(m), T, mode, out.data_ptr(), None))
+    return out.cpu().numpy()
+
+
+@pytest.mark.parametrize("mode,bound", [(0, 4.0e-7), (2, 3.0e-13)])
+def test_exp_error_bounds(mode, bound):
+    """The constants kEx2RelErr (mode 0) and kLiteErr (mode 2) in lc_resample.cu
+    must bound the tiers' exponentials (relative to exp((z-m)/T) in fp64)."""
+    rng = np.random.default_rng(mode)
     worst = 0.0
     for T in (0.01, 0.1, 0.6, 1.0, 1.3, 7.0):
         m = np.float32(rng.normal() * 4)
         z = (m - rng.random(1 << 20) * 60 * T).astype(np.float32)
         z[:1024] = np.nextafter(m, np.float32(-np.inf), dtype=np.float32) - np.arange(1024, dtype=np.float32) * 1e-6
-        zt = torch.from_numpy(z).to(DEV)
-        out = torch.empty_like(zt)
-        _capi.check(_capi.lib.lc_probe_fast_exp(zt.data_ptr(), z.size, float(m), T, out.data_ptr(), None))
-        got = out.cpu().numpy().astype(np.float64)
-        exact = np.exp((z.astype(np.float64) - np.float64(m)) / T)
+        got = _probe(z, m, T, mode)
+        # exact argument in extended precision: (z - m) exact in f64, then / T
+        exact = np.exp((z.astype(np.longdouble) - np.longdouble(m)) / np.longdouble(T)).astype(np.float64)
         ok = exact > 1e-37
-        rel = np.abs(got[ok] - exact[ok]) / exact[ok]
-        worst = max(worst, float(rel.max()))
-    assert worst < 4.0e-7, worst
+        worst = max(worst, float((np.abs(got[ok] - exact[ok]) / exact[ok]).max()))
+    assert worst < bound, worst
+
+
+def test_cheap_exp_error_model():
+    """cheap_exp: |e - exact| <= exact * (kEx2Raw + kArgRel*|a|) (+ flushed subnormals)."""
+    rng = np.random.default_rng(7)
+    kEx2Raw, kArgRel = 2.5e-7, 3.0 * 2.0 ** -24 * np.log(2) * 1.01
+    for T in (0.05, 0.6, 1.0, 3.0):
+        m = np.float32(rng.normal() * 4)
+        z = (m - rng.random(1 << 20) * 80 * T).astype(np.float32)
+        got = _probe(z, m, T, 1)
+        a = (z.astype(np.longdouble) - np.longdouble(m)) / np.longdouble(T) / np.log(np.longdouble(2))
+        exact = np.exp2(a).astype(np.float64)
+        ok = exact > 2e-38
+        bound = exact[ok] * (kEx2Raw + kArgRel * np.abs(a[ok].astype(np.float64)))
+        assert np.all(np.abs(got[ok] - exact[ok]) <= bound)
+
+
+def test_ex2_raw_bound():
+    """ex2.approx alone (a = 0 offset, exact arguments): max relative error < kEx2Raw."""
+    x = np.linspace(-125.0, 0.0, 1 << 22).astype(np.float32)
+    got = _probe(x, np.float32(0.0), 1.0 / np.log(2.0), 1)  # L = 1 exactly -> a = x
+    exact = np.exp2(x.astype(np.float64))
+    assert float((np.abs(got - exact) / exact).max()) < 2.5e-7
 
 
 # -- resample vs golden (reference) ----------------------------------------------------------
