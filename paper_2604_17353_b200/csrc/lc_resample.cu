@@ -460,7 +460,7 @@ __device__ __forceinline__ void write_all(const TaskView& tv, const DrawIO& io, 
 template <int DT>
 __global__ void __launch_bounds__(RS_THREADS, RS_MIN_BLOCKS)
 resample_kernel(const char* __restrict__ rows, int64_t row_bytes, int Vdef, const lc_task* __restrict__ tasks,
-                int n_tasks, CacheMap cm, DrawIO io, Workspace ws, unsigned long long* counters) {
+                int n_tasks, CacheMap cm, DrawIO io, Workspace ws, unsigned long long* counters, int rw_owns) {
   extern __shared__ __align__(16) unsigned char smraw[];
   Smem& sm = *reinterpret_cast<Smem*>(smraw);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -473,6 +473,10 @@ resample_kernel(const char* __restrict__ rows, int64_t row_bytes, int Vdef, cons
   for (int task_id = blockIdx.x; task_id < n_tasks; task_id += gridDim.x) {
     const lc_task tk = tasks[task_id];
     if (tk.draw_end <= tk.draw_begin) continue;  // nothing to draw (uniform across the CTA)
+    if (rw_owns) {  // the row-per-warp kernel takes tasks without an effective top-k
+      const int Vt = tk.vocab > 0 ? tk.vocab : Vdef;
+      if (!(tk.top_k > 0 && tk.top_k < Vt)) continue;
+    }
     TaskView tv;
     __syncthreads();  // previous task's smem readers are done
     if (!resolve_task(tk, rows, row_bytes, Vdef, cm, tv)) {
@@ -1224,6 +1228,563 @@ resample_kernel(const char* __restrict__ rows, int64_t row_bytes, int Vdef, cons
   }
 }
 
+// ============================== row-per-warp kernel ==============================
+//
+// The headline regime (BASELINE configs 1 and 2): many rows, V <= 65536, no
+// top-k.  One warp owns one task at a time -- no block barriers, per-warp
+// shared state, 24 warps per SM.  Lane l reads the 8-element vectors
+// l, l+32, ... so a warp instruction covers 256 consecutive ids; the row is
+// cut into 2048-id segments whose masses give the inverse-CDF search a prefix
+// table (a draw rescans one segment).
+//
+// Nucleus without top-k: the first argmax alone (fast exit), or a "big"
+// nucleus located by a per-warp fixed-point histogram (8 bins per octave of
+// distance from the max), whose bracket bins are sorted exactly; the kept mass
+// above the bracket is accumulated per segment in the same pass, so no kept
+// list is materialised -- a draw rescans its segment with the kept predicate.
+// Tasks with an effective top-k are left to the CTA kernel.
+
+constexpr int RW_THREADS = 256;
+constexpr int RW_WARPS = RW_THREADS / 32;
+constexpr int RW_MIN_BLOCKS = 2;
+constexpr int RW_CAND = 256;      // bracket candidates per warp
+constexpr int RW_NB = 256;        // histogram bins: 8 per octave over 32 octaves (+ catch-all)
+constexpr float RW_BPO = 8.0f;
+constexpr int RW_SEGSTEPS = 8;    // 8 x 256 ids = 2048 per segment
+constexpr int RW_SEG = 256 * RW_SEGSTEPS;
+constexpr int RW_MAXV = 65536;
+constexpr int RW_NSEG = RW_MAXV / RW_SEG;  // 32
+
+struct __align__(16) RwWarp {
+  unsigned long long cand[RW_CAND];
+  double ce[RW_CAND];
+  uint32_t hist[RW_NB];
+  double seg[RW_NSEG + 1];  // segment masses, then exclusive prefix
+  double dsc[4];
+  int isc[4];
+};
+
+struct __align__(16) RwSmem {
+  RwWarp w[RW_WARPS];
+  double t16[16];
+  float f8[8];  // 2^(j/8)
+};
+
+__device__ __forceinline__ int rw_bin(const ExpCtx& c, float a) {
+  // a = log2 distance below the max (<= 0)
+  return min((int)(-a * RW_BPO), RW_NB - 1);
+}
+
+// 2^(b/8) as fp32 (relative error <= 2^-24)
+__device__ __forceinline__ float rw_scale(int b, const float* f8) {
+  return __int_as_float(((b >> 3) + 127) << 23) * f8[b & 7];
+}
+
+// e-function variants: 0 CHEAP (truncated rows), 1 ACCURATE (untruncated), 2 PRECISE (lite)
+template <int EM>
+__device__ __forceinline__ double rw_e(const ExpCtx& ec, float z, const double* t16, float& aw) {
+  if (EM == 2) {
+    aw = 0.0f;
+    return lite_exp(ec, z, t16);
+  } else if (EM == 1) {
+    aw = 0.0f;
+    return (double)fast_exp(ec, z);
+  } else {
+    float a;
+    const float e = cheap_exp(ec, z, a);
+    aw = -a * e;
+    return (double)e;
+  }
+}
+
+__device__ __forceinline__ bool rw_keep(const ExpCtx& ec, float z, int id, int blo, int bhi,
+                                        unsigned long long kcut) {
+  const float a = fmaxf((z - ec.m) * ec.Lhi, -200.0f);
+  const int b = rw_bin(ec, a);
+  return b < blo || (b <= bhi && cand_key(z, id) >= kcut);
+}
+
+// One pass over the row; seg[s] = sum of e over the segment's ids (passing the
+// kept predicate when KEEP); returns the |a|-weighted W (CHEAP only).  FAST
+// variants sum 8 values in fp32 pairs then in fp64 (matched by the rescan).
+template <int DT, int EM, bool KEEP>
+__device__ double rw_seg_pass(const char* row, int V, int nseg, bool vec, int lane, const ExpCtx& ec,
+                              const double* t16, double* seg, int blo, int bhi, unsigned long long kcut) {
+  float Wl = 0.0f;
+  for (int s = 0; s < nseg; ++s) {
+    double acc = 0.0;
+    const int s0 = s * RW_SEG;
+#pragma unroll 2
+    for (int st = 0; st < RW_SEGSTEPS; ++st) {
+      const int e0 = s0 + 256 * st + 8 * lane;
+      float v[8];
+      load8<DT>(row, e0, V, vec, v);
+      double e8 = 0.0;
+      float ef[8];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        float aw;
+        double e = rw_e<EM>(ec, v[j], t16, aw);
+        if (KEEP && !rw_keep(ec, v[j], e0 + j, blo, bhi, kcut)) {
+          e = 0.0;
+          aw = 0.0f;
+        }
+        if (EM == 2) e8 += e;
+        else ef[j] = (float)e;
+        Wl += aw;
+      }
+      if (EM != 2) e8 = (double)(((ef[0] + ef[1]) + (ef[2] + ef[3])) + ((ef[4] + ef[5]) + (ef[6] + ef[7])));
+      acc += e8;
+    }
+    acc = warp_sum(acc);
+    if (lane == 0) seg[s] = acc;
+  }
+  __syncwarp();
+  return warp_sum((double)Wl) * 1.001;
+}
+
+template <int DT>
+__global__ void __launch_bounds__(RW_THREADS, RW_MIN_BLOCKS)
+rowwarp_kernel(const char* __restrict__ rows, int64_t row_bytes, int Vdef, const lc_task* __restrict__ tasks,
+               int n_tasks, CacheMap cm, DrawIO io, int* q_exact, unsigned long long* counters) {
+  __shared__ RwSmem smem;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  RwWarp& sw = smem.w[wid];
+  if (threadIdx.x < 16) smem.t16[threadIdx.x] = exp2((double)threadIdx.x / 16.0);
+  if (threadIdx.x < 8) smem.f8[threadIdx.x] = exp2f((float)threadIdx.x / 8.0f);
+  if (lane == 0) sw.isc[0] = 0;
+  __syncthreads();
+  const int gw = blockIdx.x * RW_WARPS + wid, nw = gridDim.x * RW_WARPS;
+
+  for (int task_id = gw; task_id < n_tasks; task_id += nw) {
+    const lc_task tk = tasks[task_id];
+    if (tk.draw_end <= tk.draw_begin) continue;
+    const int Vt = tk.vocab > 0 ? tk.vocab : Vdef;
+    if (tk.top_k > 0 && tk.top_k < Vt) continue;  // top-k: CTA kernel
+    TaskView tv;
+    if (!resolve_task(tk, rows, row_bytes, Vdef, cm, tv)) {
+      for (int64_t d = tv.d0 + lane; d < tv.d1; d += 32) {
+        io.token[d] = -1;
+        if (io.flags) io.flags[d] = LC_DRAW_BAD_ROW;
+      }
+      if (lane == 0) atomicAdd(&counters[2], 1ull);
+      continue;
+    }
+    const int V = tv.V;
+    const bool vec = ((reinterpret_cast<uintptr_t>(tv.row) & 15) == 0);
+    const int nseg = (V + RW_SEG - 1) / RW_SEG;
+    auto write_all_w = [&](int tok, uint8_t flag) {
+      for (int64_t d = tv.d0 + lane; d < tv.d1; d += 32) {
+        io.token[d] = tok;
+        if (io.flags) io.flags[d] = flag;
+      }
+    };
+
+    // ---------------- phase A (packed max / min / NaN)
+    float tmax = -INFINITY, tmin = INFINITY;
+    phase_a<DT>(tv.row, 0, V, vec, lane, tmax, tmin);
+    const bool bad = __any_sync(0xffffffffu, (tmax != tmax) || (tmin != tmin));
+    if (bad) tmax = -INFINITY;
+    const float m = warp_max(tmax);
+    const float zmin = -warp_max(-tmin);
+    if (bad || !(m > -INFINITY) || !(m < INFINITY)) {
+      write_all_w(-1, LC_DRAW_BAD_ROW);
+      if (lane == 0) atomicAdd(&counters[2], 1ull);
+      continue;
+    }
+    // first argmax: lanes holding m scan their own vectors
+    auto first_argmax = [&]() -> int {
+      int best = INT_MAX;
+      if (tmax == m) {
+        for (int e0 = 8 * lane; e0 < V && best == INT_MAX; e0 += 256) {
+          float v[8];
+          load8<DT>(tv.row, e0, V, vec, v);
+#pragma unroll
+          for (int j = 0; j < 8; ++j)
+            if (v[j] == m && e0 + j < best) best = e0 + j;
+        }
+      }
+      return warp_min_int(best);
+    };
+    if (tv.T == 0.0) {
+      const int a = first_argmax();
+      write_all_w(a, 0);
+      continue;
+    }
+    ExpCtx ec;
+    ec.m = m;
+    ec.T = tv.T;
+    ec.mT = __ddiv_rn((double)m, tv.T);
+    ec.md = (double)m;
+    {
+      const double Ld = 1.4426950408889634 / tv.T;
+      ec.Lhi = (float)Ld;
+      ec.Llo = (float)(Ld - (double)ec.Lhi);
+      ec.L16 = 16.0 * Ld;
+    }
+    const double zabs = fmax(fabs((double)m), isfinite(zmin) ? fabs((double)zmin) : fabs((double)m));
+    const bool sane = ec.Lhi < 1e20f && ec.Lhi > 1e-20f && fabsf(m) * ec.Lhi < 1e30f && zabs / tv.T < 1e15;
+    const double relArg = 4.440892098500626e-16 * 2.0 * zabs / tv.T;
+    const double relRef = (double)(2 * V + 64) * kEps64;
+    const bool accurate = !tv.trunc;  // untruncated: the draw itself needs tight per-element errors
+
+    // ---------------- phase B: segment masses (+ |a|-weighted bound for the cheap exp)
+    auto seg_pass = [&](bool precise, bool keep, int blo_, int bhi_, unsigned long long kcut_) -> double {
+      if (precise) {
+        return keep ? rw_seg_pass<DT, 2, true>(tv.row, V, nseg, vec, lane, ec, smem.t16, sw.seg, blo_, bhi_, kcut_)
+                    : rw_seg_pass<DT, 2, false>(tv.row, V, nseg, vec, lane, ec, smem.t16, sw.seg, 0, 0, 0ull);
+      }
+      if (accurate) return rw_seg_pass<DT, 1, false>(tv.row, V, nseg, vec, lane, ec, smem.t16, sw.seg, 0, 0, 0ull);
+      return keep ? rw_seg_pass<DT, 0, true>(tv.row, V, nseg, vec, lane, ec, smem.t16, sw.seg, blo_, bhi_, kcut_)
+                  : rw_seg_pass<DT, 0, false>(tv.row, V, nseg, vec, lane, ec, smem.t16, sw.seg, 0, 0, 0ull);
+    };
+
+    const double Wrow = seg_pass(false, false, 0, 0, 0ull);
+    bool done = false, to_exact = !sane;
+    int big_state = 0;  // 0 not built, 1 built, -1 failed
+    int blo = 0, bhi = 0, nb = 0;
+    double Mab = 0.0, Wab = 0.0;  // FAST kept mass above the bracket and its W
+
+    for (int pass = 0; pass < 2 && !done && !to_exact; ++pass) {
+      const bool precise = pass == 1;
+      const uint8_t tier_flag = precise ? LC_DRAW_PRECISE : 0;
+      if (precise) {
+        if (lane == 0) atomicAdd(&counters[0], 1ull);
+        seg_pass(true, false, 0, 0, 0ull);
+      }
+      double S = 0.0;
+      for (int s = 0; s < nseg; ++s) S += sw.seg[s];
+      const double relE = precise    ? (kLiteErr + 2.0 * kRefExpErr + relArg + (double)(V + 16) * kEps64)
+                          : accurate ? (kEx2RelErr + kCorrErr + kSum8Err + kRefExpErr + relArg +
+                                        (double)(V + 16) * kEps64)
+                                     : (kEx2Raw + kSum8Err + kRefExpErr + relArg + (double)(V + 16) * kEps64);
+      const double absE = precise ? (double)V * 1e-300 : (double)V * 2.4e-38;
+      const double E_S = S * relE + absE + ((!precise && !accurate) ? kArgRel * Wrow : 0.0);
+
+      // kept set: all ids (big == false), or bins < blo plus the first L bracket keys
+      bool big = false;
+      unsigned long long kcut = 0ull;
+      double Kmass = S, EK = E_S;  // mass of the kept set and its error bound
+      if (tv.trunc && tv.topp < 1.0) {
+        const double pmax_lo = (1.0 / (S + E_S)) * (1.0 - relRef);
+        if (pmax_lo > tv.topp) {  // nucleus = {first argmax}
+          write_all_w(first_argmax(), tier_flag);
+          done = true;
+          break;
+        }
+        const double P = tv.topp * S;
+        if (big_state == 0) {
+          // histogram: per-bin relative fixed point (bin b holds e in (2^-(b+1)/8, 2^-b/8])
+          for (int i = lane; i < RW_NB; i += 32) sw.hist[i] = 0u;
+          __syncwarp();
+          const int lgV = 32 - __clz(V + 1);
+          const float qscale = ldexpf(1.0f, 31 - lgV);
+          for (int e0 = 8 * lane; e0 < V; e0 += 256) {
+            float v[8];
+            load8<DT>(tv.row, e0, V, vec, v);
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+              float a;
+              const float e = cheap_exp(ec, v[j], a);
+              const int b = rw_bin(ec, a);
+              if (e > 0.0f) atomicAdd(&sw.hist[b], __float2uint_rn(fminf(e * rw_scale(b, smem.f8), 1.0f) * qscale));
+            }
+          }
+          __syncwarp();
+          // bracket of bins that can hold the cut
+          const double inv = 1.0 / (double)qscale;
+          const double qrel = ldexp(1.0, lgV - 31) * 1.2 + kEx2Raw + kArgRel * 33.0 + 1e-7;
+          const double qerr = qrel * S + 2.0 * E_S + P * relRef;
+          double cum = 0.0;
+          blo = RW_NB - 1;
+          bhi = RW_NB - 1;
+          bool got_lo = false;
+          for (int b0 = 0; b0 < RW_NB; b0 += 32) {
+            const double hb = (double)sw.hist[b0 + lane] * inv * exp2(-(double)(b0 + lane) / 8.0);
+            const double incl = cum + warp_incl_scan(hb);
+            const unsigned lo_m = __ballot_sync(0xffffffffu, incl >= P - qerr);
+            const unsigned hi_m = __ballot_sync(0xffffffffu, incl >= P + qerr);
+            if (!got_lo && lo_m) {
+              blo = b0 + __ffs(lo_m) - 1;
+              got_lo = true;
+            }
+            if (hi_m) {
+              bhi = b0 + __ffs(hi_m) - 1;
+              break;
+            }
+            cum = __shfl_sync(0xffffffffu, incl, 31);
+          }
+          if (bhi >= RW_NB - 1) {  // the cut may lie in the catch-all bin
+            big_state = -1;
+          } else {
+            // bracket members -> candidate list; FAST mass of bins < blo (+ its W)
+            int ovf = 0;
+            double M = 0.0;
+            float Wl = 0.0f;
+            for (int e0 = 8 * lane; e0 < V; e0 += 256) {
+              float v[8];
+              load8<DT>(tv.row, e0, V, vec, v);
+              float ms = 0.0f;
+              unsigned m8 = 0;
+#pragma unroll
+              for (int j = 0; j < 8; ++j) {
+                float a;
+                const float e = cheap_exp(ec, v[j], a);
+                const int b = rw_bin(ec, a);
+                if (b < blo) {
+                  ms += e;
+                  Wl = fmaf(e, -a, Wl);
+                } else if (b <= bhi && e0 + j < V) {
+                  m8 |= 1u << j;
+                }
+              }
+              M += (double)ms;
+              if (m8) {
+                const int pos = atomicAdd(&sw.isc[0], __popc(m8));
+                int p = pos;
+#pragma unroll
+                for (int j = 0; j < 8; ++j)
+                  if ((m8 >> j) & 1u) {
+                    if (p < RW_CAND) sw.cand[p] = cand_key(v[j], e0 + j);
+                    else ovf = 1;
+                    ++p;
+                  }
+              }
+            }
+            Mab = warp_sum(M);
+            Wab = warp_sum((double)Wl) * 1.001;
+            __syncwarp();
+            nb = sw.isc[0];
+            if (__any_sync(0xffffffffu, ovf) || nb > RW_CAND) {
+              big_state = -1;
+            } else {
+              // rank sort (z desc, id asc) through ce[] as key scratch, then precise e
+              unsigned long long* tmpk = reinterpret_cast<unsigned long long*>(sw.ce);
+              for (int i = lane; i < nb; i += 32) {
+                const unsigned long long kk = sw.cand[i];
+                int rank = 0;
+                for (int j = 0; j < nb; ++j) rank += (sw.cand[j] > kk);
+                tmpk[rank] = kk;
+              }
+              __syncwarp();
+              for (int i = lane; i < nb; i += 32) sw.cand[i] = tmpk[i];
+              __syncwarp();
+              for (int i = lane; i < nb; i += 32) sw.ce[i] = ref_exp(ec, cand_z(sw.cand[i]));
+              __syncwarp();
+              big_state = 1;
+            }
+          }
+          if (lane == 0) sw.isc[0] = 0;
+          __syncwarp();
+        }
+        if (big_state < 0) {
+          to_exact = true;
+          if (lane == 0) atomicAdd(&counters[7], 1ull);
+          break;
+        }
+        // cut inside the bracket: csum from the mass above it
+        double Mabove = Mab, EMab = Mab * relE + kArgRel * Wab + absE;
+        if (precise) {
+          // PRECISE mass above the bracket (lite_exp); reuse seg[] as scratch afterwards
+          double acc = 0.0;
+          for (int e0 = 8 * lane; e0 < V; e0 += 256) {
+            float v[8];
+            load8<DT>(tv.row, e0, V, vec, v);
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+              const float a = fmaxf((v[j] - ec.m) * ec.Lhi, -200.0f);
+              if (rw_bin(ec, a) < blo) acc += lite_exp(ec, v[j], smem.t16);
+            }
+          }
+          Mabove = warp_sum(acc);
+          EMab = Mabove * relE + absE;
+        }
+        int cut = -1;
+        bool unc = Mabove >= P - tv.topp * E_S - EMab;  // the cut would lie above the bracket
+        double off = Mabove;
+        for (int i0 = 0; i0 < nb && !unc; i0 += 32) {
+          const int i = i0 + lane;
+          const double e = i < nb ? sw.ce[i] : 0.0;
+          const double c = off + warp_incl_scan(e), prev = c - e;
+          const double tol = tv.topp * E_S + EMab + c * relRef;
+          const unsigned hm = __ballot_sync(0xffffffffu, i < nb && c >= P - tol);
+          if (hm) {
+            const int hl = __ffs(hm) - 1;
+            cut = i0 + hl;
+            const bool ok = (c - P > tol && P - prev > tol);
+            unc = !__shfl_sync(0xffffffffu, ok, hl);
+            break;
+          }
+          off = __shfl_sync(0xffffffffu, c, 31);
+        }
+        if (cut < 0) unc = true;
+        if (!unc) {
+          bool bad_order = false;
+          for (int i = max(cut, 1) + lane; i <= min(cut + 1, nb - 1); i += 32) {
+            const float za = cand_z(sw.cand[i - 1]), zb = cand_z(sw.cand[i]);
+            if (za != zb) {
+              const double da = __ddiv_rn((double)za, tv.T), db = __ddiv_rn((double)zb, tv.T);
+              if (da - db <= fmax(fabs(da), fabs(ec.mT)) * 8.0 * kEps64) bad_order = true;
+            }
+          }
+          unc = __any_sync(0xffffffffu, bad_order);
+        }
+        if (unc) {
+          if (lane == 0 && !precise) atomicAdd(&counters[4], 1ull);
+          continue;
+        }
+        big = true;
+        kcut = sw.cand[cut];
+        // kept mass per segment: e over the kept predicate, with this pass's e-function
+        const double wk = seg_pass(precise, true, blo, bhi, kcut);
+        Kmass = 0.0;
+        for (int s = 0; s < nseg; ++s) Kmass += sw.seg[s];
+        EK = Kmass * relE + absE + ((!precise && !accurate) ? kArgRel * wk : 0.0);
+      }
+
+      // ---------------- draws: segment prefix, then one rescan per segment holding targets
+      if (lane == 0) {
+        double c = 0.0;
+        for (int s = 0; s < nseg; ++s) {
+          const double x = sw.seg[s];
+          sw.seg[s] = c;
+          c += x;
+        }
+        sw.seg[nseg] = c;
+      }
+      __syncwarp();
+      const double K = sw.seg[nseg];
+      // D-bound: err(u*K - A) <= relE * ((1-u)*A + u*(K-A)) + (absolute part of EK)
+      const double relD = relE;
+      int need = 0;
+      for (int64_t dbase = tv.d0; dbase < tv.d1; dbase += 32) {
+        const int64_t d = dbase + lane;
+        double t = INFINITY, u = 0.0;
+        if (d < tv.d1) {
+          u = draw_u(io, d, tv);
+          t = u * K;
+          if (!(t < K)) need = 1;  // clamp region -> EXACT
+        }
+        // targets sorted ascending (warp bitonic on (t, lane))
+        double st = (d < tv.d1 && t < K) ? t : INFINITY;
+        int ssrc = lane;
+#pragma unroll
+        for (int k2 = 2; k2 <= 32; k2 <<= 1) {
+#pragma unroll
+          for (int j2 = k2 >> 1; j2 > 0; j2 >>= 1) {
+            const double ot = __shfl_xor_sync(0xffffffffu, st, j2);
+            const int os = __shfl_xor_sync(0xffffffffu, ssrc, j2);
+            const bool asc = (lane & k2) == 0 || k2 == 32;
+            const bool lower = (lane & j2) == 0;
+            const bool take = (lower == asc) ? (ot < st || (ot == st && os < ssrc)) : (ot > st || (ot == st && os > ssrc));
+            if (take) {
+              st = ot;
+              ssrc = os;
+            }
+          }
+        }
+        const double su = __shfl_sync(0xffffffffu, u, ssrc);
+        const int ntar = __popc(__ballot_sync(0xffffffffu, st < INFINITY));
+        int k = 0;
+        while (k < ntar) {
+          const double tk0 = __shfl_sync(0xffffffffu, st, k);
+          // segment of target k
+          int s = 0;
+          while (s + 1 < nseg && sw.seg[s + 1] <= tk0) ++s;
+          double off = sw.seg[s];
+          const double send = sw.seg[s + 1];
+          // rescan segment s for every target below its end
+          for (int stp = 0; stp < RW_SEGSTEPS && k < ntar; ++stp) {
+            const int my0 = s * RW_SEG + 256 * stp + 8 * lane;
+            float v[8];
+            load8<DT>(tv.row, my0, V, vec, v);
+            double ev[8];
+            double ls = 0.0;
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+              float aw;
+              double e = precise ? rw_e<2>(ec, v[j], smem.t16, aw)
+                                 : (accurate ? rw_e<1>(ec, v[j], smem.t16, aw) : rw_e<0>(ec, v[j], smem.t16, aw));
+              if (big && !rw_keep(ec, v[j], my0 + j, blo, bhi, kcut)) e = 0.0;
+              ev[j] = e;
+            }
+            if (!precise) {
+              // the FAST segment sums used the fp32 pair-sum association: match it
+              float f[8];
+#pragma unroll
+              for (int j = 0; j < 8; ++j) f[j] = (float)ev[j];
+              ls = (double)(((f[0] + f[1]) + (f[2] + f[3])) + ((f[4] + f[5]) + (f[6] + f[7])));
+            } else {
+#pragma unroll
+              for (int j = 0; j < 8; ++j) ls += ev[j];
+            }
+            const double x = warp_incl_scan(ls);
+            const double tot = __shfl_sync(0xffffffffu, x, 31);
+            while (k < ntar) {
+              const double tk = __shfl_sync(0xffffffffu, st, k);
+              if (!(tk < off + tot) && !(stp == RW_SEGSTEPS - 1 && tk < send)) break;
+              const unsigned hm = __ballot_sync(0xffffffffu, (ls > 0.0) && (tk < off + x));
+              int found = -1;
+              double flo = 0.0, fhi = 0.0;
+              if (hm) {
+                const int hl = __ffs(hm) - 1;
+                if (lane == hl) {
+                  double c = off + (x - ls);
+                  for (int j = 0; j < 8; ++j) {
+                    const double nc = c + ev[j];
+                    if (ev[j] > 0.0 && tk < nc) {
+                      found = my0 + j;
+                      flo = c;
+                      fhi = nc;
+                      break;
+                    }
+                    c = nc;
+                  }
+                }
+                found = __shfl_sync(0xffffffffu, found, hl);
+                flo = __shfl_sync(0xffffffffu, flo, hl);
+                fhi = __shfl_sync(0xffffffffu, fhi, hl);
+              }
+              const double uu = __shfl_sync(0xffffffffu, su, k);
+              const int src = __shfl_sync(0xffffffffu, ssrc, k);
+              if (lane == 0) {
+                const double tlo = relD * ((1.0 - uu) * flo + uu * (K - flo)) + (EK - relD * Kmass) + tk * relRef * 4.0;
+                const double thi = relD * ((1.0 - uu) * fhi + uu * (K - fhi)) + (EK - relD * Kmass) + tk * relRef * 4.0;
+                const bool ok = found >= 0 && (tk - flo > tlo || (precise && flo == 0.0)) && (fhi - tk > thi);
+                io.token[dbase + src] = found;
+                if (io.flags) io.flags[dbase + src] = tier_flag;
+                need |= !ok;
+              }
+              ++k;
+            }
+            off += tot;
+          }
+          // targets left past the segment's end by rounding: uncertain
+          while (k < ntar && __shfl_sync(0xffffffffu, st, k) < send) {
+            const int src = __shfl_sync(0xffffffffu, ssrc, k);
+            if (lane == 0) {
+              io.token[dbase + src] = -1;
+              need = 1;
+            }
+            ++k;
+          }
+        }
+      }
+      need = __any_sync(0xffffffffu, need);
+      if (!need) {
+        done = true;
+      } else if (lane == 0 && !precise) {
+        atomicAdd(&counters[5], 1ull);
+      }
+    }
+    if (!done && lane == 0) {
+      const int pos = atomicAdd(q_exact, 1);
+      q_exact[1 + pos] = task_id;
+      atomicAdd(&counters[3], 1ull);
+    }
+  }
+}
+
 // ============================== EXACT kernel ==============================
 // numpy emulation (pairwise_seq in lc_numpy.cuh).
 
@@ -1437,8 +1998,17 @@ static int launch_all(const char* rows, int64_t row_bytes, int V, const lc_task*
     LCB_CUDA_TRY(cudaFuncSetAttribute(resample_kernel<DT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     attr_set[DT] = true;
   }
+  const int rw = V <= RW_MAXV;
+  if (rw) {
+    const int grw = num_sms() * RW_MIN_BLOCKS;
+    const int64_t need = (n_tasks + RW_WARPS - 1) / RW_WARPS;
+    rowwarp_kernel<DT><<<(int)(need < grw ? need : grw), RW_THREADS, 0, st>>>(rows, row_bytes, V, tasks, (int)n_tasks,
+                                                                            cm, io, ws.q_exact, counters);
+    LCB_CUDA_TRY(cudaGetLastError());
+  }
   const int g1 = (int)(n_tasks < grid ? n_tasks : grid);
-  resample_kernel<DT><<<g1, RS_THREADS, smem, st>>>(rows, row_bytes, V, tasks, (int)n_tasks, cm, io, ws, counters);
+  resample_kernel<DT><<<g1, RS_THREADS, smem, st>>>(rows, row_bytes, V, tasks, (int)n_tasks, cm, io, ws, counters,
+                                                    rw);
   LCB_CUDA_TRY(cudaGetLastError());
   exact_kernel<DT><<<kExactCtas, EX_THREADS, 0, st>>>(rows, row_bytes, V, tasks, ws.q_exact, cm, io, ex_scr, ex_iscr,
                                                       scr_stride, counters);
