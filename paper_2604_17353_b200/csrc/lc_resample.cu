@@ -169,17 +169,17 @@ __device__ __forceinline__ void phase_a(const char* row, int cb, int ce, bool ve
   if (DT == LC_BF16 && vec) {
     const uint16_t* r = reinterpret_cast<const uint16_t*>(row);
     __nv_bfloat162 mx = __float2bfloat162_rn(-INFINITY), mn = __float2bfloat162_rn(INFINITY);
-    for (int base = cb; base < ce; base += 256 * 4) {
-      uint4 q[4];
-      bool full[4];
+    for (int base = cb; base < ce; base += 256 * 8) {
+      uint4 q[8];
+      bool full[8];
 #pragma unroll
-      for (int u = 0; u < 4; ++u) {
+      for (int u = 0; u < 8; ++u) {
         const int e0 = base + 256 * u + 8 * lane;
         full[u] = e0 + 8 <= ce;
         if (full[u]) q[u] = __ldg(reinterpret_cast<const uint4*>(r + e0));
       }
 #pragma unroll
-      for (int u = 0; u < 4; ++u) {
+      for (int u = 0; u < 8; ++u) {
         const int e0 = base + 256 * u + 8 * lane;
         if (full[u]) {
           const uint32_t w[4] = {q[u].x, q[u].y, q[u].z, q[u].w};
@@ -1247,7 +1247,7 @@ resample_kernel(const char* __restrict__ rows, int64_t row_bytes, int Vdef, cons
 constexpr int RW_THREADS = 256;
 constexpr int RW_WARPS = RW_THREADS / 32;
 constexpr int RW_MIN_BLOCKS = 2;
-constexpr int RW_CAND = 256;      // bracket candidates per warp
+constexpr int RW_CAND = 512;      // bracket candidates per warp
 constexpr int RW_NB = 256;        // histogram bins: 8 per octave over 32 octaves (+ catch-all)
 constexpr float RW_BPO = 8.0f;
 constexpr int RW_SEGSTEPS = 8;    // 8 x 256 ids = 2048 per segment
@@ -1314,7 +1314,7 @@ __device__ double rw_seg_pass(const char* row, int V, int nseg, bool vec, int la
   for (int s = 0; s < nseg; ++s) {
     double acc = 0.0;
     const int s0 = s * RW_SEG;
-#pragma unroll 2
+#pragma unroll 4
     for (int st = 0; st < RW_SEGSTEPS; ++st) {
       const int e0 = s0 + 256 * st + 8 * lane;
       float v[8];
@@ -1343,20 +1343,37 @@ __device__ double rw_seg_pass(const char* row, int V, int nseg, bool vec, int la
   return warp_sum((double)Wl) * 1.001;
 }
 
+struct RwScratch {
+  int* id;     // [warps][cap] kept-list ids (id order); bit 31 = bracket member
+  float* z;    // [warps][cap]
+  double* e;   // [warps][cap] fp64-lite e
+  int cap;
+  int* next;   // dynamic task counter
+};
+
 template <int DT>
 __global__ void __launch_bounds__(RW_THREADS, RW_MIN_BLOCKS)
 rowwarp_kernel(const char* __restrict__ rows, int64_t row_bytes, int Vdef, const lc_task* __restrict__ tasks,
-               int n_tasks, CacheMap cm, DrawIO io, int* q_exact, unsigned long long* counters) {
-  __shared__ RwSmem smem;
+               int n_tasks, CacheMap cm, DrawIO io, int* q_exact, unsigned long long* counters, RwScratch scr) {
+  extern __shared__ __align__(16) unsigned char rw_smraw[];
+  RwSmem& smem = *reinterpret_cast<RwSmem*>(rw_smraw);
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   RwWarp& sw = smem.w[wid];
   if (threadIdx.x < 16) smem.t16[threadIdx.x] = exp2((double)threadIdx.x / 16.0);
   if (threadIdx.x < 8) smem.f8[threadIdx.x] = exp2f((float)threadIdx.x / 8.0f);
   if (lane == 0) sw.isc[0] = 0;
   __syncthreads();
-  const int gw = blockIdx.x * RW_WARPS + wid, nw = gridDim.x * RW_WARPS;
+  const int gw = blockIdx.x * RW_WARPS + wid;
+  int* L_id = scr.id + (int64_t)gw * scr.cap;
+  float* L_z = scr.z + (int64_t)gw * scr.cap;
+  double* L_e = scr.e + (int64_t)gw * scr.cap;
 
-  for (int task_id = gw; task_id < n_tasks; task_id += nw) {
+  for (;;) {
+    // dynamic scheduling: tasks differ wildly in cost (fast exit vs big nucleus)
+    int task_id = 0;
+    if (lane == 0) task_id = atomicAdd(scr.next, 1);
+    task_id = __shfl_sync(0xffffffffu, task_id, 0);
+    if (task_id >= n_tasks) break;
     const lc_task tk = tasks[task_id];
     if (tk.draw_end <= tk.draw_begin) continue;
     const int Vt = tk.vocab > 0 ? tk.vocab : Vdef;
@@ -1427,44 +1444,39 @@ rowwarp_kernel(const char* __restrict__ rows, int64_t row_bytes, int Vdef, const
     const double relArg = 4.440892098500626e-16 * 2.0 * zabs / tv.T;
     const double relRef = (double)(2 * V + 64) * kEps64;
     const bool accurate = !tv.trunc;  // untruncated: the draw itself needs tight per-element errors
+    // relative bound of the fp64-lite e's (kept lists, PRECISE pass) vs the reference's e's
+    const double relLite = kLiteErr + 2.0 * kRefExpErr + relArg + (double)(V + 16) * kEps64;
 
     // ---------------- phase B: segment masses (+ |a|-weighted bound for the cheap exp)
-    auto seg_pass = [&](bool precise, bool keep, int blo_, int bhi_, unsigned long long kcut_) -> double {
-      if (precise) {
-        return keep ? rw_seg_pass<DT, 2, true>(tv.row, V, nseg, vec, lane, ec, smem.t16, sw.seg, blo_, bhi_, kcut_)
-                    : rw_seg_pass<DT, 2, false>(tv.row, V, nseg, vec, lane, ec, smem.t16, sw.seg, 0, 0, 0ull);
-      }
+    auto seg_pass = [&](bool precise) -> double {
+      if (precise) return rw_seg_pass<DT, 2, false>(tv.row, V, nseg, vec, lane, ec, smem.t16, sw.seg, 0, 0, 0ull);
       if (accurate) return rw_seg_pass<DT, 1, false>(tv.row, V, nseg, vec, lane, ec, smem.t16, sw.seg, 0, 0, 0ull);
-      return keep ? rw_seg_pass<DT, 0, true>(tv.row, V, nseg, vec, lane, ec, smem.t16, sw.seg, blo_, bhi_, kcut_)
-                  : rw_seg_pass<DT, 0, false>(tv.row, V, nseg, vec, lane, ec, smem.t16, sw.seg, 0, 0, 0ull);
+      return rw_seg_pass<DT, 0, false>(tv.row, V, nseg, vec, lane, ec, smem.t16, sw.seg, 0, 0, 0ull);
     };
-
-    const double Wrow = seg_pass(false, false, 0, 0, 0ull);
+    const double Wrow = seg_pass(false);
     bool done = false, to_exact = !sane;
     int big_state = 0;  // 0 not built, 1 built, -1 failed
-    int blo = 0, bhi = 0, nb = 0;
-    double Mab = 0.0, Wab = 0.0;  // FAST kept mass above the bracket and its W
+    int blo = 0, bhi = 0, nb = 0, nl = 0;
+    double Mab = 0.0;  // fp64-lite mass of the list entries above the bracket
 
     for (int pass = 0; pass < 2 && !done && !to_exact; ++pass) {
       const bool precise = pass == 1;
       const uint8_t tier_flag = precise ? LC_DRAW_PRECISE : 0;
       if (precise) {
         if (lane == 0) atomicAdd(&counters[0], 1ull);
-        seg_pass(true, false, 0, 0, 0ull);
+        seg_pass(true);
       }
       double S = 0.0;
       for (int s = 0; s < nseg; ++s) S += sw.seg[s];
-      const double relE = precise    ? (kLiteErr + 2.0 * kRefExpErr + relArg + (double)(V + 16) * kEps64)
+      const double relE = precise    ? relLite
                           : accurate ? (kEx2RelErr + kCorrErr + kSum8Err + kRefExpErr + relArg +
                                         (double)(V + 16) * kEps64)
                                      : (kEx2Raw + kSum8Err + kRefExpErr + relArg + (double)(V + 16) * kEps64);
       const double absE = precise ? (double)V * 1e-300 : (double)V * 2.4e-38;
       const double E_S = S * relE + absE + ((!precise && !accurate) ? kArgRel * Wrow : 0.0);
 
-      // kept set: all ids (big == false), or bins < blo plus the first L bracket keys
       bool big = false;
       unsigned long long kcut = 0ull;
-      double Kmass = S, EK = E_S;  // mass of the kept set and its error bound
       if (tv.trunc && tv.topp < 1.0) {
         const double pmax_lo = (1.0 / (S + E_S)) * (1.0 - relRef);
         if (pmax_lo > tv.topp) {  // nucleus = {first argmax}
@@ -1479,16 +1491,20 @@ rowwarp_kernel(const char* __restrict__ rows, int64_t row_bytes, int Vdef, const
           __syncwarp();
           const int lgV = 32 - __clz(V + 1);
           const float qscale = ldexpf(1.0f, 31 - lgV);
-          for (int e0 = 8 * lane; e0 < V; e0 += 256) {
-            float v[8];
-            load8<DT>(tv.row, e0, V, vec, v);
+          for (int base = 0; base < V; base += 512) {
+            float v[2][8];
+            load8<DT>(tv.row, base + 8 * lane, V, vec, v[0]);
+            load8<DT>(tv.row, base + 256 + 8 * lane, V, vec, v[1]);
 #pragma unroll
-            for (int j = 0; j < 8; ++j) {
-              float a;
-              const float e = cheap_exp(ec, v[j], a);
-              const int b = rw_bin(ec, a);
-              if (e > 0.0f) atomicAdd(&sw.hist[b], __float2uint_rn(fminf(e * rw_scale(b, smem.f8), 1.0f) * qscale));
-            }
+            for (int u2 = 0; u2 < 2; ++u2)
+#pragma unroll
+              for (int j = 0; j < 8; ++j) {
+                float a;
+                const float e = cheap_exp(ec, v[u2][j], a);
+                const int b = rw_bin(ec, a);
+                if (e > 0.0f)
+                  atomicAdd(&sw.hist[b], __float2uint_rn(fminf(e * rw_scale(b, smem.f8), 1.0f) * qscale));
+              }
           }
           __syncwarp();
           // bracket of bins that can hold the cut
@@ -1514,51 +1530,71 @@ rowwarp_kernel(const char* __restrict__ rows, int64_t row_bytes, int Vdef, const
             }
             cum = __shfl_sync(0xffffffffu, incl, 31);
           }
-          if (bhi >= RW_NB - 1) {  // the cut may lie in the catch-all bin
-            big_state = -1;
-          } else {
-            // bracket members -> candidate list; FAST mass of bins < blo (+ its W)
-            int ovf = 0;
-            double M = 0.0;
-            float Wl = 0.0f;
-            for (int e0 = 8 * lane; e0 < V; e0 += 256) {
+          big_state = (bhi >= RW_NB - 1) ? -1 : 1;  // a cut in the catch-all bin -> EXACT
+          if (big_state > 0) {
+            // kept list: ids with bin <= bhi in id order (bracket members flagged); bracket
+            // keys also go to the smem candidate list for the exact sort
+            int wn = 0, ovf = 0;
+            for (int base = 0; base < V; base += 256) {
+              const int e0 = base + 8 * lane;
               float v[8];
               load8<DT>(tv.row, e0, V, vec, v);
-              float ms = 0.0f;
-              unsigned m8 = 0;
+              unsigned lm = 0, bm = 0;
 #pragma unroll
               for (int j = 0; j < 8; ++j) {
-                float a;
-                const float e = cheap_exp(ec, v[j], a);
+                const float a = fmaxf((v[j] - ec.m) * ec.Lhi, -200.0f);
                 const int b = rw_bin(ec, a);
-                if (b < blo) {
-                  ms += e;
-                  Wl = fmaf(e, -a, Wl);
-                } else if (b <= bhi && e0 + j < V) {
-                  m8 |= 1u << j;
+                if (b <= bhi && e0 + j < V) {
+                  lm |= 1u << j;
+                  if (b >= blo) bm |= 1u << j;
                 }
               }
-              M += (double)ms;
-              if (m8) {
-                const int pos = atomicAdd(&sw.isc[0], __popc(m8));
-                int p = pos;
+              const int c = __popc(lm);
+              int incl = c;
+#pragma unroll
+              for (int o = 1; o < 32; o <<= 1) {
+                const int y = __shfl_up_sync(0xffffffffu, incl, o);
+                if (lane >= o) incl += y;
+              }
+              int pos = wn + incl - c;
+#pragma unroll
+              for (int j = 0; j < 8; ++j)
+                if ((lm >> j) & 1u) {
+                  if (pos < scr.cap) {
+                    L_id[pos] = (e0 + j) | (((bm >> j) & 1u) ? 0x80000000 : 0);
+                    L_z[pos] = v[j];
+                  } else {
+                    ovf = 1;
+                  }
+                  ++pos;
+                }
+              wn += __shfl_sync(0xffffffffu, incl, 31);
+              if (bm) {
+                int p2 = atomicAdd(&sw.isc[0], __popc(bm));
 #pragma unroll
                 for (int j = 0; j < 8; ++j)
-                  if ((m8 >> j) & 1u) {
-                    if (p < RW_CAND) sw.cand[p] = cand_key(v[j], e0 + j);
+                  if ((bm >> j) & 1u) {
+                    if (p2 < RW_CAND) sw.cand[p2] = cand_key(v[j], e0 + j);
                     else ovf = 1;
-                    ++p;
+                    ++p2;
                   }
               }
             }
-            Mab = warp_sum(M);
-            Wab = warp_sum((double)Wl) * 1.001;
             __syncwarp();
             nb = sw.isc[0];
-            if (__any_sync(0xffffffffu, ovf) || nb > RW_CAND) {
+            nl = wn;
+            if (__any_sync(0xffffffffu, ovf) || nb > RW_CAND || nl > scr.cap) {
               big_state = -1;
             } else {
-              // rank sort (z desc, id asc) through ce[] as key scratch, then precise e
+              // fp64-lite e of the list (dense); mass above the bracket
+              double acc = 0.0;
+              for (int i = lane; i < nl; i += 32) {
+                const double e = lite_exp(ec, L_z[i], smem.t16);
+                L_e[i] = e;
+                if (L_id[i] >= 0) acc += e;
+              }
+              Mab = warp_sum(acc);
+              // rank sort of the bracket keys (z desc, id asc) through ce[] as scratch
               unsigned long long* tmpk = reinterpret_cast<unsigned long long*>(sw.ce);
               for (int i = lane; i < nb; i += 32) {
                 const unsigned long long kk = sw.cand[i];
@@ -1570,10 +1606,9 @@ rowwarp_kernel(const char* __restrict__ rows, int64_t row_bytes, int Vdef, const
               for (int i = lane; i < nb; i += 32) sw.cand[i] = tmpk[i];
               __syncwarp();
               for (int i = lane; i < nb; i += 32) sw.ce[i] = ref_exp(ec, cand_z(sw.cand[i]));
-              __syncwarp();
-              big_state = 1;
             }
           }
+          __syncwarp();
           if (lane == 0) sw.isc[0] = 0;
           __syncwarp();
         }
@@ -1582,26 +1617,11 @@ rowwarp_kernel(const char* __restrict__ rows, int64_t row_bytes, int Vdef, const
           if (lane == 0) atomicAdd(&counters[7], 1ull);
           break;
         }
-        // cut inside the bracket: csum from the mass above it
-        double Mabove = Mab, EMab = Mab * relE + kArgRel * Wab + absE;
-        if (precise) {
-          // PRECISE mass above the bracket (lite_exp); reuse seg[] as scratch afterwards
-          double acc = 0.0;
-          for (int e0 = 8 * lane; e0 < V; e0 += 256) {
-            float v[8];
-            load8<DT>(tv.row, e0, V, vec, v);
-#pragma unroll
-            for (int j = 0; j < 8; ++j) {
-              const float a = fmaxf((v[j] - ec.m) * ec.Lhi, -200.0f);
-              if (rw_bin(ec, a) < blo) acc += lite_exp(ec, v[j], smem.t16);
-            }
-          }
-          Mabove = warp_sum(acc);
-          EMab = Mabove * relE + absE;
-        }
+        // cut inside the bracket: csum (precise e's) from the mass above it
+        const double EMab = Mab * relLite;
         int cut = -1;
-        bool unc = Mabove >= P - tv.topp * E_S - EMab;  // the cut would lie above the bracket
-        double off = Mabove;
+        bool unc = Mab >= P - tv.topp * E_S - EMab;  // the cut would lie above the bracket
+        double off = Mab;
         for (int i0 = 0; i0 < nb && !unc; i0 += 32) {
           const int i = i0 + lane;
           const double e = i < nb ? sw.ce[i] : 0.0;
@@ -1635,122 +1655,75 @@ rowwarp_kernel(const char* __restrict__ rows, int64_t row_bytes, int Vdef, const
         }
         big = true;
         kcut = sw.cand[cut];
-        // kept mass per segment: e over the kept predicate, with this pass's e-function
-        const double wk = seg_pass(precise, true, blo, bhi, kcut);
-        Kmass = 0.0;
-        for (int s = 0; s < nseg; ++s) Kmass += sw.seg[s];
-        EK = Kmass * relE + absE + ((!precise && !accurate) ? kArgRel * wk : 0.0);
       }
 
-      // ---------------- draws: segment prefix, then one rescan per segment holding targets
-      if (lane == 0) {
-        double c = 0.0;
-        for (int s = 0; s < nseg; ++s) {
-          const double x = sw.seg[s];
-          sw.seg[s] = c;
-          c += x;
-        }
-        sw.seg[nseg] = c;
-      }
-      __syncwarp();
-      const double K = sw.seg[nseg];
-      // D-bound: err(u*K - A) <= relE * ((1-u)*A + u*(K-A)) + (absolute part of EK)
-      const double relD = relE;
       int need = 0;
-      for (int64_t dbase = tv.d0; dbase < tv.d1; dbase += 32) {
-        const int64_t d = dbase + lane;
-        double t = INFINITY, u = 0.0;
-        if (d < tv.d1) {
-          u = draw_u(io, d, tv);
-          t = u * K;
-          if (!(t < K)) need = 1;  // clamp region -> EXACT
-        }
-        // targets sorted ascending (warp bitonic on (t, lane))
-        double st = (d < tv.d1 && t < K) ? t : INFINITY;
-        int ssrc = lane;
+      if (big) {
+        // ---------------- draws over the kept list (precise e's, id order)
+        auto kept_e = [&](int i) -> double {
+          const int idf = L_id[i];
+          if (idf >= 0) return L_e[i];
+          return cand_key(L_z[i], idf & 0x7fffffff) >= kcut ? L_e[i] : 0.0;
+        };
+        double kacc = 0.0;
+        for (int i = lane; i < nl; i += 32) kacc += kept_e(i);
+        const double K = warp_sum(kacc);
+        const double relD = relLite + (double)(nl + 64) * 4.0 * kEps64;
+        for (int64_t dbase = tv.d0; dbase < tv.d1; dbase += 32) {
+          const int64_t d = dbase + lane;
+          double t = INFINITY, u = 0.0;
+          if (d < tv.d1) {
+            u = draw_u(io, d, tv);
+            t = u * K;
+            if (!(t < K)) need = 1;
+          }
+          double st = (d < tv.d1 && t < K) ? t : INFINITY;
+          int ssrc = lane;
 #pragma unroll
-        for (int k2 = 2; k2 <= 32; k2 <<= 1) {
+          for (int k2 = 2; k2 <= 32; k2 <<= 1) {
 #pragma unroll
-          for (int j2 = k2 >> 1; j2 > 0; j2 >>= 1) {
-            const double ot = __shfl_xor_sync(0xffffffffu, st, j2);
-            const int os = __shfl_xor_sync(0xffffffffu, ssrc, j2);
-            const bool asc = (lane & k2) == 0 || k2 == 32;
-            const bool lower = (lane & j2) == 0;
-            const bool take = (lower == asc) ? (ot < st || (ot == st && os < ssrc)) : (ot > st || (ot == st && os > ssrc));
-            if (take) {
-              st = ot;
-              ssrc = os;
+            for (int j2 = k2 >> 1; j2 > 0; j2 >>= 1) {
+              const double ot = __shfl_xor_sync(0xffffffffu, st, j2);
+              const int os = __shfl_xor_sync(0xffffffffu, ssrc, j2);
+              const bool asc = (lane & k2) == 0 || k2 == 32;
+              const bool lower = (lane & j2) == 0;
+              const bool take =
+                  (lower == asc) ? (ot < st || (ot == st && os < ssrc)) : (ot > st || (ot == st && os > ssrc));
+              if (take) {
+                st = ot;
+                ssrc = os;
+              }
             }
           }
-        }
-        const double su = __shfl_sync(0xffffffffu, u, ssrc);
-        const int ntar = __popc(__ballot_sync(0xffffffffu, st < INFINITY));
-        int k = 0;
-        while (k < ntar) {
-          const double tk0 = __shfl_sync(0xffffffffu, st, k);
-          // segment of target k
-          int s = 0;
-          while (s + 1 < nseg && sw.seg[s + 1] <= tk0) ++s;
-          double off = sw.seg[s];
-          const double send = sw.seg[s + 1];
-          // rescan segment s for every target below its end
-          for (int stp = 0; stp < RW_SEGSTEPS && k < ntar; ++stp) {
-            const int my0 = s * RW_SEG + 256 * stp + 8 * lane;
-            float v[8];
-            load8<DT>(tv.row, my0, V, vec, v);
-            double ev[8];
-            double ls = 0.0;
-#pragma unroll
-            for (int j = 0; j < 8; ++j) {
-              float aw;
-              double e = precise ? rw_e<2>(ec, v[j], smem.t16, aw)
-                                 : (accurate ? rw_e<1>(ec, v[j], smem.t16, aw) : rw_e<0>(ec, v[j], smem.t16, aw));
-              if (big && !rw_keep(ec, v[j], my0 + j, blo, bhi, kcut)) e = 0.0;
-              ev[j] = e;
-            }
-            if (!precise) {
-              // the FAST segment sums used the fp32 pair-sum association: match it
-              float f[8];
-#pragma unroll
-              for (int j = 0; j < 8; ++j) f[j] = (float)ev[j];
-              ls = (double)(((f[0] + f[1]) + (f[2] + f[3])) + ((f[4] + f[5]) + (f[6] + f[7])));
-            } else {
-#pragma unroll
-              for (int j = 0; j < 8; ++j) ls += ev[j];
-            }
-            const double x = warp_incl_scan(ls);
+          const double su = __shfl_sync(0xffffffffu, u, ssrc);
+          const int ntar = __popc(__ballot_sync(0xffffffffu, st < INFINITY));
+          int k = 0;
+          double off = 0.0;
+          for (int i0 = 0; i0 < nl && k < ntar; i0 += 32) {
+            const int i = i0 + lane;
+            const double e = i < nl ? kept_e(i) : 0.0;
+            const int id = i < nl ? (L_id[i] & 0x7fffffff) : -1;
+            const double x = warp_incl_scan(e);
             const double tot = __shfl_sync(0xffffffffu, x, 31);
             while (k < ntar) {
               const double tk = __shfl_sync(0xffffffffu, st, k);
-              if (!(tk < off + tot) && !(stp == RW_SEGSTEPS - 1 && tk < send)) break;
-              const unsigned hm = __ballot_sync(0xffffffffu, (ls > 0.0) && (tk < off + x));
+              if (!(tk < off + tot)) break;
+              const unsigned hm = __ballot_sync(0xffffffffu, (e > 0.0) && (tk < off + x));
               int found = -1;
               double flo = 0.0, fhi = 0.0;
               if (hm) {
                 const int hl = __ffs(hm) - 1;
-                if (lane == hl) {
-                  double c = off + (x - ls);
-                  for (int j = 0; j < 8; ++j) {
-                    const double nc = c + ev[j];
-                    if (ev[j] > 0.0 && tk < nc) {
-                      found = my0 + j;
-                      flo = c;
-                      fhi = nc;
-                      break;
-                    }
-                    c = nc;
-                  }
-                }
-                found = __shfl_sync(0xffffffffu, found, hl);
-                flo = __shfl_sync(0xffffffffu, flo, hl);
-                fhi = __shfl_sync(0xffffffffu, fhi, hl);
+                found = __shfl_sync(0xffffffffu, id, hl);
+                flo = __shfl_sync(0xffffffffu, off + x - e, hl);
+                fhi = __shfl_sync(0xffffffffu, off + x, hl);
               }
               const double uu = __shfl_sync(0xffffffffu, su, k);
               const int src = __shfl_sync(0xffffffffu, ssrc, k);
               if (lane == 0) {
-                const double tlo = relD * ((1.0 - uu) * flo + uu * (K - flo)) + (EK - relD * Kmass) + tk * relRef * 4.0;
-                const double thi = relD * ((1.0 - uu) * fhi + uu * (K - fhi)) + (EK - relD * Kmass) + tk * relRef * 4.0;
-                const bool ok = found >= 0 && (tk - flo > tlo || (precise && flo == 0.0)) && (fhi - tk > thi);
+                const double tlo = relD * ((1.0 - uu) * flo + uu * (K - flo)) + tk * relRef * 4.0;
+                const double thi = relD * ((1.0 - uu) * fhi + uu * (K - fhi)) + tk * relRef * 4.0;
+                // nothing kept precedes flo == 0: the lower boundary is exact
+                const bool ok = found >= 0 && (tk - flo > tlo || flo == 0.0) && (fhi - tk > thi);
                 io.token[dbase + src] = found;
                 if (io.flags) io.flags[dbase + src] = tier_flag;
                 need |= !ok;
@@ -1759,14 +1732,135 @@ rowwarp_kernel(const char* __restrict__ rows, int64_t row_bytes, int Vdef, const
             }
             off += tot;
           }
-          // targets left past the segment's end by rounding: uncertain
-          while (k < ntar && __shfl_sync(0xffffffffu, st, k) < send) {
+          while (k < ntar) {  // rounding left a target past the list end
             const int src = __shfl_sync(0xffffffffu, ssrc, k);
             if (lane == 0) {
               io.token[dbase + src] = -1;
               need = 1;
             }
             ++k;
+          }
+        }
+      } else {
+        // ---------------- draws over all ids: segment prefix, one rescan per segment
+        if (lane == 0) {
+          double c = 0.0;
+          for (int s = 0; s < nseg; ++s) {
+            const double x = sw.seg[s];
+            sw.seg[s] = c;
+            c += x;
+          }
+          sw.seg[nseg] = c;
+        }
+        __syncwarp();
+        const double K = sw.seg[nseg];
+        const double absD = E_S - relE * S;  // absolute part of the bound (flushed mass, W term)
+        for (int64_t dbase = tv.d0; dbase < tv.d1; dbase += 32) {
+          const int64_t d = dbase + lane;
+          double t = INFINITY, u = 0.0;
+          if (d < tv.d1) {
+            u = draw_u(io, d, tv);
+            t = u * K;
+            if (!(t < K)) need = 1;  // clamp region -> EXACT
+          }
+          double st = (d < tv.d1 && t < K) ? t : INFINITY;
+          int ssrc = lane;
+#pragma unroll
+          for (int k2 = 2; k2 <= 32; k2 <<= 1) {
+#pragma unroll
+            for (int j2 = k2 >> 1; j2 > 0; j2 >>= 1) {
+              const double ot = __shfl_xor_sync(0xffffffffu, st, j2);
+              const int os = __shfl_xor_sync(0xffffffffu, ssrc, j2);
+              const bool asc = (lane & k2) == 0 || k2 == 32;
+              const bool lower = (lane & j2) == 0;
+              const bool take =
+                  (lower == asc) ? (ot < st || (ot == st && os < ssrc)) : (ot > st || (ot == st && os > ssrc));
+              if (take) {
+                st = ot;
+                ssrc = os;
+              }
+            }
+          }
+          const double su = __shfl_sync(0xffffffffu, u, ssrc);
+          const int ntar = __popc(__ballot_sync(0xffffffffu, st < INFINITY));
+          int k = 0;
+          while (k < ntar) {
+            const double tk0 = __shfl_sync(0xffffffffu, st, k);
+            int s = 0;
+            while (s + 1 < nseg && sw.seg[s + 1] <= tk0) ++s;
+            double off = sw.seg[s];
+            const double send = sw.seg[s + 1];
+            for (int stp = 0; stp < RW_SEGSTEPS && k < ntar; ++stp) {
+              const int my0 = s * RW_SEG + 256 * stp + 8 * lane;
+              float v[8];
+              load8<DT>(tv.row, my0, V, vec, v);
+              double ev[8];
+              double ls;
+#pragma unroll
+              for (int j = 0; j < 8; ++j) {
+                float aw;
+                ev[j] = precise ? rw_e<2>(ec, v[j], smem.t16, aw)
+                                : (accurate ? rw_e<1>(ec, v[j], smem.t16, aw) : rw_e<0>(ec, v[j], smem.t16, aw));
+              }
+              if (!precise) {  // the FAST segment sums used the fp32 pair-sum association
+                float f[8];
+#pragma unroll
+                for (int j = 0; j < 8; ++j) f[j] = (float)ev[j];
+                ls = (double)(((f[0] + f[1]) + (f[2] + f[3])) + ((f[4] + f[5]) + (f[6] + f[7])));
+              } else {
+                ls = 0.0;
+#pragma unroll
+                for (int j = 0; j < 8; ++j) ls += ev[j];
+              }
+              const double x = warp_incl_scan(ls);
+              const double tot = __shfl_sync(0xffffffffu, x, 31);
+              while (k < ntar) {
+                const double tk = __shfl_sync(0xffffffffu, st, k);
+                if (!(tk < off + tot) && !(stp == RW_SEGSTEPS - 1 && tk < send)) break;
+                const unsigned hm = __ballot_sync(0xffffffffu, (ls > 0.0) && (tk < off + x));
+                int found = -1;
+                double flo = 0.0, fhi = 0.0;
+                if (hm) {
+                  const int hl = __ffs(hm) - 1;
+                  if (lane == hl) {
+                    double c = off + (x - ls);
+                    for (int j = 0; j < 8; ++j) {
+                      const double nc = c + ev[j];
+                      if (ev[j] > 0.0 && tk < nc) {
+                        found = my0 + j;
+                        flo = c;
+                        fhi = nc;
+                        break;
+                      }
+                      c = nc;
+                    }
+                  }
+                  found = __shfl_sync(0xffffffffu, found, hl);
+                  flo = __shfl_sync(0xffffffffu, flo, hl);
+                  fhi = __shfl_sync(0xffffffffu, fhi, hl);
+                }
+                const double uu = __shfl_sync(0xffffffffu, su, k);
+                const int src = __shfl_sync(0xffffffffu, ssrc, k);
+                if (lane == 0) {
+                  const double tlo = relE * ((1.0 - uu) * flo + uu * (K - flo)) + absD + tk * relRef * 4.0;
+                  const double thi = relE * ((1.0 - uu) * fhi + uu * (K - fhi)) + absD + tk * relRef * 4.0;
+                  const bool ok = found >= 0 && (tk - flo > tlo || (precise && flo == 0.0)) && (fhi - tk > thi);
+                  io.token[dbase + src] = found;
+                  if (io.flags) io.flags[dbase + src] = tier_flag;
+                  need |= !ok;
+                }
+                ++k;
+              }
+              off += tot;
+            }
+            while (k < ntar && __shfl_sync(0xffffffffu, st, k) < send) {
+              const int src = __shfl_sync(0xffffffffu, ssrc, k);
+              if (lane == 0) {
+                io.token[dbase + src] = -1;
+                need = 1;
+              }
+              ++k;
+            }
           }
         }
       }
@@ -1953,9 +2047,14 @@ constexpr int kExactCtas = 32;
 
 static int grid_ctas() { return num_sms() * RS_MIN_BLOCKS; }
 
+static int rw_cap(int64_t V) { return (int)((V / 5 + 256 + 31) & ~31ll); }
+
 int64_t workspace_bytes(int64_t n_tasks, int64_t vocab) {
   const int64_t grid = grid_ctas();
   int64_t b = 0;
+  const int64_t rw_warps = (int64_t)num_sms() * RW_MIN_BLOCKS * RW_WARPS;
+  b += ((rw_warps * rw_cap(vocab) * 16) + 3 * 255) & ~255ll;
+  b += 512;
   b += ((n_tasks + 1) * 4 + 255) & ~255ll;
   b += ((grid * 2 * SCR_PER_CTA * 4) + 255) & ~255ll;
   b += ((grid * 2 * SCR_PER_CTA * 8) + 255) & ~255ll;
@@ -1984,6 +2083,13 @@ static int launch_all(const char* rows, int64_t row_bytes, int V, const lc_task*
   double* ex_scr = (double*)take(kExactCtas * scr_stride * 3 * 8);
   int32_t* ex_iscr = (int32_t*)take(kExactCtas * scr_stride * 4);
   unsigned long long* cnt = (unsigned long long*)take(64);
+  RwScratch rs;
+  rs.cap = rw_cap(V);
+  const int64_t rw_warps = (int64_t)num_sms() * RW_MIN_BLOCKS * RW_WARPS;
+  rs.id = (int*)take(rw_warps * rs.cap * 4);
+  rs.z = (float*)take(rw_warps * rs.cap * 4);
+  rs.e = (double*)take(rw_warps * rs.cap * 8);
+  int* rw_next = (int*)take(256);
   if (!d_ws || p - (char*)d_ws > ws_bytes) {
     lcb_set_last_error("resample workspace too small (see lc_resample_workspace_bytes)", __FILE__, __LINE__);
     return LC_E_ARG;
@@ -2002,8 +2108,17 @@ static int launch_all(const char* rows, int64_t row_bytes, int V, const lc_task*
   if (rw) {
     const int grw = num_sms() * RW_MIN_BLOCKS;
     const int64_t need = (n_tasks + RW_WARPS - 1) / RW_WARPS;
-    rowwarp_kernel<DT><<<(int)(need < grw ? need : grw), RW_THREADS, 0, st>>>(rows, row_bytes, V, tasks, (int)n_tasks,
-                                                                            cm, io, ws.q_exact, counters);
+    const int g = (int)(need < grw ? need : grw);
+    rs.next = rw_next;
+    LCB_CUDA_TRY(cudaMemsetAsync(rw_next, 0, 4, st));
+    static bool rw_attr[2] = {false, false};
+    if (!rw_attr[DT]) {
+      LCB_CUDA_TRY(cudaFuncSetAttribute(rowwarp_kernel<DT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        (int)sizeof(RwSmem)));
+      rw_attr[DT] = true;
+    }
+    rowwarp_kernel<DT><<<g, RW_THREADS, sizeof(RwSmem), st>>>(rows, row_bytes, V, tasks, (int)n_tasks, cm, io,
+                                                             ws.q_exact, counters, rs);
     LCB_CUDA_TRY(cudaGetLastError());
   }
   const int g1 = (int)(n_tasks < grid ? n_tasks : grid);
