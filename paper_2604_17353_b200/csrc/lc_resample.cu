@@ -1883,6 +1883,7 @@ rowwarp_kernel(const char* __restrict__ rows, int64_t row_bytes, int Vdef, const
 // numpy emulation (pairwise_seq in lc_numpy.cuh).
 
 constexpr int EX_THREADS = 256;
+constexpr int EX_CAND = 8192;  // exact-tier candidate set in shared memory (96 KB, dynamic)
 
 template <int DT>
 __global__ void __launch_bounds__(EX_THREADS)
@@ -1900,6 +1901,9 @@ exact_kernel(const char* __restrict__ rows, int64_t row_bytes, int Vdef, const l
   __shared__ double s_bp[EX_THREADS];
   __shared__ int s_bi[EX_THREADS];
   __shared__ int s_stop;
+  extern __shared__ __align__(16) unsigned char ex_dyn[];
+  unsigned long long* s_key = reinterpret_cast<unsigned long long*>(ex_dyn);
+  int* s_id = reinterpret_cast<int*>(ex_dyn + EX_CAND * 8);
   const int tid = threadIdx.x;
   for (int ti = blockIdx.x; ti < ntask; ti += gridDim.x) {
     const int task_id = task_list[1 + ti];
@@ -1931,50 +1935,151 @@ exact_kernel(const char* __restrict__ rows, int64_t row_bytes, int Vdef, const l
     __syncthreads();
     int L = V;
     if (tv.trunc) {
-      // kept prefix of the (p desc, id asc) order, one element per block-wide argmax
+      // kept prefix of the (p desc, id asc) order.  A threshold theta on p (bisection
+      // over its bit pattern, block-parallel counts/masses) selects a candidate set
+      // C = {p >= theta} that surely holds the prefix (>= k elements for top-k,
+      // mass >= top_p + 1e-9 for top-p); C is sorted exactly in shared memory and
+      // the sequential csum of the reference runs over it.
       const int lim = tv.topk > 0 ? tv.topk : V;
-      double last_p = INFINITY;
-      int last_id = -1;
-      double c = 0.0;
-      int n = 0;
-      if (tid == 0) s_stop = 0;
-      __syncthreads();
-      while (n < lim) {
-        double bp = -1.0;
-        int bi = INT_MAX;
+      unsigned long long lo = 0ull, hi = 0x3ff0000000000001ull;  // theta in [0, 1] as bits
+      for (int it = 0; it < 64 && lo + 1 < hi; ++it) {
+        const unsigned long long mid = lo + (hi - lo) / 2;
+        const double th = __longlong_as_double((long long)mid);
+        double mass = 0.0;
+        int cnt = 0;
         for (int i = tid; i < V; i += EX_THREADS) {
-          double pi = p[i];
-          bool after = (pi < last_p) || (pi == last_p && i > last_id);
-          if (after && (pi > bp || (pi == bp && i < bi))) {
-            bp = pi;
-            bi = i;
+          const double pi = p[i];
+          if (pi >= th) {
+            mass += pi;
+            ++cnt;
           }
         }
-        s_bp[tid] = bp;
-        s_bi[tid] = bi;
+        s_bp[tid] = mass;
+        s_bi[tid] = cnt;
         __syncthreads();
-        for (int s = EX_THREADS / 2; s > 0; s >>= 1) {
-          if (tid < s) {
-            double op = s_bp[tid + s];
-            int oi = s_bi[tid + s];
-            if (op > s_bp[tid] || (op == s_bp[tid] && oi < s_bi[tid])) {
-              s_bp[tid] = op;
-              s_bi[tid] = oi;
-            }
+        for (int st2 = EX_THREADS / 2; st2 > 0; st2 >>= 1) {
+          if (tid < st2) {
+            s_bp[tid] += s_bp[tid + st2];
+            s_bi[tid] += s_bi[tid + st2];
           }
           __syncthreads();
         }
-        bp = s_bp[0];
-        bi = s_bi[0];
+        const bool enough = tv.topk > 0 ? (s_bi[0] >= lim) : (s_bp[0] >= tv.topp + 1e-9);
         __syncthreads();
-        if (bi == INT_MAX) break;
-        if (tid == 0) ord[n] = bi;
-        ++n;
-        last_p = bp;
-        last_id = bi;
-        if (tv.topp < 1.0) {
-          c += bp;  // sequential cumsum in sorted order (all threads track it identically)
-          if (c >= tv.topp) break;
+        if (enough) lo = mid;
+        else hi = mid;
+      }
+      const double theta = __longlong_as_double((long long)lo);
+      // compact C (block-wide exclusive scan of per-thread counts), keys into smem
+      int mycnt = 0;
+      for (int i = tid; i < V; i += EX_THREADS) mycnt += (p[i] >= theta);
+      s_bi[tid] = mycnt;
+      __syncthreads();
+      if (tid == 0) {
+        int c0 = 0;
+        for (int i = 0; i < EX_THREADS; ++i) {
+          const int x = s_bi[i];
+          s_bi[i] = c0;
+          c0 += x;
+        }
+        s_stop = c0;
+      }
+      __syncthreads();
+      const int nc = s_stop;
+      int n = 0;
+      if (nc <= EX_CAND) {
+        int pos = s_bi[tid];
+        for (int i = tid; i < V; i += EX_THREADS)
+          if (p[i] >= theta) {
+            s_key[pos] = (unsigned long long)__double_as_longlong(p[i]);
+            s_id[pos] = i;
+            ++pos;
+          }
+        int n2 = 1;
+        while (n2 < nc) n2 <<= 1;
+        for (int i = nc + tid; i < n2; i += EX_THREADS) {
+          s_key[i] = 0ull;
+          s_id[i] = INT_MAX;
+        }
+        __syncthreads();
+        // bitonic sort: p descending, id ascending
+        for (int k2 = 2; k2 <= n2; k2 <<= 1)
+          for (int j2 = k2 >> 1; j2 > 0; j2 >>= 1) {
+            for (int i = tid; i < n2; i += EX_THREADS) {
+              const int pp = i ^ j2;
+              if (pp > i) {
+                const bool first_before = (s_key[i] > s_key[pp]) || (s_key[i] == s_key[pp] && s_id[i] < s_id[pp]);
+                const bool desc = (i & k2) == 0;
+                if (desc ? !first_before : first_before) {
+                  const unsigned long long tk2 = s_key[i];
+                  s_key[i] = s_key[pp];
+                  s_key[pp] = tk2;
+                  const int ti2 = s_id[i];
+                  s_id[i] = s_id[pp];
+                  s_id[pp] = ti2;
+                }
+              }
+            }
+            __syncthreads();
+          }
+        if (tid == 0) {
+          double c = 0.0;
+          int m2 = 0;
+          const int lim2 = min(lim, nc);
+          while (m2 < lim2) {
+            ord[m2] = s_id[m2];
+            ++m2;
+            if (tv.topp < 1.0) {
+              c += __longlong_as_double((long long)s_key[m2 - 1]);  // sequential csum (sampling.py:86)
+              if (c >= tv.topp) break;
+            }
+          }
+          s_L = m2;
+        }
+        __syncthreads();
+        n = s_L;
+      } else {
+        // candidate set too large for shared memory: one block-wide argmax per element
+        double last_p = INFINITY;
+        int last_id = -1;
+        double c = 0.0;
+        while (n < lim) {
+          double bp = -1.0;
+          int bi = INT_MAX;
+          for (int i = tid; i < V; i += EX_THREADS) {
+            double pi = p[i];
+            bool after = (pi < last_p) || (pi == last_p && i > last_id);
+            if (after && (pi > bp || (pi == bp && i < bi))) {
+              bp = pi;
+              bi = i;
+            }
+          }
+          s_bp[tid] = bp;
+          s_bi[tid] = bi;
+          __syncthreads();
+          for (int st2 = EX_THREADS / 2; st2 > 0; st2 >>= 1) {
+            if (tid < st2) {
+              double op = s_bp[tid + st2];
+              int oi = s_bi[tid + st2];
+              if (op > s_bp[tid] || (op == s_bp[tid] && oi < s_bi[tid])) {
+                s_bp[tid] = op;
+                s_bi[tid] = oi;
+              }
+            }
+            __syncthreads();
+          }
+          bp = s_bp[0];
+          bi = s_bi[0];
+          __syncthreads();
+          if (bi == INT_MAX) break;
+          if (tid == 0) ord[n] = bi;
+          ++n;
+          last_p = bp;
+          last_id = bi;
+          if (tv.topp < 1.0) {
+            c += bp;
+            if (c >= tv.topp) break;
+          }
         }
       }
       L = n;
@@ -2125,7 +2230,12 @@ static int launch_all(const char* rows, int64_t row_bytes, int V, const lc_task*
   resample_kernel<DT><<<g1, RS_THREADS, smem, st>>>(rows, row_bytes, V, tasks, (int)n_tasks, cm, io, ws, counters,
                                                     rw);
   LCB_CUDA_TRY(cudaGetLastError());
-  exact_kernel<DT><<<kExactCtas, EX_THREADS, 0, st>>>(rows, row_bytes, V, tasks, ws.q_exact, cm, io, ex_scr, ex_iscr,
+  static bool ex_attr[2] = {false, false};
+  if (!ex_attr[DT]) {
+    LCB_CUDA_TRY(cudaFuncSetAttribute(exact_kernel<DT>, cudaFuncAttributeMaxDynamicSharedMemorySize, EX_CAND * 12));
+    ex_attr[DT] = true;
+  }
+  exact_kernel<DT><<<kExactCtas, EX_THREADS, EX_CAND * 12, st>>>(rows, row_bytes, V, tasks, ws.q_exact, cm, io, ex_scr, ex_iscr,
                                                       scr_stride, counters);
   LCB_CUDA_TRY(cudaGetLastError());
   return LC_OK;

@@ -176,6 +176,18 @@ def test_resample_matches_oracle(V, conc, T, k, p, bf16):
     assert not np.any(fl & _capi.LC_DRAW_UNRESOLVED)
 
 
+def test_resample_large_nucleus_many_draws():
+    """Flat rows (large nucleus) with 32 draws each: exercises the bracket / kept-list
+    path and its PRECISE / EXACT fallbacks."""
+    V = 32000
+    rng = np.random.default_rng(99)
+    rows = mixing_ref.bf16_round(mixing_ref.fill_rows_np([mixing_ref.mix2(13, i) for i in range(24)], V, 0.0))
+    ulists = [rng.random(32).tolist() for _ in range(24)]
+    for T, p in ((0.6, 0.9), (1.0, 0.95), (0.3, 0.5)):
+        tok, fl, cnt = _resample_rows(rows, T, None, p, ulists, dtype=torch.bfloat16)
+        assert tok.tolist() == _oracle_tokens(rows, T, None, p, ulists), (T, p, cnt)
+
+
 def test_seed_mode_uniforms_equal_explicit_u():
     V = 1000
     rows = mixing_ref.fill_rows_np([mixing_ref.mix2(3, i) for i in range(16)], V, 1.0)
