@@ -29,6 +29,7 @@
 #include <float.h>
 #include <limits.h>
 #include <math.h>
+#include <stdlib.h>
 
 #include "lc_common.cuh"
 #include "lc_numpy.cuh"
@@ -460,7 +461,8 @@ __device__ __forceinline__ void write_all(const TaskView& tv, const DrawIO& io, 
 template <int DT>
 __global__ void __launch_bounds__(RS_THREADS, RS_MIN_BLOCKS)
 resample_kernel(const char* __restrict__ rows, int64_t row_bytes, int Vdef, const lc_task* __restrict__ tasks,
-                int n_tasks, CacheMap cm, DrawIO io, Workspace ws, unsigned long long* counters, int rw_owns) {
+                int n_tasks, CacheMap cm, DrawIO io, Workspace ws, unsigned long long* counters, int rw_owns,
+                int force) {
   extern __shared__ __align__(16) unsigned char smraw[];
   Smem& sm = *reinterpret_cast<Smem*>(smraw);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -482,6 +484,13 @@ resample_kernel(const char* __restrict__ rows, int64_t row_bytes, int Vdef, cons
     if (!resolve_task(tk, rows, row_bytes, Vdef, cm, tv)) {
       write_all(tv, io, -1, LC_DRAW_BAD_ROW);
       if (tid == 0) atomicAdd(&counters[2], 1ull);
+      continue;
+    }
+    if (force == 2) {  // test hook: everything to the EXACT tier
+      if (tid == 0) {
+        const int pos = atomicAdd(ws.q_exact, 1);
+        ws.q_exact[1 + pos] = task_id;
+      }
       continue;
     }
     const int V = tv.V;
@@ -665,7 +674,7 @@ resample_kernel(const char* __restrict__ rows, int64_t row_bytes, int Vdef, cons
     bool to_exact = !sane;
     bool done = false;
 
-    for (int pass = 0; pass < 2 && !done && !to_exact; ++pass) {
+    for (int pass = force == 1 ? 1 : 0; pass < 2 && !done && !to_exact; ++pass) {
       const bool precise = pass == 1;
       const uint8_t tier_flag = precise ? LC_DRAW_PRECISE : 0;
       if (precise) {
@@ -1354,7 +1363,8 @@ struct RwScratch {
 template <int DT>
 __global__ void __launch_bounds__(RW_THREADS, RW_MIN_BLOCKS)
 rowwarp_kernel(const char* __restrict__ rows, int64_t row_bytes, int Vdef, const lc_task* __restrict__ tasks,
-               int n_tasks, CacheMap cm, DrawIO io, int* q_exact, unsigned long long* counters, RwScratch scr) {
+               int n_tasks, CacheMap cm, DrawIO io, int* q_exact, unsigned long long* counters, RwScratch scr,
+               int force) {
   extern __shared__ __align__(16) unsigned char rw_smraw[];
   RwSmem& smem = *reinterpret_cast<RwSmem*>(rw_smraw);
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
@@ -1385,6 +1395,13 @@ rowwarp_kernel(const char* __restrict__ rows, int64_t row_bytes, int Vdef, const
         if (io.flags) io.flags[d] = LC_DRAW_BAD_ROW;
       }
       if (lane == 0) atomicAdd(&counters[2], 1ull);
+      continue;
+    }
+    if (force == 2) {  // test hook: everything to the EXACT tier
+      if (lane == 0) {
+        const int pos = atomicAdd(q_exact, 1);
+        q_exact[1 + pos] = task_id;
+      }
       continue;
     }
     const int V = tv.V;
@@ -1459,7 +1476,7 @@ rowwarp_kernel(const char* __restrict__ rows, int64_t row_bytes, int Vdef, const
     int blo = 0, bhi = 0, nb = 0, nl = 0;
     double Mab = 0.0;  // fp64-lite mass of the list entries above the bracket
 
-    for (int pass = 0; pass < 2 && !done && !to_exact; ++pass) {
+    for (int pass = force == 1 ? 1 : 0; pass < 2 && !done && !to_exact; ++pass) {
       const bool precise = pass == 1;
       const uint8_t tier_flag = precise ? LC_DRAW_PRECISE : 0;
       if (precise) {
@@ -2210,6 +2227,9 @@ static int launch_all(const char* rows, int64_t row_bytes, int V, const lc_task*
     attr_set[DT] = true;
   }
   const int rw = V <= RW_MAXV;
+  // test hook: LCB_FORCE_TIER=precise|exact routes every task to that tier
+  const char* ft = getenv("LCB_FORCE_TIER");
+  const int force = !ft ? 0 : (ft[0] == 'p' ? 1 : (ft[0] == 'e' ? 2 : 0));
   if (rw) {
     const int grw = num_sms() * RW_MIN_BLOCKS;
     const int64_t need = (n_tasks + RW_WARPS - 1) / RW_WARPS;
@@ -2223,12 +2243,12 @@ static int launch_all(const char* rows, int64_t row_bytes, int V, const lc_task*
       rw_attr[DT] = true;
     }
     rowwarp_kernel<DT><<<g, RW_THREADS, sizeof(RwSmem), st>>>(rows, row_bytes, V, tasks, (int)n_tasks, cm, io,
-                                                             ws.q_exact, counters, rs);
+                                                             ws.q_exact, counters, rs, force);
     LCB_CUDA_TRY(cudaGetLastError());
   }
   const int g1 = (int)(n_tasks < grid ? n_tasks : grid);
   resample_kernel<DT><<<g1, RS_THREADS, smem, st>>>(rows, row_bytes, V, tasks, (int)n_tasks, cm, io, ws, counters,
-                                                    rw);
+                                                    rw, force);
   LCB_CUDA_TRY(cudaGetLastError());
   static bool ex_attr[2] = {false, false};
   if (!ex_attr[DT]) {

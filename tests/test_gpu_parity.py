@@ -145,6 +145,21 @@ def test_resample_golden_cases(as_bf16):
     assert n_checked > (500 if as_bf16 else 4000)
 
 
+@pytest.mark.parametrize("tier", ["precise", "exact"])
+def test_forced_tiers_match_golden(tier, monkeypatch):
+    """Every task through the PRECISE pass / the EXACT kernel (LCB_FORCE_TIER hook)."""
+    monkeypatch.setenv("LCB_FORCE_TIER", tier)
+    cases = [c for c in sampling_cases() if len(c.z) <= 4099]
+    for c in cases:
+        tok, fl, _ = _resample_rows(c.z[None, :], c.T, c.top_k, c.top_p, [c.u])
+        assert tok.tolist() == c.tokens.tolist(), (tier, c.name, c.T, c.top_k, c.top_p)
+    rows = mixing_ref.bf16_round(mixing_ref.fill_rows_np([mixing_ref.mix2(17, i) for i in range(6)], 32000, 0.0))
+    ul = [np.random.default_rng(i).random(4).tolist() for i in range(6)]
+    for T, k, p in ((0.6, None, 0.9), (1.0, 50, 0.95), (0.6, None, 1.0)):
+        tok, _, _ = _resample_rows(rows, T, k, p, ul, dtype=torch.bfloat16)
+        assert tok.tolist() == _oracle_tokens(rows, T, k, p, ul), (tier, T, k, p)
+
+
 def _oracle_tokens(rows, T, k, p, ulists):
     out = []
     for z, us in zip(rows, ulists):
