@@ -212,6 +212,76 @@ __device__ __forceinline__ void phase_a(const char* row, int cb, int ce, bool ve
   }
 }
 
+// Phase A for the row-per-warp kernel: also records, per lane, the first
+// vector (id of its first element) holding the lane's maximum, so the first
+// argmax costs one reload instead of a scan.
+template <int DT>
+__device__ __forceinline__ void phase_a_pos(const char* row, int V, bool vec, int lane, float& tmax, float& tmin,
+                                            int& tpos) {
+  if (DT == LC_BF16 && vec) {
+    const uint16_t* r = reinterpret_cast<const uint16_t*>(row);
+    for (int base = 0; base < V; base += 256 * 8) {
+      uint4 q[8];
+      bool full[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int e0 = base + 256 * u + 8 * lane;
+        full[u] = e0 + 8 <= V;
+        if (full[u]) q[u] = __ldg(reinterpret_cast<const uint4*>(r + e0));
+      }
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int e0 = base + 256 * u + 8 * lane;
+        float vmax, vmin;
+        if (full[u]) {
+          const __nv_bfloat162 a0 = *reinterpret_cast<const __nv_bfloat162*>(&q[u].x);
+          const __nv_bfloat162 a1 = *reinterpret_cast<const __nv_bfloat162*>(&q[u].y);
+          const __nv_bfloat162 a2 = *reinterpret_cast<const __nv_bfloat162*>(&q[u].z);
+          const __nv_bfloat162 a3 = *reinterpret_cast<const __nv_bfloat162*>(&q[u].w);
+          const __nv_bfloat162 mx = __hmax2_nan(__hmax2_nan(a0, a1), __hmax2_nan(a2, a3));
+          const __nv_bfloat162 mn = __hmin2_nan(__hmin2_nan(a0, a1), __hmin2_nan(a2, a3));
+          vmax = max_nan(__low2float(mx), __high2float(mx));
+          vmin = min_nan(__low2float(mn), __high2float(mn));
+        } else {
+          vmax = -INFINITY;
+          vmin = INFINITY;
+          for (int j = 0; j < 8 && e0 + j < V; ++j) {
+            const float f = bf16_bits_to_f32(r[e0 + j]);
+            vmax = max_nan(vmax, f);
+            vmin = min_nan(vmin, f);
+          }
+        }
+        if (vmax > tmax || vmax != vmax) {
+          tmax = (vmax != vmax || tmax != tmax) ? NAN : vmax;
+          tpos = e0;
+        }
+        tmin = min_nan(tmin, vmin);
+      }
+    }
+  } else {
+    for (int base = 0; base < V; base += 256 * 4) {
+      float v[4][8];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) load8<DT>(row, base + 256 * u + 8 * lane, V, vec, v[u]);
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int e0 = base + 256 * u + 8 * lane;
+        float vmax = max_nan(max_nan(max_nan(v[u][0], v[u][1]), max_nan(v[u][2], v[u][3])),
+                             max_nan(max_nan(v[u][4], v[u][5]), max_nan(v[u][6], v[u][7])));
+        float vmin = INFINITY;
+#pragma unroll
+        for (int j = 0; j < 8; ++j)
+          if (e0 + j < V) vmin = min_nan(vmin, v[u][j]);
+        if (vmax > tmax || vmax != vmax) {
+          tmax = (vmax != vmax || tmax != tmax) ? NAN : vmax;
+          tpos = e0;
+        }
+        tmin = min_nan(tmin, vmin);
+      }
+    }
+  }
+}
+
 // PRECISE: table-driven fp64 exp of (z - m)/T.  b = 16*log2e*(z-m)/T,
 // n = rint(b), x = b - n in [-1/2, 1/2]; 2^(b/16) = 2^(n>>4) * 2^((n&15)/16) *
 // exp(x*ln2/16) with a degree-6 Taylor polynomial (|x ln2/16| <= 0.0217,
@@ -1416,7 +1486,8 @@ rowwarp_kernel(const char* __restrict__ rows, int64_t row_bytes, int Vdef, const
 
     // ---------------- phase A (packed max / min / NaN)
     float tmax = -INFINITY, tmin = INFINITY;
-    phase_a<DT>(tv.row, 0, V, vec, lane, tmax, tmin);
+    int tpos = 0;
+    phase_a_pos<DT>(tv.row, V, vec, lane, tmax, tmin, tpos);
     const bool bad = __any_sync(0xffffffffu, (tmax != tmax) || (tmin != tmin));
     if (bad) tmax = -INFINITY;
     const float m = warp_max(tmax);
@@ -1426,17 +1497,15 @@ rowwarp_kernel(const char* __restrict__ rows, int64_t row_bytes, int Vdef, const
       if (lane == 0) atomicAdd(&counters[2], 1ull);
       continue;
     }
-    // first argmax: lanes holding m scan their own vectors
+    // first argmax: lanes holding m reload the first vector that held their maximum
     auto first_argmax = [&]() -> int {
       int best = INT_MAX;
       if (tmax == m) {
-        for (int e0 = 8 * lane; e0 < V && best == INT_MAX; e0 += 256) {
-          float v[8];
-          load8<DT>(tv.row, e0, V, vec, v);
+        float v[8];
+        load8<DT>(tv.row, tpos, V, vec, v);
 #pragma unroll
-          for (int j = 0; j < 8; ++j)
-            if (v[j] == m && e0 + j < best) best = e0 + j;
-        }
+        for (int j = 7; j >= 0; --j)
+          if (v[j] == m) best = tpos + j;
       }
       return warp_min_int(best);
     };
@@ -1940,6 +2009,25 @@ exact_kernel(const char* __restrict__ rows, int64_t row_bytes, int Vdef, const l
       s_m = m;
     }
     __syncthreads();
+    if (tv.T == 0.0) {  // greedy: first argmax (sampling.py:61-64)
+      int best = INT_MAX;
+      for (int i = tid; i < V; i += EX_THREADS)
+        if (load1<DT>(tv.row, i) == s_m) best = min(best, i);
+      s_bi[tid] = best;
+      __syncthreads();
+      if (tid == 0) {
+        int b2 = INT_MAX;
+        for (int i = 0; i < EX_THREADS; ++i) b2 = min(b2, s_bi[i]);
+        s_L = b2;
+      }
+      __syncthreads();
+      for (int64_t d = tv.d0 + tid; d < tv.d1; d += EX_THREADS) {
+        io.token[d] = s_L;
+        if (io.flags) io.flags[d] = LC_DRAW_PRECISE;
+      }
+      __syncthreads();
+      continue;
+    }
     ExpCtx ec;
     ec.m = s_m;
     ec.T = tv.T;
