@@ -1339,6 +1339,8 @@ struct __align__(16) RwWarp {
   double ce[RW_CAND];
   uint32_t hist[RW_NB];
   double seg[RW_NSEG + 1];  // segment masses, then exclusive prefix
+  double segE[RW_NSEG];     // fused pass: per-segment absolute error bound
+  float segm[RW_NSEG];      // fused pass: the warp's running max at the segment end
   double dsc[4];
   int isc[4];
 };
@@ -1357,6 +1359,137 @@ __device__ __forceinline__ int rw_bin(const ExpCtx& c, float a) {
 // 2^(b/8) as fp32 (relative error <= 2^-24)
 __device__ __forceinline__ float rw_scale(int b, const float* f8) {
   return __int_as_float(((b >> 3) + 127) << 23) * f8[b & 7];
+}
+
+struct FusedOut {
+  float tmax, tmin;
+  int tpos;
+  bool nan;
+  double S, ES, relmax;
+};
+
+// FAST fused pass (phase A + B in one read): per lane a running maximum mt; the
+// lane's partial mass is kept relative to mt and rescaled (factor f with its
+// own error bound) when mt grows; at each 2048-id segment end the lanes combine
+// at the warp's running max, and at the end every segment is rescaled (fp64)
+// to the row max.  Returns the row mass S, its absolute error bound ES and the
+// largest per-segment relative bound (for prefix sums), with seg[] relative to
+// the row max.  ACC selects the corrected exponential (untruncated rows).
+template <int DT, bool ACC>
+__device__ FusedOut rw_fused_pass(const char* row, int V, int nseg, bool vec, int lane, float Lhi, float Llo,
+                                  double Ld, RwWarp& sw) {
+  FusedOut o;
+  float mt = -INFINITY, tmin = INFINITY;
+  int tpos = 0;
+  bool nan = false;
+  const float eta = (float)(ACC ? (kEx2RelErr + kCorrErr + kSum8Err) : (kEx2Raw + kSum8Err)) * 1.0001f;
+  const float ka = (float)kArgRel * 1.0001f;
+  for (int s = 0; s < nseg; ++s) {
+    double acc = 0.0;
+    float W = 0.0f, R = 0.0f;  // |a|-weighted mass (CHEAP) and rescale error, relative to mt
+#pragma unroll 1
+    for (int st = 0; st < RW_SEGSTEPS; st += 4) {
+      float v[4][8];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) load8<DT>(row, s * RW_SEG + 256 * (st + u) + 8 * lane, V, vec, v[u]);
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int e0 = s * RW_SEG + 256 * (st + u) + 8 * lane;
+        const float vmax = max_nan(max_nan(max_nan(v[u][0], v[u][1]), max_nan(v[u][2], v[u][3])),
+                                   max_nan(max_nan(v[u][4], v[u][5]), max_nan(v[u][6], v[u][7])));
+        float vmin = INFINITY;
+#pragma unroll
+        for (int j = 0; j < 8; ++j)
+          if (e0 + j < V) vmin = fminf(vmin, v[u][j]);
+        tmin = fminf(tmin, vmin);
+        nan |= (vmax != vmax);
+        if (vmax > mt) {
+          if (acc > 0.0) {  // rescale the partials to the new maximum
+            const float da = (mt - vmax) * Lhi;
+            float f;
+            if (ACC) {
+              ExpCtx c2;
+              c2.m = vmax;
+              c2.Lhi = Lhi;
+              c2.Llo = Llo;
+              f = fast_exp(c2, mt);
+            } else {
+              f = ex2_approx(da);
+            }
+            const float epsf = eta + (ACC ? 0.0f : ka * -da);
+            R = (R + (float)acc * epsf) * f;
+            W *= f;
+            acc *= (double)f;
+          }
+          mt = vmax;
+          tpos = e0;
+        }
+        float ef[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          if (ACC) {
+            ExpCtx c2;
+            c2.m = mt;
+            c2.Lhi = Lhi;
+            c2.Llo = Llo;
+            ef[j] = fast_exp(c2, v[u][j]);
+          } else {
+            const float a = fmaxf((v[u][j] - mt) * Lhi, -200.0f);
+            ef[j] = ex2_approx(a);
+            W = fmaf(ef[j], -a, W);
+          }
+        }
+        acc += (double)(((ef[0] + ef[1]) + (ef[2] + ef[3])) + ((ef[4] + ef[5]) + (ef[6] + ef[7])));
+      }
+    }
+    // segment end: combine at the warp's running maximum
+    const float ms = warp_max(mt);
+    float g = 1.0f, epsg = 0.0f;
+    if (mt < ms && acc > 0.0) {
+      const float da = (mt - ms) * Lhi;
+      if (ACC) {
+        ExpCtx c2;
+        c2.m = ms;
+        c2.Lhi = Lhi;
+        c2.Llo = Llo;
+        g = fast_exp(c2, mt);
+      } else {
+        g = ex2_approx(da);
+      }
+      epsg = eta + (ACC ? 0.0f : ka * -da);
+    }
+    const double sa = warp_sum(acc * (double)g);
+    const double sE = warp_sum((double)g * (acc * (double)(eta + epsg) + (double)R + (double)(ka * W)));
+    if (lane == 0) {
+      sw.seg[s] = sa;
+      sw.segE[s] = sE;
+      sw.segm[s] = ms;
+    }
+  }
+  __syncwarp();
+  o.tmax = mt;
+  o.tmin = tmin;
+  o.tpos = tpos;
+  o.nan = __any_sync(0xffffffffu, nan);
+  // rescale the segments to the row maximum (fp64 exp2: relative error ~2^-51)
+  const float m = warp_max(mt);
+  double S = 0.0, ES = 0.0, rel = 0.0;
+  if (lane < nseg) {
+    const double h = exp2(((double)sw.segm[lane] - (double)m) * Ld);
+    const double x = sw.seg[lane] * h;
+    const double e = sw.segE[lane] * h + x * 1e-15;
+    sw.seg[lane] = x;
+    S = x;
+    ES = e;
+    rel = x > 0.0 ? e / x : 0.0;
+  }
+  __syncwarp();
+  o.S = warp_sum(S);
+  o.ES = warp_sum(ES);
+  o.relmax = rel;
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) o.relmax = fmax(o.relmax, __shfl_xor_sync(0xffffffffu, o.relmax, off));
+  return o;
 }
 
 // e-function variants: 0 CHEAP (truncated rows), 1 ACCURATE (untruncated), 2 PRECISE (lite)
@@ -1484,10 +1617,24 @@ rowwarp_kernel(const char* __restrict__ rows, int64_t row_bytes, int Vdef, const
       }
     };
 
-    // ---------------- phase A (packed max / min / NaN)
+    // ---------------- one read of the row: max / min / NaN (+ mass for T > 0)
     float tmax = -INFINITY, tmin = INFINITY;
     int tpos = 0;
-    phase_a_pos<DT>(tv.row, V, vec, lane, tmax, tmin, tpos);
+    FusedOut fo{};
+    double Ld = 0.0;
+    float Lhi = 0.0f, Llo = 0.0f;
+    if (tv.T == 0.0) {
+      phase_a_pos<DT>(tv.row, V, vec, lane, tmax, tmin, tpos);
+    } else {
+      Ld = 1.4426950408889634 / tv.T;
+      Lhi = (float)Ld;
+      Llo = (float)(Ld - (double)Lhi);
+      fo = tv.trunc ? rw_fused_pass<DT, false>(tv.row, V, nseg, vec, lane, Lhi, Llo, Ld, sw)
+                    : rw_fused_pass<DT, true>(tv.row, V, nseg, vec, lane, Lhi, Llo, Ld, sw);
+      tmax = fo.nan ? NAN : fo.tmax;
+      tmin = fo.tmin;
+      tpos = fo.tpos;
+    }
     const bool bad = __any_sync(0xffffffffu, (tmax != tmax) || (tmin != tmin));
     if (bad) tmax = -INFINITY;
     const float m = warp_max(tmax);
@@ -1519,12 +1666,9 @@ rowwarp_kernel(const char* __restrict__ rows, int64_t row_bytes, int Vdef, const
     ec.T = tv.T;
     ec.mT = __ddiv_rn((double)m, tv.T);
     ec.md = (double)m;
-    {
-      const double Ld = 1.4426950408889634 / tv.T;
-      ec.Lhi = (float)Ld;
-      ec.Llo = (float)(Ld - (double)ec.Lhi);
-      ec.L16 = 16.0 * Ld;
-    }
+    ec.Lhi = Lhi;
+    ec.Llo = Llo;
+    ec.L16 = 16.0 * Ld;
     const double zabs = fmax(fabs((double)m), isfinite(zmin) ? fabs((double)zmin) : fabs((double)m));
     const bool sane = ec.Lhi < 1e20f && ec.Lhi > 1e-20f && fabsf(m) * ec.Lhi < 1e30f && zabs / tv.T < 1e15;
     const double relArg = 4.440892098500626e-16 * 2.0 * zabs / tv.T;
@@ -1539,7 +1683,6 @@ rowwarp_kernel(const char* __restrict__ rows, int64_t row_bytes, int Vdef, const
       if (accurate) return rw_seg_pass<DT, 1, false>(tv.row, V, nseg, vec, lane, ec, smem.t16, sw.seg, 0, 0, 0ull);
       return rw_seg_pass<DT, 0, false>(tv.row, V, nseg, vec, lane, ec, smem.t16, sw.seg, 0, 0, 0ull);
     };
-    const double Wrow = seg_pass(false);
     bool done = false, to_exact = !sane;
     int big_state = 0;  // 0 not built, 1 built, -1 failed
     int blo = 0, bhi = 0, nb = 0, nl = 0;
@@ -1554,12 +1697,12 @@ rowwarp_kernel(const char* __restrict__ rows, int64_t row_bytes, int Vdef, const
       }
       double S = 0.0;
       for (int s = 0; s < nseg; ++s) S += sw.seg[s];
-      const double relE = precise    ? relLite
-                          : accurate ? (kEx2RelErr + kCorrErr + kSum8Err + kRefExpErr + relArg +
-                                        (double)(V + 16) * kEps64)
-                                     : (kEx2Raw + kSum8Err + kRefExpErr + relArg + (double)(V + 16) * kEps64);
+      // FAST: the fused pass's bound (element exps, rescales, pair sums) + the reference's
+      // argument/exp rounding + fp64 accumulation; PRECISE: lite_exp's
+      const double relCommon = kRefExpErr + relArg + (double)(V + 16) * kEps64;
+      const double relE = precise ? relLite : fo.relmax + relCommon;
       const double absE = precise ? (double)V * 1e-300 : (double)V * 2.4e-38;
-      const double E_S = S * relE + absE + ((!precise && !accurate) ? kArgRel * Wrow : 0.0);
+      const double E_S = precise ? S * relE + absE : fo.ES + S * relCommon + absE;
 
       bool big = false;
       unsigned long long kcut = 0ull;
@@ -1840,7 +1983,7 @@ rowwarp_kernel(const char* __restrict__ rows, int64_t row_bytes, int Vdef, const
         }
         __syncwarp();
         const double K = sw.seg[nseg];
-        const double absD = E_S - relE * S;  // absolute part of the bound (flushed mass, W term)
+        const double absD = fmax(absE, E_S - relE * S);  // absolute part of the bound (flushed mass)
         for (int64_t dbase = tv.d0; dbase < tv.d1; dbase += 32) {
           const int64_t d = dbase + lane;
           double t = INFINITY, u = 0.0;
