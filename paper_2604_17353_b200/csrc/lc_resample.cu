@@ -1387,20 +1387,55 @@ __device__ FusedOut rw_fused_pass(const char* row, int V, int nseg, bool vec, in
   for (int s = 0; s < nseg; ++s) {
     double acc = 0.0;
     float W = 0.0f, R = 0.0f;  // |a|-weighted mass (CHEAP) and rescale error, relative to mt
+    constexpr int UNRF = (DT == LC_BF16) ? 8 : 4;  // 128 B per lane in flight
 #pragma unroll 1
-    for (int st = 0; st < RW_SEGSTEPS; st += 4) {
-      float v[4][8];
+    for (int st = 0; st < RW_SEGSTEPS; st += UNRF) {
+      // raw vector loads first (memory-level parallelism), unpacked one vector at a time
+      uint4 raw[UNRF][DT == LC_BF16 ? 1 : 2];
+      bool full[UNRF];
 #pragma unroll
-      for (int u = 0; u < 4; ++u) load8<DT>(row, s * RW_SEG + 256 * (st + u) + 8 * lane, V, vec, v[u]);
-#pragma unroll
-      for (int u = 0; u < 4; ++u) {
+      for (int u = 0; u < UNRF; ++u) {
         const int e0 = s * RW_SEG + 256 * (st + u) + 8 * lane;
-        const float vmax = max_nan(max_nan(max_nan(v[u][0], v[u][1]), max_nan(v[u][2], v[u][3])),
-                                   max_nan(max_nan(v[u][4], v[u][5]), max_nan(v[u][6], v[u][7])));
+        full[u] = vec && e0 + 8 <= V;
+        if (full[u]) {
+          if (DT == LC_BF16) {
+            raw[u][0] = __ldg(reinterpret_cast<const uint4*>(reinterpret_cast<const uint16_t*>(row) + e0));
+          } else {
+            raw[u][0] = __ldg(reinterpret_cast<const uint4*>(reinterpret_cast<const float*>(row) + e0));
+            raw[u][DT == LC_BF16 ? 0 : 1] =
+                __ldg(reinterpret_cast<const uint4*>(reinterpret_cast<const float*>(row) + e0 + 4));
+          }
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < UNRF; ++u) {
+        const int e0 = s * RW_SEG + 256 * (st + u) + 8 * lane;
+        float vv[8];
+        if (full[u]) {
+          if (DT == LC_BF16) {
+            const uint32_t w[4] = {raw[u][0].x, raw[u][0].y, raw[u][0].z, raw[u][0].w};
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+              vv[2 * j] = __uint_as_float(w[j] << 16);
+              vv[2 * j + 1] = __uint_as_float(w[j] & 0xffff0000u);
+            }
+          } else {
+            const uint4 a = raw[u][0], b = raw[u][DT == LC_BF16 ? 0 : 1];
+            vv[0] = __uint_as_float(a.x); vv[1] = __uint_as_float(a.y);
+            vv[2] = __uint_as_float(a.z); vv[3] = __uint_as_float(a.w);
+            vv[4] = __uint_as_float(b.x); vv[5] = __uint_as_float(b.y);
+            vv[6] = __uint_as_float(b.z); vv[7] = __uint_as_float(b.w);
+          }
+        } else {
+          load8<DT>(row, e0, V, vec, vv);
+        }
+        float (&vu)[8] = vv;
+        const float vmax = max_nan(max_nan(max_nan(vu[0], vu[1]), max_nan(vu[2], vu[3])),
+                                   max_nan(max_nan(vu[4], vu[5]), max_nan(vu[6], vu[7])));
         float vmin = INFINITY;
 #pragma unroll
         for (int j = 0; j < 8; ++j)
-          if (e0 + j < V) vmin = fminf(vmin, v[u][j]);
+          if (e0 + j < V) vmin = fminf(vmin, vu[j]);
         tmin = fminf(tmin, vmin);
         nan |= (vmax != vmax);
         if (vmax > mt) {
@@ -1432,9 +1467,9 @@ __device__ FusedOut rw_fused_pass(const char* row, int V, int nseg, bool vec, in
             c2.m = mt;
             c2.Lhi = Lhi;
             c2.Llo = Llo;
-            ef[j] = fast_exp(c2, v[u][j]);
+            ef[j] = fast_exp(c2, vu[j]);
           } else {
-            const float a = fmaxf((v[u][j] - mt) * Lhi, -200.0f);
+            const float a = fmaxf((vu[j] - mt) * Lhi, -200.0f);
             ef[j] = ex2_approx(a);
             W = fmaf(ef[j], -a, W);
           }
@@ -1889,85 +1924,80 @@ rowwarp_kernel(const char* __restrict__ rows, int64_t row_bytes, int Vdef, const
       int need = 0;
       if (big) {
         // ---------------- draws over the kept list (precise e's, id order)
-        auto kept_e = [&](int i) -> double {
-          const int idf = L_id[i];
-          if (idf >= 0) return L_e[i];
-          return cand_key(L_z[i], idf & 0x7fffffff) >= kcut ? L_e[i] : 0.0;
-        };
-        double kacc = 0.0;
-        for (int i = lane; i < nl; i += 32) kacc += kept_e(i);
-        const double K = warp_sum(kacc);
-        const double relD = relLite + (double)(nl + 64) * 4.0 * kEps64;
-        for (int64_t dbase = tv.d0; dbase < tv.d1; dbase += 32) {
-          const int64_t d = dbase + lane;
-          double t = INFINITY, u = 0.0;
-          if (d < tv.d1) {
-            u = draw_u(io, d, tv);
-            t = u * K;
-            if (!(t < K)) need = 1;
-          }
-          double st = (d < tv.d1 && t < K) ? t : INFINITY;
-          int ssrc = lane;
+        // mask the bracket members beyond the cut in place and build 32-entry chunk sums
+        // (sw.ce is free after the cut); each lane then locates one target on its own
+        double* csum = sw.ce;
+        const int nch = (nl + 31) / 32;
+        if (nch > RW_CAND) {
+          need = 1;
+        } else {
+          for (int c0 = 0; c0 < nch; c0 += 4) {
+            double part[4];
 #pragma unroll
-          for (int k2 = 2; k2 <= 32; k2 <<= 1) {
+            for (int q = 0; q < 4; ++q) {
+              const int i = (c0 + q) * 32 + lane;
+              double e = 0.0;
+              if (c0 + q < nch && i < nl) {
+                const int idf = L_id[i];
+                e = L_e[i];
+                if (idf < 0 && cand_key(L_z[i], idf & 0x7fffffff) < kcut) e = 0.0;
+              }
+              part[q] = e;
+            }
 #pragma unroll
-            for (int j2 = k2 >> 1; j2 > 0; j2 >>= 1) {
-              const double ot = __shfl_xor_sync(0xffffffffu, st, j2);
-              const int os = __shfl_xor_sync(0xffffffffu, ssrc, j2);
-              const bool asc = (lane & k2) == 0 || k2 == 32;
-              const bool lower = (lane & j2) == 0;
-              const bool take =
-                  (lower == asc) ? (ot < st || (ot == st && os < ssrc)) : (ot > st || (ot == st && os > ssrc));
-              if (take) {
-                st = ot;
-                ssrc = os;
-              }
+            for (int q = 0; q < 4; ++q) {
+              const double t2 = warp_sum(part[q]);
+              if (lane == 0 && c0 + q < nch) csum[c0 + q] = t2;
             }
           }
-          const double su = __shfl_sync(0xffffffffu, u, ssrc);
-          const int ntar = __popc(__ballot_sync(0xffffffffu, st < INFINITY));
-          int k = 0;
-          double off = 0.0;
-          for (int i0 = 0; i0 < nl && k < ntar; i0 += 32) {
-            const int i = i0 + lane;
-            const double e = i < nl ? kept_e(i) : 0.0;
-            const int id = i < nl ? (L_id[i] & 0x7fffffff) : -1;
-            const double x = warp_incl_scan(e);
-            const double tot = __shfl_sync(0xffffffffu, x, 31);
-            while (k < ntar) {
-              const double tk = __shfl_sync(0xffffffffu, st, k);
-              if (!(tk < off + tot)) break;
-              const unsigned hm = __ballot_sync(0xffffffffu, (e > 0.0) && (tk < off + x));
-              int found = -1;
-              double flo = 0.0, fhi = 0.0;
-              if (hm) {
-                const int hl = __ffs(hm) - 1;
-                found = __shfl_sync(0xffffffffu, id, hl);
-                flo = __shfl_sync(0xffffffffu, off + x - e, hl);
-                fhi = __shfl_sync(0xffffffffu, off + x, hl);
-              }
-              const double uu = __shfl_sync(0xffffffffu, su, k);
-              const int src = __shfl_sync(0xffffffffu, ssrc, k);
-              if (lane == 0) {
-                const double tlo = relD * ((1.0 - uu) * flo + uu * (K - flo)) + tk * relRef * 4.0;
-                const double thi = relD * ((1.0 - uu) * fhi + uu * (K - fhi)) + tk * relRef * 4.0;
-                // nothing kept precedes flo == 0: the lower boundary is exact
-                const bool ok = found >= 0 && (tk - flo > tlo || flo == 0.0) && (fhi - tk > thi);
-                io.token[dbase + src] = found;
-                if (io.flags) io.flags[dbase + src] = tier_flag;
-                need |= !ok;
-              }
-              ++k;
+          __syncwarp();
+          if (lane == 0) {  // exclusive prefix over chunks (sequential: exact order)
+            double c = 0.0;
+            for (int q = 0; q < nch; ++q) {
+              const double x = csum[q];
+              csum[q] = c;
+              c += x;
             }
-            off += tot;
+            csum[nch] = c;
           }
-          while (k < ntar) {  // rounding left a target past the list end
-            const int src = __shfl_sync(0xffffffffu, ssrc, k);
-            if (lane == 0) {
-              io.token[dbase + src] = -1;
-              need = 1;
+          __syncwarp();
+          const double K = csum[nch];
+          const double relD = relLite + (double)(nl + 64) * 4.0 * kEps64;
+          for (int64_t d = tv.d0 + lane; d < tv.d1; d += 32) {
+            const double u = draw_u(io, d, tv);
+            const double tk = u * K;
+            int found = -1;
+            double flo = 0.0, fhi = 0.0;
+            if (tk < K) {
+              int lo = 0, hi = nch;  // last chunk with prefix <= tk
+              while (hi - lo > 1) {
+                const int mid = (lo + hi) >> 1;
+                if (csum[mid] <= tk) lo = mid;
+                else hi = mid;
+              }
+              double c = csum[lo];
+              const int i0 = lo * 32, i1 = min(nl, i0 + 32);
+              for (int i = i0; i < i1; ++i) {
+                const int idf = L_id[i];
+                double e = L_e[i];
+                if (idf < 0 && cand_key(L_z[i], idf & 0x7fffffff) < kcut) e = 0.0;  // beyond the cut
+                const double nc = c + e;
+                if (e > 0.0 && tk < nc) {
+                  found = idf & 0x7fffffff;
+                  flo = c;
+                  fhi = nc;
+                  break;
+                }
+                c = nc;
+              }
             }
-            ++k;
+            const double tlo = relD * ((1.0 - u) * flo + u * (K - flo)) + tk * relRef * 4.0;
+            const double thi = relD * ((1.0 - u) * fhi + u * (K - fhi)) + tk * relRef * 4.0;
+            // nothing kept precedes flo == 0: the lower boundary is exact
+            const bool ok = found >= 0 && (tk - flo > tlo || flo == 0.0) && (fhi - tk > thi);
+            io.token[d] = found;
+            if (io.flags) io.flags[d] = tier_flag;
+            need |= !ok;
           }
         }
       } else {
