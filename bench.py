@@ -32,15 +32,18 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 CONFIGS = {
-    # name: (vocab, n_requests, n_branch, rows_per_entry, T, top_k, top_p, dtype, description)
-    "c1": dict(V=32000, n_req=16, nb=1, R=500, T=0.6, k=0, p=1.0, dtype="float32",
-               desc="ToT re-sampling, vocab 32000, 16 branches x 500-token expansions, fp32, top-p 1"),
-    "c2": dict(V=32000, n_req=256, nb=32, R=500, T=0.6, k=0, p=0.9, dtype="bfloat16",
+    # BASELINE.json configs, as resample workloads over HBM-resident cached trajectories:
+    # n_req entries (tree nodes / requests), R cached rows each, nb draws per row (siblings)
+    "c1": dict(V=32000, n_req=120, nb=1, R=500, T=0.6, k=0, p=1.0, dtype="float32", scaling="weak",
+               desc="ToT re-sampling, vocab 32000, 16 branches x depth 8 (120 revisits x 500 cached rows), "
+                    "fp32, T 0.6, top-p 1"),
+    "c2": dict(V=32000, n_req=256, nb=32, R=500, T=0.6, k=0, p=0.9, dtype="bfloat16", scaling="weak",
                desc="Best-of-N re-sampling, vocab 32000, 256 requests x N=32, T 0.6 + top-p 0.9, bf16"),
-    "c3": dict(V=151936, n_req=1024, nb=1, R=16, T=0.6, k=50, p=0.95, dtype="bfloat16",
-               desc="vocab 151936, 1024 branches, top-k 50 + top-p 0.95, 16-row entries, all hits"),
-    "c5": dict(V=151936, n_req=8 * 512, nb=1, R=4, T=0.6, k=50, p=0.95, dtype="bfloat16",
-               desc="8 agent trees x 512 branches, vocab 151936, top-k 50 + top-p 0.95 (per rank)"),
+    "c3": dict(V=151936, n_req=1024, nb=1, R=16, T=0.6, k=50, p=0.95, dtype="bfloat16", scaling="weak",
+               desc="vocab 151936, 1024 concurrent branches (16-row entries, all hits), top-k 50 + top-p 0.95, bf16"),
+    "c5": dict(V=151936, n_req=8 * 512, nb=1, R=4, T=0.6, k=50, p=0.95, dtype="bfloat16", scaling="strong",
+               desc="multi-agent: 8 trees x 512 branches (4 cached rows each), vocab 151936, top-k 50 + "
+                    "top-p 0.95, bf16; trees sharded tree i -> GPU i mod G"),
 }
 
 
@@ -101,7 +104,7 @@ class ClockSampler:
 # ------------------------------------------------------------------------ our arm
 
 
-def setup_workload(cfg, dev, rank):
+def setup_workload(cfg, dev, rank, world=1):
     import torch
 
     import paper_2604_17353_b200 as lcb
@@ -157,7 +160,14 @@ def run_ours(args, cfg, rank, world, dev):
 
     import paper_2604_17353_b200 as lcb
 
-    w = setup_workload(cfg, dev, rank)
+    if cfg["scaling"] == "strong":  # trees sharded across ranks: tree i -> rank i % world
+        from paper_2604_17353_b200.shard import local_trees
+
+        cfg = dict(cfg)
+        n_trees = 8
+        per_tree = cfg["n_req"] // n_trees
+        cfg["n_req"] = len(local_trees(n_trees, rank, world)) * per_tree
+    w = setup_workload(cfg, dev, rank, world)
     cache = w["cache"]
     V, n_req, nb, R = cfg["V"], cfg["n_req"], cfg["nb"], cfg["R"]
     esz = 2 if cfg["dtype"] == "bfloat16" else 4
@@ -259,7 +269,8 @@ def run_ours(args, cfg, rank, world, dev):
     accepted, precise, unresolved, bad = (int(x) for x in counts.tolist())
     if rank != 0:
         return None
-    tokens_total = n_draws * args.steps * world
+    tokens_total = (n_draws * args.steps * world if cfg["scaling"] == "weak"
+                    else CONFIGS[args.config]["n_req"] * R * nb * args.steps)
     peak, peak_src = peaks()
     algo_bytes_launch = n_rows * V * esz + n_draws * 20  # V*s per unique row + 20 B per draw
     k_avg = sum(k_ms) / max(len(k_ms), 1)
@@ -273,7 +284,7 @@ def run_ours(args, cfg, rank, world, dev):
         "warmup": args.warmup,
         "ms_per_step": ms / args.steps,
         "higher_is_better": True,
-        "scaling": "weak",
+        "scaling": cfg["scaling"],
         "vs_baseline": None,
         "dtype": "bf16" if esz == 2 else "f32",
         "data": "synthetic (reference producer fill_logits, seed 7, conc 2.5, range 5.0)",
@@ -282,7 +293,8 @@ def run_ours(args, cfg, rank, world, dev):
                    "top_k": cfg["k"] or None, "top_p": cfg["p"], "slab_gb_per_gpu": w["slab_bytes"] / 1e9,
                    "l2": "inputs larger than L2 (slab re-read every step)", "parallelism": f"tree-sharded x{world}"},
         "accepted_tokens_per_s": accepted / (ms * 1e-3),
-        "rows_per_s": n_rows * args.steps * world / (ms * 1e-3),
+        "rows_per_s": (n_rows * world if cfg["scaling"] == "weak" else CONFIGS[args.config]["n_req"] * R)
+        * args.steps / (ms * 1e-3),
         "precise_tasks": precise,
         "unresolved_draws": unresolved,
         "bad_rows": bad,

@@ -1598,8 +1598,8 @@ struct RwScratch {
   int* next;   // dynamic task counter
 };
 
-template <int DT>
-__global__ void __launch_bounds__(RW_THREADS, RW_MIN_BLOCKS)
+template <int DT, int MINB>
+__global__ void __launch_bounds__(RW_THREADS, MINB)
 rowwarp_kernel(const char* __restrict__ rows, int64_t row_bytes, int Vdef, const lc_task* __restrict__ tasks,
                int n_tasks, CacheMap cm, DrawIO io, int* q_exact, unsigned long long* counters, RwScratch scr,
                int force) {
@@ -2435,7 +2435,7 @@ static int rw_cap(int64_t V) { return (int)((V / 5 + 256 + 31) & ~31ll); }
 int64_t workspace_bytes(int64_t n_tasks, int64_t vocab) {
   const int64_t grid = grid_ctas();
   int64_t b = 0;
-  const int64_t rw_warps = (int64_t)num_sms() * RW_MIN_BLOCKS * RW_WARPS;
+  const int64_t rw_warps = (int64_t)num_sms() * 3 * RW_WARPS;
   b += ((rw_warps * rw_cap(vocab) * 16) + 3 * 255) & ~255ll;
   b += 512;
   b += ((n_tasks + 1) * 4 + 255) & ~255ll;
@@ -2468,7 +2468,7 @@ static int launch_all(const char* rows, int64_t row_bytes, int V, const lc_task*
   unsigned long long* cnt = (unsigned long long*)take(64);
   RwScratch rs;
   rs.cap = rw_cap(V);
-  const int64_t rw_warps = (int64_t)num_sms() * RW_MIN_BLOCKS * RW_WARPS;
+  const int64_t rw_warps = (int64_t)num_sms() * 3 * RW_WARPS;
   rs.id = (int*)take(rw_warps * rs.cap * 4);
   rs.z = (float*)take(rw_warps * rs.cap * 4);
   rs.e = (double*)take(rw_warps * rs.cap * 8);
@@ -2492,19 +2492,31 @@ static int launch_all(const char* rows, int64_t row_bytes, int V, const lc_task*
   const char* ft = getenv("LCB_FORCE_TIER");
   const int force = !ft ? 0 : (ft[0] == 'p' ? 1 : (ft[0] == 'e' ? 2 : 0));
   if (rw) {
-    const int grw = num_sms() * RW_MIN_BLOCKS;
+    // CTAs per SM: 2 (128 registers, no spills) by default; LCB_RW_BLOCKS=3 trades spills for warps
+    const char* rb = getenv("LCB_RW_BLOCKS");
+    const int minb = (rb && rb[0] == '3') ? 3 : RW_MIN_BLOCKS;
+    const int grw = num_sms() * minb;
     const int64_t need = (n_tasks + RW_WARPS - 1) / RW_WARPS;
     const int g = (int)(need < grw ? need : grw);
     rs.next = rw_next;
     LCB_CUDA_TRY(cudaMemsetAsync(rw_next, 0, 4, st));
-    static bool rw_attr[2] = {false, false};
-    if (!rw_attr[DT]) {
-      LCB_CUDA_TRY(cudaFuncSetAttribute(rowwarp_kernel<DT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                        (int)sizeof(RwSmem)));
-      rw_attr[DT] = true;
+    static bool rw_attr[2][2] = {{false, false}, {false, false}};
+    if (!rw_attr[DT][minb == 3]) {
+      if (minb == 3)
+        LCB_CUDA_TRY(cudaFuncSetAttribute(rowwarp_kernel<DT, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          (int)sizeof(RwSmem)));
+      else
+        LCB_CUDA_TRY(cudaFuncSetAttribute(rowwarp_kernel<DT, RW_MIN_BLOCKS>,
+                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(RwSmem)));
+      rw_attr[DT][minb == 3] = true;
     }
-    rowwarp_kernel<DT><<<g, RW_THREADS, sizeof(RwSmem), st>>>(rows, row_bytes, V, tasks, (int)n_tasks, cm, io,
-                                                             ws.q_exact, counters, rs, force);
+    if (minb == 3)
+      rowwarp_kernel<DT, 3><<<g, RW_THREADS, sizeof(RwSmem), st>>>(rows, row_bytes, V, tasks, (int)n_tasks, cm, io,
+                                                                  ws.q_exact, counters, rs, force);
+    else
+      rowwarp_kernel<DT, RW_MIN_BLOCKS><<<g, RW_THREADS, sizeof(RwSmem), st>>>(rows, row_bytes, V, tasks,
+                                                                              (int)n_tasks, cm, io, ws.q_exact,
+                                                                              counters, rs, force);
     LCB_CUDA_TRY(cudaGetLastError());
   }
   const int g1 = (int)(n_tasks < grid ? n_tasks : grid);
