@@ -1333,6 +1333,7 @@ constexpr int RW_SEGSTEPS = 8;    // 8 x 256 ids = 2048 per segment
 constexpr int RW_SEG = 256 * RW_SEGSTEPS;
 constexpr int RW_MAXV = 65536;
 constexpr int RW_NSEG = RW_MAXV / RW_SEG;  // 32
+constexpr int RW_NCH = 256;                // kept-list chunks of 32 entries per warp
 
 struct __align__(16) RwWarp {
   unsigned long long cand[RW_CAND];
@@ -1340,6 +1341,8 @@ struct __align__(16) RwWarp {
   uint32_t hist[RW_NB];
   double seg[RW_NSEG + 1];  // segment masses, then exclusive prefix
   double segE[RW_NSEG];     // fused pass: per-segment absolute error bound
+  double chunk_above[RW_NCH];    // kept list: per-32-entry mass above the bracket
+  double chunk_tot[RW_NCH + 1];  // kept list: per-chunk kept mass, then exclusive prefix
   float segm[RW_NSEG];      // fused pass: the warp's running max at the segment end
   double dsc[4];
   int isc[4];
@@ -1591,8 +1594,7 @@ __device__ double rw_seg_pass(const char* row, int V, int nseg, bool vec, int la
 }
 
 struct RwScratch {
-  int* id;     // [warps][cap] kept-list ids (id order); bit 31 = bracket member
-  float* z;    // [warps][cap]
+  int2* iz;    // [warps][cap] kept list in id order: {id | bracket-member bit 31, z bits}
   double* e;   // [warps][cap] fp64-lite e
   int cap;
   int* next;   // dynamic task counter
@@ -1612,8 +1614,7 @@ rowwarp_kernel(const char* __restrict__ rows, int64_t row_bytes, int Vdef, const
   if (lane == 0) sw.isc[0] = 0;
   __syncthreads();
   const int gw = blockIdx.x * RW_WARPS + wid;
-  int* L_id = scr.id + (int64_t)gw * scr.cap;
-  float* L_z = scr.z + (int64_t)gw * scr.cap;
+  int2* L_iz = scr.iz + (int64_t)gw * scr.cap;
   double* L_e = scr.e + (int64_t)gw * scr.cap;
 
   for (;;) {
@@ -1741,6 +1742,7 @@ rowwarp_kernel(const char* __restrict__ rows, int64_t row_bytes, int Vdef, const
 
       bool big = false;
       unsigned long long kcut = 0ull;
+      int cut = -1;
       if (tv.trunc && tv.topp < 1.0) {
         const double pmax_lo = (1.0 / (S + E_S)) * (1.0 - relRef);
         if (pmax_lo > tv.topp) {  // nucleus = {first argmax}
@@ -1825,8 +1827,7 @@ rowwarp_kernel(const char* __restrict__ rows, int64_t row_bytes, int Vdef, const
               for (int j = 0; j < 8; ++j)
                 if ((lm >> j) & 1u) {
                   if (pos < scr.cap) {
-                    L_id[pos] = (e0 + j) | (((bm >> j) & 1u) ? 0x80000000 : 0);
-                    L_z[pos] = v[j];
+                    L_iz[pos] = make_int2((e0 + j) | (((bm >> j) & 1u) ? 0x80000000 : 0), __float_as_int(v[j]));
                   } else {
                     ovf = 1;
                   }
@@ -1850,14 +1851,25 @@ rowwarp_kernel(const char* __restrict__ rows, int64_t row_bytes, int Vdef, const
             if (__any_sync(0xffffffffu, ovf) || nb > RW_CAND || nl > scr.cap) {
               big_state = -1;
             } else {
-              // fp64-lite e of the list (dense); mass above the bracket
+              // fp64-lite e of the list (dense, one 32-entry chunk per step); per-chunk mass
+              // above the bracket (bracket members are added after the cut) and its total
               double acc = 0.0;
-              for (int i = lane; i < nl; i += 32) {
-                const double e = lite_exp(ec, L_z[i], smem.t16);
-                L_e[i] = e;
-                if (L_id[i] >= 0) acc += e;
+              const int nch = (nl + 31) / 32;
+              for (int c = 0; c < nch; ++c) {
+                const int i = c * 32 + lane;
+                double e = 0.0, ea = 0.0;
+                if (i < nl) {
+                  const int2 iz = L_iz[i];
+                  e = lite_exp(ec, __int_as_float(iz.y), smem.t16);
+                  L_e[i] = e;
+                  ea = iz.x >= 0 ? e : 0.0;
+                }
+                const double cs = warp_sum(ea);
+                if (lane == 0 && c < RW_NCH) sw.chunk_above[c] = cs;
+                acc += ea;
               }
               Mab = warp_sum(acc);
+              if (nch > RW_NCH) big_state = -1;
               // rank sort of the bracket keys (z desc, id asc) through ce[] as scratch
               unsigned long long* tmpk = reinterpret_cast<unsigned long long*>(sw.ce);
               for (int i = lane; i < nb; i += 32) {
@@ -1883,7 +1895,7 @@ rowwarp_kernel(const char* __restrict__ rows, int64_t row_bytes, int Vdef, const
         }
         // cut inside the bracket: csum (precise e's) from the mass above it
         const double EMab = Mab * relLite;
-        int cut = -1;
+        cut = -1;
         bool unc = Mab >= P - tv.topp * E_S - EMab;  // the cut would lie above the bracket
         double off = Mab;
         for (int i0 = 0; i0 < nb && !unc; i0 += 32) {
@@ -1924,31 +1936,22 @@ rowwarp_kernel(const char* __restrict__ rows, int64_t row_bytes, int Vdef, const
       int need = 0;
       if (big) {
         // ---------------- draws over the kept list (precise e's, id order)
-        // mask the bracket members beyond the cut in place and build 32-entry chunk sums
-        // (sw.ce is free after the cut); each lane then locates one target on its own
-        double* csum = sw.ce;
+        // chunk sums = mass above the bracket + the kept bracket members (located by binary
+        // search on the id-ordered list); each lane then locates one target on its own
+        double* csum = sw.chunk_tot;
         const int nch = (nl + 31) / 32;
-        if (nch > RW_CAND) {
-          need = 1;
-        } else {
-          for (int c0 = 0; c0 < nch; c0 += 4) {
-            double part[4];
-#pragma unroll
-            for (int q = 0; q < 4; ++q) {
-              const int i = (c0 + q) * 32 + lane;
-              double e = 0.0;
-              if (c0 + q < nch && i < nl) {
-                const int idf = L_id[i];
-                e = L_e[i];
-                if (idf < 0 && cand_key(L_z[i], idf & 0x7fffffff) < kcut) e = 0.0;
-              }
-              part[q] = e;
+        {
+          for (int c = lane; c < nch; c += 32) csum[c] = sw.chunk_above[c];
+          __syncwarp();
+          for (int b = lane; b <= cut; b += 32) {
+            const int id = cand_id(sw.cand[b]);
+            int lo = 0, hi = nl;
+            while (lo < hi) {
+              const int mid = (lo + hi) >> 1;
+              if ((L_iz[mid].x & 0x7fffffff) < id) lo = mid + 1;
+              else hi = mid;
             }
-#pragma unroll
-            for (int q = 0; q < 4; ++q) {
-              const double t2 = warp_sum(part[q]);
-              if (lane == 0 && c0 + q < nch) csum[c0 + q] = t2;
-            }
+            if (lo < nl) atomicAdd(&csum[lo / 32], L_e[lo]);
           }
           __syncwarp();
           if (lane == 0) {  // exclusive prefix over chunks (sequential: exact order)
@@ -1978,9 +1981,10 @@ rowwarp_kernel(const char* __restrict__ rows, int64_t row_bytes, int Vdef, const
               double c = csum[lo];
               const int i0 = lo * 32, i1 = min(nl, i0 + 32);
               for (int i = i0; i < i1; ++i) {
-                const int idf = L_id[i];
+                const int2 iz = L_iz[i];
+                const int idf = iz.x;
                 double e = L_e[i];
-                if (idf < 0 && cand_key(L_z[i], idf & 0x7fffffff) < kcut) e = 0.0;  // beyond the cut
+                if (idf < 0 && cand_key(__int_as_float(iz.y), idf & 0x7fffffff) < kcut) e = 0.0;  // beyond the cut
                 const double nc = c + e;
                 if (e > 0.0 && tk < nc) {
                   found = idf & 0x7fffffff;
@@ -2430,7 +2434,10 @@ constexpr int kExactCtas = 32;
 
 static int grid_ctas() { return num_sms() * RS_MIN_BLOCKS; }
 
-static int rw_cap(int64_t V) { return (int)((V / 5 + 256 + 31) & ~31ll); }
+static int rw_cap(int64_t V) {
+  const int64_t c = (V / 5 + 256 + 31) & ~31ll;
+  return (int)(c < RW_NCH * 32 ? c : RW_NCH * 32);
+}
 
 int64_t workspace_bytes(int64_t n_tasks, int64_t vocab) {
   const int64_t grid = grid_ctas();
@@ -2469,8 +2476,7 @@ static int launch_all(const char* rows, int64_t row_bytes, int V, const lc_task*
   RwScratch rs;
   rs.cap = rw_cap(V);
   const int64_t rw_warps = (int64_t)num_sms() * 3 * RW_WARPS;
-  rs.id = (int*)take(rw_warps * rs.cap * 4);
-  rs.z = (float*)take(rw_warps * rs.cap * 4);
+  rs.iz = (int2*)take(rw_warps * rs.cap * 8);
   rs.e = (double*)take(rw_warps * rs.cap * 8);
   int* rw_next = (int*)take(256);
   if (!d_ws || p - (char*)d_ws > ws_bytes) {
