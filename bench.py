@@ -118,7 +118,8 @@ def setup_workload(cfg, dev, rank, world=1):
     cache = lcb.LogitsCache(budget, vocab=V, dtype=cfg["dtype"], key_capacity=n_req + 64, page_rows=min(R, 16),
                             max_rows=R, device=dev)
     # prompts: one per request (tree root), digests from the GPU hasher
-    prompts = [[(rank * 7919 + r * 31 + i) % 256 for i in range(49 + r % 32)] for r in range(n_req)]
+    prompts = [[rank % 256, r % 256, r // 256] + [(rank * 7919 + r * 31 + i) % 256 for i in range(46 + r % 32)]
+               for r in range(n_req)]  # unique per (rank, request)
     digests = lcb.hash_prompts(prompts, dev=dev)
     # synthetic rows from the reference producer (model seed 7, conc 2.5, range 5), per request chunk
     chunk = max(1, (1 << 30) // (R * V * (2 if bf16 else 4)))
