@@ -1387,131 +1387,122 @@ __device__ FusedOut rw_fused_pass(const char* row, int V, int nseg, bool vec, in
   bool nan = false;
   const float eta = (float)(ACC ? (kEx2RelErr + kCorrErr + kSum8Err) : (kEx2Raw + kSum8Err)) * 1.0001f;
   const float ka = (float)kArgRel * 1.0001f;
-  // software pipeline: batch b+1's raw vectors are in flight while batch b is computed
-  constexpr int B = (DT == LC_BF16) ? 4 : 2;  // vectors per batch (64 B per lane)
-  constexpr int NW = (DT == LC_BF16) ? 1 : 2;  // uint4 per vector
-  constexpr int BPS = RW_SEGSTEPS / B;         // batches per segment
-  const int nbt = nseg * BPS;
-  uint4 cur[B][NW], nxt[B][NW];
-  auto fetch = [&](uint4 (&buf)[B][NW], int bi) {
-    const int s = bi / BPS, st = (bi % BPS) * B;
-#pragma unroll
-    for (int u = 0; u < B; ++u) {
-      const int e0 = s * RW_SEG + 256 * (st + u) + 8 * lane;
-      if (vec && e0 + 8 <= V) {
-#pragma unroll
-        for (int w2 = 0; w2 < NW; ++w2)
-          buf[u][w2] = __ldg(reinterpret_cast<const uint4*>(row + (size_t)e0 * (DT == LC_BF16 ? 2 : 4)) + w2);
-      }
-    }
-  };
-  double acc = 0.0;
-  float W = 0.0f, R = 0.0f;  // |a|-weighted mass (CHEAP) and rescale error, relative to mt
-  if (nbt > 0) fetch(cur, 0);
+  for (int s = 0; s < nseg; ++s) {
+    double acc = 0.0;
+    float W = 0.0f, R = 0.0f;  // |a|-weighted mass (CHEAP) and rescale error, relative to mt
+    constexpr int UNRF = (DT == LC_BF16) ? 8 : 4;  // 128 B per lane in flight
 #pragma unroll 1
-  for (int bi = 0; bi < nbt; ++bi) {
-    if (bi + 1 < nbt) fetch(nxt, bi + 1);
-    const int s = bi / BPS, st = (bi % BPS) * B;
+    for (int st = 0; st < RW_SEGSTEPS; st += UNRF) {
+      // raw vector loads first (memory-level parallelism), unpacked one vector at a time
+      uint4 raw[UNRF][DT == LC_BF16 ? 1 : 2];
+      bool full[UNRF];
 #pragma unroll
-    for (int u = 0; u < B; ++u) {
-      const int e0 = s * RW_SEG + 256 * (st + u) + 8 * lane;
-      float vu[8];
-      if (vec && e0 + 8 <= V) {
-        if (DT == LC_BF16) {
-          const uint32_t w[4] = {cur[u][0].x, cur[u][0].y, cur[u][0].z, cur[u][0].w};
+      for (int u = 0; u < UNRF; ++u) {
+        const int e0 = s * RW_SEG + 256 * (st + u) + 8 * lane;
+        full[u] = vec && e0 + 8 <= V;
+        if (full[u]) {
+          if (DT == LC_BF16) {
+            raw[u][0] = __ldg(reinterpret_cast<const uint4*>(reinterpret_cast<const uint16_t*>(row) + e0));
+          } else {
+            raw[u][0] = __ldg(reinterpret_cast<const uint4*>(reinterpret_cast<const float*>(row) + e0));
+            raw[u][DT == LC_BF16 ? 0 : 1] =
+                __ldg(reinterpret_cast<const uint4*>(reinterpret_cast<const float*>(row) + e0 + 4));
+          }
+        }
+      }
 #pragma unroll
-          for (int j = 0; j < 4; ++j) {
-            vu[2 * j] = __uint_as_float(w[j] << 16);
-            vu[2 * j + 1] = __uint_as_float(w[j] & 0xffff0000u);
+      for (int u = 0; u < UNRF; ++u) {
+        const int e0 = s * RW_SEG + 256 * (st + u) + 8 * lane;
+        float vv[8];
+        if (full[u]) {
+          if (DT == LC_BF16) {
+            const uint32_t w[4] = {raw[u][0].x, raw[u][0].y, raw[u][0].z, raw[u][0].w};
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+              vv[2 * j] = __uint_as_float(w[j] << 16);
+              vv[2 * j + 1] = __uint_as_float(w[j] & 0xffff0000u);
+            }
+          } else {
+            const uint4 a = raw[u][0], b = raw[u][DT == LC_BF16 ? 0 : 1];
+            vv[0] = __uint_as_float(a.x); vv[1] = __uint_as_float(a.y);
+            vv[2] = __uint_as_float(a.z); vv[3] = __uint_as_float(a.w);
+            vv[4] = __uint_as_float(b.x); vv[5] = __uint_as_float(b.y);
+            vv[6] = __uint_as_float(b.z); vv[7] = __uint_as_float(b.w);
           }
         } else {
-          const uint4 a = cur[u][0], b = cur[u][NW - 1];
-          vu[0] = __uint_as_float(a.x); vu[1] = __uint_as_float(a.y);
-          vu[2] = __uint_as_float(a.z); vu[3] = __uint_as_float(a.w);
-          vu[4] = __uint_as_float(b.x); vu[5] = __uint_as_float(b.y);
-          vu[6] = __uint_as_float(b.z); vu[7] = __uint_as_float(b.w);
+          load8<DT>(row, e0, V, vec, vv);
         }
-      } else {
-        load8<DT>(row, e0, V, vec, vu);
-      }
-      const float vmax = max_nan(max_nan(max_nan(vu[0], vu[1]), max_nan(vu[2], vu[3])),
-                                 max_nan(max_nan(vu[4], vu[5]), max_nan(vu[6], vu[7])));
-      float vmin = INFINITY;
+        float (&vu)[8] = vv;
+        const float vmax = max_nan(max_nan(max_nan(vu[0], vu[1]), max_nan(vu[2], vu[3])),
+                                   max_nan(max_nan(vu[4], vu[5]), max_nan(vu[6], vu[7])));
+        float vmin = INFINITY;
 #pragma unroll
-      for (int j = 0; j < 8; ++j)
-        if (e0 + j < V) vmin = fminf(vmin, vu[j]);
-      tmin = fminf(tmin, vmin);
-      nan |= (vmax != vmax);
-      if (vmax > mt) {
-        if (acc > 0.0) {  // rescale the partials to the new maximum
-          const float da = (mt - vmax) * Lhi;
-          float f;
+        for (int j = 0; j < 8; ++j)
+          if (e0 + j < V) vmin = fminf(vmin, vu[j]);
+        tmin = fminf(tmin, vmin);
+        nan |= (vmax != vmax);
+        if (vmax > mt) {
+          if (acc > 0.0) {  // rescale the partials to the new maximum
+            const float da = (mt - vmax) * Lhi;
+            float f;
+            if (ACC) {
+              ExpCtx c2;
+              c2.m = vmax;
+              c2.Lhi = Lhi;
+              c2.Llo = Llo;
+              f = fast_exp(c2, mt);
+            } else {
+              f = ex2_approx(da);
+            }
+            const float epsf = eta + (ACC ? 0.0f : ka * -da);
+            R = (R + (float)acc * epsf) * f;
+            W *= f;
+            acc *= (double)f;
+          }
+          mt = vmax;
+          tpos = e0;
+        }
+        float ef[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
           if (ACC) {
             ExpCtx c2;
-            c2.m = vmax;
+            c2.m = mt;
             c2.Lhi = Lhi;
             c2.Llo = Llo;
-            f = fast_exp(c2, mt);
+            ef[j] = fast_exp(c2, vu[j]);
           } else {
-            f = ex2_approx(da);
+            const float a = fmaxf((vu[j] - mt) * Lhi, -200.0f);
+            ef[j] = ex2_approx(a);
+            W = fmaf(ef[j], -a, W);
           }
-          const float epsf = eta + (ACC ? 0.0f : ka * -da);
-          R = (R + (float)acc * epsf) * f;
-          W *= f;
-          acc *= (double)f;
         }
-        mt = vmax;
-        tpos = e0;
+        acc += (double)(((ef[0] + ef[1]) + (ef[2] + ef[3])) + ((ef[4] + ef[5]) + (ef[6] + ef[7])));
       }
-      float ef[8];
-#pragma unroll
-      for (int j = 0; j < 8; ++j) {
-        if (ACC) {
-          ExpCtx c2;
-          c2.m = mt;
-          c2.Lhi = Lhi;
-          c2.Llo = Llo;
-          ef[j] = fast_exp(c2, vu[j]);
-        } else {
-          const float a = fmaxf((vu[j] - mt) * Lhi, -200.0f);
-          ef[j] = ex2_approx(a);
-          W = fmaf(ef[j], -a, W);
-        }
-      }
-      acc += (double)(((ef[0] + ef[1]) + (ef[2] + ef[3])) + ((ef[4] + ef[5]) + (ef[6] + ef[7])));
     }
-    if ((bi + 1) % BPS == 0) {
-      // segment end: combine at the warp's running maximum
-      const float ms = warp_max(mt);
-      float g = 1.0f, epsg = 0.0f;
-      if (mt < ms && acc > 0.0) {
-        const float da = (mt - ms) * Lhi;
-        if (ACC) {
-          ExpCtx c2;
-          c2.m = ms;
-          c2.Lhi = Lhi;
-          c2.Llo = Llo;
-          g = fast_exp(c2, mt);
-        } else {
-          g = ex2_approx(da);
-        }
-        epsg = eta + (ACC ? 0.0f : ka * -da);
+    // segment end: combine at the warp's running maximum
+    const float ms = warp_max(mt);
+    float g = 1.0f, epsg = 0.0f;
+    if (mt < ms && acc > 0.0) {
+      const float da = (mt - ms) * Lhi;
+      if (ACC) {
+        ExpCtx c2;
+        c2.m = ms;
+        c2.Lhi = Lhi;
+        c2.Llo = Llo;
+        g = fast_exp(c2, mt);
+      } else {
+        g = ex2_approx(da);
       }
-      const double sa = warp_sum(acc * (double)g);
-      const double sE = warp_sum((double)g * (acc * (double)(eta + epsg) + (double)R + (double)(ka * W)));
-      if (lane == 0) {
-        sw.seg[s] = sa;
-        sw.segE[s] = sE;
-        sw.segm[s] = ms;
-      }
-      acc = 0.0;
-      W = 0.0f;
-      R = 0.0f;
+      epsg = eta + (ACC ? 0.0f : ka * -da);
     }
-#pragma unroll
-    for (int u = 0; u < B; ++u)
-#pragma unroll
-      for (int w2 = 0; w2 < NW; ++w2) cur[u][w2] = nxt[u][w2];
+    const double sa = warp_sum(acc * (double)g);
+    const double sE = warp_sum((double)g * (acc * (double)(eta + epsg) + (double)R + (double)(ka * W)));
+    if (lane == 0) {
+      sw.seg[s] = sa;
+      sw.segE[s] = sE;
+      sw.segm[s] = ms;
+    }
   }
   __syncwarp();
   o.tmax = mt;
