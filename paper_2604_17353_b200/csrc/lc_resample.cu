@@ -1326,9 +1326,9 @@ resample_kernel(const char* __restrict__ rows, int64_t row_bytes, int Vdef, cons
 constexpr int RW_THREADS = 256;
 constexpr int RW_WARPS = RW_THREADS / 32;
 constexpr int RW_MIN_BLOCKS = 2;
-constexpr int RW_CAND = 512;      // bracket candidates per warp
-constexpr int RW_NB = 256;        // histogram bins: 8 per octave over 32 octaves (+ catch-all)
-constexpr float RW_BPO = 8.0f;
+constexpr int RW_CAND = 256;      // bracket candidates per warp
+constexpr int RW_NB = 1024;       // histogram bins: 32 per octave over 32 octaves (+ catch-all)
+constexpr float RW_BPO = 32.0f;
 constexpr int RW_SEGSTEPS = 8;    // 8 x 256 ids = 2048 per segment
 constexpr int RW_SEG = 256 * RW_SEGSTEPS;
 constexpr int RW_MAXV = 65536;
@@ -1338,11 +1338,15 @@ constexpr int RW_NCH = 256;                // kept-list chunks of 32 entries per
 struct __align__(16) RwWarp {
   unsigned long long cand[RW_CAND];
   double ce[RW_CAND];
-  uint32_t hist[RW_NB];
+  union {
+    uint32_t hist[RW_NB];  // big nucleus: histogram (dead once the bracket is known)
+    struct {
+      double chunk_above[RW_NCH];    // kept list: per-32-entry mass above the bracket
+      double chunk_tot[RW_NCH + 1];  // kept list: per-chunk kept mass, then exclusive prefix
+    };
+  };
   double seg[RW_NSEG + 1];  // segment masses, then exclusive prefix
   double segE[RW_NSEG];     // fused pass: per-segment absolute error bound
-  double chunk_above[RW_NCH];    // kept list: per-32-entry mass above the bracket
-  double chunk_tot[RW_NCH + 1];  // kept list: per-chunk kept mass, then exclusive prefix
   float segm[RW_NSEG];      // fused pass: the warp's running max at the segment end
   double dsc[4];
   int isc[4];
@@ -1351,17 +1355,30 @@ struct __align__(16) RwWarp {
 struct __align__(16) RwSmem {
   RwWarp w[RW_WARPS];
   double t16[16];
-  float f8[8];  // 2^(j/8)
 };
 
-__device__ __forceinline__ int rw_bin(const ExpCtx& c, float a) {
+__device__ __forceinline__ int rw_bin(float a) {
   // a = log2 distance below the max (<= 0)
   return min((int)(-a * RW_BPO), RW_NB - 1);
 }
 
-// 2^(b/8) as fp32 (relative error <= 2^-24)
-__device__ __forceinline__ float rw_scale(int b, const float* f8) {
-  return __int_as_float(((b >> 3) + 127) << 23) * f8[b & 7];
+// the histogram's bin of z: monotone non-increasing in z
+__device__ __forceinline__ int rw_zbin(const ExpCtx& c, float z) {
+  return rw_bin(fmaxf((z - c.m) * c.Lhi, -200.0f));
+}
+
+// smallest z with rw_zbin(z) <= B, for 0 <= B < RW_NB - 1 (bisection over the
+// ordered fp32 keys; rw_zbin(m) = 0, rw_zbin(-inf) = RW_NB - 1); +inf for B < 0
+__device__ __forceinline__ float rw_zthr(const ExpCtx& c, int B) {
+  if (B < 0) return INFINITY;
+  auto key2f = [](uint32_t k) { return __uint_as_float((k & 0x80000000u) ? (k & 0x7fffffffu) : ~k); };
+  uint32_t lo = f32_order_key(-INFINITY), hi = f32_order_key(c.m);
+  while (hi - lo > 1u) {
+    const uint32_t mid = lo + ((hi - lo) >> 1);
+    if (rw_zbin(c, key2f(mid)) <= B) hi = mid;
+    else lo = mid;
+  }
+  return key2f(hi);
 }
 
 struct FusedOut {
@@ -1379,7 +1396,7 @@ struct FusedOut {
 // largest per-segment relative bound (for prefix sums), with seg[] relative to
 // the row max.  ACC selects the corrected exponential (untruncated rows).
 template <int DT, bool ACC>
-__device__ FusedOut rw_fused_pass(const char* row, int V, int nseg, bool vec, int lane, float Lhi, float Llo,
+__device__ __noinline__ FusedOut rw_fused_pass(const char* row, int V, int nseg, bool vec, int lane, float Lhi, float Llo,
                                   double Ld, RwWarp& sw) {
   FusedOut o;
   float mt = -INFINITY, tmin = INFINITY;
@@ -1547,19 +1564,12 @@ __device__ __forceinline__ double rw_e(const ExpCtx& ec, float z, const double* 
   }
 }
 
-__device__ __forceinline__ bool rw_keep(const ExpCtx& ec, float z, int id, int blo, int bhi,
-                                        unsigned long long kcut) {
-  const float a = fmaxf((z - ec.m) * ec.Lhi, -200.0f);
-  const int b = rw_bin(ec, a);
-  return b < blo || (b <= bhi && cand_key(z, id) >= kcut);
-}
-
-// One pass over the row; seg[s] = sum of e over the segment's ids (passing the
-// kept predicate when KEEP); returns the |a|-weighted W (CHEAP only).  FAST
-// variants sum 8 values in fp32 pairs then in fp64 (matched by the rescan).
-template <int DT, int EM, bool KEEP>
+// One pass over the row; seg[s] = sum of e over the segment's ids; returns the
+// |a|-weighted W (CHEAP only).  FAST variants sum 8 values in fp32 pairs then in
+// fp64 (matched by the rescan).
+template <int DT, int EM>
 __device__ double rw_seg_pass(const char* row, int V, int nseg, bool vec, int lane, const ExpCtx& ec,
-                              const double* t16, double* seg, int blo, int bhi, unsigned long long kcut) {
+                              const double* t16, double* seg) {
   float Wl = 0.0f;
   for (int s = 0; s < nseg; ++s) {
     double acc = 0.0;
@@ -1574,11 +1584,7 @@ __device__ double rw_seg_pass(const char* row, int V, int nseg, bool vec, int la
 #pragma unroll
       for (int j = 0; j < 8; ++j) {
         float aw;
-        double e = rw_e<EM>(ec, v[j], t16, aw);
-        if (KEEP && !rw_keep(ec, v[j], e0 + j, blo, bhi, kcut)) {
-          e = 0.0;
-          aw = 0.0f;
-        }
+        const double e = rw_e<EM>(ec, v[j], t16, aw);
         if (EM == 2) e8 += e;
         else ef[j] = (float)e;
         Wl += aw;
@@ -1610,7 +1616,6 @@ rowwarp_kernel(const char* __restrict__ rows, int64_t row_bytes, int Vdef, const
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   RwWarp& sw = smem.w[wid];
   if (threadIdx.x < 16) smem.t16[threadIdx.x] = exp2((double)threadIdx.x / 16.0);
-  if (threadIdx.x < 8) smem.f8[threadIdx.x] = exp2f((float)threadIdx.x / 8.0f);
   if (lane == 0) sw.isc[0] = 0;
   __syncthreads();
   const int gw = blockIdx.x * RW_WARPS + wid;
@@ -1714,11 +1719,6 @@ rowwarp_kernel(const char* __restrict__ rows, int64_t row_bytes, int Vdef, const
     const double relLite = kLiteErr + 2.0 * kRefExpErr + relArg + (double)(V + 16) * kEps64;
 
     // ---------------- phase B: segment masses (+ |a|-weighted bound for the cheap exp)
-    auto seg_pass = [&](bool precise) -> double {
-      if (precise) return rw_seg_pass<DT, 2, false>(tv.row, V, nseg, vec, lane, ec, smem.t16, sw.seg, 0, 0, 0ull);
-      if (accurate) return rw_seg_pass<DT, 1, false>(tv.row, V, nseg, vec, lane, ec, smem.t16, sw.seg, 0, 0, 0ull);
-      return rw_seg_pass<DT, 0, false>(tv.row, V, nseg, vec, lane, ec, smem.t16, sw.seg, 0, 0, 0ull);
-    };
     bool done = false, to_exact = !sane;
     int big_state = 0;  // 0 not built, 1 built, -1 failed
     int blo = 0, bhi = 0, nb = 0, nl = 0;
@@ -1729,7 +1729,7 @@ rowwarp_kernel(const char* __restrict__ rows, int64_t row_bytes, int Vdef, const
       const uint8_t tier_flag = precise ? LC_DRAW_PRECISE : 0;
       if (precise) {
         if (lane == 0) atomicAdd(&counters[0], 1ull);
-        seg_pass(true);
+        rw_seg_pass<DT, 2>(tv.row, V, nseg, vec, lane, ec, smem.t16, sw.seg);
       }
       double S = 0.0;
       for (int s = 0; s < nseg; ++s) S += sw.seg[s];
@@ -1752,7 +1752,8 @@ rowwarp_kernel(const char* __restrict__ rows, int64_t row_bytes, int Vdef, const
         }
         const double P = tv.topp * S;
         if (big_state == 0) {
-          // histogram: per-bin relative fixed point (bin b holds e in (2^-(b+1)/8, 2^-b/8])
+          // histogram: per-bin relative fixed point (bin b holds e in (2^-(b+1)/32, 2^-b/32]);
+          // q = e * 2^(b/32) = ex2(a + b/32), the sum exact (a and -b/32 within a factor 2)
           for (int i = lane; i < RW_NB; i += 32) sw.hist[i] = 0u;
           __syncwarp();
           const int lgV = 32 - __clz(V + 1);
@@ -1765,11 +1766,10 @@ rowwarp_kernel(const char* __restrict__ rows, int64_t row_bytes, int Vdef, const
             for (int u2 = 0; u2 < 2; ++u2)
 #pragma unroll
               for (int j = 0; j < 8; ++j) {
-                float a;
-                const float e = cheap_exp(ec, v[u2][j], a);
-                const int b = rw_bin(ec, a);
-                if (e > 0.0f)
-                  atomicAdd(&sw.hist[b], __float2uint_rn(fminf(e * rw_scale(b, smem.f8), 1.0f) * qscale));
+                const float a = fmaxf((v[u2][j] - ec.m) * ec.Lhi, -200.0f);
+                const int b = rw_bin(a);
+                const uint32_t q = __float2uint_rn(ex2_approx(fmaf((float)b, 1.0f / RW_BPO, a)) * qscale);
+                if (q) atomicAdd(&sw.hist[b], q);
               }
           }
           __syncwarp();
@@ -1782,7 +1782,7 @@ rowwarp_kernel(const char* __restrict__ rows, int64_t row_bytes, int Vdef, const
           bhi = RW_NB - 1;
           bool got_lo = false;
           for (int b0 = 0; b0 < RW_NB; b0 += 32) {
-            const double hb = (double)sw.hist[b0 + lane] * inv * exp2(-(double)(b0 + lane) / 8.0);
+            const double hb = (double)sw.hist[b0 + lane] * inv * exp2(-(double)(b0 + lane) / (double)RW_BPO);
             const double incl = cum + warp_incl_scan(hb);
             const unsigned lo_m = __ballot_sync(0xffffffffu, incl >= P - qerr);
             const unsigned hi_m = __ballot_sync(0xffffffffu, incl >= P + qerr);
@@ -1799,7 +1799,10 @@ rowwarp_kernel(const char* __restrict__ rows, int64_t row_bytes, int Vdef, const
           big_state = (bhi >= RW_NB - 1) ? -1 : 1;  // a cut in the catch-all bin -> EXACT
           if (big_state > 0) {
             // kept list: ids with bin <= bhi in id order (bracket members flagged); bracket
-            // keys also go to the smem candidate list for the exact sort
+            // keys also go to the smem candidate list for the exact sort.  Bins are
+            // monotone in z: bin <= bhi <=> z >= zhi, bin < blo <=> z >= zab.
+            const float zhi = rw_zthr(ec, bhi), zab = rw_zthr(ec, blo - 1);
+            __syncwarp();
             int wn = 0, ovf = 0;
             for (int base = 0; base < V; base += 256) {
               const int e0 = base + 8 * lane;
@@ -1808,11 +1811,9 @@ rowwarp_kernel(const char* __restrict__ rows, int64_t row_bytes, int Vdef, const
               unsigned lm = 0, bm = 0;
 #pragma unroll
               for (int j = 0; j < 8; ++j) {
-                const float a = fmaxf((v[j] - ec.m) * ec.Lhi, -200.0f);
-                const int b = rw_bin(ec, a);
-                if (b <= bhi && e0 + j < V) {
+                if (v[j] >= zhi) {  // ids >= V read as -inf
                   lm |= 1u << j;
-                  if (b >= blo) bm |= 1u << j;
+                  if (v[j] < zab) bm |= 1u << j;
                 }
               }
               const int c = __popc(lm);
@@ -1854,21 +1855,29 @@ rowwarp_kernel(const char* __restrict__ rows, int64_t row_bytes, int Vdef, const
               // above the bracket (bracket members are added after the cut) and its total
               double acc = 0.0;
               const int nch = (nl + 31) / 32;
-              for (int c = 0; c < nch; ++c) {
-                const int i = c * 32 + lane;
-                double e = 0.0, ea = 0.0;
-                if (i < nl) {
-                  const int2 iz = L_iz[i];
-                  e = lite_exp(ec, __int_as_float(iz.y), smem.t16);
-                  L_e[i] = e;
-                  ea = iz.x >= 0 ? e : 0.0;
+              if (nch > RW_NCH) big_state = -1;
+              for (int c = 0; c < nch && big_state > 0; c += 2) {  // two chunks in flight
+                const int i0 = c * 32 + lane, i1 = i0 + 32;
+                const int2 iz0 = i0 < nl ? L_iz[i0] : make_int2(0, __float_as_int(-INFINITY));
+                const int2 iz1 = i1 < nl ? L_iz[i1] : make_int2(0, __float_as_int(-INFINITY));
+                const double e0 = lite_exp(ec, __int_as_float(iz0.y), smem.t16);
+                const double e1 = lite_exp(ec, __int_as_float(iz1.y), smem.t16);
+                if (i0 < nl) L_e[i0] = e0;
+                if (i1 < nl) L_e[i1] = e1;
+                const double ea0 = iz0.x >= 0 ? e0 : 0.0, ea1 = iz1.x >= 0 ? e1 : 0.0;
+                double cs0 = ea0, cs1 = ea1;
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) {
+                  cs0 += __shfl_xor_sync(0xffffffffu, cs0, o);
+                  cs1 += __shfl_xor_sync(0xffffffffu, cs1, o);
                 }
-                const double cs = warp_sum(ea);
-                if (lane == 0 && c < RW_NCH) sw.chunk_above[c] = cs;
-                acc += ea;
+                if (lane == 0) {
+                  sw.chunk_above[c] = cs0;
+                  if (c + 1 < nch) sw.chunk_above[c + 1] = cs1;
+                }
+                acc += ea0 + ea1;
               }
               Mab = warp_sum(acc);
-              if (nch > RW_NCH) big_state = -1;
               // rank sort of the bracket keys (z desc, id asc) through ce[] as scratch
               unsigned long long* tmpk = reinterpret_cast<unsigned long long*>(sw.ce);
               for (int i = lane; i < nb; i += 32) {

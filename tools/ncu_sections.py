@@ -41,7 +41,7 @@ for r in rows:
         wi = hdr.index("Warp Stall Sampling (All Samples)")
         ii = hdr.index("Instructions Executed")
         continue
-    if hdr is None or len(r) < len(hdr) or not r[0].isdigit() or "rowwarp_kernel" not in (func or ""):
+    if hdr is None or len(r) < len(hdr) or not r[0].isdigit() or "rowwarp" not in (func or ""):
         continue
     key = section(int(r[0])) if fn == "lc_resample.cu" else "lib:" + fn
     a = agg.setdefault(key, [0, 0])
