@@ -263,11 +263,11 @@ def run_ours(args, cfg, rank, world, dev):
     from paper_2604_17353_b200.shard import reduce_stats
 
     times = torch.tensor([ms, e2e_ms], dtype=torch.float64, device=dev)
-    counts = torch.tensor([float(accepted), float(cnt[0]), float(cnt[1]), float(cnt[2])], dtype=torch.float64,
-                          device=dev)
+    counts = torch.tensor([float(accepted), float(cnt[0]), float(cnt[1]), float(cnt[2]), float(cnt[3])],
+                          dtype=torch.float64, device=dev)
     times, counts = reduce_stats(times, counts, world)  # NCCL: max of times, sum of counters
     ms, e2e_ms = float(times[0]), float(times[1])
-    accepted, precise, unresolved, bad = (int(x) for x in counts.tolist())
+    accepted, precise, unresolved, bad, exact = (int(x) for x in counts.tolist())
     if rank != 0:
         return None
     tokens_total = (n_draws * args.steps * world if cfg["scaling"] == "weak"
@@ -297,11 +297,12 @@ def run_ours(args, cfg, rank, world, dev):
         "rows_per_s": (n_rows * world if cfg["scaling"] == "weak" else CONFIGS[args.config]["n_req"] * R)
         * args.steps / (ms * 1e-3),
         "precise_tasks": precise,
+        "exact_tasks": exact,
         "unresolved_draws": unresolved,
         "bad_rows": bad,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": None, "peak_source": peak_src,
-                     "kernel": "lc_cache_resample (resample_kernel FAST + REFINE/EXACT queues)",
+                     "kernel": "lc_cache_resample (rowwarp_kernel + resample_kernel + exact_kernel)",
                      "kernel_ms_avg": k_avg, "algorithmic_bytes_per_launch": algo_bytes_launch},
         "e2e": {"value": tokens_total / (e2e_ms * 1e-3), "unit": "tokens/s", "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": d2h},

@@ -21,6 +21,7 @@ LIB = os.path.join(LIBDIR, "liblcb200.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "--expt-relaxed-constexpr", "-Xcompiler", "-fPIC,-O2",
+         *os.environ.get("LCB_NVCC_EXTRA", "").split(),
          "-I" + os.path.join(ROOT, "include")]
 
 

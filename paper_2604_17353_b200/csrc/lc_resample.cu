@@ -479,6 +479,7 @@ struct DrawIO {
 
 struct Workspace {
   int* q_exact;   // [0] = count, [1..] task ids
+  int* q_cta;     // tasks the row-warp kernel hands to the CTA kernel (same layout)
   int* scr_id;    // [grid][2][SCR_PER_CTA]
   double* scr_e;  // [grid][2][SCR_PER_CTA]
 };
@@ -542,13 +543,12 @@ resample_kernel(const char* __restrict__ rows, int64_t row_bytes, int Vdef, cons
   double* scrM_e = scrA_e + SCR_PER_CTA;
   if (tid < 16) sm.t16[tid] = exp2((double)tid / 16.0);
 
-  for (int task_id = blockIdx.x; task_id < n_tasks; task_id += gridDim.x) {
+  // with the row-warp kernel in front, only the tasks it queued (effective top-k)
+  const int n_mine = rw_owns ? *(volatile int*)ws.q_cta : n_tasks;
+  for (int qi = blockIdx.x; qi < n_mine; qi += gridDim.x) {
+    const int task_id = rw_owns ? ws.q_cta[1 + qi] : qi;
     const lc_task tk = tasks[task_id];
     if (tk.draw_end <= tk.draw_begin) continue;  // nothing to draw (uniform across the CTA)
-    if (rw_owns) {  // the row-per-warp kernel takes tasks without an effective top-k
-      const int Vt = tk.vocab > 0 ? tk.vocab : Vdef;
-      if (!(tk.top_k > 0 && tk.top_k < Vt)) continue;
-    }
     TaskView tv;
     __syncthreads();  // previous task's smem readers are done
     if (!resolve_task(tk, rows, row_bytes, Vdef, cm, tv)) {
@@ -1430,32 +1430,44 @@ __device__ __noinline__ FusedOut rw_fused_pass(const char* row, int V, int nseg,
 #pragma unroll
       for (int u = 0; u < UNRF; ++u) {
         const int e0 = s * RW_SEG + 256 * (st + u) + 8 * lane;
+        if (e0 >= V) continue;  // past the row (its -inf padding would make W NaN)
         float vv[8];
-        if (full[u]) {
-          if (DT == LC_BF16) {
-            const uint32_t w[4] = {raw[u][0].x, raw[u][0].y, raw[u][0].z, raw[u][0].w};
+        float vmax, vmin;
+        if (full[u] && DT == LC_BF16) {
+          // packed bf16x2 max (NaN-propagating) / min over the 8 values
+          const uint32_t w[4] = {raw[u][0].x, raw[u][0].y, raw[u][0].z, raw[u][0].w};
 #pragma unroll
-            for (int j = 0; j < 4; ++j) {
-              vv[2 * j] = __uint_as_float(w[j] << 16);
-              vv[2 * j + 1] = __uint_as_float(w[j] & 0xffff0000u);
-            }
-          } else {
+          for (int j = 0; j < 4; ++j) {
+            vv[2 * j] = __uint_as_float(w[j] << 16);
+            vv[2 * j + 1] = __uint_as_float(w[j] & 0xffff0000u);
+          }
+          uint32_t x01, x23, x, n01, n23, n;
+          asm("max.NaN.bf16x2 %0, %1, %2;" : "=r"(x01) : "r"(w[0]), "r"(w[1]));
+          asm("max.NaN.bf16x2 %0, %1, %2;" : "=r"(x23) : "r"(w[2]), "r"(w[3]));
+          asm("max.NaN.bf16x2 %0, %1, %2;" : "=r"(x) : "r"(x01), "r"(x23));
+          asm("min.bf16x2 %0, %1, %2;" : "=r"(n01) : "r"(w[0]), "r"(w[1]));
+          asm("min.bf16x2 %0, %1, %2;" : "=r"(n23) : "r"(w[2]), "r"(w[3]));
+          asm("min.bf16x2 %0, %1, %2;" : "=r"(n) : "r"(n01), "r"(n23));
+          vmax = max_nan(__uint_as_float(x << 16), __uint_as_float(x & 0xffff0000u));
+          vmin = fminf(__uint_as_float(n << 16), __uint_as_float(n & 0xffff0000u));
+        } else {
+          if (full[u]) {
             const uint4 a = raw[u][0], b = raw[u][DT == LC_BF16 ? 0 : 1];
             vv[0] = __uint_as_float(a.x); vv[1] = __uint_as_float(a.y);
             vv[2] = __uint_as_float(a.z); vv[3] = __uint_as_float(a.w);
             vv[4] = __uint_as_float(b.x); vv[5] = __uint_as_float(b.y);
             vv[6] = __uint_as_float(b.z); vv[7] = __uint_as_float(b.w);
+          } else {
+            load8<DT>(row, e0, V, vec, vv);
           }
-        } else {
-          load8<DT>(row, e0, V, vec, vv);
+          vmax = max_nan(max_nan(max_nan(vv[0], vv[1]), max_nan(vv[2], vv[3])),
+                         max_nan(max_nan(vv[4], vv[5]), max_nan(vv[6], vv[7])));
+          vmin = INFINITY;
+#pragma unroll
+          for (int j = 0; j < 8; ++j)
+            if (e0 + j < V) vmin = fminf(vmin, vv[j]);
         }
         float (&vu)[8] = vv;
-        const float vmax = max_nan(max_nan(max_nan(vu[0], vu[1]), max_nan(vu[2], vu[3])),
-                                   max_nan(max_nan(vu[4], vu[5]), max_nan(vu[6], vu[7])));
-        float vmin = INFINITY;
-#pragma unroll
-        for (int j = 0; j < 8; ++j)
-          if (e0 + j < V) vmin = fminf(vmin, vu[j]);
         tmin = fminf(tmin, vmin);
         nan |= (vmax != vmax);
         if (vmax > mt) {
@@ -1479,7 +1491,7 @@ __device__ __noinline__ FusedOut rw_fused_pass(const char* row, int V, int nseg,
           mt = vmax;
           tpos = e0;
         }
-        float ef[8];
+        float ef[8], aw[8];
 #pragma unroll
         for (int j = 0; j < 8; ++j) {
           if (ACC) {
@@ -1489,15 +1501,26 @@ __device__ __noinline__ FusedOut rw_fused_pass(const char* row, int V, int nseg,
             c2.Llo = Llo;
             ef[j] = fast_exp(c2, vu[j]);
           } else {
-            const float a = fmaxf((vu[j] - mt) * Lhi, -200.0f);
-            ef[j] = ex2_approx(a);
-            W = fmaf(ef[j], -a, W);
+            const float a = (vu[j] - mt) * Lhi;
+            ef[j] = ex2_approx(a);  // -inf -> +0
+            aw[j] = a;
           }
         }
-        acc += (double)(((ef[0] + ef[1]) + (ef[2] + ef[3])) + ((ef[4] + ef[5]) + (ef[6] + ef[7])));
+        const float s8 = ((ef[0] + ef[1]) + (ef[2] + ef[3])) + ((ef[4] + ef[5]) + (ef[6] + ef[7]));
+        if (mt > -INFINITY) {  // (all -inf so far: z - mt is NaN)
+          if (!ACC) {
+            // CHEAP: W = sum of e*|a| (NaN once a -inf is seen: replaced at the segment end)
+#pragma unroll
+            for (int j = 0; j < 8; ++j) W = fmaf(ef[j], -aw[j], W);
+          }
+          acc += (double)s8;
+        }
       }
     }
-    // segment end: combine at the warp's running maximum
+    // segment end: combine at the warp's running maximum.  A -inf element made W NaN:
+    // bound it by 150 octaves per unit of mass instead (beyond that e < 2^-150: absolute,
+    // in absE)
+    if (!ACC && W != W) W = 150.0f * (float)acc * 1.001f;
     const float ms = warp_max(mt);
     float g = 1.0f, epsg = 0.0f;
     if (mt < ms && acc > 0.0) {
@@ -1599,11 +1622,106 @@ __device__ double rw_seg_pass(const char* row, int V, int nseg, bool vec, int la
   return warp_sum((double)Wl) * 1.001;
 }
 
+// Big-nucleus histogram: bin b (1/32 octave below the max) accumulates
+// q = e * 2^(b/32) = ex2(a + b/32) in per-bin relative fixed point (the sum
+// a + b/32 is exact: a and -b/32 are within a factor 2).  Out of line: its own
+// register budget.
+template <int DT>
+__device__ __noinline__ void rw_hist_pass(const char* row, int V, bool vec, int lane, float m, float Lhi, float qscale,
+                                          uint32_t hist_s) {
+  for (int base = 0; base < V; base += 1024) {  // four vectors per lane in flight
+    float v[4][8];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) load8<DT>(row, base + 256 * u + 8 * lane, V, vec, v[u]);
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const float a = fmaxf((v[u][j] - m) * Lhi, -200.0f);
+        const int b = rw_bin(a);
+        const uint32_t q = __float2uint_rn(ex2_approx(fmaf((float)b, 1.0f / RW_BPO, a)) * qscale);
+        asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(hist_s + 4u * (uint32_t)b), "r"(q) : "memory");
+      }
+  }
+}
+
+// Big-nucleus kept list: ids with z >= zhi (bin <= bhi) in id order, bracket
+// members (z < zab) flagged in bit 31 and their keys appended to sw.cand.
+// Returns the list length (entries beyond cap are not written).
+template <int DT>
+__device__ __noinline__ int rw_list_pass(const char* row, int V, bool vec, int lane, float zhi, float zab, int2* L_iz,
+                                         int cap, RwWarp& sw, int& ovf) {
+  int wn = 0;
+  for (int base = 0; base < V && wn <= cap; base += 512) {  // two vectors per lane
+    const int e0 = base + 8 * lane, e1 = e0 + 256;
+    float v[2][8];
+    load8<DT>(row, e0, V, vec, v[0]);
+    load8<DT>(row, e1, V, vec, v[1]);
+    unsigned lm[2] = {0u, 0u}, bm[2] = {0u, 0u};
+#pragma unroll
+    for (int u = 0; u < 2; ++u)
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {  // ids >= V read as -inf
+        lm[u] |= (v[u][j] >= zhi ? 1u : 0u) << j;
+        bm[u] |= (v[u][j] >= zhi && v[u][j] < zab ? 1u : 0u) << j;
+      }
+    // both vectors' counts in one scan (16-bit halves)
+    const int c = __popc(lm[0]) | (__popc(lm[1]) << 16);
+    int incl = c;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += y;
+    }
+    const int tot = __shfl_sync(0xffffffffu, incl, 31);
+    const int t0 = tot & 0xffff;
+    const int pos0[2] = {wn + (incl & 0xffff) - (c & 0xffff), wn + t0 + (incl >> 16) - (c >> 16)};
+    if (wn + t0 + (tot >> 16) <= cap) {
+#pragma unroll
+      for (int u = 0; u < 2; ++u)
+#pragma unroll
+        for (int j = 0; j < 8; ++j)
+          if ((lm[u] >> j) & 1u)
+            L_iz[pos0[u] + __popc(lm[u] & ((1u << j) - 1u))] =
+                make_int2((u ? e1 : e0) + j + (int)(((bm[u] >> j) & 1u) << 31), __float_as_int(v[u][j]));
+    }
+    // bracket keys use the LIST POSITION instead of the id: the list is id-ordered,
+    // so (z desc, position asc) is the reference's (p desc, id asc) order
+    if (bm[0] | bm[1]) {
+      int p2 = atomicAdd(&sw.isc[0], __popc(bm[0]) + __popc(bm[1]));
+#pragma unroll
+      for (int u = 0; u < 2; ++u)
+        for (unsigned b = bm[u]; b; b &= b - 1u) {
+          const int j = __ffs(b) - 1;
+          if (p2 < RW_CAND) sw.cand[p2] = cand_key(v[u][j], pos0[u] + __popc(lm[u] & ((1u << j) - 1u)));
+          else ovf = 1;
+          ++p2;
+        }
+    }
+    wn += t0 + (tot >> 16);
+  }
+  return wn;
+}
+
+#ifdef LCB_RW_DEBUG
+// debug build only (LCB_NVCC_EXTRA=-DLCB_RW_DEBUG): per-task trace of the row-warp kernel
+__device__ double g_rw_dbg[256][12];
+#define RW_DBG(k, x) \
+  do {                                                          \
+    if (lane == 0 && task_id < 256) g_rw_dbg[task_id][k] = (double)(x); \
+  } while (0)
+#else
+#define RW_DBG(k, x) \
+  do {              \
+  } while (0)
+#endif
+
 struct RwScratch {
   int2* iz;    // [warps][cap] kept list in id order: {id | bracket-member bit 31, z bits}
   double* e;   // [warps][cap] fp64-lite e
   int cap;
   int* next;   // dynamic task counter
+  int* q_cta;  // [0] = count, [1..] task ids with an effective top-k (CTA kernel)
 };
 
 template <int DT, int MINB>
@@ -1631,7 +1749,13 @@ rowwarp_kernel(const char* __restrict__ rows, int64_t row_bytes, int Vdef, const
     const lc_task tk = tasks[task_id];
     if (tk.draw_end <= tk.draw_begin) continue;
     const int Vt = tk.vocab > 0 ? tk.vocab : Vdef;
-    if (tk.top_k > 0 && tk.top_k < Vt) continue;  // top-k: CTA kernel
+    if (tk.top_k > 0 && tk.top_k < Vt) {  // top-k: queued for the CTA kernel
+      if (lane == 0) {
+        const int pos = atomicAdd(scr.q_cta, 1);
+        scr.q_cta[1 + pos] = task_id;
+      }
+      continue;
+    }
     TaskView tv;
     if (!resolve_task(tk, rows, row_bytes, Vdef, cm, tv)) {
       for (int64_t d = tv.d0 + lane; d < tv.d1; d += 32) {
@@ -1733,6 +1857,11 @@ rowwarp_kernel(const char* __restrict__ rows, int64_t row_bytes, int Vdef, const
       }
       double S = 0.0;
       for (int s = 0; s < nseg; ++s) S += sw.seg[s];
+      RW_DBG(0, S);
+      RW_DBG(1, fo.ES);
+      RW_DBG(2, fo.relmax);
+      RW_DBG(3, ec.m);
+      RW_DBG(4, zmin);
       // FAST: the fused pass's bound (element exps, rescales, pair sums) + the reference's
       // argument/exp rounding + fp64 accumulation; PRECISE: lite_exp's
       const double relCommon = kRefExpErr + relArg + (double)(V + 16) * kEps64;
@@ -1758,20 +1887,7 @@ rowwarp_kernel(const char* __restrict__ rows, int64_t row_bytes, int Vdef, const
           __syncwarp();
           const int lgV = 32 - __clz(V + 1);
           const float qscale = ldexpf(1.0f, 31 - lgV);
-          for (int base = 0; base < V; base += 512) {
-            float v[2][8];
-            load8<DT>(tv.row, base + 8 * lane, V, vec, v[0]);
-            load8<DT>(tv.row, base + 256 + 8 * lane, V, vec, v[1]);
-#pragma unroll
-            for (int u2 = 0; u2 < 2; ++u2)
-#pragma unroll
-              for (int j = 0; j < 8; ++j) {
-                const float a = fmaxf((v[u2][j] - ec.m) * ec.Lhi, -200.0f);
-                const int b = rw_bin(a);
-                const uint32_t q = __float2uint_rn(ex2_approx(fmaf((float)b, 1.0f / RW_BPO, a)) * qscale);
-                if (q) atomicAdd(&sw.hist[b], q);
-              }
-          }
+          rw_hist_pass<DT>(tv.row, V, vec, lane, ec.m, ec.Lhi, qscale, (uint32_t)__cvta_generic_to_shared(sw.hist));
           __syncwarp();
           // bracket of bins that can hold the cut
           const double inv = 1.0 / (double)qscale;
@@ -1797,57 +1913,22 @@ rowwarp_kernel(const char* __restrict__ rows, int64_t row_bytes, int Vdef, const
             cum = __shfl_sync(0xffffffffu, incl, 31);
           }
           big_state = (bhi >= RW_NB - 1) ? -1 : 1;  // a cut in the catch-all bin -> EXACT
+          RW_DBG(5, blo);
+          RW_DBG(6, bhi);
           if (big_state > 0) {
             // kept list: ids with bin <= bhi in id order (bracket members flagged); bracket
             // keys also go to the smem candidate list for the exact sort.  Bins are
             // monotone in z: bin <= bhi <=> z >= zhi, bin < blo <=> z >= zab.
             const float zhi = rw_zthr(ec, bhi), zab = rw_zthr(ec, blo - 1);
             __syncwarp();
-            int wn = 0, ovf = 0;
-            for (int base = 0; base < V; base += 256) {
-              const int e0 = base + 8 * lane;
-              float v[8];
-              load8<DT>(tv.row, e0, V, vec, v);
-              unsigned lm = 0, bm = 0;
-#pragma unroll
-              for (int j = 0; j < 8; ++j) {
-                if (v[j] >= zhi) {  // ids >= V read as -inf
-                  lm |= 1u << j;
-                  if (v[j] < zab) bm |= 1u << j;
-                }
-              }
-              const int c = __popc(lm);
-              int incl = c;
-#pragma unroll
-              for (int o = 1; o < 32; o <<= 1) {
-                const int y = __shfl_up_sync(0xffffffffu, incl, o);
-                if (lane >= o) incl += y;
-              }
-              int pos = wn + incl - c;
-              // bracket keys use the LIST POSITION instead of the id: the list is id-ordered,
-              // so (z desc, position asc) is the reference's (p desc, id asc) order
-              int p2 = 0;
-              if (bm) p2 = atomicAdd(&sw.isc[0], __popc(bm));
-#pragma unroll
-              for (int j = 0; j < 8; ++j)
-                if ((lm >> j) & 1u) {
-                  if (pos < scr.cap) {
-                    L_iz[pos] = make_int2((e0 + j) | (((bm >> j) & 1u) ? 0x80000000 : 0), __float_as_int(v[j]));
-                  } else {
-                    ovf = 1;
-                  }
-                  if ((bm >> j) & 1u) {
-                    if (p2 < RW_CAND) sw.cand[p2] = cand_key(v[j], pos);
-                    else ovf = 1;
-                    ++p2;
-                  }
-                  ++pos;
-                }
-              wn += __shfl_sync(0xffffffffu, incl, 31);
-            }
+            int ovf = 0;
+            const int wn = rw_list_pass<DT>(tv.row, V, vec, lane, zhi, zab, L_iz, scr.cap, sw, ovf);
             __syncwarp();
             nb = sw.isc[0];
             nl = wn;
+            RW_DBG(7, nb);
+            RW_DBG(8, nl);
+            RW_DBG(9, ovf);
             if (__any_sync(0xffffffffu, ovf) || nb > RW_CAND || nl > scr.cap) {
               big_state = -1;
             } else {
@@ -2169,6 +2250,12 @@ exact_kernel(const char* __restrict__ rows, int64_t row_bytes, int Vdef, const l
   extern __shared__ __align__(16) unsigned char ex_dyn[];
   unsigned long long* s_key = reinterpret_cast<unsigned long long*>(ex_dyn);
   int* s_id = reinterpret_cast<int*>(ex_dyn + EX_CAND * 8);
+  // pairwise leaves alias the candidate arrays (never live at the same time)
+  constexpr int kLeafCap = EX_CAND / 2;
+  int2* s_lv = reinterpret_cast<int2*>(ex_dyn);
+  double* s_ls = reinterpret_cast<double*>(ex_dyn + kLeafCap * 8);
+  __shared__ double s_bc;
+  __shared__ int s_nl;
   const int tid = threadIdx.x;
   for (int ti = blockIdx.x; ti < ntask; ti += gridDim.x) {
     const int task_id = task_list[1 + ti];
@@ -2213,7 +2300,10 @@ exact_kernel(const char* __restrict__ rows, int64_t row_bytes, int Vdef, const l
     ec.mT = __ddiv_rn((double)s_m, tv.T);
     for (int i = tid; i < V; i += EX_THREADS) p[i] = ref_exp(ec, load1<DT>(tv.row, i));
     __syncthreads();
-    if (tid == 0) s_S = pairwise_seq(p, V);
+    {
+      const double S0 = pairwise_block(p, V, s_lv, s_ls, kLeafCap, &s_bc, &s_nl);
+      if (tid == 0) s_S = S0;
+    }
     __syncthreads();
     for (int i = tid; i < V; i += EX_THREADS) p[i] = __ddiv_rn(p[i], s_S);
     __syncthreads();
@@ -2226,11 +2316,15 @@ exact_kernel(const char* __restrict__ rows, int64_t row_bytes, int Vdef, const l
       // the sequential csum of the reference runs over it.
       const int lim = tv.topk > 0 ? tv.topk : V;
       unsigned long long lo = 0ull, hi = 0x3ff0000000000001ull;  // theta in [0, 1] as bits
-      for (int it = 0; it < 64 && lo + 1 < hi; ++it) {
+      // stop once C(lo) fits and holds at most ~12% more than C(hi) (which is too small)
+      int cnt_lo = V, cnt_hi = 0;
+      for (int it = 0; it < 64 && lo + 1 < hi && (cnt_lo > EX_CAND || cnt_lo - cnt_hi > max(64, cnt_lo >> 3));
+           ++it) {
         const unsigned long long mid = lo + (hi - lo) / 2;
         const double th = __longlong_as_double((long long)mid);
         double mass = 0.0;
         int cnt = 0;
+#pragma unroll 8
         for (int i = tid; i < V; i += EX_THREADS) {
           const double pi = p[i];
           if (pi >= th) {
@@ -2249,9 +2343,15 @@ exact_kernel(const char* __restrict__ rows, int64_t row_bytes, int Vdef, const l
           __syncthreads();
         }
         const bool enough = tv.topk > 0 ? (s_bi[0] >= lim) : (s_bp[0] >= tv.topp + 1e-9);
+        const int cmid = s_bi[0];
         __syncthreads();
-        if (enough) lo = mid;
-        else hi = mid;
+        if (enough) {
+          lo = mid;
+          cnt_lo = cmid;
+        } else {
+          hi = mid;
+          cnt_hi = cmid;
+        }
       }
       const double theta = __longlong_as_double((long long)lo);
       // compact C (block-wide exclusive scan of per-thread counts), keys into smem
@@ -2368,43 +2468,89 @@ exact_kernel(const char* __restrict__ rows, int64_t row_bytes, int Vdef, const l
       }
       L = n;
       __syncthreads();
-      if (tid == 0) {
-        for (int i = 0; i < L; ++i) tmp[i] = p[ord[i]];
-        double ks = pairwise_seq(tmp, L);
-        for (int i = 0; i < V; ++i) q[i] = 0.0;
-        for (int i = 0; i < L; ++i) q[ord[i]] = __ddiv_rn(tmp[i], ks);
-      }
+      for (int i = tid; i < L; i += EX_THREADS) tmp[i] = p[ord[i]];
+      for (int i = tid; i < V; i += EX_THREADS) q[i] = 0.0;
+      __syncthreads();
+      const double ks = pairwise_block(tmp, L, s_lv, s_ls, kLeafCap, &s_bc, &s_nl);
+      for (int i = tid; i < L; i += EX_THREADS) q[ord[i]] = __ddiv_rn(tmp[i], ks);
     } else {
       for (int i = tid; i < V; i += EX_THREADS) q[i] = p[i];
     }
     __syncthreads();
-    if (tid == 0) {
-      s_L = L;
-      s_S = pairwise_seq(q, V);  // total = q.sum()
+    const double Q = pairwise_block(q, V, s_lv, s_ls, kLeafCap, &s_bc, &s_nl);  // total = q.sum()
+    // sample (sampling.py:97-109): numpy's cumsum(q) is sequential in id order and
+    // only changes at nonzero q, so the nonzero entries are compacted in id order
+    // (ord = ids, tmp = running sums), summed sequentially once, and every draw
+    // binary-searches the first running sum > t
+    {
+      // coalesced tiles of EX_THREADS ids: ballot + per-warp offsets keep id order
+      const int lane = tid & 31, wid = tid >> 5;
+      int base_out = 0;
+      for (int b0 = 0; b0 < V; b0 += EX_THREADS) {
+        const int i = b0 + tid;
+        const double qi = i < V ? q[i] : 0.0;
+        const unsigned bal = __ballot_sync(0xffffffffu, qi != 0.0);
+        if (lane == 0) s_bi[wid] = __popc(bal);
+        __syncthreads();
+        int off = base_out, tot = 0;
+        for (int w = 0; w < EX_THREADS / 32; ++w) {
+          const int cw = s_bi[w];
+          if (w < wid) off += cw;
+          tot += cw;
+        }
+        if (qi != 0.0) {
+          const int pos = off + __popc(bal & ((1u << lane) - 1u));
+          ord[pos] = i;
+          tmp[pos] = qi;
+        }
+        base_out += tot;
+        __syncthreads();
+      }
+      if (tid == 0) s_L = base_out;
+      __syncthreads();
+      // sequential running sum, staged through shared memory in kLeafCap chunks
+      const int nzc = s_L;
+      double c = 0.0;  // (thread 0's)
+      for (int b0 = 0; b0 < nzc; b0 += kLeafCap) {
+        const int nb2 = min(kLeafCap, nzc - b0);
+        for (int i = tid; i < nb2; i += EX_THREADS) s_ls[i] = tmp[b0 + i];
+        __syncthreads();
+        if (tid == 0)
+          for (int i = 0; i < nb2; ++i) {
+            c += s_ls[i];
+            s_ls[i] = c;
+          }
+        __syncthreads();
+        for (int i = tid; i < nb2; i += EX_THREADS) tmp[b0 + i] = s_ls[i];
+        __syncthreads();
+      }
     }
-    __syncthreads();
-    const double Q = s_S;
+    const int nz = s_L;
     for (int64_t d = tv.d0 + tid; d < tv.d1; d += EX_THREADS) {
       const double u = draw_u(io, d, tv);
       const double t = u * Q;
       int tok;
       uint8_t fl = LC_DRAW_PRECISE;
-      if (!(Q > 0.0)) {
+      if (!(Q > 0.0) || nz == 0) {
         tok = -1;
         fl |= LC_DRAW_BAD_ROW;
       } else {
-        double c = 0.0, prev = 0.0;
-        int i = 0;
-        for (; i < V; ++i) {
-          prev = c;
-          c += q[i];
-          if (c > t) break;
+        int lo = 0, hi = nz;  // first running sum > t
+        while (lo < hi) {
+          const int mid = (lo + hi) >> 1;
+          if (tmp[mid] > t) hi = mid;
+          else lo = mid + 1;
         }
-        // a lower boundary of exactly 0 (no mass before) is shared with numpy exactly
-        double margin = (i < V) ? fmin(prev > 0.0 ? t - prev : INFINITY, c - t) : t - c;
-        if (i >= V) i = V - 1;
-        while (i > 0 && q[i] == 0.0) --i;
-        tok = i;
+        double margin;
+        if (lo < nz) {
+          const double c = tmp[lo], prev = lo > 0 ? tmp[lo - 1] : 0.0;
+          // a lower boundary of exactly 0 (no mass before) is shared with numpy exactly
+          margin = fmin(prev > 0.0 ? t - prev : INFINITY, c - t);
+          tok = ord[lo];
+        } else {  // past the end: clamp to V - 1, back off over zeros = the last nonzero id
+          margin = t - tmp[nz - 1];
+          tok = ord[nz - 1];
+        }
         // exp may differ from numpy's by an ulp: flag razor-thin margins
         if (margin <= fmax(t, 1e-300) * 64.0 * kEps64) {
           fl |= LC_DRAW_UNRESOLVED;
@@ -2448,6 +2594,7 @@ int64_t workspace_bytes(int64_t n_tasks, int64_t vocab) {
   b += ((rw_warps * rw_cap(vocab) * 16) + 3 * 255) & ~255ll;
   b += 512;
   b += ((n_tasks + 1) * 4 + 255) & ~255ll;
+  b += ((n_tasks + 1) * 4 + 255) & ~255ll;
   b += ((grid * 2 * SCR_PER_CTA * 4) + 255) & ~255ll;
   b += ((grid * 2 * SCR_PER_CTA * 8) + 255) & ~255ll;
   b += ((kExactCtas * vocab * 3 * 8) + 255) & ~255ll;
@@ -2469,6 +2616,7 @@ static int launch_all(const char* rows, int64_t row_bytes, int V, const lc_task*
   };
   Workspace ws;
   ws.q_exact = (int*)take((n_tasks + 1) * 4);
+  ws.q_cta = (int*)take((n_tasks + 1) * 4);
   ws.scr_id = (int*)take((int64_t)grid * 2 * SCR_PER_CTA * 4);
   ws.scr_e = (double*)take((int64_t)grid * 2 * SCR_PER_CTA * 8);
   const int64_t scr_stride = V;
@@ -2486,6 +2634,7 @@ static int launch_all(const char* rows, int64_t row_bytes, int V, const lc_task*
     return LC_E_ARG;
   }
   LCB_CUDA_TRY(cudaMemsetAsync(ws.q_exact, 0, 4, st));
+  LCB_CUDA_TRY(cudaMemsetAsync(ws.q_cta, 0, 4, st));
   unsigned long long* counters = d_counters ? (unsigned long long*)d_counters : cnt;
   if (!d_counters) LCB_CUDA_TRY(cudaMemsetAsync(cnt, 0, 64, st));
 
@@ -2507,6 +2656,7 @@ static int launch_all(const char* rows, int64_t row_bytes, int V, const lc_task*
     const int64_t need = (n_tasks + RW_WARPS - 1) / RW_WARPS;
     const int g = (int)(need < grw ? need : grw);
     rs.next = rw_next;
+    rs.q_cta = ws.q_cta;
     LCB_CUDA_TRY(cudaMemsetAsync(rw_next, 0, 4, st));
     static bool rw_attr[2][2] = {{false, false}, {false, false}};
     if (!rw_attr[DT][minb == 3]) {
@@ -2606,3 +2756,9 @@ extern "C" int lc_probe_exp(const float* d_z, int64_t n, float m, double tempera
   LCB_CUDA_TRY(cudaGetLastError());
   return LC_OK;
 }
+
+#ifdef LCB_RW_DEBUG
+extern "C" int lcb_debug_fetch(double* out) {
+  return cudaMemcpyFromSymbol(out, lcb::g_rw_dbg, sizeof(double) * 256 * 12) == cudaSuccess ? 0 : 4;
+}
+#endif
