@@ -1404,20 +1404,70 @@ __device__ __noinline__ FusedOut rw_fused_pass(const char* row, int V, int nseg,
   bool nan = false;
   const float eta = (float)(ACC ? (kEx2RelErr + kCorrErr + kSum8Err) : (kEx2Raw + kSum8Err)) * 1.0001f;
   const float ka = (float)kArgRel * 1.0001f;
+  // segments wholly inside an aligned row take the check-free vector loop
+  const int nfull = vec ? V / RW_SEG : 0;
   for (int s = 0; s < nseg; ++s) {
     double acc = 0.0;
     float W = 0.0f, R = 0.0f;  // |a|-weighted mass (CHEAP) and rescale error, relative to mt
-    constexpr int UNRF = (DT == LC_BF16) ? 8 : 4;  // 128 B per lane in flight
-#pragma unroll 1
-    for (int st = 0; st < RW_SEGSTEPS; st += UNRF) {
-      // raw vector loads first (memory-level parallelism), unpacked one vector at a time
-      uint4 raw[UNRF][DT == LC_BF16 ? 1 : 2];
-      bool full[UNRF];
+    // one vector of 8 ids at e0 (vmax NaN-propagating; vmin over ids < V)
+    auto body = [&](const float (&vu)[8], float vmax, float vmin, int e0) {
+      tmin = fminf(tmin, vmin);
+      nan |= (vmax != vmax);
+      if (vmax > mt) {
+        if (acc > 0.0) {  // rescale the partials to the new maximum
+          const float da = (mt - vmax) * Lhi;
+          float f;
+          if (ACC) {
+            ExpCtx c2;
+            c2.m = vmax;
+            c2.Lhi = Lhi;
+            c2.Llo = Llo;
+            f = fast_exp(c2, mt);
+          } else {
+            f = ex2_approx(da);
+          }
+          const float epsf = eta + (ACC ? 0.0f : ka * -da);
+          R = (R + (float)acc * epsf) * f;
+          W *= f;
+          acc *= (double)f;
+        }
+        mt = vmax;
+        tpos = e0;
+      }
+      float ef[8], aw[8];
 #pragma unroll
-      for (int u = 0; u < UNRF; ++u) {
-        const int e0 = s * RW_SEG + 256 * (st + u) + 8 * lane;
-        full[u] = vec && e0 + 8 <= V;
-        if (full[u]) {
+      for (int j = 0; j < 8; ++j) {
+        if (ACC) {
+          ExpCtx c2;
+          c2.m = mt;
+          c2.Lhi = Lhi;
+          c2.Llo = Llo;
+          ef[j] = fast_exp(c2, vu[j]);
+        } else {
+          const float a = (vu[j] - mt) * Lhi;
+          ef[j] = ex2_approx(a);  // -inf -> +0
+          aw[j] = a;
+        }
+      }
+      const float s8 = ((ef[0] + ef[1]) + (ef[2] + ef[3])) + ((ef[4] + ef[5]) + (ef[6] + ef[7]));
+      if (mt > -INFINITY) {  // (all -inf so far: z - mt is NaN)
+        if (!ACC) {
+          // CHEAP: W = sum of e*|a| (NaN once a -inf is seen: replaced at the segment end)
+#pragma unroll
+          for (int j = 0; j < 8; ++j) W = fmaf(ef[j], -aw[j], W);
+        }
+        acc += (double)s8;
+      }
+    };
+    if (s < nfull) {
+      constexpr int UNRF = (DT == LC_BF16) ? 8 : 4;  // 128 B per lane in flight
+#pragma unroll 1
+      for (int st = 0; st < RW_SEGSTEPS; st += UNRF) {
+        // raw vector loads first (memory-level parallelism), unpacked one vector at a time
+        uint4 raw[UNRF][DT == LC_BF16 ? 1 : 2];
+#pragma unroll
+        for (int u = 0; u < UNRF; ++u) {
+          const int e0 = s * RW_SEG + 256 * (st + u) + 8 * lane;
           if (DT == LC_BF16) {
             raw[u][0] = __ldg(reinterpret_cast<const uint4*>(reinterpret_cast<const uint16_t*>(row) + e0));
           } else {
@@ -1426,95 +1476,57 @@ __device__ __noinline__ FusedOut rw_fused_pass(const char* row, int V, int nseg,
                 __ldg(reinterpret_cast<const uint4*>(reinterpret_cast<const float*>(row) + e0 + 4));
           }
         }
-      }
 #pragma unroll
-      for (int u = 0; u < UNRF; ++u) {
-        const int e0 = s * RW_SEG + 256 * (st + u) + 8 * lane;
-        if (e0 >= V) continue;  // past the row (its -inf padding would make W NaN)
-        float vv[8];
-        float vmax, vmin;
-        if (full[u] && DT == LC_BF16) {
-          // packed bf16x2 max (NaN-propagating) / min over the 8 values
-          const uint32_t w[4] = {raw[u][0].x, raw[u][0].y, raw[u][0].z, raw[u][0].w};
+        for (int u = 0; u < UNRF; ++u) {
+          const int e0 = s * RW_SEG + 256 * (st + u) + 8 * lane;
+          float vv[8];
+          float vmax, vmin;
+          if (DT == LC_BF16) {
+            // packed bf16x2 max (NaN-propagating) / min over the 8 values
+            const uint32_t w[4] = {raw[u][0].x, raw[u][0].y, raw[u][0].z, raw[u][0].w};
 #pragma unroll
-          for (int j = 0; j < 4; ++j) {
-            vv[2 * j] = __uint_as_float(w[j] << 16);
-            vv[2 * j + 1] = __uint_as_float(w[j] & 0xffff0000u);
-          }
-          uint32_t x01, x23, x, n01, n23, n;
-          asm("max.NaN.bf16x2 %0, %1, %2;" : "=r"(x01) : "r"(w[0]), "r"(w[1]));
-          asm("max.NaN.bf16x2 %0, %1, %2;" : "=r"(x23) : "r"(w[2]), "r"(w[3]));
-          asm("max.NaN.bf16x2 %0, %1, %2;" : "=r"(x) : "r"(x01), "r"(x23));
-          asm("min.bf16x2 %0, %1, %2;" : "=r"(n01) : "r"(w[0]), "r"(w[1]));
-          asm("min.bf16x2 %0, %1, %2;" : "=r"(n23) : "r"(w[2]), "r"(w[3]));
-          asm("min.bf16x2 %0, %1, %2;" : "=r"(n) : "r"(n01), "r"(n23));
-          vmax = max_nan(__uint_as_float(x << 16), __uint_as_float(x & 0xffff0000u));
-          vmin = fminf(__uint_as_float(n << 16), __uint_as_float(n & 0xffff0000u));
-        } else {
-          if (full[u]) {
+            for (int j = 0; j < 4; ++j) {
+              vv[2 * j] = __uint_as_float(w[j] << 16);
+              vv[2 * j + 1] = __uint_as_float(w[j] & 0xffff0000u);
+            }
+            uint32_t x01, x23, x, n01, n23, n;
+            asm("max.NaN.bf16x2 %0, %1, %2;" : "=r"(x01) : "r"(w[0]), "r"(w[1]));
+            asm("max.NaN.bf16x2 %0, %1, %2;" : "=r"(x23) : "r"(w[2]), "r"(w[3]));
+            asm("max.NaN.bf16x2 %0, %1, %2;" : "=r"(x) : "r"(x01), "r"(x23));
+            asm("min.bf16x2 %0, %1, %2;" : "=r"(n01) : "r"(w[0]), "r"(w[1]));
+            asm("min.bf16x2 %0, %1, %2;" : "=r"(n23) : "r"(w[2]), "r"(w[3]));
+            asm("min.bf16x2 %0, %1, %2;" : "=r"(n) : "r"(n01), "r"(n23));
+            vmax = max_nan(__uint_as_float(x << 16), __uint_as_float(x & 0xffff0000u));
+            vmin = fminf(__uint_as_float(n << 16), __uint_as_float(n & 0xffff0000u));
+          } else {
             const uint4 a = raw[u][0], b = raw[u][DT == LC_BF16 ? 0 : 1];
             vv[0] = __uint_as_float(a.x); vv[1] = __uint_as_float(a.y);
             vv[2] = __uint_as_float(a.z); vv[3] = __uint_as_float(a.w);
             vv[4] = __uint_as_float(b.x); vv[5] = __uint_as_float(b.y);
             vv[6] = __uint_as_float(b.z); vv[7] = __uint_as_float(b.w);
-          } else {
-            load8<DT>(row, e0, V, vec, vv);
+            vmax = max_nan(max_nan(max_nan(vv[0], vv[1]), max_nan(vv[2], vv[3])),
+                           max_nan(max_nan(vv[4], vv[5]), max_nan(vv[6], vv[7])));
+            vmin = fminf(fminf(fminf(vv[0], vv[1]), fminf(vv[2], vv[3])),
+                         fminf(fminf(vv[4], vv[5]), fminf(vv[6], vv[7])));
           }
-          vmax = max_nan(max_nan(max_nan(vv[0], vv[1]), max_nan(vv[2], vv[3])),
-                         max_nan(max_nan(vv[4], vv[5]), max_nan(vv[6], vv[7])));
-          vmin = INFINITY;
+          body(vv, vmax, vmin, e0);
+        }
+      }
+    } else {
+      // tail segment / unaligned row: one generic vector at a time
+#pragma unroll 1
+      for (int st = 0; st < RW_SEGSTEPS && s * RW_SEG + 256 * st < V; ++st) {
+        const int e0 = s * RW_SEG + 256 * st + 8 * lane;
+        if (e0 >= V) continue;  // past the row (its -inf padding would make W NaN)
+        float vv[8];
+        load8<DT>(row, e0, V, vec, vv);
+        float vmax = vv[0], vmin = INFINITY;
 #pragma unroll
-          for (int j = 0; j < 8; ++j)
-            if (e0 + j < V) vmin = fminf(vmin, vv[j]);
-        }
-        float (&vu)[8] = vv;
-        tmin = fminf(tmin, vmin);
-        nan |= (vmax != vmax);
-        if (vmax > mt) {
-          if (acc > 0.0) {  // rescale the partials to the new maximum
-            const float da = (mt - vmax) * Lhi;
-            float f;
-            if (ACC) {
-              ExpCtx c2;
-              c2.m = vmax;
-              c2.Lhi = Lhi;
-              c2.Llo = Llo;
-              f = fast_exp(c2, mt);
-            } else {
-              f = ex2_approx(da);
-            }
-            const float epsf = eta + (ACC ? 0.0f : ka * -da);
-            R = (R + (float)acc * epsf) * f;
-            W *= f;
-            acc *= (double)f;
-          }
-          mt = vmax;
-          tpos = e0;
-        }
-        float ef[8], aw[8];
+        for (int j = 1; j < 8; ++j) vmax = max_nan(vmax, vv[j]);
 #pragma unroll
-        for (int j = 0; j < 8; ++j) {
-          if (ACC) {
-            ExpCtx c2;
-            c2.m = mt;
-            c2.Lhi = Lhi;
-            c2.Llo = Llo;
-            ef[j] = fast_exp(c2, vu[j]);
-          } else {
-            const float a = (vu[j] - mt) * Lhi;
-            ef[j] = ex2_approx(a);  // -inf -> +0
-            aw[j] = a;
-          }
-        }
-        const float s8 = ((ef[0] + ef[1]) + (ef[2] + ef[3])) + ((ef[4] + ef[5]) + (ef[6] + ef[7]));
-        if (mt > -INFINITY) {  // (all -inf so far: z - mt is NaN)
-          if (!ACC) {
-            // CHEAP: W = sum of e*|a| (NaN once a -inf is seen: replaced at the segment end)
-#pragma unroll
-            for (int j = 0; j < 8; ++j) W = fmaf(ef[j], -aw[j], W);
-          }
-          acc += (double)s8;
-        }
+        for (int j = 0; j < 8; ++j)
+          if (e0 + j < V) vmin = fminf(vmin, vv[j]);
+        body(vv, vmax, vmin, e0);
       }
     }
     // segment end: combine at the warp's running maximum.  A -inf element made W NaN:
@@ -1626,22 +1638,50 @@ __device__ double rw_seg_pass(const char* row, int V, int nseg, bool vec, int la
 // q = e * 2^(b/32) = ex2(a + b/32) in per-bin relative fixed point (the sum
 // a + b/32 is exact: a and -b/32 are within a factor 2).  Out of line: its own
 // register budget.
+// 8 consecutive logits at an aligned, in-range e0 (no checks)
+template <int DT>
+__device__ __forceinline__ void load8_full(const char* row, int e0, float v[8]) {
+  if (DT == LC_BF16) {
+    const uint4 q = __ldg(reinterpret_cast<const uint4*>(reinterpret_cast<const uint16_t*>(row) + e0));
+    const uint32_t w[4] = {q.x, q.y, q.z, q.w};
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      v[2 * j] = __uint_as_float(w[j] << 16);
+      v[2 * j + 1] = __uint_as_float(w[j] & 0xffff0000u);
+    }
+  } else {
+    const float4 a = __ldg(reinterpret_cast<const float4*>(reinterpret_cast<const float*>(row) + e0));
+    const float4 b = __ldg(reinterpret_cast<const float4*>(reinterpret_cast<const float*>(row) + e0 + 4));
+    v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w;
+    v[4] = b.x; v[5] = b.y; v[6] = b.z; v[7] = b.w;
+  }
+}
+
 template <int DT>
 __device__ __noinline__ void rw_hist_pass(const char* row, int V, bool vec, int lane, float m, float Lhi, float qscale,
                                           uint32_t hist_s) {
-  for (int base = 0; base < V; base += 1024) {  // four vectors per lane in flight
+  auto add = [&](float z) {
+    const float a = fmaxf((z - m) * Lhi, -200.0f);
+    const int b = rw_bin(a);
+    const uint32_t q = __float2uint_rn(ex2_approx(fmaf((float)b, 1.0f / RW_BPO, a)) * qscale);
+    asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(hist_s + 4u * (uint32_t)b), "r"(q) : "memory");
+  };
+  const int vfull = vec ? (V / 1024) * 1024 : 0;
+  for (int base = 0; base < vfull; base += 1024) {  // four vectors per lane in flight, no checks
     float v[4][8];
 #pragma unroll
-    for (int u = 0; u < 4; ++u) load8<DT>(row, base + 256 * u + 8 * lane, V, vec, v[u]);
+    for (int u = 0; u < 4; ++u) load8_full<DT>(row, base + 256 * u + 8 * lane, v[u]);
 #pragma unroll
     for (int u = 0; u < 4; ++u)
 #pragma unroll
-      for (int j = 0; j < 8; ++j) {
-        const float a = fmaxf((v[u][j] - m) * Lhi, -200.0f);
-        const int b = rw_bin(a);
-        const uint32_t q = __float2uint_rn(ex2_approx(fmaf((float)b, 1.0f / RW_BPO, a)) * qscale);
-        asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(hist_s + 4u * (uint32_t)b), "r"(q) : "memory");
-      }
+      for (int j = 0; j < 8; ++j) add(v[u][j]);
+  }
+#pragma unroll 1
+  for (int base = vfull; base < V; base += 256) {  // tail: ids >= V read as -inf (q = 0)
+    float v[8];
+    load8<DT>(row, base + 8 * lane, V, vec, v);
+#pragma unroll
+    for (int j = 0; j < 8; ++j) add(v[j]);
   }
 }
 
@@ -1652,19 +1692,17 @@ template <int DT>
 __device__ __noinline__ int rw_list_pass(const char* row, int V, bool vec, int lane, float zhi, float zab, int2* L_iz,
                                          int cap, RwWarp& sw, int& ovf) {
   int wn = 0;
-  for (int base = 0; base < V && wn <= cap; base += 512) {  // two vectors per lane
-    const int e0 = base + 8 * lane, e1 = e0 + 256;
-    float v[2][8];
-    load8<DT>(row, e0, V, vec, v[0]);
-    load8<DT>(row, e1, V, vec, v[1]);
+  // NV vectors (256 ids each) per step; ids >= V read as -inf (never >= zhi)
+  auto step = [&](const float (&v)[2][8], int nv, int base) {
     unsigned lm[2] = {0u, 0u}, bm[2] = {0u, 0u};
 #pragma unroll
     for (int u = 0; u < 2; ++u)
 #pragma unroll
-      for (int j = 0; j < 8; ++j) {  // ids >= V read as -inf
+      for (int j = 0; j < 8; ++j) {
         lm[u] |= (v[u][j] >= zhi ? 1u : 0u) << j;
         bm[u] |= (v[u][j] >= zhi && v[u][j] < zab ? 1u : 0u) << j;
       }
+    if (nv < 2) lm[1] = bm[1] = 0u;
     // both vectors' counts in one scan (16-bit halves)
     const int c = __popc(lm[0]) | (__popc(lm[1]) << 16);
     int incl = c;
@@ -1676,14 +1714,18 @@ __device__ __noinline__ int rw_list_pass(const char* row, int V, bool vec, int l
     const int tot = __shfl_sync(0xffffffffu, incl, 31);
     const int t0 = tot & 0xffff;
     const int pos0[2] = {wn + (incl & 0xffff) - (c & 0xffff), wn + t0 + (incl >> 16) - (c >> 16)};
+    const int e0[2] = {base + 8 * lane, base + 256 + 8 * lane};
     if (wn + t0 + (tot >> 16) <= cap) {
 #pragma unroll
-      for (int u = 0; u < 2; ++u)
+      for (int u = 0; u < 2; ++u) {
+        int pos = pos0[u];
 #pragma unroll
         for (int j = 0; j < 8; ++j)
-          if ((lm[u] >> j) & 1u)
-            L_iz[pos0[u] + __popc(lm[u] & ((1u << j) - 1u))] =
-                make_int2((u ? e1 : e0) + j + (int)(((bm[u] >> j) & 1u) << 31), __float_as_int(v[u][j]));
+          if ((lm[u] >> j) & 1u) {
+            L_iz[pos] = make_int2(e0[u] + j + (int)(((bm[u] >> j) & 1u) << 31), __float_as_int(v[u][j]));
+            ++pos;
+          }
+      }
     }
     // bracket keys use the LIST POSITION instead of the id: the list is id-ordered,
     // so (z desc, position asc) is the reference's (p desc, id asc) order
@@ -1699,6 +1741,19 @@ __device__ __noinline__ int rw_list_pass(const char* row, int V, bool vec, int l
         }
     }
     wn += t0 + (tot >> 16);
+  };
+  const int vfull = vec ? (V / 512) * 512 : 0;
+  for (int base = 0; base < vfull && wn <= cap; base += 512) {  // two vectors per lane, no checks
+    float v[2][8];
+    load8_full<DT>(row, base + 8 * lane, v[0]);
+    load8_full<DT>(row, base + 256 + 8 * lane, v[1]);
+    step(v, 2, base);
+  }
+#pragma unroll 1
+  for (int base = vfull; base < V && wn <= cap; base += 256) {  // tail, one vector per step
+    float v[2][8];
+    load8<DT>(row, base + 8 * lane, V, vec, v[0]);
+    step(v, 1, base);
   }
   return wn;
 }
