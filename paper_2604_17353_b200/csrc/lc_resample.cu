@@ -34,6 +34,7 @@
 #include "lc_common.cuh"
 #include "lc_numpy.cuh"
 #include "lc_resample.cuh"
+#include "lc_task.cuh"
 
 namespace lcb {
 
@@ -47,18 +48,6 @@ constexpr int K0_SPEC = 64;           // speculative candidate count for top-p w
 constexpr int SCR_PER_WARP = 2048;    // large-nucleus kept elements per warp (global scratch)
 constexpr int SCR_PER_CTA = SCR_PER_WARP * RS_WARPS;
 
-// ---- error model ----------------------------------------------
-// ex2.approx.ftz.f32 relative error bound (PTX ISA: ~2 ulp).  The GPU test
-// tests/test_gpu_parity.py::test_fast_exp_error_bound measures fast_exp over
-// dense argument grids and fails if this constant is ever exceeded.
-constexpr double kEx2RelErr = 4.0e-7;    // fast_exp (corrected) incl. margin
-constexpr double kEx2Raw = 2.5e-7;       // ex2.approx.ftz.f32 alone (cheap_exp), measured bound + margin
-constexpr double kArgRel = 3.0 * 5.9604644775390625e-08 * 0.6931471805599453 * 1.01;  // cheap_exp: per |a|
-constexpr double kCorrErr = 1.0e-10;                       // 2nd-order term of the argument correction
-constexpr double kSum8Err = 3.0 * 5.9604644775390625e-08;  // fp32 pairwise sum of 8 (3 roundings)
-constexpr double kRefExpErr = 8.881784197001252e-16;       // libm / numpy exp vs exact: 4 ulp
-constexpr double kLiteErr = 3.0e-13;                       // lite_exp incl. its argument (|a| <= 1100)
-constexpr double kEps64 = 1.1102230246251565e-16;          // 2^-53
 
 // ---- loading --------------------------------------------------------------------------------
 
@@ -118,50 +107,6 @@ __device__ __forceinline__ float load1(const char* row, int i) {
   return __ldg(reinterpret_cast<const float*>(row) + i);
 }
 
-// ---- exponentials ------------------------------------------------------------------------------
-
-struct ExpCtx {
-  float m;         // row max (exact)
-  float Lhi, Llo;  // log2(e)/T split, Lhi + Llo = log2e/T to ~2^-48
-  double T;
-  double mT;       // fl(m / T): the reference's scaled max (sampling.py:65-66)
-  double md;       // (double) m
-  double L16;      // 16 * log2(e) / T
-};
-
-// FAST: e ~ 2^((z-m) * log2e / T).  z - m is carried exactly (TwoSum), the
-// product error and the constant's low part go into alo, and ex2's input
-// rounding is removed by the first-order correction e*(1 + alo*ln2).
-// Relative error <= kEx2RelErr + kCorrErr; 0 for z = -inf; e(m) == 1 exactly.
-__device__ __forceinline__ float fast_exp(const ExpCtx& c, float z) {
-  float s = z - c.m;
-  float bb = s - z;
-  float err = (z - (s - bb)) + (-c.m - bb);
-  float ahi = s * c.Lhi;
-  float alo = fmaf(s, c.Lhi, -ahi) + fmaf(err, c.Lhi, s * c.Llo);
-  float e = ex2_approx(ahi);
-  return (e > 0.0f) ? fmaf(e, alo * 0.69314718055994531f, e) : 0.0f;
-}
-
-// CHEAP (truncated modes, where only the row mass and bracketing use it):
-// e = ex2(fl(fl(z - m) * Lhi)).  Relative error <= kEx2Raw + kArgRel * |a|
-// (three fp32 roundings carried into the argument); a is clamped at -200 so
-// -inf inputs give e = 0 and e*a = 0.
-__device__ __forceinline__ float cheap_exp(const ExpCtx& c, float z, float& a) {
-  a = fmaxf((z - c.m) * c.Lhi, -200.0f);
-  return ex2_approx(a);
-}
-
-__device__ __forceinline__ float max_nan(float a, float b) {
-  float r;
-  asm("max.NaN.f32 %0, %1, %2;" : "=f"(r) : "f"(a), "f"(b));
-  return r;
-}
-__device__ __forceinline__ float min_nan(float a, float b) {
-  float r;
-  asm("min.NaN.f32 %0, %1, %2;" : "=f"(r) : "f"(a), "f"(b));
-  return r;
-}
 
 // Phase A: per-thread max and min over the warp's id range, NaN-propagating,
 // packed bf16x2 for bf16 rows (one HMNMX2 per two elements).
@@ -449,79 +394,6 @@ __device__ __forceinline__ double warp_incl_scan(double x) {
   return x;
 }
 
-// ---- task plumbing ------------------------------------------------------------------------------
-
-struct TaskView {
-  const char* row;
-  int V;
-  double T;
-  int topk;  // effective top-k (0 = none / k >= V)
-  double topp;
-  bool trunc;
-  int64_t d0, d1;
-  int64_t seed_base;
-  int64_t u_index;
-};
-
-struct CacheMap {
-  const int32_t* pages;  // [slots][max_pages], -1 = unused
-  int max_pages;
-  int page_rows;
-};
-
-struct DrawIO {
-  const double* u;
-  const uint64_t* seed;
-  const int64_t* index;
-  int32_t* token;
-  uint8_t* flags;
-};
-
-struct Workspace {
-  int* q_exact;   // [0] = count, [1..] task ids
-  int* q_cta;     // tasks the row-warp kernel hands to the CTA kernel (same layout)
-  int* scr_id;    // [grid][2][SCR_PER_CTA]
-  double* scr_e;  // [grid][2][SCR_PER_CTA]
-};
-
-__device__ __forceinline__ double draw_u(const DrawIO& io, int64_t d, const TaskView& tv) {
-  if (io.u) return io.u[d];
-  if (io.index) return request_uniform(io.seed[d], (uint64_t)io.index[d]);
-  return request_uniform(io.seed[tv.seed_base + (d - tv.d0)], (uint64_t)tv.u_index);
-}
-
-__device__ __forceinline__ bool resolve_task(const lc_task& tk, const char* rows, int64_t row_bytes, int Vdef,
-                                             const CacheMap& cm, TaskView& tv) {
-  tv.d0 = tk.draw_begin;
-  tv.d1 = tk.draw_end;
-  tv.seed_base = tk.seed_base;
-  tv.u_index = tk.u_index >= 0 ? tk.u_index : tk.pos;
-  tv.V = tk.vocab > 0 ? tk.vocab : Vdef;
-  tv.T = tk.temperature;
-  tv.topk = (tk.top_k > 0 && tk.top_k < tv.V) ? tk.top_k : 0;
-  tv.topp = tk.top_p;
-  tv.trunc = !(tk.top_k <= 0 && tk.top_p == 1.0);
-  tv.row = nullptr;
-  if (tv.V < 1 || tv.V > Vdef || !(tv.T >= 0.0) || !(tv.topp > 0.0 && tv.topp <= 1.0)) return false;
-  int64_t r = tk.row;
-  if (r < 0) {
-    if (!cm.pages || tk.slot < 0 || tk.pos < 0) return false;
-    int pg = tk.pos / cm.page_rows;
-    if (pg >= cm.max_pages) return false;
-    int page = cm.pages[(int64_t)tk.slot * cm.max_pages + pg];
-    if (page < 0) return false;
-    r = (int64_t)page * cm.page_rows + tk.pos % cm.page_rows;
-  }
-  tv.row = rows + r * row_bytes;
-  return true;
-}
-
-__device__ __forceinline__ void write_all(const TaskView& tv, const DrawIO& io, int tok, uint8_t flag) {
-  for (int64_t d = tv.d0 + threadIdx.x; d < tv.d1; d += RS_THREADS) {
-    io.token[d] = tok;
-    if (io.flags) io.flags[d] = flag;
-  }
-}
 
 // counters: 0 tasks that needed the PRECISE pass, 1 unresolved draws (EXACT),
 // 2 bad rows, 3 tasks sent to EXACT, 4 uncertain cut (FAST), 5 uncertain draw
@@ -2703,7 +2575,14 @@ static int launch_all(const char* rows, int64_t row_bytes, int V, const lc_task*
   // test hook: LCB_FORCE_TIER=precise|exact routes every task to that tier
   const char* ft = getenv("LCB_FORCE_TIER");
   const int force = !ft ? 0 : (ft[0] == 'p' ? 1 : (ft[0] == 'e' ? 2 : 0));
-  if (rw) {
+  const char* ns = getenv("LCB_NO_STAGE");
+  if (rw && force == 0 && !(ns && ns[0] == '1') && stage_eligible(DT, V, row_bytes, rows)) {
+    // bf16 rows <= 32768 ids: TMA-staged persistent kernel (lc_stage.cu); it requeues
+    // what it does not handle or cannot certify to the CTA kernel below
+    LCB_CUDA_TRY(cudaMemsetAsync(rw_next, 0, 4, st));
+    const int rc = stage_launch(rows, row_bytes, V, tasks, n_tasks, cm, io, rw_next, ws.q_cta, counters, num_sms(), st);
+    if (rc != LC_OK) return rc;
+  } else if (rw) {
     // CTAs per SM: 2 (128 registers, no spills) by default; LCB_RW_BLOCKS=3 trades spills for warps
     const char* rb = getenv("LCB_RW_BLOCKS");
     const int minb = (rb && rb[0] == '3') ? 3 : RW_MIN_BLOCKS;
@@ -2800,6 +2679,13 @@ __global__ void probe_exp_kernel(const float* z, int64_t n, float m, double T, i
   c.md = (double)m;
   c.L16 = 16.0 * Ld;
   float a;
+  if (mode == 3) {  // ex2.approx.ftz.bf16x2 of bf16(z) (the staged kernel's FAST exit test)
+    const uint32_t h = f32_to_bf16_bits(z[i]);
+    uint32_t r;
+    asm("ex2.approx.ftz.bf16x2 %0, %1;" : "=r"(r) : "r"(h | (h << 16)));
+    out[i] = (double)__uint_as_float(r << 16);
+    return;
+  }
   out[i] = mode == 0 ? (double)fast_exp(c, z[i]) : mode == 1 ? (double)cheap_exp(c, z[i], a) : lite_exp(c, z[i], t16);
 }
 }  // namespace lcb

@@ -127,6 +127,20 @@ def test_ex2_raw_bound():
     assert float((np.abs(got - exact) / exact).max()) < 2.5e-7
 
 
+def test_bf16_ex2_bound():
+    """ex2.approx.ftz.bf16x2 over every non-positive bf16 input down to -126:
+    relative error (incl. the bf16 rounding of the result) well inside
+    kEx2Bf16Err = 0.01 (lc_stage.cu FAST exit bound)."""
+    h = np.arange(0x8000, 0x10000, dtype=np.uint32)  # negative bf16 bit patterns
+    x = (h << 16).view(np.float32)
+    x = x[np.isfinite(x) & (x >= -126.0)]
+    x = np.concatenate([x, np.float32([0.0])])
+    got = _probe(x, np.float32(0.0), 1.0, 3)
+    exact = np.exp2(x.astype(np.float64))
+    worst = float((np.abs(got - exact) / exact).max())
+    assert worst < 0.008, worst
+
+
 # -- resample vs golden (reference) ----------------------------------------------------------
 
 
@@ -399,3 +413,24 @@ def test_replay_stepwise_matches_oracle():
                     break
             assert rep[r, b] == want_rep, (r, b)
     assert np.all(rep[n_req] == 0)
+
+
+@pytest.mark.parametrize("conc,T,p,nd", [(2.5, 0.6, 0.9, 32), (0.0, 0.6, 0.9, 8), (2.5, 1.0, 0.5, 4),
+                                         (5.0, 0.3, 0.99, 16), (1.0, 2.0, 0.95, 8)])
+def test_staged_kernel_matches_oracle_and_other_tiers(conc, T, p, nd, monkeypatch):
+    """The TMA-staged kernel (bf16, V <= 32768, top-p) against the oracle, and
+    bit-identical to the row-warp path (LCB_NO_STAGE=1) on the same inputs."""
+    V, n = 32000, 48
+    rows = mixing_ref.bf16_round(mixing_ref.fill_rows_np([mixing_ref.mix2(23, i) for i in range(n)], V, conc))
+    rng = np.random.default_rng(int(conc * 10 + T * 100 + p * 1000))
+    ulists = [rng.random(nd) for _ in range(n)]
+    tok, fl, cnt = _resample_rows(rows, T, None, p, ulists, dtype=torch.bfloat16)
+    want = []
+    for r in range(n):
+        q = sampling_ref.truncate(sampling_ref.softmax(rows[r], T), None, p)
+        want += [sampling_ref.draw(q, float(x)) for x in ulists[r]]
+    assert tok.tolist() == want
+    assert not np.any(fl & _capi.LC_DRAW_UNRESOLVED)
+    monkeypatch.setenv("LCB_NO_STAGE", "1")
+    tok2, _, _ = _resample_rows(rows, T, None, p, ulists, dtype=torch.bfloat16)
+    assert tok2.tolist() == tok.tolist()
