@@ -56,6 +56,29 @@ __device__ __forceinline__ float cheap_exp(const ExpCtx& c, float z, float& a) {
   return ex2_approx(a);
 }
 
+// PRECISE: table-driven fp64 exp of (z - m)/T.  b = 16*log2e*(z-m)/T,
+// n = rint(b), x = b - n in [-1/2, 1/2]; 2^(b/16) = 2^(n>>4) * 2^((n&15)/16) *
+// exp(x*ln2/16) with a degree-6 Taylor polynomial (|x ln2/16| <= 0.0217,
+// truncation 5e-16).  Relative error <= kLiteErr for |b/16| <= 1100.
+__device__ __forceinline__ double lite_exp(const ExpCtx& c, float z, const double* t16) {
+  const double b = ((double)z - c.md) * c.L16;
+  if (!(b > -17000.0)) return 0.0;
+  const double t = b + 6755399441055744.0;  // 1.5 * 2^52: round to nearest
+  const int n16 = __double2loint(t);
+  const double x = b - (t - 6755399441055744.0);
+  double p = 9.181219573844438764e-12;
+  p = fma(x, p, 1.271587195055813162e-9);
+  p = fma(x, p, 1.467610032291942926e-7);
+  p = fma(x, p, 1.355080777949745604e-5);
+  p = fma(x, p, 9.383847928089871576e-4);
+  p = fma(x, p, 4.332169878499658184e-2);
+  p = fma(x, p, 1.0);
+  const double r = t16[n16 & 15] * p;
+  const int e2 = n16 >> 4;
+  if (e2 >= -1021) return __hiloint2double(__double2hiint(r) + (e2 << 20), __double2loint(r));
+  return (r * __hiloint2double((e2 + 1023 + 600) << 20, 0)) * 0x1p-600;
+}
+
 __device__ __forceinline__ float max_nan(float a, float b) {
   float r;
   asm("max.NaN.f32 %0, %1, %2;" : "=f"(r) : "f"(a), "f"(b));

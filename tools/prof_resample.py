@@ -57,6 +57,16 @@ def main():
         gb = n * a.V * rows.element_size() / 1e9
         print(f"iter {i}: {ms:.3f} ms  {n / ms / 1e3:.2f} M rows/s  {gb / ms * 1e3:.1f} GB/s  "
               f"counters {cnt.cpu().tolist()}", flush=True)
+        if os.environ.get("LCB_STAGE_PROF") == "1":
+            import ctypes
+            buf = (ctypes.c_ulonglong * 12)()
+            if _capi.lib.lcb_stage_prof_fetch(buf) == 0:
+                ph = list(buf)
+                rows_, big = max(ph[9], 1), max(ph[10], 1)
+                names = ["wait", "A", "B", "fastfin", "H", "cls+cut", "C", "D", "end"]
+                print("  stage phases, clks per row (per big row for H..D): " + "  ".join(
+                    f"{nm}={ph[k] / (big if 4 <= k <= 7 else rows_):.0f}" for k, nm in enumerate(names))
+                    + f"  post={ph[11] / big:.0f}  rows={ph[9]} big={ph[10]}", flush=True)
 
 
 if __name__ == "__main__":
