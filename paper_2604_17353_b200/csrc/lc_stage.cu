@@ -38,8 +38,8 @@ constexpr int SG_THREADS = (SG_PWARP + 1) * 32;  // 512
 constexpr int SG_MAXV = 32000;
 constexpr int SG_STAGE_BYTES = SG_MAXV * 2;
 constexpr int SG_NB = 512;                       // histogram classes below the max
-constexpr int SG_CH = 256;                       // ids per chunk (one warp x 8 per lane)
-constexpr int SG_NCH = SG_MAXV / SG_CH;          // 125
+constexpr int SG_CH = 1024;                      // ids per chunk (4 sub-chunks of one warp x 8 per lane)
+constexpr int SG_NCH = (SG_MAXV + SG_CH - 1) / SG_CH;  // 32
 constexpr int SG_NU = 32;                        // uniforms precomputed per task (one per producer lane)
 constexpr int SG_ND = 64;                        // draws per task handled here (more: CTA kernel)
 constexpr int SG_PB = 8;                         // tasks per producer grab
@@ -395,6 +395,7 @@ __global__ void __launch_bounds__(SG_THREADS, 1) stage_kernel(StageArgs a) {
       const float Lf = (float)Ld;
       const float mL = fabsf(m) * Lf;
       bool fast = false;
+      double Sfast = 1.0;  // FAST estimate of the row mass (within its bound factor)
       if (mL <= 128.0f && Lf < 1e30f) {
         const uint32_t Lb = bf16_bits(Lf);
         const float Lbf = __uint_as_float(Lb << 16);
@@ -416,6 +417,7 @@ __global__ void __launch_bounds__(SG_THREADS, 1) stage_kernel(StageArgs a) {
         const float dl = 0.001953125f * mL * 1.01f + 0.001953125f;
         const double F = (double)exp2f(0.00390625f * (40.1f + dl)) * (1.0 + kEx2Bf16Err) / (1.0 - kEx2Bf16Err);
         const double tail = fmax(Sc / (double)emax - 1.0, 0.0);
+        Sfast = 1.0 + tail;
         const double Sup = (1.0 + F * tail * (1.0 + 3e-5) + (double)V * 0x1p-40) * (1.0 + 1e-9);
         fast = Sup * tv.topp < 1.0 - 1e-15;
       }
@@ -425,89 +427,89 @@ __global__ void __launch_bounds__(SG_THREADS, 1) stage_kernel(StageArgs a) {
         ST_PH(3);
       } else {
         if (prof) ph[10]++;
-        // -------------------------------------------- B': precise row mass (fp32 MUFU, bounded)
+        // -------------------------------------------- H: one pass over the row: exact class
+        // histogram of the values that can lie above the cut (z >= z_lo, with V e(z_lo) <=
+        // (1 - top_p) S / 2), fp32 MUFU exponentials for the rest (the "tail", bounded), and
+        // every element's class offset written over its logit (16 bits) in the stage
+        for (int b = gt; b < SG_NB; b += SG_GT) G.hist[b] = 0u;
+        ExpCtx ec;
+        ec.m = m;
+        ec.T = tv.T;
+        ec.Lhi = Lf;
+        ec.Llo = (float)(Ld - (double)Lf);
+        ec.md = (double)m;
+        ec.L16 = 16.0 * Ld;
+        const uint32_t km = key16(__float_as_uint(m));
+        // S >= max(1, S_fast / 1.25): the FAST estimate is within F <= 1.14 of the truth
+        const double slo = fmax(Sfast / 1.25, 1.0);
+        const double alo = log2(fmax(0.5 * (1.0 - tv.topp) * slo / (double)V, 1e-300));
+        int nb_eff = SG_NB;
+        {
+          const float zl = m + (float)(alo / Ld);
+          if (zl > -INFINITY) nb_eff = (int)min((uint32_t)SG_NB, km - key16(__float_as_uint(zl)) + 1u);
+        }
         // e = ex2(fl(z Lf - fl(m Lf))) / ex2(fl(m Lf - fl(m Lf))): the common rounding of m Lf
-        // cancels in the ratio, the rest is |a|-weighted (W)
+        // cancels in the ratio, the rest weighs |a|
         const float nmL = -(m * Lf);
         const float emax = ex2_approx(fmaf(m, Lf, nmL));
-        double acc = 0.0;
-        float W = 0.0f;
-        for (int v = gt; v < nvec; v += SG_GT) {
-          const uint4 q = R[v];
-          const uint32_t w[4] = {q.x, q.y, q.z, q.w};
-          float e8[8];
-#pragma unroll
-          for (int j = 0; j < 8; ++j) {
-            const float z = (j & 1) ? hi_f(w[j >> 1]) : lo_f(w[j >> 1]);
-            const float aa = fmaxf(fmaf(z, Lf, nmL), -200.0f);  // -inf -> e = 0, e*a = 0
-            e8[j] = ex2_approx(aa);
-            W = fmaf(e8[j], -aa, W);
-          }
-          acc += (double)(((e8[0] + e8[1]) + (e8[2] + e8[3])) + ((e8[4] + e8[5]) + (e8[6] + e8[7])));
-        }
-        const double S = gsum_d(acc, 1) / (double)emax;
-        const double Wt = gsum_d((double)W, 2) / (double)emax;
-        // |S - sum 2^((z-m)L)| <= ES: ex2.approx (numerator and emax), fp32 sums of 8, the
-        // argument roundings (|a|-weighted: product and L; the m Lf term cancels)
-        const double ES = S * (2.0 * kEx2Raw + kSum8Err + 1e-12) + Wt * 1.001 * kLn2 * 0x1p-23 +
-                          S * kLn2 * 0x1p-24 * (2.0 + 0x1p-8 * (double)mL);
         const bool sane = mL <= 1e6f && Lf < 1e30f && Lf > 1e-30f && emax > 0.5f;
+        // positive domain (every class in range positive): offset = bits(m) - bits(z)
+        const uint32_t mb16 = __float_as_uint(m) >> 16;
+        const bool pos = m > 0.0f && (uint32_t)nb_eff <= mb16 && key16_to_f(km - (uint32_t)(nb_eff - 1)) > 0.0f;
+        gbar(g);  // hist zeroed
+        double tacc = 0.0;
+        if (pos) {
+          // offsets of both halves at once: bits(m) - bits(z) per 16-bit lane (VIADD.16x2);
+          // negative z wrap to >= bits(m) + 1 > nb_eff, never a kept class
+          const uint32_t mb2 = (mb16 | (mb16 << 16)) + 0x00010001u;
+          for (int v = gt; v < nvec; v += SG_GT) {
+            const uint4 q = R[v];
+            const uint32_t w[4] = {q.x, q.y, q.z, q.w};
+            uint32_t o[4];
+            float e8[8];
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+              o[k] = __vadd2(~w[k], mb2);
+              const uint32_t ol = o[k] & 0xffffu, oh = o[k] >> 16;
+              const bool il = ol < (uint32_t)nb_eff, ih = oh < (uint32_t)nb_eff;
+              if (il) atomicAdd(&G.hist[ol], 1u);
+              if (ih) atomicAdd(&G.hist[oh], 1u);
+              const float el = ex2_approx(fmaf(lo_f(w[k]), Lf, nmL));  // -inf -> 0
+              const float eh = ex2_approx(fmaf(hi_f(w[k]), Lf, nmL));
+              e8[2 * k] = il ? 0.0f : el;
+              e8[2 * k + 1] = ih ? 0.0f : eh;
+            }
+            tacc += (double)(((e8[0] + e8[1]) + (e8[2] + e8[3])) + ((e8[4] + e8[5]) + (e8[6] + e8[7])));
+            R[v] = make_uint4(o[0], o[1], o[2], o[3]);
+          }
+        } else {
+          for (int v = gt; v < nvec; v += SG_GT) {
+            const uint4 q = R[v];
+            const uint32_t w[4] = {q.x, q.y, q.z, q.w};
+            uint32_t o[4];
+            float e8[8];
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+              const uint32_t ol = km - key16(w[k] << 16), oh = km - key16(w[k] & 0xffff0000u);
+              const bool il = ol < (uint32_t)nb_eff, ih = oh < (uint32_t)nb_eff;
+              if (il) atomicAdd(&G.hist[ol], 1u);
+              if (ih) atomicAdd(&G.hist[oh], 1u);
+              const float el = ex2_approx(fmaf(lo_f(w[k]), Lf, nmL));
+              const float eh = ex2_approx(fmaf(hi_f(w[k]), Lf, nmL));
+              e8[2 * k] = il ? 0.0f : el;
+              e8[2 * k + 1] = ih ? 0.0f : eh;
+              o[k] = ol | (oh << 16);
+            }
+            tacc += (double)(((e8[0] + e8[1]) + (e8[2] + e8[3])) + ((e8[4] + e8[5]) + (e8[6] + e8[7])));
+            R[v] = make_uint4(o[0], o[1], o[2], o[3]);
+          }
+        }
+        const double tail = gsum_d(tacc, 1) / (double)emax;
         // numpy's S_np vs its own e's: pairwise sum, argument rounding, libm ulps
         const double relNp = (double)(2 * V + 64) * kEps64 + 4.5e-16 * (2.0 * (double)mL + 64.0) + 2.0 * kRefExpErr;
         if (!sane) {
           requeue_task = true;
         } else {
-          // ------------------------------------------ H: class histogram above z_lo;
-          // each element's class offset replaces its logit (16 bits) in the stage
-          for (int b = gt; b < SG_NB; b += SG_GT) G.hist[b] = 0u;
-          ExpCtx ec;
-          ec.m = m;
-          ec.T = tv.T;
-          ec.Lhi = Lf;
-          ec.Llo = (float)(Ld - (double)Lf);
-          ec.md = (double)m;
-          ec.L16 = 16.0 * Ld;
-          const uint32_t km = key16(__float_as_uint(m));
-          // z_lo: V e(z_lo) <= (1 - top_p) S_lo / 2, so the cut lies above it
-          const double slo = fmax(S - ES, 1.0);
-          const double alo = log2(fmax(0.5 * (1.0 - tv.topp) * slo / (double)V, 1e-300));
-          int nb_eff = SG_NB;
-          {
-            const float zl = m + (float)(alo / Ld);
-            if (zl > -INFINITY) nb_eff = (int)min((uint32_t)SG_NB, km - key16(__float_as_uint(zl)) + 1u);
-          }
-          gbar(g);  // hist zeroed
-          // positive domain (every class in range positive): offset = bits(m) - bits(z)
-          const uint32_t mb16 = __float_as_uint(m) >> 16;
-          const bool pos = m > 0.0f && (uint32_t)nb_eff <= mb16 && key16_to_f(km - (uint32_t)(nb_eff - 1)) > 0.0f;
-          if (pos) {
-            for (int v = gt; v < nvec; v += SG_GT) {
-              const uint4 q = R[v];
-              uint32_t w[4] = {q.x, q.y, q.z, q.w};
-#pragma unroll
-              for (int k = 0; k < 4; ++k) {
-                const uint32_t ol = mb16 - (w[k] & 0xffffu), oh = mb16 - (w[k] >> 16);
-                if (ol < (uint32_t)nb_eff) atomicAdd(&G.hist[ol], 1u);
-                if (oh < (uint32_t)nb_eff) atomicAdd(&G.hist[oh], 1u);
-                w[k] = min(ol, 0xffffu) | (min(oh, 0xffffu) << 16);
-              }
-              R[v] = make_uint4(w[0], w[1], w[2], w[3]);
-            }
-          } else {
-            for (int v = gt; v < nvec; v += SG_GT) {
-              const uint4 q = R[v];
-              uint32_t w[4] = {q.x, q.y, q.z, q.w};
-#pragma unroll
-              for (int k = 0; k < 4; ++k) {
-                const uint32_t ol = km - key16(w[k] << 16), oh = km - key16(w[k] & 0xffff0000u);
-                if (ol < (uint32_t)nb_eff) atomicAdd(&G.hist[ol], 1u);
-                if (oh < (uint32_t)nb_eff) atomicAdd(&G.hist[oh], 1u);
-                w[k] = min(ol, 0xffffu) | (min(oh, 0xffffu) << 16);
-              }
-              R[v] = make_uint4(w[0], w[1], w[2], w[3]);
-            }
-          }
-          gbar(g);
           ST_PH(4);
           // class values (fp64 table exp, <= kLiteErr) and masses: thread owns classes
           // SGC*gt .. SGC*gt + SGC-1
@@ -536,14 +538,24 @@ __global__ void __launch_bounds__(SG_THREADS, 1) stage_kernel(StageArgs a) {
           }
           if (lane == 31) G.rd[0][gw] = incl;
           gbar(g);
-          double wpre = 0.0;
+          double wpre = 0.0, Hm = 0.0;
 #pragma unroll
-          for (int i = 0; i < SG_GW; ++i)
+          for (int i = 0; i < SG_GW; ++i) {
             if (i < gw) wpre += G.rd[0][i];
+            Hm += G.rd[0][i];
+          }
           const double u53 = kEps64;
+          const double S = Hm + tail;
           // class values vs numpy's e: table exp + numpy's argument rounding + libm ulps
           const double relArg = 4.5e-16 * (2.0 * (double)mL + 64.0);
           const double relA = kLiteErr + kRefExpErr + relArg + (double)(SG_NB + 64) * u53;
+          // |S - sum e| <= ES: classes (relA), tail: ex2.approx (numerator and emax), fp32
+          // sums of 8, the argument roundings (|a|-weighted; the m Lf term cancels)
+          // (tail arguments |a| <= 2^8 |m L| + 130: an element below -126 octaves flushes to 0
+          // and is bounded by V 2^-126; the rounding of a weighs |a| ln2 2^-23)
+          const double amax_t = 130.0 + (double)mL;
+          const double ES = Hm * relA + tail * (2.0 * kEx2Raw + kSum8Err + 1e-12 + amax_t * kLn2 * 0x1p-23) +
+                            (double)V * 0x1p-126 + S * 64.0 * u53;
           const double target = tv.topp * S;
           int cand = INT_MAX;
           {
@@ -593,18 +605,22 @@ __global__ void __launch_bounds__(SG_THREADS, 1) stage_kernel(StageArgs a) {
             const int js = G.cut_j;
             const double es = G.cut_e;
             const int nch = (V + SG_CH - 1) / SG_CH;
+            // chunk c = ids [1024 c, 1024 c + 1024): sub-chunk k is vectors 128 c + 32 k + lane
             for (int c = gw; c < nch; c += SG_GW) {
-              const int v = c * (SG_CH / 8) + lane;
               double msum = 0.0;
               int ccnt = 0;
-              if (v < nvec) {
-                const uint4 q = R[v];
-                const uint32_t w[4] = {q.x, q.y, q.z, q.w};
 #pragma unroll
-                for (int j = 0; j < 8; ++j) {
-                  const uint32_t off = (j & 1) ? off_hi(w[j >> 1]) : off_lo(w[j >> 1]);
-                  if (off < bs) msum += G.ev[off];
-                  ccnt += (off == bs);
+              for (int k = 0; k < 4; ++k) {
+                const int v = c * (SG_CH / 8) + 32 * k + lane;
+                if (v < nvec) {
+                  const uint4 q = R[v];
+                  const uint32_t w[4] = {q.x, q.y, q.z, q.w};
+#pragma unroll
+                  for (int j = 0; j < 8; ++j) {
+                    const uint32_t off = (j & 1) ? off_hi(w[j >> 1]) : off_lo(w[j >> 1]);
+                    if (off < bs) msum += G.ev[off];
+                    ccnt += (off == bs);
+                  }
                 }
               }
               msum = warp_sum(msum);
@@ -615,48 +631,28 @@ __global__ void __launch_bounds__(SG_THREADS, 1) stage_kernel(StageArgs a) {
               }
             }
             gbar(g);
-            if (gw == 0) {
-              // exclusive prefixes over chunks (4 per lane)
-              int cq[4];
-              double cmv[4];
-              int cqs = 0;
-#pragma unroll
-              for (int k = 0; k < 4; ++k) {
-                const int c = lane * 4 + k;
-                cq[k] = c < nch ? G.chc[c] : 0;
-                cqs += cq[k];
-              }
-              int cqi = cqs;
+            if (gw == 0) {  // exclusive prefixes over the (<= 32) chunks, one per lane
+              const int cq = lane < nch ? G.chc[lane] : 0;
+              int cqi = cq;
 #pragma unroll
               for (int o = 1; o < 32; o <<= 1) {
                 const int y = __shfl_up_sync(0xffffffffu, cqi, o);
                 if (lane >= o) cqi += y;
               }
-              int cpre = cqi - cqs;
-              double kms = 0.0;
-#pragma unroll
-              for (int k = 0; k < 4; ++k) {
-                const int c = lane * 4 + k;
-                const int takes = min(max(js - cpre, 0), cq[k]);
-                cmv[k] = c < nch ? G.chm[c] + (double)takes * es : 0.0;
-                if (c < nch) G.chq[c] = cpre;
-                cpre += cq[k];
-                kms += cmv[k];
-              }
-              double kmi = kms;
+              const int cpre = cqi - cq;
+              const int takes = min(max(js - cpre, 0), cq);
+              const double cmv = lane < nch ? G.chm[lane] + (double)takes * es : 0.0;
+              double kmi = cmv;
 #pragma unroll
               for (int o = 1; o < 32; o <<= 1) {
                 const double y = __shfl_up_sync(0xffffffffu, kmi, o);
                 if (lane >= o) kmi += y;
               }
-              double p = kmi - kms;
-#pragma unroll
-              for (int k = 0; k < 4; ++k) {
-                const int c = lane * 4 + k;
-                if (c < nch) G.chp[c] = p;
-                p += cmv[k];
+              if (lane < nch) {
+                G.chq[lane] = cpre;
+                G.chp[lane] = kmi - cmv;
               }
-              if (lane == 31) G.chp[nch] = p;
+              if (lane == nch - 1) G.chp[nch] = kmi;
             }
             if (gt == 0) G.uncertain = 0;
             gbar(g);
@@ -677,82 +673,131 @@ __global__ void __launch_bounds__(SG_THREADS, 1) stage_kernel(StageArgs a) {
             }
             gbar(g);
             ST_PH(6);
-            // ---------------------------------------- D: each hit chunk resolves its draws
+            // ---------------------------------------- D: each hit chunk is scanned once by one
+            // warp; its draws are then resolved in parallel, one lane per draw
             const double beta = 8.0 * kRefExpErr + kLiteErr + relArg + (double)(6 * V + 1024) * u53;
             bool unc_any = nd > SG_ND;  // (more draws than the chunk table holds: CTA kernel)
-            for (int c = gw; c < nch; c += SG_GW) {
-              const unsigned mine0 = __ballot_sync(0xffffffffu, lane < ndd && G.dch[lane] == c);
-              const unsigned mine1 = __ballot_sync(0xffffffffu, 32 + lane < ndd && G.dch[32 + lane] == c);
-              if (!(mine0 | mine1)) continue;
-              const int v = c * (SG_CH / 8) + lane;
-              uint32_t w[4] = {0xffffffffu, 0xffffffffu, 0xffffffffu, 0xffffffffu};
-              if (v < nvec) {
-                const uint4 q = R[v];
-                w[0] = q.x;
-                w[1] = q.y;
-                w[2] = q.z;
-                w[3] = q.w;
-              }
-              double k8[8];
-              int leq = 0;
+            // kept mass of the 8 ids of vector v (offsets w), cut-class ranks from r0
+            auto kept8 = [&](const uint32_t (&w)[4], int r0, double (&k8)[8]) {
 #pragma unroll
               for (int j = 0; j < 8; ++j) {
                 const uint32_t off = (j & 1) ? off_hi(w[j >> 1]) : off_lo(w[j >> 1]);
                 k8[j] = off < bs ? G.ev[off] : 0.0;
-                leq += (off == bs);
+                if (off == bs) k8[j] = (r0++ < js) ? es : 0.0;
               }
-              // ranks of the cut class in id order: chunk prefix + lanes before + in-lane
-              int eqi = leq;
+            };
+            for (int c = gw; c < nch; c += SG_GW) {
+              const unsigned mine0 = __ballot_sync(0xffffffffu, lane < ndd && G.dch[lane] == c);
+              const unsigned mine1 = __ballot_sync(0xffffffffu, 32 + lane < ndd && G.dch[32 + lane] == c);
+              if (!(mine0 | mine1)) continue;
+              // per sub-chunk k: lane's kept mass and cut-class count, exclusive lane prefixes
+              double lb[4];   // id-order prefix (from the chunk start) before this lane's vector
+              int rb[4];      // cut-class rank before this lane's vector
+              double kt = G.chp[c];
+              int rt = G.chq[c];
 #pragma unroll
-              for (int o = 1; o < 32; o <<= 1) {
-                const int y = __shfl_up_sync(0xffffffffu, eqi, o);
-                if (lane >= o) eqi += y;
-              }
-              int rank = G.chq[c] + eqi - leq;
-#pragma unroll
-              for (int j = 0; j < 8; ++j) {
-                const uint32_t off = (j & 1) ? off_hi(w[j >> 1]) : off_lo(w[j >> 1]);
-                if (off == bs) {
-                  if (rank < js) k8[j] = es;
-                  ++rank;
+              for (int k = 0; k < 4; ++k) {
+                const int v = c * (SG_CH / 8) + 32 * k + lane;
+                uint32_t w[4] = {0xffffffffu, 0xffffffffu, 0xffffffffu, 0xffffffffu};
+                if (v < nvec) {
+                  const uint4 q = R[v];
+                  w[0] = q.x;
+                  w[1] = q.y;
+                  w[2] = q.z;
+                  w[3] = q.w;
                 }
-              }
-              double lsum = 0.0;
+                double ls = 0.0;
+                int le = 0;
 #pragma unroll
-              for (int j = 0; j < 8; ++j) lsum += k8[j];
-              double li = lsum;
+                for (int j = 0; j < 8; ++j) {
+                  const uint32_t off = (j & 1) ? off_hi(w[j >> 1]) : off_lo(w[j >> 1]);
+                  ls += off < bs ? G.ev[off] : 0.0;
+                  le += (off == bs);
+                }
+                double li = ls;
+                int ei = le;
 #pragma unroll
-              for (int o = 1; o < 32; o <<= 1) {
-                const double y = __shfl_up_sync(0xffffffffu, li, o);
-                if (lane >= o) li += y;
+                for (int o = 1; o < 32; o <<= 1) {
+                  const double y = __shfl_up_sync(0xffffffffu, li, o);
+                  const int z = __shfl_up_sync(0xffffffffu, ei, o);
+                  if (lane >= o) {
+                    li += y;
+                    ei += z;
+                  }
+                }
+                // the cut class's kept ties inside this lane's vector
+                const int r0 = rt + ei - le;
+                const double lk = ls + (double)(min(max(js - r0, 0), le)) * es;
+                // redo the inclusive prefix with the ties' masses (rare: only where le > 0)
+                double lki = lk;
+#pragma unroll
+                for (int o = 1; o < 32; o <<= 1) {
+                  const double y = __shfl_up_sync(0xffffffffu, lki, o);
+                  if (lane >= o) lki += y;
+                }
+                lb[k] = kt + lki - lk;
+                rb[k] = r0;
+                kt += __shfl_sync(0xffffffffu, lki, 31);
+                rt += __shfl_sync(0xffffffffu, ei, 31);
               }
-              const double base = G.chp[c] + (li - lsum);
+              // one lane per draw: sub-chunk and lane by comparing with the 128 vector prefixes
               for (int half = 0; half < 2; ++half) {
-                unsigned mine = half ? mine1 : mine0;
-                while (mine) {
-                  const int d = 32 * half + __ffs(mine) - 1;
-                  mine &= mine - 1;
-                  const double tau = G.dtau[d];
-                  const unsigned hit = __ballot_sync(0xffffffffu, lsum > 0.0 && base + lsum > tau);
+                const unsigned mine = half ? mine1 : mine0;
+                if (!mine) continue;
+                const int d = 32 * half + lane;
+                const bool act = (mine >> lane) & 1u;
+                const double tau = act ? G.dtau[d] : 0.0;
+                // largest (k, l) with lb[k] at lane l <= tau: search k then lane (5 steps)
+                int kk = 0;
+#pragma unroll
+                for (int k = 1; k < 4; ++k) {
+                  const double b0 = __shfl_sync(0xffffffffu, lb[k], 0);
+                  if (b0 <= tau) kk = k;
+                }
+                int hl = 0;
+#pragma unroll
+                for (int st = 16; st > 0; st >>= 1) {
+                  double bk = 0.0;
+#pragma unroll
+                  for (int k = 0; k < 4; ++k) {
+                    const double y = __shfl_sync(0xffffffffu, lb[k], (hl + st) & 31);
+                    if (k == kk) bk = y;
+                  }
+                  if (bk <= tau) hl += st;
+                }
+                double base = 0.0;
+                int r0 = 0;
+#pragma unroll
+                for (int k = 0; k < 4; ++k) {
+                  const double y = __shfl_sync(0xffffffffu, lb[k], hl);
+                  const int z = __shfl_sync(0xffffffffu, rb[k], hl);
+                  if (k == kk) {
+                    base = y;
+                    r0 = z;
+                  }
+                }
+                if (act) {
+                  const int v = c * (SG_CH / 8) + 32 * kk + hl;
                   bool unc = true;
-                  if (hit != 0) {
-                    const int hl = __ffs(hit) - 1;
-                    if (lane == hl) {
-                      double E = base;
-                      int jj = 0;
-                      for (; jj < 8; ++jj) {
-                        if (k8[jj] > 0.0 && E + k8[jj] > tau) break;
-                        E += k8[jj];
-                      }
-                      if (jj == 8) jj = 7;  // (rounding: treated as uncertain below)
+                  if (v < nvec) {
+                    const uint4 q = R[v];
+                    const uint32_t w[4] = {q.x, q.y, q.z, q.w};
+                    double k8[8];
+                    kept8(w, r0, k8);
+                    double E = base;
+                    int jj = 0;
+                    for (; jj < 8; ++jj) {
+                      if (k8[jj] > 0.0 && E + k8[jj] > tau) break;
+                      E += k8[jj];
+                    }
+                    if (jj < 8) {
                       const double Ein = E + k8[jj];
-                      unc = !(Ein - tau > 2.0 * beta * Ak) || !(tau - E > 2.0 * beta * Ak) || k8[jj] == 0.0;
+                      unc = !(Ein - tau > 2.0 * beta * Ak) || !(tau - E > 2.0 * beta * Ak);
                       if (!unc) {
                         io.token[d0 + d] = 8 * v + jj;
                         if (io.flags) io.flags[d0 + d] = 0;
                       }
                     }
-                    unc = __shfl_sync(0xffffffffu, unc, hl);
                   }
                   unc_any |= unc;
                 }
