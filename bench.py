@@ -155,6 +155,19 @@ def setup_workload(cfg, dev, rank, world=1):
                 bufs={})
 
 
+def traffic_per_launch(cfg, n_rows):
+    """DRAM bytes of one resample launch, from the committed ncu --set full capture
+    (profiles/*traffic*.json: read + write bytes per row of the staged kernel), or None."""
+    import glob
+
+    files = sorted(glob.glob(os.path.join(ROOT, "profiles", "*traffic_stage.json")))
+    if not files or cfg["dtype"] != "bfloat16" or cfg["V"] > 32000:
+        return None
+    with open(files[-1]) as f:
+        d = json.load(f)
+    return d["dram_bytes_per_row"] * n_rows
+
+
 def run_ours(args, cfg, rank, world, dev):
     import torch
     import torch.distributed as dist
@@ -301,8 +314,8 @@ def run_ours(args, cfg, rank, world, dev):
         "unresolved_draws": unresolved,
         "bad_rows": bad,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                     "frac": achieved / peak, "traffic": None, "peak_source": peak_src,
-                     "kernel": "lc_cache_resample (rowwarp_kernel + resample_kernel + exact_kernel)",
+                     "frac": achieved / peak, "traffic": traffic_per_launch(cfg, n_rows), "peak_source": peak_src,
+                     "kernel": "lc_cache_resample (stage_kernel + resample_kernel requeue + exact_kernel)",
                      "kernel_ms_avg": k_avg, "algorithmic_bytes_per_launch": algo_bytes_launch},
         "e2e": {"value": tokens_total / (e2e_ms * 1e-3), "unit": "tokens/s", "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": d2h},
