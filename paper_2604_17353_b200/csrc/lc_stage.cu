@@ -51,8 +51,8 @@ constexpr double kLn2 = 0.6931471805599453;
 constexpr float kEx2Bf16Err = 0.01f;  // measured max 0.0071 (2^-7.1)
 
 struct SgGroup {
-  uint32_t hist[SG_NB];
-  double ev[SG_NB];         // class values e_b (valid where hist[b] > 0)
+  uint32_t hist[SG_NB + 32];  // + one dump bin per lane (branch-free out-of-range increments)
+  double ev[SG_NB + 32];    // class values e_b (valid where hist[b] > 0); + one 0.0 per lane
   double chm[SG_NCH];       // chunk mass of classes above the cut class
   double chp[SG_NCH + 1];   // exclusive prefix of chunk kept masses
   int chc[SG_NCH];          // chunk count of the cut class
@@ -156,6 +156,23 @@ __device__ __forceinline__ float key16_to_f(uint32_t k) {
 }
 __device__ __forceinline__ uint32_t off_lo(uint32_t w) { return w & 0xffffu; }
 __device__ __forceinline__ uint32_t off_hi(uint32_t w) { return w >> 16; }
+
+// predicated shared-memory increment / fp64 gather-add, branch-free (no BSSY/BSYNC
+// around each element)
+__device__ __forceinline__ void pinc(uint32_t* addr, bool p) {
+  asm volatile(
+      "{\n .reg .pred q;\n setp.ne.u32 q, %1, 0;\n @q red.shared.add.u32 [%0], 1;\n}" ::"r"(smem_u32(addr)),
+      "r"((uint32_t)p)
+      : "memory");
+}
+__device__ __forceinline__ double pgather(const double* base, uint32_t idx, bool p) {
+  double r;
+  asm volatile(
+      "{\n .reg .pred q;\n setp.ne.u32 q, %2, 0;\n mov.f64 %0, 0d0000000000000000;\n @q ld.shared.f64 %0, [%1];\n}"
+      : "=d"(r)
+      : "r"(smem_u32(base) + 8u * idx), "r"((uint32_t)p));
+  return r;
+}
 
 // ---- the kernel --------------------------------------------------------------------------------
 
@@ -283,6 +300,7 @@ __global__ void __launch_bounds__(SG_THREADS, 1) stage_kernel(StageArgs a) {
     sm.fq_tail = sm.fq_head = sm.fq_done = 0;
   }
   if (tid < 16) sm.t16[tid] = exp2((double)tid / 16.0);
+  if (tid < 32 * SG_GROUPS) sm.g[tid >> 5].ev[SG_NB + (tid & 31)] = 0.0;
   __syncthreads();
 
   if (warp == SG_PWARP) {
@@ -337,6 +355,7 @@ __global__ void __launch_bounds__(SG_THREADS, 1) stage_kernel(StageArgs a) {
 
     // ------------------------------------------------ A: max (packed, NaN-propagating)
     uint32_t mx2 = 0xff80ff80u;
+    #pragma unroll 4
     for (int v = gt; v < nvec; v += SG_GT) {
       const uint4 q = R[v];
       mx2 = bmax2_nan(mx2, bmax2_nan(bmax2_nan(q.x, q.y), bmax2_nan(q.z, q.w)));
@@ -402,6 +421,7 @@ __global__ void __launch_bounds__(SG_THREADS, 1) stage_kernel(StageArgs a) {
         const uint32_t nmLb = bf16_bits(-(m * Lbf));
         const uint32_t L2 = Lb | (Lb << 16), nmL2 = nmLb | (nmLb << 16);
         float acc = 0.0f;
+        #pragma unroll 4
         for (int v = gt; v < nvec; v += SG_GT) {
           const uint4 q = R[v];
           acc = bacc2(acc, bex2(bfma2(q.x, L2, nmL2)));
@@ -462,6 +482,7 @@ __global__ void __launch_bounds__(SG_THREADS, 1) stage_kernel(StageArgs a) {
           // offsets of both halves at once: bits(m) - bits(z) per 16-bit lane (VIADD.16x2);
           // negative z wrap to >= bits(m) + 1 > nb_eff, never a kept class
           const uint32_t mb2 = (mb16 | (mb16 << 16)) + 0x00010001u;
+          #pragma unroll 4
           for (int v = gt; v < nvec; v += SG_GT) {
             const uint4 q = R[v];
             const uint32_t w[4] = {q.x, q.y, q.z, q.w};
@@ -472,8 +493,8 @@ __global__ void __launch_bounds__(SG_THREADS, 1) stage_kernel(StageArgs a) {
               o[k] = __vadd2(~w[k], mb2);
               const uint32_t ol = o[k] & 0xffffu, oh = o[k] >> 16;
               const bool il = ol < (uint32_t)nb_eff, ih = oh < (uint32_t)nb_eff;
-              if (il) atomicAdd(&G.hist[ol], 1u);
-              if (ih) atomicAdd(&G.hist[oh], 1u);
+              atomicAdd(&G.hist[il ? ol : SG_NB + lane], 1u);
+              atomicAdd(&G.hist[ih ? oh : SG_NB + lane], 1u);
               const float el = ex2_approx(fmaf(lo_f(w[k]), Lf, nmL));  // -inf -> 0
               const float eh = ex2_approx(fmaf(hi_f(w[k]), Lf, nmL));
               e8[2 * k] = il ? 0.0f : el;
@@ -483,6 +504,7 @@ __global__ void __launch_bounds__(SG_THREADS, 1) stage_kernel(StageArgs a) {
             R[v] = make_uint4(o[0], o[1], o[2], o[3]);
           }
         } else {
+          #pragma unroll 4
           for (int v = gt; v < nvec; v += SG_GT) {
             const uint4 q = R[v];
             const uint32_t w[4] = {q.x, q.y, q.z, q.w};
@@ -492,8 +514,8 @@ __global__ void __launch_bounds__(SG_THREADS, 1) stage_kernel(StageArgs a) {
             for (int k = 0; k < 4; ++k) {
               const uint32_t ol = km - key16(w[k] << 16), oh = km - key16(w[k] & 0xffff0000u);
               const bool il = ol < (uint32_t)nb_eff, ih = oh < (uint32_t)nb_eff;
-              if (il) atomicAdd(&G.hist[ol], 1u);
-              if (ih) atomicAdd(&G.hist[oh], 1u);
+              atomicAdd(&G.hist[il ? ol : SG_NB + lane], 1u);
+              atomicAdd(&G.hist[ih ? oh : SG_NB + lane], 1u);
               const float el = ex2_approx(fmaf(lo_f(w[k]), Lf, nmL));
               const float eh = ex2_approx(fmaf(hi_f(w[k]), Lf, nmL));
               e8[2 * k] = il ? 0.0f : el;
@@ -618,7 +640,7 @@ __global__ void __launch_bounds__(SG_THREADS, 1) stage_kernel(StageArgs a) {
 #pragma unroll
                   for (int j = 0; j < 8; ++j) {
                     const uint32_t off = (j & 1) ? off_hi(w[j >> 1]) : off_lo(w[j >> 1]);
-                    if (off < bs) msum += G.ev[off];
+                    msum += G.ev[off < bs ? off : SG_NB + lane];
                     ccnt += (off == bs);
                   }
                 }
@@ -682,7 +704,7 @@ __global__ void __launch_bounds__(SG_THREADS, 1) stage_kernel(StageArgs a) {
 #pragma unroll
               for (int j = 0; j < 8; ++j) {
                 const uint32_t off = (j & 1) ? off_hi(w[j >> 1]) : off_lo(w[j >> 1]);
-                k8[j] = off < bs ? G.ev[off] : 0.0;
+                k8[j] = G.ev[off < bs ? off : SG_NB + lane];
                 if (off == bs) k8[j] = (r0++ < js) ? es : 0.0;
               }
             };
@@ -711,7 +733,7 @@ __global__ void __launch_bounds__(SG_THREADS, 1) stage_kernel(StageArgs a) {
 #pragma unroll
                 for (int j = 0; j < 8; ++j) {
                   const uint32_t off = (j & 1) ? off_hi(w[j >> 1]) : off_lo(w[j >> 1]);
-                  ls += off < bs ? G.ev[off] : 0.0;
+                  ls += G.ev[off < bs ? off : SG_NB + lane];
                   le += (off == bs);
                 }
                 double li = ls;
