@@ -736,21 +736,20 @@ __global__ void __launch_bounds__(SG_THREADS, 1) stage_kernel(StageArgs a) {
                   ls += G.ev[off < bs ? off : SG_NB + lane];
                   le += (off == bs);
                 }
-                double li = ls;
-                int ei = le;
+                // the cut class's kept ties (only sub-chunks holding some pay for their ranks)
+                int r0 = rt;
+                double lk = ls;
+                if (__ballot_sync(0xffffffffu, le > 0)) {
+                  int ei = le;
 #pragma unroll
-                for (int o = 1; o < 32; o <<= 1) {
-                  const double y = __shfl_up_sync(0xffffffffu, li, o);
-                  const int z = __shfl_up_sync(0xffffffffu, ei, o);
-                  if (lane >= o) {
-                    li += y;
-                    ei += z;
+                  for (int o = 1; o < 32; o <<= 1) {
+                    const int z = __shfl_up_sync(0xffffffffu, ei, o);
+                    if (lane >= o) ei += z;
                   }
+                  r0 = rt + ei - le;
+                  lk = ls + (double)(min(max(js - r0, 0), le)) * es;
+                  rt += __shfl_sync(0xffffffffu, ei, 31);
                 }
-                // the cut class's kept ties inside this lane's vector
-                const int r0 = rt + ei - le;
-                const double lk = ls + (double)(min(max(js - r0, 0), le)) * es;
-                // redo the inclusive prefix with the ties' masses (rare: only where le > 0)
                 double lki = lk;
 #pragma unroll
                 for (int o = 1; o < 32; o <<= 1) {
@@ -760,7 +759,6 @@ __global__ void __launch_bounds__(SG_THREADS, 1) stage_kernel(StageArgs a) {
                 lb[k] = kt + lki - lk;
                 rb[k] = r0;
                 kt += __shfl_sync(0xffffffffu, lki, 31);
-                rt += __shfl_sync(0xffffffffu, ei, 31);
               }
               // one lane per draw: sub-chunk and lane by comparing with the 128 vector prefixes
               for (int half = 0; half < 2; ++half) {
