@@ -434,3 +434,46 @@ def test_staged_kernel_matches_oracle_and_other_tiers(conc, T, p, nd, monkeypatc
     monkeypatch.setenv("LCB_NO_STAGE", "1")
     tok2, _, _ = _resample_rows(rows, T, None, p, ulists, dtype=torch.bfloat16)
     assert tok2.tolist() == tok.tolist()
+
+
+def _stage_rows_and_cases():
+    """bf16 V=32000 rows that drive the staged kernel's less common branches."""
+    V = 32000
+    rng = np.random.default_rng(404)
+    rows, cases = [], []
+    base = mixing_ref.fill_rows_np([mixing_ref.mix2(31, i) for i in range(8)], V, 2.5)
+    # all-negative rows (generic key path; max < 0)
+    rows.append(base[0] - 20.0)
+    # max in [0.5, 2]: histogram classes cross zero (generic key path)
+    rows.append(base[1] * 0.2)
+    # heavy ties at the cut: values from a small set
+    rows.append(rng.choice(np.float32([3.0, 2.5, 2.0, 1.5, 1.0, 0.0, -1.0]), V).astype(np.float32))
+    # flat row: huge nucleus
+    rows.append(rng.uniform(-1, 1, V).astype(np.float32))
+    # +-0 maximum (requeued to the CTA kernel)
+    z = np.full(V, -3.0, np.float32)
+    z[5], z[17] = -0.0, 0.0
+    rows.append(z)
+    # a peak plus a dense shoulder
+    z = base[2].copy()
+    z[100:400] = 14.0
+    rows.append(z)
+    return mixing_ref.bf16_round(np.stack(rows)), V
+
+
+@pytest.mark.parametrize("T,p,nd", [(0.6, 0.9, 32), (1.0, 0.5, 8), (0.3, 0.999, 16), (0.0, 0.9, 4),
+                                    (0.8, 0.9, 100)])
+def test_staged_kernel_edge_rows(T, p, nd):
+    """Staged-kernel branches (negative / zero-crossing maxima, ties at the cut,
+    flat rows, signed-zero maxima, greedy rows, more draws than it keeps)
+    against the oracle, and bit-identical to the row-warp path."""
+    rows, V = _stage_rows_and_cases()
+    rng = np.random.default_rng(int(T * 1000 + p * 100 + nd))
+    ulists = [rng.random(nd) for _ in range(len(rows))]
+    tok, fl, _ = _resample_rows(rows, T, None, p, ulists, dtype=torch.bfloat16)
+    want = []
+    for r in range(len(rows)):
+        q = sampling_ref.truncate(sampling_ref.softmax(rows[r], T), None, p)
+        want += [sampling_ref.draw(q, float(x)) for x in ulists[r]]
+    assert tok.tolist() == want
+    assert not np.any(fl & _capi.LC_DRAW_UNRESOLVED)
