@@ -354,17 +354,23 @@ __global__ void __launch_bounds__(SG_THREADS, 1) stage_kernel(StageArgs a) {
     const int nd = (int)(tv.d1 - tv.d0);
 
     // ------------------------------------------------ A: max (packed, NaN-propagating)
-    uint32_t mx2 = 0xff80ff80u;
-    #pragma unroll 4
+    float tmax = -INFINITY;
+    int tpos = -1;  // first vector of this thread holding its maximum
+    bool nan = false;
+#pragma unroll 4
     for (int v = gt; v < nvec; v += SG_GT) {
       const uint4 q = R[v];
-      mx2 = bmax2_nan(mx2, bmax2_nan(bmax2_nan(q.x, q.y), bmax2_nan(q.z, q.w)));
+      const uint32_t x = bmax2_nan(bmax2_nan(q.x, q.y), bmax2_nan(q.z, q.w));
+      const float vm = max_nan(lo_f(x), hi_f(x));
+      nan |= vm != vm;
+      if (vm > tmax) {
+        tmax = vm;
+        tpos = v;
+      }
     }
-    const float tmax = max_nan(lo_f(mx2), hi_f(mx2));
     {
-      const bool tn = tmax != tmax;
-      const float wm = warp_max(tn ? INFINITY : tmax);
-      const bool wn = __any_sync(0xffffffffu, tn);
+      const float wm = warp_max(tmax);
+      const bool wn = __any_sync(0xffffffffu, nan);
       if (lane == 0) {
         G.rf[gw] = wm;
         G.ri[0][gw] = wn;
@@ -381,19 +387,19 @@ __global__ void __launch_bounds__(SG_THREADS, 1) stage_kernel(StageArgs a) {
     // (a zero maximum with both signed zeros present has a different first argmax
     // in the reference's value order: left to the CTA kernel, like non-finite rows)
     bad |= !(m > -INFINITY) || !(m < INFINITY) || m == 0.0f;
-    auto first_argmax = [&]() -> int {  // only threads holding the maximum search
+    // this thread's candidate for the first argmax (its first vector holding m)
+    auto argmax_cand = [&]() -> int {
       int best = INT_MAX;
-      if (tmax == m) {
-        for (int v = gt; v < nvec && best == INT_MAX; v += SG_GT) {
-          const uint4 q = R[v];
-          const uint32_t w[4] = {q.x, q.y, q.z, q.w};
+      if (tpos >= 0 && tmax == m) {
+        const uint4 q = R[tpos];
+        const uint32_t w[4] = {q.x, q.y, q.z, q.w};
 #pragma unroll
-          for (int j = 7; j >= 0; --j)
-            if (((j & 1) ? hi_f(w[j >> 1]) : lo_f(w[j >> 1])) == m) best = 8 * v + j;
-        }
+        for (int j = 7; j >= 0; --j)
+          if (((j & 1) ? hi_f(w[j >> 1]) : lo_f(w[j >> 1])) == m) best = 8 * tpos + j;
       }
-      return gmin_i(best, 1);
+      return best;
     };
+    auto first_argmax = [&]() -> int { return gmin_i(argmax_cand(), 1); };
     ST_PH(1);
     if (prof) ph[9]++;
     auto write_tok = [&](int tok) {
@@ -415,6 +421,7 @@ __global__ void __launch_bounds__(SG_THREADS, 1) stage_kernel(StageArgs a) {
       const float mL = fabsf(m) * Lf;
       bool fast = false;
       double Sfast = 1.0;  // FAST estimate of the row mass (within its bound factor)
+      int amax = INT_MAX;  // first argmax (set with the FAST mass)
       if (mL <= 128.0f && Lf < 1e30f) {
         const uint32_t Lb = bf16_bits(Lf);
         const float Lbf = __uint_as_float(Lb << 16);
@@ -429,7 +436,22 @@ __global__ void __launch_bounds__(SG_THREADS, 1) stage_kernel(StageArgs a) {
           acc = bacc2(acc, bex2(bfma2(q.z, L2, nmL2)));
           acc = bacc2(acc, bex2(bfma2(q.w, L2, nmL2)));
         }
-        const double Sc = gsum_d((double)acc, 0);
+        // one barrier for the mass and the first argmax
+        {
+          const float ws = warp_sum(acc);
+          const int wc = warp_min_int(argmax_cand());
+          if (lane == 0) {
+            G.rd[0][gw] = (double)ws;
+            G.ri[1][gw] = wc;
+          }
+        }
+        gbar(g);
+        double Sc = 0.0;
+#pragma unroll
+        for (int i = 0; i < SG_GW; ++i) {
+          Sc += G.rd[0][i];
+          amax = min(amax, G.ri[1][i]);
+        }
         const uint32_t mb = bf16_bits(m);
         const float emax = lo_f(bex2(bfma2(mb | (mb << 16), L2, nmL2)));
         // exponent error <= 2^-8 (1.001 |a| + |delta|), |delta| <= 2^-9 |m Lb|;
@@ -443,7 +465,7 @@ __global__ void __launch_bounds__(SG_THREADS, 1) stage_kernel(StageArgs a) {
       }
       ST_PH(2);
       if (fast) {
-        write_tok(first_argmax());
+        write_tok(amax);
         ST_PH(3);
       } else {
         if (prof) ph[10]++;
