@@ -427,15 +427,16 @@ __global__ void __launch_bounds__(SG_THREADS, 1) stage_kernel(StageArgs a) {
         const float Lbf = __uint_as_float(Lb << 16);
         const uint32_t nmLb = bf16_bits(-(m * Lbf));
         const uint32_t L2 = Lb | (Lb << 16), nmL2 = nmLb | (nmLb << 16);
-        float acc = 0.0f;
-        #pragma unroll 4
+        float ac0 = 0.0f, ac1 = 0.0f, ac2 = 0.0f, ac3 = 0.0f;  // independent FHADD chains
+#pragma unroll 4
         for (int v = gt; v < nvec; v += SG_GT) {
           const uint4 q = R[v];
-          acc = bacc2(acc, bex2(bfma2(q.x, L2, nmL2)));
-          acc = bacc2(acc, bex2(bfma2(q.y, L2, nmL2)));
-          acc = bacc2(acc, bex2(bfma2(q.z, L2, nmL2)));
-          acc = bacc2(acc, bex2(bfma2(q.w, L2, nmL2)));
+          ac0 = bacc2(ac0, bex2(bfma2(q.x, L2, nmL2)));
+          ac1 = bacc2(ac1, bex2(bfma2(q.y, L2, nmL2)));
+          ac2 = bacc2(ac2, bex2(bfma2(q.z, L2, nmL2)));
+          ac3 = bacc2(ac3, bex2(bfma2(q.w, L2, nmL2)));
         }
+        const float acc = (ac0 + ac1) + (ac2 + ac3);
         // one barrier for the mass and the first argmax
         {
           const float ws = warp_sum(acc);
