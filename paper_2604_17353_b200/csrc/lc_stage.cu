@@ -38,8 +38,7 @@ constexpr int SG_THREADS = (SG_PWARP + 1) * 32;  // 512
 constexpr int SG_MAXV = 32000;
 constexpr int SG_STAGE_BYTES = SG_MAXV * 2;
 constexpr int SG_NB = 512;                       // histogram classes below the max
-constexpr int SG_CH = 1024;                      // ids per chunk (4 sub-chunks of one warp x 8 per lane)
-constexpr int SG_NCH = (SG_MAXV + SG_CH - 1) / SG_CH;  // 32
+constexpr int SG_NCH = (SG_MAXV / 8 + 31) / 32;       // 256-id sub-chunks (one vector per lane): 125
 constexpr int SG_NU = 32;                        // uniforms precomputed per task (one per producer lane)
 constexpr int SG_ND = 64;                        // draws per task handled here (more: CTA kernel)
 constexpr int SG_PB = 8;                         // tasks per producer grab
@@ -53,10 +52,10 @@ constexpr float kEx2Bf16Err = 0.01f;  // measured max 0.0071 (2^-7.1)
 struct SgGroup {
   uint32_t hist[SG_NB + 32];  // + one dump bin per lane (branch-free out-of-range increments)
   double ev[SG_NB + 32];    // class values e_b (valid where hist[b] > 0); + one 0.0 per lane
-  double chm[SG_NCH];       // chunk mass of classes above the cut class
-  double chp[SG_NCH + 1];   // exclusive prefix of chunk kept masses
-  int chc[SG_NCH];          // chunk count of the cut class
-  int chq[SG_NCH + 1];      // exclusive prefix of chc
+  double chm[128];          // sub-chunk mass of classes above the cut class
+  double chp[129];          // exclusive prefix of sub-chunk kept masses
+  int chc[128];             // sub-chunk count of the cut class
+  int chq[129];             // exclusive prefix of chc
   double su[SG_NU];         // the task's first uniforms
   double dtau[SG_ND];       // big nucleus: draw targets u * K
   int dch[SG_ND];           // and their chunks
@@ -645,69 +644,110 @@ __global__ void __launch_bounds__(SG_THREADS, 1) stage_kernel(StageArgs a) {
             requeue_task = true;
             if (gt == 0) atomicAdd(&a.counters[4], 1ull);
           } else {
-            // ---------------------------------------- C: chunk kept masses (stored offsets)
+            // ---------------------------------------- C: kept mass of every 256-id sub-chunk
+            // (32 vectors: one per lane) from the stored offsets; warps take 1024-id chunks
             const uint32_t bs = (uint32_t)G.cut_b;
             const int js = G.cut_j;
             const double es = G.cut_e;
-            const int nch = (V + SG_CH - 1) / SG_CH;
-            // chunk c = ids [1024 c, 1024 c + 1024): sub-chunk k is vectors 128 c + 32 k + lane
-            for (int c = gw; c < nch; c += SG_GW) {
-              double msum = 0.0;
-              int ccnt = 0;
+            const int nsub = (nvec + 31) >> 5;  // sub-chunks of 256 ids
+            for (int c = gw; 4 * c < nsub; c += SG_GW) {
+              double msum[4];
+              int ccnt[4];
 #pragma unroll
               for (int k = 0; k < 4; ++k) {
-                const int v = c * (SG_CH / 8) + 32 * k + lane;
+                const int v = 32 * (4 * c + k) + lane;
+                msum[k] = 0.0;
+                ccnt[k] = 0;
                 if (v < nvec) {
                   const uint4 q = R[v];
                   const uint32_t w[4] = {q.x, q.y, q.z, q.w};
 #pragma unroll
                   for (int j = 0; j < 8; ++j) {
                     const uint32_t off = (j & 1) ? off_hi(w[j >> 1]) : off_lo(w[j >> 1]);
-                    msum += G.ev[off < bs ? off : SG_NB + lane];
-                    ccnt += (off == bs);
+                    msum[k] += G.ev[off < bs ? off : SG_NB + lane];
+                    ccnt[k] += (off == bs);
                   }
                 }
               }
-              msum = warp_sum(msum);
-              ccnt = warp_sum(ccnt);
-              if (lane == 0) {
-                G.chm[c] = msum;
-                G.chc[c] = ccnt;
+              // reduce-scatter of the four sub-chunk sums: lanes 8k..8k+7 end with sub-chunk k
+              {
+                const bool h16 = lane & 16, h8 = lane & 8;
+                double a0 = h16 ? msum[2] : msum[0], a1 = h16 ? msum[3] : msum[1];
+                double b0 = h16 ? msum[0] : msum[2], b1 = h16 ? msum[1] : msum[3];
+                int i0 = h16 ? ccnt[2] : ccnt[0], i1 = h16 ? ccnt[3] : ccnt[1];
+                int j0 = h16 ? ccnt[0] : ccnt[2], j1 = h16 ? ccnt[1] : ccnt[3];
+                a0 += __shfl_xor_sync(0xffffffffu, b0, 16);
+                a1 += __shfl_xor_sync(0xffffffffu, b1, 16);
+                i0 += __shfl_xor_sync(0xffffffffu, j0, 16);
+                i1 += __shfl_xor_sync(0xffffffffu, j1, 16);
+                double a = h8 ? a1 : a0, b = h8 ? a0 : a1;
+                int ia = h8 ? i1 : i0, ib = h8 ? i0 : i1;
+                a += __shfl_xor_sync(0xffffffffu, b, 8);
+                ia += __shfl_xor_sync(0xffffffffu, ib, 8);
+#pragma unroll
+                for (int o = 4; o > 0; o >>= 1) {
+                  a += __shfl_xor_sync(0xffffffffu, a, o);
+                  ia += __shfl_xor_sync(0xffffffffu, ia, o);
+                }
+                const int k = lane >> 3;
+                if ((lane & 7) == 0 && 4 * c + k < nsub) {
+                  G.chm[4 * c + k] = a;
+                  G.chc[4 * c + k] = ia;
+                }
               }
             }
             gbar(g);
-            if (gw == 0) {  // exclusive prefixes over the (<= 32) chunks, one per lane
-              const int cq = lane < nch ? G.chc[lane] : 0;
-              int cqi = cq;
+            if (gw == 0) {  // exclusive prefixes over the (<= 128) sub-chunks, 4 per lane
+              int cq[4];
+              double cmv[4];
+              int cqs = 0;
+#pragma unroll
+              for (int k = 0; k < 4; ++k) {
+                const int c = 4 * lane + k;
+                cq[k] = c < nsub ? G.chc[c] : 0;
+                cqs += cq[k];
+              }
+              int cqi = cqs;
 #pragma unroll
               for (int o = 1; o < 32; o <<= 1) {
                 const int y = __shfl_up_sync(0xffffffffu, cqi, o);
                 if (lane >= o) cqi += y;
               }
-              const int cpre = cqi - cq;
-              const int takes = min(max(js - cpre, 0), cq);
-              const double cmv = lane < nch ? G.chm[lane] + (double)takes * es : 0.0;
-              double kmi = cmv;
+              int cpre = cqi - cqs;
+              double kms = 0.0;
+#pragma unroll
+              for (int k = 0; k < 4; ++k) {
+                const int c = 4 * lane + k;
+                const int takes = min(max(js - cpre, 0), cq[k]);
+                cmv[k] = c < nsub ? G.chm[c] + (double)takes * es : 0.0;
+                if (c < nsub) G.chq[c] = cpre;
+                cpre += cq[k];
+                kms += cmv[k];
+              }
+              double kmi = kms;
 #pragma unroll
               for (int o = 1; o < 32; o <<= 1) {
                 const double y = __shfl_up_sync(0xffffffffu, kmi, o);
                 if (lane >= o) kmi += y;
               }
-              if (lane < nch) {
-                G.chq[lane] = cpre;
-                G.chp[lane] = kmi - cmv;
+              double pp = kmi - kms;
+#pragma unroll
+              for (int k = 0; k < 4; ++k) {
+                const int c = 4 * lane + k;
+                if (c < nsub) G.chp[c] = pp;
+                pp += cmv[k];
               }
-              if (lane == nch - 1) G.chp[nch] = kmi;
+              if (lane == 31) G.chp[nsub] = pp;
             }
             if (gt == 0) G.uncertain = 0;
             gbar(g);
-            const double Ak = G.chp[nch];
+            const double Ak = G.chp[nsub];
             const int ndd = min(nd, SG_ND);
-            // each draw's chunk (binary search over the prefix), lanes in parallel
+            // each draw's sub-chunk (binary search over the prefix), lanes in parallel
             for (int d = gt; d < ndd; d += SG_GT) {
               const double u = d < SG_NU ? G.su[d] : draw_u(io, d0 + d, tv);
               const double tau = u * Ak;
-              int lo = 0, hi = nch;  // first chunk whose inclusive prefix > tau
+              int lo = 0, hi = nsub;  // first sub-chunk whose inclusive prefix > tau
               while (lo < hi) {
                 const int mid = (lo + hi) >> 1;
                 if (G.chp[mid + 1] <= tau) lo = mid + 1;
@@ -718,137 +758,96 @@ __global__ void __launch_bounds__(SG_THREADS, 1) stage_kernel(StageArgs a) {
             }
             gbar(g);
             ST_PH(6);
-            // ---------------------------------------- D: each hit chunk is scanned once by one
-            // warp; its draws are then resolved in parallel, one lane per draw
+            // ---------------------------------------- D: each hit sub-chunk is scanned once by
+            // one warp (one vector per lane); its draws are resolved in parallel, one lane each
             const double beta = 8.0 * kRefExpErr + kLiteErr + relArg + (double)(6 * V + 1024) * u53;
-            bool unc_any = nd > SG_ND;  // (more draws than the chunk table holds: CTA kernel)
-            // kept mass of the 8 ids of vector v (offsets w), cut-class ranks from r0
-            auto kept8 = [&](const uint32_t (&w)[4], int r0, double (&k8)[8]) {
+            bool unc_any = nd > SG_ND;  // (more draws than the table holds: CTA kernel)
+            for (int sc = gw; sc < nsub; sc += SG_GW) {
+              const unsigned mine0 = __ballot_sync(0xffffffffu, lane < ndd && G.dch[lane] == sc);
+              const unsigned mine1 = __ballot_sync(0xffffffffu, 32 + lane < ndd && G.dch[32 + lane] == sc);
+              if (!(mine0 | mine1)) continue;
+              const int v = 32 * sc + lane;
+              uint32_t w[4] = {0xffffffffu, 0xffffffffu, 0xffffffffu, 0xffffffffu};
+              if (v < nvec) {
+                const uint4 q = R[v];
+                w[0] = q.x;
+                w[1] = q.y;
+                w[2] = q.z;
+                w[3] = q.w;
+              }
+              double k8[8];
+              int le = 0;
 #pragma unroll
               for (int j = 0; j < 8; ++j) {
                 const uint32_t off = (j & 1) ? off_hi(w[j >> 1]) : off_lo(w[j >> 1]);
                 k8[j] = G.ev[off < bs ? off : SG_NB + lane];
-                if (off == bs) k8[j] = (r0++ < js) ? es : 0.0;
+                le += (off == bs);
               }
-            };
-            for (int c = gw; c < nch; c += SG_GW) {
-              const unsigned mine0 = __ballot_sync(0xffffffffu, lane < ndd && G.dch[lane] == c);
-              const unsigned mine1 = __ballot_sync(0xffffffffu, 32 + lane < ndd && G.dch[32 + lane] == c);
-              if (!(mine0 | mine1)) continue;
-              // per sub-chunk k: lane's kept mass and cut-class count, exclusive lane prefixes
-              double lb[4];   // id-order prefix (from the chunk start) before this lane's vector
-              int rb[4];      // cut-class rank before this lane's vector
-              double kt = G.chp[c];
-              int rt = G.chq[c];
+              // the cut class's kept ties (only sub-chunks holding some pay for their ranks)
+              if (__ballot_sync(0xffffffffu, le > 0)) {
+                int ei = le;
 #pragma unroll
-              for (int k = 0; k < 4; ++k) {
-                const int v = c * (SG_CH / 8) + 32 * k + lane;
-                uint32_t w[4] = {0xffffffffu, 0xffffffffu, 0xffffffffu, 0xffffffffu};
-                if (v < nvec) {
-                  const uint4 q = R[v];
-                  w[0] = q.x;
-                  w[1] = q.y;
-                  w[2] = q.z;
-                  w[3] = q.w;
+                for (int o = 1; o < 32; o <<= 1) {
+                  const int z = __shfl_up_sync(0xffffffffu, ei, o);
+                  if (lane >= o) ei += z;
                 }
-                double ls = 0.0;
-                int le = 0;
+                int r0 = G.chq[sc] + ei - le;
 #pragma unroll
                 for (int j = 0; j < 8; ++j) {
                   const uint32_t off = (j & 1) ? off_hi(w[j >> 1]) : off_lo(w[j >> 1]);
-                  ls += G.ev[off < bs ? off : SG_NB + lane];
-                  le += (off == bs);
+                  if (off == bs) k8[j] = (r0++ < js) ? es : 0.0;
                 }
-                // the cut class's kept ties (only sub-chunks holding some pay for their ranks)
-                int r0 = rt;
-                double lk = ls;
-                if (__ballot_sync(0xffffffffu, le > 0)) {
-                  int ei = le;
-#pragma unroll
-                  for (int o = 1; o < 32; o <<= 1) {
-                    const int z = __shfl_up_sync(0xffffffffu, ei, o);
-                    if (lane >= o) ei += z;
-                  }
-                  r0 = rt + ei - le;
-                  lk = ls + (double)(min(max(js - r0, 0), le)) * es;
-                  rt += __shfl_sync(0xffffffffu, ei, 31);
-                }
-                double lki = lk;
-#pragma unroll
-                for (int o = 1; o < 32; o <<= 1) {
-                  const double y = __shfl_up_sync(0xffffffffu, lki, o);
-                  if (lane >= o) lki += y;
-                }
-                lb[k] = kt + lki - lk;
-                rb[k] = r0;
-                kt += __shfl_sync(0xffffffffu, lki, 31);
               }
-              // one lane per draw: sub-chunk and lane by comparing with the 128 vector prefixes
+              double ls = 0.0;
+#pragma unroll
+              for (int j = 0; j < 8; ++j) ls += k8[j];
+              double li = ls;
+#pragma unroll
+              for (int o = 1; o < 32; o <<= 1) {
+                const double y = __shfl_up_sync(0xffffffffu, li, o);
+                if (lane >= o) li += y;
+              }
+              const double lb = G.chp[sc] + li - ls;  // prefix before this lane's vector
               for (int half = 0; half < 2; ++half) {
                 const unsigned mine = half ? mine1 : mine0;
                 if (!mine) continue;
                 const int d = 32 * half + lane;
                 const bool act = (mine >> lane) & 1u;
                 const double tau = act ? G.dtau[d] : 0.0;
-                // largest (k, l) with lb[k] at lane l <= tau: search k then lane (5 steps)
-                int kk = 0;
-#pragma unroll
-                for (int k = 1; k < 4; ++k) {
-                  const double b0 = __shfl_sync(0xffffffffu, lb[k], 0);
-                  if (b0 <= tau) kk = k;
-                }
-                int hl = 0;
+                int hl = 0;  // last lane whose prefix <= tau
 #pragma unroll
                 for (int st = 16; st > 0; st >>= 1) {
-                  double bk = 0.0;
-#pragma unroll
-                  for (int k = 0; k < 4; ++k) {
-                    const double y = __shfl_sync(0xffffffffu, lb[k], (hl + st) & 31);
-                    if (k == kk) bk = y;
-                  }
-                  if (bk <= tau) hl += st;
+                  const double y = __shfl_sync(0xffffffffu, lb, hl + st);
+                  if (y <= tau) hl += st;
                 }
-                double base = 0.0;
-                int r0 = 0;
+                const double base = __shfl_sync(0xffffffffu, lb, hl);
+                // the hit lane's 8 kept masses, walked by the draw's lane
+                double kk[8];
 #pragma unroll
-                for (int k = 0; k < 4; ++k) {
-                  const double y = __shfl_sync(0xffffffffu, lb[k], hl);
-                  const int z = __shfl_sync(0xffffffffu, rb[k], hl);
-                  if (k == kk) {
-                    base = y;
-                    r0 = z;
-                  }
-                }
+                for (int j = 0; j < 8; ++j) kk[j] = __shfl_sync(0xffffffffu, k8[j], hl);
                 if (act) {
-                  const int v = c * (SG_CH / 8) + 32 * kk + hl;
+                  double E = base;
+                  int jj = 0;
+                  for (; jj < 8; ++jj) {
+                    if (kk[jj] > 0.0 && E + kk[jj] > tau) break;
+                    E += kk[jj];
+                  }
                   bool unc = true;
-                  if (v < nvec) {
-                    const uint4 q = R[v];
-                    const uint32_t w[4] = {q.x, q.y, q.z, q.w};
-                    double k8[8];
-                    kept8(w, r0, k8);
-                    double E = base;
-                    int jj = 0;
-                    for (; jj < 8; ++jj) {
-                      if (k8[jj] > 0.0 && E + k8[jj] > tau) break;
-                      E += k8[jj];
-                    }
-                    if (jj < 8) {
-                      const double Ein = E + k8[jj];
-                      unc = !(Ein - tau > 2.0 * beta * Ak) || !(tau - E > 2.0 * beta * Ak);
-                      if (!unc) {
-                        io.token[d0 + d] = 8 * v + jj;
-                        if (io.flags) io.flags[d0 + d] = 0;
-                      }
+                  if (jj < 8 && 32 * sc + hl < nvec) {
+                    const double Ein = E + kk[jj];
+                    unc = !(Ein - tau > 2.0 * beta * Ak) || !(tau - E > 2.0 * beta * Ak);
+                    if (!unc) {
+                      io.token[d0 + d] = 8 * (32 * sc + hl) + jj;
+                      if (io.flags) io.flags[d0 + d] = 0;
                     }
                   }
                   unc_any |= unc;
                 }
               }
             }
-            // draws whose target fell past the last chunk (rounding at u ~ 1)
+            // draws whose target fell past the last sub-chunk (rounding at u ~ 1)
             for (int d = gt; d < ndd; d += SG_GT)
-              if (G.dch[d] >= nch) unc_any = true;
+              if (G.dch[d] >= nsub) unc_any = true;
             if (unc_any) G.uncertain = 1;
             gbar(g);
             ST_PH(7);
