@@ -633,16 +633,17 @@ __global__ void __launch_bounds__(SG_THREADS, 1) stage_kernel(StageArgs a) {
             bool zero_clash = false;
             if (kb == 0x8000u) zero_clash = bstar + 1 < nb_eff && G.hist[bstar + 1] > 0;
             if (kb == 0x7fffu) zero_clash = bstar >= 1 && G.hist[bstar - 1] > 0;
-            G.cut_ok = ok_hi && ok_lo && !zero_clash;
+            G.cut_ok = zero_clash ? 2 : (ok_hi && ok_lo);
             G.cut_b = bstar;
             G.cut_j = j;
             G.cut_e = e;
           }
           gbar(g);
           ST_PH(5);
-          if (!G.cut_ok) {
+          if (G.cut_ok != 1) {
             requeue_task = true;
-            if (gt == 0) atomicAdd(&a.counters[4], 1ull);
+            // counters: 4 cut not certified, 6 no cut class in the histogram range, 7 +-0 cut
+            if (gt == 0) atomicAdd(&a.counters[bstar == INT_MAX ? 6 : (G.cut_ok == 0 ? 4 : 7)], 1ull);
           } else {
             // ---------------------------------------- C: kept mass of every 256-id sub-chunk
             // (32 vectors: one per lane) from the stored offsets; warps take 1024-id chunks
