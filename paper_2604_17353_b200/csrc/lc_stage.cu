@@ -598,52 +598,82 @@ __global__ void __launch_bounds__(SG_THREADS, 1) stage_kernel(StageArgs a) {
           // (tail arguments |a| <= 2^8 |m L| + 130: an element below -126 octaves flushes to 0
           // and is bounded by V 2^-126; the rounding of a weighs |a| ln2 2^-23)
           const double amax_t = 130.0 + (double)mL;
-          const double ES = Hm * relA + tail * (2.0 * kEx2Raw + kSum8Err + 1e-12 + amax_t * kLn2 * 0x1p-23) +
-                            (double)V * 0x1p-126 + S * 64.0 * u53;
-          const double target = tv.topp * S;
-          int cand = INT_MAX;
-          {
-            double ex = wpre + incl - tsum;
+          double Scut = S;
+          double EScut = Hm * relA + tail * (2.0 * kEx2Raw + kSum8Err + 1e-12 + amax_t * kLn2 * 0x1p-23) +
+                         (double)V * 0x1p-126 + S * 64.0 * u53;
+          int bstar = INT_MAX;
+          for (int pass = 0; pass < 2; ++pass) {
+            if (pass == 1) {
+              // PRECISE tail (rare: the FAST tail's bound left the cut undecided): every tail
+              // element's logit is recovered from its stored offset (both encodings are
+              // 16-bit bijections) and its fp64 table exponential summed
+              double tp2 = 0.0;
+              for (int v = gt; v < nvec; v += SG_GT) {
+                const uint4 q = R[v];
+                const uint32_t w[4] = {q.x, q.y, q.z, q.w};
 #pragma unroll
-            for (int k = 0; k < SGC; ++k) {
-              if (cand == INT_MAX && cnt[k] > 0 && ex + ms[k] >= target) cand = SGC * gt + k;
-              ex += ms[k];
+                for (int j = 0; j < 8; ++j) {
+                  const uint32_t off = (j & 1) ? off_hi(w[j >> 1]) : off_lo(w[j >> 1]);
+                  if (off >= (uint32_t)nb_eff) {
+                    const float z = pos ? __uint_as_float(((mb16 - off) & 0xffffu) << 16)
+                                        : key16_to_f((km - off) & 0xffffu);
+                    tp2 += lite_exp(ec, z, sm.t16);
+                  }
+                }
+              }
+              const double tailp = gsum_d(tp2, 2);
+              Scut = Hm + tailp;
+              EScut = (Hm + tailp) * relA + (double)V * 0x1p-126 + Scut * (double)(V + 64) * u53;
             }
-          }
-          const int bstar = gmin_i(cand, 0);
-          if (gt == 0) G.cut_ok = 0;
-          gbar(g);
-          if (bstar != INT_MAX && bstar / SGC == gt) {
-            double A = wpre + incl - tsum;
-            int n = 0;
+            const double target = tv.topp * Scut;
+            int cand = INT_MAX;
+            {
+              double ex = wpre + incl - tsum;
 #pragma unroll
-            for (int k = 0; k < SGC; ++k) {
-              if (SGC * gt + k < bstar) A += ms[k];
-              if (SGC * gt + k == bstar) n = cnt[k];
+              for (int k = 0; k < SGC; ++k) {
+                if (cand == INT_MAX && cnt[k] > 0 && ex + ms[k] >= target) cand = SGC * gt + k;
+                ex += ms[k];
+              }
             }
-            const double e = G.ev[bstar];
-            const double jd = ceil((target - A) / e);
-            const int j = (int)fmin(fmax(jd, 1.0), (double)n);
-            const double rho = relA + ES / S + relNp + (double)(V + 8) * u53;
-            const bool ok_hi = (A + (double)j * e) / S * (1.0 - rho) >= tv.topp;
-            const bool ok_lo = (A + (double)(j - 1) * e) / S * (1.0 + rho) < tv.topp;
-            // +-0 are one value for the reference (equal p, id order): a cut on a zero
-            // class with the other zero class present is left to the CTA kernel
-            const uint32_t kb = km - (uint32_t)bstar;
-            bool zero_clash = false;
-            if (kb == 0x8000u) zero_clash = bstar + 1 < nb_eff && G.hist[bstar + 1] > 0;
-            if (kb == 0x7fffu) zero_clash = bstar >= 1 && G.hist[bstar - 1] > 0;
-            G.cut_ok = zero_clash ? 2 : (ok_hi && ok_lo);
-            G.cut_b = bstar;
-            G.cut_j = j;
-            G.cut_e = e;
+            bstar = gmin_i(cand, 0);
+            if (gt == 0) G.cut_ok = 0;
+            gbar(g);
+            if (bstar != INT_MAX && bstar / SGC == gt) {
+              double A = wpre + incl - tsum;
+              int n = 0;
+#pragma unroll
+              for (int k = 0; k < SGC; ++k) {
+                if (SGC * gt + k < bstar) A += ms[k];
+                if (SGC * gt + k == bstar) n = cnt[k];
+              }
+              const double e = G.ev[bstar];
+              const double jd = ceil((target - A) / e);
+              const int j = (int)fmin(fmax(jd, 1.0), (double)n);
+              const double rho = relA + EScut / Scut + relNp + (double)(V + 8) * u53;
+              const bool ok_hi = (A + (double)j * e) / Scut * (1.0 - rho) >= tv.topp;
+              const bool ok_lo = (A + (double)(j - 1) * e) / Scut * (1.0 + rho) < tv.topp;
+              // +-0 are one value for the reference (equal p, id order): a cut on a zero
+              // class with the other zero class present is left to the CTA kernel
+              const uint32_t kb = km - (uint32_t)bstar;
+              bool zero_clash = false;
+              if (kb == 0x8000u) zero_clash = bstar + 1 < nb_eff && G.hist[bstar + 1] > 0;
+              if (kb == 0x7fffu) zero_clash = bstar >= 1 && G.hist[bstar - 1] > 0;
+              G.cut_ok = zero_clash ? 2 : (ok_hi && ok_lo);
+              G.cut_b = bstar;
+              G.cut_j = j;
+              G.cut_e = e;
+            }
+            gbar(g);
+            if (G.cut_ok != 0 || bstar == INT_MAX) break;
+            if (pass == 0 && gt == 0) atomicAdd(&a.counters[7], 1ull);  // precise tails computed
           }
           gbar(g);
           ST_PH(5);
           if (G.cut_ok != 1) {
             requeue_task = true;
-            // counters: 4 cut not certified, 6 no cut class in the histogram range, 7 +-0 cut
-            if (gt == 0) atomicAdd(&a.counters[bstar == INT_MAX ? 6 : (G.cut_ok == 0 ? 4 : 7)], 1ull);
+            // counters: 4 cut not certified (even with the precise tail), 6 no cut class in the
+            // histogram range (or a +-0 cut); 7 counts precise-tail recomputations
+            if (gt == 0) atomicAdd(&a.counters[(bstar == INT_MAX || G.cut_ok == 2) ? 6 : 4], 1ull);
           } else {
             // ---------------------------------------- C: kept mass of every 256-id sub-chunk
             // (32 vectors: one per lane) from the stored offsets; warps take 1024-id chunks
