@@ -81,6 +81,7 @@ struct __align__(128) SgSmem {
   // producer batch
   TaskView pbv[SG_PB];
   int pbt[SG_PB];
+  double pbu[SG_PB][SG_NU];
   double t16[16];
   unsigned long long full[SG_GROUPS];
 };
@@ -232,6 +233,19 @@ __device__ void sg_producer(const StageArgs& a, SgSmem& sm, int lane) {
         }
         __syncwarp();
         nb = __popc(okm);
+        // the batch's first SG_NU uniforms, all seed loads in flight together
+        double ub[SG_PB];
+#pragma unroll
+        for (int j = 0; j < SG_PB; ++j) {
+          ub[j] = 0.0;
+          if (j < nb) {
+            const TaskView& tj = sm.pbv[j];
+            if (tj.d0 + lane < tj.d1) ub[j] = draw_u(a.io, tj.d0 + lane, tj);
+          }
+        }
+#pragma unroll
+        for (int j = 0; j < SG_PB; ++j) sm.pbu[j][lane] = ub[j];
+        __syncwarp();
       }
     }
     const int npush = nb > 0 ? nb : (done ? SG_GROUPS - sentinels : 0);
@@ -243,7 +257,7 @@ __device__ void sg_producer(const StageArgs& a, SgSmem& sm, int lane) {
       const int slot = slot_seq % SG_FQ;
       if (nb > 0) {
         const TaskView& tj = sm.pbv[j];
-        sm.fq_u[slot][lane] = tj.d0 + lane < tj.d1 ? draw_u(a.io, tj.d0 + lane, tj) : 0.0;
+        sm.fq_u[slot][lane] = sm.pbu[j][lane];
         if (lane == 0) {
           sm.fq_tv[slot] = tj;
           sm.fq_task[slot] = sm.pbt[j];

@@ -50,13 +50,15 @@ def main():
         cnt.zero_()
         s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         s.record()
-        lcb.resample(rows, tt, seeds=seeds, n_draws=n * a.draws, counters=cnt)
+        tok_out = torch.full((n * a.draws,), -7, dtype=torch.int32, device=dev)
+        fl_out = torch.zeros(n * a.draws, dtype=torch.uint8, device=dev)
+        lcb.resample(rows, tt, seeds=seeds, n_draws=n * a.draws, counters=cnt, out=(tok_out, fl_out))
         e.record()
         torch.cuda.synchronize()
         ms = s.elapsed_time(e)
         gb = n * a.V * rows.element_size() / 1e9
         print(f"iter {i}: {ms:.3f} ms  {n / ms / 1e3:.2f} M rows/s  {gb / ms * 1e3:.1f} GB/s  "
-              f"counters {cnt.cpu().tolist()}", flush=True)
+              f"counters {cnt.cpu().tolist()}  unwritten {int((tok_out == -7).sum())}", flush=True)
         if os.environ.get("LCB_STAGE_PROF") == "1":
             import ctypes
             buf = (ctypes.c_ulonglong * 12)()
