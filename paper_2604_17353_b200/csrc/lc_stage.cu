@@ -38,7 +38,6 @@ constexpr int SG_THREADS = (SG_PWARP + 1) * 32;  // 512
 constexpr int SG_MAXV = 32000;
 constexpr int SG_STAGE_BYTES = SG_MAXV * 2;
 constexpr int SG_NB = 512;                       // histogram classes below the max
-constexpr int SG_NCH = (SG_MAXV / 8 + 31) / 32;       // 256-id sub-chunks (one vector per lane): 125
 constexpr int SG_NU = 32;                        // uniforms precomputed per task (one per producer lane)
 constexpr int SG_ND = 64;                        // draws per task handled here (more: CTA kernel)
 constexpr int SG_PB = 8;                         // tasks per producer grab
