@@ -2554,7 +2554,13 @@ static int launch_all(const char* rows, int64_t row_bytes, int V, const lc_task*
   const char* ft = getenv("LCB_FORCE_TIER");
   const int force = !ft ? 0 : (ft[0] == 'p' ? 1 : (ft[0] == 'e' ? 2 : 0));
   const char* ns = getenv("LCB_NO_STAGE");
-  if (rw && force == 0 && !(ns && ns[0] == '1') && stage_eligible(DT, V, row_bytes, rows)) {
+  const bool wide = force == 0 && !(ns && ns[0] == '1') && wide_eligible(DT, V, row_bytes, rows);
+  if (wide) {
+    // bf16 rows wider than 32000 ids: the TMA-staged top-k kernel (lc_wide.cu) takes the
+    // top-k tasks and requeues everything else to the CTA kernel below
+    const int rc = wide_launch(rows, row_bytes, V, tasks, n_tasks, cm, io, rw_next, ws.q_cta, counters, num_sms(), st);
+    if (rc != LC_OK) return rc;
+  } else if (rw && force == 0 && !(ns && ns[0] == '1') && stage_eligible(DT, V, row_bytes, rows)) {
     // bf16 rows <= 32768 ids: TMA-staged persistent kernel (lc_stage.cu); it requeues
     // what it does not handle or cannot certify to the CTA kernel below
     LCB_CUDA_TRY(cudaMemsetAsync(rw_next, 0, 4, st));
@@ -2591,7 +2597,7 @@ static int launch_all(const char* rows, int64_t row_bytes, int V, const lc_task*
   }
   const int g1 = (int)(n_tasks < grid ? n_tasks : grid);
   resample_kernel<DT><<<g1, RS_THREADS, smem, st>>>(rows, row_bytes, V, tasks, (int)n_tasks, cm, io, ws, counters,
-                                                    rw, force);
+                                                    (rw || wide) ? 1 : 0, force);
   LCB_CUDA_TRY(cudaGetLastError());
   static bool ex_attr[2] = {false, false};
   if (!ex_attr[DT]) {

@@ -27,6 +27,7 @@
 #include "lc_common.cuh"
 #include "lc_resample.cuh"
 #include "lc_task.cuh"
+#include "lc_stage.cuh"
 
 namespace lcb {
 
@@ -86,115 +87,7 @@ struct __align__(128) SgSmem {
 };
 static_assert(sizeof(SgSmem) <= 232448, "staged kernel shared memory");
 
-// ---- PTX helpers ------------------------------------------------------------------------------
-
-__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
-
-__device__ __forceinline__ void mbar_init(unsigned long long* bar, int count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
-}
-__device__ __forceinline__ void mbar_fence_init() { asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory"); }
-__device__ __forceinline__ void mbar_expect_tx(unsigned long long* bar, uint32_t bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
-}
-__device__ __forceinline__ void mbar_arrive(unsigned long long* bar) {
-  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
-}
-__device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t bytes, unsigned long long* bar) {
-  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-                   smem_u32(dst)),
-               "l"(src), "r"(bytes), "r"(smem_u32(bar))
-               : "memory");
-}
-__device__ __forceinline__ void mbar_wait(unsigned long long* bar, uint32_t phase) {
-  asm volatile(
-      "{\n"
-      " .reg .pred p;\n"
-      "WAIT_%=:\n"
-      " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
-      " @!p bra WAIT_%=;\n"
-      "}\n" ::"r"(smem_u32(bar)),
-      "r"(phase)
-      : "memory");
-}
-// named barrier of group g (ids 1..SG_GROUPS)
-__device__ __forceinline__ void gbar(int g) { asm volatile("bar.sync %0, %1;" ::"r"(g + 1), "n"(SG_GT) : "memory"); }
-
-__device__ __forceinline__ uint32_t bmax2_nan(uint32_t a, uint32_t b) {
-  uint32_t r;
-  asm("max.NaN.bf16x2 %0, %1, %2;" : "=r"(r) : "r"(a), "r"(b));
-  return r;
-}
-__device__ __forceinline__ uint32_t bfma2(uint32_t a, uint32_t b, uint32_t c) {
-  uint32_t r;
-  asm("fma.rn.bf16x2 %0, %1, %2, %3;" : "=r"(r) : "r"(a), "r"(b), "r"(c));
-  return r;
-}
-__device__ __forceinline__ uint32_t bex2(uint32_t a) {
-  uint32_t r;
-  asm("ex2.approx.ftz.bf16x2 %0, %1;" : "=r"(r) : "r"(a));
-  return r;
-}
-// acc + lo(e) + hi(e), the bf16 halves added straight into fp32 (FHADD.BF16)
-__device__ __forceinline__ float bacc2(float acc, uint32_t e) {
-  asm("{\n .reg .b16 lo, hi;\n mov.b32 {lo, hi}, %1;\n add.rn.f32.bf16 %0, lo, %0;\n add.rn.f32.bf16 %0, hi, %0;\n}"
-      : "+f"(acc)
-      : "r"(e));
-  return acc;
-}
-__device__ __forceinline__ uint32_t bf16_bits(float f) { return (uint32_t)f32_to_bf16_bits(f); }
-__device__ __forceinline__ float lo_f(uint32_t w) { return __uint_as_float(w << 16); }
-__device__ __forceinline__ float hi_f(uint32_t w) { return __uint_as_float(w & 0xffff0000u); }
-// order key of a bf16 value given as fp32 bits (larger value -> larger key; -0 < +0)
-__device__ __forceinline__ uint32_t key16(uint32_t fbits) {
-  return (fbits ^ ((uint32_t)((int32_t)fbits >> 31) | 0x80000000u)) >> 16;
-}
-__device__ __forceinline__ float key16_to_f(uint32_t k) {
-  const uint32_t h = (k & 0x8000u) ? (k & 0x7fffu) : (~k & 0xffffu);
-  return __uint_as_float(h << 16);
-}
-__device__ __forceinline__ uint32_t off_lo(uint32_t w) { return w & 0xffffu; }
-__device__ __forceinline__ uint32_t off_hi(uint32_t w) { return w >> 16; }
-
-// predicated shared-memory increment / fp64 gather-add, branch-free (no BSSY/BSYNC
-// around each element)
-__device__ __forceinline__ void pinc(uint32_t* addr, bool p) {
-  asm volatile(
-      "{\n .reg .pred q;\n setp.ne.u32 q, %1, 0;\n @q red.shared.add.u32 [%0], 1;\n}" ::"r"(smem_u32(addr)),
-      "r"((uint32_t)p)
-      : "memory");
-}
-__device__ __forceinline__ double pgather(const double* base, uint32_t idx, bool p) {
-  double r;
-  asm volatile(
-      "{\n .reg .pred q;\n setp.ne.u32 q, %2, 0;\n mov.f64 %0, 0d0000000000000000;\n @q ld.shared.f64 %0, [%1];\n}"
-      : "=d"(r)
-      : "r"(smem_u32(base) + 8u * idx), "r"((uint32_t)p));
-  return r;
-}
-
-// ---- the kernel --------------------------------------------------------------------------------
-
-struct StageArgs {
-  const char* rows;
-  int64_t row_bytes;
-  int Vdef;
-  const lc_task* tasks;
-  int n_tasks;
-  CacheMap cm;
-  DrawIO io;
-  int* next;   // dynamic task counter
-  int* q_cta;  // requeue: [0] count, [1..] task ids (CTA kernel)
-  unsigned long long* counters;
-  unsigned long long* prof;  // optional per-phase clock totals (LCB_STAGE_PROF=1)
-};
-
-__device__ __forceinline__ void requeue(const StageArgs& a, int task_id) {
-  const int pos = atomicAdd(a.q_cta, 1);
-  a.q_cta[1 + pos] = task_id;
-}
-
-__device__ __forceinline__ int vload(const int* p) { return *reinterpret_cast<const volatile int*>(p); }
+__device__ __forceinline__ void gbar(int g) { gbar_n<SG_GT>(g); }
 
 // producer warp: grab SG_PB tasks per atomic, resolve them in parallel lanes, compute
 // their first SG_NU uniforms, publish them through the FIFO; SG_GROUPS sentinels at the end
@@ -914,6 +807,17 @@ __global__ void __launch_bounds__(SG_THREADS, 1) stage_kernel(StageArgs a) {
 }
 
 static unsigned long long* g_stage_prof = nullptr;
+
+// the LCB_STAGE_PROF buffer (nullptr when profiling is off), shared with lc_wide.cu
+unsigned long long* stage_prof_buffer() {
+  static unsigned long long* prof = nullptr;
+  const char* pe = getenv("LCB_STAGE_PROF");
+  if (!(pe && pe[0] == '1')) return nullptr;
+  if (!prof && cudaMalloc(&prof, 16 * sizeof(unsigned long long)) == cudaSuccess)
+    cudaMemset(prof, 0, 16 * sizeof(unsigned long long));
+  g_stage_prof = prof;
+  return prof;
+}
 
 int stage_launch(const char* rows, int64_t row_bytes, int V, const lc_task* tasks, int64_t n_tasks, CacheMap cm,
                  DrawIO io, int* next, int* q_cta, unsigned long long* counters, int n_sms, cudaStream_t st) {

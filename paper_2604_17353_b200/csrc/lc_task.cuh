@@ -169,4 +169,10 @@ bool stage_eligible(int dtype, int64_t V, int64_t row_bytes, const void* rows);
 int stage_launch(const char* rows, int64_t row_bytes, int V, const lc_task* tasks, int64_t n_tasks, CacheMap cm,
                  DrawIO io, int* next, int* q_cta, unsigned long long* counters, int n_sms, cudaStream_t st);
 
+unsigned long long* stage_prof_buffer();
+// wide top-k kernel (lc_wide.cu): bf16 rows wider than 32000 ids with top-k <= 64
+bool wide_eligible(int dtype, int64_t V, int64_t row_bytes, const void* rows);
+int wide_launch(const char* rows, int64_t row_bytes, int V, const lc_task* tasks, int64_t n_tasks, CacheMap cm,
+                DrawIO io, int* next, int* q_cta, unsigned long long* counters, int n_sms, cudaStream_t st);
+
 }  // namespace lcb

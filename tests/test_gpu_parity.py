@@ -502,3 +502,25 @@ def test_staged_kernel_writes_every_draw_under_load():
     for r in range(0, n, 97):
         q = sampling_ref.truncate(sampling_ref.softmax(host[r], 0.6), None, 0.9)
         assert got[r * nd:(r + 1) * nd].tolist() == [sampling_ref.draw(q, float(x)) for x in u[r * nd:(r + 1) * nd]]
+
+
+@pytest.mark.parametrize("V,conc,T,k,p,nd", [(151936, 2.5, 0.6, 50, 0.95, 1), (151936, 0.0, 1.0, 50, 0.95, 4),
+                                             (128256, 2.5, 0.6, 20, 0.9, 8), (151936, 2.5, 0.0, 50, 0.95, 2),
+                                             (40000, 1.0, 0.8, 64, 1.0, 3), (151936, 5.0, 0.3, 1, 0.5, 2)])
+def test_wide_kernel_matches_oracle_and_cta_kernel(V, conc, T, k, p, nd, monkeypatch):
+    """The TMA-staged top-k kernel (bf16 rows wider than 32000 ids) against the
+    oracle, and bit-identical to the CTA kernel (LCB_NO_STAGE=1)."""
+    n = 24
+    rows = mixing_ref.bf16_round(mixing_ref.fill_rows_np([mixing_ref.mix2(29, i) for i in range(n)], V, conc))
+    rng = np.random.default_rng(int(V + conc * 10 + T * 100 + k))
+    ulists = [rng.random(nd) for _ in range(n)]
+    tok, fl, cnt = _resample_rows(rows, T, k, p, ulists, dtype=torch.bfloat16)
+    want = []
+    for r in range(n):
+        q = sampling_ref.truncate(sampling_ref.softmax(rows[r], T), k, p)
+        want += [sampling_ref.draw(q, float(x)) for x in ulists[r]]
+    assert tok.tolist() == want
+    assert not np.any(fl & _capi.LC_DRAW_UNRESOLVED)
+    monkeypatch.setenv("LCB_NO_STAGE", "1")
+    tok2, _, _ = _resample_rows(rows, T, k, p, ulists, dtype=torch.bfloat16)
+    assert tok2.tolist() == tok.tolist()

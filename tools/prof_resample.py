@@ -64,6 +64,12 @@ def main():
             buf = (ctypes.c_ulonglong * 12)()
             if _capi.lib.lcb_stage_prof_fetch(buf) == 0:
                 ph = list(buf)
+                if a.V > 32000:  # wide top-k kernel: 0 wait, 1 max, 2 threshold, 3 mass, 4 list, 5 final, 6 rows
+                    r_ = max(ph[6], 1)
+                    print("  wide phases, clks per row: " + "  ".join(
+                        f"{nm}={ph[k] / r_:.0f}" for k, nm in enumerate(["wait", "max", "thr", "mass", "list",
+                                                                      "final"])) + f"  rows={ph[6]}", flush=True)
+                    continue
                 rows_, big = max(ph[9], 1), max(ph[10], 1)
                 names = ["wait", "A", "B", "fastfin", "H", "cls+cut", "C", "D", "end"]
                 print("  stage phases, clks per row (per big row for H..D): " + "  ".join(
