@@ -59,6 +59,7 @@ struct SgGroup {
   double su[SG_NU];         // the task's first uniforms
   double dtau[SG_ND];       // big nucleus: draw targets u * K
   int dch[SG_ND];           // and their chunks
+  uint32_t hitm[4];         // sub-chunks hit by a draw
   double rd[3][SG_GW];
   float rf[SG_GW];
   int ri[2][SG_GW];
@@ -677,6 +678,7 @@ __global__ void __launch_bounds__(SG_THREADS, 1) stage_kernel(StageArgs a) {
               if (lane == 31) G.chp[nsub] = pp;
             }
             if (gt == 0) G.uncertain = 0;
+            if (gt < 4) G.hitm[gt] = 0u;
             gbar(g);
             const double Ak = G.chp[nsub];
             const int ndd = min(nd, SG_ND);
@@ -692,6 +694,7 @@ __global__ void __launch_bounds__(SG_THREADS, 1) stage_kernel(StageArgs a) {
               }
               G.dch[d] = lo;
               G.dtau[d] = tau;
+              if (lo < nsub) atomicOr(&G.hitm[lo >> 5], 1u << (lo & 31));
             }
             gbar(g);
             ST_PH(6);
@@ -699,7 +702,9 @@ __global__ void __launch_bounds__(SG_THREADS, 1) stage_kernel(StageArgs a) {
             // one warp (one vector per lane); its draws are resolved in parallel, one lane each
             const double beta = 8.0 * kRefExpErr + kLiteErr + relArg + (double)(6 * V + 1024) * u53;
             bool unc_any = nd > SG_ND;  // (more draws than the table holds: CTA kernel)
+            // this warp's hit sub-chunks (sc = gw mod SG_GW), from the hit mask
             for (int sc = gw; sc < nsub; sc += SG_GW) {
+              if (!((G.hitm[sc >> 5] >> (sc & 31)) & 1u)) continue;
               const unsigned mine0 = __ballot_sync(0xffffffffu, lane < ndd && G.dch[lane] == sc);
               const unsigned mine1 = __ballot_sync(0xffffffffu, 32 + lane < ndd && G.dch[32 + lane] == sc);
               if (!(mine0 | mine1)) continue;
