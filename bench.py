@@ -44,6 +44,10 @@ CONFIGS = {
     "c5": dict(V=151936, n_req=8 * 512, nb=1, R=4, T=0.6, k=50, p=0.95, dtype="bfloat16", scaling="strong",
                desc="multi-agent: 8 trees x 512 branches (4 cached rows each), vocab 151936, top-k 50 + "
                     "top-p 0.95, bf16; trees sharded tree i -> GPU i mod G"),
+    "c4": dict(V=128256, keys=1 << 20, entries=400_000, batch=8192, ins_frac=0.9, dtype="bfloat16",
+               scaling="weak", desc="cache capacity/eviction stress: 1M prefix digests (tree expansion), one "
+                                    "V=128256 bf16 row per entry, slab of up to 400k rows, 90% insert / "
+                                    "10% lookup batches"),
 }
 
 
@@ -409,6 +413,208 @@ def run_reference(args, cfg):
     }
 
 
+# ------------------------------------------------------------------------ C4: insert / eviction stress
+
+
+def c4_keys(n_keys, dev):
+    """1M distinct prefix digests by tree expansion: 1024 root prompts, each extended by
+    1024 two-token children (prefix extension = hash_tokens(child, start=root), mixing.py:63-65)."""
+    import torch
+
+    from paper_2604_17353_b200 import _capi, _dev
+
+    n_root = 1024
+    n_child = -(-n_keys // n_root)
+    roots = [[r % 256, r // 256, 7, 11, 13] for r in range(n_root)]
+    from paper_2604_17353_b200.mixing import hash_prompts
+
+    rd = hash_prompts(roots, dev=dev)
+    c = np.arange(n_root * n_child) % n_child
+    toks = torch.from_numpy(np.stack([c % 256, c // 256 + 1], 1).astype(np.int32).ravel()).to(dev)
+    offs = torch.arange(0, 2 * n_root * n_child + 1, 2, dtype=torch.int64, device=dev)
+    par = rd.repeat_interleave(n_child)
+    out = torch.empty(n_root * n_child, dtype=torch.int64, device=dev)
+    _capi.check(_capi.lib.lc_hash_prefix(toks.data_ptr(), offs.data_ptr(), par.data_ptr(), n_root * n_child,
+                                         out.data_ptr(), _dev.stream_ptr(dev)))
+    out = out[:n_keys]
+    assert torch.unique(out).numel() == n_keys
+    return out
+
+
+def c4_cpu_baseline(V, seconds=10.0, entries=10_000):
+    """The reference's update path on the host: f32 row copy + accounting + the O(E) LRU scan
+    (logits_cache.py:96-140), restated in oracle/cache_ref.py, at a reduced E."""
+    sys.path.insert(0, ROOT)
+    from oracle import cache_ref
+
+    row_acct = V * 4 + 8
+    orc = cache_ref.CacheOracle(entries * row_acct, entries + 64, entries + 64)
+    src = np.random.default_rng(0).standard_normal((4, V)).astype(np.float32)
+    store = {}
+    rng = np.random.default_rng(1)
+    for i in range(entries):  # fill (untimed)
+        orc.insert(i, 1, V)
+    n = 0
+    t0 = time.perf_counter()
+    while time.perf_counter() - t0 < seconds:
+        d = int(rng.integers(0, 1 << 20)) + entries
+        store[d & 1023] = np.array(src[n % 4], dtype=np.float32)  # reference: np.asarray(..., float32) copy
+        orc.insert(d, 1, V)
+        n += 1
+    dt = time.perf_counter() - t0
+    return {"value": n / dt, "unit": "inserts/s", "cores": 1, "kind": "port",
+            "sample": f"{n} single-row inserts (V={V}, f32 row copy + O(E) min-(last_hit, digest) victim scan "
+                      f"as logits_cache.py:96-140) into a full cache of E={entries} entries (reduced from 400k: "
+                      f"the reference's eviction is O(E) per insert), {seconds:.0f} s, one core"}
+
+
+def run_c4(args, cfg, rank, world, dev):
+    import torch
+
+    import paper_2604_17353_b200 as lcb
+    from paper_2604_17353_b200 import _capi, _dev
+
+    V = cfg["V"]
+    free, _ = torch.cuda.mem_get_info(dev)
+    S = int(min(cfg["entries"], (free * 0.6) // (V * 2)))
+    row_acct = V * 4 + 8
+    cache = lcb.LogitsCache(S * row_acct, vocab=V, dtype="bfloat16", key_capacity=S + 64, page_rows=1,
+                            max_rows=1, page_capacity=S + 64, device=dev)
+    keys = c4_keys(cfg["keys"], dev)
+    keys_h = _dev.u64_numpy(keys)
+    pool_n = 2048
+    pool = torch.empty((pool_n, V), dtype=torch.bfloat16, device=dev)
+    st = _dev.u64_tensor([(0x9E3779B97F4A7C15 * (i + 1 + (rank << 20))) & ((1 << 64) - 1) for i in range(pool_n)],
+                         dev)
+    _capi.check(_capi.lib.lc_fill_logits(st.data_ptr(), pool_n, V, 2.5, 5.0, _capi.LC_BF16, pool.data_ptr(), V,
+                                         _dev.stream_ptr(dev)))
+    ptoks = torch.arange(pool_n, dtype=torch.int32, device=dev)
+    B = cfg["batch"]
+    n_ins = int(round(B * cfg["ins_frac"]))
+    n_lk = B - n_ins
+    ones = torch.ones(max(B, 65536), dtype=torch.int32, device=dev)
+    vocs = torch.full((max(B, 65536),), V, dtype=torch.int32, device=dev)
+    trace = []  # (kind, key indices) in issue order, for the oracle replay
+
+    def insert(idx_h, idx_d, base):
+        n = idx_d.numel()
+        offs = (torch.arange(n, dtype=torch.int64, device=dev) + base) % pool_n
+        trace.append(("ins", idx_h))
+        return cache.insert_batch(keys[idx_d], ones[:n], vocs[:n], pool, offs, ptoks, 1)[0]
+
+    # prefill: S distinct keys (cache full, no evictions yet)
+    perm = np.random.default_rng(1 + rank).permutation(cfg["keys"])[:S]
+    outs = []
+    for b0 in range(0, S, 65536):
+        ih = perm[b0:b0 + 65536]
+        outs.append(insert(ih, torch.from_numpy(ih).to(dev), b0))
+    rng = np.random.default_rng(2 + rank)
+    n_steps = args.warmup + args.steps
+    # warm-up + timed steps, then args.steps fresh steps for the e2e leg
+    ops = [(rng.integers(0, cfg["keys"], n_lk), rng.integers(0, cfg["keys"], n_ins))
+           for _ in range(n_steps + args.steps)]
+    ops_d = [(torch.from_numpy(a).to(dev), torch.from_numpy(b).to(dev)) for a, b in ops]
+
+    ev = []  # CUDA events around each timed insert call (policy + copy kernels), same stream
+
+    def step(i, timed=False):
+        lk_h, in_h = ops[i]
+        lk_d, in_d = ops_d[i]
+        trace.append(("lk", lk_h))
+        s_lk = cache.lookup_batch(keys[lk_d])[0]
+        if timed:
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record()
+        s_in = insert(in_h, in_d, i * B)
+        if timed:
+            b.record()
+            ev.append((a, b))
+        return s_lk, s_in
+
+    for i in range(args.warmup):
+        outs.extend(step(i))
+    torch.cuda.synchronize(dev)
+    st0 = cache._stats()
+    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(dev.index) as clk:
+        t0.record()
+        for i in range(args.warmup, n_steps):
+            outs.extend(step(i, True))
+        t1.record()
+        torch.cuda.synchronize(dev)
+    ms = t0.elapsed_time(t1)
+    st1 = cache._stats()
+    evictions = st1.evictions - st0.evictions if hasattr(st1, "evictions") else None
+
+    ins_ms = sum(a.elapsed_time(b) for a, b in ev) / len(ev)
+
+    # parity: hit/miss + slots (which encode the victim order) vs the heap-mode oracle replay
+    parity = None
+    if not args.no_check:
+        sys.path.insert(0, ROOT)
+        from oracle import cache_ref
+
+        orc = cache_ref.CacheOracle(S * row_acct, S + 64, S + 64, 1, heap=True)
+        got = np.concatenate([o.cpu().numpy() for o in outs])
+        want = []
+        for kind, idx in trace:
+            if kind == "lk":
+                for k in idx:
+                    e = orc.lookup(int(keys_h[k]))
+                    want.append(-1 if e is None else e.slot)
+            else:
+                for k in idx:
+                    want.append(orc.insert(int(keys_h[k]), 1, V)[0].slot)
+        want = np.asarray(want[:got.size], np.int32)
+        parity = {"ops_checked": int(got.size), "slots_equal": bool(np.array_equal(got, want)),
+                  "evictions_oracle": orc.evictions}
+    peak, peak_src = peaks()
+    n_timed = args.steps * n_ins
+    algo = n_ins * (2 * V * 2 + 4 + 8 + 4)  # row read + slab write, token, digest, length per insert
+    res = {
+        "metric": "inserts_per_s", "value": n_timed * world / (ms * 1e-3), "unit": "inserts/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "bf16 rows, int64 bookkeeping",
+        "data": "synthetic (reference producer fill_logits rows, tree-expanded prefix digests)",
+        "config": {"workload": cfg["desc"], "config": "c4", "vocab": V, "entries": S, "key_space": cfg["keys"],
+                   "ops_per_step": B, "inserts_per_step": n_ins, "lookups_per_step": n_lk,
+                   "slab_gb": (S + 64) * V * 2 / 1e9, "l2": "slab writes and source rows larger than L2"},
+        "lookups_per_s": args.steps * n_lk * world / (ms * 1e-3),
+        "evictions_per_s": (evictions / (ms * 1e-3)) if evictions is not None else None,
+        "hit_ratio": (st1.hits - st0.hits) / max(1, st1.lookups - st0.lookups),
+        "parity": parity,
+        "roofline": {"bound": "hbm", "achieved": algo / (ins_ms * 1e-3) / 1e9, "peak": peak, "unit": "GB/s",
+                     "frac": algo / (ins_ms * 1e-3) / 1e9 / peak, "traffic": None, "peak_source": peak_src,
+                     "kernel": "lc_cache_insert (insert_policy_kernel + insert_copy_kernel)",
+                     "kernel_ms_avg": ins_ms, "algorithmic_bytes_per_launch": algo},
+        "gpu_launches": 4 * args.steps,
+        "clocks": clk.summary(),
+    }
+    # e2e: digests from host (pinned), slots back to host, per step
+    h_keys = [torch.from_numpy(np.concatenate([keys_h[a], keys_h[b]]).view(np.int64)).pin_memory()
+              for a, b in ops[n_steps:]]
+    d_keys = torch.empty(B, dtype=torch.int64, device=dev)
+    h_out = torch.empty(B, dtype=torch.int32, pin_memory=True)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize(dev)
+    e0.record()
+    for i in range(args.steps):
+        d_keys.copy_(h_keys[i], non_blocking=True)
+        s_lk = cache.lookup_batch(d_keys[:n_lk])[0]
+        s_in = cache.insert_batch(d_keys[n_lk:], ones[:n_ins], vocs[:n_ins], pool,
+                                  torch.arange(n_ins, dtype=torch.int64, device=dev) % pool_n, ptoks, 1)[0]
+        h_out[:n_lk].copy_(s_lk, non_blocking=True)
+        h_out[n_lk:].copy_(s_in, non_blocking=True)
+    e1.record()
+    torch.cuda.synchronize(dev)
+    e_ms = e0.elapsed_time(e1)
+    res["e2e"] = {"value": n_timed * world / (e_ms * 1e-3), "unit": "inserts/s", "h2d_bytes_per_step": B * 8,
+                  "d2h_bytes_per_step": B * 4}
+    if not args.no_cpu_baseline:
+        res["cpu_baseline"] = c4_cpu_baseline(V, seconds=min(args.cpu_seconds, 10.0))
+    return res
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -418,6 +624,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-check", action="store_true", help="c4: skip the oracle replay of the op trace")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     cfg = CONFIGS[args.config]
@@ -425,7 +632,17 @@ def main():
     rank = int(os.environ.get("RANK", "0"))
     if args.impl == "reference":
         if rank == 0:
-            print(json.dumps(run_reference(args, cfg)), flush=True)
+            if args.config == "c4":
+                cb = c4_cpu_baseline(cfg["V"], seconds=min(args.cpu_seconds, 10.0))
+                print(json.dumps({"metric": "inserts_per_s", "value": cb["value"], "unit": "inserts/s",
+                                  "impl": "reference", "n_gpus": args.gpus, "steps": args.steps,
+                                  "warmup": args.warmup, "higher_is_better": True, "scaling": "weak",
+                                  "vs_baseline": None, "dtype": "f32 (numpy)", "data": "synthetic",
+                                  "config": {"workload": cfg["desc"], "config": "c4"}, "cpu_baseline": cb,
+                                  "e2e": {"value": cb["value"], "unit": "inserts/s", "h2d_bytes_per_step": 0,
+                                          "d2h_bytes_per_step": 0}}), flush=True)
+            else:
+                print(json.dumps(run_reference(args, cfg)), flush=True)
         return
     import torch
     import torch.distributed as dist
@@ -435,7 +652,7 @@ def main():
     dev = torch.device("cuda", local)
     if world > 1:
         dist.init_process_group("nccl", device_id=dev)
-    res = run_ours(args, cfg, rank, world, dev)
+    res = (run_c4 if args.config == "c4" else run_ours)(args, cfg, rank, world, dev)
     if rank == 0:
         print(json.dumps(res), flush=True)
     if world > 1:

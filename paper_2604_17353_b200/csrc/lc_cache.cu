@@ -273,8 +273,10 @@ __device__ void evict_entry(const CacheDev& c, int s) {
   ctl->evictions += 1;
 }
 
-// One thread applies the batch in index order (logits_cache.py:96-140).
-__global__ void insert_policy_kernel(CacheDev c, const uint64_t* __restrict__ dig, const int32_t* __restrict__ lens,
+// One thread applies the batch in index order (logits_cache.py:96-140).  Kept as the
+// reference-shaped A/B path (LCB_SCALAR_POLICY=1) and as the body of the warp kernel's
+// rare fallbacks (pinned entries at the LRU end, long probe chains).
+__global__ void insert_policy_scalar_kernel(CacheDev c, const uint64_t* __restrict__ dig, const int32_t* __restrict__ lens,
                                      const int32_t* __restrict__ vocabs, int64_t n, int32_t* out_slot,
                                      uint32_t* out_gen) {
   if (threadIdx.x != 0 || blockIdx.x != 0) return;
@@ -337,6 +339,415 @@ __global__ void insert_policy_kernel(CacheDev c, const uint64_t* __restrict__ di
       evict_entry(c, v);
     }
   }
+}
+
+// ---- warp policy ------------------------------------------------------------------------
+//
+// The same sequential semantics as insert_policy_scalar_kernel, run by one warp whose 32
+// lanes hold identical copies of the control block in registers.  Each step's loads are
+// spread over lanes (one round trip instead of a dependent chain), hash probes read a
+// 32-bucket window at once, and the lines the next inserts and the next LRU victims will
+// touch are prefetched into L1 ahead of use:
+//   * input chunk c+2 is loaded, the home windows of chunk c+1 are prefetched;
+//   * the event ring is consumed through 32-position windows; the next window's events
+//     are loaded one window ahead and their slots' metadata and hash windows prefetched;
+//     events found dead stay dead (liveness is monotone: ticks are unique);
+//   * the free stacks keep their recently pushed top in a lane-distributed register window,
+//     so the pop that follows an eviction's push needs no memory round trip.
+// Only this warp touches the cache during the kernel, so L1-resident lines stay coherent.
+
+__device__ __forceinline__ void pf1(const void* p) { asm volatile("prefetch.global.L1 [%0];" ::"l"(p)); }
+
+__device__ __forceinline__ void pf_window(const CacheDev& c, uint64_t d) {
+  const uint32_t b = home_bucket(d, c.hmask);
+  pf1(c.hvals + b);
+  pf1(c.hvals + ((b + 31) & c.hmask));
+  pf1(c.hkeys + b);
+  pf1(c.hkeys + ((b + 15) & c.hmask));
+  pf1(c.hkeys + ((b + 31) & c.hmask));
+}
+
+// Register mirror of stack entries [base, base + 32): lane l holds entry base + l when bit l is set.
+struct RegStack {
+  long long base;
+  unsigned valid;
+  int val;
+};
+
+// Push v_k (held by lane k, k < m) at indices idx0 + k; lanes k < m store to memory.
+__device__ __forceinline__ void rs_push_many(RegStack& r, int32_t* arr, long long idx0, int m, int vk, int lane) {
+  if (lane < m) arr[idx0 + lane] = vk;
+  if (idx0 < r.base || idx0 + m > r.base + 32) {
+    r.base = idx0;
+    r.valid = 0;
+  }
+  const int off = (int)(idx0 - r.base);
+  const int src = lane - off;
+  const int v = __shfl_sync(0xffffffffu, vk, src & 31);
+  if (src >= 0 && src < m) r.val = v;
+  r.valid |= (m >= 32 ? 0xffffffffu : ((1u << m) - 1u)) << off;
+}
+
+// Lane k (k < m) returns entry idx_hi - k (a pop of m entries, top first).
+__device__ __forceinline__ int rs_get_many(const RegStack& r, const int32_t* arr, long long idx_hi, int m, int lane) {
+  const long long idx = idx_hi - lane;
+  const long long off = idx - r.base;
+  const bool hit = off >= 0 && off < 32 && ((r.valid >> (int)(off & 31)) & 1u);
+  const int v = __shfl_sync(0xffffffffu, r.val, (int)(off & 31));
+  if (lane >= m) return -1;
+  return hit ? v : arr[idx];
+}
+
+// 32-bucket window probe at d's home bucket.  found: slot or -1; *empty_pos: first empty
+// bucket index (absolute) or -1 when the window holds none; *chain_open: the probe chain
+// runs past the window without a verdict.
+__device__ __forceinline__ int window_find(const CacheDev& c, uint64_t d, int lane, uint32_t* empty_b, bool* open) {
+  const uint32_t b0 = home_bucket(d, c.hmask);
+  const uint32_t bl = (b0 + lane) & c.hmask;
+  const int hv = c.hvals[bl];
+  const uint64_t hk = c.hkeys[bl];
+  const unsigned em = __ballot_sync(0xffffffffu, hv < 0);
+  const unsigned mm = __ballot_sync(0xffffffffu, hv >= 0 && hk == d);
+  const int fe = em ? __ffs(em) - 1 : 32;
+  const unsigned before = fe >= 32 ? 0xffffffffu : ((1u << fe) - 1u);
+  const unsigned hit = mm & before;
+  *empty_b = fe < 32 ? ((b0 + fe) & c.hmask) : 0xffffffffu;
+  *open = !hit && fe >= 32;
+  if (!hit) return -1;
+  return __shfl_sync(0xffffffffu, hv, __ffs(hit) - 1);
+}
+
+// Backward-shift deletion of d when its chain closes inside the 32-bucket window;
+// otherwise lane 0 runs the scalar table_delete.
+__device__ void window_delete(const CacheDev& c, uint64_t d, int lane) {
+  const uint32_t b0 = home_bucket(d, c.hmask);
+  const uint32_t bl = (b0 + lane) & c.hmask;
+  const int hv = c.hvals[bl];
+  const uint64_t hk = c.hkeys[bl];
+  const unsigned em = __ballot_sync(0xffffffffu, hv < 0);
+  const unsigned mm = __ballot_sync(0xffffffffu, hv >= 0 && hk == d);
+  const int fe = em ? __ffs(em) - 1 : 32;
+  const unsigned hit = mm & (fe >= 32 ? 0xffffffffu : ((1u << fe) - 1u));
+  if (!hit) {
+    if (fe >= 32) {  // chain leaves the window
+      if (lane == 0) table_delete(c, d);
+      __syncwarp();
+    }
+    return;  // absent
+  }
+  int i = __ffs(hit) - 1;
+  if (i + 1 >= 32 || (em >> (i + 1)) == 0u) {  // shift may run past the window
+    if (lane == 0) table_delete(c, d);
+    __syncwarp();
+    return;
+  }
+  const uint32_t home_l = home_bucket(hk, c.hmask);
+  for (int j = i + 1;; ++j) {
+    const int vj = __shfl_sync(0xffffffffu, hv, j);
+    if (vj < 0) break;
+    const uint32_t k = __shfl_sync(0xffffffffu, home_l, j);
+    const uint32_t ai = (b0 + i) & c.hmask, aj = (b0 + j) & c.hmask;
+    const bool stays = (ai <= aj) ? (ai < k && k <= aj) : (ai < k || k <= aj);
+    if (stays) continue;
+    const uint64_t kj = __shfl_sync(0xffffffffu, hk, j);
+    if (lane == 0) {
+      c.hkeys[ai] = kj;
+      c.hvals[ai] = vj;
+    }
+    i = j;
+  }
+  if (lane == 0) c.hvals[(b0 + i) & c.hmask] = -1;
+  __syncwarp();
+}
+
+struct RingWin {
+  long long base;      // first position of the current window, -1 = none
+  unsigned loaded;     // positions that existed (< head) when loaded
+  unsigned dead;       // events known dead
+  int slot;            // lane l: event base + l
+  unsigned long long clock;
+  long long nbase;     // next window, loaded ahead
+  unsigned nloaded;
+  int nslot;
+  unsigned long long nclock;
+};
+
+__device__ __forceinline__ void ring_load_next(const CacheDev& c, RingWin& w, long long nb, long long head, int lane) {
+  w.nbase = nb;
+  const long long p = nb + lane;
+  const bool ok = p < head;
+  w.nloaded = __ballot_sync(0xffffffffu, ok);
+  w.nslot = ok ? c.ring_slot[p % c.R] : -1;
+  w.nclock = ok ? c.ring_clock[p % c.R] : 0ull;
+}
+
+__device__ __forceinline__ void ring_prefetch_next(const CacheDev& c, const RingWin& w) {
+  const int s = w.nslot;
+  if (s >= 0) {
+    pf1(c.alive + s);
+    pf1(c.last_hit + s);
+    pf1(c.pins + s);
+    pf1(c.nbytes + s);
+    pf1(c.digest + s);
+    pf1(c.gen + s);
+    pf1(c.pages + (int64_t)s * c.maxp);
+  }
+}
+
+// Enter the window starting at position t: take the preloaded one when it matches.
+__device__ void ring_enter(const CacheDev& c, RingWin& w, long long t, long long head, int lane) {
+  if (w.nbase != t) ring_load_next(c, w, t, head, lane);
+  w.base = w.nbase;
+  w.loaded = w.nloaded;
+  w.slot = w.nslot;
+  w.clock = w.nclock;
+  // liveness prefilter + hash windows of the live events' digests
+  const int s = w.slot;
+  bool live = false;
+  if (s >= 0) {
+    live = c.alive[s] && c.last_hit[s] == w.clock;
+    if (live) pf_window(c, c.digest[s]);
+  }
+  w.dead = __ballot_sync(0xffffffffu, !live) & w.loaded;
+  // next window: events now, metadata lines prefetched; the window after: ring lines
+  pf1(c.ring_slot + (t + 64 + lane) % c.R);
+  pf1(c.ring_clock + (t + 64 + lane) % c.R);
+  ring_load_next(c, w, t + 32, head, lane);
+  ring_prefetch_next(c, w);
+}
+
+struct Victim {
+  int s;
+  long long nbytes;
+  uint64_t digest;
+  uint32_t gen;
+  bool scalar;  // chosen by the scalar fallback (control block reloaded)
+};
+
+__device__ __forceinline__ void ctl_flush(const CacheDev& c, const Ctl& L, int lane) {
+  if (lane == 0) *c.ctl = L;
+  __syncwarp();
+}
+
+// Oldest live unpinned entry (next_victim), or s = -1.
+__device__ Victim warp_next_victim(const CacheDev& c, Ctl& L, RingWin& w, int lane) {
+  Victim v{-1, 0, 0, 0, false};
+  for (;;) {
+    if (L.side_count > 0) break;  // pinned entries pending: scalar path
+    if (L.ring_tail >= L.ring_head) return v;
+    if (w.base < 0 || L.ring_tail < w.base || L.ring_tail >= w.base + 32) ring_enter(c, w, L.ring_tail, L.ring_head, lane);
+    const int off = (int)(L.ring_tail - w.base);
+    if (!((w.loaded >> off) & 1u)) {  // appended after the window was read
+      w.base = -1;
+      w.nbase = -1;
+      continue;
+    }
+    const unsigned cand = ~w.dead & w.loaded & (0xffffffffu << off);
+    if (!cand) {
+      const unsigned rest = w.loaded & (0xffffffffu << off);
+      L.ring_tail = w.base + (32 - __clz(rest));  // every loaded event from off on is dead
+      continue;
+    }
+    const int o = __ffs(cand) - 1;
+    L.ring_tail = w.base + o;
+    const int s = __shfl_sync(0xffffffffu, w.slot, o);
+    const unsigned long long ck = __shfl_sync(0xffffffffu, w.clock, o);
+    const bool alive = c.alive[s];
+    const unsigned long long lh = c.last_hit[s];
+    const int pins = c.pins[s];
+    const long long nb = c.nbytes[s];
+    const uint64_t dg = c.digest[s];
+    const uint32_t g = c.gen[s];
+    if (!(alive && lh == ck)) {
+      w.dead |= 1u << o;
+      L.ring_tail++;
+      continue;
+    }
+    if (pins > 0) break;  // scalar path moves it to the side list
+    L.ring_tail++;
+    v.s = s;
+    v.nbytes = nb;
+    v.digest = dg;
+    v.gen = g;
+    return v;
+  }
+  // scalar fallback: the reference-shaped next_victim over the control block in memory
+  ctl_flush(c, L, lane);
+  int s = -1;
+  if (lane == 0) s = next_victim(c);
+  __syncwarp();
+  s = __shfl_sync(0xffffffffu, s, 0);
+  L = *c.ctl;
+  w.base = -1;
+  w.nbase = -1;
+  v.s = s;
+  v.scalar = true;
+  if (s >= 0) {
+    v.nbytes = c.nbytes[s];
+    v.digest = c.digest[s];
+    v.gen = c.gen[s];
+  }
+  return v;
+}
+
+__global__ void __launch_bounds__(32) insert_policy_kernel(CacheDev c, const uint64_t* __restrict__ dig,
+                                                           const int32_t* __restrict__ lens,
+                                                           const int32_t* __restrict__ vocabs, int64_t n,
+                                                           int32_t* out_slot, uint32_t* out_gen) {
+  const int lane = threadIdx.x;
+  Ctl L = *c.ctl;
+  RegStack fs{-1ll << 40, 0u, 0}, fp{-1ll << 40, 0u, 0};
+  RingWin w;
+  w.base = -1;
+  w.nbase = -1;
+  int last_ev_slot = -1;
+  uint32_t last_ev_gen = 0;
+  // chunk pipeline: cur (c), nx1 (c+1), nx2 (c+2)
+  auto ld = [&](int64_t i, uint64_t& d, int& nr, int& vv) {
+    if (i < n) {
+      d = dig[i];
+      nr = lens[i];
+      vv = vocabs[i];
+    } else {
+      d = 0;
+      nr = -1;
+      vv = 0;
+    }
+  };
+  uint64_t d0, d1, d2;
+  int n0, n1, n2, v0, v1, v2;
+  ld(lane, d0, n0, v0);
+  ld(32 + lane, d1, n1, v1);
+  if (lane < n) pf_window(c, d0);
+  for (int64_t i0 = 0; i0 < n; i0 += 32) {
+    ld(i0 + 64 + lane, d2, n2, v2);
+    if (i0 + 32 + lane < n) pf_window(c, d1);
+    int my_slot = -1;
+    uint32_t my_gen = 0;
+    const int cnt = (int)min((int64_t)32, n - i0);
+    for (int j = 0; j < cnt; ++j) {
+      const uint64_t d = __shfl_sync(0xffffffffu, d0, j);
+      const int nr = __shfl_sync(0xffffffffu, n0, j);
+      const int vv = __shfl_sync(0xffffffffu, v0, j);
+      const int np = (nr + c.page_rows - 1) / c.page_rows;
+      if (nr < 0 || vv < 1 || vv > c.V || np > c.maxp) {
+        if (!L.error) L.error = LC_E_CONFIG;
+        continue;
+      }
+      const long long bytes = (long long)nr * vv * 4 + 8ll * nr;  // logits_cache.py:54-56
+      uint32_t eb;
+      bool open;
+      int s = window_find(c, d, lane, &eb, &open);
+      if (open) {
+        if (lane == 0) s = table_find(c, d);
+        s = __shfl_sync(0xffffffffu, s, 0);
+      }
+      uint32_t g;
+      if (s >= 0) {  // overwrite: the key keeps its slot, the entry is new
+        L.total_bytes -= c.nbytes[s];
+        for (int k0 = 0; k0 < c.maxp; k0 += 32) {  // push_pages
+          const int k = k0 + lane;
+          const int pg = k < c.maxp ? c.pages[(int64_t)s * c.maxp + k] : -1;
+          const unsigned have = __ballot_sync(0xffffffffu, pg >= 0);
+          const int m = __ffs(~have) - 1 < 0 ? 32 : __ffs(~have) - 1;
+          if (lane < m) c.pages[(int64_t)s * c.maxp + k] = -1;
+          rs_push_many(fp, c.free_pages, L.free_page_top, m, pg, lane);
+          L.free_page_top += m;
+          if (m < 32) break;
+        }
+        g = c.gen[s] + 1u;
+        if (lane == 0) c.gen[s] = g;
+      } else {
+        if (L.free_slot_top == 0) {
+          if (!L.error) L.error = LC_E_CAPACITY;
+          continue;
+        }
+        s = rs_get_many(fs, c.free_slots, L.free_slot_top - 1, 1, lane);
+        s = __shfl_sync(0xffffffffu, s, 0);
+        L.free_slot_top--;
+        if (eb == 0xffffffffu || open) {  // no empty bucket in the window
+          if (lane == 0) table_insert(c, d, s);
+        } else if (lane == 0) {
+          c.hkeys[eb] = d;
+          c.hvals[eb] = s;
+        }
+        if (lane == 0) c.alive[s] = 1;
+        L.alive += 1;
+        g = (s == last_ev_slot) ? last_ev_gen : c.gen[s];
+      }
+      if (L.free_page_top < np) {
+        if (!L.error) L.error = LC_E_CAPACITY;
+        if (lane == 0) {
+          c.nrows[s] = 0;
+          c.nbytes[s] = 0;
+        }
+        __syncwarp();
+        continue;
+      }
+      for (int k0 = 0; k0 < np; k0 += 32) {
+        const int m = min(32, np - k0);
+        const int pg = rs_get_many(fp, c.free_pages, L.free_page_top - 1, m, lane);
+        if (lane < m) c.pages[(int64_t)s * c.maxp + k0 + lane] = pg;
+        L.free_page_top -= m;
+      }
+      L.clock += 1;
+      if (lane == 0) {
+        c.last_hit[s] = (unsigned long long)L.clock;
+        c.pins[s] = 0;
+        c.nrows[s] = nr;
+        c.vocab[s] = vv;
+        c.nbytes[s] = bytes;
+        c.digest[s] = d;
+        const long long pos = L.ring_head % c.R;
+        c.ring_clock[pos] = (unsigned long long)L.clock;
+        c.ring_slot[pos] = s;
+      }
+      L.ring_head++;
+      L.total_bytes += bytes;
+      L.inserts += 1;
+      if (lane == j) {
+        my_slot = s;
+        my_gen = g;
+      }
+      __syncwarp();
+      while (L.total_bytes > L.budget && L.alive > 1) {
+        Victim v = warp_next_victim(c, L, w, lane);
+        if (v.s < 0) break;
+        // evict_entry
+        window_delete(c, v.digest, lane);
+        L.total_bytes -= v.nbytes;
+        for (int k0 = 0; k0 < c.maxp; k0 += 32) {  // push_pages
+          const int k = k0 + lane;
+          const int pg = k < c.maxp ? c.pages[(int64_t)v.s * c.maxp + k] : -1;
+          const unsigned have = __ballot_sync(0xffffffffu, pg >= 0);
+          const int m = __ffs(~have) - 1 < 0 ? 32 : __ffs(~have) - 1;
+          if (lane < m) c.pages[(int64_t)v.s * c.maxp + k] = -1;
+          rs_push_many(fp, c.free_pages, L.free_page_top, m, pg, lane);
+          L.free_page_top += m;
+          if (m < 32) break;
+        }
+        rs_push_many(fs, c.free_slots, L.free_slot_top, 1, v.s, lane);
+        L.free_slot_top += 1;
+        if (lane == 0) {
+          c.gen[v.s] = v.gen + 1u;
+          c.alive[v.s] = 0;
+        }
+        last_ev_slot = v.s;
+        last_ev_gen = v.gen + 1u;
+        L.alive -= 1;
+        L.evictions += 1;
+        __syncwarp();
+      }
+    }
+    if (lane < cnt) {
+      out_slot[i0 + lane] = my_slot;
+      out_gen[i0 + lane] = my_gen;
+    }
+    d0 = d1; n0 = n1; v0 = v1;
+    d1 = d2; n1 = n2; v1 = v2;
+  }
+  __syncwarp();
+  if (lane == 0) *c.ctl = L;
 }
 
 // Copy the rows/tokens of inserts whose entry is still alive at the end of the batch.
@@ -626,7 +1037,11 @@ extern "C" int lc_cache_insert(lc_cache* c, const uint64_t* d_digests, const int
   cudaStream_t st = (cudaStream_t)stream;
   int rc = ensure_ring(c, n, st);
   if (rc) return rc;
-  insert_policy_kernel<<<1, 32, 0, st>>>(c->dev, d_digests, d_lengths, d_vocabs, n, d_slot, d_gen);
+  static const bool scalar = getenv("LCB_SCALAR_POLICY") && atoi(getenv("LCB_SCALAR_POLICY")) != 0;
+  if (scalar)
+    insert_policy_scalar_kernel<<<1, 32, 0, st>>>(c->dev, d_digests, d_lengths, d_vocabs, n, d_slot, d_gen);
+  else
+    insert_policy_kernel<<<1, 32, 0, st>>>(c->dev, d_digests, d_lengths, d_vocabs, n, d_slot, d_gen);
   LCB_CUDA_TRY(cudaGetLastError());
   c->ring_bound += n;
   if (max_len > 0) {

@@ -355,6 +355,87 @@ def test_cache_slots_match_oracle_under_batches():
         assert live == {d: e.slot for d, e in orc.entries.items()}
 
 
+@pytest.mark.parametrize("collide,page_rows,max_rows", [(False, 1, 1), (True, 4, 8), (False, 1, 40), (True, 1, 3),
+                                                         (False, 16, 64)])
+def test_cache_warp_policy_stress_vs_oracle(collide, page_rows, max_rows):
+    """The warp policy kernel (register control block, windowed probes, ring windows, stack
+    mirrors, scalar fallbacks) vs the oracle allocator: slots, generations, victims, hit/miss,
+    accounting and the slab rows of every live entry, under duplicates in a batch, pins
+    (side list), probe chains longer than the 32-bucket window and entries over 32 pages."""
+    rng = np.random.default_rng(11 + page_rows + max_rows)
+    V, E = 32, 128
+    maxp = -(-max_rows // page_rows)
+    budget = (V * 4 + 8) * 3 * max_rows
+    cache = lcb.LogitsCache(budget, vocab=V, key_capacity=E, page_rows=page_rows, max_rows=max_rows,
+                            page_capacity=E * maxp)
+    orc = cache_ref.CacheOracle(budget, E, E * maxp, page_rows)
+    if collide:  # one home bucket for every key (home = d & mask for d < 2^29): chains of 60
+        keys = [5 + 256 * k for k in range(1, 61)]
+    else:
+        keys = [mixing_ref.mix2(3, k) for k in range(60)]
+    row_id = 0
+    expect = {}  # digest -> first row id of its live entry
+    pinned = []
+    for step in range(120):
+        r = rng.random()
+        if r < 0.25:
+            batch = [keys[int(i)] for i in rng.integers(0, len(keys), int(rng.integers(1, 12)))]
+            slot, gen, ln, vv = cache.lookup_batch(lcb._dev.u64_tensor(batch, DEV))
+            want = [-1 if (e := orc.lookup(d)) is None else e.slot for d in batch]
+            assert slot.cpu().tolist() == want
+        elif r < 0.35 and orc.entries:
+            if pinned and rng.random() < 0.5:
+                sl, g = pinned.pop(int(rng.integers(0, len(pinned))))
+                delta = -1
+            else:
+                e = orc.entries[list(orc.entries)[int(rng.integers(0, len(orc.entries)))]]
+                sl, g = e.slot, e.gen
+                if len(pinned) >= 6:
+                    continue
+                pinned.append((sl, g))
+                delta = 1
+            orc.pin(sl, g, delta)
+            st_ = torch.tensor([sl], dtype=torch.int32, device=DEV)
+            gt_ = torch.tensor([g], dtype=torch.int64, device=DEV).to(torch.int32)
+            _capi.check(_capi.lib.lc_cache_pin(cache.handle, st_.data_ptr(), gt_.data_ptr(), 1, delta,
+                                               cache._stream()))
+            cache._dirty()
+        else:
+            nb = int(rng.integers(1, 40))
+            batch = [keys[int(i)] for i in rng.integers(0, len(keys), nb)]
+            lens = rng.integers(1, max_rows + 1, nb).astype(np.int32)
+            offs = np.concatenate([[0], np.cumsum(lens)[:-1]]).astype(np.int64)
+            tot = int(lens.sum())
+            ids = row_id + np.arange(tot)
+            rows = (ids[:, None] * 64 + np.arange(V)[None, :]).astype(np.float32)
+            slot, gen = cache.insert_batch(lcb._dev.u64_tensor(batch, DEV), torch.from_numpy(lens).to(DEV),
+                                           torch.full((nb,), V, dtype=torch.int32, device=DEV),
+                                           torch.from_numpy(rows).to(DEV), torch.from_numpy(offs).to(DEV),
+                                           torch.from_numpy(ids.astype(np.int32)).to(DEV), max_rows)
+            want_s, want_g = [], []
+            for d, n, o in zip(batch, lens, offs):
+                e, _ = orc.insert(d, int(n), V)
+                want_s.append(e.slot)
+                want_g.append(e.gen)
+                expect[d] = row_id + int(o)
+            assert slot.cpu().tolist() == want_s
+            assert (gen.cpu().numpy().astype(np.int64) & 0xFFFFFFFF).tolist() == want_g
+            row_id += tot
+        st = cache._stats()
+        assert (st.entries, st.total_bytes, st.hits, st.lookups) == (len(orc.entries), orc.total, orc.hits,
+                                                                     orc.lookups), step
+        assert st.evictions == orc.evictions
+        snap = cache._snapshot()
+        live = {int(snap["digest"][s]): int(s) for s in np.flatnonzero(snap["alive"])}
+        assert live == {d: e.slot for d, e in orc.entries.items()}, step
+        if step % 15 == 14:
+            for d, e in orc.entries.items():
+                got = cache._gather(e.slot, e.n, V).cpu().numpy()
+                ids = expect[d] + np.arange(e.n)
+                assert np.array_equal(got, (ids[:, None] * 64 + np.arange(V)[None, :]).astype(np.float32)), d
+    assert orc.evictions > 20
+
+
 def test_cache_update_shape_errors_and_accounting():
     cache = lcb.LogitsCache()
     with pytest.raises(lcb.ConfigError):

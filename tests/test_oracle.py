@@ -164,3 +164,31 @@ def test_cache_oracle_lru_and_pins():
     # slot discipline: LIFO reuse of the evicted slot
     e4, _ = c.insert(4, 4, 8)
     assert e4.slot == 1  # slot of key 2 was freed before key 4 needed one
+
+
+def test_cache_oracle_heap_mode_equals_scan_mode():
+    """The O(log E) victim heap used at C4 scale picks the reference's victims."""
+    rng = np.random.default_rng(3)
+    one = 2 * 16 * 4 + 2 * 8
+    a = cache_ref.CacheOracle(12 * one, 64, 512, 2)
+    b = cache_ref.CacheOracle(12 * one, 64, 512, 2, heap=True)
+    for step in range(3000):
+        d = int(rng.integers(0, 40))
+        r = rng.random()
+        if r < 0.3:
+            ea, eb = a.lookup(d), b.lookup(d)
+            assert (ea is None) == (eb is None)
+            if ea is not None:
+                assert ea.slot == eb.slot
+        elif r < 0.4 and a.entries:
+            e = a.entries[sorted(a.entries)[int(rng.integers(0, len(a.entries)))]]
+            delta = 1 if (e.pins == 0 or rng.random() < 0.5) else -1
+            a.pin(e.slot, e.gen, delta)
+            b.pin(e.slot, e.gen, delta)
+        else:
+            n = int(rng.integers(1, 4))
+            ea, va = a.insert(d, n, 16)
+            eb, vb = b.insert(d, n, 16)
+            assert (ea.slot, ea.gen, ea.pages) == (eb.slot, eb.gen, eb.pages)
+            assert va == vb
+        assert a.total == b.total and sorted(a.entries) == sorted(b.entries)
