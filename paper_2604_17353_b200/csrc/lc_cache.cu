@@ -69,7 +69,8 @@ struct CacheDev {
   char* slab;           // [P * page_rows * V] of dtype
   unsigned long long* ring_clock;
   int32_t* ring_slot;
-  long long R;
+  long long R;  // power of two
+  long long rmask;
   unsigned long long* side_clock;
   int32_t* side_slot;
   int side_cap;
@@ -141,7 +142,7 @@ __global__ void __launch_bounds__(1024) lookup_commit_kernel(CacheDev c, const i
     if (hit) {
       const unsigned long long ck = (unsigned long long)(s_clock + rank + 1);
       atomicMax(&c.last_hit[s], ck);
-      const long long pos = (s_head + rank) % c.R;
+      const long long pos = (s_head + rank) & c.rmask;
       c.ring_clock[pos] = ck;
       c.ring_slot[pos] = s;
     }
@@ -231,7 +232,7 @@ __device__ int next_victim(const CacheDev& c) {
   ctl->side_count = w;
   if (found >= 0) return found;
   while (ctl->ring_tail < ctl->ring_head) {
-    long long pos = ctl->ring_tail % c.R;
+    long long pos = ctl->ring_tail & c.rmask;
     int s = c.ring_slot[pos];
     unsigned long long ck = c.ring_clock[pos];
     ctl->ring_tail++;
@@ -324,7 +325,7 @@ __global__ void insert_policy_scalar_kernel(CacheDev c, const uint64_t* __restri
     c.nbytes[s] = bytes;
     c.digest[s] = d;
     {
-      long long pos = ctl->ring_head % c.R;
+      long long pos = ctl->ring_head & c.rmask;
       c.ring_clock[pos] = (unsigned long long)ctl->clock;
       c.ring_slot[pos] = s;
       ctl->ring_head++;
@@ -356,7 +357,12 @@ __global__ void insert_policy_scalar_kernel(CacheDev c, const uint64_t* __restri
 //     so the pop that follows an eviction's push needs no memory round trip.
 // Only this warp touches the cache during the kernel, so L1-resident lines stay coherent.
 
-__device__ __forceinline__ void pf1(const void* p) { asm volatile("prefetch.global.L1 [%0];" ::"l"(p)); }
+__constant__ int g_pf_mode = 1;  // 0 none, 1 L1, 2 L2 (LCB_POLICY_PF; A/B of the prefetch level)
+__device__ __forceinline__ void pf1(const void* p) {
+  const int m = g_pf_mode;
+  if (m == 1) asm volatile("prefetch.global.L1 [%0];" ::"l"(p));
+  else if (m == 2) asm volatile("prefetch.global.L2::evict_last [%0];" ::"l"(p));
+}
 
 __device__ __forceinline__ void pf_window(const CacheDev& c, uint64_t d) {
   const uint32_t b = home_bucket(d, c.hmask);
@@ -477,8 +483,8 @@ __device__ __forceinline__ void ring_load_next(const CacheDev& c, RingWin& w, lo
   const long long p = nb + lane;
   const bool ok = p < head;
   w.nloaded = __ballot_sync(0xffffffffu, ok);
-  w.nslot = ok ? c.ring_slot[p % c.R] : -1;
-  w.nclock = ok ? c.ring_clock[p % c.R] : 0ull;
+  w.nslot = ok ? c.ring_slot[p & c.rmask] : -1;
+  w.nclock = ok ? c.ring_clock[p & c.rmask] : 0ull;
 }
 
 __device__ __forceinline__ void ring_prefetch_next(const CacheDev& c, const RingWin& w) {
@@ -510,8 +516,8 @@ __device__ void ring_enter(const CacheDev& c, RingWin& w, long long t, long long
   }
   w.dead = __ballot_sync(0xffffffffu, !live) & w.loaded;
   // next window: events now, metadata lines prefetched; the window after: ring lines
-  pf1(c.ring_slot + (t + 64 + lane) % c.R);
-  pf1(c.ring_clock + (t + 64 + lane) % c.R);
+  pf1(c.ring_slot + ((t + 64 + lane) & c.rmask));
+  pf1(c.ring_clock + ((t + 64 + lane) & c.rmask));
   ring_load_next(c, w, t + 32, head, lane);
   ring_prefetch_next(c, w);
 }
@@ -622,6 +628,15 @@ __global__ void __launch_bounds__(32) insert_policy_kernel(CacheDev c, const uin
   for (int64_t i0 = 0; i0 < n; i0 += 32) {
     ld(i0 + 64 + lane, d2, n2, v2);
     if (i0 + 32 + lane < n) pf_window(c, d1);
+    if (i0 + lane < n) {  // this chunk's keys found at their home bucket: prefetch the overwrite path's lines
+      const uint32_t hb = home_bucket(d0, c.hmask);
+      const int hs = c.hvals[hb];
+      if (hs >= 0 && c.hkeys[hb] == d0) {
+        pf1(c.nbytes + hs);
+        pf1(c.gen + hs);
+        pf1(c.pages + (int64_t)hs * c.maxp);
+      }
+    }
     int my_slot = -1;
     uint32_t my_gen = 0;
     const int cnt = (int)min((int64_t)32, n - i0);
@@ -629,7 +644,7 @@ __global__ void __launch_bounds__(32) insert_policy_kernel(CacheDev c, const uin
       const uint64_t d = __shfl_sync(0xffffffffu, d0, j);
       const int nr = __shfl_sync(0xffffffffu, n0, j);
       const int vv = __shfl_sync(0xffffffffu, v0, j);
-      const int np = (nr + c.page_rows - 1) / c.page_rows;
+      const int np = c.page_rows == 1 ? nr : (nr + c.page_rows - 1) / c.page_rows;
       if (nr < 0 || vv < 1 || vv > c.V || np > c.maxp) {
         if (!L.error) L.error = LC_E_CONFIG;
         continue;
@@ -698,7 +713,7 @@ __global__ void __launch_bounds__(32) insert_policy_kernel(CacheDev c, const uin
         c.vocab[s] = vv;
         c.nbytes[s] = bytes;
         c.digest[s] = d;
-        const long long pos = L.ring_head % c.R;
+        const long long pos = L.ring_head & c.rmask;
         c.ring_clock[pos] = (unsigned long long)L.clock;
         c.ring_slot[pos] = s;
       }
@@ -916,6 +931,10 @@ extern "C" int lc_cache_create(const lc_cache_config* cfg, lc_cache** out) {
       cfg->page_capacity > (1ll << 31) - 1 || cfg->max_pages < 1 || cfg->budget_bytes < 0)
     return LC_E_CONFIG;
   LCB_CUDA_TRY(cudaSetDevice(cfg->device));
+  if (const char* e = getenv("LCB_POLICY_PF")) {
+    const int m = atoi(e);
+    LCB_CUDA_TRY(cudaMemcpyToSymbol(g_pf_mode, &m, sizeof(int)));
+  }
   lc_cache* c = new (std::nothrow) lc_cache();
   if (!c) return LC_E_CAPACITY;
   c->cfg = *cfg;
@@ -929,7 +948,9 @@ extern "C" int lc_cache_create(const lc_cache_config* cfg, lc_cache** out) {
   uint32_t H = 16;
   while (H < 2u * (uint32_t)d.E) H <<= 1;
   d.hmask = H - 1;
-  d.R = 4ll * d.E + 4096;
+  d.R = 4096;
+  while (d.R < 4ll * d.E + 4096) d.R <<= 1;
+  d.rmask = d.R - 1;
   d.side_cap = d.E < 65536 ? d.E : 65536;
   const size_t esz = cfg->dtype == LC_F32 ? 4 : 2;
   int rc = 0;
