@@ -413,6 +413,121 @@ def run_reference(args, cfg):
     }
 
 
+# ------------------------------------------------------------------------ C3 hit-ratio sweep
+
+
+def run_c3_sweep(args, cfg, rank, world, dev):
+    """C3 with a lookup hit ratio h: 1024 branch keys per step, a fraction h of them
+    cached (16-row bf16 entries, V=151936); each step hashes nothing new (digests precomputed),
+    looks up all 1024 and replays the hits (lookup + step-wise resample + acceptance, one fused
+    path), and runs the miss path for the rest: fresh producer rows (lc_fill_logits, the
+    reference producer) -> resample -> insert.  The two legs are timed separately."""
+    import torch
+
+    import paper_2604_17353_b200 as lcb
+    from paper_2604_17353_b200 import _capi, _dev
+    from paper_2604_17353_b200.mixing import mix2
+
+    h = args.hit_ratio
+    V, n, R = cfg["V"], cfg["n_req"], cfg["R"]
+    n_hit = int(round(h * n))
+    n_miss = n - n_hit
+    steps_all = args.warmup + args.steps
+    budget = n * R * (V * 4 + 8) + 1024
+    cache = lcb.LogitsCache(budget, vocab=V, dtype="bfloat16", key_capacity=2 * n + 64, page_rows=16, max_rows=R,
+                            page_capacity=2 * n + 64, device=dev)
+    # keys: hit set = branches 0..n_hit-1 (fixed); miss set = fresh branches every step
+    prompts = [[rank % 256, 3, j % 256, j // 256, 9] for j in range(n_hit)]
+    miss_prompts = [[rank % 256, 4, s % 256, s // 256, j % 256, j // 256] for s in range(steps_all)
+                    for j in range(n_miss)]
+    hit_d = lcb.hash_prompts(prompts, dev=dev) if n_hit else torch.empty(0, dtype=torch.int64, device=dev)
+    miss_d = (lcb.hash_prompts(miss_prompts, dev=dev) if n_miss else torch.empty(0, dtype=torch.int64, device=dev))
+    tdt = torch.bfloat16
+    fill_states = lambda base, m: lcb._dev.u64_tensor([mix2(7, base + i) for i in range(m)], dev)  # noqa: E731
+    miss_tasks = lcb.make_tasks(row=np.arange(n_miss * R), pos=np.tile(np.arange(R), n_miss), temperature=cfg["T"],
+                                top_k=cfg["k"], top_p=cfg["p"], draw_begin=np.arange(n_miss * R),
+                                draw_end=np.arange(n_miss * R) + 1, seed_base=np.repeat(np.arange(n_miss), R))
+    miss_tasks_d = torch.from_numpy(np.ascontiguousarray(miss_tasks).view(np.uint8)).to(dev)
+    if n_hit:  # pre-insert the hit set (untimed)
+        rows = torch.empty((n_hit * R, V), dtype=tdt, device=dev)
+        st = fill_states((rank << 40) + (1 << 32), n_hit * R)
+        _capi.check(_capi.lib.lc_fill_logits(st.data_ptr(), n_hit * R, V, 2.5, 5.0, _capi.LC_BF16, rows.data_ptr(),
+                                             V, _dev.stream_ptr(dev)))
+        tasks = lcb.make_tasks(row=np.arange(n_hit * R), pos=np.tile(np.arange(R), n_hit), temperature=cfg["T"],
+                               top_k=cfg["k"], top_p=cfg["p"], draw_begin=np.arange(n_hit * R),
+                               draw_end=np.arange(n_hit * R) + 1, seed_base=np.repeat(np.arange(n_hit), R))
+        tok, _ = lcb.resample(rows, tasks, seeds=lcb._dev.u64_tensor([mix2(99, j) for j in range(n_hit)], dev),
+                              n_draws=n_hit * R)
+        cache.insert_batch(hit_d, torch.full((n_hit,), R, dtype=torch.int32, device=dev),
+                           torch.full((n_hit,), V, dtype=torch.int32, device=dev), rows,
+                           torch.arange(n_hit, dtype=torch.int64, device=dev) * R, tok.contiguous(), R)
+        del rows
+    T = torch.full((n,), cfg["T"], dtype=torch.float64, device=dev)
+    K = torch.full((n,), cfg["k"], dtype=torch.int32, device=dev)
+    P = torch.full((n,), cfg["p"], dtype=torch.float64, device=dev)
+    step_in = []
+    for s in range(steps_all):
+        dg = torch.cat([hit_d, miss_d[s * n_miss:(s + 1) * n_miss]])
+        seeds = lcb._dev.u64_tensor([mix2(1, (rank << 40) + s * n + j) for j in range(n)], dev)
+        st = fill_states((rank << 40) + (2 << 32) + s * n_miss * R, n_miss * R) if n_miss else None
+        step_in.append((dg, seeds, st))
+    rows_m = torch.empty((max(n_miss, 1) * R, V), dtype=tdt, device=dev)
+    lens_m = torch.full((max(n_miss, 1),), R, dtype=torch.int32, device=dev)
+    vocs_m = torch.full((max(n_miss, 1),), V, dtype=torch.int32, device=dev)
+    offs_m = torch.arange(max(n_miss, 1), dtype=torch.int64, device=dev) * R
+    bufs = {}
+    ev_hit, ev_miss, outs = [], [], []
+
+    def step(s, timed):
+        dg, seeds, st = step_in[s]
+        a, b, c_ = (torch.cuda.Event(enable_timing=True) for _ in range(3))
+        a.record()
+        tok, rep, div, slot, ln = cache.replay_stepwise(dg, R, 1, seeds, T, K, P, bufs=bufs)
+        b.record()
+        if n_miss:
+            _capi.check(_capi.lib.lc_fill_logits(st.data_ptr(), n_miss * R, V, 2.5, 5.0, _capi.LC_BF16,
+                                                 rows_m.data_ptr(), V, _dev.stream_ptr(dev)))
+            mt, _ = lcb.resample(rows_m, miss_tasks_d, seeds=seeds[n_hit:], n_draws=n_miss * R)
+            cache.insert_batch(dg[n_hit:], lens_m, vocs_m, rows_m, offs_m, mt, R)
+        c_.record()
+        if timed:
+            ev_hit.append((a, b))
+            ev_miss.append((b, c_))
+            outs.append((slot, rep.clone()))
+
+    for s in range(args.warmup):
+        step(s, False)
+    torch.cuda.synchronize(dev)
+    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(dev.index) as clk:
+        t0.record()
+        for s in range(args.warmup, steps_all):
+            step(s, True)
+        t1.record()
+        torch.cuda.synchronize(dev)
+    ms = t0.elapsed_time(t1)
+    hit_ms = sum(a.elapsed_time(b) for a, b in ev_hit) / args.steps
+    miss_ms = sum(a.elapsed_time(b) for a, b in ev_miss) / args.steps
+    slots = torch.stack([o[0] for o in outs]).cpu().numpy()
+    reps = torch.stack([o[1] for o in outs]).cpu().numpy()
+    lookup_hits = float((slots >= 0).mean())
+    assert np.all(slots[:, :n_hit] >= 0) and np.all(slots[:, n_hit:] < 0), "hit/miss pattern"
+    pos_hit = float(reps.sum() / (n * R * args.steps))  # replayed positions / all positions (ReplayOutcome)
+    tokens = n * R * args.steps
+    return {
+        "metric": "resampled_tokens_per_s", "value": tokens * world / (ms * 1e-3), "unit": "tokens/s",
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
+        "data": "synthetic (reference producer fill_logits, seed 7, conc 2.5, range 5.0)",
+        "config": {"workload": cfg["desc"] + f"; lookup hit ratio {h}", "config": "c3", "hit_ratio": h,
+                   "branches": n, "rows_per_entry": R, "vocab": V},
+        "lookup_hit_ratio": lookup_hits, "position_hit_ratio": pos_hit,
+        "lookup_resample_ms_per_step": hit_ms, "miss_path_ms_per_step": miss_ms,
+        "miss_path": "lc_fill_logits (producer) -> resample -> lc_cache_insert",
+        "gpu_launches": None, "clocks": clk.summary(),
+    }
+
+
 # ------------------------------------------------------------------------ C4: insert / eviction stress
 
 
@@ -625,6 +740,8 @@ def main():
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-check", action="store_true", help="c4: skip the oracle replay of the op trace")
+    ap.add_argument("--hit-ratio", type=float, default=None,
+                    help="c3: lookup hit ratio h of the sweep (default: every branch cached)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     cfg = CONFIGS[args.config]
@@ -652,7 +769,12 @@ def main():
     dev = torch.device("cuda", local)
     if world > 1:
         dist.init_process_group("nccl", device_id=dev)
-    res = (run_c4 if args.config == "c4" else run_ours)(args, cfg, rank, world, dev)
+    if args.config == "c4":
+        res = run_c4(args, cfg, rank, world, dev)
+    elif args.config == "c3" and args.hit_ratio is not None:
+        res = run_c3_sweep(args, cfg, rank, world, dev)
+    else:
+        res = run_ours(args, cfg, rank, world, dev)
     if rank == 0:
         print(json.dumps(res), flush=True)
     if world > 1:
