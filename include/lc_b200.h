@@ -229,6 +229,20 @@ int lc_replay_tasks(const int32_t* d_slot, const int32_t* d_len, int64_t n_req, 
 int lc_replay_accept(const int32_t* d_tokens, const int32_t* d_cached, const int32_t* d_len, int64_t n_req,
                      int32_t max_pos, int32_t n_branch, int32_t* d_replayed, int32_t* d_diverged, void* stream);
 
+/* Hotspot replay policy (engine.py:311-326, ReplayPolicy.HOTSPOT).
+ * d_draw_index[r*max_pos + t] = number of hotspots of request r before t when
+ * t is a hotspot (the RngStream draw number of that sample), else -1.
+ * lc_replay_tasks_hotspot: as lc_replay_tasks, but only hotspot positions get
+ * draws.  lc_replay_accept_hotspot: non-hotspot positions copy the cached
+ * token (written into d_tokens, so d_tokens is the engine's `out` list); the
+ * replay stops after the first hotspot whose sample differs from the cache.   */
+int lc_replay_tasks_hotspot(const int32_t* d_slot, const int32_t* d_len, const int32_t* d_draw_index, int64_t n_req,
+                            int32_t max_pos, int32_t n_branch, const double* d_temperature, const int32_t* d_top_k,
+                            const double* d_top_p, lc_task* d_tasks, void* stream);
+int lc_replay_accept_hotspot(int32_t* d_tokens, const int32_t* d_cached, const int32_t* d_len,
+                             const int32_t* d_draw_index, int64_t n_req, int32_t max_pos, int32_t n_branch,
+                             int32_t* d_replayed, int32_t* d_diverged, void* stream);
+
 /* Test probe: the resample tiers' exponentials e(z) ~ exp((z - m)/T) for given
  * z (mode 0 FAST corrected, 1 FAST cheap, 2 PRECISE table fp64), so tests can
  * pin their error bounds against fp64 (not on the hot path).                  */

@@ -103,6 +103,8 @@ _SIGS = {
     "lc_probe_exp": (C.c_int, [P, I64, C.c_float, D, C.c_int, P, P]),
     "lc_replay_tasks": (C.c_int, [P, P, I64, I32, I32, P, P, P, P, P]),
     "lc_replay_accept": (C.c_int, [P, P, P, I64, I32, I32, P, P, P]),
+    "lc_replay_tasks_hotspot": (C.c_int, [P, P, P, I64, I32, I32, P, P, P, P, P]),
+    "lc_replay_accept_hotspot": (C.c_int, [P, P, P, P, I64, I32, I32, P, P, P]),
 }
 
 

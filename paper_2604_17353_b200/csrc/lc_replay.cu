@@ -53,7 +53,92 @@ __global__ void replay_accept_kernel(const int32_t* __restrict__ tok, const int3
   if (diverged) diverged[i] = div;
 }
 
+// Hotspot policy (engine.py:311-326): only hotspot positions draw; the stream's
+// draw number at position t is the count of hotspots before t (d_draw_index,
+// -1 = not a hotspot); every other position copies the cached token.
+__global__ void replay_tasks_hot_kernel(const int32_t* __restrict__ slot, const int32_t* __restrict__ len,
+                                        const int32_t* __restrict__ draw_index, int64_t n_req, int max_pos, int nb,
+                                        const double* __restrict__ temp, const int32_t* __restrict__ topk,
+                                        const double* __restrict__ topp, lc_task* __restrict__ tasks) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n_req * (int64_t)max_pos) return;
+  const int64_t r = i / max_pos;
+  const int t = (int)(i % max_pos);
+  const int s = slot[r];
+  const int lim = s >= 0 ? min(len[r], max_pos) : 0;
+  const int di = draw_index[i];
+  lc_task tk;
+  tk.row = -1;
+  tk.slot = s;
+  tk.pos = t;
+  tk.temperature = temp[r];
+  tk.top_k = topk[r];
+  tk.vocab = 0;
+  tk.top_p = topp[r];
+  tk.draw_begin = i * nb;
+  tk.draw_end = (t < lim && di >= 0) ? i * nb + nb : i * nb;
+  tk.seed_base = r * nb;
+  tk.u_index = di >= 0 ? di : 0;
+  tasks[i] = tk;
+}
+
+// Hotspot acceptance: non-hotspot positions take the cached token (written into
+// d_tokens so the output is the engine's `out` list); the replay stops after the
+// first hotspot whose sample differs from the cached token.
+__global__ void replay_accept_hot_kernel(int32_t* __restrict__ tok, const int32_t* __restrict__ cached,
+                                         const int32_t* __restrict__ len, const int32_t* __restrict__ draw_index,
+                                         int64_t n_req, int max_pos, int nb, int32_t* __restrict__ replayed,
+                                         int32_t* __restrict__ diverged) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n_req * (int64_t)nb) return;
+  const int64_t r = i / nb;
+  const int b = (int)(i % nb);
+  const int lim = min(len[r], max_pos);
+  int rep = 0, div = -1;
+  for (int t = 0; t < lim; ++t) {
+    const int64_t o = ((r * max_pos) + t) * (int64_t)nb + b;
+    const int yc = cached[r * max_pos + t];
+    int y = yc;
+    if (draw_index[r * max_pos + t] >= 0) y = tok[o];
+    else tok[o] = yc;
+    rep = t + 1;
+    if (y != yc) {
+      div = t;
+      break;
+    }
+  }
+  replayed[i] = rep;
+  if (diverged) diverged[i] = div;
+}
+
 }  // namespace lcb
+
+extern "C" int lc_replay_tasks_hotspot(const int32_t* d_slot, const int32_t* d_len, const int32_t* d_draw_index,
+                                       int64_t n_req, int32_t max_pos, int32_t n_branch,
+                                       const double* d_temperature, const int32_t* d_top_k, const double* d_top_p,
+                                       lc_task* d_tasks, void* stream) {
+  if (n_req < 0 || max_pos < 0 || n_branch < 0) return LC_E_ARG;
+  const int64_t n = n_req * (int64_t)max_pos;
+  if (n == 0) return LC_OK;
+  if (!d_slot || !d_len || !d_draw_index || !d_temperature || !d_top_k || !d_top_p || !d_tasks) return LC_E_ARG;
+  lcb::replay_tasks_hot_kernel<<<lcb::ceil_div(n, 256), 256, 0, (cudaStream_t)stream>>>(
+      d_slot, d_len, d_draw_index, n_req, max_pos, n_branch, d_temperature, d_top_k, d_top_p, d_tasks);
+  LCB_CUDA_TRY(cudaGetLastError());
+  return LC_OK;
+}
+
+extern "C" int lc_replay_accept_hotspot(int32_t* d_tokens, const int32_t* d_cached, const int32_t* d_len,
+                                        const int32_t* d_draw_index, int64_t n_req, int32_t max_pos,
+                                        int32_t n_branch, int32_t* d_replayed, int32_t* d_diverged, void* stream) {
+  if (n_req < 0 || max_pos < 0 || n_branch < 0) return LC_E_ARG;
+  const int64_t n = n_req * (int64_t)n_branch;
+  if (n == 0) return LC_OK;
+  if (!d_tokens || !d_cached || !d_len || !d_draw_index || !d_replayed) return LC_E_ARG;
+  lcb::replay_accept_hot_kernel<<<lcb::ceil_div(n, 256), 256, 0, (cudaStream_t)stream>>>(
+      d_tokens, d_cached, d_len, d_draw_index, n_req, max_pos, n_branch, d_replayed, d_diverged);
+  LCB_CUDA_TRY(cudaGetLastError());
+  return LC_OK;
+}
 
 extern "C" int lc_replay_tasks(const int32_t* d_slot, const int32_t* d_len, int64_t n_req, int32_t max_pos,
                                int32_t n_branch, const double* d_temperature, const int32_t* d_top_k,

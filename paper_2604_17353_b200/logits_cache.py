@@ -348,6 +348,51 @@ class LogitsCache:
                     "lc_replay_accept")
         return tok, b["rep"], b["div"], slot, ln
 
+    def replay_hotspot(self, digests: torch.Tensor, max_pos: int, n_branch: int, seeds: torch.Tensor,
+                       temperature: torch.Tensor, top_k: torch.Tensor, top_p: torch.Tensor, hotspots,
+                       counters=None, bufs: dict | None = None):
+        """ReplayPolicy.HOTSPOT for a batch (engine.py:311-326): request r samples only at
+        the positions in ``hotspots[r]`` (RngStream draw number = hotspots before t) and
+        copies the cached token elsewhere; the replay stops after the first hotspot sample
+        that differs from the cache.  Same returns as ``replay_stepwise``; the token array
+        holds the engine's ``out`` tokens at every replayed position."""
+        n_req = digests.numel()
+        d = self.dev
+        if len(hotspots) != n_req:
+            raise ConfigError("one hotspot tuple per request")
+        di = np.full((n_req, max_pos), -1, dtype=np.int32)
+        for r, hs in enumerate(hotspots):
+            hs = sorted(t for t in hs if 0 <= t < max_pos)
+            di[r, hs] = np.arange(len(hs), dtype=np.int32)
+        d_di = torch.from_numpy(di.reshape(-1)).to(d)
+        slot, gen, ln, vv = self.lookup_batch(digests)
+        b = bufs if bufs is not None else {}
+        ntask = n_req * max_pos
+        ndraw = ntask * n_branch
+        if "tasks" not in b or b["tasks"].numel() < ntask * _capi.TASK_DTYPE.itemsize:
+            b["tasks"] = torch.empty(ntask * _capi.TASK_DTYPE.itemsize, dtype=torch.uint8, device=d)
+            b["tok"] = torch.empty(ndraw, dtype=torch.int32, device=d)
+            b["flags"] = torch.empty(ndraw, dtype=torch.uint8, device=d)
+            b["cached"] = torch.empty(ntask, dtype=torch.int32, device=d)
+            b["pos"] = torch.arange(max_pos, dtype=torch.int32, device=d).repeat(n_req)
+            b["rep"] = torch.empty(n_req * n_branch, dtype=torch.int32, device=d)
+            b["div"] = torch.empty(n_req * n_branch, dtype=torch.int32, device=d)
+        st = self._stream()
+        _capi.check(_capi.lib.lc_replay_tasks_hotspot(slot.data_ptr(), ln.data_ptr(), d_di.data_ptr(), n_req,
+                                                      max_pos, n_branch, temperature.data_ptr(), top_k.data_ptr(),
+                                                      top_p.data_ptr(), b["tasks"].data_ptr(), st),
+                    "lc_replay_tasks_hotspot")
+        tok, flags = sampling.resample(None, b["tasks"][: ntask * _capi.TASK_DTYPE.itemsize], seeds=seeds,
+                                       n_draws=ndraw, cache=self, counters=counters, out=(b["tok"], b["flags"]))
+        slots_rep = slot.repeat_interleave(max_pos)
+        _capi.check(_capi.lib.lc_cache_tokens(self.handle, slots_rep.data_ptr(), b["pos"].data_ptr(), ntask,
+                                              b["cached"].data_ptr(), st), "lc_cache_tokens")
+        _capi.check(_capi.lib.lc_replay_accept_hotspot(tok.data_ptr(), b["cached"].data_ptr(), ln.data_ptr(),
+                                                       d_di.data_ptr(), n_req, max_pos, n_branch,
+                                                       b["rep"].data_ptr(), b["div"].data_ptr(), st),
+                    "lc_replay_accept_hotspot")
+        return tok, b["rep"], b["div"], slot, ln
+
     # -- reference API --------------------------------------------------------------------
 
     def lookup(self, key: StateKey) -> CachedTrajectory | None:

@@ -496,6 +496,61 @@ def test_replay_stepwise_matches_oracle():
     assert np.all(rep[n_req] == 0)
 
 
+def test_replay_hotspot_matches_oracle():
+    """ReplayPolicy.HOTSPOT on the device (engine.py:311-326) vs the oracle loop: draws only at
+    hotspots with draw number = hotspots before t, cached tokens copied elsewhere, stop after the
+    first differing hotspot sample; tokens equal the engine's out list."""
+    V, n_req, L, nb = 2048, 6, 40, 4
+    cache = lcb.LogitsCache(1 << 30, vocab=V, dtype="bfloat16", max_rows=64)
+    keys = [mixing_ref.hash_tokens([r, 9, 4]) for r in range(n_req)]
+    rows = mixing_ref.bf16_round(mixing_ref.fill_rows_np([mixing_ref.mix2(6, i) for i in range(n_req * L)], V, 2.5))
+    rng = np.random.default_rng(4)
+    cached_tok = rng.integers(0, V, n_req * L).astype(np.int32)
+    cached_tok = np.where(np.arange(n_req * L) % L < 12, rows.argmax(1), cached_tok).astype(np.int32)
+    lens = np.full(n_req, L, np.int32)
+    lens[2] = 9
+    offs = (np.arange(n_req) * L).astype(np.int64)
+    cache.insert_batch(lcb._dev.u64_tensor(keys, DEV), torch.from_numpy(lens).to(DEV),
+                       torch.full((n_req,), V, dtype=torch.int32, device=DEV),
+                       torch.from_numpy(rows).to(DEV).to(torch.bfloat16), torch.from_numpy(offs).to(DEV),
+                       torch.from_numpy(cached_tok).to(DEV), L)
+    hot = [tuple(sorted(rng.choice(L, int(rng.integers(0, 14)), replace=False).tolist())) for _ in range(n_req)]
+    hot[0] = ()
+    hot.append((1, 2))  # the missing request
+    digests = lcb._dev.u64_tensor(keys + [777], DEV)
+    seeds = [mixing_ref.mix2(2, b) for b in range((n_req + 1) * nb)]
+    T = torch.full((n_req + 1,), 0.6, dtype=torch.float64, device=DEV)
+    K = torch.zeros(n_req + 1, dtype=torch.int32, device=DEV)
+    Pp = torch.full((n_req + 1,), 0.9, dtype=torch.float64, device=DEV)
+    max_pos = 32
+    tok, rep, div, slot, ln = cache.replay_hotspot(digests, max_pos, nb, lcb._dev.u64_tensor(seeds, DEV), T, K,
+                                                   Pp, hot)
+    tok = tok.cpu().numpy().reshape(n_req + 1, max_pos, nb)
+    rep = rep.cpu().numpy().reshape(n_req + 1, nb)
+    div = div.cpu().numpy().reshape(n_req + 1, nb)
+    for r in range(n_req):
+        lim = min(int(lens[r]), max_pos)
+        hs = set(hot[r])
+        for b in range(nb):
+            out, k, want_div = [], 0, -1
+            for t in range(lim):
+                yc = int(cached_tok[r * L + t])
+                if t in hs:
+                    u = mixing_ref.uniform(seeds[r * nb + b], k)
+                    k += 1
+                    y = _oracle_tokens(rows[r * L + t: r * L + t + 1], 0.6, None, 0.9, [[u]])[0]
+                else:
+                    y = yc
+                out.append(y)
+                if y != yc:
+                    want_div = t
+                    break
+            assert rep[r, b] == len(out), (r, b)
+            assert div[r, b] == want_div, (r, b)
+            assert tok[r, :len(out), b].tolist() == out, (r, b)
+    assert np.all(rep[n_req] == 0)
+
+
 @pytest.mark.parametrize("conc,T,p,nd", [(2.5, 0.6, 0.9, 32), (0.0, 0.6, 0.9, 8), (2.5, 1.0, 0.5, 4),
                                          (5.0, 0.3, 0.99, 16), (1.0, 2.0, 0.95, 8)])
 def test_staged_kernel_matches_oracle_and_other_tiers(conc, T, p, nd, monkeypatch):
