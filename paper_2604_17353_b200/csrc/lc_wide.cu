@@ -405,48 +405,55 @@ __global__ void __launch_bounds__(WG_THREADS, 1) wide_kernel(StageArgs a) {
       float W = 0.0f;
       uint32_t cm2 = 0xff80ff80u;
       if (!bad && ref > -INFINITY) {
-        // (warp-uniform trip count: the candidate appends use warp collectives)
-        for (int v0 = gw * 32; v0 < nv; v0 += WG_GT) {
-          const int v = v0 + lane;
-          const uint4 q = v < nv ? R[v] : make_uint4(0xff80ff80u, 0xff80ff80u, 0xff80ff80u, 0xff80ff80u);
+        // two vectors
+        // per lane and iteration, so the MUFU / add chains of one hide the other's latency
+        auto cand_block = [&](const uint4 q, const uint32_t vm2, const int v) {
           const uint32_t w[4] = {q.x, q.y, q.z, q.w};
-          const uint32_t vm2 = bmax2_nan(bmax2_nan(w[0], w[1]), bmax2_nan(w[2], w[3]));
-          cm2 = bmax2_nan(cm2, vm2);
-          float e8[8];  // (-inf -> 0; the argument roundings are bounded with |a| <= 130)
-#pragma unroll
-          for (int j = 0; j < 8; ++j) e8[j] = ex2_approx(fmaf((j & 1) ? hi_f(w[j >> 1]) : lo_f(w[j >> 1]), Lf, nmL));
-          acc += (double)(((e8[0] + e8[1]) + (e8[2] + e8[3])) + ((e8[4] + e8[5]) + (e8[6] + e8[7])));
           // (once the list was compacted, only values above the k-th value can still enter)
           const float vmx = max_nan(lo_f(vm2), hi_f(vm2));
           const bool any_c = thrk ? vmx > thr : vmx >= thr;
-          if (__any_sync(0xffffffffu, any_c)) {
+          if (any_c) {
             // (ties of the k-th value with larger ids than the k-th key cannot enter: ids grow
-            // with the chunks, so the list stops growing once it has been compacted)
-            unsigned m8 = 0u;
+            // with the chunks, so the list stops growing once it has been compacted).  Few
+            // lanes ever get here (~0.3% of the values clear the threshold): one shared
+            // atomic per candidate, no warp-wide scan.
+            const int id0 = c * WG_CH + 8 * v;
 #pragma unroll
             for (int j = 0; j < 8; ++j) {
               const float z = (j & 1) ? hi_f(w[j >> 1]) : lo_f(w[j >> 1]);
-              m8 |= (unsigned)(z >= thr && z > -INFINITY && wkey(z, c * WG_CH + 8 * v + j) > thrk) << j;
-            }
-            const int cntj = __popc(m8);
-            int inc = cntj;
-#pragma unroll
-            for (int o = 1; o < 32; o <<= 1) {
-              const int y = __shfl_up_sync(0xffffffffu, inc, o);
-              if (lane >= o) inc += y;
-            }
-            int base = 0;
-            if (lane == 31) base = atomicAdd(&G.ncand, inc);
-            base = __shfl_sync(0xffffffffu, base, 31) + inc - cntj;
-            while (m8) {
-              const int j = __ffs(m8) - 1;
-              m8 &= m8 - 1;
-              const float z = (j & 1) ? hi_f(w[j >> 1]) : lo_f(w[j >> 1]);
-              if (base < WG_CAP) G.cand[base] = wkey(z, c * WG_CH + 8 * v + j);
-              ++base;
+              if (z >= thr && z > -INFINITY) {
+                const unsigned long long key = wkey(z, id0 + j);
+                if (key > thrk) {
+                  const int b = atomicAdd(&G.ncand, 1);
+                  if (b < WG_CAP) G.cand[b] = key;
+                }
+              }
             }
           }
+        };
+        double acc1 = 0.0;
+        for (int v0 = gw * 32; v0 < nv; v0 += 2 * WG_GT) {
+          const int va = v0 + lane, vb = v0 + WG_GT + lane;
+          const uint4 ninf = make_uint4(0xff80ff80u, 0xff80ff80u, 0xff80ff80u, 0xff80ff80u);
+          const uint4 qa = va < nv ? R[va] : ninf;
+          const uint4 qb = vb < nv ? R[vb] : ninf;
+          const uint32_t wa[4] = {qa.x, qa.y, qa.z, qa.w};
+          const uint32_t wb[4] = {qb.x, qb.y, qb.z, qb.w};
+          const uint32_t vma = bmax2_nan(bmax2_nan(wa[0], wa[1]), bmax2_nan(wa[2], wa[3]));
+          const uint32_t vmb = bmax2_nan(bmax2_nan(wb[0], wb[1]), bmax2_nan(wb[2], wb[3]));
+          cm2 = bmax2_nan(cm2, bmax2_nan(vma, vmb));
+          float ea[8], eb[8];  // (-inf -> 0; the argument roundings are bounded with |a| <= 130)
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            ea[j] = ex2_approx(fmaf((j & 1) ? hi_f(wa[j >> 1]) : lo_f(wa[j >> 1]), Lf, nmL));
+            eb[j] = ex2_approx(fmaf((j & 1) ? hi_f(wb[j >> 1]) : lo_f(wb[j >> 1]), Lf, nmL));
+          }
+          acc += (double)(((ea[0] + ea[1]) + (ea[2] + ea[3])) + ((ea[4] + ea[5]) + (ea[6] + ea[7])));
+          acc1 += (double)(((eb[0] + eb[1]) + (eb[2] + eb[3])) + ((eb[4] + eb[5]) + (eb[6] + eb[7])));
+          cand_block(qa, vma, va);
+          if (v0 + WG_GT < nv) cand_block(qb, vmb, vb);
         }
+        acc += acc1;
       }
       {
         const double ws = warp_sum(acc), ww = warp_sum((double)W);
