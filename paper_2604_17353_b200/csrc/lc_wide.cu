@@ -175,66 +175,52 @@ __device__ void wg_pop(WgSmem& sm, WgGroup& G, int lane) {
   __syncwarp();
 }
 
-// descending bitonic sort of the group's candidate list (n <= WG_CAP, padded with 0)
-__device__ void warp_sort128(unsigned long long* keys, int n, int lane);
+// descending sort of the group's candidate list (n <= WG_CAP) by its warp 0: a
+// shuffle bitonic network in registers, no group barriers inside
+template <int RL>
+__device__ __noinline__ void warp_sort(unsigned long long* keys, int n, int lane);
 
 __device__ void wg_sort(WgGroup& G, int g, int gt, int n) {
-  if (n <= 128) {  // one warp, no barriers inside
-    if (gt < 32) warp_sort128(G.cand, n, gt);
-    wbar(g);
-    return;
+  static_assert(WG_CAP <= 512, "warp sort covers 512 keys");
+  if (gt < 32) {
+    if (n <= 128) warp_sort<4>(G.cand, n, gt);
+    else if (n <= 256) warp_sort<8>(G.cand, n, gt);
+    else warp_sort<16>(G.cand, n, gt);
   }
-  int n2 = 32;
-  while (n2 < n) n2 <<= 1;
-  for (int i = n + gt; i < n2; i += WG_GT) G.cand[i] = 0ull;
   wbar(g);
-  for (int k = 2; k <= n2; k <<= 1) {
-    for (int j = k >> 1; j > 0; j >>= 1) {
-      for (int i = gt; i < n2; i += WG_GT) {
-        const int p = i ^ j;
-        if (p > i) {
-          const unsigned long long x = G.cand[i], y = G.cand[p];
-          const bool desc = (i & k) == 0;
-          if (desc ? (x < y) : (x > y)) {
-            G.cand[i] = y;
-            G.cand[p] = x;
-          }
-        }
-      }
-      wbar(g);
-    }
-  }
 }
 
 // (value order, id) -> descending order = (value desc, id asc), the reference's lexsort
 __device__ __forceinline__ unsigned long long wkey(float v, int idx) {
   return ((unsigned long long)f32_order_key(v) << 32) | (unsigned long long)(0xffffffffu - (uint32_t)idx);
 }
-// descending bitonic sort of up to 128 keys by one warp (4 per lane, shuffles only)
-__device__ void warp_sort128(unsigned long long* keys, int n, int lane) {
-  unsigned long long x[4];
+// descending bitonic sort of up to 32*RL keys by one warp (RL per lane, shuffles only)
+template <int RL>
+__device__ __noinline__ void warp_sort(unsigned long long* keys, int n, int lane) {
+  constexpr int NK = 32 * RL;
+  unsigned long long x[RL];
 #pragma unroll
-  for (int r = 0; r < 4; ++r) x[r] = 4 * lane + r < n ? keys[4 * lane + r] : 0ull;
+  for (int r = 0; r < RL; ++r) x[r] = RL * lane + r < n ? keys[RL * lane + r] : 0ull;
 #pragma unroll
-  for (int k = 2; k <= 128; k <<= 1) {
+  for (int k = 2; k <= NK; k <<= 1) {
 #pragma unroll
     for (int j = k >> 1; j > 0; j >>= 1) {
-      if (j >= 4) {
-        const int lj = j >> 2;
+      if (j >= RL) {
+        const int lj = j / RL;
         const bool lower = (lane & lj) == 0;
 #pragma unroll
-        for (int r = 0; r < 4; ++r) {
-          const int i = 4 * lane + r;
+        for (int r = 0; r < RL; ++r) {
+          const int i = RL * lane + r;
           const bool desc = (i & k) == 0;
           const unsigned long long y = __shfl_xor_sync(0xffffffffu, x[r], lj);
           x[r] = (desc == lower) ? (x[r] > y ? x[r] : y) : (x[r] < y ? x[r] : y);
         }
       } else {
 #pragma unroll
-        for (int r = 0; r < 4; ++r) {
+        for (int r = 0; r < RL; ++r) {
           const int rp = r ^ j;
           if (rp > r) {
-            const int i = 4 * lane + r;
+            const int i = RL * lane + r;
             const bool desc = (i & k) == 0;
             const unsigned long long a = x[r], b = x[rp];
             if (desc ? (a < b) : (a > b)) {
@@ -247,8 +233,8 @@ __device__ void warp_sort128(unsigned long long* keys, int n, int lane) {
     }
   }
 #pragma unroll
-  for (int r = 0; r < 4; ++r)
-    if (4 * lane + r < n) keys[4 * lane + r] = x[r];
+  for (int r = 0; r < RL; ++r)
+    if (RL * lane + r < n) keys[RL * lane + r] = x[r];
 }
 
 __device__ __forceinline__ float key_val(unsigned long long k) {
