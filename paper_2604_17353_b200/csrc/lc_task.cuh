@@ -18,6 +18,7 @@ constexpr double kEx2Raw = 2.5e-7;       // ex2.approx.ftz.f32 alone (cheap_exp)
 constexpr double kArgRel = 3.0 * 5.9604644775390625e-08 * 0.6931471805599453 * 1.01;  // cheap_exp: per |a|
 constexpr double kCorrErr = 1.0e-10;                       // 2nd-order term of the argument correction
 constexpr double kSum8Err = 3.0 * 5.9604644775390625e-08;  // fp32 pairwise sum of 8 (3 roundings)
+constexpr double kSum16Err = 4.0 * 5.9604644775390625e-08;  // fp32 pairwise sum of 16 (4 roundings)
 constexpr double kRefExpErr = 8.881784197001252e-16;       // libm / numpy exp vs exact: 4 ulp
 constexpr double kLiteErr = 3.0e-13;                       // lite_exp incl. its argument (|a| <= 1100)
 constexpr double kEps64 = 1.1102230246251565e-16;          // 2^-53

@@ -417,7 +417,6 @@ __global__ void __launch_bounds__(WG_THREADS, 1) wide_kernel(StageArgs a) {
             }
           }
         };
-        double acc1 = 0.0;
         for (int v0 = gw * 32; v0 < nv; v0 += 2 * WG_GT) {
           const int va = v0 + lane, vb = v0 + WG_GT + lane;
           const uint4 ninf = make_uint4(0xff80ff80u, 0xff80ff80u, 0xff80ff80u, 0xff80ff80u);
@@ -434,12 +433,13 @@ __global__ void __launch_bounds__(WG_THREADS, 1) wide_kernel(StageArgs a) {
             ea[j] = ex2_approx(fmaf((j & 1) ? hi_f(wa[j >> 1]) : lo_f(wa[j >> 1]), Lf, nmL));
             eb[j] = ex2_approx(fmaf((j & 1) ? hi_f(wb[j >> 1]) : lo_f(wb[j >> 1]), Lf, nmL));
           }
-          acc += (double)(((ea[0] + ea[1]) + (ea[2] + ea[3])) + ((ea[4] + ea[5]) + (ea[6] + ea[7])));
-          acc1 += (double)(((eb[0] + eb[1]) + (eb[2] + eb[3])) + ((eb[4] + eb[5]) + (eb[6] + eb[7])));
+          // fp32 pairwise sum of the 16 (4 roundings, kSum16Err), one fp64 add per iteration
+          const float sa = ((ea[0] + ea[1]) + (ea[2] + ea[3])) + ((ea[4] + ea[5]) + (ea[6] + ea[7]));
+          const float sb = ((eb[0] + eb[1]) + (eb[2] + eb[3])) + ((eb[4] + eb[5]) + (eb[6] + eb[7]));
+          acc += (double)(sa + sb);
           cand_block(qa, vma, va);
           if (v0 + WG_GT < nv) cand_block(qb, vmb, vb);
         }
-        acc += acc1;
       }
       {
         const double ws = warp_sum(acc), ww = warp_sum((double)W);
@@ -520,7 +520,7 @@ __global__ void __launch_bounds__(WG_THREADS, 1) wide_kernel(StageArgs a) {
           const float mL = fabsf(M) * Lf;
           // (exponentials: ex2.approx + argument rounding ln2 2^-23 |a|, |a| <= 130 below which
           // they flush to 0 and are bounded by V 2^-126)
-          const double ES = S * (kEx2Raw + kSum8Err + 1e-12 + 130.0 * kLn2W * 0x1p-23) + Wt * 0.0 +
+          const double ES = S * (kEx2Raw + kSum16Err + 1e-12 + 130.0 * kLn2W * 0x1p-23) + Wt * 0.0 +
                             S * kLn2W * 0x1p-24 * (2.0 + 2.0 * (double)fmaxf(mL, mLr)) + (double)V * 0x1p-126;
           ExpCtx ec;
           ec.m = M;
