@@ -404,6 +404,24 @@ __device__ __forceinline__ int rs_get_many(const RegStack& r, const int32_t* arr
   return hit ? v : arr[idx];
 }
 
+// Single-entry push / pop (the common case: one slot, single-page entries).
+__device__ __forceinline__ void rs_push1(RegStack& r, int32_t* arr, long long idx, int v, int lane) {
+  if (lane == 0) arr[idx] = v;
+  if (idx < r.base || idx >= r.base + 32) {
+    r.base = idx;
+    r.valid = 0;
+  }
+  const int off = (int)(idx - r.base);
+  if (lane == off) r.val = v;
+  r.valid |= 1u << off;
+}
+__device__ __forceinline__ int rs_get1(const RegStack& r, const int32_t* arr, long long idx) {
+  const long long off = idx - r.base;
+  const bool hit = off >= 0 && off < 32 && ((r.valid >> (int)(off & 31)) & 1u);
+  const int v = __shfl_sync(0xffffffffu, r.val, (int)(off & 31));
+  return hit ? v : arr[idx];
+}
+
 // 32-bucket window probe at d's home bucket.  found: slot or -1; *empty_pos: first empty
 // bucket index (absolute) or -1 when the window holds none; *chain_open: the probe chain
 // runs past the window without a verdict.
@@ -425,7 +443,7 @@ __device__ __forceinline__ int window_find(const CacheDev& c, uint64_t d, int la
 
 // Backward-shift deletion of d when its chain closes inside the 32-bucket window;
 // otherwise lane 0 runs the scalar table_delete.
-__device__ void window_delete(const CacheDev& c, uint64_t d, int lane) {
+__device__ __forceinline__ void window_delete(const CacheDev& c, uint64_t d, int lane) {
   const uint32_t b0 = home_bucket(d, c.hmask);
   const uint32_t bl = (b0 + lane) & c.hmask;
   const int hv = c.hvals[bl];
@@ -501,7 +519,7 @@ __device__ __forceinline__ void ring_prefetch_next(const CacheDev& c, const Ring
 }
 
 // Enter the window starting at position t: take the preloaded one when it matches.
-__device__ void ring_enter(const CacheDev& c, RingWin& w, long long t, long long head, int lane) {
+__device__ __forceinline__ void ring_enter(const CacheDev& c, RingWin& w, long long t, long long head, int lane) {
   if (w.nbase != t) ring_load_next(c, w, t, head, lane);
   w.base = w.nbase;
   w.loaded = w.nloaded;
@@ -536,7 +554,7 @@ __device__ __forceinline__ void ctl_flush(const CacheDev& c, const Ctl& L, int l
 }
 
 // Oldest live unpinned entry (next_victim), or s = -1.
-__device__ Victim warp_next_victim(const CacheDev& c, Ctl& L, RingWin& w, int lane) {
+__device__ __forceinline__ Victim warp_next_victim(const CacheDev& c, Ctl& L, RingWin& w, int lane) {
   Victim v{-1, 0, 0, 0, false};
   for (;;) {
     if (L.side_count > 0) break;  // pinned entries pending: scalar path
@@ -594,6 +612,29 @@ __device__ Victim warp_next_victim(const CacheDev& c, Ctl& L, RingWin& w, int la
     v.gen = c.gen[s];
   }
   return v;
+}
+
+// push_pages for the warp policy: the entry's pages go on the free stack in page order
+__device__ __forceinline__ void warp_push_pages(const CacheDev& c, Ctl& L, RegStack& fp, int s, int lane) {
+  if (c.maxp == 1) {
+    const int pg = c.pages[s];
+    if (pg >= 0) {
+      if (lane == 0) c.pages[s] = -1;
+      rs_push1(fp, c.free_pages, L.free_page_top, pg, lane);
+      L.free_page_top += 1;
+    }
+    return;
+  }
+  for (int k0 = 0; k0 < c.maxp; k0 += 32) {
+    const int k = k0 + lane;
+    const int pg = k < c.maxp ? c.pages[(int64_t)s * c.maxp + k] : -1;
+    const unsigned have = __ballot_sync(0xffffffffu, pg >= 0);
+    const int m = __ffs(~have) - 1 < 0 ? 32 : __ffs(~have) - 1;
+    if (lane < m) c.pages[(int64_t)s * c.maxp + k] = -1;
+    rs_push_many(fp, c.free_pages, L.free_page_top, m, pg, lane);
+    L.free_page_top += m;
+    if (m < 32) break;
+  }
 }
 
 __global__ void __launch_bounds__(32) insert_policy_kernel(CacheDev c, const uint64_t* __restrict__ dig,
@@ -660,16 +701,7 @@ __global__ void __launch_bounds__(32) insert_policy_kernel(CacheDev c, const uin
       uint32_t g;
       if (s >= 0) {  // overwrite: the key keeps its slot, the entry is new
         L.total_bytes -= c.nbytes[s];
-        for (int k0 = 0; k0 < c.maxp; k0 += 32) {  // push_pages
-          const int k = k0 + lane;
-          const int pg = k < c.maxp ? c.pages[(int64_t)s * c.maxp + k] : -1;
-          const unsigned have = __ballot_sync(0xffffffffu, pg >= 0);
-          const int m = __ffs(~have) - 1 < 0 ? 32 : __ffs(~have) - 1;
-          if (lane < m) c.pages[(int64_t)s * c.maxp + k] = -1;
-          rs_push_many(fp, c.free_pages, L.free_page_top, m, pg, lane);
-          L.free_page_top += m;
-          if (m < 32) break;
-        }
+        warp_push_pages(c, L, fp, s, lane);
         g = c.gen[s] + 1u;
         if (lane == 0) c.gen[s] = g;
       } else {
@@ -677,8 +709,7 @@ __global__ void __launch_bounds__(32) insert_policy_kernel(CacheDev c, const uin
           if (!L.error) L.error = LC_E_CAPACITY;
           continue;
         }
-        s = rs_get_many(fs, c.free_slots, L.free_slot_top - 1, 1, lane);
-        s = __shfl_sync(0xffffffffu, s, 0);
+        s = rs_get1(fs, c.free_slots, L.free_slot_top - 1);
         L.free_slot_top--;
         if (eb == 0xffffffffu || open) {  // no empty bucket in the window
           if (lane == 0) table_insert(c, d, s);
@@ -699,11 +730,17 @@ __global__ void __launch_bounds__(32) insert_policy_kernel(CacheDev c, const uin
         __syncwarp();
         continue;
       }
-      for (int k0 = 0; k0 < np; k0 += 32) {
-        const int m = min(32, np - k0);
-        const int pg = rs_get_many(fp, c.free_pages, L.free_page_top - 1, m, lane);
-        if (lane < m) c.pages[(int64_t)s * c.maxp + k0 + lane] = pg;
-        L.free_page_top -= m;
+      if (np == 1) {  // (single-page entries: one broadcast value, no lane scatter)
+        const int pg = rs_get1(fp, c.free_pages, L.free_page_top - 1);
+        if (lane == 0) c.pages[(int64_t)s * c.maxp] = pg;
+        L.free_page_top -= 1;
+      } else {
+        for (int k0 = 0; k0 < np; k0 += 32) {
+          const int m = min(32, np - k0);
+          const int pg = rs_get_many(fp, c.free_pages, L.free_page_top - 1, m, lane);
+          if (lane < m) c.pages[(int64_t)s * c.maxp + k0 + lane] = pg;
+          L.free_page_top -= m;
+        }
       }
       L.clock += 1;
       if (lane == 0) {
@@ -731,17 +768,8 @@ __global__ void __launch_bounds__(32) insert_policy_kernel(CacheDev c, const uin
         // evict_entry
         window_delete(c, v.digest, lane);
         L.total_bytes -= v.nbytes;
-        for (int k0 = 0; k0 < c.maxp; k0 += 32) {  // push_pages
-          const int k = k0 + lane;
-          const int pg = k < c.maxp ? c.pages[(int64_t)v.s * c.maxp + k] : -1;
-          const unsigned have = __ballot_sync(0xffffffffu, pg >= 0);
-          const int m = __ffs(~have) - 1 < 0 ? 32 : __ffs(~have) - 1;
-          if (lane < m) c.pages[(int64_t)v.s * c.maxp + k] = -1;
-          rs_push_many(fp, c.free_pages, L.free_page_top, m, pg, lane);
-          L.free_page_top += m;
-          if (m < 32) break;
-        }
-        rs_push_many(fs, c.free_slots, L.free_slot_top, 1, v.s, lane);
+        warp_push_pages(c, L, fp, v.s, lane);
+        rs_push1(fs, c.free_slots, L.free_slot_top, v.s, lane);
         L.free_slot_top += 1;
         if (lane == 0) {
           c.gen[v.s] = v.gen + 1u;
