@@ -814,8 +814,10 @@ __global__ void insert_copy_kernel(CacheDev c, const int32_t* __restrict__ lens,
     if (same && al) {
       const int per = 16 / sizeof(DstT);
       const int nv = vv / per;
+      // streaming (evict-first) loads and stores: rows pass through L2 once and must not
+      // evict the index / event ring / entry metadata the policy warp works on
       for (int k = threadIdx.x; k < nv; k += blockDim.x)
-        reinterpret_cast<uint4*>(drow)[k] = __ldg(reinterpret_cast<const uint4*>(srow) + k);
+        __stcs(reinterpret_cast<uint4*>(drow) + k, __ldcs(reinterpret_cast<const uint4*>(srow) + k));
       for (int k = nv * per + threadIdx.x; k < vv; k += blockDim.x) drow[k] = reinterpret_cast<const DstT*>(srow)[k];
     } else {
       for (int k = threadIdx.x; k < vv; k += blockDim.x) {
