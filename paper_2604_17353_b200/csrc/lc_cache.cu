@@ -443,7 +443,8 @@ __device__ __forceinline__ int window_find(const CacheDev& c, uint64_t d, int la
 
 // Backward-shift deletion of d when its chain closes inside the 32-bucket window;
 // otherwise lane 0 runs the scalar table_delete.
-__device__ __forceinline__ void window_delete(const CacheDev& c, uint64_t d, int lane) {
+__device__ __forceinline__ void window_delete(const CacheDev& c, uint64_t d, int lane, uint32_t sh_b,
+                                              unsigned& st_home) {
   const uint32_t b0 = home_bucket(d, c.hmask);
   const uint32_t bl = (b0 + lane) & c.hmask;
   const int hv = c.hvals[bl];
@@ -456,6 +457,7 @@ __device__ __forceinline__ void window_delete(const CacheDev& c, uint64_t d, int
     if (fe >= 32) {  // chain leaves the window
       if (lane == 0) table_delete(c, d);
       __syncwarp();
+      st_home = 0xffffffffu;
     }
     return;  // absent
   }
@@ -463,6 +465,7 @@ __device__ __forceinline__ void window_delete(const CacheDev& c, uint64_t d, int
   if (i + 1 >= 32 || (em >> (i + 1)) == 0u) {  // shift may run past the window
     if (lane == 0) table_delete(c, d);
     __syncwarp();
+    st_home = 0xffffffffu;
     return;
   }
   const uint32_t home_l = home_bucket(hk, c.hmask);
@@ -478,9 +481,11 @@ __device__ __forceinline__ void window_delete(const CacheDev& c, uint64_t d, int
       c.hkeys[ai] = kj;
       c.hvals[ai] = vj;
     }
+    st_home |= __ballot_sync(0xffffffffu, sh_b == ai);
     i = j;
   }
   if (lane == 0) c.hvals[(b0 + i) & c.hmask] = -1;
+  st_home |= __ballot_sync(0xffffffffu, sh_b == ((b0 + i) & c.hmask));
   __syncwarp();
 }
 
@@ -490,6 +495,11 @@ struct RingWin {
   unsigned dead;       // events known dead
   int slot;            // lane l: event base + l
   unsigned long long clock;
+  unsigned stale;      // records whose slot was written since the window was entered
+  int pins, pg;        // lane l's entry when live: pins, first page (maxp == 1), bytes, digest, gen
+  long long nb;
+  uint64_t dg;
+  uint32_t gen;
   long long nbase;     // next window, loaded ahead
   unsigned nloaded;
   int nslot;
@@ -525,14 +535,28 @@ __device__ __forceinline__ void ring_enter(const CacheDev& c, RingWin& w, long l
   w.loaded = w.nloaded;
   w.slot = w.nslot;
   w.clock = w.nclock;
-  // liveness prefilter + hash windows of the live events' digests
+  // liveness prefilter, the live events' entry records (valid until their slot is written:
+  // w.stale) and the hash windows of their digests
   const int s = w.slot;
   bool live = false;
+  w.pins = 0;
+  w.pg = -2;
+  w.nb = 0;
+  w.dg = 0;
+  w.gen = 0;
   if (s >= 0) {
     live = c.alive[s] && c.last_hit[s] == w.clock;
-    if (live) pf_window(c, c.digest[s]);
+    if (live) {
+      w.dg = c.digest[s];
+      w.pins = c.pins[s];
+      w.nb = c.nbytes[s];
+      w.gen = c.gen[s];
+      if (c.maxp == 1) w.pg = c.pages[s];
+      pf_window(c, w.dg);
+    }
   }
   w.dead = __ballot_sync(0xffffffffu, !live) & w.loaded;
+  w.stale = 0u;
   // next window: events now, metadata lines prefetched; the window after: ring lines
   pf1(c.ring_slot + ((t + 64 + lane) & c.rmask));
   pf1(c.ring_clock + ((t + 64 + lane) & c.rmask));
@@ -545,6 +569,7 @@ struct Victim {
   long long nbytes;
   uint64_t digest;
   uint32_t gen;
+  int pg;       // first page when known (maxp == 1), else -2
   bool scalar;  // chosen by the scalar fallback (control block reloaded)
 };
 
@@ -555,7 +580,7 @@ __device__ __forceinline__ void ctl_flush(const CacheDev& c, const Ctl& L, int l
 
 // Oldest live unpinned entry (next_victim), or s = -1.
 __device__ __forceinline__ Victim warp_next_victim(const CacheDev& c, Ctl& L, RingWin& w, int lane) {
-  Victim v{-1, 0, 0, 0, false};
+  Victim v{-1, 0, 0, 0, -2, false};
   for (;;) {
     if (L.side_count > 0) break;  // pinned entries pending: scalar path
     if (L.ring_tail >= L.ring_head) return v;
@@ -576,6 +601,17 @@ __device__ __forceinline__ Victim warp_next_victim(const CacheDev& c, Ctl& L, Ri
     L.ring_tail = w.base + o;
     const int s = __shfl_sync(0xffffffffu, w.slot, o);
     const unsigned long long ck = __shfl_sync(0xffffffffu, w.clock, o);
+    if (!((w.stale >> o) & 1u)) {  // the record taken at window entry still holds: live
+      const int pins = __shfl_sync(0xffffffffu, w.pins, o);
+      if (pins > 0) break;  // scalar path moves it to the side list
+      L.ring_tail++;
+      v.s = s;
+      v.nbytes = __shfl_sync(0xffffffffu, w.nb, o);
+      v.digest = __shfl_sync(0xffffffffu, w.dg, o);
+      v.gen = __shfl_sync(0xffffffffu, w.gen, o);
+      v.pg = __shfl_sync(0xffffffffu, w.pg, o);
+      return v;
+    }
     const bool alive = c.alive[s];
     const unsigned long long lh = c.last_hit[s];
     const int pins = c.pins[s];
@@ -615,9 +651,10 @@ __device__ __forceinline__ Victim warp_next_victim(const CacheDev& c, Ctl& L, Ri
 }
 
 // push_pages for the warp policy: the entry's pages go on the free stack in page order
-__device__ __forceinline__ void warp_push_pages(const CacheDev& c, Ctl& L, RegStack& fp, int s, int lane) {
+__device__ __forceinline__ void warp_push_pages(const CacheDev& c, Ctl& L, RegStack& fp, int s, int lane,
+                                                int known_pg = -2) {
   if (c.maxp == 1) {
-    const int pg = c.pages[s];
+    const int pg = known_pg != -2 ? known_pg : c.pages[s];
     if (pg >= 0) {
       if (lane == 0) c.pages[s] = -1;
       rs_push1(fp, c.free_pages, L.free_page_top, pg, lane);
@@ -647,6 +684,8 @@ __global__ void __launch_bounds__(32) insert_policy_kernel(CacheDev c, const uin
   RingWin w;
   w.base = -1;
   w.nbase = -1;
+  w.slot = -1;
+  w.stale = 0u;
   int last_ev_slot = -1;
   uint32_t last_ev_gen = 0;
   // chunk pipeline: cur (c), nx1 (c+1), nx2 (c+2)
@@ -669,15 +708,30 @@ __global__ void __launch_bounds__(32) insert_policy_kernel(CacheDev c, const uin
   for (int64_t i0 = 0; i0 < n; i0 += 32) {
     ld(i0 + 64 + lane, d2, n2, v2);
     if (i0 + 32 + lane < n) pf_window(c, d1);
-    if (i0 + lane < n) {  // this chunk's keys found at their home bucket: prefetch the overwrite path's lines
-      const uint32_t hb = home_bucket(d0, c.hmask);
-      const int hs = c.hvals[hb];
-      if (hs >= 0 && c.hkeys[hb] == d0) {
-        pf1(c.nbytes + hs);
-        pf1(c.gen + hs);
-        pf1(c.pages + (int64_t)hs * c.maxp);
+    // speculative records of this chunk's keys (lane l = element l): the home bucket and,
+    // when it holds the key, the entry's bytes / generation / first page.  A record is used
+    // only while nothing it depends on was written since (st_home: its home bucket;
+    // st_slot: its entry); every table or entry write below marks the records it touches.
+    const uint32_t sh_b = home_bucket(d0, c.hmask);
+    int sh_v = -1, sp_s = -1, sp_pg = -2;
+    uint64_t sh_k = 0;
+    long long sp_nb = 0;
+    uint32_t sp_gen = 0;
+    if (i0 + lane < n) {
+      sh_v = c.hvals[sh_b];
+      sh_k = c.hkeys[sh_b];
+      if (sh_v >= 0 && sh_k == d0) {
+        sp_s = sh_v;
+        sp_nb = c.nbytes[sp_s];
+        sp_gen = c.gen[sp_s];
+        if (c.maxp == 1) sp_pg = c.pages[sp_s];
       }
     }
+    unsigned st_home = 0u, st_slot = 0u;
+    auto mark_slot = [&](int x) {
+      st_slot |= __ballot_sync(0xffffffffu, sp_s == x);
+      w.stale |= __ballot_sync(0xffffffffu, w.slot == x);
+    };
     int my_slot = -1;
     uint32_t my_gen = 0;
     const int cnt = (int)min((int64_t)32, n - i0);
@@ -692,17 +746,40 @@ __global__ void __launch_bounds__(32) insert_policy_kernel(CacheDev c, const uin
       }
       const long long bytes = (long long)nr * vv * 4 + 8ll * nr;  // logits_cache.py:54-56
       uint32_t eb;
-      bool open;
-      int s = window_find(c, d, lane, &eb, &open);
-      if (open) {
-        if (lane == 0) s = table_find(c, d);
-        s = __shfl_sync(0xffffffffu, s, 0);
+      bool open = false;
+      int s;
+      const bool rec = !((st_home >> j) & 1u);
+      const int hv0 = __shfl_sync(0xffffffffu, sh_v, j);
+      const uint64_t hk0 = __shfl_sync(0xffffffffu, sh_k, j);
+      bool from_rec = false;
+      if (rec && hv0 >= 0 && hk0 == d) {  // found at its home bucket
+        s = hv0;
+        from_rec = !((st_slot >> j) & 1u);
+      } else if (rec && hv0 < 0) {  // empty home bucket: absent, and the insert goes there
+        s = -1;
+        eb = __shfl_sync(0xffffffffu, sh_b, j);
+      } else {
+        s = window_find(c, d, lane, &eb, &open);
+        if (open) {
+          if (lane == 0) s = table_find(c, d);
+          s = __shfl_sync(0xffffffffu, s, 0);
+        }
       }
       uint32_t g;
       if (s >= 0) {  // overwrite: the key keeps its slot, the entry is new
-        L.total_bytes -= c.nbytes[s];
-        warp_push_pages(c, L, fp, s, lane);
-        g = c.gen[s] + 1u;
+        long long onb;
+        int opg = -2;
+        if (from_rec) {
+          onb = __shfl_sync(0xffffffffu, sp_nb, j);
+          g = __shfl_sync(0xffffffffu, sp_gen, j) + 1u;
+          opg = __shfl_sync(0xffffffffu, sp_pg, j);
+        } else {
+          onb = c.nbytes[s];
+          g = c.gen[s] + 1u;
+        }
+        mark_slot(s);
+        L.total_bytes -= onb;
+        warp_push_pages(c, L, fp, s, lane, opg);
         if (lane == 0) c.gen[s] = g;
       } else {
         if (L.free_slot_top == 0) {
@@ -711,11 +788,16 @@ __global__ void __launch_bounds__(32) insert_policy_kernel(CacheDev c, const uin
         }
         s = rs_get1(fs, c.free_slots, L.free_slot_top - 1);
         L.free_slot_top--;
+        mark_slot(s);
         if (eb == 0xffffffffu || open) {  // no empty bucket in the window
           if (lane == 0) table_insert(c, d, s);
-        } else if (lane == 0) {
-          c.hkeys[eb] = d;
-          c.hvals[eb] = s;
+          st_home = 0xffffffffu;
+        } else {
+          if (lane == 0) {
+            c.hkeys[eb] = d;
+            c.hvals[eb] = s;
+          }
+          st_home |= __ballot_sync(0xffffffffu, sh_b == eb);
         }
         if (lane == 0) c.alive[s] = 1;
         L.alive += 1;
@@ -766,9 +848,10 @@ __global__ void __launch_bounds__(32) insert_policy_kernel(CacheDev c, const uin
         Victim v = warp_next_victim(c, L, w, lane);
         if (v.s < 0) break;
         // evict_entry
-        window_delete(c, v.digest, lane);
+        mark_slot(v.s);
+        window_delete(c, v.digest, lane, sh_b, st_home);
         L.total_bytes -= v.nbytes;
-        warp_push_pages(c, L, fp, v.s, lane);
+        warp_push_pages(c, L, fp, v.s, lane, v.pg);
         rs_push1(fs, c.free_slots, L.free_slot_top, v.s, lane);
         L.free_slot_top += 1;
         if (lane == 0) {
