@@ -444,7 +444,11 @@ __device__ __forceinline__ int window_find(const CacheDev& c, uint64_t d, int la
 // Backward-shift deletion of d when its chain closes inside the 32-bucket window;
 // otherwise lane 0 runs the scalar table_delete.
 __device__ __forceinline__ void window_delete(const CacheDev& c, uint64_t d, int lane, uint32_t sh_b,
-                                              unsigned& st_home) {
+                                              unsigned& st_home, uint32_t w_hb, unsigned& w_bstale) {
+  auto mark = [&](uint32_t b) {
+    st_home |= __ballot_sync(0xffffffffu, sh_b == b);
+    w_bstale |= __ballot_sync(0xffffffffu, w_hb == b || ((w_hb + 1) & c.hmask) == b);
+  };
   const uint32_t b0 = home_bucket(d, c.hmask);
   const uint32_t bl = (b0 + lane) & c.hmask;
   const int hv = c.hvals[bl];
@@ -458,6 +462,7 @@ __device__ __forceinline__ void window_delete(const CacheDev& c, uint64_t d, int
       if (lane == 0) table_delete(c, d);
       __syncwarp();
       st_home = 0xffffffffu;
+      w_bstale = 0xffffffffu;
     }
     return;  // absent
   }
@@ -466,6 +471,7 @@ __device__ __forceinline__ void window_delete(const CacheDev& c, uint64_t d, int
     if (lane == 0) table_delete(c, d);
     __syncwarp();
     st_home = 0xffffffffu;
+    w_bstale = 0xffffffffu;
     return;
   }
   const uint32_t home_l = home_bucket(hk, c.hmask);
@@ -481,11 +487,11 @@ __device__ __forceinline__ void window_delete(const CacheDev& c, uint64_t d, int
       c.hkeys[ai] = kj;
       c.hvals[ai] = vj;
     }
-    st_home |= __ballot_sync(0xffffffffu, sh_b == ai);
+    mark(ai);
     i = j;
   }
   if (lane == 0) c.hvals[(b0 + i) & c.hmask] = -1;
-  st_home |= __ballot_sync(0xffffffffu, sh_b == ((b0 + i) & c.hmask));
+  mark((b0 + i) & c.hmask);
   __syncwarp();
 }
 
@@ -496,6 +502,9 @@ struct RingWin {
   int slot;            // lane l: event base + l
   unsigned long long clock;
   unsigned stale;      // records whose slot was written since the window was entered
+  unsigned bstale;     // records whose home bucket (or the one after it) was written since
+  uint32_t hb;         // lane l's digest home bucket
+  bool quick;          // its key sits at hb with hb + 1 empty: deletion = clearing hb
   int pins, pg;        // lane l's entry when live: pins, first page (maxp == 1), bytes, digest, gen
   long long nb;
   uint64_t dg;
@@ -552,11 +561,14 @@ __device__ __forceinline__ void ring_enter(const CacheDev& c, RingWin& w, long l
       w.nb = c.nbytes[s];
       w.gen = c.gen[s];
       if (c.maxp == 1) w.pg = c.pages[s];
-      pf_window(c, w.dg);
     }
   }
+  w.hb = home_bucket(w.dg, c.hmask);
+  w.quick = false;
+  if (live) w.quick = c.hvals[w.hb] == s && c.hkeys[w.hb] == w.dg && c.hvals[(w.hb + 1) & c.hmask] < 0;
   w.dead = __ballot_sync(0xffffffffu, !live) & w.loaded;
   w.stale = 0u;
+  w.bstale = 0u;
   // next window: events now, metadata lines prefetched; the window after: ring lines
   pf1(c.ring_slot + ((t + 64 + lane) & c.rmask));
   pf1(c.ring_clock + ((t + 64 + lane) & c.rmask));
@@ -571,6 +583,8 @@ struct Victim {
   uint32_t gen;
   int pg;       // first page when known (maxp == 1), else -2
   bool scalar;  // chosen by the scalar fallback (control block reloaded)
+  bool quick;   // deletion = clearing bucket hb (record still valid)
+  uint32_t hb;
 };
 
 __device__ __forceinline__ void ctl_flush(const CacheDev& c, const Ctl& L, int lane) {
@@ -580,7 +594,7 @@ __device__ __forceinline__ void ctl_flush(const CacheDev& c, const Ctl& L, int l
 
 // Oldest live unpinned entry (next_victim), or s = -1.
 __device__ __forceinline__ Victim warp_next_victim(const CacheDev& c, Ctl& L, RingWin& w, int lane) {
-  Victim v{-1, 0, 0, 0, -2, false};
+  Victim v{-1, 0, 0, 0, -2, false, false, 0u};
   for (;;) {
     if (L.side_count > 0) break;  // pinned entries pending: scalar path
     if (L.ring_tail >= L.ring_head) return v;
@@ -610,6 +624,8 @@ __device__ __forceinline__ Victim warp_next_victim(const CacheDev& c, Ctl& L, Ri
       v.digest = __shfl_sync(0xffffffffu, w.dg, o);
       v.gen = __shfl_sync(0xffffffffu, w.gen, o);
       v.pg = __shfl_sync(0xffffffffu, w.pg, o);
+      v.quick = __shfl_sync(0xffffffffu, (int)w.quick, o) && !((w.bstale >> o) & 1u);
+      v.hb = __shfl_sync(0xffffffffu, w.hb, o);
       return v;
     }
     const bool alive = c.alive[s];
@@ -686,6 +702,9 @@ __global__ void __launch_bounds__(32) insert_policy_kernel(CacheDev c, const uin
   w.nbase = -1;
   w.slot = -1;
   w.stale = 0u;
+  w.bstale = 0u;
+  w.hb = 0u;
+  w.quick = false;
   int last_ev_slot = -1;
   uint32_t last_ev_gen = 0;
   // chunk pipeline: cur (c), nx1 (c+1), nx2 (c+2)
@@ -792,12 +811,14 @@ __global__ void __launch_bounds__(32) insert_policy_kernel(CacheDev c, const uin
         if (eb == 0xffffffffu || open) {  // no empty bucket in the window
           if (lane == 0) table_insert(c, d, s);
           st_home = 0xffffffffu;
+          w.bstale = 0xffffffffu;
         } else {
           if (lane == 0) {
             c.hkeys[eb] = d;
             c.hvals[eb] = s;
           }
           st_home |= __ballot_sync(0xffffffffu, sh_b == eb);
+          w.bstale |= __ballot_sync(0xffffffffu, w.hb == eb || ((w.hb + 1) & c.hmask) == eb);
         }
         if (lane == 0) c.alive[s] = 1;
         L.alive += 1;
@@ -849,7 +870,13 @@ __global__ void __launch_bounds__(32) insert_policy_kernel(CacheDev c, const uin
         if (v.s < 0) break;
         // evict_entry
         mark_slot(v.s);
-        window_delete(c, v.digest, lane, sh_b, st_home);
+        if (v.quick) {  // key at its home bucket, next bucket empty: no shift
+          if (lane == 0) c.hvals[v.hb] = -1;
+          st_home |= __ballot_sync(0xffffffffu, sh_b == v.hb);
+          w.bstale |= __ballot_sync(0xffffffffu, w.hb == v.hb || ((w.hb + 1) & c.hmask) == v.hb);
+        } else {
+          window_delete(c, v.digest, lane, sh_b, st_home, w.hb, w.bstale);
+        }
         L.total_bytes -= v.nbytes;
         warp_push_pages(c, L, fp, v.s, lane, v.pg);
         rs_push1(fs, c.free_slots, L.free_slot_top, v.s, lane);
