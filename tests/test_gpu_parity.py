@@ -436,6 +436,56 @@ def test_cache_warp_policy_stress_vs_oracle(collide, page_rows, max_rows):
     assert orc.evictions > 20
 
 
+def test_cache_warp_policy_large_batches_vs_oracle():
+    """Batches of hundreds of inserts (many 32-key chunks, duplicates within a batch, several
+    evictions per batch spanning many LRU windows) interleaved with lookups and pins: slots and
+    generations bit-exact vs the oracle, accounting and the live map equal after every batch."""
+    rng = np.random.default_rng(5)
+    V, E = 16, 4096
+    budget = (V * 4 + 8) * 900
+    cache = lcb.LogitsCache(budget, vocab=V, key_capacity=E, page_rows=1, max_rows=1, page_capacity=E)
+    orc = cache_ref.CacheOracle(budget, E, E, 1)
+    keys = [mixing_ref.mix2(9, k) for k in range(3000)]
+    pinned = []
+    for step in range(30):
+        if rng.random() < 0.3:
+            batch = [keys[int(i)] for i in rng.integers(0, len(keys), int(rng.integers(1, 400)))]
+            slot = cache.lookup_batch(lcb._dev.u64_tensor(batch, DEV))[0]
+            want = [-1 if (e := orc.lookup(d)) is None else e.slot for d in batch]
+            assert slot.cpu().tolist() == want
+        if rng.random() < 0.3 and orc.entries:
+            ds = list(orc.entries)
+            for _ in range(int(rng.integers(1, 6))):
+                e = orc.entries[ds[int(rng.integers(0, len(ds)))]]
+                delta = -1 if (e.slot, e.gen) in pinned and rng.random() < 0.5 else 1
+                if delta == 1:
+                    pinned.append((e.slot, e.gen))
+                else:
+                    pinned.remove((e.slot, e.gen))
+                orc.pin(e.slot, e.gen, delta)
+                st_ = torch.tensor([e.slot], dtype=torch.int32, device=DEV)
+                gt_ = torch.tensor([e.gen], dtype=torch.int64, device=DEV).to(torch.int32)
+                _capi.check(_capi.lib.lc_cache_pin(cache.handle, st_.data_ptr(), gt_.data_ptr(), 1, delta,
+                                                   cache._stream()))
+            cache._dirty()
+        nb = int(rng.integers(100, 700))
+        batch = [keys[int(i)] for i in rng.integers(0, len(keys), nb)]
+        rows = torch.zeros((nb, V), dtype=torch.float32, device=DEV)
+        slot, gen = cache.insert_batch(lcb._dev.u64_tensor(batch, DEV), torch.ones(nb, dtype=torch.int32, device=DEV),
+                                       torch.full((nb,), V, dtype=torch.int32, device=DEV), rows,
+                                       torch.arange(nb, dtype=torch.int64, device=DEV), None, 1)
+        want = [orc.insert(d, 1, V)[0] for d in batch]
+        assert slot.cpu().tolist() == [e.slot for e in want], step
+        assert (gen.cpu().numpy().astype(np.int64) & 0xFFFFFFFF).tolist() == [e.gen for e in want], step
+        st = cache._stats()
+        assert (st.entries, st.total_bytes, st.hits, st.lookups, st.evictions) == (
+            len(orc.entries), orc.total, orc.hits, orc.lookups, orc.evictions), step
+        snap = cache._snapshot()
+        live = {int(snap["digest"][s]): int(s) for s in np.flatnonzero(snap["alive"])}
+        assert live == {d: e.slot for d, e in orc.entries.items()}, step
+    assert orc.evictions > 3000
+
+
 def test_cache_update_shape_errors_and_accounting():
     cache = lcb.LogitsCache()
     with pytest.raises(lcb.ConfigError):
