@@ -498,6 +498,11 @@ def run_c3_sweep(args, cfg, rank, world, dev):
     for s in range(args.warmup):
         step(s, False)
     torch.cuda.synchronize(dev)
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.barrier()
+        torch.cuda.synchronize(dev)
     t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(dev.index) as clk:
         t0.record()
@@ -506,6 +511,10 @@ def run_c3_sweep(args, cfg, rank, world, dev):
         t1.record()
         torch.cuda.synchronize(dev)
     ms = t0.elapsed_time(t1)
+    from paper_2604_17353_b200.shard import reduce_stats
+
+    ms = float(reduce_stats(torch.tensor([ms], dtype=torch.float64, device=dev),
+                            torch.zeros(1, dtype=torch.float64, device=dev), world)[0][0])  # max over ranks
     hit_ms = sum(a.elapsed_time(b) for a, b in ev_hit) / args.steps
     miss_ms = sum(a.elapsed_time(b) for a, b in ev_miss) / args.steps
     slots = torch.stack([o[0] for o in outs]).cpu().numpy()
@@ -650,6 +659,11 @@ def run_c4(args, cfg, rank, world, dev):
         outs.extend(step(i))
     torch.cuda.synchronize(dev)
     st0 = cache._stats()
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.barrier()
+        torch.cuda.synchronize(dev)
     t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(dev.index) as clk:
         t0.record()
@@ -660,6 +674,11 @@ def run_c4(args, cfg, rank, world, dev):
     ms = t0.elapsed_time(t1)
     st1 = cache._stats()
     evictions = st1.evictions - st0.evictions if hasattr(st1, "evictions") else None
+    from paper_2604_17353_b200.shard import reduce_stats
+
+    tt, cc = reduce_stats(torch.tensor([ms], dtype=torch.float64, device=dev),
+                          torch.tensor([float(evictions or 0)], dtype=torch.float64, device=dev), world)
+    ms, evictions = float(tt[0]), int(cc[0])  # max over ranks; evictions summed over ranks
 
     ins_ms = sum(a.elapsed_time(b) for a, b in ev) / len(ev)
 
@@ -725,7 +744,7 @@ def run_c4(args, cfg, rank, world, dev):
     e_ms = e0.elapsed_time(e1)
     res["e2e"] = {"value": n_timed * world / (e_ms * 1e-3), "unit": "inserts/s", "h2d_bytes_per_step": B * 8,
                   "d2h_bytes_per_step": B * 4}
-    if not args.no_cpu_baseline:
+    if not args.no_cpu_baseline and rank == 0:
         res["cpu_baseline"] = c4_cpu_baseline(V, seconds=min(args.cpu_seconds, 10.0))
     return res
 
