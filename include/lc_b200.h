@@ -206,6 +206,12 @@ int lc_cache_gather(lc_cache* cache, const int32_t* d_slot, const int32_t* d_pos
 int lc_cache_tokens(lc_cache* cache, const int32_t* d_slot, const int32_t* d_pos, int64_t n, int32_t* d_out,
                     void* stream);
 
+/* Hotspot scoring straight from the slab (sampling.py:112-125 on entry.logits_seq):
+ * entropy H and max probability of softmax(z / T) for cached rows (slot, pos), fp64,
+ * without gathering the rows; a missing row gives H = 0, max p = 1.             */
+int lc_cache_row_entropy(lc_cache* cache, const int32_t* d_slot, const int32_t* d_pos, int64_t n, double temperature,
+                         double* d_entropy, double* d_pmax, void* stream);
+
 /* Resample cached rows: tasks use (slot, pos) with row = -1. */
 int lc_cache_resample(lc_cache* cache, const lc_task* d_tasks, int64_t n_tasks, lc_draws draws, void* d_workspace,
                       int64_t workspace_bytes, int64_t* d_counters, void* stream);

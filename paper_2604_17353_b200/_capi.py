@@ -94,6 +94,7 @@ _SIGS = {
     "lc_cache_insert": (C.c_int, [P, P, P, P, I64, P, I32, I64, P, P, I32, P, P, P]),
     "lc_cache_pin": (C.c_int, [P, P, P, I64, I32, P]),
     "lc_cache_gather": (C.c_int, [P, P, P, I64, P, I32, I64, P]),
+    "lc_cache_row_entropy": (C.c_int, [P, P, P, I64, C.c_double, P, P, P]),
     "lc_cache_tokens": (C.c_int, [P, P, P, I64, P, P]),
     "lc_cache_resample": (C.c_int, [P, P, I64, LcDraws, P, I64, P, P]),
     "lc_cache_stats_get": (C.c_int, [P, C.POINTER(LcCacheStats), P]),

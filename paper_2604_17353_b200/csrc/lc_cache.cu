@@ -972,6 +972,20 @@ __global__ void gather_kernel(CacheDev c, const int32_t* __restrict__ slot, cons
   }
 }
 
+// slab address of cached row (slot, pos) -- null when the entry or position is gone
+__global__ void row_ptr_kernel(CacheDev c, const int32_t* __restrict__ slot, const int32_t* __restrict__ pos,
+                               int64_t n, const char** out, int32_t* vocab_out) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const int s = slot[i], t = pos[i];
+  const bool ok = s >= 0 && s < c.E && c.alive[s] && t >= 0 && t < c.nrows[s];
+  const size_t esz = c.dtype == LC_F32 ? 4 : 2;
+  out[i] = ok ? c.slab + ((int64_t)c.pages[(int64_t)s * c.maxp + t / c.page_rows] * c.page_rows + t % c.page_rows) *
+                             (int64_t)c.V * esz
+              : nullptr;
+  vocab_out[i] = ok ? c.vocab[s] : 1;
+}
+
 __global__ void tokens_kernel(CacheDev c, const int32_t* __restrict__ slot, const int32_t* __restrict__ pos, int64_t n,
                               int32_t* out) {
   int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -1263,6 +1277,29 @@ extern "C" int lc_cache_tokens(lc_cache* c, const int32_t* d_slot, const int32_t
   tokens_kernel<<<ceil_div(n, 256), 256, 0, (cudaStream_t)stream>>>(c->dev, d_slot, d_pos, n, d_out);
   LCB_CUDA_TRY(cudaGetLastError());
   return LC_OK;
+}
+
+namespace lcb {
+int launch_entropy_ptrs(const char* const* d_rows, const int32_t* d_vocab, int dtype, int64_t n, double T, double* H,
+                        double* pmax, cudaStream_t st);
+}
+
+extern "C" int lc_cache_row_entropy(lc_cache* c, const int32_t* d_slot, const int32_t* d_pos, int64_t n,
+                                    double temperature, double* d_entropy, double* d_pmax, void* stream) {
+  if (!c || n < 0 || !(temperature >= 0.0) || (n > 0 && (!d_slot || !d_pos || !d_entropy || !d_pmax)))
+    return LC_E_ARG;
+  if (n == 0) return LC_OK;
+  cudaStream_t st = (cudaStream_t)stream;
+  void* scratch = nullptr;  // row addresses + vocab sizes, stream-ordered
+  LCB_CUDA_TRY(cudaMallocAsync(&scratch, (size_t)n * (sizeof(char*) + sizeof(int32_t)) + 16, st));
+  const char** ptrs = reinterpret_cast<const char**>(scratch);
+  int32_t* voc = reinterpret_cast<int32_t*>(ptrs + n);
+  row_ptr_kernel<<<ceil_div(n, 256), 256, 0, st>>>(c->dev, d_slot, d_pos, n, ptrs, voc);
+  int rc = LC_OK;
+  if (cudaGetLastError() != cudaSuccess) rc = LC_E_CUDA;
+  if (rc == LC_OK) rc = lcb::launch_entropy_ptrs(ptrs, voc, c->dev.dtype, n, temperature, d_entropy, d_pmax, st);
+  LCB_CUDA_TRY(cudaFreeAsync(scratch, st));
+  return rc;
 }
 
 extern "C" int lc_cache_resample(lc_cache* c, const lc_task* d_tasks, int64_t n_tasks, lc_draws draws,

@@ -97,19 +97,18 @@ __global__ void draw_probs_kernel(const double* probs, int64_t V, int64_t stride
 
 // H = -sum p ln p = ln S - sum(e*s)/S with s <= 0 the shifted scaled logits;
 // pmax = max p = 1/S (sampling.py:112-126).
+// one block per row: H = log S - sum(e s) / S and max p = 1 / S of softmax(z / T), fp64
 template <int DT>
-__global__ void __launch_bounds__(PB_THREADS)
-entropy_kernel(const char* rows, int64_t row_bytes, int64_t V, double T, double* H, double* pmax) {
+__device__ __forceinline__ void entropy_row(const char* row, int64_t V, double T, double* H, double* pmax) {
   __shared__ float fred[PB_THREADS / 32];
   __shared__ double dred[PB_THREADS / 32];
-  const char* row = rows + blockIdx.x * row_bytes;
   float m = -INFINITY;
   for (int64_t i = threadIdx.x; i < V; i += PB_THREADS) m = fmaxf(m, ld<DT>(row, i));
   m = block_max(m, fred);
   if (T == 0.0) {
     if (threadIdx.x == 0) {
-      H[blockIdx.x] = 0.0;
-      pmax[blockIdx.x] = 1.0;
+      *H = 0.0;
+      *pmax = 1.0;
     }
     return;
   }
@@ -124,9 +123,40 @@ entropy_kernel(const char* rows, int64_t row_bytes, int64_t V, double T, double*
   se = block_sum(se, dred);
   ses = block_sum(ses, dred);
   if (threadIdx.x == 0) {
-    H[blockIdx.x] = log(se) - ses / se;
-    pmax[blockIdx.x] = 1.0 / se;
+    *H = log(se) - ses / se;
+    *pmax = 1.0 / se;
   }
+}
+
+template <int DT>
+__global__ void __launch_bounds__(PB_THREADS)
+entropy_kernel(const char* rows, int64_t row_bytes, int64_t V, double T, double* H, double* pmax) {
+  entropy_row<DT>(rows + blockIdx.x * row_bytes, V, T, H + blockIdx.x, pmax + blockIdx.x);
+}
+
+// rows given by address (slab rows of cached entries, lc_cache_row_entropy); a null
+// address (missing row) yields H = 0, max p = 1
+template <int DT>
+__global__ void __launch_bounds__(PB_THREADS)
+entropy_ptr_kernel(const char* const* rows, const int32_t* vocab, double T, double* H, double* pmax) {
+  const char* row = rows[blockIdx.x];
+  if (!row) {
+    if (threadIdx.x == 0) {
+      H[blockIdx.x] = 0.0;
+      pmax[blockIdx.x] = 1.0;
+    }
+    return;
+  }
+  entropy_row<DT>(row, vocab[blockIdx.x], T, H + blockIdx.x, pmax + blockIdx.x);
+}
+
+int launch_entropy_ptrs(const char* const* d_rows, const int32_t* d_vocab, int dtype, int64_t n, double T, double* H,
+                        double* pmax, cudaStream_t st) {
+  if (n <= 0) return LC_OK;
+  if (dtype == LC_F32) entropy_ptr_kernel<LC_F32><<<(unsigned)n, PB_THREADS, 0, st>>>(d_rows, d_vocab, T, H, pmax);
+  else entropy_ptr_kernel<LC_BF16><<<(unsigned)n, PB_THREADS, 0, st>>>(d_rows, d_vocab, T, H, pmax);
+  LCB_CUDA_TRY(cudaGetLastError());
+  return LC_OK;
 }
 
 }  // namespace lcb

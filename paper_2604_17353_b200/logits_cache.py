@@ -487,15 +487,28 @@ class LogitsCache:
 
     # -- hotspot precomputation (logits_cache.py:153-183) --------------------------------
 
+    def row_scores(self, entry: CachedTrajectory, temperature: float, decay: float) -> np.ndarray:
+        """sampling.row_scores of the entry's rows, read from the slab in place
+        (lc_cache_row_entropy: no gather of the rows)."""
+        n = len(entry)
+        d = self.dev
+        s = torch.full((n,), entry.slot, dtype=torch.int32, device=d)
+        p = torch.arange(n, dtype=torch.int32, device=d)
+        H = torch.empty(n, dtype=torch.float64, device=d)
+        pm = torch.empty(n, dtype=torch.float64, device=d)
+        _capi.check(_capi.lib.lc_cache_row_entropy(self.handle, s.data_ptr(), p.data_ptr(), n, float(temperature),
+                                                   H.data_ptr(), pm.data_ptr(), self._stream()),
+                    "lc_cache_row_entropy")
+        t = torch.arange(n, dtype=torch.float64, device=d)
+        return (H * (1.0 - pm) / (1.0 + decay * t)).cpu().numpy()
+
     def hotspots_for(self, entry: CachedTrajectory, cfg: SamplingConfig, params: HotspotParams) -> tuple[int, ...]:
         key = params.cache_key(cfg.temperature)
         cached = entry.hotspots.get(key)
         if cached is None:
-            rows = entry.logits_device()
-            cached = sampling.select_hotspots(sampling.row_scores(rows, cfg.temperature, params.decay, self.dev),
-                                              params) if len(entry) else ()
             if len(entry) == 0:
                 raise ConfigError("logits_seq must be non-empty")
+            cached = sampling.select_hotspots(self.row_scores(entry, cfg.temperature, params.decay), params)
             entry.hotspots[key] = cached
             self.hotspot_computations += 1
         return cached

@@ -289,6 +289,31 @@ def test_hotspots_golden():
         assert list(lcb.identify_hotspots(list(rows), cfg, hp)) == case["hotspots"]
 
 
+@pytest.mark.parametrize("dtype", ["float32", "bfloat16"])
+def test_cache_hotspots_from_slab_match_golden(dtype):
+    """hotspots_for scores the entry's rows in place (lc_cache_row_entropy) -- same hotspots as
+    the reference's identify_hotspots on the same rows (golden cases), and the same scores as
+    row_scores on the gathered rows."""
+    for case in load_json("hotspots.json"):
+        rows = np.array(case["rows"], dtype=np.uint32).view(np.float32)
+        if dtype == "bfloat16":
+            rows = mixing_ref.bf16_round(rows)
+        n, V = rows.shape
+        cache = lcb.LogitsCache(1 << 30, vocab=V, dtype=dtype, max_rows=max(n, 1))
+        cache.insert_batch(lcb._dev.u64_tensor([77], DEV), torch.tensor([n], dtype=torch.int32, device=DEV),
+                           torch.tensor([V], dtype=torch.int32, device=DEV), torch.from_numpy(rows).to(DEV),
+                           torch.zeros(1, dtype=torch.int64, device=DEV), None, n)
+        e = cache.lookup(lcb.StateKey(77))
+        cfg = lcb.SamplingConfig(temperature=case["T"], max_tokens=1)
+        hp = lcb.HotspotParams(decay=case["decay"], threshold=case["threshold"], max_hotspots=case["max_hotspots"])
+        got = cache.row_scores(e, case["T"], case["decay"])
+        want = lcb.sampling.row_scores(e.logits_device(), case["T"], case["decay"], DEV)
+        assert np.array_equal(got, want)
+        assert list(cache.hotspots_for(e, cfg, hp)) == list(lcb.identify_hotspots(list(rows), cfg, hp))
+        if dtype == "float32":
+            assert list(cache.hotspots_for(e, cfg, hp)) == case["hotspots"]
+
+
 # -- cache ---------------------------------------------------------------------------------------
 
 
