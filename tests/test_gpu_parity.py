@@ -511,6 +511,48 @@ def test_cache_warp_policy_large_batches_vs_oracle():
     assert orc.evictions > 3000
 
 
+def test_miss_path_producer_resample_insert_then_replay():
+    """The C3-sweep miss path end to end at a small size: producer rows (lc_fill_logits) ->
+    resample with the branch seeds -> insert; the tokens equal the oracle's draws on the
+    bf16 producer rows, and a later replay of the same keys hits, reads back the same rows
+    and cached tokens, and (same seeds, draw number = position) replays every position."""
+    V, n, R = 4096, 12, 6
+    cache = lcb.LogitsCache(1 << 30, vocab=V, dtype="bfloat16", max_rows=R, page_rows=2)
+    keys = [mixing_ref.hash_tokens([7, 7, j]) for j in range(n)]
+    states = [mixing_ref.mix2(7, 1000 + i) for i in range(n * R)]
+    rows = torch.empty((n * R, V), dtype=torch.bfloat16, device=DEV)
+    st = lcb._dev.u64_tensor(states, DEV)
+    _capi.check(_capi.lib.lc_fill_logits(st.data_ptr(), n * R, V, 2.5, 5.0, _capi.LC_BF16, rows.data_ptr(), V, None))
+    ref_rows = mixing_ref.bf16_round(mixing_ref.fill_rows_np(states, V, 2.5))
+    assert np.array_equal(rows.float().cpu().numpy(), ref_rows)
+    seeds = [mixing_ref.mix2(1, j) for j in range(n)]
+    tasks = lcb.make_tasks(row=np.arange(n * R), pos=np.tile(np.arange(R), n), temperature=0.6, top_k=50,
+                           top_p=0.95, draw_begin=np.arange(n * R), draw_end=np.arange(n * R) + 1,
+                           seed_base=np.repeat(np.arange(n), R))
+    tok, _ = lcb.resample(rows, tasks, seeds=lcb._dev.u64_tensor(seeds, DEV), n_draws=n * R)
+    tok = tok.cpu().numpy()
+    for j in range(n):
+        for t in range(R):
+            u = mixing_ref.uniform(seeds[j], t)
+            assert tok[j * R + t] == _oracle_tokens(ref_rows[j * R + t: j * R + t + 1], 0.6, 50, 0.95, [[u]])[0]
+    dig = lcb._dev.u64_tensor(keys, DEV)
+    cache.insert_batch(dig, torch.full((n,), R, dtype=torch.int32, device=DEV),
+                       torch.full((n,), V, dtype=torch.int32, device=DEV), rows,
+                       torch.arange(n, dtype=torch.int64, device=DEV) * R, torch.from_numpy(tok).to(DEV), R)
+    for j in range(n):
+        e = cache.lookup(lcb.StateKey(keys[j]))
+        assert e is not None and len(e) == R
+        assert np.array_equal(e.logits_seq, ref_rows[j * R:(j + 1) * R])
+        assert e.token_seq == tok[j * R:(j + 1) * R].tolist()
+    T = torch.full((n,), 0.6, dtype=torch.float64, device=DEV)
+    K = torch.full((n,), 50, dtype=torch.int32, device=DEV)
+    P = torch.full((n,), 0.95, dtype=torch.float64, device=DEV)
+    rtok, rep, div, slot, ln = cache.replay_stepwise(dig, R, 1, lcb._dev.u64_tensor(seeds, DEV), T, K, P)
+    assert np.all(slot.cpu().numpy() >= 0)
+    assert np.all(rep.cpu().numpy() == R) and np.all(div.cpu().numpy() == -1)
+    assert np.array_equal(rtok.cpu().numpy(), tok)
+
+
 def test_cache_update_shape_errors_and_accounting():
     cache = lcb.LogitsCache()
     with pytest.raises(lcb.ConfigError):
