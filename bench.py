@@ -533,7 +533,9 @@ def run_c3_sweep(args, cfg, rank, world, dev):
         "lookup_hit_ratio": lookup_hits, "position_hit_ratio": pos_hit,
         "lookup_resample_ms_per_step": hit_ms, "miss_path_ms_per_step": miss_ms,
         "miss_path": "lc_fill_logits (producer) -> resample -> lc_cache_insert",
-        "gpu_launches": None, "clocks": clk.summary(),
+        # per step: lookup (probe + commit), replay tasks, resample (row kernel + requeue + exact),
+        # cached tokens, acceptance; misses: producer, resample (3), insert (policy + copy)
+        "gpu_launches": (8 + (6 if n_miss else 0)) * args.steps, "clocks": clk.summary(),
     }
 
 
