@@ -602,7 +602,7 @@ __global__ void __launch_bounds__(SG_THREADS, 1) stage_kernel(StageArgs a) {
 #pragma unroll
                   for (int j = 0; j < 8; ++j) {
                     const uint32_t off = (j & 1) ? off_hi(w[j >> 1]) : off_lo(w[j >> 1]);
-                    msum[k] += G.ev[off < bs ? off : SG_NB + lane];
+                    if (off < bs) msum[k] += G.ev[off];
                     ccnt[k] += (off == bs);
                   }
                 }
