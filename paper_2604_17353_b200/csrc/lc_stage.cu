@@ -722,7 +722,7 @@ __global__ void __launch_bounds__(SG_THREADS, 1) stage_kernel(StageArgs a) {
 #pragma unroll
               for (int j = 0; j < 8; ++j) {
                 const uint32_t off = (j & 1) ? off_hi(w[j >> 1]) : off_lo(w[j >> 1]);
-                k8[j] = G.ev[off < bs ? off : SG_NB + lane];
+                k8[j] = off < bs ? G.ev[off] : 0.0;
                 le += (off == bs);
               }
               // the cut class's kept ties (only sub-chunks holding some pay for their ranks)
