@@ -205,9 +205,25 @@ def run_ours(args, cfg, rank, world, dev):
         ev.append((s, e))
         return r
 
-    def step():
-        return cache.replay_stepwise(w["digests"], R, nb, w["seeds"], w["T"], w["K"], w["P"], counters=counters,
-                                     bufs=w["bufs"])
+    hot_rows = n_rows
+    if args.policy == "hotspot":  # ReplayPolicy.HOTSPOT: hotspots per entry (memoised, untimed like the reference)
+        cfg_s = lcb.SamplingConfig(temperature=cfg["T"], top_k=cfg["k"] or None, top_p=cfg["p"], max_tokens=R)
+        hp = lcb.HotspotParams(decay=0.001, threshold=0.6)
+        dig_h = lcb._dev.u64_numpy(w["digests"])
+        hots = []
+        for dg in dig_h:
+            e = cache.lookup(lcb.StateKey(int(dg)))
+            hots.append(cache.hotspots_for(e, cfg_s, hp))
+        d_di = cache.hotspot_draw_index(hots, R, dev)
+        hot_rows = sum(len(h) for h in hots)
+
+        def step():
+            return cache.replay_hotspot(w["digests"], R, nb, w["seeds"], w["T"], w["K"], w["P"], counters=counters,
+                                        bufs=w["bufs"], draw_index=d_di)
+    else:
+        def step():
+            return cache.replay_stepwise(w["digests"], R, nb, w["seeds"], w["T"], w["K"], w["P"],
+                                         counters=counters, bufs=w["bufs"])
 
     lcb.sampling.resample = timed_resample
     try:
@@ -268,8 +284,12 @@ def run_ours(args, cfg, rank, world, dev):
         d_seed.copy_(h_seed, non_blocking=True)
         _capi.check(_capi.lib.lc_hash_prefix(d_tok.data_ptr(), d_off.data_ptr(), None, n_req, d_dig.data_ptr(),
                                              _dev.stream_ptr(dev)))
-        tok, rep, div, slot, ln = cache.replay_stepwise(d_dig, R, nb, d_seed, w["T"], w["K"], w["P"],
-                                                        bufs=bufsets[k])
+        if args.policy == "hotspot":
+            tok, rep, div, slot, ln = cache.replay_hotspot(d_dig, R, nb, d_seed, w["T"], w["K"], w["P"],
+                                                           bufs=bufsets[k], draw_index=d_di)
+        else:
+            tok, rep, div, slot, ln = cache.replay_stepwise(d_dig, R, nb, d_seed, w["T"], w["K"], w["P"],
+                                                            bufs=bufsets[k])
         done = torch.cuda.Event()
         done.record(main)
         with torch.cuda.stream(copy_stream):
@@ -311,8 +331,10 @@ def run_ours(args, cfg, rank, world, dev):
         return None
     tokens_total = (n_draws * args.steps * world if cfg["scaling"] == "weak"
                     else CONFIGS[args.config]["n_req"] * R * nb * args.steps)
+    if args.policy == "hotspot":  # only hotspot positions draw
+        tokens_total = hot_rows * nb * args.steps * world
     peak, peak_src = peaks()
-    algo_bytes_launch = n_rows * V * esz + n_draws * 20  # V*s per unique row + 20 B per draw
+    algo_bytes_launch = hot_rows * V * esz + hot_rows * nb * 20  # V*s per unique row + 20 B per draw
     k_avg = sum(k_ms) / max(len(k_ms), 1)
     achieved = algo_bytes_launch / (k_avg * 1e-3) / 1e9
     res = {
@@ -331,7 +353,10 @@ def run_ours(args, cfg, rank, world, dev):
         "config": {"workload": cfg["desc"], "config": args.config, "vocab": V, "requests_per_gpu": n_req,
                    "branches": nb, "rows_per_entry": R, "draws_per_row": nb, "temperature": cfg["T"],
                    "top_k": cfg["k"] or None, "top_p": cfg["p"], "slab_gb_per_gpu": w["slab_bytes"] / 1e9,
-                   "l2": "inputs larger than L2 (slab re-read every step)", "parallelism": f"tree-sharded x{world}"},
+                   "l2": "inputs larger than L2 (slab re-read every step)", "parallelism": f"tree-sharded x{world}",
+                   "replay_policy": args.policy,
+                   **({"hotspot_decay": 0.001, "hotspot_threshold": 0.6, "hotspot_rows": hot_rows}
+                      if args.policy == "hotspot" else {})},
         "accepted_tokens_per_s": accepted / (ms * 1e-3),
         "rows_per_s": (n_rows * world if cfg["scaling"] == "weak" else CONFIGS[args.config]["n_req"] * R)
         * args.steps / (ms * 1e-3),
@@ -761,6 +786,8 @@ def main():
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-check", action="store_true", help="c4: skip the oracle replay of the op trace")
+    ap.add_argument("--policy", default="step_wise", choices=["step_wise", "hotspot"],
+                    help="replay policy of the resample step (ReplayPolicy)")
     ap.add_argument("--hit-ratio", type=float, default=None,
                     help="c3: lookup hit ratio h of the sweep (default: every branch cached)")
     args = ap.parse_args()

@@ -348,9 +348,19 @@ class LogitsCache:
                     "lc_replay_accept")
         return tok, b["rep"], b["div"], slot, ln
 
+    @staticmethod
+    def hotspot_draw_index(hotspots, max_pos: int, dev=None) -> torch.Tensor:
+        """Device array [n_req * max_pos]: the RngStream draw number of each hotspot position
+        (hotspots of the request before it), -1 elsewhere -- the layout replay_hotspot takes."""
+        di = np.full((len(hotspots), max_pos), -1, dtype=np.int32)
+        for r, hs in enumerate(hotspots):
+            hs = sorted(t for t in hs if 0 <= t < max_pos)
+            di[r, hs] = np.arange(len(hs), dtype=np.int32)
+        return torch.from_numpy(di.reshape(-1)).to(_dev.device(dev))
+
     def replay_hotspot(self, digests: torch.Tensor, max_pos: int, n_branch: int, seeds: torch.Tensor,
-                       temperature: torch.Tensor, top_k: torch.Tensor, top_p: torch.Tensor, hotspots,
-                       counters=None, bufs: dict | None = None):
+                       temperature: torch.Tensor, top_k: torch.Tensor, top_p: torch.Tensor, hotspots=None,
+                       counters=None, bufs: dict | None = None, draw_index: torch.Tensor | None = None):
         """ReplayPolicy.HOTSPOT for a batch (engine.py:311-326): request r samples only at
         the positions in ``hotspots[r]`` (RngStream draw number = hotspots before t) and
         copies the cached token elsewhere; the replay stops after the first hotspot sample
@@ -358,13 +368,14 @@ class LogitsCache:
         holds the engine's ``out`` tokens at every replayed position."""
         n_req = digests.numel()
         d = self.dev
-        if len(hotspots) != n_req:
-            raise ConfigError("one hotspot tuple per request")
-        di = np.full((n_req, max_pos), -1, dtype=np.int32)
-        for r, hs in enumerate(hotspots):
-            hs = sorted(t for t in hs if 0 <= t < max_pos)
-            di[r, hs] = np.arange(len(hs), dtype=np.int32)
-        d_di = torch.from_numpy(di.reshape(-1)).to(d)
+        if draw_index is None:
+            if hotspots is None or len(hotspots) != n_req:
+                raise ConfigError("one hotspot tuple per request")
+            d_di = self.hotspot_draw_index(hotspots, max_pos, d)
+        else:
+            if draw_index.numel() != n_req * max_pos:
+                raise ConfigError("draw_index must hold n_req * max_pos entries")
+            d_di = draw_index
         slot, gen, ln, vv = self.lookup_batch(digests)
         b = bufs if bufs is not None else {}
         ntask = n_req * max_pos
