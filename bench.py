@@ -215,11 +215,12 @@ def run_ours(args, cfg, rank, world, dev):
             e = cache.lookup(lcb.StateKey(int(dg)))
             hots.append(cache.hotspots_for(e, cfg_s, hp))
         d_di = cache.hotspot_draw_index(hots, R, dev)
+        hot_l = cache.hotspot_list(d_di)
         hot_rows = sum(len(h) for h in hots)
 
         def step():
             return cache.replay_hotspot(w["digests"], R, nb, w["seeds"], w["T"], w["K"], w["P"], counters=counters,
-                                        bufs=w["bufs"], draw_index=d_di)
+                                        bufs=w["bufs"], draw_index=d_di, hot_list=hot_l)
     else:
         def step():
             return cache.replay_stepwise(w["digests"], R, nb, w["seeds"], w["T"], w["K"], w["P"],
@@ -286,7 +287,7 @@ def run_ours(args, cfg, rank, world, dev):
                                              _dev.stream_ptr(dev)))
         if args.policy == "hotspot":
             tok, rep, div, slot, ln = cache.replay_hotspot(d_dig, R, nb, d_seed, w["T"], w["K"], w["P"],
-                                                           bufs=bufsets[k], draw_index=d_di)
+                                                           bufs=bufsets[k], draw_index=d_di, hot_list=hot_l)
         else:
             tok, rep, div, slot, ln = cache.replay_stepwise(d_dig, R, nb, d_seed, w["T"], w["K"], w["P"],
                                                             bufs=bufsets[k])

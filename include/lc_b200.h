@@ -245,6 +245,13 @@ int lc_replay_accept(const int32_t* d_tokens, const int32_t* d_cached, const int
 int lc_replay_tasks_hotspot(const int32_t* d_slot, const int32_t* d_len, const int32_t* d_draw_index, int64_t n_req,
                             int32_t max_pos, int32_t n_branch, const double* d_temperature, const int32_t* d_top_k,
                             const double* d_top_p, lc_task* d_tasks, void* stream);
+/* The hotspot tasks for a compact list: d_hot_pos[j] = r * max_pos + t of the j-th
+ * hotspot position, d_hot_draw[j] its draw number; writes n_hot tasks (draws at the
+ * same indices as lc_replay_tasks_hotspot), so the resample skips non-hotspot rows.   */
+int lc_replay_tasks_hotspot_list(const int32_t* d_slot, const int32_t* d_len, const int64_t* d_hot_pos,
+                                 const int32_t* d_hot_draw, int64_t n_hot, int32_t max_pos, int32_t n_branch,
+                                 const double* d_temperature, const int32_t* d_top_k, const double* d_top_p,
+                                 lc_task* d_tasks, void* stream);
 int lc_replay_accept_hotspot(int32_t* d_tokens, const int32_t* d_cached, const int32_t* d_len,
                              const int32_t* d_draw_index, int64_t n_req, int32_t max_pos, int32_t n_branch,
                              int32_t* d_replayed, int32_t* d_diverged, void* stream);

@@ -106,6 +106,7 @@ _SIGS = {
     "lc_replay_accept": (C.c_int, [P, P, P, I64, I32, I32, P, P, P]),
     "lc_replay_tasks_hotspot": (C.c_int, [P, P, P, I64, I32, I32, P, P, P, P, P]),
     "lc_replay_accept_hotspot": (C.c_int, [P, P, P, P, I64, I32, I32, P, P, P]),
+    "lc_replay_tasks_hotspot_list": (C.c_int, [P, P, P, P, I64, I32, I32, P, P, P, P, P]),
 }
 
 

@@ -82,6 +82,35 @@ __global__ void replay_tasks_hot_kernel(const int32_t* __restrict__ slot, const 
   tasks[i] = tk;
 }
 
+// The same tasks for a compact list of hotspot positions only (flat index r * max_pos + t
+// and its draw number): the resample sees n_hot tasks instead of n_req * max_pos.
+__global__ void replay_tasks_hot_list_kernel(const int32_t* __restrict__ slot, const int32_t* __restrict__ len,
+                                             const int64_t* __restrict__ hot_pos, const int32_t* __restrict__ hot_di,
+                                             int64_t n_hot, int max_pos, int nb, const double* __restrict__ temp,
+                                             const int32_t* __restrict__ topk, const double* __restrict__ topp,
+                                             lc_task* __restrict__ tasks) {
+  const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= n_hot) return;
+  const int64_t i = hot_pos[j];
+  const int64_t r = i / max_pos;
+  const int t = (int)(i % max_pos);
+  const int s = slot[r];
+  const int lim = s >= 0 ? min(len[r], max_pos) : 0;
+  lc_task tk;
+  tk.row = -1;
+  tk.slot = s;
+  tk.pos = t;
+  tk.temperature = temp[r];
+  tk.top_k = topk[r];
+  tk.vocab = 0;
+  tk.top_p = topp[r];
+  tk.draw_begin = i * nb;
+  tk.draw_end = t < lim ? i * nb + nb : i * nb;
+  tk.seed_base = r * nb;
+  tk.u_index = hot_di[j];
+  tasks[j] = tk;
+}
+
 // Hotspot acceptance: non-hotspot positions take the cached token (written into
 // d_tokens so the output is the engine's `out` list); the replay stops after the
 // first hotspot whose sample differs from the cached token.
@@ -123,6 +152,20 @@ extern "C" int lc_replay_tasks_hotspot(const int32_t* d_slot, const int32_t* d_l
   if (!d_slot || !d_len || !d_draw_index || !d_temperature || !d_top_k || !d_top_p || !d_tasks) return LC_E_ARG;
   lcb::replay_tasks_hot_kernel<<<lcb::ceil_div(n, 256), 256, 0, (cudaStream_t)stream>>>(
       d_slot, d_len, d_draw_index, n_req, max_pos, n_branch, d_temperature, d_top_k, d_top_p, d_tasks);
+  LCB_CUDA_TRY(cudaGetLastError());
+  return LC_OK;
+}
+
+extern "C" int lc_replay_tasks_hotspot_list(const int32_t* d_slot, const int32_t* d_len, const int64_t* d_hot_pos,
+                                            const int32_t* d_hot_draw, int64_t n_hot, int32_t max_pos,
+                                            int32_t n_branch, const double* d_temperature, const int32_t* d_top_k,
+                                            const double* d_top_p, lc_task* d_tasks, void* stream) {
+  if (n_hot < 0 || max_pos < 0 || n_branch < 0) return LC_E_ARG;
+  if (n_hot == 0) return LC_OK;
+  if (!d_slot || !d_len || !d_hot_pos || !d_hot_draw || !d_temperature || !d_top_k || !d_top_p || !d_tasks)
+    return LC_E_ARG;
+  lcb::replay_tasks_hot_list_kernel<<<lcb::ceil_div(n_hot, 256), 256, 0, (cudaStream_t)stream>>>(
+      d_slot, d_len, d_hot_pos, d_hot_draw, n_hot, max_pos, n_branch, d_temperature, d_top_k, d_top_p, d_tasks);
   LCB_CUDA_TRY(cudaGetLastError());
   return LC_OK;
 }

@@ -358,9 +358,16 @@ class LogitsCache:
             di[r, hs] = np.arange(len(hs), dtype=np.int32)
         return torch.from_numpy(di.reshape(-1)).to(_dev.device(dev))
 
+    @staticmethod
+    def hotspot_list(draw_index: torch.Tensor):
+        """Compact (flat position, draw number) lists of the hotspots in a draw-index array."""
+        pos = torch.nonzero(draw_index >= 0).flatten()
+        return pos.to(torch.int64), draw_index[pos].to(torch.int32).contiguous()
+
     def replay_hotspot(self, digests: torch.Tensor, max_pos: int, n_branch: int, seeds: torch.Tensor,
                        temperature: torch.Tensor, top_k: torch.Tensor, top_p: torch.Tensor, hotspots=None,
-                       counters=None, bufs: dict | None = None, draw_index: torch.Tensor | None = None):
+                       counters=None, bufs: dict | None = None, draw_index: torch.Tensor | None = None,
+                       hot_list=None):
         """ReplayPolicy.HOTSPOT for a batch (engine.py:311-326): request r samples only at
         the positions in ``hotspots[r]`` (RngStream draw number = hotspots before t) and
         copies the cached token elsewhere; the replay stops after the first hotspot sample
@@ -389,11 +396,22 @@ class LogitsCache:
             b["rep"] = torch.empty(n_req * n_branch, dtype=torch.int32, device=d)
             b["div"] = torch.empty(n_req * n_branch, dtype=torch.int32, device=d)
         st = self._stream()
-        _capi.check(_capi.lib.lc_replay_tasks_hotspot(slot.data_ptr(), ln.data_ptr(), d_di.data_ptr(), n_req,
-                                                      max_pos, n_branch, temperature.data_ptr(), top_k.data_ptr(),
-                                                      top_p.data_ptr(), b["tasks"].data_ptr(), st),
-                    "lc_replay_tasks_hotspot")
-        tok, flags = sampling.resample(None, b["tasks"][: ntask * _capi.TASK_DTYPE.itemsize], seeds=seeds,
+        if hot_list is not None:  # only the hotspot positions become tasks
+            hp, hd = hot_list
+            n_hot = hp.numel()
+            _capi.check(_capi.lib.lc_replay_tasks_hotspot_list(slot.data_ptr(), ln.data_ptr(), hp.data_ptr(),
+                                                               hd.data_ptr(), n_hot, max_pos, n_branch,
+                                                               temperature.data_ptr(), top_k.data_ptr(),
+                                                               top_p.data_ptr(), b["tasks"].data_ptr(), st),
+                        "lc_replay_tasks_hotspot_list")
+            ntask_run = n_hot
+        else:
+            _capi.check(_capi.lib.lc_replay_tasks_hotspot(slot.data_ptr(), ln.data_ptr(), d_di.data_ptr(), n_req,
+                                                          max_pos, n_branch, temperature.data_ptr(),
+                                                          top_k.data_ptr(), top_p.data_ptr(), b["tasks"].data_ptr(),
+                                                          st), "lc_replay_tasks_hotspot")
+            ntask_run = ntask
+        tok, flags = sampling.resample(None, b["tasks"][: ntask_run * _capi.TASK_DTYPE.itemsize], seeds=seeds,
                                        n_draws=ndraw, cache=self, counters=counters, out=(b["tok"], b["flags"]))
         slots_rep = slot.repeat_interleave(max_pos)
         _capi.check(_capi.lib.lc_cache_tokens(self.handle, slots_rep.data_ptr(), b["pos"].data_ptr(), ntask,

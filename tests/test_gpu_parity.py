@@ -642,6 +642,18 @@ def test_replay_hotspot_matches_oracle():
     max_pos = 32
     tok, rep, div, slot, ln = cache.replay_hotspot(digests, max_pos, nb, lcb._dev.u64_tensor(seeds, DEV), T, K,
                                                    Pp, hot)
+    tok, rep, div = tok.clone(), rep.clone(), div.clone()
+    # compact task list (only hotspot positions become tasks): identical results
+    d_di = cache.hotspot_draw_index(hot, max_pos, DEV)
+    tl, rl, dl, _, _ = cache.replay_hotspot(digests, max_pos, nb, lcb._dev.u64_tensor(seeds, DEV), T, K, Pp,
+                                            draw_index=d_di, hot_list=cache.hotspot_list(d_di))
+    assert torch.equal(rl, rep) and torch.equal(dl, div)
+    rep_np = rep.cpu().numpy().reshape(n_req + 1, nb)
+    tk, tkl = tok.cpu().numpy().reshape(n_req + 1, max_pos, nb), tl.cpu().numpy().reshape(n_req + 1, max_pos, nb)
+    for r in range(n_req + 1):
+        for b in range(nb):
+            n_out = int(rep_np[r, b])
+            assert np.array_equal(tk[r, :n_out, b], tkl[r, :n_out, b])
     tok = tok.cpu().numpy().reshape(n_req + 1, max_pos, nb)
     rep = rep.cpu().numpy().reshape(n_req + 1, nb)
     div = div.cpu().numpy().reshape(n_req + 1, nb)
