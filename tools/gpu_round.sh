@@ -1,15 +1,25 @@
 #!/bin/bash
-# One GPU round: build check, gpu tests, bench (c2 default + c3), ncu launch list, ncu full capture of rowwarp.
+# One GPU round: gpu tests, smoke, every bench line (C2 default + reference arm, C1, C3, C5, C4,
+# C3 hit-ratio sweep, hotspot replay), the C2 ncu launch list and full captures of the hot kernels.
 set -x
 cd "$GRAFT_REPO_ROOT"
 O=gpurun_out
+mkdir -p $O
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm --format=csv > $O/smi.txt 2>&1
-timeout 900 python -m pytest tests -m gpu -x -q > $O/pytest_gpu.log 2>&1; echo "pytest rc=$?" >> $O/pytest_gpu.log
+timeout 1200 python -m pytest tests -m gpu -x -q > $O/pytest_gpu.log 2>&1; echo "pytest rc=$?" >> $O/pytest_gpu.log
+timeout 300 python -c "import __graft_entry__ as g; g.smoke(); print('smoke ok')" > $O/smoke.log 2>&1
 timeout 600 python bench.py > $O/bench_c2.json 2> $O/bench_c2.err
-timeout 600 python bench.py --config c3 --no-cpu-baseline > $O/bench_c3.json 2> $O/bench_c3.err
 timeout 600 python bench.py --impl reference --steps 3 --warmup 3 > $O/bench_ref.json 2> $O/bench_ref.err
+for c in c1 c3 c5; do
+  timeout 600 python bench.py --config $c --no-cpu-baseline > $O/bench_$c.json 2> $O/bench_$c.err
+done
+timeout 900 python bench.py --config c4 --cpu-seconds 5 > $O/bench_c4.json 2> $O/bench_c4.err
+timeout 600 python bench.py --config c1 --policy hotspot --no-cpu-baseline > $O/bench_c1h.json 2> $O/bench_c1h.err
+STEPS=5 bash tools/c3_sweep.sh
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $O/launches.csv \
     python bench.py --steps 2 --warmup 3 --no-cpu-baseline > $O/bench_ncu.log 2>&1
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:rowwarp -s 2 -c 1 -o $O/rowwarp -f \
-    python tools/prof_resample.py --V 32000 --rows 16384 --draws 32 --top-p 0.9 --bf16 --iters 3 > $O/ncu_full.log 2>&1
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:stage_kernel -s 9 -c 1 -o $O/stage -f \
+    python bench.py --steps 1 --warmup 3 --no-cpu-baseline > $O/ncu_stage.log 2>&1
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:wide_kernel -s 2 -c 1 -o $O/wide -f \
+    python tools/prof_resample.py --V 151936 --rows 8192 --draws 1 --top-k 50 --top-p 0.95 --bf16 --iters 3 > $O/ncu_wide.log 2>&1
 echo done
