@@ -48,6 +48,7 @@ constexpr double kLn2 = 0.6931471805599453;
 // ex2.approx.ftz.bf16x2 relative error incl. the bf16 rounding of its result
 // (pinned by tests/test_gpu_parity.py::test_bf16_ex2_bound over every bf16 input)
 constexpr float kEx2Bf16Err = 0.01f;  // measured max 0.0071 (2^-7.1)
+constexpr double kEx2Bf16F = (1.0 + (double)kEx2Bf16Err) / (1.0 - (double)kEx2Bf16Err);  // ratio bound factor
 
 struct SgGroup {
   uint32_t hist[SG_NB + 32];  // + one dump bin per lane (branch-free out-of-range increments)
@@ -364,8 +365,10 @@ __global__ void __launch_bounds__(SG_THREADS, 1) stage_kernel(StageArgs a) {
         // exponent error <= 2^-8 (1.001 |a| + |delta|), |delta| <= 2^-9 |m Lb|;
         // elements below 2^-40 bounded absolutely; fp32 accumulation of <= 200 terms + 32 + 5
         const float dl = 0.001953125f * mL * 1.01f + 0.001953125f;
-        const double F = (double)exp2f(0.00390625f * (40.1f + dl)) * (1.0 + kEx2Bf16Err) / (1.0 - kEx2Bf16Err);
-        const double tail = fmax(Sc / (double)emax - 1.0, 0.0);
+        // (no fp64 divisions on this per-row path: the ratio is a constant, 1/emax a correctly
+        // rounded reciprocal -- one extra 2^-53 rounding, far inside the 1e-9 / V 2^-40 slack)
+        const double F = (double)exp2f(0.00390625f * (40.1f + dl)) * kEx2Bf16F;
+        const double tail = fmax(Sc * __drcp_rn((double)emax) - 1.0, 0.0);
         Sfast = 1.0 + tail;
         const double Sup = (1.0 + F * tail * (1.0 + 3e-5) + (double)V * 0x1p-40) * (1.0 + 1e-9);
         fast = Sup * tv.topp < 1.0 - 1e-15;
