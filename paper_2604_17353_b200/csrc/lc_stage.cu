@@ -394,10 +394,12 @@ __global__ void __launch_bounds__(SG_THREADS, 1) stage_kernel(StageArgs a) {
         const uint32_t km = key16(__float_as_uint(m));
         // S >= max(1, S_fast / 1.25): the FAST estimate is within F <= 1.14 of the truth
         const double slo = fmax(Sfast / 1.25, 1.0);
-        const double alo = log2(fmax(0.5 * (1.0 - tv.topp) * slo / (double)V, 1e-300));
+        // (z_lo only sizes the exact histogram: a cut outside it is detected and requeued,
+        // so fp32 log2 and a multiply by T ln 2 are as good as fp64 here)
+        const float alo = log2f(fmaxf((float)(0.5 * (1.0 - tv.topp) * slo) / (float)V, 1e-37f));
         int nb_eff = SG_NB;
         {
-          const float zl = m + (float)(alo / Ld);
+          const float zl = m + alo * (float)(tv.T * kLn2);
           if (zl > -INFINITY) nb_eff = (int)min((uint32_t)SG_NB, km - key16(__float_as_uint(zl)) + 1u);
         }
         // e = ex2(fl(z Lf - fl(m Lf))) / ex2(fl(m Lf - fl(m Lf))): the common rounding of m Lf
@@ -458,7 +460,7 @@ __global__ void __launch_bounds__(SG_THREADS, 1) stage_kernel(StageArgs a) {
             R[v] = make_uint4(o[0], o[1], o[2], o[3]);
           }
         }
-        const double tail = gsum_d(tacc, 1) / (double)emax;
+        const double tail = gsum_d(tacc, 1) * __drcp_rn((double)emax);  // (2^-53 inside the 1e-12 slack)
         // numpy's S_np vs its own e's: pairwise sum, argument rounding, libm ulps
         const double relNp = (double)(2 * V + 64) * kEps64 + 4.5e-16 * (2.0 * (double)mL + 64.0) + 2.0 * kRefExpErr;
         if (!sane) {
