@@ -323,7 +323,7 @@ __global__ void __launch_bounds__(SG_THREADS, 1) stage_kernel(StageArgs a) {
       write_tok(first_argmax());
     } else {
       // ---------------------------------------------- B: FAST exit test (packed bf16x2)
-      const double Ld = kLog2e / tv.T;
+      const double Ld = tv.Ld;  // = kLog2e / tv.T, divided once by the producer
       const float Lf = (float)Ld;
       const float mL = fabsf(m) * Lf;
       bool fast = false;

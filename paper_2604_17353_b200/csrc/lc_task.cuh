@@ -97,6 +97,7 @@ struct TaskView {
   const char* row;
   int V;
   double T;
+  double Ld;  // log2(e) / T (0 when T == 0), computed once per task by whoever resolves it
   int topk;  // effective top-k (0 = none / k >= V)
   double topp;
   bool trunc;
@@ -140,6 +141,7 @@ __device__ __forceinline__ bool resolve_task(const lc_task& tk, const char* rows
   tv.u_index = tk.u_index >= 0 ? tk.u_index : tk.pos;
   tv.V = tk.vocab > 0 ? tk.vocab : Vdef;
   tv.T = tk.temperature;
+  tv.Ld = tv.T > 0.0 ? 1.4426950408889634 / tv.T : 0.0;
   tv.topk = (tk.top_k > 0 && tk.top_k < tv.V) ? tk.top_k : 0;
   tv.topp = tk.top_p;
   tv.trunc = !(tk.top_k <= 0 && tk.top_p == 1.0);
