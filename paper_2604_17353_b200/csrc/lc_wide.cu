@@ -297,7 +297,7 @@ __global__ void __launch_bounds__(WG_THREADS, 1) wide_kernel(StageArgs a) {
       issue(tv, 0);
       if (nch > 1) issue(tv, 1);
     }
-    const double Ld = tv.T > 0.0 ? kLog2eW / tv.T : 0.0;
+    const double Ld = tv.Ld;  // log2(e) / T from the producer (0 when T == 0)
     const float Lf = (float)Ld;
     bool bad = false;
     float M_run = -INFINITY;  // running max of the chunks seen
@@ -547,7 +547,9 @@ __global__ void __launch_bounds__(WG_THREADS, 1) wide_kernel(StageArgs a) {
           const double relArg = 4.5e-16 * (2.0 * (double)mL + 64.0);
           const double relA = kLiteErr + kRefExpErr + relArg + 128.0 * u53;
           const double relNp = (double)(2 * V + 64) * u53 + relArg + 2.0 * kRefExpErr;
-          const double rho = relA + ES / S + relNp + (double)(K + 8) * u53;
+          // (1/S as a correctly rounded reciprocal: one more rounding per ratio, in the (K + 10) u53)
+          const double invS = __drcp_rn(S);
+          const double rho = relA + ES * invS + relNp + (double)(K + 10) * u53;
           // inclusive csum of the masses in that order
           double c0 = e2[0];
 #pragma unroll
@@ -567,8 +569,8 @@ __global__ void __launch_bounds__(WG_THREADS, 1) wide_kernel(StageArgs a) {
           // on csum of p = e / S_np), all n when top_p == 1 or when it is never reached
           int kstar = n;
           if (tv.topp < 1.0) {
-            const unsigned h0 = __ballot_sync(0xffffffffu, lane < n && c0 / S >= tv.topp);
-            const unsigned h1 = __ballot_sync(0xffffffffu, lane + 32 < n && c1 / S >= tv.topp);
+            const unsigned h0 = __ballot_sync(0xffffffffu, lane < n && c0 * invS >= tv.topp);
+            const unsigned h1 = __ballot_sync(0xffffffffu, lane + 32 < n && c1 * invS >= tv.topp);
             kstar = h0 ? __ffs(h0) : (h1 ? 32 + __ffs(h1) : n);
             // certify both neighbours of the cut
             auto csum_at = [&](int i) -> double {  // inclusive csum at sorted index i
@@ -577,9 +579,9 @@ __global__ void __launch_bounds__(WG_THREADS, 1) wide_kernel(StageArgs a) {
             };
             const double cK = csum_at(min(kstar, n) - 1);
             const double cP = kstar >= 2 ? csum_at(kstar - 2) : 0.0;
-            if (kstar < n || (h0 | h1)) unc |= !(cK / S * (1.0 - rho) >= tv.topp);
-            else unc |= !(cK / S * (1.0 + rho) < tv.topp);  // never reached: all n kept
-            if (kstar >= 2) unc |= !(cP / S * (1.0 + rho) < tv.topp);
+            if (kstar < n || (h0 | h1)) unc |= !(cK * invS * (1.0 - rho) >= tv.topp);
+            else unc |= !(cK * invS * (1.0 + rho) < tv.topp);  // never reached: all n kept
+            if (kstar >= 2) unc |= !(cP * invS * (1.0 + rho) < tv.topp);
           }
           // kept set in id order: ranks by counting
           if (!unc) {
