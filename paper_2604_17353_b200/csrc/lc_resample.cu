@@ -1696,7 +1696,7 @@ rowwarp_kernel(const char* __restrict__ rows, int64_t row_bytes, int Vdef, const
     if (tv.T == 0.0) {
       phase_a_pos<DT>(tv.row, V, vec, lane, tmax, tmin, tpos);
     } else {
-      Ld = 1.4426950408889634 / tv.T;
+      Ld = tv.Ld;  // log2(e) / T, divided once per task when it was resolved
       Lhi = (float)Ld;
       Llo = (float)(Ld - (double)Lhi);
       fo = tv.trunc ? rw_fused_pass<DT, false>(tv.row, V, nseg, vec, lane, Lhi, Llo, Ld, sw)
@@ -1740,8 +1740,9 @@ rowwarp_kernel(const char* __restrict__ rows, int64_t row_bytes, int Vdef, const
     ec.Llo = Llo;
     ec.L16 = 16.0 * Ld;
     const double zabs = fmax(fabs((double)m), isfinite(zmin) ? fabs((double)zmin) : fabs((double)m));
-    const bool sane = ec.Lhi < 1e20f && ec.Lhi > 1e-20f && fabsf(m) * ec.Lhi < 1e30f && zabs / tv.T < 1e15;
-    const double relArg = 4.440892098500626e-16 * 2.0 * zabs / tv.T;
+    const double zT = zabs / tv.T;
+    const bool sane = ec.Lhi < 1e20f && ec.Lhi > 1e-20f && fabsf(m) * ec.Lhi < 1e30f && zT < 1e15;
+    const double relArg = 4.440892098500626e-16 * 2.0 * zT;
     const double relRef = (double)(2 * V + 64) * kEps64;
     const bool accurate = !tv.trunc;  // untruncated: the draw itself needs tight per-element errors
     // relative bound of the fp64-lite e's (kept lists, PRECISE pass) vs the reference's e's
