@@ -375,8 +375,91 @@ def run_ours(args, cfg, rank, world, dev):
         "gpu_launches": 8 * args.steps,
         "clocks": clk.summary(),
     }
+    if not args.no_check and args.policy == "step_wise":
+        res["check"] = run_check(args, cfg, w, rank, world, dev)
     if not args.no_cpu_baseline:
         res["cpu_baseline"] = cpu_baseline(cfg, seconds=args.cpu_seconds)
+    return res
+
+
+# ------------------------------------------------------------------------ check leg (untimed)
+
+
+def _pool_map(fn, jobs, cores):
+    import multiprocessing as mp
+
+    if cores <= 1 or len(jobs) <= 1:
+        return [fn(j) for j in jobs]
+    with mp.get_context("spawn").Pool(min(cores, len(jobs))) as pool:
+        return pool.map(fn, jobs)
+
+
+def run_check(args, cfg, w, rank, world, dev):
+    """Validate whole steps against the oracle (oracle/bulk.py) on the host cores, after the
+    timed region: S extra step-wise replay steps with fresh seed families, every token and every
+    task's kept-set size recomputed by the oracle from the same rows and uniforms, the replay
+    acceptance (replayed_len) recomputed from those tokens and the cached tokens, and (bf16
+    slabs) one step cross-checked bit-for-bit against the non-staged kernels (LCB_NO_STAGE=1)."""
+    import torch
+
+    import paper_2604_17353_b200 as lcb
+    from oracle import bulk
+    from paper_2604_17353_b200.mixing import mix2
+
+    t_start = time.perf_counter()
+    cache = w["cache"]
+    V, n_req, nb, R = cfg["V"], cfg["n_req"], cfg["nb"], cfg["R"]
+    n_rows = n_req * R
+    target = args.check_draws if args.check_draws is not None else (10_000_000 if V <= 32000 else 100_000)
+    S = max(1, -(-target // (n_rows * nb)))
+    toks, reps, seeds_all = [], [], []
+    kept = torch.zeros(n_rows, dtype=torch.int32, device=dev)
+    for s in range(S):
+        seeds_h = [mix2(1 + s, (rank << 32) + b) for b in range(n_req * nb)]
+        seeds = lcb._dev.u64_tensor(seeds_h, dev)
+        tok, rep, div, slot, ln = cache.replay_stepwise(w["digests"], R, nb, seeds, w["T"], w["K"], w["P"],
+                                                        bufs=w["bufs"], kept=kept if s == 0 else None)
+        toks.append(tok.cpu().numpy().reshape(n_req, R, nb))
+        reps.append(rep.cpu().numpy().reshape(n_req, nb))
+        seeds_all.append(np.array(seeds_h, dtype=np.uint64).reshape(n_req, nb))
+    kept_h = kept.cpu().numpy()
+    cached = w["bufs"]["cached"].cpu().numpy()[: n_rows].reshape(n_req, R)
+    # replay acceptance from the tokens (engine.py:301-310): first t with tok != cached, + 1
+    acc_bad = 0
+    for s in range(S):
+        diff = toks[s] != cached[:, :, None]
+        first = np.where(diff.any(1), diff.argmax(1) + 1, R)
+        acc_bad += int((first != reps[s]).sum())
+    # cross-check one step against the non-staged kernels, bit for bit
+    cross = None
+    if cfg["dtype"] == "bfloat16":
+        os.environ["LCB_NO_STAGE"] = "1"
+        try:
+            seeds = lcb._dev.u64_tensor([mix2(1, (rank << 32) + b) for b in range(n_req * nb)], dev)
+            k2 = torch.zeros(n_rows, dtype=torch.int32, device=dev)
+            tok2 = cache.replay_stepwise(w["digests"], R, nb, seeds, w["T"], w["K"], w["P"], kept=k2)[0]
+            t2 = tok2.cpu().numpy().reshape(n_req, R, nb)
+            cross = {"path": "LCB_NO_STAGE=1 (row-warp / CTA kernels)", "draws": int(t2.size),
+                     "token_mismatches": int((t2 != toks[0]).sum()),
+                     "kept_mismatches": int((k2.cpu().numpy() != kept_h).sum())}
+        finally:
+            del os.environ["LCB_NO_STAGE"]
+    cores = max(1, (os.cpu_count() or 1) // max(world, 1))
+    states = np.array([mix2(7, (rank << 40) + i) for i in range(n_rows)], dtype=np.uint64)  # row r*R+t
+    tok_rows = np.stack(toks, 2).reshape(n_rows, S * nb)  # [r, t] x [s, b]
+    seed_rows = np.repeat(np.stack(seeds_all, 1).reshape(n_req, S * nb), R, axis=0)
+    index = np.tile(np.arange(R), n_req)
+    n_jobs = max(cores * 4, 1)
+    bounds = np.linspace(0, n_rows, n_jobs + 1).astype(int)
+    jobs = [dict(V=V, T=cfg["T"], k=cfg["k"] or None, p=cfg["p"], bf16=cfg["dtype"] == "bfloat16", conc=2.5,
+                 states=states[a:b], seeds=seed_rows[a:b], index=index[a:b], tokens=tok_rows[a:b],
+                 kept=kept_h[a:b], row_ids=np.arange(a, b))
+            for a, b in zip(bounds[:-1], bounds[1:]) if b > a]
+    res = bulk.merge(_pool_map(bulk.check_rows, jobs, cores))
+    res.update({"steps": S, "seed_families": S, "acceptance_mismatches": acc_bad, "cores": cores,
+                "seconds": round(time.perf_counter() - t_start, 1), "cross_check": cross,
+                "oracle": "oracle/bulk.py: sample(truncate(softmax(z,T),k,p)) per row (sampling.py:57-109), "
+                          "rows from the reference producer, u = RngStream(seed) at draw number = position"})
     return res
 
 
@@ -786,7 +869,10 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--no-check", action="store_true", help="c4: skip the oracle replay of the op trace")
+    ap.add_argument("--no-check", action="store_true",
+                    help="skip the untimed oracle validation leg (c4: the op-trace replay)")
+    ap.add_argument("--check-draws", type=int, default=None,
+                    help="draws the check leg validates (default 10M at V=32000, 100K for the wide configs)")
     ap.add_argument("--policy", default="step_wise", choices=["step_wise", "hotspot"],
                     help="replay policy of the resample step (ReplayPolicy)")
     ap.add_argument("--hit-ratio", type=float, default=None,

@@ -29,7 +29,7 @@
 extern "C" {
 #endif
 
-#define LC_ABI_VERSION 1
+#define LC_ABI_VERSION 2
 
 typedef enum lc_status {
   LC_OK = 0,
@@ -102,6 +102,10 @@ typedef struct lc_draws {
   const int64_t* d_index;
   int32_t* d_token; /* out */
   uint8_t* d_flags; /* out, LC_DRAW_* (may be NULL) */
+  int32_t* d_kept;  /* out, per TASK (may be NULL): |kept| of truncate() (sampling.py:71-94) --
+                     * the kept set is the first d_kept[t] ids of the row in (logit desc, id asc)
+                     * order, i.e. the reference's lexsort((ids, -p)) prefix; V for an untruncated
+                     * row, 1 for T == 0, -1 for a bad row (NaN / non-finite max)            */
 } lc_draws;
 
 /* Bytes of scratch the resample entry points need for n_tasks tasks. */
@@ -199,18 +203,20 @@ int lc_cache_insert(lc_cache* cache, const uint64_t* d_digests, const int32_t* d
 int lc_cache_pin(lc_cache* cache, const int32_t* d_slot, const uint32_t* d_gen, int64_t n, int32_t delta,
                  void* stream);
 
-/* Copy cached rows (slot, pos) out as out_dtype (entry.logits_seq[pos]). */
-int lc_cache_gather(lc_cache* cache, const int32_t* d_slot, const int32_t* d_pos, int64_t n, void* d_out,
-                    int32_t out_dtype, int64_t out_stride, void* stream);
-/* Cached tokens (entry.token_seq[pos]). */
-int lc_cache_tokens(lc_cache* cache, const int32_t* d_slot, const int32_t* d_pos, int64_t n, int32_t* d_out,
-                    void* stream);
+/* Copy cached rows (slot, pos) out as out_dtype (entry.logits_seq[pos]).  d_gen (may be
+ * NULL) holds each row's (slot, generation) handle generation: a row whose entry was
+ * overwritten or evicted since reads as zeros (tokens: -1), like a dead slot.      */
+int lc_cache_gather(lc_cache* cache, const int32_t* d_slot, const int32_t* d_pos, const uint32_t* d_gen, int64_t n,
+                    void* d_out, int32_t out_dtype, int64_t out_stride, void* stream);
+/* Cached tokens (entry.token_seq[pos]); -1 for a dead / stale row. */
+int lc_cache_tokens(lc_cache* cache, const int32_t* d_slot, const int32_t* d_pos, const uint32_t* d_gen, int64_t n,
+                    int32_t* d_out, void* stream);
 
 /* Hotspot scoring straight from the slab (sampling.py:112-125 on entry.logits_seq):
  * entropy H and max probability of softmax(z / T) for cached rows (slot, pos), fp64,
  * without gathering the rows; a missing row gives H = 0, max p = 1.             */
-int lc_cache_row_entropy(lc_cache* cache, const int32_t* d_slot, const int32_t* d_pos, int64_t n, double temperature,
-                         double* d_entropy, double* d_pmax, void* stream);
+int lc_cache_row_entropy(lc_cache* cache, const int32_t* d_slot, const int32_t* d_pos, const uint32_t* d_gen, int64_t n,
+                         double temperature, double* d_entropy, double* d_pmax, void* stream);
 
 /* Resample cached rows: tasks use (slot, pos) with row = -1. */
 int lc_cache_resample(lc_cache* cache, const lc_task* d_tasks, int64_t n_tasks, lc_draws draws, void* d_workspace,
@@ -223,8 +229,11 @@ int lc_cache_resample(lc_cache* cache, const lc_task* d_tasks, int64_t n_tasks, 
  * branches with draws [(r*max_pos + t)*n_branch, +n_branch), branch b using
  * seed d_seeds[r*n_branch + b] at draw number t (step-wise: one draw per
  * position, engine.py:301-310).  Positions past the limit get empty draw
- * ranges.  d_temperature/d_top_k/d_top_p are per request.                    */
-int lc_replay_tasks(const int32_t* d_slot, const int32_t* d_len, int64_t n_req, int32_t max_pos, int32_t n_branch,
+ * ranges.  d_temperature/d_top_k/d_top_p are per request; d_vocab (may be NULL =
+ * the slab width) is the entry's own row width from lc_cache_lookup, so an
+ * entry narrower than the slab is resampled over its own columns only.        */
+int lc_replay_tasks(const int32_t* d_slot, const int32_t* d_len, const int32_t* d_vocab, int64_t n_req,
+                    int32_t max_pos, int32_t n_branch,
                     const double* d_temperature, const int32_t* d_top_k, const double* d_top_p, lc_task* d_tasks,
                     void* stream);
 /* Step-wise acceptance: for request r, branch b, the replay keeps positions up
@@ -242,13 +251,15 @@ int lc_replay_accept(const int32_t* d_tokens, const int32_t* d_cached, const int
  * draws.  lc_replay_accept_hotspot: non-hotspot positions copy the cached
  * token (written into d_tokens, so d_tokens is the engine's `out` list); the
  * replay stops after the first hotspot whose sample differs from the cache.   */
-int lc_replay_tasks_hotspot(const int32_t* d_slot, const int32_t* d_len, const int32_t* d_draw_index, int64_t n_req,
+int lc_replay_tasks_hotspot(const int32_t* d_slot, const int32_t* d_len, const int32_t* d_vocab,
+                            const int32_t* d_draw_index, int64_t n_req,
                             int32_t max_pos, int32_t n_branch, const double* d_temperature, const int32_t* d_top_k,
                             const double* d_top_p, lc_task* d_tasks, void* stream);
 /* The hotspot tasks for a compact list: d_hot_pos[j] = r * max_pos + t of the j-th
  * hotspot position, d_hot_draw[j] its draw number; writes n_hot tasks (draws at the
  * same indices as lc_replay_tasks_hotspot), so the resample skips non-hotspot rows.   */
-int lc_replay_tasks_hotspot_list(const int32_t* d_slot, const int32_t* d_len, const int64_t* d_hot_pos,
+int lc_replay_tasks_hotspot_list(const int32_t* d_slot, const int32_t* d_len, const int32_t* d_vocab,
+                                 const int64_t* d_hot_pos,
                                  const int32_t* d_hot_draw, int64_t n_hot, int32_t max_pos, int32_t n_branch,
                                  const double* d_temperature, const int32_t* d_top_k, const double* d_top_p,
                                  lc_task* d_tasks, void* stream);

@@ -76,6 +76,7 @@ class CacheOracle:
         self.hits = 0
         self.inserts = 0
         self.evictions = 0
+        self.capacity_errors = 0
 
     def __len__(self):
         return len(self.entries)
@@ -112,7 +113,15 @@ class CacheOracle:
             slot = self.free_slots.pop()
         npages = self._pages_for(n)
         if len(self.free_pages) < npages:
-            raise MemoryError("slab pages exhausted")
+            # out of slab pages (the reference has no slab): the insert is rolled back -- the
+            # key leaves the cache (an overwritten entry is already gone) and its slot returns
+            # to the free stack; the GPU latches LC_E_CAPACITY
+            if old is not None:
+                del self.entries[digest]
+                del self.by_slot[slot]
+            self.free_slots.append(slot)
+            self.capacity_errors += 1
+            return None, []
         pages = [self.free_pages.pop() for _ in range(npages)]
         self.clock += 1
         e = Entry(digest, slot, self.gen[slot], n, vocab, self.clock, pages, 0, list(tokens))

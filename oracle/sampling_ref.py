@@ -55,6 +55,67 @@ def kept_order(p: np.ndarray, top_k, top_p: float) -> np.ndarray | None:
     return order
 
 
+def kept_order_fast(p: np.ndarray, top_k, top_p: float, cand: int = 8192) -> np.ndarray | None:
+    """``kept_order`` without the full O(V log V) lexsort (for bulk checks; equal by
+    construction and pinned against ``kept_order`` in tests/test_oracle.py).
+
+    The kept set is a prefix of the (p desc, id asc) order.  Every id outside
+    C = {p >= theta} (theta = the m-th largest p) sorts after every id of C, so when
+    the prefix ends inside C's sorted order -- top-k with k <= |C|, or the csum over
+    C reaching top_p -- it is C's prefix: same ids, same order, and the sequential
+    csum over it is the same sequence of additions.  Otherwise fall back to the full sort."""
+    V = len(p)
+    if top_k is None and top_p == 1.0:
+        return None
+    k = top_k if (top_k is not None and top_k < V) else None
+    m = min(V, max(cand, k or 0))
+    if m < V:
+        theta = np.partition(p, V - m)[V - m]
+        ids = np.flatnonzero(p >= theta)
+        ids = ids[np.argsort(-p[ids], kind="stable")]  # (p desc, id asc): ids ascend into the sort
+        if k is not None:
+            ids = ids[:k]
+        if top_p < 1.0:
+            mass = np.cumsum(p[ids])
+            j = int(np.searchsorted(mass, top_p, side="left"))
+            if j < len(ids):
+                return ids[: j + 1]
+            if k is not None and len(ids) == k:
+                return ids  # the top-k survivors never reach top_p: all kept
+        elif k is not None:
+            return ids
+    return kept_order(p, top_k, top_p)
+
+
+def draw_many(q: np.ndarray, us) -> np.ndarray:
+    """``[draw(q, u) for u in us]`` with the total and cdf computed once (the same values
+    ``draw`` computes on every call: numpy's pairwise sum and sequential cumsum)."""
+    total = float(q.sum())
+    if total <= 0.0:
+        raise RuntimeError("sample() called with no probability mass")
+    cdf = np.cumsum(q)
+    idx = np.searchsorted(cdf, np.asarray(us, dtype=np.float64) * total, side="right")
+    idx = np.minimum(idx, len(q) - 1)
+    out = idx.copy()
+    nz = np.flatnonzero(q != 0.0)
+    # back off over zero-probability ids: the last nonzero id <= idx (id 0 if none)
+    pos = np.searchsorted(nz, idx, side="right") - 1
+    back = q[idx] == 0.0
+    out[back] = np.where(pos[back] >= 0, nz[np.maximum(pos[back], 0)], 0)
+    return out
+
+
+def truncate_fast(p: np.ndarray, top_k=None, top_p: float = 1.0) -> tuple[np.ndarray, int]:
+    """(truncate(p, top_k, top_p), len(kept_order) or V) via ``kept_order_fast``."""
+    order = kept_order_fast(p, top_k, top_p)
+    if order is None:
+        return p, len(p)
+    q = np.zeros(len(p), dtype=np.float64)
+    kept = p[order]
+    q[order] = kept / kept.sum()
+    return q, len(order)
+
+
 def truncate(p: np.ndarray, top_k=None, top_p: float = 1.0) -> np.ndarray:
     order = kept_order(p, top_k, top_p)
     if order is None:

@@ -41,6 +41,7 @@ class LcDraws(C.Structure):
         ("d_index", C.c_void_p),
         ("d_token", C.c_void_p),
         ("d_flags", C.c_void_p),
+        ("d_kept", C.c_void_p),
     ]
 
 
@@ -93,20 +94,20 @@ _SIGS = {
     "lc_cache_lookup": (C.c_int, [P, P, I64, P, P, P, P, P]),
     "lc_cache_insert": (C.c_int, [P, P, P, P, I64, P, I32, I64, P, P, I32, P, P, P]),
     "lc_cache_pin": (C.c_int, [P, P, P, I64, I32, P]),
-    "lc_cache_gather": (C.c_int, [P, P, P, I64, P, I32, I64, P]),
-    "lc_cache_row_entropy": (C.c_int, [P, P, P, I64, C.c_double, P, P, P]),
-    "lc_cache_tokens": (C.c_int, [P, P, P, I64, P, P]),
+    "lc_cache_gather": (C.c_int, [P, P, P, P, I64, P, I32, I64, P]),
+    "lc_cache_row_entropy": (C.c_int, [P, P, P, P, I64, C.c_double, P, P, P]),
+    "lc_cache_tokens": (C.c_int, [P, P, P, P, I64, P, P]),
     "lc_cache_resample": (C.c_int, [P, P, I64, LcDraws, P, I64, P, P]),
     "lc_cache_stats_get": (C.c_int, [P, C.POINTER(LcCacheStats), P]),
     "lc_cache_slab": (C.c_int, [P, C.POINTER(P), C.POINTER(I64), C.POINTER(I32)]),
     "lc_cache_page_table": (C.c_int, [P, C.POINTER(P), C.POINTER(I32), C.POINTER(I32)]),
     "lc_cache_snapshot": (C.c_int, [P, P, P, P, P, P, P, P, P]),
     "lc_probe_exp": (C.c_int, [P, I64, C.c_float, D, C.c_int, P, P]),
-    "lc_replay_tasks": (C.c_int, [P, P, I64, I32, I32, P, P, P, P, P]),
+    "lc_replay_tasks": (C.c_int, [P, P, P, I64, I32, I32, P, P, P, P, P]),
     "lc_replay_accept": (C.c_int, [P, P, P, I64, I32, I32, P, P, P]),
-    "lc_replay_tasks_hotspot": (C.c_int, [P, P, P, I64, I32, I32, P, P, P, P, P]),
+    "lc_replay_tasks_hotspot": (C.c_int, [P, P, P, P, I64, I32, I32, P, P, P, P, P]),
     "lc_replay_accept_hotspot": (C.c_int, [P, P, P, P, I64, I32, I32, P, P, P]),
-    "lc_replay_tasks_hotspot_list": (C.c_int, [P, P, P, P, I64, I32, I32, P, P, P, P, P]),
+    "lc_replay_tasks_hotspot_list": (C.c_int, [P, P, P, P, P, I64, I32, I32, P, P, P, P, P]),
 }
 
 
@@ -123,7 +124,7 @@ def _load():
         fn = getattr(lib, name)
         fn.restype = res
         fn.argtypes = args
-    if lib.lc_abi_version() != 1:
+    if lib.lc_abi_version() != 2:
         raise ImportError("liblcb200 ABI version mismatch")
     return lib
 

@@ -310,10 +310,17 @@ __global__ void insert_policy_scalar_kernel(CacheDev c, const uint64_t* __restri
       ctl->alive += 1;
     }
     if (ctl->free_page_top < np) {
+      // out of slab pages (possible when entries narrower than the slab make the accounted
+      // budget admit more rows than the slab holds): roll the insert back -- the key leaves
+      // the index (an overwritten entry is already gone, as in the reference), its slot goes
+      // back on the free stack -- and latch the error (oracle/cache_ref.py does the same)
       if (!ctl->error) ctl->error = LC_E_CAPACITY;
-      // keep the index consistent: an entry without rows cannot be replayed
+      table_delete(c, d);
+      c.free_slots[ctl->free_slot_top++] = s;
+      c.alive[s] = 0;
       c.nrows[s] = 0;
       c.nbytes[s] = 0;
+      ctl->alive -= 1;
       continue;
     }
     for (int k = 0; k < np; ++k) c.pages[(int64_t)s * c.maxp + k] = c.free_pages[--ctl->free_page_top];
@@ -825,11 +832,21 @@ __global__ void __launch_bounds__(32) insert_policy_kernel(CacheDev c, const uin
         g = (s == last_ev_slot) ? last_ev_gen : c.gen[s];
       }
       if (L.free_page_top < np) {
+        // out of slab pages: roll back as insert_policy_scalar_kernel does (key out of the
+        // index, slot back on the free stack, error latched)
         if (!L.error) L.error = LC_E_CAPACITY;
+        mark_slot(s);
+        window_delete(c, d, lane, sh_b, st_home, w.hb, w.bstale);
+        rs_push1(fs, c.free_slots, L.free_slot_top, s, lane);
+        L.free_slot_top += 1;
         if (lane == 0) {
+          c.alive[s] = 0;
           c.nrows[s] = 0;
           c.nbytes[s] = 0;
         }
+        last_ev_slot = s;
+        last_ev_gen = g;
+        L.alive -= 1;
         __syncwarp();
         continue;
       }
@@ -950,14 +967,20 @@ __global__ void pin_kernel(CacheDev c, const int32_t* __restrict__ slot, const u
   if (c.alive[s] && c.gen[s] == gen[i]) atomicAdd(&c.pins[s], delta);
 }
 
+// (slot, pos[, gen]) names a live row: a handle whose entry was overwritten or evicted
+// (generation moved on) reads nothing
+__device__ __forceinline__ bool row_live(const CacheDev& c, int s, int t, const uint32_t* gen, int64_t i) {
+  return s >= 0 && s < c.E && c.alive[s] && (!gen || c.gen[s] == gen[i]) && t >= 0 && t < c.nrows[s];
+}
+
 template <typename DstT>
-__global__ void gather_kernel(CacheDev c, const int32_t* __restrict__ slot, const int32_t* __restrict__ pos, int64_t n,
-                              DstT* out, int64_t out_stride) {
+__global__ void gather_kernel(CacheDev c, const int32_t* __restrict__ slot, const int32_t* __restrict__ pos,
+                              const uint32_t* __restrict__ gen, int64_t n, DstT* out, int64_t out_stride) {
   const int64_t i = blockIdx.x;
   if (i >= n) return;
   const int s = slot[i], t = pos[i];
   DstT* o = out + i * out_stride;
-  bool ok = s >= 0 && s < c.E && c.alive[s] && t >= 0 && t < c.nrows[s];
+  bool ok = row_live(c, s, t, gen, i);
   const int vv = ok ? c.vocab[s] : 0;
   const int64_t slab_row =
       ok ? (int64_t)c.pages[(int64_t)s * c.maxp + t / c.page_rows] * c.page_rows + t % c.page_rows : 0;
@@ -974,11 +997,11 @@ __global__ void gather_kernel(CacheDev c, const int32_t* __restrict__ slot, cons
 
 // slab address of cached row (slot, pos) -- null when the entry or position is gone
 __global__ void row_ptr_kernel(CacheDev c, const int32_t* __restrict__ slot, const int32_t* __restrict__ pos,
-                               int64_t n, const char** out, int32_t* vocab_out) {
+                               const uint32_t* __restrict__ gen, int64_t n, const char** out, int32_t* vocab_out) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
   const int s = slot[i], t = pos[i];
-  const bool ok = s >= 0 && s < c.E && c.alive[s] && t >= 0 && t < c.nrows[s];
+  const bool ok = row_live(c, s, t, gen, i);
   const size_t esz = c.dtype == LC_F32 ? 4 : 2;
   out[i] = ok ? c.slab + ((int64_t)c.pages[(int64_t)s * c.maxp + t / c.page_rows] * c.page_rows + t % c.page_rows) *
                              (int64_t)c.V * esz
@@ -986,12 +1009,12 @@ __global__ void row_ptr_kernel(CacheDev c, const int32_t* __restrict__ slot, con
   vocab_out[i] = ok ? c.vocab[s] : 1;
 }
 
-__global__ void tokens_kernel(CacheDev c, const int32_t* __restrict__ slot, const int32_t* __restrict__ pos, int64_t n,
-                              int32_t* out) {
+__global__ void tokens_kernel(CacheDev c, const int32_t* __restrict__ slot, const int32_t* __restrict__ pos,
+                              const uint32_t* __restrict__ gen, int64_t n, int32_t* out) {
   int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
   int s = slot[i], t = pos[i];
-  if (s < 0 || s >= c.E || !c.alive[s] || t < 0 || t >= c.nrows[s]) {
+  if (!row_live(c, s, t, gen, i)) {
     out[i] = -1;
     return;
   }
@@ -1212,7 +1235,8 @@ extern "C" int lc_cache_insert(lc_cache* c, const uint64_t* d_digests, const int
   cudaStream_t st = (cudaStream_t)stream;
   int rc = ensure_ring(c, n, st);
   if (rc) return rc;
-  static const bool scalar = getenv("LCB_SCALAR_POLICY") && atoi(getenv("LCB_SCALAR_POLICY")) != 0;
+  const char* sp = getenv("LCB_SCALAR_POLICY");  // A/B hook, read per call (tests switch it)
+  const bool scalar = sp && atoi(sp) != 0;
   if (scalar)
     insert_policy_scalar_kernel<<<1, 32, 0, st>>>(c->dev, d_digests, d_lengths, d_vocabs, n, d_slot, d_gen);
   else
@@ -1252,29 +1276,29 @@ extern "C" int lc_cache_pin(lc_cache* c, const int32_t* d_slot, const uint32_t* 
   return LC_OK;
 }
 
-extern "C" int lc_cache_gather(lc_cache* c, const int32_t* d_slot, const int32_t* d_pos, int64_t n, void* d_out,
-                               int32_t out_dtype, int64_t out_stride, void* stream) {
+extern "C" int lc_cache_gather(lc_cache* c, const int32_t* d_slot, const int32_t* d_pos, const uint32_t* d_gen,
+                               int64_t n, void* d_out, int32_t out_dtype, int64_t out_stride, void* stream) {
   if (!c || n < 0 || (n > 0 && (!d_slot || !d_pos || !d_out)) || out_stride < 1) return LC_E_ARG;
   if (n == 0) return LC_OK;
   cudaStream_t st = (cudaStream_t)stream;
   for (int64_t i0 = 0; i0 < n; i0 += (1 << 30)) {
     int64_t nn = n - i0 < (1 << 30) ? n - i0 : (1 << 30);
     if (out_dtype == LC_F32)
-      gather_kernel<float><<<(unsigned)nn, 256, 0, st>>>(c->dev, d_slot + i0, d_pos + i0, nn,
+      gather_kernel<float><<<(unsigned)nn, 256, 0, st>>>(c->dev, d_slot + i0, d_pos + i0, d_gen ? d_gen + i0 : nullptr, nn,
                                                          (float*)d_out + i0 * out_stride, out_stride);
     else
-      gather_kernel<uint16_t><<<(unsigned)nn, 256, 0, st>>>(c->dev, d_slot + i0, d_pos + i0, nn,
+      gather_kernel<uint16_t><<<(unsigned)nn, 256, 0, st>>>(c->dev, d_slot + i0, d_pos + i0, d_gen ? d_gen + i0 : nullptr, nn,
                                                             (uint16_t*)d_out + i0 * out_stride, out_stride);
     LCB_CUDA_TRY(cudaGetLastError());
   }
   return LC_OK;
 }
 
-extern "C" int lc_cache_tokens(lc_cache* c, const int32_t* d_slot, const int32_t* d_pos, int64_t n, int32_t* d_out,
-                               void* stream) {
+extern "C" int lc_cache_tokens(lc_cache* c, const int32_t* d_slot, const int32_t* d_pos, const uint32_t* d_gen,
+                               int64_t n, int32_t* d_out, void* stream) {
   if (!c || n < 0 || (n > 0 && (!d_slot || !d_pos || !d_out))) return LC_E_ARG;
   if (n == 0) return LC_OK;
-  tokens_kernel<<<ceil_div(n, 256), 256, 0, (cudaStream_t)stream>>>(c->dev, d_slot, d_pos, n, d_out);
+  tokens_kernel<<<ceil_div(n, 256), 256, 0, (cudaStream_t)stream>>>(c->dev, d_slot, d_pos, d_gen, n, d_out);
   LCB_CUDA_TRY(cudaGetLastError());
   return LC_OK;
 }
@@ -1284,8 +1308,8 @@ int launch_entropy_ptrs(const char* const* d_rows, const int32_t* d_vocab, int d
                         double* pmax, cudaStream_t st);
 }
 
-extern "C" int lc_cache_row_entropy(lc_cache* c, const int32_t* d_slot, const int32_t* d_pos, int64_t n,
-                                    double temperature, double* d_entropy, double* d_pmax, void* stream) {
+extern "C" int lc_cache_row_entropy(lc_cache* c, const int32_t* d_slot, const int32_t* d_pos, const uint32_t* d_gen,
+                                    int64_t n, double temperature, double* d_entropy, double* d_pmax, void* stream) {
   if (!c || n < 0 || !(temperature >= 0.0) || (n > 0 && (!d_slot || !d_pos || !d_entropy || !d_pmax)))
     return LC_E_ARG;
   if (n == 0) return LC_OK;
@@ -1294,7 +1318,7 @@ extern "C" int lc_cache_row_entropy(lc_cache* c, const int32_t* d_slot, const in
   LCB_CUDA_TRY(cudaMallocAsync(&scratch, (size_t)n * (sizeof(char*) + sizeof(int32_t)) + 16, st));
   const char** ptrs = reinterpret_cast<const char**>(scratch);
   int32_t* voc = reinterpret_cast<int32_t*>(ptrs + n);
-  row_ptr_kernel<<<ceil_div(n, 256), 256, 0, st>>>(c->dev, d_slot, d_pos, n, ptrs, voc);
+  row_ptr_kernel<<<ceil_div(n, 256), 256, 0, st>>>(c->dev, d_slot, d_pos, d_gen, n, ptrs, voc);
   int rc = LC_OK;
   if (cudaGetLastError() != cudaSuccess) rc = LC_E_CUDA;
   if (rc == LC_OK) rc = lcb::launch_entropy_ptrs(ptrs, voc, c->dev.dtype, n, temperature, d_entropy, d_pmax, st);

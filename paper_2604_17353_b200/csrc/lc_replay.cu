@@ -5,7 +5,8 @@
 
 namespace lcb {
 
-__global__ void replay_tasks_kernel(const int32_t* __restrict__ slot, const int32_t* __restrict__ len, int64_t n_req,
+__global__ void replay_tasks_kernel(const int32_t* __restrict__ slot, const int32_t* __restrict__ len,
+                                    const int32_t* __restrict__ vocab, int64_t n_req,
                                     int max_pos, int nb, const double* __restrict__ temp,
                                     const int32_t* __restrict__ topk, const double* __restrict__ topp,
                                     lc_task* __restrict__ tasks) {
@@ -21,7 +22,7 @@ __global__ void replay_tasks_kernel(const int32_t* __restrict__ slot, const int3
   tk.pos = t;
   tk.temperature = temp[r];
   tk.top_k = topk[r];
-  tk.vocab = 0;
+  tk.vocab = (vocab && s >= 0) ? vocab[r] : 0;  // the entry's own width (may be < the slab's)
   tk.top_p = topp[r];
   tk.draw_begin = i * nb;
   tk.draw_end = t < lim ? i * nb + nb : i * nb;
@@ -57,7 +58,7 @@ __global__ void replay_accept_kernel(const int32_t* __restrict__ tok, const int3
 // draw number at position t is the count of hotspots before t (d_draw_index,
 // -1 = not a hotspot); every other position copies the cached token.
 __global__ void replay_tasks_hot_kernel(const int32_t* __restrict__ slot, const int32_t* __restrict__ len,
-                                        const int32_t* __restrict__ draw_index, int64_t n_req, int max_pos, int nb,
+                                        const int32_t* __restrict__ vocab, const int32_t* __restrict__ draw_index, int64_t n_req, int max_pos, int nb,
                                         const double* __restrict__ temp, const int32_t* __restrict__ topk,
                                         const double* __restrict__ topp, lc_task* __restrict__ tasks) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -73,7 +74,7 @@ __global__ void replay_tasks_hot_kernel(const int32_t* __restrict__ slot, const 
   tk.pos = t;
   tk.temperature = temp[r];
   tk.top_k = topk[r];
-  tk.vocab = 0;
+  tk.vocab = (vocab && s >= 0) ? vocab[r] : 0;  // the entry's own width (may be < the slab's)
   tk.top_p = topp[r];
   tk.draw_begin = i * nb;
   tk.draw_end = (t < lim && di >= 0) ? i * nb + nb : i * nb;
@@ -85,7 +86,7 @@ __global__ void replay_tasks_hot_kernel(const int32_t* __restrict__ slot, const 
 // The same tasks for a compact list of hotspot positions only (flat index r * max_pos + t
 // and its draw number): the resample sees n_hot tasks instead of n_req * max_pos.
 __global__ void replay_tasks_hot_list_kernel(const int32_t* __restrict__ slot, const int32_t* __restrict__ len,
-                                             const int64_t* __restrict__ hot_pos, const int32_t* __restrict__ hot_di,
+                                             const int32_t* __restrict__ vocab, const int64_t* __restrict__ hot_pos, const int32_t* __restrict__ hot_di,
                                              int64_t n_hot, int max_pos, int nb, const double* __restrict__ temp,
                                              const int32_t* __restrict__ topk, const double* __restrict__ topp,
                                              lc_task* __restrict__ tasks) {
@@ -102,7 +103,7 @@ __global__ void replay_tasks_hot_list_kernel(const int32_t* __restrict__ slot, c
   tk.pos = t;
   tk.temperature = temp[r];
   tk.top_k = topk[r];
-  tk.vocab = 0;
+  tk.vocab = (vocab && s >= 0) ? vocab[r] : 0;  // the entry's own width (may be < the slab's)
   tk.top_p = topp[r];
   tk.draw_begin = i * nb;
   tk.draw_end = t < lim ? i * nb + nb : i * nb;
@@ -142,7 +143,8 @@ __global__ void replay_accept_hot_kernel(int32_t* __restrict__ tok, const int32_
 
 }  // namespace lcb
 
-extern "C" int lc_replay_tasks_hotspot(const int32_t* d_slot, const int32_t* d_len, const int32_t* d_draw_index,
+extern "C" int lc_replay_tasks_hotspot(const int32_t* d_slot, const int32_t* d_len, const int32_t* d_vocab,
+                                       const int32_t* d_draw_index,
                                        int64_t n_req, int32_t max_pos, int32_t n_branch,
                                        const double* d_temperature, const int32_t* d_top_k, const double* d_top_p,
                                        lc_task* d_tasks, void* stream) {
@@ -151,12 +153,13 @@ extern "C" int lc_replay_tasks_hotspot(const int32_t* d_slot, const int32_t* d_l
   if (n == 0) return LC_OK;
   if (!d_slot || !d_len || !d_draw_index || !d_temperature || !d_top_k || !d_top_p || !d_tasks) return LC_E_ARG;
   lcb::replay_tasks_hot_kernel<<<lcb::ceil_div(n, 256), 256, 0, (cudaStream_t)stream>>>(
-      d_slot, d_len, d_draw_index, n_req, max_pos, n_branch, d_temperature, d_top_k, d_top_p, d_tasks);
+      d_slot, d_len, d_vocab, d_draw_index, n_req, max_pos, n_branch, d_temperature, d_top_k, d_top_p, d_tasks);
   LCB_CUDA_TRY(cudaGetLastError());
   return LC_OK;
 }
 
-extern "C" int lc_replay_tasks_hotspot_list(const int32_t* d_slot, const int32_t* d_len, const int64_t* d_hot_pos,
+extern "C" int lc_replay_tasks_hotspot_list(const int32_t* d_slot, const int32_t* d_len, const int32_t* d_vocab,
+                                            const int64_t* d_hot_pos,
                                             const int32_t* d_hot_draw, int64_t n_hot, int32_t max_pos,
                                             int32_t n_branch, const double* d_temperature, const int32_t* d_top_k,
                                             const double* d_top_p, lc_task* d_tasks, void* stream) {
@@ -165,7 +168,7 @@ extern "C" int lc_replay_tasks_hotspot_list(const int32_t* d_slot, const int32_t
   if (!d_slot || !d_len || !d_hot_pos || !d_hot_draw || !d_temperature || !d_top_k || !d_top_p || !d_tasks)
     return LC_E_ARG;
   lcb::replay_tasks_hot_list_kernel<<<lcb::ceil_div(n_hot, 256), 256, 0, (cudaStream_t)stream>>>(
-      d_slot, d_len, d_hot_pos, d_hot_draw, n_hot, max_pos, n_branch, d_temperature, d_top_k, d_top_p, d_tasks);
+      d_slot, d_len, d_vocab, d_hot_pos, d_hot_draw, n_hot, max_pos, n_branch, d_temperature, d_top_k, d_top_p, d_tasks);
   LCB_CUDA_TRY(cudaGetLastError());
   return LC_OK;
 }
@@ -183,7 +186,8 @@ extern "C" int lc_replay_accept_hotspot(int32_t* d_tokens, const int32_t* d_cach
   return LC_OK;
 }
 
-extern "C" int lc_replay_tasks(const int32_t* d_slot, const int32_t* d_len, int64_t n_req, int32_t max_pos,
+extern "C" int lc_replay_tasks(const int32_t* d_slot, const int32_t* d_len, const int32_t* d_vocab, int64_t n_req,
+                               int32_t max_pos,
                                int32_t n_branch, const double* d_temperature, const int32_t* d_top_k,
                                const double* d_top_p, lc_task* d_tasks, void* stream) {
   if (n_req < 0 || max_pos < 0 || n_branch < 0) return LC_E_ARG;
@@ -191,7 +195,7 @@ extern "C" int lc_replay_tasks(const int32_t* d_slot, const int32_t* d_len, int6
   if (n == 0) return LC_OK;
   if (!d_slot || !d_len || !d_temperature || !d_top_k || !d_top_p || !d_tasks) return LC_E_ARG;
   lcb::replay_tasks_kernel<<<lcb::ceil_div(n, 256), 256, 0, (cudaStream_t)stream>>>(
-      d_slot, d_len, n_req, max_pos, n_branch, d_temperature, d_top_k, d_top_p, d_tasks);
+      d_slot, d_len, d_vocab, n_req, max_pos, n_branch, d_temperature, d_top_k, d_top_p, d_tasks);
   LCB_CUDA_TRY(cudaGetLastError());
   return LC_OK;
 }

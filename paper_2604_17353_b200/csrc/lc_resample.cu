@@ -403,7 +403,10 @@ resample_kernel(const char* __restrict__ rows, int64_t row_bytes, int Vdef, cons
     __syncthreads();  // previous task's smem readers are done
     if (!resolve_task(tk, rows, row_bytes, Vdef, cm, tv)) {
       write_all(tv, io, -1, LC_DRAW_BAD_ROW);
-      if (tid == 0) atomicAdd(&counters[2], 1ull);
+      if (tid == 0) {
+        atomicAdd(&counters[2], 1ull);
+        set_kept(io, task_id, -1);
+      }
       continue;
     }
     if (force == 2) {  // test hook: everything to the EXACT tier
@@ -445,7 +448,10 @@ resample_kernel(const char* __restrict__ rows, int64_t row_bytes, int Vdef, cons
     const uint8_t base_flag = 0;
     if (sm.isc[1] || !(m > -INFINITY) || !(m < INFINITY)) {
       write_all(tv, io, -1, LC_DRAW_BAD_ROW);
-      if (tid == 0) atomicAdd(&counters[2], 1ull);
+      if (tid == 0) {
+        atomicAdd(&counters[2], 1ull);
+        set_kept(io, task_id, -1);
+      }
       continue;
     }
     // first argmax (lowest id with z == m), computed lazily: greedy rows need it now
@@ -467,6 +473,7 @@ resample_kernel(const char* __restrict__ rows, int64_t row_bytes, int Vdef, cons
     if (tv.T == 0.0) {  // greedy: one-hot at the first argmax, still one draw (sampling.py:61-64)
       const int amax = first_argmax();
       write_all(tv, io, amax, base_flag);
+      if (tid == 0) set_kept(io, task_id, greedy_kept(V, tv.topk, tv.topp));
       continue;
     }
     ExpCtx ec;
@@ -634,6 +641,7 @@ resample_kernel(const char* __restrict__ rows, int64_t row_bytes, int Vdef, cons
         if (pmax_lo > tv.topp) {
           if (amax == INT_MAX) amax = first_argmax();
           write_all(tv, io, amax, tier_flag);
+          if (tid == 0) set_kept(io, task_id, 1);
           done = true;
           break;
         }
@@ -929,6 +937,7 @@ resample_kernel(const char* __restrict__ rows, int64_t row_bytes, int Vdef, cons
         need = __syncthreads_or(need);
         if (!need) {
           done = true;
+          if (tid == 0) set_kept(io, task_id, L);  // the first L of the (z desc, id asc) order
         } else if (tid == 0 && !precise) {
           atomicAdd(&counters[5], 1ull);
         }
@@ -991,6 +1000,11 @@ resample_kernel(const char* __restrict__ rows, int64_t row_bytes, int Vdef, cons
           if (tid == 0) atomicAdd(&counters[7], 1ull);
           break;
         }
+      }
+      int Kc = V;  // mode 0 (untruncated or top_p == 1 without an effective top-k): identity
+      if (mode == 2) {
+        Kc = 0;  // warp-range lists above the bracket + the kept bracket members
+        for (int w = 0; w < RS_WARPS; ++w) Kc += sm.wcount[w];
       }
       if (tid == 0) {
         double c = 0.0;
@@ -1141,6 +1155,7 @@ resample_kernel(const char* __restrict__ rows, int64_t row_bytes, int Vdef, cons
       need = __syncthreads_or(need);
       if (!need) {
         done = true;
+        if (tid == 0) set_kept(io, task_id, Kc);
       } else if (tid == 0 && !precise) {
         atomicAdd(&counters[5], 1ull);
       }
@@ -1667,7 +1682,10 @@ rowwarp_kernel(const char* __restrict__ rows, int64_t row_bytes, int Vdef, const
         io.token[d] = -1;
         if (io.flags) io.flags[d] = LC_DRAW_BAD_ROW;
       }
-      if (lane == 0) atomicAdd(&counters[2], 1ull);
+      if (lane == 0) {
+        atomicAdd(&counters[2], 1ull);
+        set_kept(io, task_id, -1);
+      }
       continue;
     }
     if (force == 2) {  // test hook: everything to the EXACT tier
@@ -1711,7 +1729,10 @@ rowwarp_kernel(const char* __restrict__ rows, int64_t row_bytes, int Vdef, const
     const float zmin = -warp_max(-tmin);
     if (bad || !(m > -INFINITY) || !(m < INFINITY)) {
       write_all_w(-1, LC_DRAW_BAD_ROW);
-      if (lane == 0) atomicAdd(&counters[2], 1ull);
+      if (lane == 0) {
+        atomicAdd(&counters[2], 1ull);
+        set_kept(io, task_id, -1);
+      }
       continue;
     }
     // first argmax: lanes holding m reload the first vector that held their maximum
@@ -1729,6 +1750,7 @@ rowwarp_kernel(const char* __restrict__ rows, int64_t row_bytes, int Vdef, const
     if (tv.T == 0.0) {
       const int a = first_argmax();
       write_all_w(a, 0);
+      if (lane == 0) set_kept(io, task_id, greedy_kept(V, tv.topk, tv.topp));
       continue;
     }
     ExpCtx ec;
@@ -1782,6 +1804,7 @@ rowwarp_kernel(const char* __restrict__ rows, int64_t row_bytes, int Vdef, const
         const double pmax_lo = (1.0 / (S + E_S)) * (1.0 - relRef);
         if (pmax_lo > tv.topp) {  // nucleus = {first argmax}
           write_all_w(first_argmax(), tier_flag);
+          if (lane == 0) set_kept(io, task_id, 1);
           done = true;
           break;
         }
@@ -2119,6 +2142,9 @@ rowwarp_kernel(const char* __restrict__ rows, int64_t row_bytes, int Vdef, const
       need = __any_sync(0xffffffffu, need);
       if (!need) {
         done = true;
+        // big nucleus: the list entries above the bracket + bracket members 0..cut (sorted);
+        // otherwise untruncated (identity)
+        if (lane == 0) set_kept(io, task_id, big ? (nl - nb) + cut + 1 : V);
       } else if (lane == 0 && !precise) {
         atomicAdd(&counters[5], 1ull);
       }
@@ -2197,6 +2223,7 @@ exact_kernel(const char* __restrict__ rows, int64_t row_bytes, int Vdef, const l
         io.token[d] = s_L;
         if (io.flags) io.flags[d] = LC_DRAW_PRECISE;
       }
+      if (tid == 0) set_kept(io, task_id, greedy_kept(V, tv.topk, tv.topp));
       __syncthreads();
       continue;
     }
@@ -2373,6 +2400,7 @@ exact_kernel(const char* __restrict__ rows, int64_t row_bytes, int Vdef, const l
         }
       }
       L = n;
+      if (tid == 0) set_kept(io, task_id, L);  // the reference's kept prefix, (p desc, id asc)
       __syncthreads();
       for (int i = tid; i < L; i += EX_THREADS) tmp[i] = p[ord[i]];
       for (int i = tid; i < V; i += EX_THREADS) q[i] = 0.0;
@@ -2381,6 +2409,7 @@ exact_kernel(const char* __restrict__ rows, int64_t row_bytes, int Vdef, const l
       for (int i = tid; i < L; i += EX_THREADS) q[ord[i]] = __ddiv_rn(tmp[i], ks);
     } else {
       for (int i = tid; i < V; i += EX_THREADS) q[i] = p[i];
+      if (tid == 0) set_kept(io, task_id, V);
     }
     __syncthreads();
     const double Q = pairwise_block(q, V, s_lv, s_ls, kLeafCap, &s_bc, &s_nl);  // total = q.sum()
@@ -2617,7 +2646,7 @@ int resample_launch(const void* rows, int dtype, int64_t vocab, int64_t row_stri
   if (n_tasks < 0 || vocab < 1 || vocab > (1 << 28) || !draws.d_token) return LC_E_ARG;
   if (!draws.d_u && !draws.d_seed) return LC_E_ARG;
   if (n_tasks == 0) return LC_OK;
-  DrawIO io{draws.d_u, draws.d_seed, draws.d_index, draws.d_token, draws.d_flags};
+  DrawIO io{draws.d_u, draws.d_seed, draws.d_index, draws.d_token, draws.d_flags, draws.d_kept};
   CacheMap cm{pages, max_pages, page_rows};
   const int64_t esz = dtype == LC_BF16 ? 2 : 4;
   if (dtype == LC_BF16)

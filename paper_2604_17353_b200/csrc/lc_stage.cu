@@ -79,7 +79,7 @@ struct __align__(128) SgSmem {
   double fq_u[SG_FQ][SG_NU];
   int fq_tail;  // slots published (producer)
   int fq_head;  // slots claimed (groups)
-  int fq_done;  // slots consumed (groups)
+  int fq_free[SG_FQ];  // per slot: the sequence number it may next be written for
   // producer batch
   TaskView pbv[SG_PB];
   int pbt[SG_PB];
@@ -145,8 +145,10 @@ __device__ void sg_producer(const StageArgs& a, SgSmem& sm, int lane) {
     const int npush = nb > 0 ? nb : (done ? SG_GROUPS - sentinels : 0);
     for (int j = 0; j < npush; ++j) {
       const int slot_seq = vload(&sm.fq_tail);
-      if (lane == 0)  // wait for a free slot
-        while (slot_seq - vload(&sm.fq_done) >= SG_FQ) __nanosleep(64);
+      // wait until the slot's previous occupant (sequence slot_seq - SG_FQ) was copied out by
+      // its own consumer: consumers finish out of order, so a completion count is not enough
+      if (lane == 0)
+        while (vload(&sm.fq_free[slot_seq % SG_FQ]) != slot_seq) __nanosleep(64);
       __syncwarp();
       const int slot = slot_seq % SG_FQ;
       if (nb > 0) {
@@ -186,7 +188,7 @@ __device__ void sg_pop(SgSmem& sm, SgGroup& G, int g, int lane) {
     G.task = t;
     if (t >= 0) G.tv = sm.fq_tv[slot];
     __threadfence_block();
-    atomicAdd(&sm.fq_done, 1);
+    *reinterpret_cast<volatile int*>(&sm.fq_free[slot]) = h + SG_FQ;  // slot h released
     if (t >= 0) {
       mbar_expect_tx(&sm.full[g], (uint32_t)(G.tv.V * 2));  // release: G.task/tv/su visible
       bulk_load(sm.ring[g], G.tv.row, (uint32_t)(G.tv.V * 2), &sm.full[g]);
@@ -204,7 +206,8 @@ __global__ void __launch_bounds__(SG_THREADS, 1) stage_kernel(StageArgs a) {
   if (tid == 0) {
     for (int s = 0; s < SG_GROUPS; ++s) mbar_init(&sm.full[s], 1);
     mbar_fence_init();
-    sm.fq_tail = sm.fq_head = sm.fq_done = 0;
+    sm.fq_tail = sm.fq_head = 0;
+    for (int s = 0; s < SG_FQ; ++s) sm.fq_free[s] = s;
   }
   if (tid < 16) sm.t16[tid] = exp2((double)tid / 16.0);
   if (tid < 32 * SG_GROUPS) sm.g[tid >> 5].ev[SG_NB + (tid & 31)] = 0.0;
@@ -321,6 +324,7 @@ __global__ void __launch_bounds__(SG_THREADS, 1) stage_kernel(StageArgs a) {
       requeue_task = true;  // the CTA kernel flags the row (LC_DRAW_BAD_ROW) and counts it
     } else if (tv.T == 0.0) {
       write_tok(first_argmax());
+      if (gt == 0) set_kept(io, task_id, greedy_kept(V, tv.topk, tv.topp));
     } else {
       // ---------------------------------------------- B: FAST exit test (packed bf16x2)
       const double Ld = tv.Ld;  // = kLog2e / tv.T, divided once by the producer
@@ -376,6 +380,7 @@ __global__ void __launch_bounds__(SG_THREADS, 1) stage_kernel(StageArgs a) {
       ST_PH(2);
       if (fast) {
         write_tok(amax);
+        if (gt == 0) set_kept(io, task_id, 1);
         ST_PH(3);
       } else {
         if (prof) ph[10]++;
@@ -801,6 +806,12 @@ __global__ void __launch_bounds__(SG_THREADS, 1) stage_kernel(StageArgs a) {
             if (G.uncertain) {
               requeue_task = true;
               if (gt == 0) atomicAdd(&a.counters[5], 1ull);
+            } else if (io.kept && gw == 0) {
+              // |kept| = every class above the cut class + its first js ties in id order
+              int kc = 0;
+              for (int b = lane; b < (int)bs; b += 32) kc += (int)G.hist[b];
+              kc = warp_sum(kc);
+              if (lane == 0) io.kept[task_id] = kc + js;
             }
           }
         }

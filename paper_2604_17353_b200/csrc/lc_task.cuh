@@ -118,7 +118,18 @@ struct DrawIO {
   const int64_t* index;
   int32_t* token;
   uint8_t* flags;
+  int32_t* kept;  // per task |kept| (lc_draws.d_kept), may be null
 };
+
+// the kept-set size of task t (first K ids in (z desc, id asc) order), when requested
+__device__ __forceinline__ void set_kept(const DrawIO& io, int t, int K) {
+  if (io.kept) io.kept[t] = K;
+}
+// |kept_order| of the one-hot softmax at T == 0 (sampling.py:61-64 then :71-94): the argmax
+// alone under a nucleus, else the top-k prefix (argmax + zero-probability ids), else identity
+__device__ __forceinline__ int greedy_kept(int V, int topk, double topp) {
+  return topp < 1.0 ? 1 : (topk > 0 ? topk : V);
+}
 
 struct Workspace {
   int* q_exact;   // [0] = count, [1..] task ids

@@ -64,7 +64,8 @@ struct __align__(128) WgSmem {
   TaskView fq_tv[WG_FQ];
   int fq_task[WG_FQ];
   double fq_u[WG_FQ][WG_NU];
-  int fq_tail, fq_head, fq_done;
+  int fq_tail, fq_head;
+  int fq_free[WG_FQ];  // per slot: the sequence number it may next be written for
   TaskView pbv[WG_PB];
   int pbt[WG_PB];
   double pbu[WG_PB][WG_NU];
@@ -126,8 +127,10 @@ __device__ void wg_producer(const StageArgs& a, WgSmem& sm, int lane) {
     const int npush = nb > 0 ? nb : (done ? WG_GROUPS - sentinels : 0);
     for (int j = 0; j < npush; ++j) {
       const int slot_seq = vload(&sm.fq_tail);
+      // wait until the slot's previous occupant (sequence slot_seq - WG_FQ) was copied out by
+      // its own consumer: consumers finish out of order, so a completion count is not enough
       if (lane == 0)
-        while (slot_seq - vload(&sm.fq_done) >= WG_FQ) __nanosleep(64);
+        while (vload(&sm.fq_free[slot_seq % WG_FQ]) != slot_seq) __nanosleep(64);
       __syncwarp();
       const int slot = slot_seq % WG_FQ;
       if (nb > 0) {
@@ -170,7 +173,7 @@ __device__ void wg_pop(WgSmem& sm, WgGroup& G, int lane) {
     G.thr = -INFINITY;
     G.thrk = 0ull;
     __threadfence_block();
-    atomicAdd(&sm.fq_done, 1);
+    *reinterpret_cast<volatile int*>(&sm.fq_free[slot]) = h + WG_FQ;  // slot h released
   }
   __syncwarp();
 }
@@ -253,7 +256,8 @@ __global__ void __launch_bounds__(WG_THREADS, 1) wide_kernel(StageArgs a) {
       mbar_init(&sm.full[s][1], 1);
     }
     mbar_fence_init();
-    sm.fq_tail = sm.fq_head = sm.fq_done = 0;
+    sm.fq_tail = sm.fq_head = 0;
+    for (int s = 0; s < WG_FQ; ++s) sm.fq_free[s] = s;
   }
   if (tid < 16) sm.t16[tid] = exp2((double)tid / 16.0);
   __syncthreads();
@@ -501,12 +505,14 @@ __global__ void __launch_bounds__(WG_THREADS, 1) wide_kernel(StageArgs a) {
         const int n = min(K, nc);
         const float M = M_run;
         bool unc = n < 1 || nc < K || !(M > -INFINITY) || M == 0.0f;  // (signed-zero maxima: CTA kernel)
+        int kept_k = -1;
         if (!unc && tv.T == 0.0) {
           const int am = key_id(G.cand[0]);
           for (int d = lane; d < nd; d += 32) {
             io.token[d0 + d] = am;
             if (io.flags) io.flags[d0 + d] = 0;
           }
+          kept_k = greedy_kept(V, K, tv.topp);
         } else if (!unc) {
           // S = sum_c S_c 2^((m_c - M) L); the chunk bounds carry over (fp64 rescale ~1 ulp)
           double S = 0.0, Wt = 0.0;
@@ -641,10 +647,14 @@ __global__ void __launch_bounds__(WG_THREADS, 1) wide_kernel(StageArgs a) {
                 unc |= du;
               }
             }
+            kept_k = kstar;  // the kept set = the first kstar candidates (value desc, id asc)
           }
         }
         unc = __any_sync(0xffffffffu, unc);
-        if (lane == 0) G.flag = unc;
+        if (lane == 0) {
+          G.flag = unc;
+          if (!unc) set_kept(io, task_id, kept_k);
+        }
       }
       wbar(g);
       requeue_task = G.flag != 0;

@@ -17,7 +17,13 @@ Deliberate differences:
   is read back from the device on access;
 * the slab width (vocabulary) is fixed when the device cache is created (the
   ``vocab`` argument, else the first update); narrower entries are stored
-  as-is, a wider one rebuilds the device cache.
+  as-is (and resampled over their own width), a wider or longer one rebuilds
+  the device cache (live entries, pins, rounds and hotspot memos carried over;
+  handles taken before the rebuild go stale);
+* the slab holds ``page_capacity * page_rows`` rows: entries much narrower
+  than the slab can make the accounted budget admit more rows than that, and
+  such an insert raises ``CapacityError`` (rolled back) where the reference
+  would store it.
 
 Batched entry points (``lookup_batch``, ``insert_batch``, ``resample``,
 ``replay_stepwise``) take device tensors and never synchronise the host.
@@ -81,6 +87,7 @@ class CachedTrajectory:
         self._cache = cache
         self.slot = slot
         self.gen = gen
+        self.epoch = cache._epoch  # device cache generation: a rebuild (``_grow``) makes the handle stale
         self._n = n
         self.vocab_size = vocab
         self.digest = digest
@@ -96,25 +103,34 @@ class CachedTrajectory:
         d = self._cache.dev
         s = torch.full((self._n,), self.slot, dtype=torch.int32, device=d)
         p = torch.arange(self._n, dtype=torch.int32, device=d)
-        return s, p
+        g = torch.full((self._n,), self.gen, dtype=torch.int64, device=d).to(torch.int32)
+        return s, p, g
+
+    def _check_live(self):
+        if self.epoch != self._cache._epoch:
+            raise ConfigError("stale CachedTrajectory: the device cache was rebuilt since it was looked up")
 
     @property
     def logits_seq(self) -> np.ndarray:
         if self._logits is None:
-            self._logits = self._cache._gather(self.slot, self._n, self.vocab_size).cpu().numpy()
+            self._logits = self.logits_device().cpu().numpy()
         return self._logits
 
     def logits_device(self) -> torch.Tensor:
-        return self._cache._gather(self.slot, self._n, self.vocab_size)
+        """The entry's rows as a float32 device tensor (zeros once the entry was overwritten
+        or evicted: the read is checked against the handle's generation)."""
+        self._check_live()
+        return self._cache._gather(self.slot, self.gen, self._n, self.vocab_size)
 
     @property
     def token_seq(self) -> list[int]:
         if self._tokens is None:
-            s, p = self._positions()
+            self._check_live()
+            s, p, g = self._positions()
             out = torch.empty(self._n, dtype=torch.int32, device=self._cache.dev)
             if self._n:
-                _capi.check(_capi.lib.lc_cache_tokens(self._cache.handle, s.data_ptr(), p.data_ptr(), self._n,
-                                                      out.data_ptr(), _dev.stream_ptr(self._cache.dev)),
+                _capi.check(_capi.lib.lc_cache_tokens(self._cache.handle, s.data_ptr(), p.data_ptr(), g.data_ptr(),
+                                                      self._n, out.data_ptr(), _dev.stream_ptr(self._cache.dev)),
                             "lc_cache_tokens")
             self._tokens = out.cpu().tolist()
         return self._tokens
@@ -124,6 +140,8 @@ class CachedTrajectory:
         return self._n * self.vocab_size * 4 + TOKEN_OVERHEAD_BYTES * self._n
 
     def _meta(self, name):
+        if self.epoch != self._cache._epoch:
+            return None
         snap = self._cache._snapshot()
         if not snap["alive"][self.slot] or snap["gen"][self.slot] != self.gen:
             return None
@@ -160,7 +178,8 @@ class LogitsCache:
         self._memo: dict[tuple[int, int], dict] = {}
         self._round: dict[tuple[int, int], int] = {}
         self._snap = None
-        self._base = {"lookups": 0, "hits": 0}
+        self._base = {"lookups": 0, "hits": 0, "hotspot_computations": 0}
+        self._epoch = 0
         if vocab is not None:
             self._create(vocab)
 
@@ -172,7 +191,7 @@ class LogitsCache:
         budget_rows = self.budget_bytes // row_acct + 1
         page_rows = self._page_rows or (1 if self._max_rows <= 4 else 16)
         max_pages = -(-self._max_rows // page_rows)
-        keys = self._key_capacity or int(min(65536, budget_rows + 64))
+        keys = self._key_capacity or max(int(min(65536, budget_rows + 64)), getattr(self, "_min_keys", 0))
         pages = self._page_capacity or int(budget_rows // page_rows + keys + 2 * max_pages + 8)
         cfg = _capi.LcCacheConfig(V, _capi.LC_F32 if self._dtype == "float32" else _capi.LC_BF16, page_rows,
                                   keys, pages, max_pages, self.dev.index or 0, self.budget_bytes)
@@ -315,38 +334,58 @@ class LogitsCache:
 
     def replay_stepwise(self, digests: torch.Tensor, max_pos: int, n_branch: int, seeds: torch.Tensor,
                         temperature: torch.Tensor, top_k: torch.Tensor, top_p: torch.Tensor, counters=None,
-                        bufs: dict | None = None):
+                        bufs: dict | None = None, kept: torch.Tensor | None = None):
         """Lookup -> step-wise speculative resample of every cached position for
         n_branch branches per request -> acceptance (engine.py:285-331), all on
         the device.  Returns (tokens [n_req*max_pos*n_branch], replayed_len
-        [n_req*n_branch], diverged_at, slot, len)."""
+        [n_req*n_branch], diverged_at, slot, len).  ``kept`` (int32 [n_req*max_pos],
+        optional) receives each position's kept-set size (sampling.resample)."""
         n_req = digests.numel()
-        d = self.dev
         slot, gen, ln, vv = self.lookup_batch(digests)
-        b = bufs if bufs is not None else {}
+        b = self._replay_bufs(bufs, n_req, max_pos, n_branch)
         ntask = n_req * max_pos
         ndraw = ntask * n_branch
-        if "tasks" not in b or b["tasks"].numel() < ntask * _capi.TASK_DTYPE.itemsize:
-            b["tasks"] = torch.empty(ntask * _capi.TASK_DTYPE.itemsize, dtype=torch.uint8, device=d)
-            b["tok"] = torch.empty(ndraw, dtype=torch.int32, device=d)
-            b["flags"] = torch.empty(ndraw, dtype=torch.uint8, device=d)
-            b["cached"] = torch.empty(ntask, dtype=torch.int32, device=d)
-            b["pos"] = torch.arange(max_pos, dtype=torch.int32, device=d).repeat(n_req)
-            b["rep"] = torch.empty(n_req * n_branch, dtype=torch.int32, device=d)
-            b["div"] = torch.empty(n_req * n_branch, dtype=torch.int32, device=d)
         st = self._stream()
-        _capi.check(_capi.lib.lc_replay_tasks(slot.data_ptr(), ln.data_ptr(), n_req, max_pos, n_branch,
-                                              temperature.data_ptr(), top_k.data_ptr(), top_p.data_ptr(),
+        _capi.check(_capi.lib.lc_replay_tasks(slot.data_ptr(), ln.data_ptr(), vv.data_ptr(), n_req, max_pos,
+                                              n_branch, temperature.data_ptr(), top_k.data_ptr(), top_p.data_ptr(),
                                               b["tasks"].data_ptr(), st), "lc_replay_tasks")
-        tok, flags = sampling.resample(None, b["tasks"][: ntask * _capi.TASK_DTYPE.itemsize], seeds=seeds,
-                                       n_draws=ndraw, cache=self, counters=counters, out=(b["tok"], b["flags"]))
-        slots_rep = slot.repeat_interleave(max_pos)
-        _capi.check(_capi.lib.lc_cache_tokens(self.handle, slots_rep.data_ptr(), b["pos"].data_ptr(), ntask,
-                                              b["cached"].data_ptr(), st), "lc_cache_tokens")
+        tok, flags = sampling.resample(None, b["tasks"], seeds=seeds, n_draws=ndraw, cache=self, counters=counters,
+                                       out=(b["tok"], b["flags"]), kept=kept)
+        self._cached_tokens(slot, gen, b, st)
         _capi.check(_capi.lib.lc_replay_accept(tok.data_ptr(), b["cached"].data_ptr(), ln.data_ptr(), n_req, max_pos,
                                                n_branch, b["rep"].data_ptr(), b["div"].data_ptr(), st),
                     "lc_replay_accept")
         return tok, b["rep"], b["div"], slot, ln
+
+    def _replay_bufs(self, bufs, n_req: int, max_pos: int, n_branch: int) -> dict:
+        """Device buffers of a replay call, reused across calls of the same shape (a
+        caller's ``bufs`` dict is rebuilt whenever (n_req, max_pos, n_branch) changes)."""
+        b = bufs if bufs is not None else {}
+        shape = (n_req, max_pos, n_branch)
+        if b.get("shape") != shape:
+            d = self.dev
+            ntask = n_req * max_pos
+            ndraw = ntask * n_branch
+            b.clear()
+            b["shape"] = shape
+            b["tasks"] = torch.empty(ntask * _capi.TASK_DTYPE.itemsize, dtype=torch.uint8, device=d)
+            b["tok"] = torch.empty(max(ndraw, 1), dtype=torch.int32, device=d)
+            b["flags"] = torch.empty(max(ndraw, 1), dtype=torch.uint8, device=d)
+            b["cached"] = torch.empty(max(ntask, 1), dtype=torch.int32, device=d)
+            b["pos"] = torch.arange(max_pos, dtype=torch.int32, device=d).repeat(n_req)
+            b["rep"] = torch.empty(max(n_req * n_branch, 1), dtype=torch.int32, device=d)
+            b["div"] = torch.empty(max(n_req * n_branch, 1), dtype=torch.int32, device=d)
+        return b
+
+    def _cached_tokens(self, slot, gen, b, st):
+        """b["cached"][r * max_pos + t] = the looked-up entry's token t (-1 past its end)."""
+        n_req, max_pos, _ = b["shape"]
+        ntask = n_req * max_pos
+        slots_rep = slot.repeat_interleave(max_pos)
+        gens_rep = gen.repeat_interleave(max_pos)
+        _capi.check(_capi.lib.lc_cache_tokens(self.handle, slots_rep.data_ptr(), b["pos"].data_ptr(),
+                                              gens_rep.data_ptr(), ntask, b["cached"].data_ptr(), st),
+                    "lc_cache_tokens")
 
     @staticmethod
     def hotspot_draw_index(hotspots, max_pos: int, dev=None) -> torch.Tensor:
@@ -367,7 +406,7 @@ class LogitsCache:
     def replay_hotspot(self, digests: torch.Tensor, max_pos: int, n_branch: int, seeds: torch.Tensor,
                        temperature: torch.Tensor, top_k: torch.Tensor, top_p: torch.Tensor, hotspots=None,
                        counters=None, bufs: dict | None = None, draw_index: torch.Tensor | None = None,
-                       hot_list=None):
+                       hot_list=None, kept: torch.Tensor | None = None):
         """ReplayPolicy.HOTSPOT for a batch (engine.py:311-326): request r samples only at
         the positions in ``hotspots[r]`` (RngStream draw number = hotspots before t) and
         copies the cached token elsewhere; the replay stops after the first hotspot sample
@@ -384,38 +423,29 @@ class LogitsCache:
                 raise ConfigError("draw_index must hold n_req * max_pos entries")
             d_di = draw_index
         slot, gen, ln, vv = self.lookup_batch(digests)
-        b = bufs if bufs is not None else {}
+        b = self._replay_bufs(bufs, n_req, max_pos, n_branch)
         ntask = n_req * max_pos
         ndraw = ntask * n_branch
-        if "tasks" not in b or b["tasks"].numel() < ntask * _capi.TASK_DTYPE.itemsize:
-            b["tasks"] = torch.empty(ntask * _capi.TASK_DTYPE.itemsize, dtype=torch.uint8, device=d)
-            b["tok"] = torch.empty(ndraw, dtype=torch.int32, device=d)
-            b["flags"] = torch.empty(ndraw, dtype=torch.uint8, device=d)
-            b["cached"] = torch.empty(ntask, dtype=torch.int32, device=d)
-            b["pos"] = torch.arange(max_pos, dtype=torch.int32, device=d).repeat(n_req)
-            b["rep"] = torch.empty(n_req * n_branch, dtype=torch.int32, device=d)
-            b["div"] = torch.empty(n_req * n_branch, dtype=torch.int32, device=d)
         st = self._stream()
         if hot_list is not None:  # only the hotspot positions become tasks
             hp, hd = hot_list
             n_hot = hp.numel()
-            _capi.check(_capi.lib.lc_replay_tasks_hotspot_list(slot.data_ptr(), ln.data_ptr(), hp.data_ptr(),
-                                                               hd.data_ptr(), n_hot, max_pos, n_branch,
+            _capi.check(_capi.lib.lc_replay_tasks_hotspot_list(slot.data_ptr(), ln.data_ptr(), vv.data_ptr(),
+                                                               hp.data_ptr(), hd.data_ptr(), n_hot, max_pos, n_branch,
                                                                temperature.data_ptr(), top_k.data_ptr(),
                                                                top_p.data_ptr(), b["tasks"].data_ptr(), st),
                         "lc_replay_tasks_hotspot_list")
             ntask_run = n_hot
         else:
-            _capi.check(_capi.lib.lc_replay_tasks_hotspot(slot.data_ptr(), ln.data_ptr(), d_di.data_ptr(), n_req,
-                                                          max_pos, n_branch, temperature.data_ptr(),
-                                                          top_k.data_ptr(), top_p.data_ptr(), b["tasks"].data_ptr(),
-                                                          st), "lc_replay_tasks_hotspot")
+            _capi.check(_capi.lib.lc_replay_tasks_hotspot(slot.data_ptr(), ln.data_ptr(), vv.data_ptr(),
+                                                          d_di.data_ptr(), n_req, max_pos, n_branch,
+                                                          temperature.data_ptr(), top_k.data_ptr(), top_p.data_ptr(),
+                                                          b["tasks"].data_ptr(), st), "lc_replay_tasks_hotspot")
             ntask_run = ntask
         tok, flags = sampling.resample(None, b["tasks"][: ntask_run * _capi.TASK_DTYPE.itemsize], seeds=seeds,
-                                       n_draws=ndraw, cache=self, counters=counters, out=(b["tok"], b["flags"]))
-        slots_rep = slot.repeat_interleave(max_pos)
-        _capi.check(_capi.lib.lc_cache_tokens(self.handle, slots_rep.data_ptr(), b["pos"].data_ptr(), ntask,
-                                              b["cached"].data_ptr(), st), "lc_cache_tokens")
+                                       n_draws=ndraw, cache=self, counters=counters, out=(b["tok"], b["flags"]),
+                                       kept=kept)
+        self._cached_tokens(slot, gen, b, st)
         _capi.check(_capi.lib.lc_replay_accept_hotspot(tok.data_ptr(), b["cached"].data_ptr(), ln.data_ptr(),
                                                        d_di.data_ptr(), n_req, max_pos, n_branch,
                                                        b["rep"].data_ptr(), b["div"].data_ptr(), st),
@@ -445,12 +475,11 @@ class LogitsCache:
         if z.dim() != 2 or z.shape[0] != len(tokens):  # logits_cache.py:110-113
             raise ConfigError(f"logits/token length mismatch: {tuple(z.shape)} vs {len(tokens)}")
         n, V = z.shape
-        if n > self._max_rows:
-            raise ConfigError(f"trajectory of {n} rows exceeds max_rows={self._max_rows}")
         if self.handle is None:
+            self._max_rows = max(self._max_rows, n)
             self._create(max(V, self.vocab or 0))
-        elif V > self.vocab:
-            self._grow(V)
+        elif V > self.vocab or n > self._max_rows:
+            self._rebuild(max(V, self.vocab), max(n, self._max_rows))
         z = z.to(self.dev).contiguous()
         if n == 0:
             z = torch.zeros((1, V), dtype=z.dtype, device=self.dev)
@@ -469,35 +498,46 @@ class LogitsCache:
             self._prefetch_queue.append((key.digest, *prefetch_config))
         return entry
 
-    def _grow(self, V: int):
-        """Rebuild the device cache wider, re-inserting live entries in LRU order."""
+    def _rebuild(self, V: int, max_rows: int):
+        """Rebuild the device cache wider and/or longer (an entry wider than the slab or
+        longer than ``max_rows`` arrived).  Live entries are re-inserted in LRU order, so
+        their relative last-hit order -- hence every later victim choice -- is kept, with
+        their pins, rounds and hotspot memos; handles taken before go stale (epoch)."""
         snap = self._snapshot()
-        live = [int(s) for s in np.flatnonzero(snap["alive"])]
-        live.sort(key=lambda s: int(snap["last_hit"][s]))
+        live = sorted((int(s) for s in np.flatnonzero(snap["alive"])), key=lambda s: int(snap["last_hit"][s]))
         saved = []
         for s in live:
-            e = self._entry(s, int(snap["gen"][s]), int(snap["nrows"][s]), int(snap["vocab"][s]),
-                            int(snap["digest"][s]))
-            saved.append((e.digest, e.logits_device(), e.token_seq, int(snap["pins"][s])))
+            g, n, v, dg = int(snap["gen"][s]), int(snap["nrows"][s]), int(snap["vocab"][s]), int(snap["digest"][s])
+            toks = self._entry(s, g, n, v, dg).token_seq
+            saved.append((dg, self._gather(s, g, n, v), toks, int(snap["pins"][s]), self._round.get((s, g), 0),
+                          self._memo.get((s, g), {})))
         st = self._stats()
         self._base["lookups"] += int(st.lookups)
         self._base["hits"] += int(st.hits)
         _capi.lib.lc_cache_destroy(self.handle)
         self.handle = None
-        self._memo.clear()
-        self._round.clear()
+        self._memo = {}
+        self._round = {}
+        self._epoch += 1
+        self._max_rows = max_rows
+        self._min_keys = len(saved) + 64
         self._create(V)
-        for dg, rows, toks, _pins in saved:
-            self.update(StateKey(dg), rows, toks)
+        for dg, rows, toks, pins, rnd, memo in saved:
+            e = self.update(StateKey(dg), rows, toks, round_index=rnd)
+            self._memo[(e.slot, e.gen)] = memo
+            for _ in range(pins):
+                self._pin(e, 1)
 
-    def _gather(self, slot: int, n: int, vocab: int) -> torch.Tensor:
+    def _gather(self, slot: int, gen: int, n: int, vocab: int) -> torch.Tensor:
         d = self.dev
         out = torch.empty((max(n, 0), vocab), dtype=torch.float32, device=d)
         if n:
             s = torch.full((n,), slot, dtype=torch.int32, device=d)
             p = torch.arange(n, dtype=torch.int32, device=d)
-            _capi.check(_capi.lib.lc_cache_gather(self.handle, s.data_ptr(), p.data_ptr(), n, out.data_ptr(),
-                                                  _capi.LC_F32, vocab, self._stream()), "lc_cache_gather")
+            g = torch.full((n,), gen, dtype=torch.int64, device=d).to(torch.int32)
+            _capi.check(_capi.lib.lc_cache_gather(self.handle, s.data_ptr(), p.data_ptr(), g.data_ptr(), n,
+                                                  out.data_ptr(), _capi.LC_F32, vocab, self._stream()),
+                        "lc_cache_gather")
         return out
 
     def _pin(self, entry: CachedTrajectory, delta: int):
@@ -521,12 +561,12 @@ class LogitsCache:
         (lc_cache_row_entropy: no gather of the rows)."""
         n = len(entry)
         d = self.dev
-        s = torch.full((n,), entry.slot, dtype=torch.int32, device=d)
-        p = torch.arange(n, dtype=torch.int32, device=d)
+        entry._check_live()
+        s, p, g = entry._positions()
         H = torch.empty(n, dtype=torch.float64, device=d)
         pm = torch.empty(n, dtype=torch.float64, device=d)
-        _capi.check(_capi.lib.lc_cache_row_entropy(self.handle, s.data_ptr(), p.data_ptr(), n, float(temperature),
-                                                   H.data_ptr(), pm.data_ptr(), self._stream()),
+        _capi.check(_capi.lib.lc_cache_row_entropy(self.handle, s.data_ptr(), p.data_ptr(), g.data_ptr(), n,
+                                                   float(temperature), H.data_ptr(), pm.data_ptr(), self._stream()),
                     "lc_cache_row_entropy")
         t = torch.arange(n, dtype=torch.float64, device=d)
         return (H * (1.0 - pm) / (1.0 + decay * t)).cpu().numpy()

@@ -217,12 +217,15 @@ def _workspace(dev) -> Workspace:
 
 def resample(rows: torch.Tensor, tasks, u: torch.Tensor | None = None, seeds: torch.Tensor | None = None,
              index: torch.Tensor | None = None, n_draws: int | None = None, counters: torch.Tensor | None = None,
-             cache=None, out: tuple | None = None):
+             cache=None, out: tuple | None = None, kept: torch.Tensor | None = None):
     """Fused resample of device rows (or of cached rows when ``cache`` is given).
 
     ``tasks``: numpy TASK_DTYPE array or a uint8 device tensor of packed tasks.
     Draws come from ``u`` (fp64, one per draw) or from ``seeds`` (+ ``index``).
     Returns (tokens int32, flags uint8) device tensors, one entry per draw.
+    ``kept`` (int32 device tensor, one per task, optional) receives each task's
+    kept-set size K: truncate()'s kept ids are the first K of the row in
+    (logit desc, id asc) order (sampling.py:71-94; V = untruncated, -1 = bad row).
     """
     dev = rows.device if rows is not None else cache.dev
     if isinstance(tasks, np.ndarray):
@@ -241,7 +244,10 @@ def resample(rows: torch.Tensor, tasks, u: torch.Tensor | None = None, seeds: to
         tok, flags = out
     vocab = rows.shape[1] if rows is not None else cache.vocab
     ws = _workspace(dev).get(n_tasks, vocab)
-    draws = _capi.LcDraws(_dev.ptr(u), _dev.ptr(seeds), _dev.ptr(index), tok.data_ptr(), _dev.ptr(flags))
+    if kept is not None and (kept.dtype != torch.int32 or kept.numel() < n_tasks):
+        raise ConfigError("kept must be an int32 tensor with one entry per task")
+    draws = _capi.LcDraws(_dev.ptr(u), _dev.ptr(seeds), _dev.ptr(index), tok.data_ptr(), _dev.ptr(flags),
+                          _dev.ptr(kept))
     cnt = _dev.ptr(counters)
     if cache is None:
         if rows.dtype == torch.bfloat16:

@@ -455,7 +455,7 @@ def test_cache_warp_policy_stress_vs_oracle(collide, page_rows, max_rows):
         assert live == {d: e.slot for d, e in orc.entries.items()}, step
         if step % 15 == 14:
             for d, e in orc.entries.items():
-                got = cache._gather(e.slot, e.n, V).cpu().numpy()
+                got = cache._gather(e.slot, e.gen, e.n, V).cpu().numpy()
                 ids = expect[d] + np.arange(e.n)
                 assert np.array_equal(got, (ids[:, None] * 64 + np.arange(V)[None, :]).astype(np.float32)), d
     assert orc.evictions > 20

@@ -192,3 +192,50 @@ def test_cache_oracle_heap_mode_equals_scan_mode():
             assert (ea.slot, ea.gen, ea.pages) == (eb.slot, eb.gen, eb.pages)
             assert va == vb
         assert a.total == b.total and sorted(a.entries) == sorted(b.entries)
+
+
+def test_fast_kept_order_and_draw_many_equal_the_reference_order():
+    """oracle.sampling_ref.kept_order_fast / draw_many (bulk-check helpers) == the
+    reference-order kept_order / per-draw draw on producer rows and golden cases."""
+    rng = np.random.default_rng(0)
+    cases = [(mixing_ref.fill_logits_np(mixing_ref.mix2(5, i), V, conc, 5.0), T, k, p)
+             for i, (V, conc, T, k, p) in enumerate([(32000, 2.5, 0.6, None, 0.9), (32000, 0.0, 0.6, None, 0.9),
+                                                      (32000, 0.0, 1.0, None, 0.99), (20000, 2.5, 0.6, 50, 0.95),
+                                                      (20000, 0.0, 1.0, 50, 0.95), (9000, 1.0, 0.3, 7000, 1.0),
+                                                      (9000, 0.0, 2.0, None, 0.999), (512, 0.0, 1.0, 40, 0.2)])]
+    for c in sampling_cases()[::7]:
+        cases.append((c.z, c.T, c.top_k, c.top_p))
+    for z, T, k, p in cases:
+        prob = sampling_ref.softmax(z, T)
+        a, b = sampling_ref.kept_order(prob, k, p), sampling_ref.kept_order_fast(prob, k, p, cand=256)
+        assert (a is None and b is None) or np.array_equal(a, b), (T, k, p)
+        q = sampling_ref.truncate(prob, k, p)
+        q2, K = sampling_ref.truncate_fast(prob, k, p)
+        assert np.array_equal(q, q2) and K == (len(z) if a is None else len(a))
+        us = np.concatenate([rng.random(40), [0.0, 1.0 - 2 ** -53]])
+        assert sampling_ref.draw_many(q, us).tolist() == [sampling_ref.draw(q, float(u)) for u in us]
+
+
+def test_bulk_check_counts_and_catches_mismatches():
+    from oracle import bulk
+
+    V, n, D = 2048, 6, 5
+    states = np.array([mixing_ref.mix2(7, i) for i in range(n)], dtype=np.uint64)
+    seeds = np.array([[mixing_ref.mix2(1, 10 * r + b) for b in range(D)] for r in range(n)], dtype=np.uint64)
+    index = np.arange(n)
+    toks, kept = [], []
+    for r in range(n):
+        z = mixing_ref.bf16_round(mixing_ref.fill_logits_np(int(states[r]), V, 2.5, 5.0))
+        prob = sampling_ref.softmax(z, 0.6)
+        q = sampling_ref.truncate(prob, None, 0.9)
+        toks.append([sampling_ref.draw(q, mixing_ref.uniform(int(seeds[r, b]), r)) for b in range(D)])
+        kept.append(len(sampling_ref.kept_order(prob, None, 0.9)))
+    toks, kept = np.array(toks, np.int32), np.array(kept, np.int32)
+    job = dict(V=V, T=0.6, k=None, p=0.9, bf16=True, conc=2.5, states=states, seeds=seeds, index=index,
+               tokens=toks, kept=kept)
+    r = bulk.check_rows(job)
+    assert (r["draws"], r["token_mismatches"], r["kept_checked"], r["kept_mismatches"]) == (n * D, 0, n, 0)
+    toks[2, 3] += 1
+    kept[4] += 1
+    r = bulk.check_rows(dict(job, tokens=toks, kept=kept))
+    assert r["token_mismatches"] == 1 and r["kept_mismatches"] == 1
