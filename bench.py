@@ -159,6 +159,23 @@ def setup_workload(cfg, dev, rank, world=1):
                 bufs={})
 
 
+def workload_config(args, cfg, world):
+    """The ``config`` object of a resample bench line -- identical for our arm and the
+    reference arm (same workload, same keys)."""
+    n_req = cfg["n_req"]
+    if cfg["scaling"] == "strong":
+        from paper_2604_17353_b200.shard import local_trees
+
+        n_req = len(local_trees(8, 0, world)) * (cfg["n_req"] // 8)
+    esz = 2 if cfg["dtype"] == "bfloat16" else 4
+    return {"workload": cfg["desc"], "config": args.config, "vocab": cfg["V"], "requests_per_gpu": n_req,
+            "branches": cfg["nb"], "rows_per_entry": cfg["R"], "draws_per_row": cfg["nb"], "temperature": cfg["T"],
+            "top_k": cfg["k"] or None, "top_p": cfg["p"], "slab_gb_per_gpu": n_req * cfg["R"] * cfg["V"] * esz / 1e9,
+            "l2": "inputs larger than L2 (slab re-read every step)", "parallelism": f"tree-sharded x{world}",
+            "replay_policy": args.policy,
+            **({"hotspot_decay": 0.001, "hotspot_threshold": 0.6} if args.policy == "hotspot" else {})}
+
+
 def traffic_per_launch(cfg, n_rows):
     """DRAM bytes of one resample launch, from the committed ncu --set full capture
     (profiles/*traffic*.json: read + write bytes per row of the staged kernel), or None."""
@@ -226,11 +243,34 @@ def run_ours(args, cfg, rank, world, dev):
             return cache.replay_stepwise(w["digests"], R, nb, w["seeds"], w["T"], w["K"], w["P"],
                                          counters=counters, bufs=w["bufs"])
 
+    graph = None
+    if args.graph:
+        # capture one whole step (lookup -> tasks -> resample -> cached tokens -> acceptance, ~8
+        # launches, no host sync) in a CUDA graph: small per-rank batches (C5 at G=8: 2048 rows per
+        # GPU) are otherwise bound by launch latency and Python glue.  The dominant kernel's time
+        # is still taken from eager launches (events cannot be read inside a graph).
+        for _ in range(args.warmup):
+            step()
+        torch.cuda.synchronize(dev)
+        graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(graph):
+            g_out = step()
+        eager_step = step
+
+        def step():
+            graph.replay()
+            return g_out
+
     lcb.sampling.resample = timed_resample
     try:
         for _ in range(args.warmup):
             step()
         torch.cuda.synchronize(dev)
+        if graph is not None:  # eager launches for the kernel-time share
+            for _ in range(args.steps):
+                eager_step()
+            torch.cuda.synchronize(dev)
+            k_ev = list(ev)
         ev.clear()
         counters.zero_()
         if world > 1:
@@ -246,7 +286,7 @@ def run_ours(args, cfg, rank, world, dev):
         if world > 1:
             dist.barrier()
         ms = t0.elapsed_time(t1)
-        k_ms = [s.elapsed_time(e) for s, e in ev]
+        k_ms = [s.elapsed_time(e) for s, e in (k_ev if graph is not None else ev)]
     finally:
         lcb.sampling.resample = orig
     accepted = int(rep.sum().item()) * args.steps
@@ -351,13 +391,8 @@ def run_ours(args, cfg, rank, world, dev):
         "vs_baseline": None,
         "dtype": "bf16" if esz == 2 else "f32",
         "data": "synthetic (reference producer fill_logits, seed 7, conc 2.5, range 5.0)",
-        "config": {"workload": cfg["desc"], "config": args.config, "vocab": V, "requests_per_gpu": n_req,
-                   "branches": nb, "rows_per_entry": R, "draws_per_row": nb, "temperature": cfg["T"],
-                   "top_k": cfg["k"] or None, "top_p": cfg["p"], "slab_gb_per_gpu": w["slab_bytes"] / 1e9,
-                   "l2": "inputs larger than L2 (slab re-read every step)", "parallelism": f"tree-sharded x{world}",
-                   "replay_policy": args.policy,
-                   **({"hotspot_decay": 0.001, "hotspot_threshold": 0.6, "hotspot_rows": hot_rows}
-                      if args.policy == "hotspot" else {})},
+        "config": {**workload_config(args, CONFIGS[args.config], world),
+                   **({"hotspot_rows": hot_rows} if args.policy == "hotspot" else {})},
         "accepted_tokens_per_s": accepted / (ms * 1e-3),
         "rows_per_s": (n_rows * world if cfg["scaling"] == "weak" else CONFIGS[args.config]["n_req"] * R)
         * args.steps / (ms * 1e-3),
@@ -373,6 +408,7 @@ def run_ours(args, cfg, rank, world, dev):
                 "d2h_overlap": "step i's tokens copied out on a second stream while step i+1 computes",
                 "d2h_bytes_per_step": d2h},
         "gpu_launches": 8 * args.steps,
+        "cuda_graph": graph is not None,
         "clocks": clk.summary(),
     }
     if not args.no_check and args.policy == "step_wise":
@@ -467,8 +503,10 @@ def run_check(args, cfg, w, rank, world, dev):
 
 
 def _cpu_worker(a):
-    """Reference per-draw path: sample(truncate(softmax(z, T), k, p), u) on rows of the workload."""
-    V, R, T, k, p, bf16, seconds, wid = a
+    """Reference per-draw path: sample(truncate(softmax(z, T), k, p), u) on rows of the workload,
+    in steps: ``warmup`` calibration steps, then ``steps`` timed steps of a fixed draw count sized
+    so one step takes about ``step_s`` seconds."""
+    V, T, k, p, bf16, warmup, steps, step_s, wid = a
     sys.path.insert(0, ROOT)
     from oracle import mixing_ref, sampling_ref
 
@@ -476,47 +514,71 @@ def _cpu_worker(a):
     rows = mixing_ref.fill_rows_np([mixing_ref.mix2(7, wid * 1000 + i) for i in range(16)], V, 2.5)
     if bf16:
         rows = mixing_ref.bf16_round(rows)
-    n = 0
+    n = [0]
+
+    def run(count):
+        for _ in range(count):
+            z = rows[n[0] % len(rows)]
+            q = sampling_ref.truncate(sampling_ref.softmax(z, T), k or None, p)
+            sampling_ref.draw(q, float(rng.random()))
+            n[0] += 1
+
     t0 = time.perf_counter()
-    while time.perf_counter() - t0 < seconds:
-        z = rows[n % len(rows)]
-        q = sampling_ref.truncate(sampling_ref.softmax(z, T), k or None, p)
-        sampling_ref.draw(q, float(rng.random()))
-        n += 1
-    return n, time.perf_counter() - t0
+    for _ in range(max(warmup, 1)):
+        run(4)
+    per_draw = (time.perf_counter() - t0) / (4 * max(warmup, 1))
+    per_step = max(1, int(step_s / max(per_draw, 1e-9)))
+    times = []
+    for _ in range(steps):
+        t = time.perf_counter()
+        run(per_step)
+        times.append(time.perf_counter() - t)
+    return per_step, times
 
 
-def cpu_baseline(cfg, seconds=12.0, cores=None):
+def _cpu_model():
+    try:
+        return [l.split(":", 1)[1].strip() for l in open("/proc/cpuinfo") if l.startswith("model name")][0]
+    except Exception:
+        return "unknown"
+
+
+def cpu_baseline(cfg, seconds=12.0, cores=None, steps=1, warmup=1):
+    """The oracle port on every host core: ``steps`` steps, each a bounded sample of the
+    workload's draws (about seconds/steps of CPU time per worker).  Step time = max over
+    workers; value = all workers' draws / the summed step times."""
     import multiprocessing as mp
 
     cores = cores or os.cpu_count() or 1
-    args = [(cfg["V"], cfg["R"], cfg["T"], cfg["k"], cfg["p"], cfg["dtype"] == "bfloat16", seconds, i)
+    args = [(cfg["V"], cfg["T"], cfg["k"], cfg["p"], cfg["dtype"] == "bfloat16", warmup, steps, seconds / steps, i)
             for i in range(cores)]
-    ctx = mp.get_context("spawn")
-    with ctx.Pool(cores) as pool:
+    with mp.get_context("spawn").Pool(cores) as pool:
         out = pool.map(_cpu_worker, args)
-    n = sum(o[0] for o in out)
-    t = max(o[1] for o in out)
-    try:
-        model = [l.split(":", 1)[1].strip() for l in open("/proc/cpuinfo") if l.startswith("model name")][0]
-    except Exception:
-        model = "unknown"
+    step_times = [max(o[1][s] for o in out) for s in range(steps)]
+    n = sum(o[0] * steps for o in out)
+    t = sum(step_times)
     return {"value": n / t, "unit": "tokens/s", "cores": cores, "kind": "port",
-            "sample": f"{n} draws of the workload's rows (V={cfg['V']}, T={cfg['T']}, top_k={cfg['k'] or None}, "
-                      f"top_p={cfg['p']}), one softmax+truncate+sample per draw as the reference engine does "
-                      f"(engine.py:302-305), {seconds:.0f} s per worker, {model}"}
+            "ms_per_step": 1e3 * t / steps, "draws_per_step": n // steps,
+            "sample": f"{steps} step(s) x {n // steps} draws of the workload's rows (V={cfg['V']}, T={cfg['T']}, "
+                      f"top_k={cfg['k'] or None}, top_p={cfg['p']}; {cores} workers x {n // steps // cores} draws "
+                      f"per step), one softmax+truncate+sample per draw as the reference engine does "
+                      f"(engine.py:302-305), ~{seconds / steps:.1f} s per step, {_cpu_model()}"}
 
 
 def run_reference(args, cfg):
-    res_cpu = cpu_baseline(cfg, seconds=args.cpu_seconds)
+    """--impl reference: the reference's CPU path (the oracle port, oracle/sampling_ref.py) on the
+    host cores, K timed steps after W warm-up steps, each step a bounded sample of the workload's
+    draws; ms_per_step is the measured wall time of a step (max over workers)."""
+    res_cpu = cpu_baseline(cfg, seconds=args.cpu_seconds, steps=args.steps, warmup=args.warmup)
     v = res_cpu["value"]
-    per_step_tokens = cfg["n_req"] * cfg["R"] * cfg["nb"]
     return {
         "metric": "resampled_tokens_per_s", "value": v, "unit": "tokens/s", "impl": "reference",
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": per_step_tokens / v * 1e3, "higher_is_better": True, "scaling": "weak",
-        "vs_baseline": None, "dtype": "f64 (numpy)", "data": "synthetic",
-        "config": {"workload": cfg["desc"], "config": args.config},
+        "ms_per_step": res_cpu["ms_per_step"], "higher_is_better": True, "scaling": cfg["scaling"],
+        "vs_baseline": None, "dtype": "f64 (numpy)",
+        "data": "synthetic (reference producer fill_logits, seed 7, conc 2.5, range 5.0)",
+        "config": workload_config(args, cfg, args.gpus),
+        "step": "a bounded sample of the workload's draws per step (see cpu_baseline.sample)",
         "cpu_baseline": res_cpu,
         "e2e": {"value": v, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
@@ -860,6 +922,54 @@ def run_c4(args, cfg, rank, world, dev):
     return res
 
 
+def spawn_ranks(args):
+    """``--gpus N`` without a torchrun environment: re-launch this script under
+    torch.distributed.run, one process per GPU on this node (127.0.0.1 rendezvous);
+    rank 0 prints the line."""
+    import socket
+
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__), *sys.argv[1:]]
+    sys.stdout.flush()
+    os.execv(sys.executable, cmd)
+
+
+def run_dry(args, cfg, rank, world):
+    """The multi-rank host logic without a GPU (gloo): every rank derives its shard of the
+    workload exactly as the GPU run does (tree i -> rank i mod G for the tree-sharded configs,
+    its own requests otherwise), then the statistics vector (max of times, sum of counters)
+    is reduced as after a timed interval.  Used by tests/test_shard_gloo.py."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_2604_17353_b200.shard import local_trees, reduce_stats
+
+    if world > 1:
+        dist.init_process_group("gloo")
+    n_req = cfg.get("n_req", 0)
+    trees = None
+    if cfg.get("scaling") == "strong":
+        trees = local_trees(8, rank, world)
+        n_req = len(trees) * (cfg["n_req"] // 8)
+    rows = n_req * cfg.get("R", 1)
+    times = torch.tensor([1.0 + rank, 2.0 * (rank + 1)], dtype=torch.float64)
+    counts = torch.tensor([float(rows), float(rows * cfg.get("nb", 1)), 1.0], dtype=torch.float64)
+    t, c = reduce_stats(times, counts, world)
+    shards = [None] * world
+    if world > 1:
+        dist.all_gather_object(shards, {"rank": rank, "trees": trees, "requests": n_req, "rows": rows})
+        dist.destroy_process_group()
+    else:
+        shards = [{"rank": 0, "trees": trees, "requests": n_req, "rows": rows}]
+    return {"dry_run": True, "n_gpus": world, "config": args.config, "scaling": cfg.get("scaling"),
+            "shards": shards, "rows_total": int(c[0]), "draws_total": int(c[1]), "ranks_reporting": int(c[2]),
+            "max_times": t.tolist(), "backend": "gloo"}
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -877,11 +987,24 @@ def main():
                     help="replay policy of the resample step (ReplayPolicy)")
     ap.add_argument("--hit-ratio", type=float, default=None,
                     help="c3: lookup hit ratio h of the sweep (default: every branch cached)")
+    ap.add_argument("--graph", action=argparse.BooleanOptionalAction, default=None,
+                    help="replay the step from a CUDA graph (default: on for the tree-sharded c5)")
+    ap.add_argument("--dry-run", action="store_true",
+                    help="no GPU: run the N-rank host logic (shard plan + statistics reduction) over gloo")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     cfg = CONFIGS[args.config]
+    if args.graph is None:
+        args.graph = cfg.get("scaling") == "strong"
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        spawn_ranks(args)  # re-executes this script under torchrun; does not return
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
+    if args.dry_run:
+        res = run_dry(args, cfg, rank, world)
+        if rank == 0:
+            print(json.dumps(res), flush=True)
+        return
     if args.impl == "reference":
         if rank == 0:
             if args.config == "c4":

@@ -54,3 +54,22 @@ def test_stats_reduction_world2_gloo():
     for _, _, t, c in out:
         assert t == [11.0, 10.0]          # max over ranks
         assert c == [8 * 512.0, 3.0]      # sum over ranks
+
+
+def test_bench_spawns_ranks_dry_run():
+    """bench.py --gpus 2 re-launches itself under torchrun (two ranks) and runs the per-rank
+    host path over gloo: tree-sharded C5 (tree i -> rank i mod 2) and the stats reduction."""
+    import json
+    import subprocess
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, os.path.join(root, "bench.py"), "--gpus", "2", "--config", "c5",
+                        "--dry-run"], capture_output=True, text=True, timeout=300, cwd=root)
+    assert r.returncode == 0, r.stderr[-2000:]
+    line = [l for l in r.stdout.splitlines() if l.startswith("{")][-1]
+    d = json.loads(line)
+    assert d["n_gpus"] == 2 and d["ranks_reporting"] == 2
+    assert [s["trees"] for s in d["shards"]] == [[0, 2, 4, 6], [1, 3, 5, 7]]
+    assert d["rows_total"] == 8 * 512 * 4  # every tree's rows exactly once across the ranks
+    assert d["max_times"] == [2.0, 4.0]
