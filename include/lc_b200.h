@@ -29,7 +29,7 @@
 extern "C" {
 #endif
 
-#define LC_ABI_VERSION 2
+#define LC_ABI_VERSION 3
 
 typedef enum lc_status {
   LC_OK = 0,
@@ -37,7 +37,8 @@ typedef enum lc_status {
   LC_E_ZERO_MASS = 2, /* -> RuntimeError (sampling.py:101-102) */
   LC_E_CAPACITY = 3,  /* slab pages or entry slots exhausted */
   LC_E_CUDA = 4,      /* CUDA runtime failure (lc_last_error has the text) */
-  LC_E_ARG = 5        /* bad argument (null pointer, negative size ...) */
+  LC_E_ARG = 5,       /* bad argument (null pointer, negative size ...) */
+  LC_E_STATE = 6      /* a write-back's replayed prefix is no longer the key's live entry */
 } lc_status;
 
 typedef enum lc_dtype { LC_F32 = 0, LC_BF16 = 1 } lc_dtype;
@@ -197,6 +198,36 @@ int lc_cache_insert(lc_cache* cache, const uint64_t* d_digests, const int32_t* d
                     const int64_t* d_row_offsets, const int32_t* d_tokens, int32_t max_len, int32_t* d_slot,
                     uint32_t* d_gen, void* stream);
 
+/* Write-back (engine.py:349-361: merged = Z[:replayed] ++ new_rows; cache.update(key,
+ * merged, out)) without copying the replayed rows.  As lc_cache_insert,
+ * plus per entry keep[i] = rows already in the slab: when keep[i] > 0 the insert must
+ * overwrite the key's live entry of generation keep_gen[i] (the caller holds a pin on it,
+ * lc_cache_pin), whose first keep[i] rows become rows 0 .. keep[i]-1 of the new entry in
+ * place (an overwrite returns the old pages in page order, oracle/cache_ref.py); anything
+ * else latches LC_E_STATE.  Rows keep[i] .. len-1 are copied from d_rows when given, else
+ * left for lc_cache_fill_rows; tokens (all len of them) from d_tokens when given.
+ * Accounted bytes follow the reference (n*V*4 + 8n) as for any update.              */
+int lc_cache_writeback(lc_cache* cache, const uint64_t* d_digests, const int32_t* d_lengths, const int32_t* d_vocabs,
+                       const int32_t* d_keep, const uint32_t* d_keep_gen, int64_t n, const void* d_rows,
+                       int32_t rows_dtype, int64_t rows_stride, const int64_t* d_row_offsets, const int32_t* d_tokens,
+                       int32_t max_len, int32_t* d_slot, uint32_t* d_gen, void* stream);
+
+/* The synthetic producer (model.py:67-83 logits_from_state -> kernels.py:47-60
+ * fill_logits) writing straight into cached rows (slot, pos) of live entries, over the
+ * entry's vocab, as the slab dtype (the miss path's rows never pass
+ * through a staging buffer or an insert copy).                                      */
+int lc_cache_fill_rows(lc_cache* cache, const int32_t* d_slot, const uint32_t* d_gen, const int32_t* d_pos,
+                       const uint64_t* d_states, int64_t n, double concentration, double logit_range, void* stream);
+
+/* len(entry) of (slot, generation) handles, -1 when the entry was overwritten or
+ * evicted (the reference's entry object is no longer in cache.entries).            */
+int lc_cache_entry_len(lc_cache* cache, const int32_t* d_slot, const uint32_t* d_gen, int64_t n, int32_t* d_len,
+                       void* stream);
+
+/* entry.token_seq[pos] = tokens[i] for cached rows (slot, pos) of live entries. */
+int lc_cache_set_tokens(lc_cache* cache, const int32_t* d_slot, const uint32_t* d_gen, const int32_t* d_pos,
+                        const int32_t* d_tokens, int64_t n, void* stream);
+
 /* pin/unpin (logits_cache.py:145-149) by (slot, generation) handles; a
  * handle whose entry was overwritten or evicted is ignored (the reference
  * pins the old entry object).  delta = +1 pin, -1 unpin.                     */
@@ -285,6 +316,51 @@ int lc_cache_snapshot(lc_cache* cache, uint64_t* d_digest, unsigned long long* d
                       int32_t* d_pins, int32_t* d_nrows, int32_t* d_vocab, uint8_t* d_alive, void* stream);
 /* Page table [key_capacity][max_pages] (-1 = unused), for fused consumers. */
 int lc_cache_page_table(lc_cache* cache, const int32_t** d_pages, int32_t* max_pages, int32_t* page_rows);
+
+/* ------------------------------------------------------------------ engine
+ * The miss path of replay-aware generate (engine.py:336-347) for a WAVE of requests
+ * (distinct prompt keys; the caller orders waves as the reference orders calls).    */
+
+/* digest_out[r] = fold_token over tokens[r*stride .. r*stride + count[r]) starting at
+ * digest_in[r]: StateKey digest of prompt + out[:replayed] (engine.py:337 prefill of
+ * prompt + out; fold_token prefix extension, mixing.py:63-65).                       */
+int lc_engine_fold(const uint64_t* d_digest_in, const int32_t* d_tokens, int64_t stride, const int32_t* d_count,
+                   int64_t n, uint64_t* d_digest_out, void* stream);
+
+/* One decode step `step` of every request r of the wave: position t = start[r] + step
+ * (inactive once t >= max_tokens); for step > 0 the digest absorbs the previous token
+ * out[r*max_tokens + t - 1] (engine.py:227); the row fill_logits(mix2(model_seed,
+ * digest)) (model.py:62-83, engine.py:213/231) is written into the write-back entry's
+ * slab row (slot[r], gen[r], t) when that row is live (f1: no staging, no copy) and into
+ * staging row r when d_staging != NULL; task r (resample of that row, draw number
+ * u_start[r] + step, token -> out[r*max_tokens + t]) goes to d_tasks[r]: resample it with
+ * lc_cache_resample (no staging) or lc_resample over the staging rows.
+ * Without a cache handle, d_staging is required.                                     */
+typedef struct lc_decode_step {
+  int64_t n;                  /* requests in the wave (<= 65535) */
+  int32_t vocab;              /* model vocab (ModelConfig.vocab_size) */
+  int32_t max_tokens;         /* SamplingConfig.max_tokens of the wave */
+  int32_t step;               /* decode step index (0 = the prefill row) */
+  int32_t staging_dtype;      /* lc_dtype of d_staging (must equal the slab dtype with a cache) */
+  uint64_t model_seed;        /* ModelConfig.seed */
+  double concentration;       /* ModelConfig.concentration */
+  double logit_range;         /* ModelConfig.logit_range */
+  const int32_t* d_start;     /* [n] first decoded position (= replayed_len) */
+  const int64_t* d_u_start;   /* [n] RngStream draws consumed before the decode */
+  const uint64_t* d_digest_in;/* [n] digest before this step's fold */
+  uint64_t* d_digest_out;     /* [n] digest after it (ping-pong with d_digest_in) */
+  const int32_t* d_out;       /* [n * max_tokens] generated tokens (previous step's token read) */
+  const int32_t* d_slot;      /* [n] write-back entry (cache mode) */
+  const uint32_t* d_gen;      /* [n] its generation */
+  const double* d_temperature;/* [n] */
+  const int32_t* d_top_k;     /* [n] (<= 0: none) */
+  const double* d_top_p;      /* [n] */
+  void* d_staging;            /* [n * staging_stride] rows or NULL */
+  int64_t staging_stride;     /* elements */
+  lc_task* d_tasks;           /* [n] out */
+} lc_decode_step;
+
+int lc_engine_decode_step(lc_cache* cache, const lc_decode_step* step, void* stream);
 
 #ifdef __cplusplus
 }

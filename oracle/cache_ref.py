@@ -25,8 +25,9 @@ allocator must match it bit-for-bit -- "cache slot indices bit-exact"):
   an overwrite keeps the key's slot and bumps its generation;
 * row pages (``page_rows`` rows each) come from a LIFO free stack, initially
   ``0, 1, 2, ...``; at each insert the overwritten entry's pages are pushed
-  first (in page order), then the new entry's pages are popped, then each
-  victim's pages are pushed (in page order) as it is evicted;
+  first (in REVERSE page order, so the new entry gets them back in place),
+  then the new entry's pages are popped, then each victim's pages are pushed
+  (in page order) as it is evicted;
 * a batch of operations is the sequence of its elements in index order.
 """
 
@@ -103,7 +104,9 @@ class CacheOracle:
         old = self.entries.get(digest)
         if old is not None:
             self.total -= old.nbytes
-            for p in old.pages:
+            # pushed in reverse page order: the new entry's pops (page 0 first) return
+            # them in place, so a write-back's replayed prefix rows need no copy
+            for p in reversed(old.pages):
                 self.free_pages.append(p)
             slot = old.slot
             self.gen[slot] += 1

@@ -13,7 +13,8 @@ import os
 from . import build as _build
 from .errors import CapacityError, ConfigError
 
-LC_OK, LC_E_CONFIG, LC_E_ZERO_MASS, LC_E_CAPACITY, LC_E_CUDA, LC_E_ARG = range(6)
+LC_OK, LC_E_CONFIG, LC_E_ZERO_MASS, LC_E_CAPACITY, LC_E_CUDA, LC_E_ARG, LC_E_STATE = range(7)
+ABI_VERSION = 3
 LC_F32, LC_BF16 = 0, 1
 LC_DRAW_PRECISE, LC_DRAW_UNRESOLVED, LC_DRAW_BAD_ROW = 1, 2, 4
 
@@ -58,6 +59,32 @@ class LcCacheConfig(C.Structure):
     ]
 
 
+class LcDecodeStep(C.Structure):
+    _fields_ = [
+        ("n", C.c_int64),
+        ("vocab", C.c_int32),
+        ("max_tokens", C.c_int32),
+        ("step", C.c_int32),
+        ("staging_dtype", C.c_int32),
+        ("model_seed", C.c_uint64),
+        ("concentration", C.c_double),
+        ("logit_range", C.c_double),
+        ("d_start", C.c_void_p),
+        ("d_u_start", C.c_void_p),
+        ("d_digest_in", C.c_void_p),
+        ("d_digest_out", C.c_void_p),
+        ("d_out", C.c_void_p),
+        ("d_slot", C.c_void_p),
+        ("d_gen", C.c_void_p),
+        ("d_temperature", C.c_void_p),
+        ("d_top_k", C.c_void_p),
+        ("d_top_p", C.c_void_p),
+        ("d_staging", C.c_void_p),
+        ("staging_stride", C.c_int64),
+        ("d_tasks", C.c_void_p),
+    ]
+
+
 class LcCacheStats(C.Structure):
     _fields_ = [(n, C.c_int64) for n in (
         "entries", "total_bytes", "budget_bytes", "lookups", "hits", "inserts", "evictions", "clock",
@@ -94,6 +121,12 @@ _SIGS = {
     "lc_cache_lookup": (C.c_int, [P, P, I64, P, P, P, P, P]),
     "lc_cache_insert": (C.c_int, [P, P, P, P, I64, P, I32, I64, P, P, I32, P, P, P]),
     "lc_cache_pin": (C.c_int, [P, P, P, I64, I32, P]),
+    "lc_cache_writeback": (C.c_int, [P, P, P, P, P, P, I64, P, I32, I64, P, P, I32, P, P, P]),
+    "lc_cache_fill_rows": (C.c_int, [P, P, P, P, P, I64, D, D, P]),
+    "lc_cache_set_tokens": (C.c_int, [P, P, P, P, P, I64, P]),
+    "lc_cache_entry_len": (C.c_int, [P, P, P, I64, P, P]),
+    "lc_engine_fold": (C.c_int, [P, P, I64, P, I64, P, P]),
+    "lc_engine_decode_step": (C.c_int, [P, C.POINTER(LcDecodeStep), P]),
     "lc_cache_gather": (C.c_int, [P, P, P, P, I64, P, I32, I64, P]),
     "lc_cache_row_entropy": (C.c_int, [P, P, P, P, I64, C.c_double, P, P, P]),
     "lc_cache_tokens": (C.c_int, [P, P, P, P, I64, P, P]),
@@ -124,7 +157,7 @@ def _load():
         fn = getattr(lib, name)
         fn.restype = res
         fn.argtypes = args
-    if lib.lc_abi_version() != 2:
+    if lib.lc_abi_version() != ABI_VERSION:
         raise ImportError("liblcb200 ABI version mismatch")
     return lib
 
@@ -148,4 +181,6 @@ def check(rc: int, what: str = "") -> None:
         raise CapacityError(msg)
     if rc == LC_E_ARG:
         raise ValueError(msg)
+    if rc == LC_E_STATE:
+        raise RuntimeError(msg)
     raise RuntimeError(msg)

@@ -27,55 +27,11 @@
 #include <new>
 #include <vector>
 
+#include "lc_cache.cuh"
 #include "lc_common.cuh"
 #include "lc_resample.cuh"
 
 namespace lcb {
-
-struct Ctl {
-  long long total_bytes;
-  long long budget;
-  long long clock;
-  long long lookups;
-  long long hits;
-  long long inserts;
-  long long evictions;
-  long long ring_head;  // positions grow monotonically; index = pos % R
-  long long ring_tail;
-  int alive;
-  int free_slot_top;
-  int free_page_top;
-  int side_count;
-  int error;  // first lc_status raised inside a kernel (sticky until read)
-};
-
-struct CacheDev {
-  Ctl* ctl;
-  uint64_t* hkeys;
-  int32_t* hvals;  // slot, -1 empty
-  uint32_t hmask;
-  uint64_t* digest;
-  unsigned long long* last_hit;
-  uint32_t* gen;
-  int32_t* pins;
-  int32_t* nrows;
-  int32_t* vocab;
-  uint8_t* alive;
-  long long* nbytes;
-  int32_t* pages;       // [E][maxp]
-  int32_t* free_slots;  // stack
-  int32_t* free_pages;  // stack
-  int32_t* tokens;      // [P * page_rows]
-  char* slab;           // [P * page_rows * V] of dtype
-  unsigned long long* ring_clock;
-  int32_t* ring_slot;
-  long long R;  // power of two
-  long long rmask;
-  unsigned long long* side_clock;
-  int32_t* side_slot;
-  int side_cap;
-  int E, P, maxp, page_rows, V, dtype;
-};
 
 __device__ __forceinline__ uint32_t home_bucket(uint64_t d, uint32_t mask) {
   return (uint32_t)((d ^ (d >> 29) ^ (d >> 47)) & mask);
@@ -262,6 +218,28 @@ __device__ void push_pages(const CacheDev& c, int s) {
   }
 }
 
+// Overwrite: the old entry's pages are pushed in REVERSE page order, so the new entry's
+// pops (page 0 first) get them back in place -- page k of the new entry is page k of the
+// old one.  A write-back (engine.py:349-361) whose first `keep` rows are the replayed
+// prefix of the old entry therefore finds them where they are: no copy (DESIGN.md f3).
+__device__ void push_pages_rev(const CacheDev& c, int s) {
+  Ctl* ctl = c.ctl;
+  int np = 0;
+  while (np < c.maxp && c.pages[(int64_t)s * c.maxp + np] >= 0) ++np;
+  for (int k = np - 1; k >= 0; --k) {
+    c.free_pages[ctl->free_page_top++] = c.pages[(int64_t)s * c.maxp + k];
+    c.pages[(int64_t)s * c.maxp + k] = -1;
+  }
+}
+
+// keep[i] > 0 (write-back): the insert must overwrite the key's live entry whose generation
+// is keep_gen[i], with at least keep[i] rows of the same vocab; its first keep[i] rows stay
+// in place.  Anything else latches LC_E_STATE (the rows were not copied).
+__device__ __forceinline__ bool keep_ok(const CacheDev& c, bool overwrite, int s, uint32_t old_gen, int keep,
+                                        uint32_t want_gen, int nr, int vv) {
+  return overwrite && old_gen == want_gen && keep <= nr && c.nrows[s] >= keep && c.vocab[s] == vv;
+}
+
 __device__ void evict_entry(const CacheDev& c, int s) {
   Ctl* ctl = c.ctl;
   table_delete(c, c.digest[s]);
@@ -279,7 +257,8 @@ __device__ void evict_entry(const CacheDev& c, int s) {
 // rare fallbacks (pinned entries at the LRU end, long probe chains).
 __global__ void insert_policy_scalar_kernel(CacheDev c, const uint64_t* __restrict__ dig, const int32_t* __restrict__ lens,
                                      const int32_t* __restrict__ vocabs, int64_t n, int32_t* out_slot,
-                                     uint32_t* out_gen) {
+                                     uint32_t* out_gen, const int32_t* __restrict__ keep,
+                                     const uint32_t* __restrict__ keep_gen) {
   if (threadIdx.x != 0 || blockIdx.x != 0) return;
   Ctl* ctl = c.ctl;
   for (int64_t i = 0; i < n; ++i) {
@@ -295,9 +274,12 @@ __global__ void insert_policy_scalar_kernel(CacheDev c, const uint64_t* __restri
     }
     const long long bytes = (long long)nr * vv * 4 + 8ll * nr;  // logits_cache.py:54-56
     int s = table_find(c, d);
+    if (keep && keep[i] > 0 && !keep_ok(c, s >= 0, s, s >= 0 ? c.gen[s] : 0u, keep[i], keep_gen[i], nr, vv)) {
+      if (!ctl->error) ctl->error = LC_E_STATE;
+    }
     if (s >= 0) {  // overwrite: the key keeps its slot, the entry is new
       ctl->total_bytes -= c.nbytes[s];
-      push_pages(c, s);
+      push_pages_rev(c, s);
       c.gen[s] += 1u;
     } else {
       if (ctl->free_slot_top == 0) {
@@ -697,10 +679,32 @@ __device__ __forceinline__ void warp_push_pages(const CacheDev& c, Ctl& L, RegSt
   }
 }
 
+// Overwrite push (see push_pages_rev): pages np-1 .. 0 of entry s, so the pops that follow
+// return page 0 first.
+__device__ __forceinline__ void warp_push_pages_rev(const CacheDev& c, Ctl& L, RegStack& fp, int s, int lane,
+                                                    int known_pg = -2) {
+  if (c.maxp == 1) {
+    warp_push_pages(c, L, fp, s, lane, known_pg);
+    return;
+  }
+  const int nr = c.nrows[s];
+  const int np = min(c.maxp, (nr + c.page_rows - 1) / c.page_rows);
+  for (int k0 = 0; k0 < np; k0 += 32) {
+    const int m = min(32, np - k0);
+    const int k = np - 1 - (k0 + lane);
+    const int pg = lane < m ? c.pages[(int64_t)s * c.maxp + k] : -1;
+    if (lane < m) c.pages[(int64_t)s * c.maxp + k] = -1;
+    rs_push_many(fp, c.free_pages, L.free_page_top, m, pg, lane);
+    L.free_page_top += m;
+  }
+}
+
 __global__ void __launch_bounds__(32) insert_policy_kernel(CacheDev c, const uint64_t* __restrict__ dig,
                                                            const int32_t* __restrict__ lens,
                                                            const int32_t* __restrict__ vocabs, int64_t n,
-                                                           int32_t* out_slot, uint32_t* out_gen) {
+                                                           int32_t* out_slot, uint32_t* out_gen,
+                                                           const int32_t* __restrict__ keep,
+                                                           const uint32_t* __restrict__ keep_gen) {
   const int lane = threadIdx.x;
   Ctl L = *c.ctl;
   RegStack fs{-1ll << 40, 0u, 0}, fp{-1ll << 40, 0u, 0};
@@ -804,10 +808,16 @@ __global__ void __launch_bounds__(32) insert_policy_kernel(CacheDev c, const uin
           g = c.gen[s] + 1u;
         }
         mark_slot(s);
+        if (keep) {
+          const int i = (int)(i0 + j);
+          if (keep[i] > 0 && !keep_ok(c, true, s, g - 1u, keep[i], keep_gen[i], nr, vv) && !L.error)
+            L.error = LC_E_STATE;
+        }
         L.total_bytes -= onb;
-        warp_push_pages(c, L, fp, s, lane, opg);
+        warp_push_pages_rev(c, L, fp, s, lane, opg);
         if (lane == 0) c.gen[s] = g;
       } else {
+        if (keep && keep[i0 + j] > 0 && !L.error) L.error = LC_E_STATE;  // write-back of a gone entry
         if (L.free_slot_top == 0) {
           if (!L.error) L.error = LC_E_CAPACITY;
           continue;
@@ -925,17 +935,20 @@ template <typename SrcT, typename DstT>
 __global__ void insert_copy_kernel(CacheDev c, const int32_t* __restrict__ lens, const int32_t* __restrict__ vocabs,
                                    const char* __restrict__ src, int64_t src_stride, const int64_t* __restrict__ offs,
                                    const int32_t* __restrict__ toks, const int32_t* __restrict__ out_slot,
-                                   const uint32_t* __restrict__ out_gen, int64_t i0) {
+                                   const uint32_t* __restrict__ out_gen, int64_t i0,
+                                   const int32_t* __restrict__ keep) {
   const int64_t i = i0 + blockIdx.y;
   const int s = out_slot[i];
   if (s < 0 || !c.alive[s] || c.gen[s] != out_gen[i]) return;
   const int nr = lens[i], vv = vocabs[i];
+  const int kp = keep ? keep[i] : 0;
   for (int t = blockIdx.x; t < nr; t += gridDim.x) {
     const int pg = c.pages[(int64_t)s * c.maxp + t / c.page_rows];
     const int64_t slab_row = (int64_t)pg * c.page_rows + t % c.page_rows;
+    if (threadIdx.x == 0 && (toks || t >= kp)) c.tokens[slab_row] = toks ? toks[offs[i] + t] : 0;
+    if (t < kp || !src) continue;  // replayed prefix in place / rows written later by the producer
     const SrcT* srow = reinterpret_cast<const SrcT*>(src) + (offs[i] + t) * src_stride;
     DstT* drow = reinterpret_cast<DstT*>(c.slab) + slab_row * (int64_t)c.V;
-    if (threadIdx.x == 0) c.tokens[slab_row] = toks ? toks[offs[i] + t] : 0;
     const bool same = sizeof(SrcT) == sizeof(DstT);
     const bool al = ((reinterpret_cast<uintptr_t>(srow) | reinterpret_cast<uintptr_t>(drow)) & 15) == 0;
     if (same && al) {
@@ -965,12 +978,6 @@ __global__ void pin_kernel(CacheDev c, const int32_t* __restrict__ slot, const u
   int s = slot[i];
   if (s < 0 || s >= c.E) return;
   if (c.alive[s] && c.gen[s] == gen[i]) atomicAdd(&c.pins[s], delta);
-}
-
-// (slot, pos[, gen]) names a live row: a handle whose entry was overwritten or evicted
-// (generation moved on) reads nothing
-__device__ __forceinline__ bool row_live(const CacheDev& c, int s, int t, const uint32_t* gen, int64_t i) {
-  return s >= 0 && s < c.E && c.alive[s] && (!gen || c.gen[s] == gen[i]) && t >= 0 && t < c.nrows[s];
 }
 
 template <typename DstT>
@@ -1077,6 +1084,11 @@ struct lc_cache {
   long long ring_bound;  // host upper bound of ring occupancy
   std::vector<void*> allocs;
 };
+
+namespace lcb {
+// device view of a handle, for kernels in other translation units (lc_engine.cu)
+const CacheDev* cache_dev(const lc_cache* c) { return c ? &c->dev : nullptr; }
+}  // namespace lcb
 
 static int cache_alloc(lc_cache* c, void** p, size_t bytes) {
   cudaError_t e = cudaMalloc(p, bytes ? bytes : 16);
@@ -1223,6 +1235,47 @@ extern "C" int lc_cache_lookup(lc_cache* c, const uint64_t* d_digests, int64_t n
   return LC_OK;
 }
 
+static int insert_impl(lc_cache* c, const uint64_t* d_digests, const int32_t* d_lengths, const int32_t* d_vocabs,
+                       int64_t n, const void* d_rows, int32_t rows_dtype, int64_t rows_stride,
+                       const int64_t* d_row_offsets, const int32_t* d_tokens, int32_t max_len, int32_t* d_slot,
+                       uint32_t* d_gen, const int32_t* d_keep, const uint32_t* d_keep_gen, cudaStream_t st) {
+  int rc = ensure_ring(c, n, st);
+  if (rc) return rc;
+  const char* sp = getenv("LCB_SCALAR_POLICY");  // A/B hook, read per call (tests switch it)
+  const bool scalar = sp && atoi(sp) != 0;
+  if (scalar)
+    insert_policy_scalar_kernel<<<1, 32, 0, st>>>(c->dev, d_digests, d_lengths, d_vocabs, n, d_slot, d_gen, d_keep,
+                                                  d_keep_gen);
+  else
+    insert_policy_kernel<<<1, 32, 0, st>>>(c->dev, d_digests, d_lengths, d_vocabs, n, d_slot, d_gen, d_keep,
+                                           d_keep_gen);
+  LCB_CUDA_TRY(cudaGetLastError());
+  c->ring_bound += n;
+  if (max_len > 0 && (d_rows || d_tokens)) {
+    const int bx = max_len < 64 ? max_len : 64;
+    for (int64_t i0 = 0; i0 < n; i0 += 65535) {
+      const int ny = (int)((n - i0) < 65535 ? (n - i0) : 65535);
+      dim3 grid(bx, ny);
+      const char* src = (const char*)d_rows;
+      if (rows_dtype == LC_F32 && c->cfg.dtype == LC_F32)
+        insert_copy_kernel<float, float><<<grid, 256, 0, st>>>(c->dev, d_lengths, d_vocabs, src, rows_stride,
+                                                               d_row_offsets, d_tokens, d_slot, d_gen, i0, d_keep);
+      else if (rows_dtype == LC_F32)
+        insert_copy_kernel<float, uint16_t><<<grid, 256, 0, st>>>(c->dev, d_lengths, d_vocabs, src, rows_stride,
+                                                                  d_row_offsets, d_tokens, d_slot, d_gen, i0, d_keep);
+      else if (c->cfg.dtype == LC_BF16)
+        insert_copy_kernel<uint16_t, uint16_t><<<grid, 256, 0, st>>>(c->dev, d_lengths, d_vocabs, src, rows_stride,
+                                                                     d_row_offsets, d_tokens, d_slot, d_gen, i0,
+                                                                     d_keep);
+      else
+        insert_copy_kernel<uint16_t, float><<<grid, 256, 0, st>>>(c->dev, d_lengths, d_vocabs, src, rows_stride,
+                                                                  d_row_offsets, d_tokens, d_slot, d_gen, i0, d_keep);
+      LCB_CUDA_TRY(cudaGetLastError());
+    }
+  }
+  return LC_OK;
+}
+
 extern "C" int lc_cache_insert(lc_cache* c, const uint64_t* d_digests, const int32_t* d_lengths,
                                const int32_t* d_vocabs, int64_t n, const void* d_rows, int32_t rows_dtype,
                                int64_t rows_stride, const int64_t* d_row_offsets, const int32_t* d_tokens,
@@ -1232,38 +1285,96 @@ extern "C" int lc_cache_insert(lc_cache* c, const uint64_t* d_digests, const int
   if (!d_digests || !d_lengths || !d_vocabs || !d_slot || !d_gen || !d_row_offsets) return LC_E_ARG;
   if (max_len > 0 && !d_rows) return LC_E_ARG;
   if (rows_dtype != LC_F32 && rows_dtype != LC_BF16) return LC_E_ARG;
-  cudaStream_t st = (cudaStream_t)stream;
-  int rc = ensure_ring(c, n, st);
-  if (rc) return rc;
-  const char* sp = getenv("LCB_SCALAR_POLICY");  // A/B hook, read per call (tests switch it)
-  const bool scalar = sp && atoi(sp) != 0;
-  if (scalar)
-    insert_policy_scalar_kernel<<<1, 32, 0, st>>>(c->dev, d_digests, d_lengths, d_vocabs, n, d_slot, d_gen);
-  else
-    insert_policy_kernel<<<1, 32, 0, st>>>(c->dev, d_digests, d_lengths, d_vocabs, n, d_slot, d_gen);
+  return insert_impl(c, d_digests, d_lengths, d_vocabs, n, d_rows, rows_dtype, rows_stride, d_row_offsets, d_tokens,
+                     max_len, d_slot, d_gen, nullptr, nullptr, (cudaStream_t)stream);
+}
+
+extern "C" int lc_cache_writeback(lc_cache* c, const uint64_t* d_digests, const int32_t* d_lengths,
+                                  const int32_t* d_vocabs, const int32_t* d_keep, const uint32_t* d_keep_gen,
+                                  int64_t n, const void* d_rows, int32_t rows_dtype, int64_t rows_stride,
+                                  const int64_t* d_row_offsets, const int32_t* d_tokens, int32_t max_len,
+                                  int32_t* d_slot, uint32_t* d_gen, void* stream) {
+  if (!c || n < 0) return LC_E_ARG;
+  if (n == 0) return LC_OK;
+  if (!d_digests || !d_lengths || !d_vocabs || !d_keep || !d_keep_gen || !d_slot || !d_gen) return LC_E_ARG;
+  if ((d_rows || d_tokens) && !d_row_offsets) return LC_E_ARG;
+  if (rows_dtype != LC_F32 && rows_dtype != LC_BF16) return LC_E_ARG;
+  return insert_impl(c, d_digests, d_lengths, d_vocabs, n, d_rows, rows_dtype, rows_stride, d_row_offsets, d_tokens,
+                     max_len, d_slot, d_gen, d_keep, d_keep_gen, (cudaStream_t)stream);
+}
+
+// f1: the synthetic producer writing straight into cached rows (slot, pos) of live entries
+// (model.py:67-83, kernels.py:47-60): no staging row, no insert copy.
+template <typename OutT>
+__global__ void fill_rows_kernel(CacheDev c, const int32_t* __restrict__ slot, const uint32_t* __restrict__ gen,
+                                 const int32_t* __restrict__ pos, const uint64_t* __restrict__ states, int64_t n,
+                                 double conc, double range) {
+  const int64_t i = blockIdx.y;
+  if (i >= n) return;
+  const int s = slot[i], t = pos[i];
+  if (!row_live(c, s, t, gen, i)) return;
+  const int64_t vocab = c.vocab[s];
+  const int64_t slab_row = (int64_t)c.pages[(int64_t)s * c.maxp + t / c.page_rows] * c.page_rows + t % c.page_rows;
+  OutT* o = reinterpret_cast<OutT*>(c.slab) + slab_row * (int64_t)c.V;
+  const uint64_t st = states[i];
+  const uint64_t peak = avalanche64(st ^ kPeakSalt) % (uint64_t)vocab;
+  const float boost = (float)__dmul_rn(conc, range);
+  for (int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; v < vocab; v += (int64_t)gridDim.x * blockDim.x)
+    o[v] = producer_value<OutT>(st, v, peak, boost, range);
+}
+
+__global__ void set_tokens_kernel(CacheDev c, const int32_t* __restrict__ slot, const uint32_t* __restrict__ gen,
+                                  const int32_t* __restrict__ pos, const int32_t* __restrict__ tok, int64_t n) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const int s = slot[i], t = pos[i];
+  if (!row_live(c, s, t, gen, i)) return;
+  c.tokens[(int64_t)c.pages[(int64_t)s * c.maxp + t / c.page_rows] * c.page_rows + t % c.page_rows] = tok[i];
+}
+
+__global__ void entry_len_kernel(CacheDev c, const int32_t* __restrict__ slot, const uint32_t* __restrict__ gen,
+                                 int64_t n, int32_t* __restrict__ out) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const int s = slot[i];
+  out[i] = (s >= 0 && s < c.E && c.alive[s] && c.gen[s] == gen[i]) ? c.nrows[s] : -1;
+}
+
+extern "C" int lc_cache_entry_len(lc_cache* c, const int32_t* d_slot, const uint32_t* d_gen, int64_t n,
+                                  int32_t* d_len, void* stream) {
+  if (!c || n < 0 || (n > 0 && (!d_slot || !d_gen || !d_len))) return LC_E_ARG;
+  if (n == 0) return LC_OK;
+  entry_len_kernel<<<ceil_div(n, 256), 256, 0, (cudaStream_t)stream>>>(c->dev, d_slot, d_gen, n, d_len);
   LCB_CUDA_TRY(cudaGetLastError());
-  c->ring_bound += n;
-  if (max_len > 0) {
-    const int bx = max_len < 64 ? max_len : 64;
-    for (int64_t i0 = 0; i0 < n; i0 += 65535) {
-      const int ny = (int)((n - i0) < 65535 ? (n - i0) : 65535);
-      dim3 grid(bx, ny);
-      const char* src = (const char*)d_rows;
-      if (rows_dtype == LC_F32 && c->cfg.dtype == LC_F32)
-        insert_copy_kernel<float, float><<<grid, 256, 0, st>>>(c->dev, d_lengths, d_vocabs, src, rows_stride,
-                                                               d_row_offsets, d_tokens, d_slot, d_gen, i0);
-      else if (rows_dtype == LC_F32)
-        insert_copy_kernel<float, uint16_t><<<grid, 256, 0, st>>>(c->dev, d_lengths, d_vocabs, src, rows_stride,
-                                                                  d_row_offsets, d_tokens, d_slot, d_gen, i0);
-      else if (c->cfg.dtype == LC_BF16)
-        insert_copy_kernel<uint16_t, uint16_t><<<grid, 256, 0, st>>>(c->dev, d_lengths, d_vocabs, src, rows_stride,
-                                                                     d_row_offsets, d_tokens, d_slot, d_gen, i0);
-      else
-        insert_copy_kernel<uint16_t, float><<<grid, 256, 0, st>>>(c->dev, d_lengths, d_vocabs, src, rows_stride,
-                                                                  d_row_offsets, d_tokens, d_slot, d_gen, i0);
-      LCB_CUDA_TRY(cudaGetLastError());
-    }
+  return LC_OK;
+}
+
+extern "C" int lc_cache_fill_rows(lc_cache* c, const int32_t* d_slot, const uint32_t* d_gen, const int32_t* d_pos,
+                                  const uint64_t* d_states, int64_t n, double concentration, double logit_range,
+                                  void* stream) {
+  if (!c || n < 0 || (n > 0 && (!d_slot || !d_gen || !d_pos || !d_states))) return LC_E_ARG;
+  cudaStream_t st = (cudaStream_t)stream;
+  for (int64_t i0 = 0; i0 < n; i0 += 65535) {
+    const int ny = (int)((n - i0) < 65535 ? (n - i0) : 65535);
+    const int bx = (int)(ceil_div(c->cfg.vocab, 256) < 32 ? ceil_div(c->cfg.vocab, 256) : 32);
+    dim3 grid(bx, ny);
+    if (c->cfg.dtype == LC_F32)
+      fill_rows_kernel<float><<<grid, 256, 0, st>>>(c->dev, d_slot + i0, d_gen + i0, d_pos + i0, d_states + i0, ny,
+                                                    concentration, logit_range);
+    else
+      fill_rows_kernel<uint16_t><<<grid, 256, 0, st>>>(c->dev, d_slot + i0, d_gen + i0, d_pos + i0, d_states + i0, ny,
+                                                       concentration, logit_range);
+    LCB_CUDA_TRY(cudaGetLastError());
   }
+  return LC_OK;
+}
+
+extern "C" int lc_cache_set_tokens(lc_cache* c, const int32_t* d_slot, const uint32_t* d_gen, const int32_t* d_pos,
+                                   const int32_t* d_tokens, int64_t n, void* stream) {
+  if (!c || n < 0 || (n > 0 && (!d_slot || !d_gen || !d_pos || !d_tokens))) return LC_E_ARG;
+  if (n == 0) return LC_OK;
+  set_tokens_kernel<<<ceil_div(n, 256), 256, 0, (cudaStream_t)stream>>>(c->dev, d_slot, d_gen, d_pos, d_tokens, n);
+  LCB_CUDA_TRY(cudaGetLastError());
   return LC_OK;
 }
 

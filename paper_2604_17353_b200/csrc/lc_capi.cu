@@ -22,6 +22,7 @@ extern "C" const char* lc_status_string(int status) {
     case LC_E_CAPACITY: return "capacity exhausted";
     case LC_E_CUDA: return "CUDA error";
     case LC_E_ARG: return "bad argument";
+    case LC_E_STATE: return "write-back prefix no longer live";
     default: return "unknown status";
   }
 }

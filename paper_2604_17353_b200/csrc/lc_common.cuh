@@ -36,6 +36,9 @@ __host__ __device__ __forceinline__ double unit_float(uint64_t u) {
   return (double)(u >> 11) * 0x1.0p-53;  // exact: 53-bit integer times 2^-53
 }
 
+// mix2(a, b) = avalanche64(avalanche64(a) ^ b)  (mixing.py:76-78)
+__host__ __device__ __forceinline__ uint64_t mix2(uint64_t a, uint64_t b) { return avalanche64(avalanche64(a) ^ b); }
+
 __host__ __device__ __forceinline__ uint64_t fold_token(uint64_t h, int64_t t) {
   return avalanche64(h ^ (uint64_t)(t + 1));
 }
@@ -57,6 +60,19 @@ __device__ __forceinline__ uint16_t f32_to_bf16_bits(float f) {
   if ((u & 0x7fffffffu) > 0x7f800000u) return (uint16_t)((u >> 16) | 0x40);
   u += 0x7fffu + ((u >> 16) & 1u);
   return (uint16_t)(u >> 16);
+}
+
+// One element of the synthetic producer row (kernels.py:47-60, _mixcore.pyx:27-40):
+// base_v = f32((2*unit_float(stream_u64(state, v)) - 1) * r) evaluated in f64 (no FMA
+// contraction: __dmul_rn/__dsub_rn keep the reference's two roundings), then the peak
+// element += f32(c*r) in f32; bf16 outputs are the RNE of that fp32 value.
+template <typename OutT>
+__device__ __forceinline__ OutT producer_value(uint64_t st, int64_t v, uint64_t peak, float boost, double range) {
+  const double x = unit_float(stream_u64(st, (uint64_t)v));
+  float f = (float)__dmul_rn(__dsub_rn(__dmul_rn(2.0, x), 1.0), range);
+  if ((uint64_t)v == peak) f = __fadd_rn(f, boost);
+  if constexpr (sizeof(OutT) == 4) return f;
+  else return f32_to_bf16_bits(f);
 }
 
 // Monotone map float -> uint32 (larger float -> larger key; -0 < +0 handled as

@@ -48,16 +48,8 @@ __global__ void fill_logits_kernel(const uint64_t* __restrict__ states, int64_t 
   uint64_t peak = avalanche64(st ^ kPeakSalt) % (uint64_t)vocab;
   float boost = (float)__dmul_rn(conc, range);
   OutT* o = out + row * stride;
-  for (int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; v < vocab; v += (int64_t)gridDim.x * blockDim.x) {
-    double x = unit_float(stream_u64(st, (uint64_t)v));
-    float f = (float)__dmul_rn(__dsub_rn(__dmul_rn(2.0, x), 1.0), range);
-    if ((uint64_t)v == peak) f = __fadd_rn(f, boost);
-    if constexpr (sizeof(OutT) == 4) {
-      o[v] = f;
-    } else {
-      o[v] = f32_to_bf16_bits(f);
-    }
-  }
+  for (int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; v < vocab; v += (int64_t)gridDim.x * blockDim.x)
+    o[v] = producer_value<OutT>(st, v, peak, boost, range);
 }
 
 }  // namespace lcb

@@ -222,6 +222,8 @@ class LogitsCache:
             code = int(st.error)
             if code == _capi.LC_E_CONFIG:
                 raise ConfigError("entry wider than the slab or longer than max_rows")
+            if code == _capi.LC_E_STATE:
+                raise RuntimeError("write-back: the replayed prefix is no longer the key's live entry")
             raise CapacityError("logits cache slots/pages exhausted")
         return st
 
@@ -340,22 +342,56 @@ class LogitsCache:
         the device.  Returns (tokens [n_req*max_pos*n_branch], replayed_len
         [n_req*n_branch], diverged_at, slot, len).  ``kept`` (int32 [n_req*max_pos],
         optional) receives each position's kept-set size (sampling.resample)."""
-        n_req = digests.numel()
         slot, gen, ln, vv = self.lookup_batch(digests)
+        tok, rep, div = self.replay_looked_up(slot, gen, ln, vv, max_pos, n_branch, seeds, temperature, top_k, top_p,
+                                              counters=counters, bufs=bufs, kept=kept)
+        return tok, rep, div, slot, ln
+
+    def replay_looked_up(self, slot, gen, ln, vv, max_pos: int, n_branch: int, seeds: torch.Tensor,
+                         temperature: torch.Tensor, top_k: torch.Tensor, top_p: torch.Tensor, counters=None,
+                         bufs: dict | None = None, kept: torch.Tensor | None = None, draw_index=None,
+                         hot_list=None):
+        """The replay of ``replay_stepwise`` / ``replay_hotspot`` (``draw_index`` given) on
+        lookup results the caller already holds (slot -1 = no replay; len capped at max_pos).
+        Returns (tokens, replayed_len, diverged_at) device tensors."""
+        n_req = slot.numel()
         b = self._replay_bufs(bufs, n_req, max_pos, n_branch)
         ntask = n_req * max_pos
         ndraw = ntask * n_branch
         st = self._stream()
-        _capi.check(_capi.lib.lc_replay_tasks(slot.data_ptr(), ln.data_ptr(), vv.data_ptr(), n_req, max_pos,
-                                              n_branch, temperature.data_ptr(), top_k.data_ptr(), top_p.data_ptr(),
-                                              b["tasks"].data_ptr(), st), "lc_replay_tasks")
-        tok, flags = sampling.resample(None, b["tasks"], seeds=seeds, n_draws=ndraw, cache=self, counters=counters,
-                                       out=(b["tok"], b["flags"]), kept=kept)
+        if draw_index is None:
+            _capi.check(_capi.lib.lc_replay_tasks(slot.data_ptr(), ln.data_ptr(), vv.data_ptr(), n_req, max_pos,
+                                                  n_branch, temperature.data_ptr(), top_k.data_ptr(),
+                                                  top_p.data_ptr(), b["tasks"].data_ptr(), st), "lc_replay_tasks")
+            ntask_run = ntask
+        elif hot_list is not None:  # only the hotspot positions become tasks
+            hp, hd = hot_list
+            ntask_run = hp.numel()
+            _capi.check(_capi.lib.lc_replay_tasks_hotspot_list(slot.data_ptr(), ln.data_ptr(), vv.data_ptr(),
+                                                               hp.data_ptr(), hd.data_ptr(), ntask_run, max_pos,
+                                                               n_branch, temperature.data_ptr(), top_k.data_ptr(),
+                                                               top_p.data_ptr(), b["tasks"].data_ptr(), st),
+                        "lc_replay_tasks_hotspot_list")
+        else:
+            _capi.check(_capi.lib.lc_replay_tasks_hotspot(slot.data_ptr(), ln.data_ptr(), vv.data_ptr(),
+                                                          draw_index.data_ptr(), n_req, max_pos, n_branch,
+                                                          temperature.data_ptr(), top_k.data_ptr(), top_p.data_ptr(),
+                                                          b["tasks"].data_ptr(), st), "lc_replay_tasks_hotspot")
+            ntask_run = ntask
+        tok, flags = sampling.resample(None, b["tasks"][: ntask_run * _capi.TASK_DTYPE.itemsize], seeds=seeds,
+                                       n_draws=ndraw, cache=self, counters=counters, out=(b["tok"], b["flags"]),
+                                       kept=kept)
         self._cached_tokens(slot, gen, b, st)
-        _capi.check(_capi.lib.lc_replay_accept(tok.data_ptr(), b["cached"].data_ptr(), ln.data_ptr(), n_req, max_pos,
-                                               n_branch, b["rep"].data_ptr(), b["div"].data_ptr(), st),
-                    "lc_replay_accept")
-        return tok, b["rep"], b["div"], slot, ln
+        if draw_index is None:
+            _capi.check(_capi.lib.lc_replay_accept(tok.data_ptr(), b["cached"].data_ptr(), ln.data_ptr(), n_req,
+                                                   max_pos, n_branch, b["rep"].data_ptr(), b["div"].data_ptr(), st),
+                        "lc_replay_accept")
+        else:
+            _capi.check(_capi.lib.lc_replay_accept_hotspot(tok.data_ptr(), b["cached"].data_ptr(), ln.data_ptr(),
+                                                           draw_index.data_ptr(), n_req, max_pos, n_branch,
+                                                           b["rep"].data_ptr(), b["div"].data_ptr(), st),
+                        "lc_replay_accept_hotspot")
+        return tok, b["rep"], b["div"]
 
     def _replay_bufs(self, bufs, n_req: int, max_pos: int, n_branch: int) -> dict:
         """Device buffers of a replay call, reused across calls of the same shape (a
@@ -413,44 +449,17 @@ class LogitsCache:
         that differs from the cache.  Same returns as ``replay_stepwise``; the token array
         holds the engine's ``out`` tokens at every replayed position."""
         n_req = digests.numel()
-        d = self.dev
         if draw_index is None:
             if hotspots is None or len(hotspots) != n_req:
                 raise ConfigError("one hotspot tuple per request")
-            d_di = self.hotspot_draw_index(hotspots, max_pos, d)
-        else:
-            if draw_index.numel() != n_req * max_pos:
-                raise ConfigError("draw_index must hold n_req * max_pos entries")
-            d_di = draw_index
+            draw_index = self.hotspot_draw_index(hotspots, max_pos, self.dev)
+        elif draw_index.numel() != n_req * max_pos:
+            raise ConfigError("draw_index must hold n_req * max_pos entries")
         slot, gen, ln, vv = self.lookup_batch(digests)
-        b = self._replay_bufs(bufs, n_req, max_pos, n_branch)
-        ntask = n_req * max_pos
-        ndraw = ntask * n_branch
-        st = self._stream()
-        if hot_list is not None:  # only the hotspot positions become tasks
-            hp, hd = hot_list
-            n_hot = hp.numel()
-            _capi.check(_capi.lib.lc_replay_tasks_hotspot_list(slot.data_ptr(), ln.data_ptr(), vv.data_ptr(),
-                                                               hp.data_ptr(), hd.data_ptr(), n_hot, max_pos, n_branch,
-                                                               temperature.data_ptr(), top_k.data_ptr(),
-                                                               top_p.data_ptr(), b["tasks"].data_ptr(), st),
-                        "lc_replay_tasks_hotspot_list")
-            ntask_run = n_hot
-        else:
-            _capi.check(_capi.lib.lc_replay_tasks_hotspot(slot.data_ptr(), ln.data_ptr(), vv.data_ptr(),
-                                                          d_di.data_ptr(), n_req, max_pos, n_branch,
-                                                          temperature.data_ptr(), top_k.data_ptr(), top_p.data_ptr(),
-                                                          b["tasks"].data_ptr(), st), "lc_replay_tasks_hotspot")
-            ntask_run = ntask
-        tok, flags = sampling.resample(None, b["tasks"][: ntask_run * _capi.TASK_DTYPE.itemsize], seeds=seeds,
-                                       n_draws=ndraw, cache=self, counters=counters, out=(b["tok"], b["flags"]),
-                                       kept=kept)
-        self._cached_tokens(slot, gen, b, st)
-        _capi.check(_capi.lib.lc_replay_accept_hotspot(tok.data_ptr(), b["cached"].data_ptr(), ln.data_ptr(),
-                                                       d_di.data_ptr(), n_req, max_pos, n_branch,
-                                                       b["rep"].data_ptr(), b["div"].data_ptr(), st),
-                    "lc_replay_accept_hotspot")
-        return tok, b["rep"], b["div"], slot, ln
+        tok, rep, div = self.replay_looked_up(slot, gen, ln, vv, max_pos, n_branch, seeds, temperature, top_k, top_p,
+                                              counters=counters, bufs=bufs, kept=kept, draw_index=draw_index,
+                                              hot_list=hot_list)
+        return tok, rep, div, slot, ln
 
     # -- reference API --------------------------------------------------------------------
 

@@ -43,7 +43,8 @@ def test_exports_are_exactly_the_header(tmp_path):
 def test_abi_version_and_status_strings():
     from paper_2604_17353_b200 import _capi
 
-    assert _capi.lib.lc_abi_version() == 2
+    assert _capi.lib.lc_abi_version() == 3
+    assert _capi.lib.lc_status_string(6) == b"write-back prefix no longer live"
     assert _capi.lib.lc_status_string(0) == b"ok"
     assert _capi.lib.lc_status_string(1) == b"config error"
 
@@ -60,6 +61,10 @@ def test_struct_layouts_match_header():
     fields = re.findall(r"^\s+\w+_t\s+(\w+);|^\s+double\s+(\w+);", body, re.M)
     names = [a or b for a, b in fields]
     assert names == [f[0] for f in _capi.LcTask._fields_]
+    body = src[src.index("typedef struct lc_decode_step {"): src.index("} lc_decode_step;")]
+    names = re.findall(r"^\s+(?:const\s+)?\w+\*?\s+\*?(\w+);", body, re.M)
+    assert names == [f[0] for f in _capi.LcDecodeStep._fields_]
+    assert C.sizeof(_capi.LcDecodeStep) == 8 + 4 * 4 + 8 * 3 + 8 * 13
 
 
 def test_workspace_query_needs_no_gpu():
