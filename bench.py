@@ -224,16 +224,14 @@ def run_ours(args, cfg, rank, world, dev):
 
     hot_rows = n_rows
     if args.policy == "hotspot":  # ReplayPolicy.HOTSPOT: hotspots per entry (memoised, untimed like the reference)
-        cfg_s = lcb.SamplingConfig(temperature=cfg["T"], top_k=cfg["k"] or None, top_p=cfg["p"], max_tokens=R)
+        # hotspot scores kept beside the rows + selection on the device (lc_cache_score_rows /
+        # lc_cache_hotspots), no row or score leaves the GPU
         hp = lcb.HotspotParams(decay=0.001, threshold=0.6)
-        dig_h = lcb._dev.u64_numpy(w["digests"])
-        hots = []
-        for dg in dig_h:
-            e = cache.lookup(lcb.StateKey(int(dg)))
-            hots.append(cache.hotspots_for(e, cfg_s, hp))
-        d_di = cache.hotspot_draw_index(hots, R, dev)
+        slot0, gen0, _, _ = cache.lookup_batch(w["digests"])
+        d_di, n_hot, hs_flags = cache.hotspot_draw_index_device(slot0, gen0, R, cfg["T"], hp)
         hot_l = cache.hotspot_list(d_di)
-        hot_rows = sum(len(h) for h in hots)
+        hot_rows = int(n_hot.sum().item())
+        hotspot_uncertain = int((hs_flags & 1).sum().item())
 
         def step():
             return cache.replay_hotspot(w["digests"], R, nb, w["seeds"], w["T"], w["K"], w["P"], counters=counters,
@@ -392,7 +390,8 @@ def run_ours(args, cfg, rank, world, dev):
         "dtype": "bf16" if esz == 2 else "f32",
         "data": "synthetic (reference producer fill_logits, seed 7, conc 2.5, range 5.0)",
         "config": {**workload_config(args, CONFIGS[args.config], world),
-                   **({"hotspot_rows": hot_rows} if args.policy == "hotspot" else {})},
+                   **({"hotspot_rows": hot_rows, "hotspot_uncertain_entries": hotspot_uncertain}
+                      if args.policy == "hotspot" else {})},
         "accepted_tokens_per_s": accepted / (ms * 1e-3),
         "rows_per_s": (n_rows * world if cfg["scaling"] == "weak" else CONFIGS[args.config]["n_req"] * R)
         * args.steps / (ms * 1e-3),

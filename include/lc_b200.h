@@ -249,6 +249,24 @@ int lc_cache_tokens(lc_cache* cache, const int32_t* d_slot, const int32_t* d_pos
 int lc_cache_row_entropy(lc_cache* cache, const int32_t* d_slot, const int32_t* d_pos, const uint32_t* d_gen, int64_t n,
                          double temperature, double* d_entropy, double* d_pmax, void* stream);
 
+/* Hotspot scores kept beside the cached rows (sampling.py:112-130):
+ * b = H * (1 - pmax) of softmax(z / T) for rows (slot, pos) of live entries, with a
+ * bound on its distance to the reference's numpy evaluation; only_stale != 0 skips
+ * rows already scored at this T (a row write makes its score stale).              */
+int lc_cache_score_rows(lc_cache* cache, const int32_t* d_slot, const uint32_t* d_gen, const int32_t* d_pos, int64_t n,
+                        double temperature, int32_t only_stale, void* stream);
+
+/* Hotspot selection (select_hotspots over the entry's scores, sampling.py:133-160 /
+ * hotspots_for, logits_cache.py:153-163) for n entries, on the device: rows must be
+ * scored at `temperature` (lc_cache_score_rows).  Per entry r: d_draw_index[r*max_pos
+ * + t] = number of hotspots before t when t is a hotspot, else -1 (the layout of
+ * lc_replay_tasks_hotspot; may be NULL), d_n_hot[r] = hotspot count, d_flags[r]: 1 =
+ * a decision within the score bounds of the threshold / cap (undecidable against the
+ * reference), 2 = some row not scored at T, 4 = dead handle.  max_hotspots < 0: none. */
+int lc_cache_hotspots(lc_cache* cache, const int32_t* d_slot, const uint32_t* d_gen, int64_t n_entries, int32_t max_pos,
+                      double temperature, double decay, double threshold, int32_t max_hotspots, int32_t* d_draw_index,
+                      int32_t* d_n_hot, uint8_t* d_flags, void* stream);
+
 /* Resample cached rows: tasks use (slot, pos) with row = -1. */
 int lc_cache_resample(lc_cache* cache, const lc_task* d_tasks, int64_t n_tasks, lc_draws draws, void* d_workspace,
                       int64_t workspace_bytes, int64_t* d_counters, void* stream);

@@ -125,6 +125,8 @@ _SIGS = {
     "lc_cache_fill_rows": (C.c_int, [P, P, P, P, P, I64, D, D, P]),
     "lc_cache_set_tokens": (C.c_int, [P, P, P, P, P, I64, P]),
     "lc_cache_entry_len": (C.c_int, [P, P, P, I64, P, P]),
+    "lc_cache_score_rows": (C.c_int, [P, P, P, P, I64, D, I32, P]),
+    "lc_cache_hotspots": (C.c_int, [P, P, P, I64, I32, D, D, D, I32, P, P, P, P]),
     "lc_engine_fold": (C.c_int, [P, P, I64, P, I64, P, P]),
     "lc_engine_decode_step": (C.c_int, [P, C.POINTER(LcDecodeStep), P]),
     "lc_cache_gather": (C.c_int, [P, P, P, P, I64, P, I32, I64, P]),

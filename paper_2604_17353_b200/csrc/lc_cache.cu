@@ -946,7 +946,8 @@ __global__ void insert_copy_kernel(CacheDev c, const int32_t* __restrict__ lens,
     const int pg = c.pages[(int64_t)s * c.maxp + t / c.page_rows];
     const int64_t slab_row = (int64_t)pg * c.page_rows + t % c.page_rows;
     if (threadIdx.x == 0 && (toks || t >= kp)) c.tokens[slab_row] = toks ? toks[offs[i] + t] : 0;
-    if (t < kp || !src) continue;  // replayed prefix in place / rows written later by the producer
+    if (t < kp || !src) continue;
+    if (threadIdx.x == 0) invalidate_score(c, slab_row);  // replayed prefix in place / rows written later by the producer
     const SrcT* srow = reinterpret_cast<const SrcT*>(src) + (offs[i] + t) * src_stride;
     DstT* drow = reinterpret_cast<DstT*>(c.slab) + slab_row * (int64_t)c.V;
     const bool same = sizeof(SrcT) == sizeof(DstT);
@@ -1065,6 +1066,7 @@ __global__ void init_kernel(CacheDev c) {
   }
   for (int64_t k = i; k < (int64_t)c.E * c.maxp; k += stride) c.pages[k] = -1;
   for (int64_t k = i; k < c.P; k += stride) c.free_pages[k] = c.P - 1 - (int)k;
+  for (int64_t k = i; k < (int64_t)c.P * c.page_rows; k += stride) invalidate_score(c, k);
 }
 
 }  // namespace lcb
@@ -1167,6 +1169,9 @@ extern "C" int lc_cache_create(const lc_cache_config* cfg, lc_cache** out) {
   ALLOC(d.free_slots, d.E);
   ALLOC(d.free_pages, d.P);
   ALLOC(d.tokens, (int64_t)d.P * d.page_rows);
+  ALLOC(d.score, (int64_t)d.P * d.page_rows);
+  ALLOC(d.score_err, (int64_t)d.P * d.page_rows);
+  ALLOC(d.score_T, (int64_t)d.P * d.page_rows);
   rc = cache_alloc(c, (void**)&d.slab, (size_t)d.P * d.page_rows * d.V * esz);
   if (rc) {
     lc_cache_destroy(c);
@@ -1316,6 +1321,7 @@ __global__ void fill_rows_kernel(CacheDev c, const int32_t* __restrict__ slot, c
   const int64_t vocab = c.vocab[s];
   const int64_t slab_row = (int64_t)c.pages[(int64_t)s * c.maxp + t / c.page_rows] * c.page_rows + t % c.page_rows;
   OutT* o = reinterpret_cast<OutT*>(c.slab) + slab_row * (int64_t)c.V;
+  if (blockIdx.x == 0 && threadIdx.x == 0) invalidate_score(c, slab_row);
   const uint64_t st = states[i];
   const uint64_t peak = avalanche64(st ^ kPeakSalt) % (uint64_t)vocab;
   const float boost = (float)__dmul_rn(conc, range);

@@ -41,6 +41,9 @@ struct CacheDev {
   int32_t* free_slots;  // stack
   int32_t* free_pages;  // stack
   int32_t* tokens;      // [P * page_rows]
+  double* score;        // [P * page_rows] hotspot base score H (1 - pmax) of the row (lc_hotspot.cu)
+  double* score_err;    // its bound vs the reference's evaluation
+  double* score_T;      // the temperature it was computed at (NaN: none / row rewritten)
   char* slab;           // [P * page_rows * V] of dtype
   unsigned long long* ring_clock;
   int32_t* ring_slot;
@@ -61,6 +64,11 @@ __device__ __forceinline__ int64_t slab_row_of(const CacheDev& c, int s, int t) 
 // (generation moved on) reads nothing
 __device__ __forceinline__ bool row_live(const CacheDev& c, int s, int t, const uint32_t* gen, int64_t i) {
   return s >= 0 && s < c.E && c.alive[s] && (!gen || c.gen[s] == gen[i]) && t >= 0 && t < c.nrows[s];
+}
+
+// a row write makes the row's hotspot score stale
+__device__ __forceinline__ void invalidate_score(const CacheDev& c, int64_t sr) {
+  c.score_T[sr] = __longlong_as_double(0x7ff8000000000000ll);
 }
 
 }  // namespace lcb

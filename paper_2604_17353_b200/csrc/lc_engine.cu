@@ -46,6 +46,7 @@ __global__ void engine_decode_kernel(CacheDev c, bool cache_rows, lc_decode_step
     if (live) srow = slab_row_of(c, s, t);
   }
   if (lead) {
+    if (live) invalidate_score(c, srow);
     a.d_digest_out[r] = d;
     lc_task tk;
     tk.row = a.d_staging ? r : (live ? srow : 0);

@@ -123,6 +123,7 @@ class WaveEngine:
         self.agents: set[str] = set()
         self.generate_count = 0
         self.request_log: list[GenerateResult] = []
+        self.hotspot_flags: list[torch.Tensor] = []  # per hotspot wave: selection flags (lc_cache_hotspots)
 
     def register_agent(self, agent_id: str) -> None:
         self.agents.add(agent_id)
@@ -189,9 +190,8 @@ class WaveEngine:
             _capi.check(_capi.lib.lc_cache_pin(cache.handle, slot_r.data_ptr(), gen.data_ptr(), B, 1, st),
                         "lc_cache_pin")  # engine.py:297
             draw_index = None
-            if policy is ReplayPolicy.HOTSPOT:
-                hs = self._hotspots(requests, slot_r, gen, ln)
-                draw_index = cache.hotspot_draw_index(hs, L, dev)
+            if policy is ReplayPolicy.HOTSPOT:  # hotspots_for of every hit (engine.py:312), on the device
+                draw_index = self._hotspot_draw_index(requests, slot_r, gen, L)
             tok, rep, div = cache.replay_looked_up(slot_r, gen, ln_r, vv, L, 1, seeds, T, K, P,
                                                    draw_index=draw_index)
             out.copy_(tok[: B * L])
@@ -230,7 +230,10 @@ class WaveEngine:
         need = rep_h < L
         n_steps = int(L - rep_h[need].min()) if need.any() else 0
         if n_steps:
-            self._decode(B, L, n_steps, rep_h, used_h, digests, out, flags, seeds, T, K, P, wslot, wgen, staging)
+            temps = {c.temperature for c in cfgs}
+            score_T = temps.pop() if (policy is ReplayPolicy.HOTSPOT and len(temps) == 1) else None
+            self._decode(B, L, n_steps, rep_h, used_h, digests, out, flags, seeds, T, K, P, wslot, wgen, staging,
+                         score_T)
         if cache is not None:
             pos = torch.arange(L, dtype=torch.int32, device=dev).repeat(B)
             s_rep, g_rep = wslot.repeat_interleave(L), wgen.repeat_interleave(L)  # (kept alive for the launch)
@@ -262,19 +265,23 @@ class WaveEngine:
 
     # ------------------------------------------------------------------------------------
 
-    def _hotspots(self, requests, slot_r, gen, ln):
-        """hotspots_for (logits_cache.py:153-163) of every hit's entry, memoised per entry."""
-        s_h, g_h, l_h = (x.cpu().numpy() for x in (slot_r, gen, ln))
-        hs = []
+    def _hotspot_draw_index(self, requests, slot_r, gen, L):
+        """Device draw-index array [B * L] of the hits' hotspots, grouped by parameter set."""
+        B = len(requests)
+        di = torch.full((B * L,), -1, dtype=torch.int32, device=self.dev)
+        groups = {}
         for r, q in enumerate(requests):
-            if s_h[r] < 0:
-                hs.append(())
-                continue
-            e = self.cache._entry(int(s_h[r]), int(g_h[r]) & 0xFFFFFFFF, int(l_h[r]), self.model.vocab_size, 0)
-            hs.append(self.cache.hotspots_for(e, q.sampling, q.hotspot or self.hotspot_params))
-        return hs
+            hp = q.hotspot or self.hotspot_params
+            groups.setdefault((q.sampling.temperature, hp), []).append(r)
+        for (T, hp), rs in groups.items():
+            idx = torch.tensor(rs, dtype=torch.int64, device=self.dev)
+            d, _, fl = self.cache.hotspot_draw_index_device(slot_r[idx], gen[idx], L, T, hp)
+            di.view(B, L)[idx] = d.view(len(rs), L)
+            self.hotspot_flags.append(fl)
+        return di
 
-    def _decode(self, B, L, n_steps, rep_h, used_h, digests, out, flags, seeds, T, K, P, wslot, wgen, staging):
+    def _decode(self, B, L, n_steps, rep_h, used_h, digests, out, flags, seeds, T, K, P, wslot, wgen, staging,
+                score_T=None):
         dev, V = self.dev, self.model.vocab_size
         st = _dev.stream_ptr(dev)
         start = torch.from_numpy(rep_h.astype(np.int32)).to(dev)
@@ -302,8 +309,12 @@ class WaveEngine:
                                    V, tasks.data_ptr())
             steps.append(a)
 
+        pos_steps = None
+        if score_T is not None and cache is not None:  # f2 epilogue: score each new row while it is in L2
+            pos_steps = (start[None, :] + torch.arange(n_steps, dtype=torch.int32, device=dev)[:, None]).contiguous()
+
         def run():
-            for a in steps:
+            for s_, a in enumerate(steps):
                 _capi.check(_capi.lib.lc_engine_decode_step(cache.handle if cache else None, C.byref(a), st),
                             "lc_engine_decode_step")
                 if stg is None:
@@ -313,5 +324,9 @@ class WaveEngine:
                     rc = _capi.lib.lc_resample(stg.data_ptr(), sdt, V, V, tasks.data_ptr(), B, draws, ws.data_ptr(),
                                                ws.numel(), None, st)
                 _capi.check(rc, "lc_resample")
+                if pos_steps is not None:
+                    _capi.check(_capi.lib.lc_cache_score_rows(cache.handle, wslot.data_ptr(), wgen.data_ptr(),
+                                                              pos_steps[s_].data_ptr(), B, float(score_T), 0, st),
+                                "lc_cache_score_rows")
 
         run()

@@ -175,6 +175,7 @@ class LogitsCache:
         self.handle = None
         self._prefetch_queue: deque = deque()
         self.hotspot_computations = 0
+        self.hotspot_uncertain = 0  # selections with a decision inside the score bounds (reported)
         self._memo: dict[tuple[int, int], dict] = {}
         self._round: dict[tuple[int, int], int] = {}
         self._snap = None
@@ -580,13 +581,64 @@ class LogitsCache:
         t = torch.arange(n, dtype=torch.float64, device=d)
         return (H * (1.0 - pm) / (1.0 + decay * t)).cpu().numpy()
 
+    def score_rows(self, slot: torch.Tensor, gen: torch.Tensor, temperature: float, max_len: int | None = None):
+        """Hotspot scores of every row of the entries (slot, gen) at ``temperature``, kept
+        beside the rows in the slab (lc_cache_score_rows; rows already scored at this T
+        are skipped)."""
+        n = slot.numel()
+        L = int(max_len or self.max_pages * self.page_rows)
+        if n == 0 or L == 0:
+            return
+        s_rep = slot.to(torch.int32).repeat_interleave(L)
+        g_rep = gen.to(torch.int32).repeat_interleave(L)
+        pos = torch.arange(L, dtype=torch.int32, device=self.dev).repeat(n)
+        _capi.check(_capi.lib.lc_cache_score_rows(self.handle, s_rep.data_ptr(), g_rep.data_ptr(), pos.data_ptr(),
+                                                  n * L, float(temperature), 1, self._stream()),
+                    "lc_cache_score_rows")
+
+    def hotspot_draw_index_device(self, slot: torch.Tensor, gen: torch.Tensor, max_pos: int, temperature: float,
+                                  params: HotspotParams, score: bool = True):
+        """Hotspots of n entries selected on the device (select_hotspots over the entries'
+        scores, sampling.py:133-160) in the replay's draw-index layout: [n * max_pos] int32,
+        the draw number of hotspot t (= hotspots before t), -1 elsewhere (dead or missing
+        entries: none).  Returns (draw_index, n_hot, flags) device tensors; flags bit 0 = a
+        decision the score bounds cannot certify against the reference."""
+        n = slot.numel()
+        d = self.dev
+        di = torch.full((max(n * max_pos, 1),), -1, dtype=torch.int32, device=d)
+        nh = torch.zeros(max(n, 1), dtype=torch.int32, device=d)
+        fl = torch.zeros(max(n, 1), dtype=torch.uint8, device=d)
+        if n == 0:
+            return di[:0], nh[:0], fl[:0]
+        s32, g32 = slot.to(torch.int32).contiguous(), gen.to(torch.int32).contiguous()
+        if score:
+            self.score_rows(s32, g32, temperature)
+        mh = -1 if params.max_hotspots is None else int(params.max_hotspots)
+        _capi.check(_capi.lib.lc_cache_hotspots(self.handle, s32.data_ptr(), g32.data_ptr(), n, int(max_pos),
+                                                float(temperature), float(params.decay), float(params.threshold), mh,
+                                                di.data_ptr(), nh.data_ptr(), fl.data_ptr(), self._stream()),
+                    "lc_cache_hotspots")
+        return di[: n * max_pos], nh[:n], fl[:n]
+
     def hotspots_for(self, entry: CachedTrajectory, cfg: SamplingConfig, params: HotspotParams) -> tuple[int, ...]:
+        """logits_cache.py:153-163: memoised per entry and parameter set; computed on the
+        device from the scores kept beside the rows (no row leaves the slab)."""
         key = params.cache_key(cfg.temperature)
         cached = entry.hotspots.get(key)
         if cached is None:
             if len(entry) == 0:
                 raise ConfigError("logits_seq must be non-empty")
-            cached = sampling.select_hotspots(self.row_scores(entry, cfg.temperature, params.decay), params)
+            entry._check_live()
+            n = len(entry)
+            s = torch.tensor([entry.slot], dtype=torch.int32, device=self.dev)
+            g = torch.tensor([entry.gen], dtype=torch.int64, device=self.dev).to(torch.int32)
+            di, nh, fl = self.hotspot_draw_index_device(s, g, n, cfg.temperature, params)
+            fl_h = int(fl.item())
+            if fl_h & 4:
+                raise ConfigError("stale CachedTrajectory: the entry was overwritten or evicted")
+            if fl_h & 1:
+                self.hotspot_uncertain += 1
+            cached = tuple(int(t) for t in torch.nonzero(di >= 0).flatten().cpu().tolist())
             entry.hotspots[key] = cached
             self.hotspot_computations += 1
         return cached
