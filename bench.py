@@ -641,8 +641,16 @@ def run_c3_sweep(args, cfg, rank, world, dev):
         seeds = lcb._dev.u64_tensor([mix2(1, (rank << 40) + s * n + j) for j in range(n)], dev)
         st = fill_states((rank << 40) + (2 << 32) + s * n_miss * R, n_miss * R) if n_miss else None
         step_in.append((dg, seeds, st))
-    rows_m = torch.empty((max(n_miss, 1) * R, V), dtype=tdt, device=dev)
+    fused = args.miss_path == "fused"
+    rows_m = torch.empty((0 if fused else max(n_miss, 1) * R, V), dtype=tdt, device=dev)
     lens_m = torch.full((max(n_miss, 1),), R, dtype=torch.int32, device=dev)
+    keep_m = torch.zeros(max(n_miss, 1), dtype=torch.int32, device=dev)
+    slot_m = torch.empty(max(n_miss, 1), dtype=torch.int32, device=dev)
+    gen_m = torch.empty(max(n_miss, 1), dtype=torch.int32, device=dev)
+    pos_m = torch.arange(R, dtype=torch.int32, device=dev).repeat(max(n_miss, 1))
+    tasks_m = torch.empty(max(n_miss, 1) * R * lcb._capi.TASK_DTYPE.itemsize, dtype=torch.uint8, device=dev)
+    tok_m = torch.empty(max(n_miss, 1) * R, dtype=torch.int32, device=dev)
+    st_ = _dev.stream_ptr(dev)
     vocs_m = torch.full((max(n_miss, 1),), V, dtype=torch.int32, device=dev)
     offs_m = torch.arange(max(n_miss, 1), dtype=torch.int64, device=dev) * R
     bufs = {}
@@ -654,7 +662,25 @@ def run_c3_sweep(args, cfg, rank, world, dev):
         a.record()
         tok, rep, div, slot, ln = cache.replay_stepwise(dg, R, 1, seeds, T, K, P, bufs=bufs)
         b.record()
-        if n_miss:
+        if n_miss and fused:
+            # f1: entries first (no rows), the producer writes straight into their slab rows,
+            # resample from the slab, tokens into the entries -- no staging rows, no insert copy
+            _capi.check(_capi.lib.lc_cache_writeback(cache.handle, dg[n_hit:].data_ptr(), lens_m.data_ptr(),
+                                                     vocs_m.data_ptr(), keep_m.data_ptr(), gen_m.data_ptr(), n_miss,
+                                                     None, _capi.LC_BF16, 0, None, None, R, slot_m.data_ptr(),
+                                                     gen_m.data_ptr(), st_))
+            s_rep, g_rep = slot_m.repeat_interleave(R), gen_m.repeat_interleave(R)
+            _capi.check(_capi.lib.lc_cache_fill_rows(cache.handle, s_rep.data_ptr(), g_rep.data_ptr(),
+                                                     pos_m.data_ptr(), st.data_ptr(), n_miss * R, 2.5, 5.0, st_))
+            _capi.check(_capi.lib.lc_replay_tasks(slot_m.data_ptr(), lens_m.data_ptr(), vocs_m.data_ptr(), n_miss, R,
+                                                  1, T.data_ptr(), K.data_ptr(), P.data_ptr(), tasks_m.data_ptr(),
+                                                  st_))
+            lcb.sampling.resample(None, tasks_m, seeds=seeds[n_hit:], n_draws=n_miss * R, cache=cache,
+                                  out=(tok_m, torch.empty_like(tok_m, dtype=torch.uint8)))
+            _capi.check(_capi.lib.lc_cache_set_tokens(cache.handle, s_rep.data_ptr(), g_rep.data_ptr(),
+                                                      pos_m.data_ptr(), tok_m.data_ptr(), n_miss * R, st_))
+            cache._dirty()
+        elif n_miss:
             _capi.check(_capi.lib.lc_fill_logits(st.data_ptr(), n_miss * R, V, 2.5, 5.0, _capi.LC_BF16,
                                                  rows_m.data_ptr(), V, _dev.stream_ptr(dev)))
             mt, _ = lcb.resample(rows_m, miss_tasks_d, seeds=seeds[n_hit:], n_draws=n_miss * R)
@@ -702,7 +728,9 @@ def run_c3_sweep(args, cfg, rank, world, dev):
                    "branches": n, "rows_per_entry": R, "vocab": V},
         "lookup_hit_ratio": lookup_hits, "position_hit_ratio": pos_hit,
         "lookup_resample_ms_per_step": hit_ms, "miss_path_ms_per_step": miss_ms,
-        "miss_path": "lc_fill_logits (producer) -> resample -> lc_cache_insert",
+        "miss_path": ("lc_cache_writeback (entries, no rows) -> lc_cache_fill_rows (producer straight into the "
+                      "slab) -> lc_cache_resample -> lc_cache_set_tokens" if fused else
+                      "lc_fill_logits (producer, staging rows) -> resample -> lc_cache_insert (copy)"),
         # per step: lookup (probe + commit), replay tasks, resample (row kernel + requeue + exact),
         # cached tokens, acceptance; misses: producer, resample (3), insert (policy + copy)
         "gpu_launches": (8 + (6 if n_miss else 0)) * args.steps, "clocks": clk.summary(),
@@ -984,6 +1012,8 @@ def main():
                     help="draws the check leg validates (default 10M at V=32000, 100K for the wide configs)")
     ap.add_argument("--policy", default="step_wise", choices=["step_wise", "hotspot"],
                     help="replay policy of the resample step (ReplayPolicy)")
+    ap.add_argument("--miss-path", default="fused", choices=["fused", "staged"],
+                    help="c3 sweep miss path: producer straight into the slab (f1) or via staging rows + copy")
     ap.add_argument("--hit-ratio", type=float, default=None,
                     help="c3: lookup hit ratio h of the sweep (default: every branch cached)")
     ap.add_argument("--graph", action=argparse.BooleanOptionalAction, default=None,

@@ -320,6 +320,7 @@ __global__ void __launch_bounds__(SG_THREADS, 1) stage_kernel(StageArgs a) {
     };
 
     bool requeue_task = false;
+    bool popped = false;  // the next task was popped (and its row load issued) early
     if (bad) {
       requeue_task = true;  // the CTA kernel flags the row (LC_DRAW_BAD_ROW) and counts it
     } else if (tv.T == 0.0) {
@@ -379,6 +380,10 @@ __global__ void __launch_bounds__(SG_THREADS, 1) stage_kernel(StageArgs a) {
       }
       ST_PH(2);
       if (fast) {
+        // the stage is free (only m and amax are needed now): start the next row's load while
+        // the tokens are written
+        if (gw == 0) sg_pop(sm, G, g, lane);
+        popped = true;
         write_tok(amax);
         if (gt == 0) set_kept(io, task_id, 1);
         ST_PH(3);
@@ -609,12 +614,17 @@ __global__ void __launch_bounds__(SG_THREADS, 1) stage_kernel(StageArgs a) {
                 if (v < nvec) {
                   const uint4 q = R[v];
                   const uint32_t w[4] = {q.x, q.y, q.z, q.w};
+                  double a0 = 0.0, a1 = 0.0;  // two chains (predicated gathers: only kept elements load)
 #pragma unroll
                   for (int j = 0; j < 8; ++j) {
                     const uint32_t off = (j & 1) ? off_hi(w[j >> 1]) : off_lo(w[j >> 1]);
-                    if (off < bs) msum[k] += G.ev[off];
+                    if (off < bs) {
+                      if (j & 1) a1 += G.ev[off];
+                      else a0 += G.ev[off];
+                    }
                     ccnt[k] += (off == bs);
                   }
+                  msum[k] = a0 + a1;
                 }
               }
               // reduce-scatter of the four sub-chunk sums: lanes 8k..8k+7 end with sub-chunk k
@@ -750,9 +760,7 @@ __global__ void __launch_bounds__(SG_THREADS, 1) stage_kernel(StageArgs a) {
                   if (off == bs) k8[j] = (r0++ < js) ? es : 0.0;
                 }
               }
-              double ls = 0.0;
-#pragma unroll
-              for (int j = 0; j < 8; ++j) ls += k8[j];
+              const double ls = ((k8[0] + k8[1]) + (k8[2] + k8[3])) + ((k8[4] + k8[5]) + (k8[6] + k8[7]));
               double li = ls;
 #pragma unroll
               for (int o = 1; o < 32; o <<= 1) {
@@ -802,6 +810,9 @@ __global__ void __launch_bounds__(SG_THREADS, 1) stage_kernel(StageArgs a) {
               if (G.dch[d] >= nsub) unc_any = true;
             if (unc_any) G.uncertain = 1;
             gbar(g);
+            // the stage is free: the next row's load overlaps the kept count and the requeue
+            if (gw == 0) sg_pop(sm, G, g, lane);
+            popped = true;
             ST_PH(7);
             if (G.uncertain) {
               requeue_task = true;
@@ -819,7 +830,7 @@ __global__ void __launch_bounds__(SG_THREADS, 1) stage_kernel(StageArgs a) {
     }
     if (requeue_task && gt == 0) requeue(a, task_id);
     gbar(g);  // the group is done with its stage
-    if (gw == 0) sg_pop(sm, G, g, lane);
+    if (gw == 0 && !popped) sg_pop(sm, G, g, lane);
     ST_PH(8);
   }
   if (prof)
