@@ -43,6 +43,8 @@ constexpr int SG_NU = 32;                        // uniforms precomputed per tas
 constexpr int SG_ND = 64;                        // draws per task handled here (more: CTA kernel)
 constexpr int SG_PB = 8;                         // tasks per producer grab
 constexpr int SG_FQ = 6;                         // task FIFO slots
+constexpr int SG_RB = 5;                         // C: vectors per batch of independent loads
+constexpr int SG_RQ = ((SG_MAXV / 8 + SG_GW * 32 - 1) / (SG_GW * 32) + 3) / 4;  // D: vectors per quarter range (7)
 constexpr double kLog2e = 1.4426950408889634;
 constexpr double kLn2 = 0.6931471805599453;
 // ex2.approx.ftz.bf16x2 relative error incl. the bf16 rounding of its result
@@ -53,14 +55,9 @@ constexpr double kEx2Bf16F = (1.0 + (double)kEx2Bf16Err) / (1.0 - (double)kEx2Bf
 struct SgGroup {
   uint32_t hist[SG_NB + 32];  // + one dump bin per lane (branch-free out-of-range increments)
   double ev[SG_NB + 32];    // class values e_b (valid where hist[b] > 0); + one 0.0 per lane
-  double chm[128];          // sub-chunk mass of classes above the cut class
-  double chp[129];          // exclusive prefix of sub-chunk kept masses
-  int chc[128];             // sub-chunk count of the cut class
-  int chq[129];             // exclusive prefix of chc
+  double pt[SG_GT + 1];     // C: prefix of every thread's range kept mass (+ the total)
+  int tb[SG_GT];            // C: cut-class elements before every thread's range
   double su[SG_NU];         // the task's first uniforms
-  double dtau[SG_ND];       // big nucleus: draw targets u * K
-  int dch[SG_ND];           // and their chunks
-  uint32_t hitm[4];         // sub-chunks hit by a draw
   double rd[3][SG_GW];
   float rf[SG_GW];
   int ri[2][SG_GW];
@@ -144,57 +141,57 @@ __device__ void sg_producer(const StageArgs& a, SgSmem& sm, int lane) {
     }
     const int npush = nb > 0 ? nb : (done ? SG_GROUPS - sentinels : 0);
     for (int j = 0; j < npush; ++j) {
-      const int slot_seq = vload(&sm.fq_tail);
+      const int slot_seq = sm.fq_tail;  // (only this warp writes it)
       // wait until the slot's previous occupant (sequence slot_seq - SG_FQ) was copied out by
       // its own consumer: consumers finish out of order, so a completion count is not enough
       if (lane == 0)
-        while (vload(&sm.fq_free[slot_seq % SG_FQ]) != slot_seq) __nanosleep(64);
+        while (ld_acquire(&sm.fq_free[slot_seq % SG_FQ]) != slot_seq) __nanosleep(64);
       __syncwarp();
       const int slot = slot_seq % SG_FQ;
       if (nb > 0) {
-        const TaskView& tj = sm.pbv[j];
         sm.fq_u[slot][lane] = sm.pbu[j][lane];
-        if (lane == 0) {
-          sm.fq_tv[slot] = tj;
-          sm.fq_task[slot] = sm.pbt[j];
-        }
+        warp_copy(sm.fq_tv[slot], sm.pbv[j], lane);
+        if (lane == 0) sm.fq_task[slot] = sm.pbt[j];
       } else {
         if (lane == 0) sm.fq_task[slot] = -1;
         ++sentinels;
       }
-      __threadfence_block();
       __syncwarp();
-      if (lane == 0) *reinterpret_cast<volatile int*>(&sm.fq_tail) = slot_seq + 1;
+      if (lane == 0) st_release(&sm.fq_tail, slot_seq + 1);  // publishes the slot (cumulative release)
       __syncwarp();
     }
     if (done && sentinels >= SG_GROUPS) return;
   }
 }
 
-// group warp 0: claim the next FIFO slot, copy it into the group and start its row load
+// group warp 0: claim the next FIFO slot, start its row load, copy the task into the group.
+// The bulk copy is issued first (its complete_tx may precede the expect_tx arrive: the phase
+// still needs that arrive), the arrive (release) then publishes G.task / tv / su to the group.
 __device__ void sg_pop(SgSmem& sm, SgGroup& G, int g, int lane) {
   int h = 0;
   if (lane == 0) {
     h = atomicAdd(&sm.fq_head, 1);
-    while (vload(&sm.fq_tail) <= h) __nanosleep(32);
+    while (ld_acquire(&sm.fq_tail) <= h) __nanosleep(32);
   }
   h = __shfl_sync(0xffffffffu, h, 0);
-  __threadfence_block();
+  __syncwarp();  // lane 0's acquire orders the other lanes' slot reads
   const int slot = h % SG_FQ;
   const int t = sm.fq_task[slot];
-  if (t >= 0) G.su[lane] = sm.fq_u[slot][lane];
+  uint32_t bytes = 0;
+  if (t >= 0) {
+    if (lane == 0) {
+      bytes = (uint32_t)(sm.fq_tv[slot].V * 2);
+      bulk_load(sm.ring[g], sm.fq_tv[slot].row, bytes, &sm.full[g]);
+    }
+    G.su[lane] = sm.fq_u[slot][lane];
+    warp_copy(G.tv, sm.fq_tv[slot], lane);
+  }
   __syncwarp();
   if (lane == 0) {
     G.task = t;
-    if (t >= 0) G.tv = sm.fq_tv[slot];
-    __threadfence_block();
-    *reinterpret_cast<volatile int*>(&sm.fq_free[slot]) = h + SG_FQ;  // slot h released
-    if (t >= 0) {
-      mbar_expect_tx(&sm.full[g], (uint32_t)(G.tv.V * 2));  // release: G.task/tv/su visible
-      bulk_load(sm.ring[g], G.tv.row, (uint32_t)(G.tv.V * 2), &sm.full[g]);
-    } else {
-      mbar_arrive(&sm.full[g]);  // completes the phase with no bytes: the group sees -1
-    }
+    st_release(&sm.fq_free[slot], h + SG_FQ);  // slot h released
+    if (t >= 0) mbar_expect_tx(&sm.full[g], bytes);  // release: G.task/tv/su visible to the group
+    else mbar_arrive(&sm.full[g]);  // completes the phase with no bytes: the group sees -1
   }
   __syncwarp();
 }
@@ -382,7 +379,9 @@ __global__ void __launch_bounds__(SG_THREADS, 1) stage_kernel(StageArgs a) {
       if (fast) {
         // the stage is free (only m and amax are needed now): start the next row's load while
         // the tokens are written
+        ST_PH(2);
         if (gw == 0) sg_pop(sm, G, g, lane);
+        ST_PH(11);
         popped = true;
         write_tok(amax);
         if (gt == 0) set_kept(io, task_id, 1);
@@ -597,223 +596,193 @@ __global__ void __launch_bounds__(SG_THREADS, 1) stage_kernel(StageArgs a) {
             // histogram range (or a +-0 cut); 7 counts precise-tail recomputations
             if (gt == 0) atomicAdd(&a.counters[(bstar == INT_MAX || G.cut_ok == 2) ? 6 : 4], 1ull);
           } else {
-            // ---------------------------------------- C: kept mass of every 256-id sub-chunk
-            // (32 vectors: one per lane) from the stored offsets; warps take 1024-id chunks
+            // ---------------------------------------- C: every thread sums the kept mass of its
+            // own contiguous range of Rv vectors (classes above the cut class, fp64 values
+            // gathered for kept elements only, plus a count of the cut class); one group scan
+            // turns the ranges into prefixes P_t (tie ranks: the first js cut-class elements
+            // in id order are kept, so the ties before range t contribute min(js, tb_t) es)
             const uint32_t bs = (uint32_t)G.cut_b;
             const int js = G.cut_j;
             const double es = G.cut_e;
-            const int nsub = (nvec + 31) >> 5;  // sub-chunks of 256 ids
-            for (int c = gw; 4 * c < nsub; c += SG_GW) {
-              double msum[4];
-              int ccnt[4];
+            const int Rv = (nvec + SG_GT - 1) / SG_GT;  // vectors per range (25 at V = 32000)
+            const int v0 = min(Rv * gt, nvec), v1 = min(v0 + Rv, nvec);
+            double ma = 0.0;
+            int mc = 0;
+            for (int vb = v0; vb < v1; vb += SG_RB) {
+              uint32_t w[SG_RB][4];
 #pragma unroll
-              for (int k = 0; k < 4; ++k) {
-                const int v = 32 * (4 * c + k) + lane;
-                msum[k] = 0.0;
-                ccnt[k] = 0;
-                if (v < nvec) {
-                  const uint4 q = R[v];
-                  const uint32_t w[4] = {q.x, q.y, q.z, q.w};
-                  double a0 = 0.0, a1 = 0.0;  // two chains (predicated gathers: only kept elements load)
+              for (int k = 0; k < SG_RB; ++k) {
+                uint4 q = make_uint4(0xffffffffu, 0xffffffffu, 0xffffffffu, 0xffffffffu);
+                if (vb + k < v1) q = R[vb + k];
+                w[k][0] = q.x;
+                w[k][1] = q.y;
+                w[k][2] = q.z;
+                w[k][3] = q.w;
+              }
+              double a0 = 0.0, a1 = 0.0;
 #pragma unroll
-                  for (int j = 0; j < 8; ++j) {
-                    const uint32_t off = (j & 1) ? off_hi(w[j >> 1]) : off_lo(w[j >> 1]);
-                    if (off < bs) {
-                      if (j & 1) a1 += G.ev[off];
-                      else a0 += G.ev[off];
-                    }
-                    ccnt[k] += (off == bs);
-                  }
-                  msum[k] = a0 + a1;
+              for (int k = 0; k < SG_RB; ++k) {
+#pragma unroll
+                for (int j = 0; j < 8; ++j) {
+                  const uint32_t off = (j & 1) ? off_hi(w[k][j >> 1]) : off_lo(w[k][j >> 1]);
+                  const double e = pgather_nv(G.ev, off, off < bs);
+                  if (j & 1) a1 += e;
+                  else a0 += e;
+                  mc += (off == bs);
                 }
               }
-              // reduce-scatter of the four sub-chunk sums: lanes 8k..8k+7 end with sub-chunk k
-              {
-                const bool h16 = lane & 16, h8 = lane & 8;
-                double a0 = h16 ? msum[2] : msum[0], a1 = h16 ? msum[3] : msum[1];
-                double b0 = h16 ? msum[0] : msum[2], b1 = h16 ? msum[1] : msum[3];
-                int i0 = h16 ? ccnt[2] : ccnt[0], i1 = h16 ? ccnt[3] : ccnt[1];
-                int j0 = h16 ? ccnt[0] : ccnt[2], j1 = h16 ? ccnt[1] : ccnt[3];
-                a0 += __shfl_xor_sync(0xffffffffu, b0, 16);
-                a1 += __shfl_xor_sync(0xffffffffu, b1, 16);
-                i0 += __shfl_xor_sync(0xffffffffu, j0, 16);
-                i1 += __shfl_xor_sync(0xffffffffu, j1, 16);
-                double a = h8 ? a1 : a0, b = h8 ? a0 : a1;
-                int ia = h8 ? i1 : i0, ib = h8 ? i0 : i1;
-                a += __shfl_xor_sync(0xffffffffu, b, 8);
-                ia += __shfl_xor_sync(0xffffffffu, ib, 8);
+              ma += a0 + a1;
+            }
+            // group inclusive scan of (ma, mc)
+            double mi = ma;
+            int ci = mc;
 #pragma unroll
-                for (int o = 4; o > 0; o >>= 1) {
-                  a += __shfl_xor_sync(0xffffffffu, a, o);
-                  ia += __shfl_xor_sync(0xffffffffu, ia, o);
-                }
-                const int k = lane >> 3;
-                if ((lane & 7) == 0 && 4 * c + k < nsub) {
-                  G.chm[4 * c + k] = a;
-                  G.chc[4 * c + k] = ia;
-                }
+            for (int o = 1; o < 32; o <<= 1) {
+              const double y = __shfl_up_sync(0xffffffffu, mi, o);
+              const int z = __shfl_up_sync(0xffffffffu, ci, o);
+              if (lane >= o) {
+                mi += y;
+                ci += z;
               }
             }
-            gbar(g);
-            if (gw == 0) {  // exclusive prefixes over the (<= 128) sub-chunks, 4 per lane
-              int cq[4];
-              double cmv[4];
-              int cqs = 0;
-#pragma unroll
-              for (int k = 0; k < 4; ++k) {
-                const int c = 4 * lane + k;
-                cq[k] = c < nsub ? G.chc[c] : 0;
-                cqs += cq[k];
-              }
-              int cqi = cqs;
-#pragma unroll
-              for (int o = 1; o < 32; o <<= 1) {
-                const int y = __shfl_up_sync(0xffffffffu, cqi, o);
-                if (lane >= o) cqi += y;
-              }
-              int cpre = cqi - cqs;
-              double kms = 0.0;
-#pragma unroll
-              for (int k = 0; k < 4; ++k) {
-                const int c = 4 * lane + k;
-                const int takes = min(max(js - cpre, 0), cq[k]);
-                cmv[k] = c < nsub ? G.chm[c] + (double)takes * es : 0.0;
-                if (c < nsub) G.chq[c] = cpre;
-                cpre += cq[k];
-                kms += cmv[k];
-              }
-              double kmi = kms;
-#pragma unroll
-              for (int o = 1; o < 32; o <<= 1) {
-                const double y = __shfl_up_sync(0xffffffffu, kmi, o);
-                if (lane >= o) kmi += y;
-              }
-              double pp = kmi - kms;
-#pragma unroll
-              for (int k = 0; k < 4; ++k) {
-                const int c = 4 * lane + k;
-                if (c < nsub) G.chp[c] = pp;
-                pp += cmv[k];
-              }
-              if (lane == 31) G.chp[nsub] = pp;
+            if (lane == 31) {
+              G.rd[2][gw] = mi;
+              G.ri[1][gw] = ci;
             }
             if (gt == 0) G.uncertain = 0;
-            if (gt < 4) G.hitm[gt] = 0u;
             gbar(g);
-            const double Ak = G.chp[nsub];
-            const int ndd = min(nd, SG_ND);
-            // each draw's sub-chunk (binary search over the prefix), lanes in parallel
-            for (int d = gt; d < ndd; d += SG_GT) {
-              const double u = d < SG_NU ? G.su[d] : draw_u(io, d0 + d, tv);
-              const double tau = u * Ak;
-              int lo = 0, hi = nsub;  // first sub-chunk whose inclusive prefix > tau
-              while (lo < hi) {
-                const int mid = (lo + hi) >> 1;
-                if (G.chp[mid + 1] <= tau) lo = mid + 1;
-                else hi = mid;
+            double mw = 0.0, mtot = 0.0;
+            int cw = 0, ctot = 0;
+#pragma unroll
+            for (int i = 0; i < SG_GW; ++i) {
+              if (i < gw) {
+                mw += G.rd[2][i];
+                cw += G.ri[1][i];
               }
-              G.dch[d] = lo;
-              G.dtau[d] = tau;
-              if (lo < nsub) atomicOr(&G.hitm[lo >> 5], 1u << (lo & 31));
+              mtot += G.rd[2][i];
+              ctot += G.ri[1][i];
+            }
+            {
+              const int tb = cw + ci - mc;  // cut-class elements before this range
+              G.pt[gt] = (mw + mi - ma) + (double)min(js, tb) * es;
+              G.tb[gt] = tb;
+              if (gt == 0) G.pt[SG_GT] = mtot + (double)min(js, ctot) * es;
             }
             gbar(g);
+            const double Ak = G.pt[SG_GT];
+            const int ndd = min(nd, SG_ND);
             ST_PH(6);
-            // ---------------------------------------- D: each hit sub-chunk is scanned once by
-            // one warp (one vector per lane); its draws are resolved in parallel, one lane each
+            // ---------------------------------------- D: a quad of lanes per draw.  Every lane
+            // finds the range holding the draw's target (binary search over the prefixes), takes
+            // a quarter of that range's vectors (independent loads, per-vector kept masses kept in
+            // registers), the quad scans its quarters, and the lane whose quarter holds the target
+            // walks its vectors and then the hit vector's 8 elements
             const double beta = 8.0 * kRefExpErr + kLiteErr + relArg + (double)(6 * V + 1024) * u53;
-            bool unc_any = nd > SG_ND;  // (more draws than the table holds: CTA kernel)
-            // this warp's hit sub-chunks (sc = gw mod SG_GW), from the hit mask
-            for (int sc = gw; sc < nsub; sc += SG_GW) {
-              if (!((G.hitm[sc >> 5] >> (sc & 31)) & 1u)) continue;
-              const unsigned mine0 = __ballot_sync(0xffffffffu, lane < ndd && G.dch[lane] == sc);
-              const unsigned mine1 = __ballot_sync(0xffffffffu, 32 + lane < ndd && G.dch[32 + lane] == sc);
-              if (!(mine0 | mine1)) continue;
-              const int v = 32 * sc + lane;
-              uint32_t w[4] = {0xffffffffu, 0xffffffffu, 0xffffffffu, 0xffffffffu};
-              if (v < nvec) {
-                const uint4 q = R[v];
-                w[0] = q.x;
-                w[1] = q.y;
-                w[2] = q.z;
-                w[3] = q.w;
-              }
-              double k8[8];
-              int le = 0;
+            bool unc_any = nd > SG_ND;  // (more draws than handled here: CTA kernel)
+            const int Rq = (Rv + 3) >> 2;  // vectors per quarter (<= SG_RQ)
+            const int q = lane & 3;
+            for (int db = 0; db < ndd; db += SG_GT / 4) {
+              const int d = db + (gt >> 2);
+              const bool act = d < ndd;
+              double tau = 0.0;
+              if (act) tau = (d < SG_NU ? G.su[d] : draw_u(io, d0 + d, tv)) * Ak;
+              int t = 0;  // the last range whose prefix is <= tau
 #pragma unroll
-              for (int j = 0; j < 8; ++j) {
-                const uint32_t off = (j & 1) ? off_hi(w[j >> 1]) : off_lo(w[j >> 1]);
-                k8[j] = off < bs ? G.ev[off] : 0.0;
-                le += (off == bs);
-              }
-              // the cut class's kept ties (only sub-chunks holding some pay for their ranks)
-              if (__ballot_sync(0xffffffffu, le > 0)) {
-                int ei = le;
+              for (int st = 128; st > 0; st >>= 1)
+                if (t + st < SG_GT && G.pt[t + st] <= tau) t += st;
+              const int w0 = min(Rv * t, nvec), w1 = min(w0 + Rv, nvec);
+              const int x0 = min(w0 + Rq * q, w1), x1 = min(x0 + Rq, w1);
+              double mk[SG_RQ];
+              int tk[SG_RQ];
+              double ma_q = 0.0;
+              int c_q = 0;
 #pragma unroll
-                for (int o = 1; o < 32; o <<= 1) {
-                  const int z = __shfl_up_sync(0xffffffffu, ei, o);
-                  if (lane >= o) ei += z;
-                }
-                int r0 = G.chq[sc] + ei - le;
+              for (int k = 0; k < SG_RQ; ++k) {
+                uint4 qv = make_uint4(0xffffffffu, 0xffffffffu, 0xffffffffu, 0xffffffffu);
+                if (act && x0 + k < x1) qv = R[x0 + k];
+                const uint32_t w[4] = {qv.x, qv.y, qv.z, qv.w};
+                double a0 = 0.0, a1 = 0.0;
+                int c = 0;
 #pragma unroll
                 for (int j = 0; j < 8; ++j) {
                   const uint32_t off = (j & 1) ? off_hi(w[j >> 1]) : off_lo(w[j >> 1]);
-                  if (off == bs) k8[j] = (r0++ < js) ? es : 0.0;
+                  const double e = pgather_nv(G.ev, off, off < bs);
+                  if (j & 1) a1 += e;
+                  else a0 += e;
+                  c += (off == bs);
+                }
+                mk[k] = a0 + a1;
+                tk[k] = c;
+                ma_q += mk[k];
+                c_q += c;
+              }
+              // exclusive scan of (ma, c) over the quad
+              double ea = ma_q;
+              int ec = c_q;
+#pragma unroll
+              for (int o = 1; o < 4; o <<= 1) {
+                const double y = __shfl_up_sync(0xffffffffu, ea, o, 4);
+                const int z = __shfl_up_sync(0xffffffffu, ec, o, 4);
+                if (q >= o) {
+                  ea += y;
+                  ec += z;
                 }
               }
-              const double ls = ((k8[0] + k8[1]) + (k8[2] + k8[3])) + ((k8[4] + k8[5]) + (k8[6] + k8[7]));
-              double li = ls;
+              ea -= ma_q;
+              ec -= c_q;
+              const int tb0 = G.tb[t];
+              int rank = tb0 + ec;  // cut-class elements before this quarter
+              double E = G.pt[t] + ea + (double)(min(js, rank) - min(js, tb0)) * es;
+              const double Eend = E + ma_q + (double)(min(js, rank + c_q) - min(js, rank)) * es;
+              const bool mine = act && E <= tau && tau < Eend;
+              const unsigned qm = (__ballot_sync(0xffffffffu, mine) >> (lane & ~3)) & 0xfu;
+              bool unc = act && (qm == 0u || !(tau < Ak));  // (rounding at a range end, u ~ 1)
+              if (mine && !unc) {
+                int hv = -1;
 #pragma unroll
-              for (int o = 1; o < 32; o <<= 1) {
-                const double y = __shfl_up_sync(0xffffffffu, li, o);
-                if (lane >= o) li += y;
-              }
-              const double lb = G.chp[sc] + li - ls;  // prefix before this lane's vector
-              for (int half = 0; half < 2; ++half) {
-                const unsigned mine = half ? mine1 : mine0;
-                if (!mine) continue;
-                const int d = 32 * half + lane;
-                const bool act = (mine >> lane) & 1u;
-                const double tau = act ? G.dtau[d] : 0.0;
-                int hl = 0;  // last lane whose prefix <= tau
-#pragma unroll
-                for (int st = 16; st > 0; st >>= 1) {
-                  const double y = __shfl_sync(0xffffffffu, lb, hl + st);
-                  if (y <= tau) hl += st;
-                }
-                const double base = __shfl_sync(0xffffffffu, lb, hl);
-                // the hit lane's 8 kept masses, walked by the draw's lane
-                double kk[8];
-#pragma unroll
-                for (int j = 0; j < 8; ++j) kk[j] = __shfl_sync(0xffffffffu, k8[j], hl);
-                if (act) {
-                  double E = base;
-                  int jj = 0;
-                  for (; jj < 8; ++jj) {
-                    if (kk[jj] > 0.0 && E + kk[jj] > tau) break;
-                    E += kk[jj];
+                for (int k = 0; k < SG_RQ; ++k) {
+                  if (hv < 0 && x0 + k < x1) {
+                    const double m_k = mk[k] + (double)(min(js, rank + tk[k]) - min(js, rank)) * es;
+                    if (E + m_k > tau) {
+                      hv = x0 + k;
+                    } else {
+                      E += m_k;
+                      rank += tk[k];
+                    }
                   }
-                  bool unc = true;
-                  if (jj < 8 && 32 * sc + hl < nvec) {
-                    const double Ein = E + kk[jj];
+                }
+                unc = true;
+                if (hv >= 0) {
+                  const uint4 hq = R[hv];
+                  const uint32_t hw[4] = {hq.x, hq.y, hq.z, hq.w};
+                  int jj = 0;
+                  double kk = 0.0;
+                  for (; jj < 8; ++jj) {
+                    const uint32_t off = (jj & 1) ? off_hi(hw[jj >> 1]) : off_lo(hw[jj >> 1]);
+                    kk = off < bs ? G.ev[off] : 0.0;
+                    if (off == bs) kk = (rank++ < js) ? es : 0.0;
+                    if (kk > 0.0 && E + kk > tau) break;
+                    E += kk;
+                  }
+                  if (jj < 8) {
+                    const double Ein = E + kk;
                     unc = !(Ein - tau > 2.0 * beta * Ak) || !(tau - E > 2.0 * beta * Ak);
                     if (!unc) {
-                      io.token[d0 + d] = 8 * (32 * sc + hl) + jj;
+                      io.token[d0 + d] = 8 * hv + jj;
                       if (io.flags) io.flags[d0 + d] = 0;
                     }
                   }
-                  unc_any |= unc;
                 }
               }
+              unc_any |= unc;
             }
-            // draws whose target fell past the last sub-chunk (rounding at u ~ 1)
-            for (int d = gt; d < ndd; d += SG_GT)
-              if (G.dch[d] >= nsub) unc_any = true;
             if (unc_any) G.uncertain = 1;
             gbar(g);
             // the stage is free: the next row's load overlaps the kept count and the requeue
-            if (gw == 0) sg_pop(sm, G, g, lane);
-            popped = true;
             ST_PH(7);
+            if (gw == 0) sg_pop(sm, G, g, lane);
+            ST_PH(11);
+            popped = true;
             if (G.uncertain) {
               requeue_task = true;
               if (gt == 0) atomicAdd(&a.counters[5], 1ull);
@@ -830,8 +799,9 @@ __global__ void __launch_bounds__(SG_THREADS, 1) stage_kernel(StageArgs a) {
     }
     if (requeue_task && gt == 0) requeue(a, task_id);
     gbar(g);  // the group is done with its stage
-    if (gw == 0 && !popped) sg_pop(sm, G, g, lane);
     ST_PH(8);
+    if (gw == 0 && !popped) sg_pop(sm, G, g, lane);
+    ST_PH(11);
   }
   if (prof)
     for (int k = 0; k < 12; ++k) atomicAdd(&a.prof[k], ph[k]);
@@ -881,7 +851,8 @@ bool stage_eligible(int dtype, int64_t V, int64_t row_bytes, const void* rows) {
 }  // namespace lcb
 
 // Debug: per-phase clock totals of each group's thread 0 across CTAs (LCB_STAGE_PROF=1):
-// 0 wait, 1 A, 2 B, 3 fast finish, 4 B'+H, 5 classes+cut, 6 C, 7 D, 8 end, 9 rows, 10 big rows.
+// 0 wait, 1 A, 2 B, 3 fast finish, 4 B'+H, 5 classes+cut, 6 C, 7 D, 8 end, 9 rows, 10 big rows,
+// 11 task pops (group warp 0: FIFO claim, task copy, row load issue).
 // Copies and resets the counters (synchronising).
 extern "C" int lcb_stage_prof_fetch(unsigned long long* h_out) {
   if (!lcb::g_stage_prof) return LC_E_ARG;

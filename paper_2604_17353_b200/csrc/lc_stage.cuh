@@ -95,6 +95,16 @@ __device__ __forceinline__ double pgather(const double* base, uint32_t idx, bool
   return r;
 }
 
+// the same gather without `volatile`: the compiler may batch independent gathers ahead of their
+// uses (the table must not change between the caller's last barrier and the gather)
+__device__ __forceinline__ double pgather_nv(const double* base, uint32_t idx, bool p) {
+  double r;
+  asm("{\n .reg .pred q;\n setp.ne.u32 q, %2, 0;\n mov.f64 %0, 0d0000000000000000;\n @q ld.shared.f64 %0, [%1];\n}"
+      : "=d"(r)
+      : "r"(smem_u32(base) + 8u * idx), "r"((uint32_t)p));
+  return r;
+}
+
 // ---- the kernel --------------------------------------------------------------------------------
 
 struct StageArgs {
@@ -117,6 +127,25 @@ __device__ __forceinline__ void requeue(const StageArgs& a, int task_id) {
 }
 
 __device__ __forceinline__ int vload(const int* p) { return *reinterpret_cast<const volatile int*>(p); }
+
+// CTA-scope acquire load / release store of a shared int (the task FIFO's indices): lighter than a
+// sequentially consistent __threadfence_block() around volatile accesses
+__device__ __forceinline__ int ld_acquire(const int* p) {
+  int v;
+  asm volatile("ld.acquire.cta.shared.s32 %0, [%1];" : "=r"(v) : "r"(smem_u32(p)) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release(int* p, int v) {
+  asm volatile("st.release.cta.shared.s32 [%0], %1;" ::"r"(smem_u32(p)), "r"(v) : "memory");
+}
+
+// one 4-byte word per lane (lanes 0 .. sizeof(T)/4 - 1)
+template <typename T>
+__device__ __forceinline__ void warp_copy(T& dst, const T& src, int lane) {
+  static_assert(sizeof(T) % 4 == 0 && sizeof(T) <= 128, "warp_copy");
+  if (lane < (int)(sizeof(T) / 4))
+    reinterpret_cast<uint32_t*>(&dst)[lane] = reinterpret_cast<const uint32_t*>(&src)[lane];
+}
 
 
 }  // namespace lcb

@@ -74,7 +74,7 @@ def main():
                 names = ["wait", "A", "B", "fastfin", "H", "cls+cut", "C", "D", "end"]
                 print("  stage phases, clks per row (per big row for H..D): " + "  ".join(
                     f"{nm}={ph[k] / (big if 4 <= k <= 7 else rows_):.0f}" for k, nm in enumerate(names))
-                    + f"  post={ph[11] / big:.0f}  rows={ph[9]} big={ph[10]}", flush=True)
+                    + f"  pop={ph[11] / rows_:.0f}  rows={ph[9]} big={ph[10]}", flush=True)
 
 
 if __name__ == "__main__":
