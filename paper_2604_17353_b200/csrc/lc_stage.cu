@@ -43,6 +43,7 @@ constexpr int SG_NU = 32;                        // uniforms precomputed per tas
 constexpr int SG_ND = 64;                        // draws per task handled here (more: CTA kernel)
 constexpr int SG_PB = 8;                         // tasks per producer grab
 constexpr int SG_FQ = 6;                         // task FIFO slots
+constexpr int SG_POPW = SG_GW - 1;               // the group warp that pops tasks (it writes no tokens for <= 128 draws)
 constexpr int SG_RB = 5;                         // C: vectors per batch of independent loads
 constexpr int SG_RQ = ((SG_MAXV / 8 + SG_GW * 32 - 1) / (SG_GW * 32) + 3) / 4;  // D: vectors per quarter range (7)
 constexpr double kLog2e = 1.4426950408889634;
@@ -51,6 +52,9 @@ constexpr double kLn2 = 0.6931471805599453;
 // (pinned by tests/test_gpu_parity.py::test_bf16_ex2_bound over every bf16 input)
 constexpr float kEx2Bf16Err = 0.01f;  // measured max 0.0071 (2^-7.1)
 constexpr double kEx2Bf16F = (1.0 + (double)kEx2Bf16Err) / (1.0 - (double)kEx2Bf16Err);  // ratio bound factor
+// B's summation error relative to the exact sum of its (positive) bf16 exponentials: two packed
+// bf16 roundings ((1 + 2^-9)^2 - 1) plus fp32 chains of <= 25 + 5 + 2 additions (2^-24 each)
+constexpr double kPairAcc = 0x1p-8 + 0x1p-18 + 40.0 * 0x1p-24;
 
 struct SgGroup {
   uint32_t hist[SG_NB + 32];  // + one dump bin per lane (branch-free out-of-range increments)
@@ -85,6 +89,7 @@ struct __align__(128) SgSmem {
   unsigned long long full[SG_GROUPS];
 };
 static_assert(sizeof(SgSmem) <= 232448, "staged kernel shared memory");
+static_assert((SG_MAXV / 8 + SG_GT - 1) / SG_GT <= 32, "argmax search: one lane per vector of a thread");
 
 __device__ __forceinline__ void gbar(int g) { gbar_n<SG_GT>(g); }
 
@@ -249,7 +254,7 @@ __global__ void __launch_bounds__(SG_THREADS, 1) stage_kernel(StageArgs a) {
     return r;
   };
 
-  if (gw == 0) sg_pop(sm, G, g, lane);
+  if (gw == SG_POPW) sg_pop(sm, G, g, lane);
   for (uint32_t phase = 0;; phase ^= 1u) {
     mbar_wait(&sm.full[g], phase);
     ST_PH(0);
@@ -261,20 +266,18 @@ __global__ void __launch_bounds__(SG_THREADS, 1) stage_kernel(StageArgs a) {
     const int nd = (int)(tv.d1 - tv.d0);
 
     // ------------------------------------------------ A: max (packed, NaN-propagating)
-    float tmax = -INFINITY;
-    int tpos = -1;  // first vector of this thread holding its maximum
-    bool nan = false;
-#pragma unroll 4
+    // two packed running maxima per thread (3-input VHMNMX); the first argmax is searched only
+    // where it is needed (FAST and greedy rows), by the threads whose maximum is the row's
+    uint32_t am0 = 0xff80ff80u, am1 = 0xff80ff80u;  // (-inf, -inf)
+#pragma unroll 5
     for (int v = gt; v < nvec; v += SG_GT) {
       const uint4 q = R[v];
-      const uint32_t x = bmax2_nan(bmax2_nan(q.x, q.y), bmax2_nan(q.z, q.w));
-      const float vm = max_nan(lo_f(x), hi_f(x));
-      nan |= vm != vm;
-      if (vm > tmax) {
-        tmax = vm;
-        tpos = v;
-      }
+      am0 = bmax2_nan(am0, bmax2_nan(q.x, q.y));
+      am1 = bmax2_nan(am1, bmax2_nan(q.z, q.w));
     }
+    const uint32_t amx = bmax2_nan(am0, am1);
+    const float tmax = max_nan(lo_f(amx), hi_f(amx));
+    const bool nan = tmax != tmax;
     {
       const float wm = warp_max(tmax);
       const bool wn = __any_sync(0xffffffffu, nan);
@@ -294,15 +297,25 @@ __global__ void __launch_bounds__(SG_THREADS, 1) stage_kernel(StageArgs a) {
     // (a zero maximum with both signed zeros present has a different first argmax
     // in the reference's value order: left to the CTA kernel, like non-finite rows)
     bad |= !(m > -INFINITY) || !(m < INFINITY) || m == 0.0f;
-    // this thread's candidate for the first argmax (its first vector holding m)
+    // the first argmax among this warp's "holders" (threads whose maximum is m): for each
+    // holder the warp's lanes check its <= 32 vectors at once (lane k: the holder's k-th
+    // vector), so the search is one round of loads + a warp min (warp-uniform result)
     auto argmax_cand = [&]() -> int {
+      unsigned hm = __ballot_sync(0xffffffffu, tmax == m);
       int best = INT_MAX;
-      if (tpos >= 0 && tmax == m) {
-        const uint4 q = R[tpos];
-        const uint32_t w[4] = {q.x, q.y, q.z, q.w};
+      while (hm) {
+        const int th = gt - lane + (__ffs(hm) - 1);
+        hm &= hm - 1;
+        const int v = th + lane * SG_GT;
+        int pos = INT_MAX;
+        if (v < nvec) {
+          const uint4 q = R[v];
+          const uint32_t w[4] = {q.x, q.y, q.z, q.w};
 #pragma unroll
-        for (int j = 7; j >= 0; --j)
-          if (((j & 1) ? hi_f(w[j >> 1]) : lo_f(w[j >> 1])) == m) best = 8 * tpos + j;
+          for (int j = 7; j >= 0; --j)
+            if (((j & 1) ? hi_f(w[j >> 1]) : lo_f(w[j >> 1])) == m) pos = 8 * v + j;
+        }
+        best = min(best, warp_min_int(pos));
       }
       return best;
     };
@@ -336,20 +349,23 @@ __global__ void __launch_bounds__(SG_THREADS, 1) stage_kernel(StageArgs a) {
         const float Lbf = __uint_as_float(Lb << 16);
         const uint32_t nmLb = bf16_bits(-(m * Lbf));
         const uint32_t L2 = Lb | (Lb << 16), nmL2 = nmLb | (nmLb << 16);
-        float ac0 = 0.0f, ac1 = 0.0f, ac2 = 0.0f, ac3 = 0.0f;  // independent FHADD chains
+        // the 8 exponentials of a vector are summed pairwise in packed bf16 (two roundings,
+        // relative 2^-8 + 2^-18 on positive terms) and the pair sums added into fp32
+        float ac0 = 0.0f, ac1 = 0.0f;
 #pragma unroll 4
         for (int v = gt; v < nvec; v += SG_GT) {
           const uint4 q = R[v];
-          ac0 = bacc2(ac0, bex2(bfma2(q.x, L2, nmL2)));
-          ac1 = bacc2(ac1, bex2(bfma2(q.y, L2, nmL2)));
-          ac2 = bacc2(ac2, bex2(bfma2(q.z, L2, nmL2)));
-          ac3 = bacc2(ac3, bex2(bfma2(q.w, L2, nmL2)));
+          const uint32_t e0 = bex2(bfma2(q.x, L2, nmL2)), e1 = bex2(bfma2(q.y, L2, nmL2));
+          const uint32_t e2 = bex2(bfma2(q.z, L2, nmL2)), e3 = bex2(bfma2(q.w, L2, nmL2));
+          const uint32_t s4 = badd2(badd2(e0, e1), badd2(e2, e3));
+          ac0 = bacc_lo(ac0, s4);
+          ac1 = bacc_hi(ac1, s4);
         }
-        const float acc = (ac0 + ac1) + (ac2 + ac3);
+        const float acc = ac0 + ac1;
         // one barrier for the mass and the first argmax
         {
           const float ws = warp_sum(acc);
-          const int wc = warp_min_int(argmax_cand());
+          const int wc = argmax_cand();
           if (lane == 0) {
             G.rd[0][gw] = (double)ws;
             G.ri[1][gw] = wc;
@@ -365,14 +381,16 @@ __global__ void __launch_bounds__(SG_THREADS, 1) stage_kernel(StageArgs a) {
         const uint32_t mb = bf16_bits(m);
         const float emax = lo_f(bex2(bfma2(mb | (mb << 16), L2, nmL2)));
         // exponent error <= 2^-8 (1.001 |a| + |delta|), |delta| <= 2^-9 |m Lb|;
-        // elements below 2^-40 bounded absolutely; fp32 accumulation of <= 200 terms + 32 + 5
+        // elements below 2^-40 bounded absolutely.  Summation: Sc <= (1 + kPairAcc) sum E_i
+        // (packed bf16 pair sums, then fp32 chains of <= 25 + 5 + 2 terms, all positive), so
+        // sum_{i != amax} E_i / E_max <= Sc (1 + kPairAcc) / E_max - 1
         const float dl = 0.001953125f * mL * 1.01f + 0.001953125f;
         // (no fp64 divisions on this per-row path: the ratio is a constant, 1/emax a correctly
         // rounded reciprocal -- one extra 2^-53 rounding, far inside the 1e-9 / V 2^-40 slack)
         const double F = (double)exp2f(0.00390625f * (40.1f + dl)) * kEx2Bf16F;
-        const double tail = fmax(Sc * __drcp_rn((double)emax) - 1.0, 0.0);
+        const double tail = fmax(Sc * (1.0 + kPairAcc) * __drcp_rn((double)emax) - 1.0, 0.0);
         Sfast = 1.0 + tail;
-        const double Sup = (1.0 + F * tail * (1.0 + 3e-5) + (double)V * 0x1p-40) * (1.0 + 1e-9);
+        const double Sup = (1.0 + F * tail + (double)V * 0x1p-40) * (1.0 + 1e-9);
         fast = Sup * tv.topp < 1.0 - 1e-15;
       }
       ST_PH(2);
@@ -380,7 +398,7 @@ __global__ void __launch_bounds__(SG_THREADS, 1) stage_kernel(StageArgs a) {
         // the stage is free (only m and amax are needed now): start the next row's load while
         // the tokens are written
         ST_PH(2);
-        if (gw == 0) sg_pop(sm, G, g, lane);
+        if (gw == SG_POPW) sg_pop(sm, G, g, lane);
         ST_PH(11);
         popped = true;
         write_tok(amax);
@@ -401,16 +419,11 @@ __global__ void __launch_bounds__(SG_THREADS, 1) stage_kernel(StageArgs a) {
         ec.md = (double)m;
         ec.L16 = 16.0 * Ld;
         const uint32_t km = key16(__float_as_uint(m));
-        // S >= max(1, S_fast / 1.25): the FAST estimate is within F <= 1.14 of the truth
-        const double slo = fmax(Sfast / 1.25, 1.0);
-        // (z_lo only sizes the exact histogram: a cut outside it is detected and requeued,
-        // so fp32 log2 and a multiply by T ln 2 are as good as fp64 here)
-        const float alo = log2f(fmaxf((float)(0.5 * (1.0 - tv.topp) * slo) / (float)V, 1e-37f));
-        int nb_eff = SG_NB;
-        {
-          const float zl = m + alo * (float)(tv.T * kLn2);
-          if (zl > -INFINITY) nb_eff = (int)min((uint32_t)SG_NB, km - key16(__float_as_uint(zl)) + 1u);
-        }
+        // the exact histogram spans the SG_NB classes (bf16 values) below the max: every value
+        // there is counted exactly, everything further down is the "tail" (a cut outside the
+        // histogram is detected and requeued).  A fixed span lets one packed min clamp every
+        // offset >= SG_NB onto the lane's dump bin.
+        const int nb_eff = SG_NB;
         // e = ex2(fl(z Lf - fl(m Lf))) / ex2(fl(m Lf - fl(m Lf))): the common rounding of m Lf
         // cancels in the ratio, the rest weighs |a|
         const float nmL = -(m * Lf);
@@ -425,6 +438,7 @@ __global__ void __launch_bounds__(SG_THREADS, 1) stage_kernel(StageArgs a) {
           // offsets of both halves at once: bits(m) - bits(z) per 16-bit lane (VIADD.16x2);
           // negative z wrap to >= bits(m) + 1 > nb_eff, never a kept class
           const uint32_t mb2 = (mb16 | (mb16 << 16)) + 0x00010001u;
+          const uint32_t dump2 = (uint32_t)(SG_NB + lane) * 0x00010001u;
           #pragma unroll 4
           for (int v = gt; v < nvec; v += SG_GT) {
             const uint4 q = R[v];
@@ -434,10 +448,13 @@ __global__ void __launch_bounds__(SG_THREADS, 1) stage_kernel(StageArgs a) {
 #pragma unroll
             for (int k = 0; k < 4; ++k) {
               o[k] = __vadd2(~w[k], mb2);
+              // histogram bins: offsets clamped (one packed min) to the lane's dump bin; bins in
+              // [nb_eff, SG_NB) also count tail elements and are never read
+              const uint32_t hc = __vminu2(o[k], dump2);
+              atomicAdd(&G.hist[hc & 0xffffu], 1u);
+              atomicAdd(&G.hist[hc >> 16], 1u);
               const uint32_t ol = o[k] & 0xffffu, oh = o[k] >> 16;
               const bool il = ol < (uint32_t)nb_eff, ih = oh < (uint32_t)nb_eff;
-              atomicAdd(&G.hist[il ? ol : SG_NB + lane], 1u);
-              atomicAdd(&G.hist[ih ? oh : SG_NB + lane], 1u);
               const float el = ex2_approx(fmaf(lo_f(w[k]), Lf, nmL));  // -inf -> 0
               const float eh = ex2_approx(fmaf(hi_f(w[k]), Lf, nmL));
               e8[2 * k] = il ? 0.0f : el;
@@ -457,8 +474,8 @@ __global__ void __launch_bounds__(SG_THREADS, 1) stage_kernel(StageArgs a) {
             for (int k = 0; k < 4; ++k) {
               const uint32_t ol = km - key16(w[k] << 16), oh = km - key16(w[k] & 0xffff0000u);
               const bool il = ol < (uint32_t)nb_eff, ih = oh < (uint32_t)nb_eff;
-              atomicAdd(&G.hist[il ? ol : SG_NB + lane], 1u);
-              atomicAdd(&G.hist[ih ? oh : SG_NB + lane], 1u);
+              atomicAdd(&G.hist[min(ol, (uint32_t)(SG_NB + lane))], 1u);
+              atomicAdd(&G.hist[min(oh, (uint32_t)(SG_NB + lane))], 1u);
               const float el = ex2_approx(fmaf(lo_f(w[k]), Lf, nmL));
               const float eh = ex2_approx(fmaf(hi_f(w[k]), Lf, nmL));
               e8[2 * k] = il ? 0.0f : el;
@@ -588,6 +605,9 @@ __global__ void __launch_bounds__(SG_THREADS, 1) stage_kernel(StageArgs a) {
             if (G.cut_ok != 0 || bstar == INT_MAX) break;
             if (pass == 0 && gt == 0) atomicAdd(&a.counters[7], 1ull);  // precise tails computed
           }
+          // the cut class's table entry is zeroed: C and D clamp every offset >= bs onto it
+          // (its value stays in G.cut_e)
+          if (gt == 0 && G.cut_ok == 1) G.ev[G.cut_b] = 0.0;
           gbar(g);
           ST_PH(5);
           if (G.cut_ok != 1) {
@@ -602,6 +622,7 @@ __global__ void __launch_bounds__(SG_THREADS, 1) stage_kernel(StageArgs a) {
             // turns the ranges into prefixes P_t (tie ranks: the first js cut-class elements
             // in id order are kept, so the ties before range t contribute min(js, tb_t) es)
             const uint32_t bs = (uint32_t)G.cut_b;
+            const uint32_t bs2 = bs | (bs << 16);
             const int js = G.cut_j;
             const double es = G.cut_e;
             const int Rv = (nvec + SG_GT - 1) / SG_GT;  // vectors per range (25 at V = 32000)
@@ -623,12 +644,12 @@ __global__ void __launch_bounds__(SG_THREADS, 1) stage_kernel(StageArgs a) {
 #pragma unroll
               for (int k = 0; k < SG_RB; ++k) {
 #pragma unroll
-                for (int j = 0; j < 8; ++j) {
-                  const uint32_t off = (j & 1) ? off_hi(w[k][j >> 1]) : off_lo(w[k][j >> 1]);
-                  const double e = pgather_nv(G.ev, off, off < bs);
-                  if (j & 1) a1 += e;
-                  else a0 += e;
-                  mc += (off == bs);
+                for (int h = 0; h < 4; ++h) {
+                  // offsets >= bs clamped (one packed min) onto the zeroed entry bs
+                  const uint32_t c = __vminu2(w[k][h], bs2);
+                  a0 += G.ev[c & 0xffffu];
+                  a1 += G.ev[c >> 16];
+                  mc += (int)(off_lo(w[k][h]) == bs) + (int)(off_hi(w[k][h]) == bs);
                 }
               }
               ma += a0 + a1;
@@ -704,12 +725,11 @@ __global__ void __launch_bounds__(SG_THREADS, 1) stage_kernel(StageArgs a) {
                 double a0 = 0.0, a1 = 0.0;
                 int c = 0;
 #pragma unroll
-                for (int j = 0; j < 8; ++j) {
-                  const uint32_t off = (j & 1) ? off_hi(w[j >> 1]) : off_lo(w[j >> 1]);
-                  const double e = pgather_nv(G.ev, off, off < bs);
-                  if (j & 1) a1 += e;
-                  else a0 += e;
-                  c += (off == bs);
+                for (int h = 0; h < 4; ++h) {
+                  const uint32_t cl = __vminu2(w[h], bs2);
+                  a0 += G.ev[cl & 0xffffu];
+                  a1 += G.ev[cl >> 16];
+                  c += (int)(off_lo(w[h]) == bs) + (int)(off_hi(w[h]) == bs);
                 }
                 mk[k] = a0 + a1;
                 tk[k] = c;
@@ -780,7 +800,7 @@ __global__ void __launch_bounds__(SG_THREADS, 1) stage_kernel(StageArgs a) {
             gbar(g);
             // the stage is free: the next row's load overlaps the kept count and the requeue
             ST_PH(7);
-            if (gw == 0) sg_pop(sm, G, g, lane);
+            if (gw == SG_POPW) sg_pop(sm, G, g, lane);
             ST_PH(11);
             popped = true;
             if (G.uncertain) {
@@ -800,7 +820,7 @@ __global__ void __launch_bounds__(SG_THREADS, 1) stage_kernel(StageArgs a) {
     if (requeue_task && gt == 0) requeue(a, task_id);
     gbar(g);  // the group is done with its stage
     ST_PH(8);
-    if (gw == 0 && !popped) sg_pop(sm, G, g, lane);
+    if (gw == SG_POPW && !popped) sg_pop(sm, G, g, lane);
     ST_PH(11);
   }
   if (prof)

@@ -64,6 +64,20 @@ __device__ __forceinline__ float bacc2(float acc, uint32_t e) {
       : "r"(e));
   return acc;
 }
+__device__ __forceinline__ uint32_t badd2(uint32_t a, uint32_t b) {
+  uint32_t r;
+  asm("add.rn.bf16x2 %0, %1, %2;" : "=r"(r) : "r"(a), "r"(b));
+  return r;
+}
+// acc + lo(e) / acc + hi(e): one bf16 half added straight into fp32 (FHADD.BF16)
+__device__ __forceinline__ float bacc_lo(float acc, uint32_t e) {
+  asm("{\n .reg .b16 lo, hi;\n mov.b32 {lo, hi}, %1;\n add.rn.f32.bf16 %0, lo, %0;\n}" : "+f"(acc) : "r"(e));
+  return acc;
+}
+__device__ __forceinline__ float bacc_hi(float acc, uint32_t e) {
+  asm("{\n .reg .b16 lo, hi;\n mov.b32 {lo, hi}, %1;\n add.rn.f32.bf16 %0, hi, %0;\n}" : "+f"(acc) : "r"(e));
+  return acc;
+}
 __device__ __forceinline__ uint32_t bf16_bits(float f) { return (uint32_t)f32_to_bf16_bits(f); }
 __device__ __forceinline__ float lo_f(uint32_t w) { return __uint_as_float(w << 16); }
 __device__ __forceinline__ float hi_f(uint32_t w) { return __uint_as_float(w & 0xffff0000u); }
