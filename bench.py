@@ -417,6 +417,74 @@ def run_ours(args, cfg, rank, world, dev):
     return res
 
 
+def run_windowed(args, cfg, rank, world, dev):
+    """C1/C2 step-wise replay in windows of ``--window`` positions (LogitsCache.replay_windowed):
+    rows are resampled only while a branch of the request is still replaying, so the line's
+    metric is ACCEPTED tokens/s (the replayed tokens the engine keeps, engine.py:296-331).  The
+    full replay (resample every cached position, bench default) gives the same replayed_len /
+    diverged_at; that equality is checked after the timed region."""
+    import torch
+
+    import paper_2604_17353_b200 as lcb
+
+    w = setup_workload(cfg, dev, rank, world)
+    cache = w["cache"]
+    V, n_req, nb, R = cfg["V"], cfg["n_req"], cfg["nb"], cfg["R"]
+    esz = 2 if cfg["dtype"] == "bfloat16" else 4
+    counters = torch.zeros(8, dtype=torch.int64, device=dev)
+    def step():
+        slot, gen, ln, vv = cache.lookup_batch(w["digests"])
+        tok, rep, div, nwin = cache.replay_windowed(slot, gen, ln, vv, R, nb, w["seeds"], w["T"], w["K"], w["P"],
+                                                    window=args.window, counters=counters, bufs=w["bufs"])
+        return tok, rep, div, nwin
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize(dev)
+    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(dev.index) as clk:
+        t0.record()
+        wins = 0
+        for _ in range(args.steps):
+            tok, rep, div, nwin = step()
+            wins += nwin
+        t1.record()
+        torch.cuda.synchronize(dev)
+    ms = t0.elapsed_time(t1)
+    rep_w, div_w = rep.clone(), div.clone()
+    accepted = int(rep_w.sum().item())
+    rows_per_step = n_req * min(R, wins // args.steps * args.window)  # upper bound on rows resampled
+    # equality with the full replay (untimed)
+    _, rep_f, div_f, _, _ = cache.replay_stepwise(w["digests"], R, nb, w["seeds"], w["T"], w["K"], w["P"])
+    same = bool(torch.equal(rep_f, rep_w) and torch.equal(div_f, div_w))
+    if rank != 0:
+        return None
+    return {
+        "metric": "accepted_tokens_per_s",
+        "value": accepted * args.steps * world / (ms * 1e-3),
+        "unit": "tokens/s",
+        "n_gpus": world,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": ms / args.steps,
+        "higher_is_better": True,
+        "scaling": cfg["scaling"],
+        "vs_baseline": None,
+        "dtype": "bf16" if esz == 2 else "f32",
+        "data": "synthetic (reference producer fill_logits, seed 7, conc 2.5, range 5.0)",
+        "config": {**workload_config(args, CONFIGS[args.config], world), "window": args.window},
+        "accepted_tokens_per_step": accepted,
+        "windows_per_step": wins / args.steps,
+        "rows_resampled_per_step_max": rows_per_step,
+        "equals_full_replay": same,
+        "precise_tasks": int(counters[0].item()),
+        "note": "windowed step-wise replay: same replayed_len/diverged_at as the full replay (checked); "
+                "one host read of the live-branch count per window",
+        "gpu_launches": None,
+        "clocks": clk.summary(),
+    }
+
+
 # ------------------------------------------------------------------------ check leg (untimed)
 
 
@@ -1010,7 +1078,8 @@ def main():
                     help="skip the untimed oracle validation leg (c4: the op-trace replay)")
     ap.add_argument("--check-draws", type=int, default=None,
                     help="draws the check leg validates (default 10M at V=32000, 100K for the wide configs)")
-    ap.add_argument("--policy", default="step_wise", choices=["step_wise", "hotspot"],
+    ap.add_argument("--window", type=int, default=8, help="positions per window for --policy windowed")
+    ap.add_argument("--policy", default="step_wise", choices=["step_wise", "hotspot", "windowed"],
                     help="replay policy of the resample step (ReplayPolicy)")
     ap.add_argument("--miss-path", default="fused", choices=["fused", "staged"],
                     help="c3 sweep miss path: producer straight into the slab (f1) or via staging rows + copy")
@@ -1061,7 +1130,7 @@ def main():
     elif args.config == "c3" and args.hit_ratio is not None:
         res = run_c3_sweep(args, cfg, rank, world, dev)
     else:
-        res = run_ours(args, cfg, rank, world, dev)
+        res = (run_windowed if args.policy == "windowed" else run_ours)(args, cfg, rank, world, dev)
     if rank == 0:
         print(json.dumps(res), flush=True)
     if world > 1:

@@ -29,7 +29,7 @@
 extern "C" {
 #endif
 
-#define LC_ABI_VERSION 3
+#define LC_ABI_VERSION 4
 
 typedef enum lc_status {
   LC_OK = 0,
@@ -292,6 +292,28 @@ int lc_replay_tasks(const int32_t* d_slot, const int32_t* d_len, const int32_t* 
  * replayed_len and diverged_at (-1 = none) per (r, b).                        */
 int lc_replay_accept(const int32_t* d_tokens, const int32_t* d_cached, const int32_t* d_len, int64_t n_req,
                      int32_t max_pos, int32_t n_branch, int32_t* d_replayed, int32_t* d_diverged, void* stream);
+
+/* Windowed step-wise replay: the acceptance of lc_replay_accept evaluated W
+ * positions at a time, so rows are resampled only while a branch of the request
+ * is still replaying (same replayed_len / diverged_at / accepted tokens as the
+ * full replay; engine.py:296-331).  lc_replay_window_init sets replayed 0,
+ * diverged -1, d_live[r] = n_branch for requests with a cached prefix (else 0)
+ * and *d_n_live = their sum.  lc_replay_window_tasks writes n_req*window tasks
+ * (task r*window + k = row (slot, w0 + k), the draws of lc_replay_tasks' task
+ * r*max_pos + w0 + k; empty when the request has no live branch or past the
+ * limit).  lc_replay_window_accept advances the live branches through the
+ * window's draws and decrements d_live / *d_n_live for every branch that
+ * diverges or reaches the limit; the caller stops when *d_n_live == 0.        */
+int lc_replay_window_init(const int32_t* d_len, int64_t n_req, int32_t max_pos, int32_t n_branch,
+                          int32_t* d_replayed, int32_t* d_diverged, int32_t* d_live, int32_t* d_n_live,
+                          void* stream);
+int lc_replay_window_tasks(const int32_t* d_slot, const int32_t* d_len, const int32_t* d_vocab,
+                           const int32_t* d_live, int64_t n_req, int32_t max_pos, int32_t n_branch, int32_t w0,
+                           int32_t window, const double* d_temperature, const int32_t* d_top_k,
+                           const double* d_top_p, lc_task* d_tasks, void* stream);
+int lc_replay_window_accept(const int32_t* d_tokens, const int32_t* d_cached, const int32_t* d_len, int64_t n_req,
+                            int32_t max_pos, int32_t n_branch, int32_t w0, int32_t window, int32_t* d_replayed,
+                            int32_t* d_diverged, int32_t* d_live, int32_t* d_n_live, void* stream);
 
 /* Hotspot replay policy (engine.py:311-326, ReplayPolicy.HOTSPOT).
  * d_draw_index[r*max_pos + t] = number of hotspots of request r before t when

@@ -14,7 +14,7 @@ from . import build as _build
 from .errors import CapacityError, ConfigError
 
 LC_OK, LC_E_CONFIG, LC_E_ZERO_MASS, LC_E_CAPACITY, LC_E_CUDA, LC_E_ARG, LC_E_STATE = range(7)
-ABI_VERSION = 3
+ABI_VERSION = 4
 LC_F32, LC_BF16 = 0, 1
 LC_DRAW_PRECISE, LC_DRAW_UNRESOLVED, LC_DRAW_BAD_ROW = 1, 2, 4
 
@@ -143,6 +143,9 @@ _SIGS = {
     "lc_replay_tasks_hotspot": (C.c_int, [P, P, P, P, I64, I32, I32, P, P, P, P, P]),
     "lc_replay_accept_hotspot": (C.c_int, [P, P, P, P, I64, I32, I32, P, P, P]),
     "lc_replay_tasks_hotspot_list": (C.c_int, [P, P, P, P, P, I64, I32, I32, P, P, P, P, P]),
+    "lc_replay_window_init": (C.c_int, [P, I64, I32, I32, P, P, P, P, P]),
+    "lc_replay_window_tasks": (C.c_int, [P, P, P, P, I64, I32, I32, I32, I32, P, P, P, P, P]),
+    "lc_replay_window_accept": (C.c_int, [P, P, P, I64, I32, I32, I32, I32, P, P, P, P, P]),
 }
 
 

@@ -141,6 +141,83 @@ __global__ void replay_accept_hot_kernel(int32_t* __restrict__ tok, const int32_
   if (diverged) diverged[i] = div;
 }
 
+
+// Windowed step-wise replay: the same acceptance (engine.py:296-331), evaluated W positions at a
+// time so that rows are resampled only while one of the request's branches is still replaying
+// (live[r] = its branches that neither diverged nor reached the limit).  Task j = r * W + k of
+// window w0 is row (slot, w0 + k) with the draws of lc_replay_tasks' task r * max_pos + w0 + k,
+// so tokens land where the full replay puts them.
+__global__ void replay_window_init_kernel(const int32_t* __restrict__ len, int64_t n_req, int max_pos, int nb,
+                                          int32_t* __restrict__ replayed, int32_t* __restrict__ diverged,
+                                          int32_t* __restrict__ live, int32_t* __restrict__ n_live) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n_req * (int64_t)nb) return;
+  const int64_t r = i / nb;
+  replayed[i] = 0;
+  diverged[i] = -1;
+  if (i % nb == 0) {
+    const int lv = min(len[r], max_pos) > 0 ? nb : 0;
+    live[r] = lv;
+    if (lv) atomicAdd(n_live, lv);
+  }
+}
+
+__global__ void replay_window_tasks_kernel(const int32_t* __restrict__ slot, const int32_t* __restrict__ len,
+                                           const int32_t* __restrict__ vocab, const int32_t* __restrict__ live,
+                                           int64_t n_req, int max_pos, int nb, int w0, int W,
+                                           const double* __restrict__ temp, const int32_t* __restrict__ topk,
+                                           const double* __restrict__ topp, lc_task* __restrict__ tasks) {
+  const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= n_req * (int64_t)W) return;
+  const int64_t r = j / W;
+  const int t = w0 + (int)(j % W);
+  const int s = slot[r];
+  const int lim = s >= 0 ? min(len[r], max_pos) : 0;
+  const int64_t i = r * max_pos + min(t, max_pos - 1);
+  lc_task tk;
+  tk.row = -1;
+  tk.slot = s;
+  tk.pos = t;
+  tk.temperature = temp[r];
+  tk.top_k = topk[r];
+  tk.vocab = (vocab && s >= 0) ? vocab[r] : 0;
+  tk.top_p = topp[r];
+  tk.draw_begin = i * nb;
+  tk.draw_end = (t < lim && live[r] > 0) ? i * nb + nb : i * nb;
+  tk.seed_base = r * nb;
+  tk.u_index = t;
+  tasks[j] = tk;
+}
+
+__global__ void replay_window_accept_kernel(const int32_t* __restrict__ tok, const int32_t* __restrict__ cached,
+                                            const int32_t* __restrict__ len, int64_t n_req, int max_pos, int nb,
+                                            int w0, int W, int32_t* __restrict__ replayed,
+                                            int32_t* __restrict__ diverged, int32_t* __restrict__ live,
+                                            int32_t* __restrict__ n_live) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n_req * (int64_t)nb) return;
+  const int64_t r = i / nb;
+  const int b = (int)(i % nb);
+  const int lim = min(len[r], max_pos);
+  int rep = replayed[i];
+  if (diverged[i] >= 0 || rep != w0 || rep >= lim) return;  // not live in this window
+  const int t1 = min(w0 + W, lim);
+  int div = -1;
+  for (int t = w0; t < t1; ++t) {
+    rep = t + 1;
+    if (tok[((r * max_pos) + t) * (int64_t)nb + b] != cached[r * max_pos + t]) {
+      div = t;
+      break;
+    }
+  }
+  replayed[i] = rep;
+  if (div >= 0) diverged[i] = div;
+  if (div >= 0 || rep >= lim) {
+    atomicSub(&live[r], 1);
+    atomicSub(n_live, 1);
+  }
+}
+
 }  // namespace lcb
 
 extern "C" int lc_replay_tasks_hotspot(const int32_t* d_slot, const int32_t* d_len, const int32_t* d_vocab,
@@ -209,6 +286,48 @@ extern "C" int lc_replay_accept(const int32_t* d_tokens, const int32_t* d_cached
   if (!d_tokens || !d_cached || !d_len || !d_replayed) return LC_E_ARG;
   lcb::replay_accept_kernel<<<lcb::ceil_div(n, 256), 256, 0, (cudaStream_t)stream>>>(
       d_tokens, d_cached, d_len, n_req, max_pos, n_branch, d_replayed, d_diverged);
+  LCB_CUDA_TRY(cudaGetLastError());
+  return LC_OK;
+}
+
+extern "C" int lc_replay_window_init(const int32_t* d_len, int64_t n_req, int32_t max_pos, int32_t n_branch,
+                                     int32_t* d_replayed, int32_t* d_diverged, int32_t* d_live, int32_t* d_n_live,
+                                     void* stream) {
+  if (n_req < 0 || max_pos < 0 || n_branch < 0) return LC_E_ARG;
+  if (!d_len || !d_replayed || !d_diverged || !d_live || !d_n_live) return LC_E_ARG;
+  LCB_CUDA_TRY(cudaMemsetAsync(d_n_live, 0, sizeof(int32_t), (cudaStream_t)stream));
+  const int64_t n = n_req * (int64_t)n_branch;
+  if (n == 0) return LC_OK;
+  lcb::replay_window_init_kernel<<<lcb::ceil_div(n, 256), 256, 0, (cudaStream_t)stream>>>(
+      d_len, n_req, max_pos, n_branch, d_replayed, d_diverged, d_live, d_n_live);
+  LCB_CUDA_TRY(cudaGetLastError());
+  return LC_OK;
+}
+
+extern "C" int lc_replay_window_tasks(const int32_t* d_slot, const int32_t* d_len, const int32_t* d_vocab,
+                                      const int32_t* d_live, int64_t n_req, int32_t max_pos, int32_t n_branch,
+                                      int32_t w0, int32_t window, const double* d_temperature,
+                                      const int32_t* d_top_k, const double* d_top_p, lc_task* d_tasks, void* stream) {
+  if (n_req < 0 || max_pos <= 0 || n_branch < 0 || w0 < 0 || window <= 0) return LC_E_ARG;
+  const int64_t n = n_req * (int64_t)window;
+  if (n == 0) return LC_OK;
+  if (!d_slot || !d_len || !d_live || !d_temperature || !d_top_k || !d_top_p || !d_tasks) return LC_E_ARG;
+  lcb::replay_window_tasks_kernel<<<lcb::ceil_div(n, 256), 256, 0, (cudaStream_t)stream>>>(
+      d_slot, d_len, d_vocab, d_live, n_req, max_pos, n_branch, w0, window, d_temperature, d_top_k, d_top_p, d_tasks);
+  LCB_CUDA_TRY(cudaGetLastError());
+  return LC_OK;
+}
+
+extern "C" int lc_replay_window_accept(const int32_t* d_tokens, const int32_t* d_cached, const int32_t* d_len,
+                                       int64_t n_req, int32_t max_pos, int32_t n_branch, int32_t w0, int32_t window,
+                                       int32_t* d_replayed, int32_t* d_diverged, int32_t* d_live, int32_t* d_n_live,
+                                       void* stream) {
+  if (n_req < 0 || max_pos < 0 || n_branch < 0 || w0 < 0 || window <= 0) return LC_E_ARG;
+  const int64_t n = n_req * (int64_t)n_branch;
+  if (n == 0) return LC_OK;
+  if (!d_tokens || !d_cached || !d_len || !d_replayed || !d_diverged || !d_live || !d_n_live) return LC_E_ARG;
+  lcb::replay_window_accept_kernel<<<lcb::ceil_div(n, 256), 256, 0, (cudaStream_t)stream>>>(
+      d_tokens, d_cached, d_len, n_req, max_pos, n_branch, w0, window, d_replayed, d_diverged, d_live, d_n_live);
   LCB_CUDA_TRY(cudaGetLastError());
   return LC_OK;
 }

@@ -1661,6 +1661,9 @@ rowwarp_kernel(const char* __restrict__ rows, int64_t row_bytes, int Vdef, const
   double* L_e = scr.e + (int64_t)gw * scr.cap;
 
   for (;;) {
+    // (the previous task's reads of the warp's shared scratch are ordered before this task's
+    // writes: lanes may otherwise run ahead under independent thread scheduling)
+    __syncwarp();
     // dynamic scheduling: tasks differ wildly in cost (fast exit vs big nucleus)
     int task_id = 0;
     if (lane == 0) task_id = atomicAdd(scr.next, 1);

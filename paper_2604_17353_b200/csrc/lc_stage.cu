@@ -43,6 +43,7 @@ constexpr int SG_NU = 32;                        // uniforms precomputed per tas
 constexpr int SG_ND = 64;                        // draws per task handled here (more: CTA kernel)
 constexpr int SG_PB = 8;                         // tasks per producer grab
 constexpr int SG_FQ = 6;                         // task FIFO slots
+constexpr int SG_NCK = 4;                        // a row arrives as 4 bulk copies (A starts on the first)
 constexpr int SG_POPW = SG_GW - 1;               // the group warp that pops tasks (it writes no tokens for <= 128 draws)
 constexpr int SG_RB = 5;                         // C: vectors per batch of independent loads
 constexpr int SG_RQ = ((SG_MAXV / 8 + SG_GW * 32 - 1) / (SG_GW * 32) + 3) / 4;  // D: vectors per quarter range (7)
@@ -86,7 +87,7 @@ struct __align__(128) SgSmem {
   int pbt[SG_PB];
   double pbu[SG_PB][SG_NU];
   double t16[16];
-  unsigned long long full[SG_GROUPS];
+  unsigned long long full[SG_GROUPS][4];  // per group: one mbarrier per quarter of the row
 };
 static_assert(sizeof(SgSmem) <= 232448, "staged kernel shared memory");
 static_assert((SG_MAXV / 8 + SG_GT - 1) / SG_GT <= 32, "argmax search: one lane per vector of a thread");
@@ -182,11 +183,17 @@ __device__ void sg_pop(SgSmem& sm, SgGroup& G, int g, int lane) {
   __syncwarp();  // lane 0's acquire orders the other lanes' slot reads
   const int slot = h % SG_FQ;
   const int t = sm.fq_task[slot];
-  uint32_t bytes = 0;
+  int cv = 0, nv = 0;  // vectors per chunk, per row
   if (t >= 0) {
     if (lane == 0) {
-      bytes = (uint32_t)(sm.fq_tv[slot].V * 2);
-      bulk_load(sm.ring[g], sm.fq_tv[slot].row, bytes, &sm.full[g]);
+      nv = sm.fq_tv[slot].V >> 3;
+      cv = (nv + SG_NCK - 1) / SG_NCK;
+      const char* src = sm.fq_tv[slot].row;
+      for (int c = 0; c < SG_NCK; ++c) {
+        const int v0 = min(c * cv, nv), v1 = min(v0 + cv, nv);
+        if (v1 > v0)
+          bulk_load(sm.ring[g] + v0, src + (size_t)v0 * 16, (uint32_t)(v1 - v0) * 16u, &sm.full[g][c]);
+      }
     }
     G.su[lane] = sm.fq_u[slot][lane];
     warp_copy(G.tv, sm.fq_tv[slot], lane);
@@ -195,8 +202,12 @@ __device__ void sg_pop(SgSmem& sm, SgGroup& G, int g, int lane) {
   if (lane == 0) {
     G.task = t;
     st_release(&sm.fq_free[slot], h + SG_FQ);  // slot h released
-    if (t >= 0) mbar_expect_tx(&sm.full[g], bytes);  // release: G.task/tv/su visible to the group
-    else mbar_arrive(&sm.full[g]);  // completes the phase with no bytes: the group sees -1
+    // release: G.task/tv/su visible to the group (a sentinel completes the phases with no bytes)
+    for (int c = 0; c < SG_NCK; ++c) {
+      const int v0 = min(c * cv, nv), v1 = min(v0 + cv, nv);
+      if (v1 > v0) mbar_expect_tx(&sm.full[g][c], (uint32_t)(v1 - v0) * 16u);
+      else mbar_arrive(&sm.full[g][c]);
+    }
   }
   __syncwarp();
 }
@@ -206,13 +217,15 @@ __global__ void __launch_bounds__(SG_THREADS, 1) stage_kernel(StageArgs a) {
   SgSmem& sm = *reinterpret_cast<SgSmem*>(st_raw);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   if (tid == 0) {
-    for (int s = 0; s < SG_GROUPS; ++s) mbar_init(&sm.full[s], 1);
+    for (int s = 0; s < SG_GROUPS; ++s)
+      for (int c = 0; c < SG_NCK; ++c) mbar_init(&sm.full[s][c], 1);
     mbar_fence_init();
     sm.fq_tail = sm.fq_head = 0;
     for (int s = 0; s < SG_FQ; ++s) sm.fq_free[s] = s;
   }
   if (tid < 16) sm.t16[tid] = exp2((double)tid / 16.0);
   if (tid < 32 * SG_GROUPS) sm.g[tid >> 5].ev[SG_NB + (tid & 31)] = 0.0;
+  for (int i = tid; i < SG_GROUPS * SG_NB; i += SG_THREADS) sm.g[i / SG_NB].hist[i % SG_NB] = 0u;
   __syncthreads();
 
   if (warp == SG_PWARP) {
@@ -255,8 +268,9 @@ __global__ void __launch_bounds__(SG_THREADS, 1) stage_kernel(StageArgs a) {
   };
 
   if (gw == SG_POPW) sg_pop(sm, G, g, lane);
+  bool hist_dirty = false;
   for (uint32_t phase = 0;; phase ^= 1u) {
-    mbar_wait(&sm.full[g], phase);
+    mbar_wait(&sm.full[g][0], phase);
     ST_PH(0);
     const int task_id = G.task;
     if (task_id < 0) break;
@@ -268,12 +282,21 @@ __global__ void __launch_bounds__(SG_THREADS, 1) stage_kernel(StageArgs a) {
     // ------------------------------------------------ A: max (packed, NaN-propagating)
     // two packed running maxima per thread (3-input VHMNMX); the first argmax is searched only
     // where it is needed (FAST and greedy rows), by the threads whose maximum is the row's
+    // (the row arrives in SG_NCK chunks: each chunk is waited for right before its vectors)
     uint32_t am0 = 0xff80ff80u, am1 = 0xff80ff80u;  // (-inf, -inf)
-#pragma unroll 5
-    for (int v = gt; v < nvec; v += SG_GT) {
-      const uint4 q = R[v];
-      am0 = bmax2_nan(am0, bmax2_nan(q.x, q.y));
-      am1 = bmax2_nan(am1, bmax2_nan(q.z, q.w));
+    {
+      const int cv = (nvec + SG_NCK - 1) / SG_NCK;
+      int v = gt;
+      for (int c = 0; c < SG_NCK; ++c) {
+        if (c > 0) mbar_wait(&sm.full[g][c], phase);
+        const int v1 = min((c + 1) * cv, nvec);
+#pragma unroll 4
+        for (; v < v1; v += SG_GT) {
+          const uint4 q = R[v];
+          am0 = bmax2_nan(am0, bmax2_nan(q.x, q.y));
+          am1 = bmax2_nan(am1, bmax2_nan(q.z, q.w));
+        }
+      }
     }
     const uint32_t amx = bmax2_nan(am0, am1);
     const float tmax = max_nan(lo_f(amx), hi_f(amx));
@@ -410,7 +433,7 @@ __global__ void __launch_bounds__(SG_THREADS, 1) stage_kernel(StageArgs a) {
         // histogram of the values that can lie above the cut (z >= z_lo, with V e(z_lo) <=
         // (1 - top_p) S / 2), fp32 MUFU exponentials for the rest (the "tail", bounded), and
         // every element's class offset written over its logit (16 bits) in the stage
-        for (int b = gt; b < SG_NB; b += SG_GT) G.hist[b] = 0u;
+        hist_dirty = true;  // (zero on entry: cleared after the previous big row)
         ExpCtx ec;
         ec.m = m;
         ec.T = tv.T;
@@ -432,7 +455,6 @@ __global__ void __launch_bounds__(SG_THREADS, 1) stage_kernel(StageArgs a) {
         // positive domain (every class in range positive): offset = bits(m) - bits(z)
         const uint32_t mb16 = __float_as_uint(m) >> 16;
         const bool pos = m > 0.0f && (uint32_t)nb_eff <= mb16 && key16_to_f(km - (uint32_t)(nb_eff - 1)) > 0.0f;
-        gbar(g);  // hist zeroed
         double tacc = 0.0;
         if (pos) {
           // offsets of both halves at once: bits(m) - bits(z) per 16-bit lane (VIADD.16x2);
@@ -540,6 +562,7 @@ __global__ void __launch_bounds__(SG_THREADS, 1) stage_kernel(StageArgs a) {
           double EScut = Hm * relA + tail * (2.0 * kEx2Raw + kSum8Err + 1e-12 + amax_t * kLn2 * 0x1p-23) +
                          (double)V * 0x1p-126 + S * 64.0 * u53;
           int bstar = INT_MAX;
+          int cut_ok = 0;
           for (int pass = 0; pass < 2; ++pass) {
             if (pass == 1) {
               // PRECISE tail (rare: the FAST tail's bound left the cut undecided): every tail
@@ -574,9 +597,8 @@ __global__ void __launch_bounds__(SG_THREADS, 1) stage_kernel(StageArgs a) {
               }
             }
             bstar = gmin_i(cand, 0);
-            if (gt == 0) G.cut_ok = 0;
-            gbar(g);
-            if (bstar != INT_MAX && bstar / SGC == gt) {
+            if (bstar == INT_MAX) break;  // (uniform) no cut class in the histogram range
+            if (bstar / SGC == gt) {  // the owner of the cut class decides (0 uncertain, 1 ok, 2 +-0)
               double A = wpre + incl - tsum;
               int n = 0;
 #pragma unroll
@@ -596,25 +618,26 @@ __global__ void __launch_bounds__(SG_THREADS, 1) stage_kernel(StageArgs a) {
               bool zero_clash = false;
               if (kb == 0x8000u) zero_clash = bstar + 1 < nb_eff && G.hist[bstar + 1] > 0;
               if (kb == 0x7fffu) zero_clash = bstar >= 1 && G.hist[bstar - 1] > 0;
-              G.cut_ok = zero_clash ? 2 : (ok_hi && ok_lo);
+              const int ok = zero_clash ? 2 : (ok_hi && ok_lo);
+              G.cut_ok = ok;
               G.cut_b = bstar;
               G.cut_j = j;
               G.cut_e = e;
+              // the cut class's table entry is zeroed: C and D clamp every offset >= bs onto
+              // it (its value stays in G.cut_e)
+              if (ok == 1) G.ev[bstar] = 0.0;
             }
             gbar(g);
-            if (G.cut_ok != 0 || bstar == INT_MAX) break;
+            cut_ok = G.cut_ok;
+            if (cut_ok != 0) break;
             if (pass == 0 && gt == 0) atomicAdd(&a.counters[7], 1ull);  // precise tails computed
           }
-          // the cut class's table entry is zeroed: C and D clamp every offset >= bs onto it
-          // (its value stays in G.cut_e)
-          if (gt == 0 && G.cut_ok == 1) G.ev[G.cut_b] = 0.0;
-          gbar(g);
           ST_PH(5);
-          if (G.cut_ok != 1) {
+          if (cut_ok != 1) {
             requeue_task = true;
             // counters: 4 cut not certified (even with the precise tail), 6 no cut class in the
             // histogram range (or a +-0 cut); 7 counts precise-tail recomputations
-            if (gt == 0) atomicAdd(&a.counters[(bstar == INT_MAX || G.cut_ok == 2) ? 6 : 4], 1ull);
+            if (gt == 0) atomicAdd(&a.counters[(bstar == INT_MAX || cut_ok == 2) ? 6 : 4], 1ull);
           } else {
             // ---------------------------------------- C: every thread sums the kept mass of its
             // own contiguous range of Rv vectors (classes above the cut class, fp64 values
@@ -819,6 +842,10 @@ __global__ void __launch_bounds__(SG_THREADS, 1) stage_kernel(StageArgs a) {
     }
     if (requeue_task && gt == 0) requeue(a, task_id);
     gbar(g);  // the group is done with its stage
+    if (hist_dirty) {  // ready for the next big row (its H comes after at least one barrier)
+      for (int b = gt; b < SG_NB; b += SG_GT) G.hist[b] = 0u;
+      hist_dirty = false;
+    }
     ST_PH(8);
     if (gw == SG_POPW && !popped) sg_pop(sm, G, g, lane);
     ST_PH(11);

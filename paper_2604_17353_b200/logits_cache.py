@@ -394,6 +394,50 @@ class LogitsCache:
                         "lc_replay_accept_hotspot")
         return tok, b["rep"], b["div"]
 
+    def replay_windowed(self, slot, gen, ln, vv, max_pos: int, n_branch: int, seeds: torch.Tensor,
+                        temperature: torch.Tensor, top_k: torch.Tensor, top_p: torch.Tensor, window: int = 8,
+                        counters=None, bufs: dict | None = None):
+        """Step-wise replay (engine.py:296-331) evaluated ``window`` positions at a time on
+        lookup results: a request's rows are resampled only while one of its branches is still
+        replaying.  Same (tokens at accepted positions, replayed_len, diverged_at) as
+        ``replay_looked_up`` with no ``draw_index``; rows past every branch's divergence are
+        never read.  One small host read per window (the live-branch count) decides whether
+        the next window runs.  Returns (tokens, replayed_len, diverged_at, windows run)."""
+        n_req = slot.numel()
+        b = self._replay_bufs(bufs, n_req, max_pos, n_branch)
+        W = max(1, min(int(window), max_pos))
+        st = self._stream()
+        d = self.dev
+        if b.get("wshape") != (n_req, W):
+            b["wshape"] = (n_req, W)
+            b["wtasks"] = torch.empty(max(n_req * W, 1) * _capi.TASK_DTYPE.itemsize, dtype=torch.uint8, device=d)
+            b["live"] = torch.empty(max(n_req, 1), dtype=torch.int32, device=d)
+            b["nlive"] = torch.zeros(1, dtype=torch.int32, device=d)
+            b["nlive_h"] = torch.zeros(1, dtype=torch.int32, pin_memory=True)
+        ndraw = n_req * max_pos * n_branch
+        _capi.check(_capi.lib.lc_replay_window_init(ln.data_ptr(), n_req, max_pos, n_branch, b["rep"].data_ptr(),
+                                                    b["div"].data_ptr(), b["live"].data_ptr(), b["nlive"].data_ptr(),
+                                                    st), "lc_replay_window_init")
+        self._cached_tokens(slot, gen, b, st)
+        windows = 0
+        for w0 in range(0, max_pos, W):
+            _capi.check(_capi.lib.lc_replay_window_tasks(slot.data_ptr(), ln.data_ptr(), vv.data_ptr(),
+                                                         b["live"].data_ptr(), n_req, max_pos, n_branch, w0, W,
+                                                         temperature.data_ptr(), top_k.data_ptr(), top_p.data_ptr(),
+                                                         b["wtasks"].data_ptr(), st), "lc_replay_window_tasks")
+            sampling.resample(None, b["wtasks"], seeds=seeds, n_draws=ndraw, cache=self, counters=counters,
+                              out=(b["tok"], b["flags"]))
+            _capi.check(_capi.lib.lc_replay_window_accept(b["tok"].data_ptr(), b["cached"].data_ptr(), ln.data_ptr(),
+                                                          n_req, max_pos, n_branch, w0, W, b["rep"].data_ptr(),
+                                                          b["div"].data_ptr(), b["live"].data_ptr(),
+                                                          b["nlive"].data_ptr(), st), "lc_replay_window_accept")
+            windows += 1
+            b["nlive_h"].copy_(b["nlive"], non_blocking=True)  # (st is torch's current stream)
+            torch.cuda.current_stream(d).synchronize()
+            if int(b["nlive_h"][0]) == 0:
+                break
+        return b["tok"], b["rep"], b["div"], windows
+
     def _replay_bufs(self, bufs, n_req: int, max_pos: int, n_branch: int) -> dict:
         """Device buffers of a replay call, reused across calls of the same shape (a
         caller's ``bufs`` dict is rebuilt whenever (n_req, max_pos, n_branch) changes)."""

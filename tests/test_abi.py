@@ -43,7 +43,7 @@ def test_exports_are_exactly_the_header(tmp_path):
 def test_abi_version_and_status_strings():
     from paper_2604_17353_b200 import _capi
 
-    assert _capi.lib.lc_abi_version() == 3
+    assert _capi.lib.lc_abi_version() == 4
     assert _capi.lib.lc_status_string(6) == b"write-back prefix no longer live"
     assert _capi.lib.lc_status_string(0) == b"ok"
     assert _capi.lib.lc_status_string(1) == b"config error"

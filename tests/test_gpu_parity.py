@@ -789,3 +789,45 @@ def test_wide_kernel_matches_oracle_and_cta_kernel(V, conc, T, k, p, nd, monkeyp
     monkeypatch.setenv("LCB_NO_STAGE", "1")
     tok2, _, _ = _resample_rows(rows, T, k, p, ulists, dtype=torch.bfloat16)
     assert tok2.tolist() == tok.tolist()
+
+
+@pytest.mark.parametrize("window", [1, 3, 8, 64])
+def test_replay_windowed_equals_full_replay(window):
+    """Windowed step-wise replay (rows resampled only while a branch is live) gives the full
+    replay's replayed_len / diverged_at and the same tokens at every accepted position."""
+    V, n_req, L, nb, max_pos = 4096, 9, 40, 6, 32
+    cache = lcb.LogitsCache(1 << 30, vocab=V, dtype="bfloat16", max_rows=64)
+    keys = [mixing_ref.hash_tokens([r, 7, 1]) for r in range(n_req)]
+    rows = mixing_ref.bf16_round(mixing_ref.fill_rows_np([mixing_ref.mix2(9, i) for i in range(n_req * L)], V, 2.5))
+    rng = np.random.default_rng(4)
+    cached_tok = rng.integers(0, V, n_req * L).astype(np.int32)
+    # agree with the argmax for a request-dependent prefix so replays end at different windows
+    agree = np.arange(n_req * L) % L < (np.arange(n_req * L) // L) * 3
+    cached_tok = np.where(agree, rows.argmax(1), cached_tok).astype(np.int32)
+    lens = np.full(n_req, L, np.int32)
+    lens[2] = 5
+    lens[4] = 1
+    offs = (np.arange(n_req) * L).astype(np.int64)
+    cache.insert_batch(lcb._dev.u64_tensor(keys, DEV), torch.from_numpy(lens).to(DEV),
+                       torch.full((n_req,), V, dtype=torch.int32, device=DEV),
+                       torch.from_numpy(rows).to(DEV).to(torch.bfloat16), torch.from_numpy(offs).to(DEV),
+                       torch.from_numpy(cached_tok).to(DEV), L)
+    digests = lcb._dev.u64_tensor(keys + [999], DEV)  # the last request misses
+    n = n_req + 1
+    seeds = lcb._dev.u64_tensor([mixing_ref.mix2(3, b) for b in range(n * nb)], DEV)
+    T = torch.full((n,), 0.6, dtype=torch.float64, device=DEV)
+    K = torch.zeros(n, dtype=torch.int32, device=DEV)
+    Pp = torch.full((n,), 0.9, dtype=torch.float64, device=DEV)
+    tok_f, rep_f, div_f, slot, ln = cache.replay_stepwise(digests, max_pos, nb, seeds, T, K, Pp)
+    tok_f, rep_f, div_f = tok_f.clone(), rep_f.clone(), div_f.clone()
+    s2, g2, l2, v2 = cache.lookup_batch(digests)
+    tok_w, rep_w, div_w, nwin = cache.replay_windowed(s2, g2, l2, v2, max_pos, nb, seeds, T, K, Pp, window=window)
+    assert torch.equal(rep_w, rep_f) and torch.equal(div_w, div_f)
+    rep = rep_f.cpu().numpy().reshape(n, nb)
+    tf = tok_f.cpu().numpy().reshape(n, max_pos, nb)
+    tw = tok_w.cpu().numpy().reshape(n, max_pos, nb)
+    for r in range(n):
+        for b in range(nb):
+            assert np.array_equal(tf[r, : rep[r, b], b], tw[r, : rep[r, b], b]), (r, b)
+    assert nwin <= -(-max_pos // window)
+    assert rep.max() > window or window >= max_pos  # some replay crosses a window boundary
