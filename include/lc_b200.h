@@ -139,6 +139,10 @@ int lc_softmax(const void* d_rows, int dtype, int64_t vocab, int64_t row_stride,
 
 /* Per-row entropy (nats) and max probability of softmax(z, T), the hotspot
  * scores' inputs (sampling.py:112-126).                                       */
+/* Entropy -sum_{p>0} p ln p and max p of explicit probability rows
+ * (sampling.py:112-119, `entropy` / `max_prob`), one block per row.         */
+int lc_prob_stats(const double* d_probs, int64_t vocab, int64_t n_rows, int64_t row_stride, double* d_entropy,
+                  double* d_pmax, void* stream);
 int lc_row_entropy(const void* d_rows, int dtype, int64_t vocab, int64_t row_stride, int64_t n_rows,
                    double temperature, double* d_entropy, double* d_pmax, void* stream);
 

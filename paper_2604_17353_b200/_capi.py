@@ -143,6 +143,7 @@ _SIGS = {
     "lc_replay_tasks_hotspot": (C.c_int, [P, P, P, P, I64, I32, I32, P, P, P, P, P]),
     "lc_replay_accept_hotspot": (C.c_int, [P, P, P, P, I64, I32, I32, P, P, P]),
     "lc_replay_tasks_hotspot_list": (C.c_int, [P, P, P, P, P, I64, I32, I32, P, P, P, P, P]),
+    "lc_prob_stats": (C.c_int, [P, I64, I64, I64, P, P, P]),
     "lc_replay_window_init": (C.c_int, [P, I64, I32, I32, P, P, P, P, P]),
     "lc_replay_window_tasks": (C.c_int, [P, P, P, P, I64, I32, I32, I32, I32, P, P, P, P, P]),
     "lc_replay_window_accept": (C.c_int, [P, P, P, I64, I32, I32, I32, I32, P, P, P, P, P]),

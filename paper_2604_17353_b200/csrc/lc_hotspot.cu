@@ -153,6 +153,7 @@ hotspot_select_kernel(CacheDev c, const int32_t* __restrict__ slot, const uint32
   double* sv = hs_sm;       // s_t
   double* se = hs_sm + n;   // its bound
   int* sel = reinterpret_cast<int*>(hs_sm + 2 * n);
+  int* drop = sel + n;  // cap decisions, kept apart from sel while other threads still read it
   double lmn = INFINITY, lmx = -INFINITY, lem = 0.0;
   for (int t = threadIdx.x; t < n; t += HS_THREADS) {
     const int64_t sr = slab_row_of(c, s, t);
@@ -240,13 +241,13 @@ hotspot_select_kernel(CacheDev c, const int32_t* __restrict__ slot, const uint32
         if (sv[u] > sv[t] || (sv[u] == sv[t] && u < t)) ++rank;
         if (fabs(sv[u] - sv[t]) <= se[u] + se[t] && (se[u] + se[t]) > 0.0) close = true;
       }
-      sel[t] = rank < max_hot ? 1 : 2;  // 2: dropped by the cap (keep the mark until all ranks are known)
+      drop[t] = rank >= max_hot;  // (sel stays as read by the other threads' ranks)
       // an undecidable order only matters across the cap boundary
       if (close && (rank == max_hot - 1 || rank == max_hot)) atomicOr(&s_flag, 1);
     }
     __syncthreads();
     for (int t = threadIdx.x; t < n; t += HS_THREADS)
-      if (sel[t] == 2) sel[t] = 0;
+      if (sel[t] && drop[t]) sel[t] = 0;
     __syncthreads();
     cnt = max_hot;
   }
@@ -313,7 +314,7 @@ extern "C" int lc_cache_hotspots(lc_cache* cache, const int32_t* d_slot, const u
     return LC_E_ARG;
   if (n_entries == 0) return LC_OK;
   const int max_rows = cd->maxp * cd->page_rows;
-  const size_t smem = (size_t)max_rows * (2 * sizeof(double) + sizeof(int));
+  const size_t smem = (size_t)max_rows * (2 * sizeof(double) + 2 * sizeof(int));
   if (smem > 200 * 1024) return LC_E_CONFIG;
   static size_t attr = 0;
   if (smem > 48 * 1024 && smem > attr) {

@@ -39,11 +39,40 @@ __device__ double block_sum(double v, double* red) {
 }
 
 // softmax: s = f64(z)/T - max (sampling.py:65-66), e = exp(s), p = e / pairwise_sum(e)
+constexpr int PB_LEAVES = 2048;  // numpy pairwise-tree leaves summed in parallel (V <~ 130K; beyond: sequential)
+
+struct PbShared {
+  int2 lv[PB_LEAVES];
+  double ls[PB_LEAVES];
+  double bcast;
+  int nleaf;
+};
+
+// first index i with row[i] == m (block-wide min)
+template <int DT>
+__device__ int64_t block_first_eq(const char* row, int64_t V, float m, int64_t* red) {
+  int64_t a = INT64_MAX;
+  for (int64_t i = threadIdx.x; i < V && a == INT64_MAX; i += PB_THREADS)
+    if (ld<DT>(row, i) == m) a = i;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const int64_t y = __shfl_xor_sync(0xffffffffu, a, o);
+    a = y < a ? y : a;
+  }
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = a;
+  __syncthreads();
+  int64_t r = INT64_MAX;
+  for (int w = 0; w < PB_THREADS / 32; ++w) r = red[w] < r ? red[w] : r;
+  __syncthreads();
+  return r;
+}
+
 template <int DT>
 __global__ void __launch_bounds__(PB_THREADS)
 softmax_kernel(const char* rows, int64_t row_bytes, int64_t V, const double* temps, double* out) {
   __shared__ float fred[PB_THREADS / 32];
-  __shared__ double s_S;
+  __shared__ int64_t ired[PB_THREADS / 32];
+  __shared__ PbShared pb;
   const char* row = rows + blockIdx.x * row_bytes;
   double* o = out + blockIdx.x * V;
   const double T = temps[blockIdx.x];
@@ -51,48 +80,124 @@ softmax_kernel(const char* rows, int64_t row_bytes, int64_t V, const double* tem
   for (int64_t i = threadIdx.x; i < V; i += PB_THREADS) m = fmaxf(m, ld<DT>(row, i));
   m = block_max(m, fred);
   if (T == 0.0) {  // one-hot at the first argmax (sampling.py:61-64)
-    __shared__ int s_arg;
-    if (threadIdx.x == 0) {
-      int a = 0;
-      while (ld<DT>(row, a) != m) ++a;
-      s_arg = a;
-    }
-    __syncthreads();
-    for (int64_t i = threadIdx.x; i < V; i += PB_THREADS) o[i] = (i == s_arg) ? 1.0 : 0.0;
+    const int64_t arg = block_first_eq<DT>(row, V, m, ired);
+    for (int64_t i = threadIdx.x; i < V; i += PB_THREADS) o[i] = (i == arg) ? 1.0 : 0.0;
     return;
   }
   const double mT = __ddiv_rn((double)m, T);
   for (int64_t i = threadIdx.x; i < V; i += PB_THREADS) o[i] = exp(__dsub_rn(__ddiv_rn((double)ld<DT>(row, i), T), mT));
   __syncthreads();
-  if (threadIdx.x == 0) s_S = pairwise_seq(o, V);
-  __syncthreads();
-  const double S = s_S;
+  // e.sum() in numpy's pairwise tree: leaves in parallel, the tree combined in order
+  const double S = pairwise_block(o, V, pb.lv, pb.ls, PB_LEAVES, &pb.bcast, &pb.nleaf);
   for (int64_t i = threadIdx.x; i < V; i += PB_THREADS) o[i] = __ddiv_rn(o[i], S);
 }
 
 // sample(): total = pairwise_sum(q); cdf = sequential cumsum; first index with
 // cdf > u*total; clamp to V-1; back off over zeros (sampling.py:97-109).
-__global__ void draw_probs_kernel(const double* probs, int64_t V, int64_t stride, const double* u, int32_t* tok,
-                                  uint8_t* flags) {
-  if (threadIdx.x != 0) return;
+// One block per row: the total in numpy's pairwise tree (block-parallel); the
+// sequential cumsum's crossing is located from per-thread chunk sums (an
+// exclusive block scan), then walked inside the owning chunk; the decision is
+// certified against the rounding gap between that walk and numpy's sequential
+// cumsum (both within (i + 1) 2^-53 * total of the exact prefix), else the
+// sequential scan runs on one thread.
+__global__ void __launch_bounds__(PB_THREADS)
+draw_probs_kernel(const double* probs, int64_t V, int64_t stride, const double* u, int32_t* tok, uint8_t* flags) {
+  __shared__ PbShared pb;
+  __shared__ double dred[PB_THREADS / 32];
+  __shared__ int64_t s_idx;
+  __shared__ int s_unc;
   const double* q = probs + blockIdx.x * stride;
-  const double total = pairwise_seq(q, V);
+  const double total = pairwise_block(q, V, pb.lv, pb.ls, PB_LEAVES, &pb.bcast, &pb.nleaf);
   if (!(total > 0.0)) {
-    tok[blockIdx.x] = -1;
-    if (flags) flags[blockIdx.x] = LC_DRAW_BAD_ROW;
+    if (threadIdx.x == 0) {
+      tok[blockIdx.x] = -1;
+      if (flags) flags[blockIdx.x] = LC_DRAW_BAD_ROW;
+    }
     return;
   }
   const double t = u[blockIdx.x] * total;
-  double c = 0.0;
-  int64_t i = 0;
-  for (; i < V; ++i) {
-    c += q[i];
-    if (c > t) break;
+  const int64_t ch = (V + PB_THREADS - 1) / PB_THREADS;
+  const int64_t i0 = min((int64_t)threadIdx.x * ch, V), i1 = min(i0 + ch, V);
+  double cs = 0.0;
+  for (int64_t i = i0; i < i1; ++i) cs += q[i];
+  // exclusive block scan of the chunk sums
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  double incl = cs;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const double y = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += y;
   }
-  if (i >= V) i = V - 1;
-  while (i > 0 && q[i] == 0.0) --i;
-  tok[blockIdx.x] = (int32_t)i;
-  if (flags) flags[blockIdx.x] = 0;
+  if (lane == 31) dred[w] = incl;
+  if (threadIdx.x == 0) {
+    s_idx = V;  // "never crossed": the reference clamps to V - 1
+    s_unc = 0;
+  }
+  __syncthreads();
+  double pre = incl - cs;
+  for (int k = 0; k < w; ++k) pre += dred[k];
+  const double eps = 4.0 * (double)(V + 2) * 0x1p-53 * total;  // both cumsums' gap to the exact prefix
+  // the chunk whose (approximate) range holds t walks it; chunks near t on either side flag
+  if (pre - eps <= t && t < pre + cs + eps && i1 > i0) {
+    double c = pre;
+    int64_t i = i0;
+    for (; i < i1; ++i) {
+      c += q[i];
+      if (c > t) break;
+    }
+    if (i < i1) {
+      const double cprev = c - q[i];
+      if (!(c - t > eps) || !(t - cprev >= eps)) s_unc = 1;
+      else atomicMin(reinterpret_cast<unsigned long long*>(&s_idx), (unsigned long long)i);
+    } else if (!(t - c >= eps)) {
+      s_unc = 1;
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int64_t i = s_idx;
+    if (s_unc) {  // undecided within the rounding gap: numpy's sequential cumsum
+      double c = 0.0;
+      for (i = 0; i < V; ++i) {
+        c += q[i];
+        if (c > t) break;
+      }
+    }
+    if (i >= V) i = V - 1;
+    while (i > 0 && q[i] == 0.0) --i;
+    tok[blockIdx.x] = (int32_t)i;
+    if (flags) flags[blockIdx.x] = 0;
+  }
+}
+
+// Entropy and max of explicit probability rows (sampling.py:112-126):
+// H = -sum_{p > 0} p ln p, pmax = max p (one block per row).
+__global__ void __launch_bounds__(PB_THREADS)
+prob_stats_kernel(const double* probs, int64_t V, int64_t stride, double* H, double* pmax) {
+  __shared__ double dred[PB_THREADS / 32];
+  const double* q = probs + blockIdx.x * stride;
+  double h = 0.0, mx = -INFINITY;
+  for (int64_t i = threadIdx.x; i < V; i += PB_THREADS) {
+    const double p = q[i];
+    if (p > 0.0) h -= p * log(p);
+    mx = fmax(mx, p);
+  }
+  h = warp_sum(h);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+  if ((threadIdx.x & 31) == 0) dred[threadIdx.x >> 5] = h;
+  __syncthreads();
+  double hs = 0.0;
+  for (int k = 0; k < PB_THREADS / 32; ++k) hs += dred[k];
+  __syncthreads();
+  if ((threadIdx.x & 31) == 0) dred[threadIdx.x >> 5] = mx;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double m = -INFINITY;
+    for (int k = 0; k < PB_THREADS / 32; ++k) m = fmax(m, dred[k]);
+    H[blockIdx.x] = hs + 0.0;  // (-0 -> +0: a one-hot row has entropy 0.0)
+    pmax[blockIdx.x] = m;
+  }
 }
 
 // H = -sum p ln p = ln S - sum(e*s)/S with s <= 0 the shifted scaled logits;
@@ -184,8 +289,18 @@ extern "C" int lc_draw_probs(const double* d_probs, int64_t vocab, int64_t n_row
                              const double* d_u, int32_t* d_token, uint8_t* d_flags, void* stream) {
   if (n_rows < 0 || vocab < 1 || (n_rows > 0 && (!d_probs || !d_u || !d_token))) return LC_E_ARG;
   if (n_rows == 0) return LC_OK;
-  draw_probs_kernel<<<(unsigned)n_rows, 32, 0, (cudaStream_t)stream>>>(d_probs, vocab, row_stride, d_u, d_token,
-                                                                       d_flags);
+  draw_probs_kernel<<<(unsigned)n_rows, PB_THREADS, 0, (cudaStream_t)stream>>>(d_probs, vocab, row_stride, d_u,
+                                                                               d_token, d_flags);
+  LCB_CUDA_TRY(cudaGetLastError());
+  return LC_OK;
+}
+
+extern "C" int lc_prob_stats(const double* d_probs, int64_t vocab, int64_t n_rows, int64_t row_stride,
+                             double* d_entropy, double* d_pmax, void* stream) {
+  if (n_rows < 0 || vocab < 1 || (n_rows > 0 && (!d_probs || !d_entropy || !d_pmax))) return LC_E_ARG;
+  if (n_rows == 0) return LC_OK;
+  prob_stats_kernel<<<(unsigned)n_rows, PB_THREADS, 0, (cudaStream_t)stream>>>(d_probs, vocab, row_stride,
+                                                                               d_entropy, d_pmax);
   LCB_CUDA_TRY(cudaGetLastError());
   return LC_OK;
 }

@@ -989,6 +989,7 @@ resample_kernel(const char* __restrict__ rows, int64_t row_bytes, int Vdef, cons
             add += sm.sl_e[b];
           }
           add = warp_sum(add);
+          __syncwarp();  // every lane read sm.wcount[warp] above before lane 0 rewrites it
           if (lane == 0) {
             sm.wsum[warp] = sm.werr[warp] + add;  // kept mass of this warp's range (precise e's)
             sm.wcount[warp] = na + (s1 - s0);
@@ -1470,6 +1471,7 @@ __device__ __forceinline__ double rw_e(const ExpCtx& ec, float z, const double* 
 template <int DT, int EM>
 __device__ double rw_seg_pass(const char* row, int V, int nseg, bool vec, int lane, const ExpCtx& ec,
                               const double* t16, double* seg) {
+  __syncwarp();  // earlier reads of seg (a previous tier's draws) before this pass rewrites it
   float Wl = 0.0f;
   for (int s = 0; s < nseg; ++s) {
     double acc = 0.0;

@@ -431,16 +431,21 @@ __global__ void __launch_bounds__(WG_THREADS, 1) wide_kernel(StageArgs a) {
           const uint32_t vma = bmax2_nan(bmax2_nan(wa[0], wa[1]), bmax2_nan(wa[2], wa[3]));
           const uint32_t vmb = bmax2_nan(bmax2_nan(wb[0], wb[1]), bmax2_nan(wb[2], wb[3]));
           cm2 = bmax2_nan(cm2, bmax2_nan(vma, vmb));
-          float ea[8], eb[8];  // (-inf -> 0; the argument roundings are bounded with |a| <= 130)
+          // (-inf -> 0; the argument roundings are bounded with |a| <= 130).  Arguments as packed
+          // FFMA2 pairs (the two halves of a bf16x2 word), exponentials per element, and a balanced
+          // 4-level fp32 tree over the 16 (kSum16Err) with packed FADD2; one fp64 add per iteration
+          float2 ea[4], eb[4];
 #pragma unroll
-          for (int j = 0; j < 8; ++j) {
-            ea[j] = ex2_approx(fmaf((j & 1) ? hi_f(wa[j >> 1]) : lo_f(wa[j >> 1]), Lf, nmL));
-            eb[j] = ex2_approx(fmaf((j & 1) ? hi_f(wb[j >> 1]) : lo_f(wb[j >> 1]), Lf, nmL));
+          for (int h = 0; h < 4; ++h) {
+            const float2 xa = ffma2_rn(make_float2(lo_f(wa[h]), hi_f(wa[h])), Lf, nmL);
+            const float2 xb = ffma2_rn(make_float2(lo_f(wb[h]), hi_f(wb[h])), Lf, nmL);
+            ea[h] = make_float2(ex2_approx(xa.x), ex2_approx(xa.y));
+            eb[h] = make_float2(ex2_approx(xb.x), ex2_approx(xb.y));
           }
-          // fp32 pairwise sum of the 16 (4 roundings, kSum16Err), one fp64 add per iteration
-          const float sa = ((ea[0] + ea[1]) + (ea[2] + ea[3])) + ((ea[4] + ea[5]) + (ea[6] + ea[7]));
-          const float sb = ((eb[0] + eb[1]) + (eb[2] + eb[3])) + ((eb[4] + eb[5]) + (eb[6] + eb[7]));
-          acc += (double)(sa + sb);
+          const float2 sa = fadd2_rn(fadd2_rn(ea[0], ea[1]), fadd2_rn(ea[2], ea[3]));
+          const float2 sb = fadd2_rn(fadd2_rn(eb[0], eb[1]), fadd2_rn(eb[2], eb[3]));
+          const float2 sab = fadd2_rn(sa, sb);
+          acc += (double)(sab.x + sab.y);
           cand_block(qa, vma, va);
           if (v0 + WG_GT < nv) cand_block(qb, vmb, vb);
         }

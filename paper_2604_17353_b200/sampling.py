@@ -113,20 +113,31 @@ def sample(probs: np.ndarray, stream) -> int:
     return int(tok.item())
 
 
-def entropy(probs: np.ndarray) -> float:
-    p = torch.as_tensor(np.asarray(probs, dtype=np.float64), device=_dev.device())
-    nz = p[p > 0]
-    return float(-(nz * torch.log(nz)).sum().item())
+def _prob_stats(probs) -> tuple[float, float]:
+    """(-sum_{p>0} p ln p, max p) of one probability row on the device (lc_prob_stats)."""
+    d = _dev.device()
+    p = torch.as_tensor(np.asarray(probs, dtype=np.float64)).reshape(1, -1).to(d)
+    out = torch.empty(2, dtype=torch.float64, device=d)
+    V = p.shape[1]
+    _capi.check(_capi.lib.lc_prob_stats(p.data_ptr(), V, 1, V, out[0:1].data_ptr(), out[1:2].data_ptr(),
+                                        _dev.stream_ptr(d)), "lc_prob_stats")
+    h, m = out.cpu().tolist()
+    return h, m
 
 
-def max_prob(probs: np.ndarray) -> float:
-    return float(np.asarray(probs).max())
+def entropy(probs: np.ndarray) -> float:  # sampling.py:112-115
+    return _prob_stats(probs)[0]
+
+
+def max_prob(probs: np.ndarray) -> float:  # sampling.py:118-119
+    return _prob_stats(probs)[1]
 
 
 def hotspot_score(probs: np.ndarray, step: int, params: HotspotParams) -> float:
     if step < 0:
         raise ConfigError(f"step must be >= 0, got {step}")
-    return entropy(probs) * (1.0 - max_prob(probs)) / (1.0 + params.decay * step)
+    h, m = _prob_stats(probs)  # one launch for both (sampling.py:122-130)
+    return h * (1.0 - m) / (1.0 + params.decay * step)
 
 
 def select_hotspots(scores: np.ndarray, params: HotspotParams) -> tuple[int, ...]:
