@@ -831,3 +831,40 @@ def test_replay_windowed_equals_full_replay(window):
             assert np.array_equal(tf[r, : rep[r, b], b], tw[r, : rep[r, b], b]), (r, b)
     assert nwin <= -(-max_pos // window)
     assert rep.max() > window or window >= max_pos  # some replay crosses a window boundary
+
+
+@pytest.mark.parametrize("V", [5, 1000, 32000, 151936])
+def test_draw_probs_block_parallel_matches_oracle(V):
+    """lc_draw_probs (block-parallel pairwise total, scanned chunk sums, certified crossing with the
+    sequential fallback) vs numpy's searchsorted(cumsum(q), u*q.sum(), 'right'), including targets
+    placed exactly on cumsum values and zero-probability runs."""
+    rng = np.random.default_rng(V)
+    q = rng.random(V) ** 4
+    q[rng.random(V) < 0.3] = 0.0
+    q[-3:] = 0.0
+    q /= q.sum()
+    cdf = np.cumsum(q)
+    tot = q.sum()
+    us = list(rng.random(300)) + [0.0, 1.0 - 2 ** -53]
+    us += [float(cdf[i] / tot) for i in rng.integers(0, V, 40)]  # targets on (or next to) a cdf value
+    n = len(us)
+    d = DEV
+    p = torch.from_numpy(q).to(d).reshape(1, V).expand(n, V).contiguous()
+    ut = torch.tensor(us, dtype=torch.float64, device=d)
+    tok = torch.empty(n, dtype=torch.int32, device=d)
+    fl = torch.empty(n, dtype=torch.uint8, device=d)
+    _capi.check(_capi.lib.lc_draw_probs(p.data_ptr(), V, n, V, ut.data_ptr(), tok.data_ptr(), fl.data_ptr(),
+                                        lcb._dev.stream_ptr(d)), "lc_draw_probs")
+    want = [sampling_ref.draw(q, u) for u in us]
+    assert tok.cpu().tolist() == want
+
+
+def test_prob_stats_match_numpy():
+    rng = np.random.default_rng(3)
+    for V in (2, 17, 32000):
+        p = rng.random(V)
+        p[rng.random(V) < 0.2] = 0.0
+        p /= p.sum()
+        nz = p[p > 0]
+        assert abs(lcb.entropy(p) - float(-(nz * np.log(nz)).sum())) < 1e-12 * max(1.0, np.log(V))
+        assert lcb.max_prob(p) == float(p.max())

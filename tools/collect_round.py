@@ -17,7 +17,7 @@ O = os.path.join(ROOT, "gpurun_out")
 P = os.path.join(ROOT, "profiles")
 tag = sys.argv[1] if len(sys.argv) > 1 else "round"
 
-for name in ["bench_c2", "bench_ref", "bench_c1", "bench_c3", "bench_c5", "bench_c4", "bench_c1h"]:
+for name in ["bench_c2", "bench_ref", "bench_c1", "bench_c3", "bench_c5", "bench_c4", "bench_c1h", "bench_c2w"]:
     f = os.path.join(O, name + ".json")
     try:
         d = json.loads(open(f).read().strip().splitlines()[-1])
@@ -49,7 +49,7 @@ WANT = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum
         "sm__throughput.avg.pct_of_peak_sustained_elapsed",
         "gpu__compute_memory_throughput.avg.pct_of_peak_sustained_elapsed",
         "l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum"]
-for rep in ["stage", "wide"]:
+for rep in ["stage", "wide", "rowwarp"]:
     f = os.path.join(O, rep + ".ncu-rep")
     if not os.path.exists(f):
         continue
