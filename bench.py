@@ -275,12 +275,17 @@ def run_ours(args, cfg, rank, world, dev):
             dist.barrier()
         torch.cuda.synchronize(dev)
         t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        prof = os.environ.get("LCB_PROFILE_TIMED") == "1"  # ncu --profile-from-start off: timed steps only
         with ClockSampler(dev.index) as clk:
+            if prof:
+                torch.cuda.profiler.start()
             t0.record()
             for _ in range(args.steps):
                 tok, rep, div, slot, ln = step()
             t1.record()
             torch.cuda.synchronize(dev)
+            if prof:
+                torch.cuda.profiler.stop()
         if world > 1:
             dist.barrier()
         ms = t0.elapsed_time(t1)

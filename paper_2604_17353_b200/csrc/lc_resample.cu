@@ -1064,14 +1064,18 @@ resample_kernel(const char* __restrict__ rows, int64_t row_bytes, int Vdef, cons
         int k = 0;
         double off = sm.wpre[warp];
         // certify + write target k (found/flo/fhi broadcast to all lanes)
-        auto finish = [&](int found, double flo, double fhi) {
+        // gm: the hit group's mass when the walk's group sums are fp32 trees (FAST mode 0): the
+        // elements inside it are walked in fp64, which differs from that tree by <= kSum8Err gm
+        auto finish = [&](int found, double flo, double fhi, double gm = 0.0) {
           const double tt = __shfl_sync(0xffffffffu, st, k);
           const double uu = __shfl_sync(0xffffffffu, su, k);
           const int src = __shfl_sync(0xffffffffu, ssrc, k);
           if (lane == 0) {
             // correlated bound: err(u*K - A) <= rel * ((1-u)*A + u*(K - A)) + abs
-            const double tlo = relD * ((1.0 - uu) * flo + uu * (K - flo)) + absD + tt * relRef * 4.0;
-            const double thi = relD * ((1.0 - uu) * fhi + uu * (K - fhi)) + absD + tt * relRef * 4.0;
+            const double tlo = relD * ((1.0 - uu) * flo + uu * (K - flo)) + absD + tt * relRef * 4.0 +
+                               kSum8Err * gm;
+            const double thi = relD * ((1.0 - uu) * fhi + uu * (K - fhi)) + absD + tt * relRef * 4.0 +
+                               kSum8Err * gm;
             const bool ok = found >= 0 && (tt - flo > tlo || (exact_zero_left && flo == 0.0)) && (fhi - tt > thi);
             io.token[dbase + src] = found;
             if (io.flags) io.flags[dbase + src] = tier_flag;
@@ -1091,6 +1095,16 @@ resample_kernel(const char* __restrict__ rows, int64_t row_bytes, int Vdef, cons
               ev[j] = precise ? lite_exp(ec, v[j], sm.t16) : (double)fast_exp(ec, v[j]);
               ls += ev[j];
             }
+            if (!precise) {
+              // the FAST mass pass summed each group of 8 as an fp32 tree: the walk's group sums
+              // must be the same numbers, or the walked prefix and the warp-range prefix / K
+              // (from that pass) differ by up to kSum8Err x the walked mass -- an error the
+              // correlated bound does not cover (cf. the row-warp fix, round 2)
+              float f[8];
+#pragma unroll
+              for (int j = 0; j < 8; ++j) f[j] = (float)ev[j];
+              ls = (double)(((f[0] + f[1]) + (f[2] + f[3])) + ((f[4] + f[5]) + (f[6] + f[7])));
+            }
             const double x = warp_incl_scan(ls);
             const double tot = __shfl_sync(0xffffffffu, x, 31);
             while (k < nown) {
@@ -1098,7 +1112,7 @@ resample_kernel(const char* __restrict__ rows, int64_t row_bytes, int Vdef, cons
               if (!(tk < off + tot)) break;
               const unsigned hm = __ballot_sync(0xffffffffu, (ls > 0.0) && (tk < off + x));
               int found = -1;
-              double flo = 0.0, fhi = 0.0;
+              double flo = 0.0, fhi = 0.0, gm = 0.0;
               if (hm) {
                 const int hl = __ffs(hm) - 1;
                 if (lane == hl) {
@@ -1117,8 +1131,9 @@ resample_kernel(const char* __restrict__ rows, int64_t row_bytes, int Vdef, cons
                 found = __shfl_sync(0xffffffffu, found, hl);
                 flo = __shfl_sync(0xffffffffu, flo, hl);
                 fhi = __shfl_sync(0xffffffffu, fhi, hl);
+                gm = precise ? 0.0 : __shfl_sync(0xffffffffu, ls, hl);
               }
-              finish(found, flo, fhi);
+              finish(found, flo, fhi, gm);
             }
             off += tot;
           }
@@ -2035,6 +2050,8 @@ rowwarp_kernel(const char* __restrict__ rows, int64_t row_bytes, int Vdef, const
         __syncwarp();
         const double K = sw.seg[nseg];
         const double absD = fmax(absE, E_S - relE * S);  // absolute part of the bound (flushed mass)
+        // FAST: walk e's vs fused-pass e's inside a segment (PRECISE: the same lite_exp values)
+        const double relX = precise ? 0.0 : (fo.relmax + kEx2RelErr + kCorrErr + kSum8Err + relArg) * 1.01;
         for (int64_t dbase = tv.d0; dbase < tv.d1; dbase += 32) {
           const int64_t d = dbase + lane;
           double t = INFINITY, u = 0.0;
@@ -2069,6 +2086,7 @@ rowwarp_kernel(const char* __restrict__ rows, int64_t row_bytes, int Vdef, const
             int s = 0;
             while (s + 1 < nseg && sw.seg[s + 1] <= tk0) ++s;
             double off = sw.seg[s];
+            const double seg0 = off;  // the segment's prefix (from the fused pass)
             const double send = sw.seg[s + 1];
             for (int stp = 0; stp < RW_SEGSTEPS && k < ntar; ++stp) {
               const int my0 = s * RW_SEG + 256 * stp + 8 * lane;
@@ -2099,7 +2117,7 @@ rowwarp_kernel(const char* __restrict__ rows, int64_t row_bytes, int Vdef, const
                 if (!(tk < off + tot) && !(stp == RW_SEGSTEPS - 1 && tk < send)) break;
                 const unsigned hm = __ballot_sync(0xffffffffu, (ls > 0.0) && (tk < off + x));
                 int found = -1;
-                double flo = 0.0, fhi = 0.0;
+                double flo = 0.0, fhi = 0.0, gm = 0.0;
                 if (hm) {
                   const int hl = __ffs(hm) - 1;
                   if (lane == hl) {
@@ -2118,12 +2136,19 @@ rowwarp_kernel(const char* __restrict__ rows, int64_t row_bytes, int Vdef, const
                   found = __shfl_sync(0xffffffffu, found, hl);
                   flo = __shfl_sync(0xffffffffu, flo, hl);
                   fhi = __shfl_sync(0xffffffffu, fhi, hl);
+                  gm = precise ? 0.0 : __shfl_sync(0xffffffffu, ls, hl);  // (fp32-tree group sum)
                 }
                 const double uu = __shfl_sync(0xffffffffu, su, k);
                 const int src = __shfl_sync(0xffffffffu, ssrc, k);
                 if (lane == 0) {
-                  const double tlo = relE * ((1.0 - uu) * flo + uu * (K - flo)) + absD + tk * relRef * 4.0;
-                  const double thi = relE * ((1.0 - uu) * fhi + uu * (K - fhi)) + absD + tk * relRef * 4.0;
+                  // correlated bound over the segment prefixes (the fused pass's e's on both sides),
+                  // plus the uncorrelated part: inside segment s the walk sums its own e's (relative
+                  // to the row max), not the fused pass's (relative to running maxima, rescaled), so
+                  // their difference is bounded by both errors times the walked mass
+                  const double tlo = relE * ((1.0 - uu) * flo + uu * (K - flo)) + relX * (flo - seg0) + absD +
+                                     tk * relRef * 4.0 + kSum8Err * gm;
+                  const double thi = relE * ((1.0 - uu) * fhi + uu * (K - fhi)) + relX * (fhi - seg0) + absD +
+                                     tk * relRef * 4.0 + kSum8Err * gm;
                   const bool ok = found >= 0 && (tk - flo > tlo || (precise && flo == 0.0)) && (fhi - tk > thi);
                   io.token[dbase + src] = found;
                   if (io.flags) io.flags[dbase + src] = tier_flag;

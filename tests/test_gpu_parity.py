@@ -868,3 +868,42 @@ def test_prob_stats_match_numpy():
         nz = p[p > 0]
         assert abs(lcb.entropy(p) - float(-(nz * np.log(nz)).sum())) < 1e-12 * max(1.0, np.log(V))
         assert lcb.max_prob(p) == float(p.max())
+
+
+def test_rowwarp_untruncated_draw_regression_c1():
+    """C1 bench check leg, round 2: row 10479 (state mix2(7, 10479)), seed mix2(137, 20), draw
+    number 479 -> numpy 23235 (margins ~2e-8 of the mass on both sides), the row-warp FAST tier
+    returned 23236: its correlated bound ignored that inside the hit segment the walk sums its own
+    exponentials, not the fused pass's (which produced the segment prefixes and K)."""
+    V = 32000
+    row = mixing_ref.fill_rows_np([mixing_ref.mix2(7, 10479)], V, 2.5)
+    u = float(mixing_ref.uniforms_np(np.array([mixing_ref.mix2(137, 20)], dtype=np.uint64), np.array([479]))[0])
+    tok, fl, _ = _resample_rows(row, 0.6, None, 1.0, [[u]])
+    assert tok.tolist() == _oracle_tokens(row, 0.6, None, 1.0, [[u]]) == [23235]
+
+
+@pytest.mark.parametrize("V,conc,T", [(32000, 2.5, 0.6), (32000, 0.0, 1.0), (32000, 2.5, 1.3),
+                                       (128256, 2.5, 0.6), (128256, 0.0, 1.0)])
+def test_untruncated_targets_near_cdf_boundaries(V, conc, T):
+    """Untruncated fp32 rows (C1 shape): targets placed within 1e-9 .. 1e-6 of the mass from a cdf
+    boundary, at every depth of the row (segment starts, inside segments, u -> 1), on both sides;
+    every token must equal numpy's searchsorted(cumsum(p), u * p.sum(), 'right')."""
+    nrows = 12 if V <= 32000 else 6  # (V > 65536: the CTA kernel)
+    rng = np.random.default_rng(int(conc * 10 + T * 100) + V)
+    rows = mixing_ref.fill_rows_np([mixing_ref.mix2(11, 777 + i) for i in range(nrows)], V, conc)
+    ulists = []
+    for z in rows:
+        p = sampling_ref.softmax(z, T)
+        cdf = np.cumsum(p) / p.sum()
+        js = np.concatenate([rng.integers(0, V - 1, 40), np.arange(2047, V - 1, 2048)[:8], [V - 2, V // 2]])
+        us = []
+        for j in js:
+            for rel in (1e-9, 1e-8, 1e-7, 1e-6):
+                for sgn in (-1.0, 1.0):
+                    x = cdf[j] + sgn * rel
+                    if 0.0 <= x < 1.0:
+                        us.append(float(x))
+        ulists.append(us)
+    tok, fl, cnt = _resample_rows(rows, T, None, 1.0, ulists)
+    assert tok.tolist() == _oracle_tokens(rows, T, None, 1.0, ulists)
+    assert not np.any(fl & _capi.LC_DRAW_UNRESOLVED)

@@ -18,12 +18,12 @@ timeout 600 python bench.py --policy windowed --no-cpu-baseline > $O/bench_c2w.j
 timeout 900 python bench.py --config c4 --cpu-seconds 5 > $O/bench_c4.json 2> $O/bench_c4.err
 timeout 600 python bench.py --config c1 --policy hotspot --no-cpu-baseline > $O/bench_c1h.json 2> $O/bench_c1h.err
 STEPS=5 bash tools/c3_sweep.sh
-timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $O/launches.csv \
+LCB_PROFILE_TIMED=1 timeout 600 ncu --profile-from-start off --metrics gpu__time_duration.sum --clock-control none --csv --log-file $O/launches.csv \
     python bench.py --steps 2 --warmup 3 --no-cpu-baseline --no-check > $O/bench_ncu.log 2>&1
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:stage_kernel -s 4 -c 1 -o $O/stage -f \
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:stage_kernel -s 8 -c 1 -o $O/stage -f \
     python bench.py --steps 1 --warmup 3 --no-cpu-baseline --no-check > $O/ncu_stage.log 2>&1
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:rowwarp_kernel -s 4 -c 1 -o $O/rowwarp -f \
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:rowwarp_kernel -s 8 -c 1 -o $O/rowwarp -f \
     python bench.py --config c1 --steps 1 --warmup 3 --no-cpu-baseline --no-check > $O/ncu_rowwarp.log 2>&1
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:wide_kernel -s 4 -c 1 -o $O/wide -f \
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:wide_kernel -s 5 -c 1 -o $O/wide -f \
     python bench.py --config c3 --steps 1 --warmup 3 --no-cpu-baseline --no-check > $O/ncu_wide.log 2>&1
 echo done
