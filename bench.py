@@ -177,16 +177,18 @@ def workload_config(args, cfg, world):
 
 
 def traffic_per_launch(cfg, n_rows):
-    """DRAM bytes of one resample launch, from the committed ncu --set full capture
-    (profiles/*traffic*.json: read + write bytes per row of the staged kernel), or None."""
-    import glob
-
-    files = sorted(glob.glob(os.path.join(ROOT, "profiles", "*traffic_stage.json")))
-    if not files or cfg["dtype"] != "bfloat16" or cfg["V"] > 32000:
+    """DRAM bytes (read + write) of one resample launch, from the committed ncu --set full captures
+    of the bench launches (profiles/r2_traffic.json: bytes per row of the stage / row-warp / wide
+    kernel), or None for a shape without a capture."""
+    f = os.path.join(ROOT, "profiles", "r2_traffic.json")
+    if not os.path.exists(f):
         return None
-    with open(files[-1]) as f:
-        d = json.load(f)
-    return d["dram_bytes_per_row"] * n_rows
+    with open(f) as fh:
+        d = json.load(fh)
+    key = ("c2" if cfg["dtype"] == "bfloat16" else "c1") if cfg["V"] <= 32000 else "c3"
+    if key == "c3" and cfg["dtype"] != "bfloat16":
+        return None
+    return d[key]["dram_bytes_per_row"] * n_rows if key in d else None
 
 
 def run_ours(args, cfg, rank, world, dev):
