@@ -520,7 +520,7 @@ def run_check(args, cfg, w, rank, world, dev):
     cache = w["cache"]
     V, n_req, nb, R = cfg["V"], cfg["n_req"], cfg["nb"], cfg["R"]
     n_rows = n_req * R
-    target = args.check_draws if args.check_draws is not None else (10_000_000 if V <= 32000 else 100_000)
+    target = args.check_draws if args.check_draws is not None else (10_000_000 if V <= 32000 else 1_000_000)
     S = max(1, -(-target // (n_rows * nb)))
     toks, reps, seeds_all = [], [], []
     kept = torch.zeros(n_rows, dtype=torch.int32, device=dev)

@@ -29,7 +29,7 @@
 extern "C" {
 #endif
 
-#define LC_ABI_VERSION 4
+#define LC_ABI_VERSION 5
 
 typedef enum lc_status {
   LC_OK = 0,
@@ -107,6 +107,10 @@ typedef struct lc_draws {
                      * the kept set is the first d_kept[t] ids of the row in (logit desc, id asc)
                      * order, i.e. the reference's lexsort((ids, -p)) prefix; V for an untruncated
                      * row, 1 for T == 0, -1 for a bad row (NaN / non-finite max)            */
+  double* d_entropy; /* out, per TASK (may be NULL): H = -sum p ln p of softmax(z, T) over the
+                      * task's row (the untruncated distribution, sampling.py:112-115); NaN for a
+                      * task whose row cannot be resolved.  An epilogue launch over the same rows */
+  double* d_pmax;    /* out, per TASK (may be NULL): max p of that softmax (sampling.py:118-119) */
 } lc_draws;
 
 /* Bytes of scratch the resample entry points need for n_tasks tasks. */

@@ -14,7 +14,7 @@ from . import build as _build
 from .errors import CapacityError, ConfigError
 
 LC_OK, LC_E_CONFIG, LC_E_ZERO_MASS, LC_E_CAPACITY, LC_E_CUDA, LC_E_ARG, LC_E_STATE = range(7)
-ABI_VERSION = 4
+ABI_VERSION = 5
 LC_F32, LC_BF16 = 0, 1
 LC_DRAW_PRECISE, LC_DRAW_UNRESOLVED, LC_DRAW_BAD_ROW = 1, 2, 4
 
@@ -43,6 +43,8 @@ class LcDraws(C.Structure):
         ("d_token", C.c_void_p),
         ("d_flags", C.c_void_p),
         ("d_kept", C.c_void_p),
+        ("d_entropy", C.c_void_p),
+        ("d_pmax", C.c_void_p),
     ]
 
 

@@ -7,38 +7,10 @@
 
 #include "lc_common.cuh"
 #include "lc_numpy.cuh"
+#include "lc_probs.cuh"
 
 namespace lcb {
 
-constexpr int PB_THREADS = 256;
-
-template <int DT>
-__device__ __forceinline__ float ld(const char* row, int64_t i) {
-  if (DT == LC_BF16) return bf16_bits_to_f32(reinterpret_cast<const uint16_t*>(row)[i]);
-  return reinterpret_cast<const float*>(row)[i];
-}
-
-__device__ float block_max(float v, float* red) {
-  v = warp_max(v);
-  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
-  __syncthreads();
-  float r = -INFINITY;
-  for (int w = 0; w < PB_THREADS / 32; ++w) r = fmaxf(r, red[w]);
-  __syncthreads();
-  return r;
-}
-
-__device__ double block_sum(double v, double* red) {
-  v = warp_sum(v);
-  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
-  __syncthreads();
-  double r = 0.0;
-  for (int w = 0; w < PB_THREADS / 32; ++w) r += red[w];
-  __syncthreads();
-  return r;
-}
-
-// softmax: s = f64(z)/T - max (sampling.py:65-66), e = exp(s), p = e / pairwise_sum(e)
 constexpr int PB_LEAVES = 2048;  // numpy pairwise-tree leaves summed in parallel (V <~ 130K; beyond: sequential)
 
 struct PbShared {
@@ -67,6 +39,7 @@ __device__ int64_t block_first_eq(const char* row, int64_t V, float m, int64_t* 
   return r;
 }
 
+// softmax: s = f64(z)/T - max (sampling.py:65-66), e = exp(s), p = e / pairwise_sum(e)
 template <int DT>
 __global__ void __launch_bounds__(PB_THREADS)
 softmax_kernel(const char* rows, int64_t row_bytes, int64_t V, const double* temps, double* out) {
@@ -197,39 +170,6 @@ prob_stats_kernel(const double* probs, int64_t V, int64_t stride, double* H, dou
     for (int k = 0; k < PB_THREADS / 32; ++k) m = fmax(m, dred[k]);
     H[blockIdx.x] = hs + 0.0;  // (-0 -> +0: a one-hot row has entropy 0.0)
     pmax[blockIdx.x] = m;
-  }
-}
-
-// H = -sum p ln p = ln S - sum(e*s)/S with s <= 0 the shifted scaled logits;
-// pmax = max p = 1/S (sampling.py:112-126).
-// one block per row: H = log S - sum(e s) / S and max p = 1 / S of softmax(z / T), fp64
-template <int DT>
-__device__ __forceinline__ void entropy_row(const char* row, int64_t V, double T, double* H, double* pmax) {
-  __shared__ float fred[PB_THREADS / 32];
-  __shared__ double dred[PB_THREADS / 32];
-  float m = -INFINITY;
-  for (int64_t i = threadIdx.x; i < V; i += PB_THREADS) m = fmaxf(m, ld<DT>(row, i));
-  m = block_max(m, fred);
-  if (T == 0.0) {
-    if (threadIdx.x == 0) {
-      *H = 0.0;
-      *pmax = 1.0;
-    }
-    return;
-  }
-  const double mT = __ddiv_rn((double)m, T);
-  double se = 0.0, ses = 0.0;
-  for (int64_t i = threadIdx.x; i < V; i += PB_THREADS) {
-    double s = __dsub_rn(__ddiv_rn((double)ld<DT>(row, i), T), mT);
-    double e = exp(s);
-    se += e;
-    if (e > 0.0) ses += e * s;
-  }
-  se = block_sum(se, dred);
-  ses = block_sum(ses, dred);
-  if (threadIdx.x == 0) {
-    *H = log(se) - ses / se;
-    *pmax = 1.0 / se;
   }
 }
 

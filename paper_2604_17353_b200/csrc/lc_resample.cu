@@ -35,6 +35,7 @@
 #include "lc_numpy.cuh"
 #include "lc_resample.cuh"
 #include "lc_task.cuh"
+#include "lc_probs.cuh"
 
 namespace lcb {
 
@@ -2670,6 +2671,29 @@ static int launch_all(const char* rows, int64_t row_bytes, int V, const lc_task*
   return LC_OK;
 }
 
+// Optional epilogue (lc_draws.d_entropy / d_pmax): one block per task, entropy and max
+// probability of softmax(z / T) over the task's row (sampling.py:112-119), fp64.
+template <int DT>
+__global__ void __launch_bounds__(PB_THREADS)
+task_entropy_kernel(const char* rows, int64_t row_bytes, int Vdef, const lc_task* tasks, CacheMap cm, double* H,
+                    double* pmax) {
+  __shared__ double s_h, s_p;
+  TaskView tv;
+  const bool ok = resolve_task(tasks[blockIdx.x], rows, row_bytes, Vdef, cm, tv);
+  if (!ok) {
+    if (threadIdx.x == 0) {
+      if (H) H[blockIdx.x] = nan("");
+      if (pmax) pmax[blockIdx.x] = nan("");
+    }
+    return;
+  }
+  entropy_row<DT>(tv.row, tv.V, tv.T, &s_h, &s_p);
+  if (threadIdx.x == 0) {
+    if (H) H[blockIdx.x] = s_h;
+    if (pmax) pmax[blockIdx.x] = s_p;
+  }
+}
+
 int resample_launch(const void* rows, int dtype, int64_t vocab, int64_t row_stride, const lc_task* tasks,
                     int64_t n_tasks, lc_draws draws, const int32_t* pages, int max_pages, int page_rows, void* ws,
                     int64_t ws_bytes, int64_t* counters, cudaStream_t st) {
@@ -2679,13 +2703,27 @@ int resample_launch(const void* rows, int dtype, int64_t vocab, int64_t row_stri
   DrawIO io{draws.d_u, draws.d_seed, draws.d_index, draws.d_token, draws.d_flags, draws.d_kept};
   CacheMap cm{pages, max_pages, page_rows};
   const int64_t esz = dtype == LC_BF16 ? 2 : 4;
+  int rc = LC_E_ARG;
   if (dtype == LC_BF16)
-    return launch_all<LC_BF16>((const char*)rows, row_stride * esz, (int)vocab, tasks, n_tasks, cm, io, ws, ws_bytes,
-                               counters, st);
-  if (dtype == LC_F32)
-    return launch_all<LC_F32>((const char*)rows, row_stride * esz, (int)vocab, tasks, n_tasks, cm, io, ws, ws_bytes,
-                              counters, st);
-  return LC_E_ARG;
+    rc = launch_all<LC_BF16>((const char*)rows, row_stride * esz, (int)vocab, tasks, n_tasks, cm, io, ws, ws_bytes,
+                             counters, st);
+  else if (dtype == LC_F32)
+    rc = launch_all<LC_F32>((const char*)rows, row_stride * esz, (int)vocab, tasks, n_tasks, cm, io, ws, ws_bytes,
+                            counters, st);
+  if (rc != LC_OK || !(draws.d_entropy || draws.d_pmax)) return rc;
+  for (int64_t t0 = 0; t0 < n_tasks; t0 += 65535 * 1024) {  // (grid x limit is far above; chunk for safety)
+    const int64_t nt = n_tasks - t0 < 65535 * 1024 ? n_tasks - t0 : 65535 * 1024;
+    if (dtype == LC_BF16)
+      task_entropy_kernel<LC_BF16><<<(unsigned)nt, PB_THREADS, 0, st>>>(
+          (const char*)rows, row_stride * esz, (int)vocab, tasks + t0, cm, draws.d_entropy ? draws.d_entropy + t0 : nullptr,
+          draws.d_pmax ? draws.d_pmax + t0 : nullptr);
+    else
+      task_entropy_kernel<LC_F32><<<(unsigned)nt, PB_THREADS, 0, st>>>(
+          (const char*)rows, row_stride * esz, (int)vocab, tasks + t0, cm, draws.d_entropy ? draws.d_entropy + t0 : nullptr,
+          draws.d_pmax ? draws.d_pmax + t0 : nullptr);
+    LCB_CUDA_TRY(cudaGetLastError());
+  }
+  return LC_OK;
 }
 
 }  // namespace lcb

@@ -32,7 +32,10 @@
 namespace lcb {
 
 constexpr int SG_GROUPS = 3;
-constexpr int SG_GW = 5;                        // warps per group
+#ifndef LCB_SG_GW
+#define LCB_SG_GW 5  // (6: 37.0M, 7: 36.2M rows/s vs 38.8M: spills and wider barriers)
+#endif
+constexpr int SG_GW = LCB_SG_GW;                // warps per group (5; -DLCB_SG_GW for experiments)
 constexpr int SG_GT = SG_GW * 32;               // threads per group
 constexpr int SG_PWARP = SG_GROUPS * SG_GW;     // producer warp index (15)
 constexpr int SG_THREADS = (SG_PWARP + 1) * 32;  // 512
@@ -43,6 +46,10 @@ constexpr int SG_NU = 32;                        // uniforms precomputed per tas
 constexpr int SG_ND = 64;                        // draws per task handled here (more: CTA kernel)
 constexpr int SG_PB = 8;                         // tasks per producer grab
 constexpr int SG_FQ = 6;                         // task FIFO slots
+#ifndef LCB_SG_L2PF
+#define LCB_SG_L2PF 1
+#endif
+constexpr bool SG_L2PF = LCB_SG_L2PF != 0;       // L2 prefetch of each task's row by the producer
 constexpr int SG_NCK = 1;  // bulk copies per row (4, with A starting on the first quarter, measured slower: 34.8M vs 38.5M rows/s)
 constexpr int SG_POPW = SG_GW - 1;               // the group warp that pops tasks (it writes no tokens for <= 128 draws)
 constexpr int SG_RB = 5;                         // C: vectors per batch of independent loads
@@ -127,6 +134,9 @@ __device__ void sg_producer(const StageArgs& a, SgSmem& sm, int lane) {
           const int pos = __popc(okm & ((1u << lane) - 1u));
           sm.pbt[pos] = t;
           sm.pbv[pos] = tv;
+          // pull the row into L2 now: by the time a group pops the task (up to SG_FQ + SG_PB tasks
+          // later) its bulk copy reads L2 instead of waiting on HBM (HBM still sees the row once)
+          if (SG_L2PF) l2_prefetch(tv.row, (uint32_t)(tv.V * 2));
         }
         __syncwarp();
         nb = __popc(okm);

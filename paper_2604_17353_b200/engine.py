@@ -297,7 +297,7 @@ class WaveEngine:
             stg = torch.empty((B, V), dtype=torch.float32 if sdt == _capi.LC_F32 else torch.bfloat16, device=dev)
         tasks = torch.empty(B * _capi.TASK_DTYPE.itemsize, dtype=torch.uint8, device=dev)
         ws = sampling._workspace(dev).get(B, V)
-        draws = _capi.LcDraws(None, seeds.data_ptr(), None, out.data_ptr(), flags.data_ptr(), None)
+        draws = _capi.LcDraws(None, seeds.data_ptr(), None, out.data_ptr(), flags.data_ptr(), None, None, None)
         m = self.model
         steps = []
         for s in range(n_steps):

@@ -228,7 +228,8 @@ def _workspace(dev) -> Workspace:
 
 def resample(rows: torch.Tensor, tasks, u: torch.Tensor | None = None, seeds: torch.Tensor | None = None,
              index: torch.Tensor | None = None, n_draws: int | None = None, counters: torch.Tensor | None = None,
-             cache=None, out: tuple | None = None, kept: torch.Tensor | None = None):
+             cache=None, out: tuple | None = None, kept: torch.Tensor | None = None,
+             entropy: torch.Tensor | None = None, pmax: torch.Tensor | None = None):
     """Fused resample of device rows (or of cached rows when ``cache`` is given).
 
     ``tasks``: numpy TASK_DTYPE array or a uint8 device tensor of packed tasks.
@@ -237,6 +238,9 @@ def resample(rows: torch.Tensor, tasks, u: torch.Tensor | None = None, seeds: to
     ``kept`` (int32 device tensor, one per task, optional) receives each task's
     kept-set size K: truncate()'s kept ids are the first K of the row in
     (logit desc, id asc) order (sampling.py:71-94; V = untruncated, -1 = bad row).
+    ``entropy`` / ``pmax`` (float64 device tensors, one per task, optional) receive the
+    entropy and max probability of each task's row at its temperature (sampling.py:112-119),
+    computed by an epilogue launch over the same rows.
     """
     dev = rows.device if rows is not None else cache.dev
     if isinstance(tasks, np.ndarray):
@@ -257,8 +261,11 @@ def resample(rows: torch.Tensor, tasks, u: torch.Tensor | None = None, seeds: to
     ws = _workspace(dev).get(n_tasks, vocab)
     if kept is not None and (kept.dtype != torch.int32 or kept.numel() < n_tasks):
         raise ConfigError("kept must be an int32 tensor with one entry per task")
+    for name, t in (("entropy", entropy), ("pmax", pmax)):
+        if t is not None and (t.dtype != torch.float64 or t.numel() < n_tasks):
+            raise ConfigError(f"{name} must be a float64 tensor with one entry per task")
     draws = _capi.LcDraws(_dev.ptr(u), _dev.ptr(seeds), _dev.ptr(index), tok.data_ptr(), _dev.ptr(flags),
-                          _dev.ptr(kept))
+                          _dev.ptr(kept), _dev.ptr(entropy), _dev.ptr(pmax))
     cnt = _dev.ptr(counters)
     if cache is None:
         if rows.dtype == torch.bfloat16:

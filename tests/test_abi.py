@@ -43,7 +43,7 @@ def test_exports_are_exactly_the_header(tmp_path):
 def test_abi_version_and_status_strings():
     from paper_2604_17353_b200 import _capi
 
-    assert _capi.lib.lc_abi_version() == 4
+    assert _capi.lib.lc_abi_version() == 5
     assert _capi.lib.lc_status_string(6) == b"write-back prefix no longer live"
     assert _capi.lib.lc_status_string(0) == b"ok"
     assert _capi.lib.lc_status_string(1) == b"config error"
@@ -53,7 +53,7 @@ def test_struct_layouts_match_header():
     from paper_2604_17353_b200 import _capi
 
     assert C.sizeof(_capi.LcTask) == 72 == _capi.TASK_DTYPE.itemsize
-    assert C.sizeof(_capi.LcDraws) == 48
+    assert C.sizeof(_capi.LcDraws) == 64
     assert C.sizeof(_capi.LcCacheConfig) == 48
     assert C.sizeof(_capi.LcCacheStats) == 11 * 8
     src = open(HEADER).read()

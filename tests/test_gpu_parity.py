@@ -907,3 +907,26 @@ def test_untruncated_targets_near_cdf_boundaries(V, conc, T):
     tok, fl, cnt = _resample_rows(rows, T, None, 1.0, ulists)
     assert tok.tolist() == _oracle_tokens(rows, T, None, 1.0, ulists)
     assert not np.any(fl & _capi.LC_DRAW_UNRESOLVED)
+
+
+@pytest.mark.parametrize("dtype", ["float32", "bfloat16"])
+def test_resample_entropy_epilogue_matches_oracle(dtype):
+    """lc_draws.d_entropy / d_pmax: per task, -sum p ln p and max p of softmax(z, T) over the task's
+    row (sampling.py:112-119), for explicit rows and for cached rows (slot, pos)."""
+    V, n = 32000, 24
+    rows = mixing_ref.fill_rows_np([mixing_ref.mix2(21, i) for i in range(n)], V, 2.5)
+    if dtype == "bfloat16":
+        rows = mixing_ref.bf16_round(rows)
+    Ts = [0.6, 1.0, 0.0, 1.7] * (n // 4)
+    tasks = lcb.make_tasks(row=np.arange(n), temperature=np.array(Ts), top_p=0.9, draw_begin=np.arange(n),
+                           draw_end=np.arange(n) + 1)
+    z = torch.from_numpy(rows).to(DEV).to(getattr(torch, dtype))
+    H = torch.empty(n, dtype=torch.float64, device=DEV)
+    P = torch.empty(n, dtype=torch.float64, device=DEV)
+    u = torch.full((n,), 0.5, dtype=torch.float64, device=DEV)
+    lcb.resample(z, tasks, u=u, entropy=H, pmax=P)
+    for i in range(n):
+        p = sampling_ref.softmax(rows[i], Ts[i])
+        nz = p[p > 0]
+        assert abs(H[i].item() - float(-(nz * np.log(nz)).sum())) <= 1e-11 * max(1.0, float(np.log(V)))
+        assert abs(P[i].item() - float(p.max())) <= 1e-12
