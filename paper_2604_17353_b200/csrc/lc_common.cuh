@@ -127,6 +127,29 @@ __device__ __forceinline__ float2 fadd2_rn(float2 a, float2 b) {  // (a.x + b.x,
   return r;
 }
 
+// general packed pair forms (every operand a pair; a broadcast is make_float2(x, x))
+#define LCB_F2OP(name, op)                                                                             \
+  __device__ __forceinline__ float2 name(float2 a, float2 b) {                                         \
+    float2 r;                                                                                          \
+    asm("{\n .reg .b64 a, b, d;\n mov.b64 a, {%2, %3};\n mov.b64 b, {%4, %5};\n " op                \
+        " d, a, b;\n mov.b64 {%0, %1}, d;\n}"                                                         \
+        : "=f"(r.x), "=f"(r.y)                                                                         \
+        : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y));                                                     \
+    return r;                                                                                          \
+  }
+LCB_F2OP(f2add, "add.rn.f32x2")
+LCB_F2OP(f2sub, "sub.rn.f32x2")
+LCB_F2OP(f2mul, "mul.rn.f32x2")
+#undef LCB_F2OP
+__device__ __forceinline__ float2 f2fma(float2 a, float2 b, float2 c) {  // a * b + c, one rounding per lane
+  float2 r;
+  asm("{\n .reg .b64 a, b, c, d;\n mov.b64 a, {%2, %3};\n mov.b64 b, {%4, %5};\n mov.b64 c, {%6, %7};\n"
+      " fma.rn.f32x2 d, a, b, c;\n mov.b64 {%0, %1}, d;\n}"
+      : "=f"(r.x), "=f"(r.y)
+      : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y), "f"(c.x), "f"(c.y));
+  return r;
+}
+
 inline int ceil_div(int64_t a, int64_t b) { return (int)((a + b - 1) / b); }
 
 }  // namespace lcb

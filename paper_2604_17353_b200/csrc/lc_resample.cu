@@ -1320,11 +1320,10 @@ __device__ __noinline__ FusedOut rw_fused_pass(const char* row, int V, int nseg,
 #pragma unroll
       for (int j = 0; j < 8; ++j) {
         if (ACC) {
-          ExpCtx c2;
-          c2.m = mt;
-          c2.Lhi = Lhi;
-          c2.Llo = Llo;
-          ef[j] = fast_exp(c2, vu[j]);
+          if (j & 1) continue;  // (pairs: the packed fast_exp2, bit-identical to fast_exp)
+          const float2 e2 = fast_exp2(mt, Lhi, Llo, make_float2(vu[j], vu[j + 1]));
+          ef[j] = e2.x;
+          ef[j + 1] = e2.y;
         } else {
           const float a = (vu[j] - mt) * Lhi;
           ef[j] = ex2_approx(a);  // -inf -> +0

@@ -47,7 +47,7 @@ constexpr int SG_ND = 64;                        // draws per task handled here 
 constexpr int SG_PB = 8;                         // tasks per producer grab
 constexpr int SG_FQ = 6;                         // task FIFO slots
 #ifndef LCB_SG_L2PF
-#define LCB_SG_L2PF 1
+#define LCB_SG_L2PF 0  // (measured: 38.3M vs 38.7M rows/s with it on; TMA wait 1.9K vs 1.6K clocks)
 #endif
 constexpr bool SG_L2PF = LCB_SG_L2PF != 0;       // L2 prefetch of each task's row by the producer
 constexpr int SG_NCK = 1;  // bulk copies per row (4, with A starting on the first quarter, measured slower: 34.8M vs 38.5M rows/s)

@@ -48,6 +48,22 @@ __device__ __forceinline__ float fast_exp(const ExpCtx& c, float z) {
   return (e > 0.0f) ? fmaf(e, alo * 0.69314718055994531f, e) : 0.0f;
 }
 
+// fast_exp of two elements with packed pair instructions: the same IEEE operations in the same
+// order per lane (bit-identical to two fast_exp calls), about half the FP32 instructions
+__device__ __forceinline__ float2 fast_exp2(float m, float Lhi, float Llo, float2 z) {
+  const float2 M = make_float2(m, m), nM = make_float2(-m, -m);
+  const float2 H = make_float2(Lhi, Lhi), Lo = make_float2(Llo, Llo);
+  const float2 s = f2sub(z, M);
+  const float2 bb = f2sub(s, z);
+  const float2 err = f2add(f2sub(z, f2sub(s, bb)), f2sub(nM, bb));
+  const float2 ahi = f2mul(s, H);
+  const float2 nahi = make_float2(-ahi.x, -ahi.y);
+  const float2 alo = f2add(f2fma(s, H, nahi), f2fma(err, H, f2mul(s, Lo)));
+  const float2 e = make_float2(ex2_approx(ahi.x), ex2_approx(ahi.y));
+  const float2 r = f2fma(e, f2mul(alo, make_float2(0.69314718055994531f, 0.69314718055994531f)), e);
+  return make_float2(e.x > 0.0f ? r.x : 0.0f, e.y > 0.0f ? r.y : 0.0f);
+}
+
 // CHEAP (truncated modes, where only the row mass and bracketing use it):
 // e = ex2(fl(fl(z - m) * Lhi)).  Relative error <= kEx2Raw + kArgRel * |a|
 // (three fp32 roundings carried into the argument); a is clamped at -200 so
