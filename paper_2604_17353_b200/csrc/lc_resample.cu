@@ -1341,7 +1341,10 @@ __device__ __noinline__ FusedOut rw_fused_pass(const char* row, int V, int nseg,
       }
     };
     if (s < nfull) {
-      constexpr int UNRF = (DT == LC_BF16) ? 8 : 4;  // 128 B per lane in flight
+#ifndef LCB_RW_UNRF_F32
+#define LCB_RW_UNRF_F32 4  // (6 spills: 10.2M rows/s)
+#endif
+      constexpr int UNRF = (DT == LC_BF16) ? 8 : LCB_RW_UNRF_F32;  // 128 B per lane in flight
 #pragma unroll 1
       for (int st = 0; st < RW_SEGSTEPS; st += UNRF) {
         // raw vector loads first (memory-level parallelism), unpacked one vector at a time
