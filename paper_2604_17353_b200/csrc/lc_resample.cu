@@ -1330,7 +1330,10 @@ __device__ __noinline__ FusedOut rw_fused_pass(const char* row, int V, int nseg,
           aw[j] = a;
         }
       }
-      const float s8 = ((ef[0] + ef[1]) + (ef[2] + ef[3])) + ((ef[4] + ef[5]) + (ef[6] + ef[7]));
+      // balanced 3-level fp32 tree over the 8 (kSum8Err), two lanes per packed FADD2
+      const float2 s2 = f2add(f2add(make_float2(ef[0], ef[1]), make_float2(ef[2], ef[3])),
+                              f2add(make_float2(ef[4], ef[5]), make_float2(ef[6], ef[7])));
+      const float s8 = s2.x + s2.y;
       if (mt > -INFINITY) {  // (all -inf so far: z - mt is NaN)
         if (!ACC) {
           // CHEAP: W = sum of e*|a| (NaN once a -inf is seen: replaced at the segment end)
@@ -2107,7 +2110,9 @@ rowwarp_kernel(const char* __restrict__ rows, int64_t row_bytes, int Vdef, const
                 float f[8];
 #pragma unroll
                 for (int j = 0; j < 8; ++j) f[j] = (float)ev[j];
-                ls = (double)(((f[0] + f[1]) + (f[2] + f[3])) + ((f[4] + f[5]) + (f[6] + f[7])));
+                const float2 s2 = f2add(f2add(make_float2(f[0], f[1]), make_float2(f[2], f[3])),
+                                        f2add(make_float2(f[4], f[5]), make_float2(f[6], f[7])));
+                ls = (double)(s2.x + s2.y);  // (the fused pass's association)
               } else {
                 ls = 0.0;
 #pragma unroll
