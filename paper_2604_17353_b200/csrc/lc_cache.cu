@@ -1325,8 +1325,8 @@ __global__ void fill_rows_kernel(CacheDev c, const int32_t* __restrict__ slot, c
   const uint64_t st = states[i];
   const uint64_t peak = avalanche64(st ^ kPeakSalt) % (uint64_t)vocab;
   const float boost = (float)__dmul_rn(conc, range);
-  for (int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; v < vocab; v += (int64_t)gridDim.x * blockDim.x)
-    o[v] = producer_value<OutT>(st, v, peak, boost, range);
+  produce_row<OutT>(o, vocab, st, peak, boost, range, (int64_t)blockIdx.x * blockDim.x + threadIdx.x,
+                    (int64_t)gridDim.x * blockDim.x);
 }
 
 __global__ void set_tokens_kernel(CacheDev c, const int32_t* __restrict__ slot, const uint32_t* __restrict__ gen,

@@ -48,8 +48,8 @@ __global__ void fill_logits_kernel(const uint64_t* __restrict__ states, int64_t 
   uint64_t peak = avalanche64(st ^ kPeakSalt) % (uint64_t)vocab;
   float boost = (float)__dmul_rn(conc, range);
   OutT* o = out + row * stride;
-  for (int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; v < vocab; v += (int64_t)gridDim.x * blockDim.x)
-    o[v] = producer_value<OutT>(st, v, peak, boost, range);
+  produce_row<OutT>(o, vocab, st, peak, boost, range, (int64_t)blockIdx.x * blockDim.x + threadIdx.x,
+                    (int64_t)gridDim.x * blockDim.x);
 }
 
 }  // namespace lcb
