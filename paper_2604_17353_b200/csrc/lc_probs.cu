@@ -262,21 +262,15 @@ extern "C" int lc_row_entropy(const void* d_rows, int dtype, int64_t vocab, int6
   return LC_OK;
 }
 
-// truncate() on explicit probabilities (sampling.py:71-94): kept prefix of the
+// truncate() on explicit probabilities (sampling.py:71-94), slow reference-shaped path: kept prefix of the
 // (p desc, id asc) order by block-wide argmax steps, sequential csum against
 // top_p ('left' cut, inclusive), renormalised by numpy's pairwise sum of the
 // kept values in sorted order.  O(V * kept) -- an API-parity path, not the hot
 // path (the fused lc_resample never materialises truncated probabilities).
 namespace lcb {
-__global__ void __launch_bounds__(PB_THREADS)
-truncate_probs_kernel(const double* probs, int64_t V, int64_t stride, int topk, double topp, double* out,
-                      int32_t* ord_scr, double* val_scr) {
-  __shared__ double s_bp[PB_THREADS];
-  __shared__ int64_t s_bi[PB_THREADS];
-  const double* p = probs + blockIdx.x * stride;
-  double* o = out + blockIdx.x * stride;
-  int32_t* ord = ord_scr + blockIdx.x * V;
-  double* val = val_scr + blockIdx.x * V;
+// fallback (rows the fast path below cannot take): kept prefix by block-wide argmax steps
+__device__ void truncate_row_slow(const double* p, int64_t V, int topk, double topp, double* o, int32_t* ord,
+                                  double* val, double* s_bp, int64_t* s_bi) {
   const int64_t lim = (topk > 0 && topk < V) ? topk : V;
   double last_p = INFINITY;
   int64_t last_id = -1, n = 0;
@@ -331,6 +325,208 @@ truncate_probs_kernel(const double* probs, int64_t V, int64_t stride, int topk, 
 }
 }  // namespace lcb
 
+namespace lcb {
+// Fast path of truncate(): a radix select over the order keys of p (8-bit digits from the top,
+// per-bin counts and masses) finds a key bound L such that C = {key >= L} -- a prefix of the
+// (p desc, id asc) order -- holds the kept set (|C| >= top_k, or mass(C) >= top_p with a margin
+// covering the summation-order gap to numpy's sequential cumsum) with |C| <= TR_CAP.  C is
+// gathered, sorted (bitonic on (p desc, id asc)), one thread runs numpy's sequential cumsum
+// over it (a prefix's csum values depend only on that prefix) and the pairwise-sum normaliser
+// over the kept values in sorted order, and the block scatters kept / ks.  Rows it cannot take
+// (> TR_CAP values at the boundary, NaN, a mass target above the row's total) take the slow path.
+constexpr int TR_CAP = 4096;
+
+struct TrSmem {
+  unsigned long long ck[TR_CAP];  // candidate order keys (after the sort: their p values)
+  int ci[TR_CAP];                 // candidate ids
+  unsigned int hc[256];
+  double hm[256];
+  double s_bp[PB_THREADS];
+  int64_t s_bi[PB_THREADS];
+  unsigned long long prefix, lbound;
+  long long acnt;
+  double amass, ks;
+  int pbits, mode, ncand, K;  // mode: 0 refining, 1 bound found, 2 slow path
+};
+
+__device__ __forceinline__ unsigned long long tr_key(double p) {
+  const unsigned long long u = (unsigned long long)__double_as_longlong(p == 0.0 ? 0.0 : p);  // -0 == +0
+  return (u >> 63) ? ~u : (u | 0x8000000000000000ull);
+}
+__device__ __forceinline__ double tr_val(unsigned long long k) {
+  const unsigned long long u = (k >> 63) ? (k & 0x7fffffffffffffffull) : ~k;
+  return __longlong_as_double((long long)u);
+}
+
+__global__ void __launch_bounds__(PB_THREADS)
+truncate_probs_kernel(const double* probs, int64_t V, int64_t stride, int topk, double topp, double* out,
+                      int32_t* ord_scr, double* val_scr) {
+  extern __shared__ __align__(16) unsigned char tr_raw[];
+  TrSmem& sm = *reinterpret_cast<TrSmem*>(tr_raw);
+  const double* p = probs + blockIdx.x * stride;
+  double* o = out + blockIdx.x * stride;
+  const int tid = threadIdx.x;
+  const long long Ktk = (topk > 0 && topk < V) ? topk : V;
+  const bool by_k = Ktk < V, by_p = topp < 1.0;
+  const double target = topp * (1.0 + 4.0 * (double)(V + 8) * 0x1p-53);
+  if (tid == 0) {
+    sm.prefix = 0ull;
+    sm.pbits = 0;
+    sm.acnt = 0;
+    sm.amass = 0.0;
+    sm.mode = 0;
+    sm.ncand = 0;
+  }
+  __syncthreads();
+  for (int pass = 0; pass < 8 && sm.mode == 0; ++pass) {
+    const int shift = 56 - 8 * pass;
+    const int pbits = sm.pbits;
+    const unsigned long long prefix = sm.prefix;
+    for (int b = tid; b < 256; b += PB_THREADS) {
+      sm.hc[b] = 0u;
+      sm.hm[b] = 0.0;
+    }
+    __syncthreads();
+    bool nan = false;
+    for (int64_t i = tid; i < V; i += PB_THREADS) {
+      const double pi = p[i];
+      nan |= pi != pi;
+      const unsigned long long k = tr_key(pi);
+      if (pbits == 0 || (k >> (64 - pbits)) == prefix) {
+        const int b = (int)((k >> shift) & 255ull);
+        atomicAdd(&sm.hc[b], 1u);
+        atomicAdd(&sm.hm[b], pi);
+      }
+    }
+    nan = __syncthreads_or(nan);
+    if (tid == 0) {
+      if (nan) {
+        sm.mode = 2;
+      } else {
+        long long c = sm.acnt;
+        double m = sm.amass;
+        int bs = -1;
+        for (int b = 255; b >= 0; --b) {
+          c += sm.hc[b];
+          m += sm.hm[b];
+          if ((by_k && c >= Ktk) || (by_p && m >= target)) {
+            bs = b;
+            break;
+          }
+        }
+        if (bs < 0) {
+          // never reached inside this range: only possible at the top level (target above the
+          // row's mass, or no truncation asked): every element is a candidate
+          if (pbits == 0 && c <= TR_CAP) {
+            sm.mode = 1;
+            sm.lbound = 0ull;
+          } else {
+            sm.mode = 2;
+          }
+        } else if (c <= TR_CAP) {
+          sm.mode = 1;
+          sm.lbound = ((prefix << 8) | (unsigned long long)bs) << shift;
+          if (pbits > 0) sm.lbound |= 0ull;  // (prefix bits already in place above the digit)
+        } else if (pass == 7) {
+          sm.mode = 2;  // one value holds more than TR_CAP elements
+        } else {
+          for (int b = 255; b > bs; --b) {
+            sm.acnt += sm.hc[b];
+            sm.amass += sm.hm[b];
+          }
+          sm.prefix = (prefix << 8) | (unsigned long long)bs;
+          sm.pbits = pbits + 8;
+        }
+      }
+    }
+    __syncthreads();
+  }
+  if (sm.mode != 1) {
+    truncate_row_slow(p, V, topk, topp, o, ord_scr + blockIdx.x * V, val_scr + blockIdx.x * V, sm.s_bp, sm.s_bi);
+    return;
+  }
+  // gather C = {key >= lbound}
+  const unsigned long long L = sm.lbound;
+  for (int64_t i = tid; i < V; i += PB_THREADS) {
+    const unsigned long long k = tr_key(p[i]);
+    if (k >= L) {
+      const int slot = atomicAdd(&sm.ncand, 1);
+      if (slot < TR_CAP) {
+        sm.ck[slot] = k;
+        sm.ci[slot] = (int)i;
+      }
+    }
+  }
+  __syncthreads();
+  const int nc = sm.ncand;
+  if (nc > TR_CAP) {  // (cannot happen: the count above is exact) -- defensive
+    truncate_row_slow(p, V, topk, topp, o, ord_scr + blockIdx.x * V, val_scr + blockIdx.x * V, sm.s_bp, sm.s_bi);
+    return;
+  }
+  int np2 = 1;
+  while (np2 < nc) np2 <<= 1;
+  for (int i = nc + tid; i < np2; i += PB_THREADS) {  // padding sorts last
+    sm.ck[i] = 0ull;
+    sm.ci[i] = 0x7fffffff;
+  }
+  __syncthreads();
+  // bitonic sort, "before" = (key desc, id asc) first
+  for (int k = 2; k <= np2; k <<= 1) {
+    for (int j = k >> 1; j > 0; j >>= 1) {
+      for (int i = tid; i < np2; i += PB_THREADS) {
+        const int l = i ^ j;
+        if (l > i) {
+          const unsigned long long ka = sm.ck[i], kb = sm.ck[l];
+          const int ia = sm.ci[i], ib = sm.ci[l];
+          const bool a_first = ka > kb || (ka == kb && ia < ib);
+          const bool asc = (i & k) == 0;  // this block of the network puts "before" first
+          if (asc != a_first) {
+            sm.ck[i] = kb;
+            sm.ck[l] = ka;
+            sm.ci[i] = ib;
+            sm.ci[l] = ia;
+          }
+        }
+      }
+      __syncthreads();
+    }
+  }
+  // values in sorted order (in place), then numpy's cumsum cut and pairwise normaliser
+  for (int i = tid; i < nc; i += PB_THREADS) sm.ck[i] = (unsigned long long)__double_as_longlong(tr_val(sm.ck[i]));
+  __syncthreads();
+  if (tid == 0) {
+    const double* v = reinterpret_cast<const double*>(sm.ck);
+    long long K = Ktk < nc ? Ktk : nc;
+    bool ok = Ktk <= nc;
+    if (by_p) {
+      double c = 0.0;
+      long long i = 0;
+      for (; i < K; ++i) {
+        c += v[i];
+        if (c >= topp) break;
+      }
+      if (i < K) {
+        K = i + 1;
+        ok = true;
+      }  // else: no index reached top_p within the first min(top_k, nc): all top_k kept (ok iff nc >= Ktk)
+    }
+    sm.K = ok ? (int)K : -1;
+    if (ok) sm.ks = pairwise_seq(v, K);
+  }
+  __syncthreads();
+  const int K = sm.K;
+  if (K < 0) {
+    truncate_row_slow(p, V, topk, topp, o, ord_scr + blockIdx.x * V, val_scr + blockIdx.x * V, sm.s_bp, sm.s_bi);
+    return;
+  }
+  for (int64_t i = tid; i < V; i += PB_THREADS) o[i] = 0.0;
+  __syncthreads();
+  const double ks = sm.ks;
+  const double* v = reinterpret_cast<const double*>(sm.ck);
+  for (int i = tid; i < K; i += PB_THREADS) o[sm.ci[i]] = __ddiv_rn(v[i], ks);
+}
+}  // namespace lcb
+
 extern "C" int lc_truncate_probs(const double* d_probs, int64_t vocab, int64_t n_rows, int64_t row_stride,
                                  int32_t top_k, double top_p, double* d_out, void* d_scratch, void* stream) {
   if (n_rows < 0 || vocab < 1 || (n_rows > 0 && (!d_probs || !d_out || !d_scratch))) return LC_E_ARG;
@@ -338,7 +534,13 @@ extern "C" int lc_truncate_probs(const double* d_probs, int64_t vocab, int64_t n
   if (n_rows == 0) return LC_OK;
   int32_t* ord = (int32_t*)d_scratch;
   double* val = (double*)((char*)d_scratch + ((n_rows * vocab * 4 + 255) & ~255ll));
-  lcb::truncate_probs_kernel<<<(unsigned)n_rows, lcb::PB_THREADS, 0, (cudaStream_t)stream>>>(
+  static bool attr = false;
+  if (!attr) {
+    LCB_CUDA_TRY(cudaFuncSetAttribute(lcb::truncate_probs_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      (int)sizeof(lcb::TrSmem)));
+    attr = true;
+  }
+  lcb::truncate_probs_kernel<<<(unsigned)n_rows, lcb::PB_THREADS, sizeof(lcb::TrSmem), (cudaStream_t)stream>>>(
       d_probs, vocab, row_stride, top_k, top_p, d_out, ord, val);
   LCB_CUDA_TRY(cudaGetLastError());
   return LC_OK;

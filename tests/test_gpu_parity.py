@@ -930,3 +930,21 @@ def test_resample_entropy_epilogue_matches_oracle(dtype):
         nz = p[p > 0]
         assert abs(H[i].item() - float(-(nz * np.log(nz)).sum())) <= 1e-11 * max(1.0, float(np.log(V)))
         assert abs(P[i].item() - float(p.max())) <= 1e-12
+
+
+@pytest.mark.parametrize("V,conc,T,k,p", [(32000, 2.5, 0.6, None, 0.9), (32000, 0.0, 1.0, None, 0.9),
+                                         (151936, 2.5, 0.6, 50, 0.95), (32000, 2.5, 0.6, 7, 1.0),
+                                         (1000, 0.0, 5.0, None, 0.5), (128256, 0.0, 0.6, None, 0.99)])
+def test_truncate_probs_fast_path_matches_oracle(V, conc, T, k, p):
+    """lc_truncate_probs (radix-select fast path; rows with > 4096 kept values or an unreachable
+    target take the slow path) vs numpy truncate(softmax(z, T), k, p), bit for bit, including
+    rows with many equal probabilities (quantised logits)."""
+    rng = np.random.default_rng(V + int(T * 10))
+    rows = mixing_ref.fill_rows_np([mixing_ref.mix2(31, i) for i in range(4)], V, conc)
+    rows[3] = np.round(rows[3] * 2) / 2  # ties
+    for z in rows:
+        prob = sampling_ref.softmax(z, T)
+        want = sampling_ref.truncate(prob, k, p)
+        got = lcb.truncate(prob, k, p)
+        assert np.array_equal(np.asarray(got), want), (V, k, p)
+    assert rng is not None
