@@ -407,7 +407,7 @@ def run_ours(args, cfg, rank, world, dev):
         "unresolved_draws": unresolved,
         "bad_rows": bad,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                     "frac": achieved / peak, "traffic": traffic_per_launch(cfg, n_rows), "peak_source": peak_src,
+                     "frac": achieved / peak, "traffic": traffic_per_launch(cfg, hot_rows), "peak_source": peak_src,
                      "kernel": "lc_cache_resample (stage_kernel + resample_kernel requeue + exact_kernel)",
                      "kernel_ms_avg": k_avg, "algorithmic_bytes_per_launch": algo_bytes_launch},
         "e2e": {"value": tokens_total / (e2e_ms * 1e-3), "unit": "tokens/s", "h2d_bytes_per_step": h2d,
