@@ -1212,6 +1212,9 @@ constexpr int RW_CAND = 256;      // bracket candidates per warp
 constexpr int RW_NB = 1024;       // histogram bins: 32 per octave over 32 octaves (+ catch-all)
 constexpr float RW_BPO = 32.0f;
 constexpr int RW_SEGSTEPS = 8;    // 8 x 256 ids = 2048 per segment
+#ifndef LCB_RW_PF
+#define LCB_RW_PF 0  // segments prefetched into L2 ahead of the fused pass (2: +0.3%, 4: -5%; off)
+#endif
 constexpr int RW_SEG = 256 * RW_SEGSTEPS;
 constexpr int RW_MAXV = 65536;
 constexpr int RW_NSEG = RW_MAXV / RW_SEG;  // 32
@@ -1288,7 +1291,18 @@ __device__ __noinline__ FusedOut rw_fused_pass(const char* row, int V, int nseg,
   const float ka = (float)kArgRel * 1.0001f;
   // segments wholly inside an aligned row take the check-free vector loop
   const int nfull = vec ? V / RW_SEG : 0;
+  // L2 prefetch LCB_RW_PF segments ahead (one bulk prefetch instruction per segment): the
+  // warp's own loads then mostly hit L2, so more of the row is in flight than the registers of
+  // its LDG pipeline hold (HBM still sees each byte once)
+  constexpr int esz = DT == LC_BF16 ? 2 : 4;
+  if (LCB_RW_PF > 0 && lane == 0 && vec)
+    for (int s2 = 0; s2 < LCB_RW_PF && s2 < nfull; ++s2)
+      asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(row + (size_t)s2 * RW_SEG * esz),
+                   "r"((uint32_t)(RW_SEG * esz)) : "memory");
   for (int s = 0; s < nseg; ++s) {
+    if (LCB_RW_PF > 0 && lane == 0 && vec && s + LCB_RW_PF < nfull)
+      asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(row + (size_t)(s + LCB_RW_PF) * RW_SEG * esz),
+                   "r"((uint32_t)(RW_SEG * esz)) : "memory");
     double acc = 0.0;
     float W = 0.0f, R = 0.0f;  // |a|-weighted mass (CHEAP) and rescale error, relative to mt
     // one vector of 8 ids at e0 (vmax NaN-propagating; vmin over ids < V)
