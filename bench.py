@@ -197,13 +197,15 @@ def run_ours(args, cfg, rank, world, dev):
 
     import paper_2604_17353_b200 as lcb
 
+    sim = getattr(args, "one_rank_of", None)  # measure one rank's share of a G-GPU run on this GPU
+    pw = sim or world
     if cfg["scaling"] == "strong":  # trees sharded across ranks: tree i -> rank i % world
         from paper_2604_17353_b200.shard import local_trees
 
         cfg = dict(cfg)
         n_trees = 8
         per_tree = cfg["n_req"] // n_trees
-        cfg["n_req"] = len(local_trees(n_trees, rank, world)) * per_tree
+        cfg["n_req"] = len(local_trees(n_trees, rank if not sim else 0, pw)) * per_tree
     w = setup_workload(cfg, dev, rank, world)
     cache = w["cache"]
     V, n_req, nb, R = cfg["V"], cfg["n_req"], cfg["nb"], cfg["R"]
@@ -375,7 +377,7 @@ def run_ours(args, cfg, rank, world, dev):
     accepted, precise, unresolved, bad, exact = (int(x) for x in counts.tolist())
     if rank != 0:
         return None
-    tokens_total = (n_draws * args.steps * world if cfg["scaling"] == "weak"
+    tokens_total = (n_draws * args.steps * world if cfg["scaling"] == "weak" or sim
                     else CONFIGS[args.config]["n_req"] * R * nb * args.steps)
     if args.policy == "hotspot":  # only hotspot positions draw
         tokens_total = hot_rows * nb * args.steps * world
@@ -400,7 +402,7 @@ def run_ours(args, cfg, rank, world, dev):
                    **({"hotspot_rows": hot_rows, "hotspot_uncertain_entries": hotspot_uncertain}
                       if args.policy == "hotspot" else {})},
         "accepted_tokens_per_s": accepted / (ms * 1e-3),
-        "rows_per_s": (n_rows * world if cfg["scaling"] == "weak" else CONFIGS[args.config]["n_req"] * R)
+        "rows_per_s": (n_rows * world if cfg["scaling"] == "weak" or sim else CONFIGS[args.config]["n_req"] * R)
         * args.steps / (ms * 1e-3),
         "precise_tasks": precise,
         "exact_tasks": exact,
@@ -415,6 +417,11 @@ def run_ours(args, cfg, rank, world, dev):
                 "d2h_bytes_per_step": d2h},
         "gpu_launches": 8 * args.steps,
         "cuda_graph": graph is not None,
+        **({"simulated_rank": {"of": sim, "rank": 0, "rows_per_step": n_rows,
+                               "note": "one rank's share of a G-GPU run, measured alone on this GPU (ranks share "
+                                       "nothing on the data path); value is that rank's throughput",
+                               "aggregate_if_ranks_independent": tokens_total / (ms * 1e-3) * sim}}
+           if sim else {}),
         "clocks": clk.summary(),
     }
     if not args.no_check and args.policy == "step_wise":
@@ -1094,6 +1101,9 @@ def main():
                     help="c3: lookup hit ratio h of the sweep (default: every branch cached)")
     ap.add_argument("--graph", action=argparse.BooleanOptionalAction, default=None,
                     help="replay the step from a CUDA graph (default: on for the tree-sharded c5)")
+    ap.add_argument("--one-rank-of", type=int, default=None, metavar="G",
+                    help="run rank 0's share of a G-GPU run on this one GPU (no process group): the per-rank "
+                         "throughput behind the scaling curve")
     ap.add_argument("--dry-run", action="store_true",
                     help="no GPU: run the N-rank host logic (shard plan + statistics reduction) over gloo")
     args = ap.parse_args()
