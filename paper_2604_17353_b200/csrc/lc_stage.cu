@@ -242,7 +242,9 @@ __global__ void __launch_bounds__(SG_THREADS, 1) stage_kernel(StageArgs a) {
     return;
   }
 
-  const int g = warp / SG_GW, gw = warp % SG_GW, gt = tid - g * SG_GT;
+  // (the group index broadcast from lane 0: provably warp-uniform, so the group's shared-memory
+  // bases live in uniform registers and gathers / atomics address [R + UR] without an IADD)
+  const int g = __shfl_sync(0xffffffffu, warp / SG_GW, 0), gw = warp % SG_GW, gt = tid - g * SG_GT;
   SgGroup& G = sm.g[g];
   uint4* R = sm.ring[g];
   const DrawIO& io = a.io;
@@ -667,8 +669,12 @@ __global__ void __launch_bounds__(SG_THREADS, 1) stage_kernel(StageArgs a) {
             const int Rv = (nvec + SG_GT - 1) / SG_GT;  // vectors per range (25 at V = 32000)
             const int v0 = min(Rv * gt, nvec), v1 = min(v0 + Rv, nvec);
             double ma = 0.0;
-            int mc = 0;
+            // cut-class elements counted packed: per 16-bit half, 1 unless the offset is bs
+            // (xor + one packed min), subtracted from the number of halves visited
+            uint32_t ne2 = 0u;
+            int nvis = 0;
             for (int vb = v0; vb < v1; vb += SG_RB) {
+              nvis += SG_RB;
               uint32_t w[SG_RB][4];
 #pragma unroll
               for (int k = 0; k < SG_RB; ++k) {
@@ -688,11 +694,12 @@ __global__ void __launch_bounds__(SG_THREADS, 1) stage_kernel(StageArgs a) {
                   const uint32_t c = __vminu2(w[k][h], bs2);
                   a0 += G.ev[c & 0xffffu];
                   a1 += G.ev[c >> 16];
-                  mc += (int)(off_lo(w[k][h]) == bs) + (int)(off_hi(w[k][h]) == bs);
+                  ne2 += __vminu2(w[k][h] ^ bs2, 0x00010001u);
                 }
               }
               ma += a0 + a1;
             }
+            const int mc = 8 * nvis - (int)((ne2 & 0xffffu) + (ne2 >> 16));
             // group inclusive scan of (ma, mc)
             double mi = ma;
             int ci = mc;
@@ -762,14 +769,15 @@ __global__ void __launch_bounds__(SG_THREADS, 1) stage_kernel(StageArgs a) {
                 if (act && x0 + k < x1) qv = R[x0 + k];
                 const uint32_t w[4] = {qv.x, qv.y, qv.z, qv.w};
                 double a0 = 0.0, a1 = 0.0;
-                int c = 0;
+                uint32_t n2 = 0u;  // packed: halves whose offset is not bs
 #pragma unroll
                 for (int h = 0; h < 4; ++h) {
                   const uint32_t cl = __vminu2(w[h], bs2);
                   a0 += G.ev[cl & 0xffffu];
                   a1 += G.ev[cl >> 16];
-                  c += (int)(off_lo(w[h]) == bs) + (int)(off_hi(w[h]) == bs);
+                  n2 += __vminu2(w[h] ^ bs2, 0x00010001u);
                 }
+                const int c = 8 - (int)((n2 & 0xffffu) + (n2 >> 16));
                 mk[k] = a0 + a1;
                 tk[k] = c;
                 ma_q += mk[k];
