@@ -246,6 +246,12 @@ __global__ void __launch_bounds__(SG_THREADS, 1) stage_kernel(StageArgs a) {
   // bases live in uniform registers and gathers / atomics address [R + UR] without an IADD)
   const int g = __shfl_sync(0xffffffffu, warp / SG_GW, 0), gw = warp % SG_GW, gt = tid - g * SG_GT;
   SgGroup& G = sm.g[g];
+  // byte bases of the histogram and the class-value table: bins and (clamped) classes are
+  // < 2^13, so the high half's byte offset is one shift of the packed word
+  char* const hb = reinterpret_cast<char*>(G.hist);
+  const char* const evb = reinterpret_cast<const char*>(G.ev);
+  auto ev_at = [](const char* b, uint32_t c) { return *reinterpret_cast<const double*>(b + (lo16(c) << 3)); };
+  auto ev_hi = [](const char* b, uint32_t c) { return *reinterpret_cast<const double*>(b + (c >> 13)); };
   uint4* R = sm.ring[g];
   const DrawIO& io = a.io;
   const bool prof = a.prof != nullptr && gt == 0;
@@ -491,8 +497,9 @@ __global__ void __launch_bounds__(SG_THREADS, 1) stage_kernel(StageArgs a) {
               // histogram bins: offsets clamped (one packed min) to the lane's dump bin; bins in
               // [nb_eff, SG_NB) also count tail elements and are never read
               const uint32_t hc = __vminu2(o[k], dump2);
-              atomicAdd(&G.hist[hc & 0xffffu], 1u);
-              atomicAdd(&G.hist[hc >> 16], 1u);
+              // (both bins < 2^14: the high bin's byte offset is hc >> 14, one LEA.HI)
+              atomicAdd(reinterpret_cast<uint32_t*>(hb + (lo16(hc) << 2)), 1u);
+              atomicAdd(reinterpret_cast<uint32_t*>(hb + (hc >> 14)), 1u);
               const uint32_t ol = o[k] & 0xffffu, oh = o[k] >> 16;
               const bool il = ol < (uint32_t)nb_eff, ih = oh < (uint32_t)nb_eff;
               // both halves' arguments in one FFMA2; -inf -> 0
@@ -692,8 +699,8 @@ __global__ void __launch_bounds__(SG_THREADS, 1) stage_kernel(StageArgs a) {
                 for (int h = 0; h < 4; ++h) {
                   // offsets >= bs clamped (one packed min) onto the zeroed entry bs
                   const uint32_t c = __vminu2(w[k][h], bs2);
-                  a0 += G.ev[c & 0xffffu];
-                  a1 += G.ev[c >> 16];
+                  a0 += ev_at(evb, c);
+                  a1 += ev_hi(evb, c);
                   ne2 += __vminu2(w[k][h] ^ bs2, 0x00010001u);
                 }
               }
@@ -773,8 +780,8 @@ __global__ void __launch_bounds__(SG_THREADS, 1) stage_kernel(StageArgs a) {
 #pragma unroll
                 for (int h = 0; h < 4; ++h) {
                   const uint32_t cl = __vminu2(w[h], bs2);
-                  a0 += G.ev[cl & 0xffffu];
-                  a1 += G.ev[cl >> 16];
+                  a0 += ev_at(evb, cl);
+                  a1 += ev_hi(evb, cl);
                   n2 += __vminu2(w[h] ^ bs2, 0x00010001u);
                 }
                 const int c = 8 - (int)((n2 & 0xffffu) + (n2 >> 16));

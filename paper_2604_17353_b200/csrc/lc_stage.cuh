@@ -93,6 +93,9 @@ __device__ __forceinline__ float key16_to_f(uint32_t k) {
   const uint32_t h = (k & 0x8000u) ? (k & 0x7fffu) : (~k & 0xffffu);
   return __uint_as_float(h << 16);
 }
+// the low half zero-extended by a byte permute (PRMT): kept apart from the shift that follows, so
+// base + (lo << s) is one LEA instead of shift + mask + add
+__device__ __forceinline__ uint32_t lo16(uint32_t w) { return __byte_perm(w, 0u, 0x4410); }
 __device__ __forceinline__ uint32_t off_lo(uint32_t w) { return w & 0xffffu; }
 __device__ __forceinline__ uint32_t off_hi(uint32_t w) { return w >> 16; }
 
