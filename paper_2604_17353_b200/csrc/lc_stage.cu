@@ -60,9 +60,10 @@ constexpr double kLn2 = 0.6931471805599453;
 // (pinned by tests/test_gpu_parity.py::test_bf16_ex2_bound over every bf16 input)
 constexpr float kEx2Bf16Err = 0.01f;  // measured max 0.0071 (2^-7.1)
 constexpr double kEx2Bf16F = (1.0 + (double)kEx2Bf16Err) / (1.0 - (double)kEx2Bf16Err);  // ratio bound factor
-// B's summation error relative to the exact sum of its (positive) bf16 exponentials: two packed
-// bf16 roundings ((1 + 2^-9)^2 - 1) plus fp32 chains of <= 25 + 5 + 2 additions (2^-24 each)
-constexpr double kPairAcc = 0x1p-8 + 0x1p-18 + 40.0 * 0x1p-24;
+// B's summation error relative to the exact sum of its (positive) bf16 exponentials: every
+// exponential is added exactly-representable into fp32 (FHADD.BF16): four chains of <= 50 terms
+// per thread, + 2 (the chains combined) + 5 (warp tree) additions of 2^-24 each (first order x 1.01)
+constexpr double kPairAcc = 64.0 * 0x1p-24;
 
 struct SgGroup {
   uint32_t hist[SG_NB + 32];  // + one dump bin per lane (branch-free out-of-range increments)
@@ -395,19 +396,18 @@ __global__ void __launch_bounds__(SG_THREADS, 1) stage_kernel(StageArgs a) {
         const float Lbf = __uint_as_float(Lb << 16);
         const uint32_t nmLb = bf16_bits(-(m * Lbf));
         const uint32_t L2 = Lb | (Lb << 16), nmL2 = nmLb | (nmLb << 16);
-        // the 8 exponentials of a vector are summed pairwise in packed bf16 (two roundings,
-        // relative 2^-8 + 2^-18 on positive terms) and the pair sums added into fp32
-        float ac0 = 0.0f, ac1 = 0.0f;
+        // the 8 bf16 exponentials of a vector are added straight into four fp32 chains (one per
+        // word: <= 50 terms each)
+        float ac0 = 0.0f, ac1 = 0.0f, ac2 = 0.0f, ac3 = 0.0f;
 #pragma unroll 4
         for (int v = gt; v < nvec; v += SG_GT) {
           const uint4 q = R[v];
-          const uint32_t e0 = bex2(bfma2(q.x, L2, nmL2)), e1 = bex2(bfma2(q.y, L2, nmL2));
-          const uint32_t e2 = bex2(bfma2(q.z, L2, nmL2)), e3 = bex2(bfma2(q.w, L2, nmL2));
-          const uint32_t s4 = badd2(badd2(e0, e1), badd2(e2, e3));
-          ac0 = bacc_lo(ac0, s4);
-          ac1 = bacc_hi(ac1, s4);
+          ac0 = bex2_acc(ac0, bfma2(q.x, L2, nmL2));
+          ac1 = bex2_acc(ac1, bfma2(q.y, L2, nmL2));
+          ac2 = bex2_acc(ac2, bfma2(q.z, L2, nmL2));
+          ac3 = bex2_acc(ac3, bfma2(q.w, L2, nmL2));
         }
-        const float acc = ac0 + ac1;
+        const float acc = (ac0 + ac1) + (ac2 + ac3);
         // one barrier for the mass and the first argmax
         {
           const float ws = warp_sum(acc);
@@ -428,7 +428,7 @@ __global__ void __launch_bounds__(SG_THREADS, 1) stage_kernel(StageArgs a) {
         const float emax = lo_f(bex2(bfma2(mb | (mb << 16), L2, nmL2)));
         // exponent error <= 2^-8 (1.001 |a| + |delta|), |delta| <= 2^-9 |m Lb|;
         // elements below 2^-40 bounded absolutely.  Summation: Sc <= (1 + kPairAcc) sum E_i
-        // (packed bf16 pair sums, then fp32 chains of <= 25 + 5 + 2 terms, all positive), so
+        // (fp32 chains of <= 50 + 2 + 5 terms, all positive), so
         // sum_{i != amax} E_i / E_max <= Sc (1 + kPairAcc) / E_max - 1
         const float dl = 0.001953125f * mL * 1.01f + 0.001953125f;
         // (no fp64 divisions on this per-row path: the ratio is a constant, 1/emax a correctly

@@ -73,6 +73,15 @@ __device__ __forceinline__ uint32_t badd2(uint32_t a, uint32_t b) {
   asm("add.rn.bf16x2 %0, %1, %2;" : "=r"(r) : "r"(a), "r"(b));
   return r;
 }
+// acc + ex2(lo(a)) + ex2(hi(a)): the two bf16 exponentials (MUFU.EX2.BF16 per half) added straight
+// into fp32 (FHADD.BF16) -- no repacking of the halves, no bf16 rounding of pair sums
+__device__ __forceinline__ float bex2_acc(float acc, uint32_t a) {
+  asm("{\n .reg .b16 l, h, el, eh;\n mov.b32 {l, h}, %1;\n ex2.approx.ftz.bf16 el, l;\n ex2.approx.ftz.bf16 eh, h;\n"
+      " add.rn.f32.bf16 %0, el, %0;\n add.rn.f32.bf16 %0, eh, %0;\n}"
+      : "+f"(acc)
+      : "r"(a));
+  return acc;
+}
 // acc + lo(e) / acc + hi(e): one bf16 half added straight into fp32 (FHADD.BF16)
 __device__ __forceinline__ float bacc_lo(float acc, uint32_t e) {
   asm("{\n .reg .b16 lo, hi;\n mov.b32 {lo, hi}, %1;\n add.rn.f32.bf16 %0, lo, %0;\n}" : "+f"(acc) : "r"(e));
