@@ -387,6 +387,9 @@ __global__ void __launch_bounds__(WG_THREADS, 1) wide_kernel(StageArgs a) {
       WG_PH(2);
       const float thr = G.thr;
       const unsigned long long thrk = G.thrk;
+      // the vector pre-test as one compare: "> thr" once the list was compacted is ">= the next
+      // float above thr" (NaN when thr is +inf: nothing passes)
+      const float thr_c = !thrk ? thr : (thr < INFINITY ? nextafterf(thr, INFINITY) : __int_as_float(0x7fc00000));
       // mass relative to ref (fp32 MUFU, |a|-weighted bound), the chunk max, candidates >= thr
       const float ref = (c == 0 || need_thr) ? mc : M_run;
       const float nmL = -(ref * Lf);
@@ -401,7 +404,7 @@ __global__ void __launch_bounds__(WG_THREADS, 1) wide_kernel(StageArgs a) {
           const uint32_t w[4] = {q.x, q.y, q.z, q.w};
           // (once the list was compacted, only values above the k-th value can still enter)
           const float vmx = max_nan(lo_f(vm2), hi_f(vm2));
-          const bool any_c = thrk ? vmx > thr : vmx >= thr;
+          const bool any_c = vmx >= thr_c;
           if (any_c) {
             // (ties of the k-th value with larger ids than the k-th key cannot enter: ids grow
             // with the chunks, so the list stops growing once it has been compacted).  Few
