@@ -130,7 +130,9 @@ __device__ void wg_producer(const StageArgs& a, WgSmem& sm, int lane) {
       // wait until the slot's previous occupant (sequence slot_seq - WG_FQ) was copied out by
       // its own consumer: consumers finish out of order, so a completion count is not enough
       if (lane == 0)
-        while (vload(&sm.fq_free[slot_seq % WG_FQ]) != slot_seq) __nanosleep(64);
+        // (the FIFO is full for most of a wide row: back off, so the spin takes few issue slots
+        // from the group warps on this SM sub-partition)
+        for (unsigned ns = 64; vload(&sm.fq_free[slot_seq % WG_FQ]) != slot_seq; ns = min(2 * ns, 2048u)) __nanosleep(ns);
       __syncwarp();
       const int slot = slot_seq % WG_FQ;
       if (nb > 0) {
