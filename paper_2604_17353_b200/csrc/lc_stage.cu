@@ -162,7 +162,9 @@ __device__ void sg_producer(const StageArgs& a, SgSmem& sm, int lane) {
       // wait until the slot's previous occupant (sequence slot_seq - SG_FQ) was copied out by
       // its own consumer: consumers finish out of order, so a completion count is not enough
       if (lane == 0)
-        while (ld_acquire(&sm.fq_free[slot_seq % SG_FQ]) != slot_seq) __nanosleep(64);
+        // (the FIFO is usually full: back off, so the spin takes few issue slots from the group
+        // warps on this SM sub-partition; ~2 rows of look-ahead per group absorb the late wake-up)
+        for (unsigned ns = 64; ld_acquire(&sm.fq_free[slot_seq % SG_FQ]) != slot_seq; ns = min(2 * ns, 1024u)) __nanosleep(ns);
       __syncwarp();
       const int slot = slot_seq % SG_FQ;
       if (nb > 0) {
