@@ -634,11 +634,15 @@ __global__ void __launch_bounds__(SG_THREADS, 1) stage_kernel(StageArgs a) {
                 if (SGC * gt + k == bstar) n = cnt[k];
               }
               const double e = G.ev[bstar];
-              const double jd = ceil((target - A) / e);
+              // (no fp64 divisions on this serial path: correctly rounded reciprocals, one more
+              // rounding per quotient inside rho's slack; j only proposes the tie count, the two
+              // certified inequalities decide it)
+              const double rS = __drcp_rn(Scut);
+              const double jd = ceil((target - A) * __drcp_rn(e));
               const int j = (int)fmin(fmax(jd, 1.0), (double)n);
-              const double rho = relA + EScut / Scut + relNp + (double)(V + 8) * u53;
-              const bool ok_hi = (A + (double)j * e) / Scut * (1.0 - rho) >= tv.topp;
-              const bool ok_lo = (A + (double)(j - 1) * e) / Scut * (1.0 + rho) < tv.topp;
+              const double rho = relA + EScut * rS * (1.0 + 4.0 * u53) + relNp + (double)(V + 12) * u53;
+              const bool ok_hi = (A + (double)j * e) * rS * (1.0 - rho) >= tv.topp;
+              const bool ok_lo = (A + (double)(j - 1) * e) * rS * (1.0 + rho) < tv.topp;
               // +-0 are one value for the reference (equal p, id order): a cut on a zero
               // class with the other zero class present is left to the CTA kernel
               const uint32_t kb = km - (uint32_t)bstar;
