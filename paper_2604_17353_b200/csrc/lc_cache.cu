@@ -30,6 +30,7 @@
 #include "lc_cache.cuh"
 #include "lc_common.cuh"
 #include "lc_resample.cuh"
+#include "lc_stage.cuh"
 
 namespace lcb {
 
@@ -699,13 +700,32 @@ __device__ __forceinline__ void warp_push_pages_rev(const CacheDev& c, Ctl& L, R
   }
 }
 
+// resume (optional, written by commit_kernel): [0] = first insert still to apply, [1] = 1 when
+// the insert before it still owes its evictions; the warp applies inserts [resume[0], n).
 __global__ void __launch_bounds__(32) insert_policy_kernel(CacheDev c, const uint64_t* __restrict__ dig,
                                                            const int32_t* __restrict__ lens,
                                                            const int32_t* __restrict__ vocabs, int64_t n,
                                                            int32_t* out_slot, uint32_t* out_gen,
                                                            const int32_t* __restrict__ keep,
-                                                           const uint32_t* __restrict__ keep_gen) {
+                                                           const uint32_t* __restrict__ keep_gen,
+                                                           const int* __restrict__ resume) {
   const int lane = threadIdx.x;
+  bool pend = false;
+  if (resume) {
+    const int64_t start = resume[0];
+    pend = resume[1] != 0;
+    if (start >= n && !pend) return;
+    dig += start;
+    lens += start;
+    vocabs += start;
+    out_slot += start;
+    out_gen += start;
+    if (keep) {
+      keep += start;
+      keep_gen += start;
+    }
+    n -= start;
+  }
   Ctl L = *c.ctl;
   RegStack fs{-1ll << 40, 0u, 0}, fp{-1ll << 40, 0u, 0};
   RingWin w;
@@ -730,6 +750,44 @@ __global__ void __launch_bounds__(32) insert_policy_kernel(CacheDev c, const uin
       vv = 0;
     }
   };
+  // the LRU eviction loop after an insert (logits_cache.py:134-140); sh_b / sp_s / st_home /
+  // st_slot are the current chunk's speculative records, marked by every write
+  auto evict_loop = [&](uint32_t sh_b, int sp_s, unsigned& st_home, unsigned& st_slot) {
+    auto mark_slot = [&](int x) {
+      st_slot |= __ballot_sync(0xffffffffu, sp_s == x);
+      w.stale |= __ballot_sync(0xffffffffu, w.slot == x);
+    };
+    while (L.total_bytes > L.budget && L.alive > 1) {
+      Victim v = warp_next_victim(c, L, w, lane);
+      if (v.s < 0) break;
+      // evict_entry
+      mark_slot(v.s);
+      if (v.quick) {  // key at its home bucket, next bucket empty: no shift
+        if (lane == 0) c.hvals[v.hb] = -1;
+        st_home |= __ballot_sync(0xffffffffu, sh_b == v.hb);
+        w.bstale |= __ballot_sync(0xffffffffu, w.hb == v.hb || ((w.hb + 1) & c.hmask) == v.hb);
+      } else {
+        window_delete(c, v.digest, lane, sh_b, st_home, w.hb, w.bstale);
+      }
+      L.total_bytes -= v.nbytes;
+      warp_push_pages(c, L, fp, v.s, lane, v.pg);
+      rs_push1(fs, c.free_slots, L.free_slot_top, v.s, lane);
+      L.free_slot_top += 1;
+      if (lane == 0) {
+        c.gen[v.s] = v.gen + 1u;
+        c.alive[v.s] = 0;
+      }
+      last_ev_slot = v.s;
+      last_ev_gen = v.gen + 1u;
+      L.alive -= 1;
+      L.evictions += 1;
+      __syncwarp();
+    }
+  };
+  if (pend) {  // the fast commit stopped inside an insert's eviction loop
+    unsigned h0 = 0u, s0 = 0u;
+    evict_loop(0xffffffffu, -1, h0, s0);
+  }
   uint64_t d0, d1, d2;
   int n0, n1, n2, v0, v1, v2;
   ld(lane, d0, n0, v0);
@@ -892,32 +950,7 @@ __global__ void __launch_bounds__(32) insert_policy_kernel(CacheDev c, const uin
         my_gen = g;
       }
       __syncwarp();
-      while (L.total_bytes > L.budget && L.alive > 1) {
-        Victim v = warp_next_victim(c, L, w, lane);
-        if (v.s < 0) break;
-        // evict_entry
-        mark_slot(v.s);
-        if (v.quick) {  // key at its home bucket, next bucket empty: no shift
-          if (lane == 0) c.hvals[v.hb] = -1;
-          st_home |= __ballot_sync(0xffffffffu, sh_b == v.hb);
-          w.bstale |= __ballot_sync(0xffffffffu, w.hb == v.hb || ((w.hb + 1) & c.hmask) == v.hb);
-        } else {
-          window_delete(c, v.digest, lane, sh_b, st_home, w.hb, w.bstale);
-        }
-        L.total_bytes -= v.nbytes;
-        warp_push_pages(c, L, fp, v.s, lane, v.pg);
-        rs_push1(fs, c.free_slots, L.free_slot_top, v.s, lane);
-        L.free_slot_top += 1;
-        if (lane == 0) {
-          c.gen[v.s] = v.gen + 1u;
-          c.alive[v.s] = 0;
-        }
-        last_ev_slot = v.s;
-        last_ev_gen = v.gen + 1u;
-        L.alive -= 1;
-        L.evictions += 1;
-        __syncwarp();
-      }
+      evict_loop(sh_b, sp_s, st_home, st_slot);
     }
     if (lane < cnt) {
       out_slot[i0 + lane] = my_slot;
@@ -928,6 +961,534 @@ __global__ void __launch_bounds__(32) insert_policy_kernel(CacheDev c, const uin
   }
   __syncwarp();
   if (lane == 0) *c.ctl = L;
+}
+
+// ---- batched fast commit (single-page entries: BASELINE config 4) ---------------------------
+//
+// The warp policy spends ~400 dependent warp instructions per insert on probes, LRU window
+// bookkeeping and hash-table edits (profiles/r1_ncu_policy_v3.txt).  For caches of
+// single-page entries (maxp == 1) a batch is split three ways instead:
+//   * prep_keys_kernel / prep_prev_kernel (parallel): each insert's start-of-batch view -- the
+//     slot holding its key and that entry's generation / bytes / page -- and the previous
+//     insert of the same key in the batch;
+//   * prep_cand_kernel (parallel): the LRU end of the event ring at batch start, compacted per
+//     256-position tile to the live events with their entries' records;
+//   * commit_kernel: ONE thread applies the batch in index order from those records (streamed
+//     into shared memory by bulk copies), with the free-stack tops mirrored in shared memory
+//     and a bitmap of the start-of-batch entries gone (overwritten or evicted) during the
+//     batch -- the only thing that can invalidate a record, since entries created in the
+//     batch are younger than every start-of-batch candidate and so never its victims.
+//     Hash-table edits decide nothing (slots and pages come from the stacks), so the commit
+//     thread only logs them and a second warp applies the log in order, overlapped.
+// Anything outside that model (a side list of pinned entries at batch start, a config or
+// capacity error, the scanned candidates used up) stops the commit at that insert with the
+// control block flushed, and insert_policy_kernel resumes from there.  Slots, generations,
+// victims and accounting are those of insert_policy_scalar_kernel (logits_cache.py:96-140).
+
+struct alignas(16) InsRec {  // 48 B
+  uint64_t d;
+  long long nb0;   // bytes of the entry holding d at batch start
+  int32_t s0;      // its slot, -1 absent
+  uint32_t gen0;   // its generation
+  int32_t pg0;     // its page, -1 none
+  int32_t nr, vv;  // the insert's rows / vocab
+  int32_t prev;    // largest j < i with d_j == d_i, -1 none
+};
+struct alignas(16) CandRec {  // 48 B: one live event at batch start
+  uint64_t dg;
+  long long nb;
+  unsigned long long ck;
+  int32_t s;
+  uint32_t gen;
+  int32_t pg;
+  int32_t off;  // ring position - tail0
+  int32_t pins;
+  int32_t pad;
+};
+struct HashOp {  // s >= 0: insert d -> s; s < 0: delete d
+  uint64_t d;
+  int32_t s;
+  int32_t pad;
+};
+constexpr int kFcTile = 256;    // records per bulk-copied tile
+constexpr int kFcMirror = 2048;  // free-stack entries mirrored in shared memory
+
+__global__ void prep_keys_kernel(CacheDev c, const uint64_t* __restrict__ dig, const int32_t* __restrict__ lens,
+                                 const int32_t* __restrict__ vocabs, int64_t n, InsRec* __restrict__ rec) {
+  const int64_t key = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 3;
+  const int sub = threadIdx.x & 7;
+  const int lane = threadIdx.x & 31;
+  const unsigned tile_bits = 0xffu << (lane & 24);
+  const bool active = key < n;
+  const uint64_t d = active ? dig[key] : 0ull;
+  const uint32_t start = home_bucket(d, c.hmask);
+  int result = -1;
+  bool done = !active;
+  for (uint32_t round = 0; __any_sync(0xffffffffu, !done); ++round) {
+    bool match = false, empty = false;
+    if (!done) {
+      const uint32_t b = (start + round * 8u + sub) & c.hmask;
+      const int32_t v = c.hvals[b];
+      match = v >= 0 && c.hkeys[b] == d;
+      empty = v < 0;
+      if (match) result = v;
+      if (round * 8u > c.hmask) empty = true;
+    }
+    const unsigned mm = __ballot_sync(0xffffffffu, match) & tile_bits;
+    const unsigned em = __ballot_sync(0xffffffffu, empty) & tile_bits;
+    if (!done) {
+      if (mm) {
+        result = __shfl_sync(tile_bits, result, __ffs(mm) - 1, 32);
+        done = true;
+      } else if (em) {
+        result = -1;
+        done = true;
+      }
+    }
+  }
+  if (active && sub == 0) {
+    InsRec r;
+    r.d = d;
+    r.s0 = result;
+    r.nr = lens[key];
+    r.vv = vocabs[key];
+    r.prev = -1;
+    r.gen0 = result >= 0 ? c.gen[result] : 0u;
+    r.nb0 = result >= 0 ? c.nbytes[result] : 0;
+    r.pg0 = result >= 0 ? c.pages[(int64_t)result * c.maxp] : -1;
+    rec[key] = r;
+  }
+}
+
+// prev[i] = the largest j < i with d_j == d_i: block b scans the key tiles b, b-1, ... 0 from
+// shared memory until every key of the block found one (duplicates are rare: usually all tiles)
+__global__ void __launch_bounds__(256) prep_prev_kernel(const uint64_t* __restrict__ dig, int64_t n,
+                                                        InsRec* __restrict__ rec) {
+  __shared__ uint64_t t[256];
+  const int64_t i = (int64_t)blockIdx.x * 256 + threadIdx.x;
+  const uint64_t d = i < n ? dig[i] : 0ull;
+  int prev = -1;
+  for (int tb = blockIdx.x; tb >= 0; --tb) {
+    const int64_t j0 = (int64_t)tb * 256;
+    __syncthreads();
+    t[threadIdx.x] = j0 + threadIdx.x < n ? dig[j0 + threadIdx.x] : 0ull;
+    __syncthreads();
+    if (prev < 0 && i < n) {
+      const int jm = (int)min((int64_t)256, i - j0);
+      for (int k0 = jm - 1; k0 >= 0 && prev < 0; k0 -= 16) {
+        int f = -1;
+#pragma unroll
+        for (int u = 15; u >= 0; --u) {  // the highest matching k of the 16 wins
+          const int k = k0 - u;
+          if (k >= 0 && t[k] == d) f = k;
+        }
+        if (f >= 0) prev = (int)(j0 + f);
+      }
+    }
+    if (__syncthreads_and(prev >= 0 || i >= n)) break;
+  }
+  if (i < n && prev >= 0) rec[i].prev = prev;
+}
+
+// Tile b: ring positions tail0 + 256 b + [0, 256) below min(head0, tail0 + mcap); the live
+// events (alive, last_hit == event clock) in position order with their entries' records.
+__global__ void __launch_bounds__(256) prep_cand_kernel(CacheDev c, long long mcap, CandRec* __restrict__ cand,
+                                                        int* __restrict__ cnt) {
+  __shared__ int wcnt[8];
+  const long long tail0 = c.ctl->ring_tail, head0 = c.ctl->ring_head;
+  const long long lim = min(head0, tail0 + mcap);
+  const long long p = tail0 + (long long)blockIdx.x * 256 + threadIdx.x;
+  bool live = false;
+  int s = -1;
+  unsigned long long ck = 0;
+  if (p < lim) {
+    s = c.ring_slot[p & c.rmask];
+    ck = c.ring_clock[p & c.rmask];
+    live = c.alive[s] && c.last_hit[s] == ck;
+  }
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const unsigned b = __ballot_sync(0xffffffffu, live);
+  if (lane == 0) wcnt[wid] = __popc(b);
+  __syncthreads();
+  int off = __popc(b & ((1u << lane) - 1u)), tot = 0;
+  for (int k = 0; k < 8; ++k) {
+    if (k < wid) off += wcnt[k];
+    tot += wcnt[k];
+  }
+  if (live) {
+    CandRec r;
+    r.dg = c.digest[s];
+    r.nb = c.nbytes[s];
+    r.ck = ck;
+    r.s = s;
+    r.gen = c.gen[s];
+    r.pg = c.pages[(int64_t)s * c.maxp];
+    r.off = (int)(p - tail0);
+    r.pins = c.pins[s];
+    r.pad = 0;
+    cand[(int64_t)blockIdx.x * 256 + off] = r;
+  }
+  if (threadIdx.x == 0) cnt[blockIdx.x] = tot;
+}
+
+__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+
+// grid (1), block 128: warp 0 lane 0 commits, warp 1 applies the hash log; all four warps
+// fill the shared-memory mirrors first.  Dynamic shared memory: see fc_smem_bytes.
+__global__ void __launch_bounds__(128) commit_kernel(CacheDev c, const InsRec* __restrict__ rec, int64_t n,
+                                                     const CandRec* __restrict__ cand, const int* __restrict__ cnt,
+                                                     int ntiles, long long mcap, HashOp* __restrict__ hlog,
+                                                     int32_t* __restrict__ out_slot, uint32_t* __restrict__ out_gen,
+                                                     int* __restrict__ resume) {
+  extern __shared__ __align__(16) unsigned char fc_smem[];
+  unsigned long long* bars = reinterpret_cast<unsigned long long*>(fc_smem);  // rec 0/1, cand 0/1
+  volatile int* s_flag = reinterpret_cast<volatile int*>(fc_smem + 32);       // [0] log count, [1] finished
+  InsRec* rbuf = reinterpret_cast<InsRec*>(fc_smem + 64);
+  CandRec* cbuf = reinterpret_cast<CandRec*>(fc_smem + 64 + 2 * kFcTile * sizeof(InsRec));
+  unsigned long long* wk =  // the log warp's staged hash windows: 32 edits x 32 buckets
+      reinterpret_cast<unsigned long long*>(fc_smem + 64 + 2 * kFcTile * (sizeof(InsRec) + sizeof(CandRec)));
+  int* wv = reinterpret_cast<int*>(wk + 32 * 32);
+  int* ms_val = wv + 32 * 32;
+  uint32_t* ms_gen = reinterpret_cast<uint32_t*>(ms_val + kFcMirror);
+  int* mp_val = reinterpret_cast<int*>(ms_gen + kFcMirror);
+  int* cnt_s = mp_val + kFcMirror;
+  uint32_t* gone = reinterpret_cast<uint32_t*>(cnt_s + ntiles);
+  const int tid = threadIdx.x;
+  Ctl L = *c.ctl;
+  const int bs = max(0, L.free_slot_top - kFcMirror / 2);
+  const int bp = max(0, L.free_page_top - kFcMirror / 2);
+  for (int k = tid; k < (c.E + 31) / 32; k += blockDim.x) gone[k] = 0u;
+  for (int k = tid; k < kFcMirror; k += blockDim.x) {
+    if (bs + k < L.free_slot_top) {
+      const int v = c.free_slots[bs + k];
+      ms_val[k] = v;
+      ms_gen[k] = c.gen[v];
+    }
+    if (bp + k < L.free_page_top) mp_val[k] = c.free_pages[bp + k];
+  }
+  for (int k = tid; k < ntiles; k += blockDim.x) cnt_s[k] = cnt[k];
+  if (tid == 0) {
+    for (int k = 0; k < 4; ++k) mbar_init(&bars[k], 1);
+    mbar_fence_init();
+    s_flag[0] = 0;
+    s_flag[1] = 0;
+  }
+  __syncthreads();
+
+  if (tid >= 32 && tid < 64) {  // ---- log warp: apply the hash edits in log order ----
+    const int lane = tid & 31;
+    int k = 0;
+    for (;;) {
+      const int fin = s_flag[1];
+      __threadfence_block();
+      const int avail = s_flag[0];
+      if (k >= avail) {
+        if (fin) break;
+        __nanosleep(100);
+        continue;
+      }
+      __threadfence_block();
+      const int m = min(32, avail - k);
+      HashOp op{0ull, -1, 0};
+      if (lane < m) op = hlog[k + lane];
+      const uint32_t hb = home_bucket(op.d, c.hmask);
+      // stage the m windows with all their loads in flight (L2: the warp's own edits land there)
+      for (int j0 = 0; j0 < m; j0 += 16) {
+        int v[16];
+        unsigned long long kk[16];
+#pragma unroll
+        for (int u = 0; u < 16; ++u) {
+          const uint32_t b = (__shfl_sync(0xffffffffu, hb, (j0 + u) & 31) + lane) & c.hmask;
+          if (j0 + u < m) {
+            v[u] = __ldcg(c.hvals + b);
+            kk[u] = __ldcg(reinterpret_cast<const unsigned long long*>(c.hkeys) + b);
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < 16; ++u)
+          if (j0 + u < m) {
+            wv[(j0 + u) * 32 + lane] = v[u];
+            wk[(j0 + u) * 32 + lane] = kk[u];
+          }
+      }
+      __syncwarp();
+      bool stale = false;  // this lane's staged window (op lane) saw a bucket written since
+      auto mark = [&](uint32_t b) { stale |= ((b - hb) & c.hmask) < 32u; };
+      for (int j = 0; j < m; ++j) {
+        const uint64_t d = __shfl_sync(0xffffffffu, op.d, j);
+        const int s = __shfl_sync(0xffffffffu, op.s, j);
+        const uint32_t b0 = __shfl_sync(0xffffffffu, hb, j);
+        const bool st = __shfl_sync(0xffffffffu, (int)stale, j);
+        const uint32_t bl = (b0 + lane) & c.hmask;
+        const int hv = st ? __ldcg(c.hvals + bl) : wv[j * 32 + lane];
+        const uint64_t hk = st ? __ldcg(reinterpret_cast<const unsigned long long*>(c.hkeys) + bl) : wk[j * 32 + lane];
+        const unsigned em = __ballot_sync(0xffffffffu, hv < 0);
+        if (s >= 0) {  // insert d -> s at the first empty bucket of its chain
+          if (em) {
+            const uint32_t b = (b0 + __ffs(em) - 1) & c.hmask;
+            if (lane == 0) {
+              c.hkeys[b] = d;
+              c.hvals[b] = s;
+            }
+            mark(b);
+          } else {
+            if (lane == 0) table_insert(c, d, s);
+            stale = true;
+          }
+          __syncwarp();
+          continue;
+        }
+        // delete d: backward shift inside the window when its chain closes there
+        const unsigned mm = __ballot_sync(0xffffffffu, hv >= 0 && hk == d);
+        const int fe = em ? __ffs(em) - 1 : 32;
+        const unsigned hit = mm & (fe >= 32 ? 0xffffffffu : ((1u << fe) - 1u));
+        if (!hit) {
+          if (fe >= 32) {  // chain leaves the window
+            if (lane == 0) table_delete(c, d);
+            stale = true;
+          }
+          __syncwarp();
+          continue;
+        }
+        int i = __ffs(hit) - 1;
+        if (i + 1 >= 32 || (em >> (i + 1)) == 0u) {  // the shift may run past the window
+          if (lane == 0) table_delete(c, d);
+          stale = true;
+          __syncwarp();
+          continue;
+        }
+        const uint32_t home_l = home_bucket(hk, c.hmask);
+        for (int jj = i + 1;; ++jj) {
+          const int vj = __shfl_sync(0xffffffffu, hv, jj);
+          if (vj < 0) break;
+          const uint32_t kh = __shfl_sync(0xffffffffu, home_l, jj);
+          const uint32_t ai = (b0 + i) & c.hmask, aj = (b0 + jj) & c.hmask;
+          const bool stays = (ai <= aj) ? (ai < kh && kh <= aj) : (ai < kh || kh <= aj);
+          if (stays) continue;
+          const uint64_t kj = __shfl_sync(0xffffffffu, hk, jj);
+          if (lane == 0) {
+            c.hkeys[ai] = kj;
+            c.hvals[ai] = vj;
+          }
+          mark(ai);
+          i = jj;
+        }
+        if (lane == 0) c.hvals[(b0 + i) & c.hmask] = -1;
+        mark((b0 + i) & c.hmask);
+        __syncwarp();
+      }
+      k += m;
+    }
+    return;
+  }
+  if (tid != 0) return;
+
+  // ---- commit thread ----
+  const long long tail0 = L.ring_tail, head0 = L.ring_head;
+  const long long lim = min(head0, tail0 + mcap);
+  const int nct = (int)((lim - tail0 + kFcTile - 1) / kFcTile);  // candidate tiles to walk
+  const int nrt = (int)((n + kFcTile - 1) / kFcTile);
+  constexpr uint32_t kRecTile = kFcTile * sizeof(InsRec), kCandTile = kFcTile * sizeof(CandRec);
+  for (int t = 0; t < 2; ++t) {
+    if (t < nrt) {
+      mbar_expect_tx(&bars[t], kRecTile);
+      bulk_load(rbuf + t * kFcTile, rec + (int64_t)t * kFcTile, kRecTile, &bars[t]);
+    }
+    if (t < nct) {
+      mbar_expect_tx(&bars[2 + t], kCandTile);
+      bulk_load(cbuf + t * kFcTile, cand + (int64_t)t * kFcTile, kCandTile, &bars[2 + t]);
+    }
+  }
+  int rt_issued = min(nrt, 2) - 1, rt_waited = -1, ct_issued = min(nct, 2) - 1;
+  int ct = 0, ci = 0, ccnt = 0;
+  if (nct > 0) {
+    mbar_wait(&bars[2], 0);
+    ccnt = cnt_s[0];
+  }
+  auto is_gone = [&](int s) { return (gone[s >> 5] >> (s & 31)) & 1u; };
+  auto set_gone = [&](int s) { gone[s >> 5] |= 1u << (s & 31); };
+  auto spush = [&](int v, uint32_t g) {
+    const int x = L.free_slot_top++;
+    c.free_slots[x] = v;
+    const unsigned m = (unsigned)(x - bs);
+    if (m < (unsigned)kFcMirror) {
+      ms_val[m] = v;
+      ms_gen[m] = g;
+    }
+  };
+  auto ppush = [&](int v) {
+    const int x = L.free_page_top++;
+    c.free_pages[x] = v;
+    const unsigned m = (unsigned)(x - bp);
+    if (m < (unsigned)kFcMirror) mp_val[m] = v;
+  };
+  int log_n = 0;
+  int64_t stop = n;
+  int pend = 0;
+  bool side_pending = L.side_count > 0;
+  if (side_pending) stop = 0;  // pinned entries wait at the LRU end: the warp policy handles them
+  for (int64_t i = 0; i < stop; ++i) {
+    const int t = (int)(i / kFcTile), k = (int)(i % kFcTile);
+    if (k == 0) {
+      mbar_wait(&bars[t & 1], (t >> 1) & 1);
+      rt_waited = t;
+    }
+    const InsRec r = rbuf[(t & 1) * kFcTile + k];
+    if (k == kFcTile - 1 && t + 2 < nrt) {  // tile consumed: fetch tile t + 2 into its buffer
+      rt_issued = t + 2;
+      fence_proxy_async();
+      mbar_expect_tx(&bars[t & 1], kRecTile);
+      bulk_load(rbuf + (t & 1) * kFcTile, rec + (int64_t)(t + 2) * kFcTile, kRecTile, &bars[t & 1]);
+    }
+    const int nr = r.nr, vv = r.vv;
+    if (nr < 0 || vv < 1 || vv > c.V || nr > c.page_rows) {  // config error: the warp latches it
+      stop = i;
+      break;
+    }
+    const int np = nr > 0 ? 1 : 0;
+    const long long bytes = (long long)nr * vv * 4 + 8ll * nr;  // logits_cache.py:54-56
+    int s = -1, pg_old = -1;
+    uint32_t g_old = 0;
+    long long nb_old = 0;
+    bool ow = false;
+    if (r.prev >= 0) {  // the key's entry is the one an earlier insert of this batch made (own writes)
+      s = out_slot[r.prev];
+      g_old = out_gen[r.prev];
+      nb_old = c.nbytes[s];
+      pg_old = c.pages[s];
+      ow = true;
+    } else if (r.s0 >= 0 && !is_gone(r.s0)) {
+      s = r.s0;
+      g_old = r.gen0;
+      nb_old = r.nb0;
+      pg_old = r.pg0;
+      ow = true;
+    }
+    if ((!ow && L.free_slot_top == 0) || L.free_page_top + (ow && pg_old >= 0 ? 1 : 0) < np) {
+      stop = i;  // capacity: the warp latches the error / rolls back exactly as the reference shape
+      break;
+    }
+    uint32_t g;
+    if (ow) {  // overwrite: the key keeps its slot, the entry is new
+      L.total_bytes -= nb_old;
+      if (pg_old >= 0) ppush(pg_old);
+      g = g_old + 1u;
+      c.gen[s] = g;
+      if (r.prev < 0) set_gone(s);
+    } else {
+      const int x = --L.free_slot_top;
+      const unsigned m = (unsigned)(x - bs);
+      if (m < (unsigned)kFcMirror) {
+        s = ms_val[m];
+        g = ms_gen[m];
+      } else {
+        s = c.free_slots[x];
+        g = c.gen[s];
+      }
+      hlog[log_n++] = HashOp{r.d, s, 0};
+      c.alive[s] = 1;
+      L.alive += 1;
+    }
+    int pg = -1;
+    if (np) {
+      const int x = --L.free_page_top;
+      const unsigned m = (unsigned)(x - bp);
+      pg = m < (unsigned)kFcMirror ? mp_val[m] : c.free_pages[x];
+    }
+    c.pages[s] = pg;
+    L.clock += 1;
+    c.last_hit[s] = (unsigned long long)L.clock;
+    c.pins[s] = 0;
+    c.nrows[s] = nr;
+    c.vocab[s] = vv;
+    c.nbytes[s] = bytes;
+    c.digest[s] = r.d;
+    {
+      const long long pos = L.ring_head & c.rmask;
+      c.ring_clock[pos] = (unsigned long long)L.clock;
+      c.ring_slot[pos] = s;
+      L.ring_head++;
+    }
+    L.total_bytes += bytes;
+    L.inserts += 1;
+    out_slot[i] = s;
+    out_gen[i] = g;
+    while (L.total_bytes > L.budget && L.alive > 1) {
+      // next_victim over the start-of-batch candidates
+      bool found = false;
+      CandRec v;
+      for (;;) {
+        if (ci >= ccnt) {
+          if (ct + 1 >= nct) break;  // scanned window used up
+          if (ct + 2 < nct) {
+            ct_issued = ct + 2;
+            fence_proxy_async();
+            mbar_expect_tx(&bars[2 + (ct & 1)], kCandTile);
+            bulk_load(cbuf + (ct & 1) * kFcTile, cand + (int64_t)(ct + 2) * kFcTile, kCandTile, &bars[2 + (ct & 1)]);
+          }
+          ++ct;
+          ci = 0;
+          mbar_wait(&bars[2 + (ct & 1)], (ct >> 1) & 1);
+          ccnt = cnt_s[ct];
+          continue;
+        }
+        v = cbuf[(ct & 1) * kFcTile + ci++];
+        L.ring_tail = tail0 + v.off + 1;
+        if (is_gone(v.s)) continue;  // overwritten during the batch: its event died
+        if (v.pins > 0) {            // pinned: to the side list (next_victim)
+          if (L.side_count < c.side_cap) {
+            c.side_slot[L.side_count] = v.s;
+            c.side_clock[L.side_count] = v.ck;
+            L.side_count++;
+          } else if (!L.error) {
+            L.error = LC_E_CAPACITY;
+          }
+          continue;
+        }
+        found = true;
+        break;
+      }
+      if (!found) {  // every scanned event consumed: the warp continues from the ring tail
+        L.ring_tail = lim;
+        pend = 1;
+        break;
+      }
+      // evict_entry
+      set_gone(v.s);
+      hlog[log_n++] = HashOp{v.dg, -1, 0};
+      L.total_bytes -= v.nb;
+      if (v.pg >= 0) {
+        c.pages[v.s] = -1;
+        ppush(v.pg);
+      }
+      spush(v.s, v.gen + 1u);
+      c.gen[v.s] = v.gen + 1u;
+      c.alive[v.s] = 0;
+      L.alive -= 1;
+      L.evictions += 1;
+    }
+    __threadfence_block();
+    s_flag[0] = log_n;
+    if (pend) {
+      stop = i + 1;
+      break;
+    }
+  }
+  // drain the tile loads still in flight (a CTA must not exit with bulk copies pending)
+  for (int t = rt_waited + 1; t <= rt_issued; ++t) mbar_wait(&bars[t & 1], (t >> 1) & 1);
+  for (int t = (nct > 0 ? ct : -1) + 1; t <= ct_issued; ++t) mbar_wait(&bars[2 + (t & 1)], (t >> 1) & 1);
+  *c.ctl = L;
+  resume[0] = (int)stop;
+  resume[1] = pend;
+  __threadfence_block();
+  s_flag[0] = log_n;
+  s_flag[1] = 1;
+}
+
+__host__ __device__ constexpr size_t fc_smem_bytes(int ntiles, int E) {
+  return 64 + 2 * kFcTile * (sizeof(InsRec) + sizeof(CandRec)) + 32 * 32 * 12 + (size_t)kFcMirror * 12 +
+         (size_t)ntiles * 4 +
+         (size_t)((E + 31) / 32) * 4;
 }
 
 // Copy the rows/tokens of inserts whose entry is still alive at the end of the batch.
@@ -1085,6 +1646,8 @@ struct lc_cache {
   int64_t probe_cap;
   long long ring_bound;  // host upper bound of ring occupancy
   std::vector<void*> allocs;
+  void* fc_buf;  // fast-commit scratch (records, candidates, hash log), grown on demand
+  size_t fc_cap;
 };
 
 namespace lcb {
@@ -1109,6 +1672,7 @@ extern "C" int lc_cache_destroy(lc_cache* c) {
   cudaSetDevice(c->cfg.device);
   cudaDeviceSynchronize();
   for (void* p : c->allocs) cudaFree(p);
+  if (c->fc_buf) cudaFree(c->fc_buf);
   cudaSetDevice(dev);
   delete c;
   return LC_OK;
@@ -1246,14 +1810,55 @@ static int insert_impl(lc_cache* c, const uint64_t* d_digests, const int32_t* d_
                        uint32_t* d_gen, const int32_t* d_keep, const uint32_t* d_keep_gen, cudaStream_t st) {
   int rc = ensure_ring(c, n, st);
   if (rc) return rc;
-  const char* sp = getenv("LCB_SCALAR_POLICY");  // A/B hook, read per call (tests switch it)
+  const char* sp = getenv("LCB_SCALAR_POLICY");  // A/B hooks, read per call (tests switch them)
   const bool scalar = sp && atoi(sp) != 0;
-  if (scalar)
+  const char* fe = getenv("LCB_FAST_COMMIT");
+  const bool fast = !scalar && !d_keep && c->dev.maxp == 1 && n <= 65536 && c->dev.E <= (1 << 20) &&
+                    !(fe && atoi(fe) == 0);
+  if (scalar) {
     insert_policy_scalar_kernel<<<1, 32, 0, st>>>(c->dev, d_digests, d_lengths, d_vocabs, n, d_slot, d_gen, d_keep,
                                                   d_keep_gen);
-  else
+  } else if (fast) {
+    long long mcap = 8 * n + 4096;
+    if (mcap > c->dev.R) mcap = c->dev.R;
+    mcap = (mcap + kFcTile - 1) / kFcTile * kFcTile;
+    const int ntiles = (int)(mcap / kFcTile);
+    const size_t nrec = (size_t)(n + kFcTile - 1) / kFcTile * kFcTile;
+    const size_t o_cand = nrec * sizeof(InsRec);
+    const size_t o_cnt = o_cand + (size_t)mcap * sizeof(CandRec);
+    const size_t o_log = (o_cnt + (size_t)ntiles * 4 + 15) / 16 * 16;
+    const size_t o_res = o_log + (size_t)(n + mcap) * sizeof(HashOp);
+    const size_t need = o_res + 16;
+    if (need > c->fc_cap) {
+      if (c->fc_buf) LCB_CUDA_TRY(cudaFree(c->fc_buf));
+      c->fc_buf = nullptr;
+      c->fc_cap = 0;
+      LCB_CUDA_TRY(cudaMalloc(&c->fc_buf, need));
+      c->fc_cap = need;
+    }
+    char* b = (char*)c->fc_buf;
+    InsRec* rec = (InsRec*)b;
+    CandRec* cand = (CandRec*)(b + o_cand);
+    int* cnt = (int*)(b + o_cnt);
+    HashOp* hlog = (HashOp*)(b + o_log);
+    int* resume = (int*)(b + o_res);
+    static bool smem_set = false;
+    if (!smem_set) {
+      LCB_CUDA_TRY(cudaFuncSetAttribute(commit_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 232448));
+      smem_set = true;
+    }
+    const size_t smem = fc_smem_bytes(ntiles, c->dev.E);
+    if (smem > 232448) return LC_E_CAPACITY;
+    prep_keys_kernel<<<ceil_div(n * 8, 256), 256, 0, st>>>(c->dev, d_digests, d_lengths, d_vocabs, n, rec);
+    prep_prev_kernel<<<ceil_div(n, 256), 256, 0, st>>>(d_digests, n, rec);
+    prep_cand_kernel<<<ntiles, 256, 0, st>>>(c->dev, mcap, cand, cnt);
+    commit_kernel<<<1, 128, smem, st>>>(c->dev, rec, n, cand, cnt, ntiles, mcap, hlog, d_slot, d_gen, resume);
     insert_policy_kernel<<<1, 32, 0, st>>>(c->dev, d_digests, d_lengths, d_vocabs, n, d_slot, d_gen, d_keep,
-                                           d_keep_gen);
+                                           d_keep_gen, resume);
+  } else {
+    insert_policy_kernel<<<1, 32, 0, st>>>(c->dev, d_digests, d_lengths, d_vocabs, n, d_slot, d_gen, d_keep,
+                                           d_keep_gen, nullptr);
+  }
   LCB_CUDA_TRY(cudaGetLastError());
   c->ring_bound += n;
   if (max_len > 0 && (d_rows || d_tokens)) {
