@@ -24,6 +24,7 @@
 //   * slots and pages come from LIFO free stacks -- the discipline restated in
 //     oracle/cache_ref.py, so slot and page indices are bit-exact vs the oracle.
 #include <cub/cub.cuh>
+#include <cstdio>
 #include <new>
 #include <vector>
 
@@ -988,11 +989,14 @@ __global__ void __launch_bounds__(32) insert_policy_kernel(CacheDev c, const uin
 struct alignas(16) InsRec {  // 48 B
   uint64_t d;
   long long nb0;   // bytes of the entry holding d at batch start
+  long long nb;    // the insert's bytes (logits_cache.py:54-56)
   int32_t s0;      // its slot, -1 absent
   uint32_t gen0;   // its generation
   int32_t pg0;     // its page, -1 none
-  int32_t nr, vv;  // the insert's rows / vocab
+  int32_t nr;      // the insert's rows (-1: invalid -- the warp policy latches the error)
+  int32_t vv;      // its vocab
   int32_t prev;    // largest j < i with d_j == d_i, -1 none
+  int32_t pad;
 };
 struct alignas(16) CandRec {  // 48 B: one live event at batch start
   uint64_t dg;
@@ -1010,6 +1014,7 @@ struct HashOp {  // s >= 0: insert d -> s; s < 0: delete d
   int32_t s;
   int32_t pad;
 };
+static_assert(sizeof(InsRec) % 16 == 0 && sizeof(CandRec) % 16 == 0, "bulk-copied records");
 constexpr int kFcTile = 256;    // records per bulk-copied tile
 constexpr int kFcMirror = 2048;  // free-stack entries mirrored in shared memory
 
@@ -1052,6 +1057,8 @@ __global__ void prep_keys_kernel(CacheDev c, const uint64_t* __restrict__ dig, c
     r.s0 = result;
     r.nr = lens[key];
     r.vv = vocabs[key];
+    if (r.nr < 0 || r.vv < 1 || r.vv > c.V || r.nr > c.page_rows * c.maxp) r.nr = -1;
+    r.nb = r.nr >= 0 ? (long long)r.nr * r.vv * 4 + 8ll * r.nr : 0;  // logits_cache.py:54-56
     r.prev = -1;
     r.gen0 = result >= 0 ? c.gen[result] : 0u;
     r.nb0 = result >= 0 ? c.nbytes[result] : 0;
@@ -1131,10 +1138,29 @@ __global__ void __launch_bounds__(256) prep_cand_kernel(CacheDev c, long long mc
   if (threadIdx.x == 0) cnt[blockIdx.x] = tot;
 }
 
+__device__ __forceinline__ unsigned long long globaltimer_ns() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
 __device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 
-// grid (1), block 128: warp 0 lane 0 commits, warp 1 applies the hash log; all four warps
-// fill the shared-memory mirrors first.  Dynamic shared memory: see fc_smem_bytes.
+// Entry-metadata writes of one committed insert (i >= 0) or eviction (i < 0), queued by the
+// commit thread for the writer warp.
+struct alignas(16) WRec {  // 32 B
+  uint64_t d;
+  int32_t s;
+  uint32_t g;   // the entry's generation (insert) / the slot's next generation (eviction)
+  int32_t pg;   // insert: its page (-1 none); eviction: 1 when pages[s] must be cleared
+  int32_t i;    // insert index, -1 eviction
+  int32_t nr, vv;
+};
+constexpr int kFcWRing = 1024;  // writer records in flight
+constexpr int kFcWin = 33;      // staged window row stride (conflict-free transposed access)
+
+// grid (1), block 128.  Warp 0 lane 0 commits; warp 1 applies the hash-edit log; warp 2 writes
+// the entries' metadata, ring events and outputs from the commit records; all four warps fill
+// the shared-memory mirrors first.  Dynamic shared memory: fc_smem_bytes.
 __global__ void __launch_bounds__(128) commit_kernel(CacheDev c, const InsRec* __restrict__ rec, int64_t n,
                                                      const CandRec* __restrict__ cand, const int* __restrict__ cnt,
                                                      int ntiles, long long mcap, HashOp* __restrict__ hlog,
@@ -1142,18 +1168,19 @@ __global__ void __launch_bounds__(128) commit_kernel(CacheDev c, const InsRec* _
                                                      int* __restrict__ resume) {
   extern __shared__ __align__(16) unsigned char fc_smem[];
   unsigned long long* bars = reinterpret_cast<unsigned long long*>(fc_smem);  // rec 0/1, cand 0/1
-  volatile int* s_flag = reinterpret_cast<volatile int*>(fc_smem + 32);       // [0] log count, [1] finished
+  // [0] log count, [1] finished, [2] writer records queued, [3] writer records done
+  volatile int* s_flag = reinterpret_cast<volatile int*>(fc_smem + 32);
   InsRec* rbuf = reinterpret_cast<InsRec*>(fc_smem + 64);
-  CandRec* cbuf = reinterpret_cast<CandRec*>(fc_smem + 64 + 2 * kFcTile * sizeof(InsRec));
-  unsigned long long* wk =  // the log warp's staged hash windows: 32 edits x 32 buckets
-      reinterpret_cast<unsigned long long*>(fc_smem + 64 + 2 * kFcTile * (sizeof(InsRec) + sizeof(CandRec)));
-  int* wv = reinterpret_cast<int*>(wk + 32 * 32);
-  int* ms_val = wv + 32 * 32;
+  CandRec* cbuf = reinterpret_cast<CandRec*>(rbuf + 2 * kFcTile);
+  WRec* wring = reinterpret_cast<WRec*>(cbuf + 2 * kFcTile);
+  unsigned long long* wk = reinterpret_cast<unsigned long long*>(wring + kFcWRing);  // staged windows
+  int* wv = reinterpret_cast<int*>(wk + 32 * kFcWin);
+  int* ms_val = wv + 32 * kFcWin;
   uint32_t* ms_gen = reinterpret_cast<uint32_t*>(ms_val + kFcMirror);
   int* mp_val = reinterpret_cast<int*>(ms_gen + kFcMirror);
   int* cnt_s = mp_val + kFcMirror;
   uint32_t* gone = reinterpret_cast<uint32_t*>(cnt_s + ntiles);
-  const int tid = threadIdx.x;
+  const int tid = threadIdx.x, lane = tid & 31;
   Ctl L = *c.ctl;
   const int bs = max(0, L.free_slot_top - kFcMirror / 2);
   const int bp = max(0, L.free_page_top - kFcMirror / 2);
@@ -1170,13 +1197,11 @@ __global__ void __launch_bounds__(128) commit_kernel(CacheDev c, const InsRec* _
   if (tid == 0) {
     for (int k = 0; k < 4; ++k) mbar_init(&bars[k], 1);
     mbar_fence_init();
-    s_flag[0] = 0;
-    s_flag[1] = 0;
+    for (int k = 0; k < 4; ++k) s_flag[k] = 0;
   }
   __syncthreads();
 
   if (tid >= 32 && tid < 64) {  // ---- log warp: apply the hash edits in log order ----
-    const int lane = tid & 31;
     int k = 0;
     for (;;) {
       const int fin = s_flag[1];
@@ -1184,7 +1209,7 @@ __global__ void __launch_bounds__(128) commit_kernel(CacheDev c, const InsRec* _
       const int avail = s_flag[0];
       if (k >= avail) {
         if (fin) break;
-        __nanosleep(100);
+        __nanosleep(64);
         continue;
       }
       __threadfence_block();
@@ -1192,7 +1217,8 @@ __global__ void __launch_bounds__(128) commit_kernel(CacheDev c, const InsRec* _
       HashOp op{0ull, -1, 0};
       if (lane < m) op = hlog[k + lane];
       const uint32_t hb = home_bucket(op.d, c.hmask);
-      // stage the m windows with all their loads in flight (L2: the warp's own edits land there)
+      // stage the m windows, all loads in flight together (from L2, where this warp's edits
+      // land); bucket hb_j + t of edit j at [t][j]
       for (int j0 = 0; j0 < m; j0 += 16) {
         int v[16];
         unsigned long long kk[16];
@@ -1207,83 +1233,146 @@ __global__ void __launch_bounds__(128) commit_kernel(CacheDev c, const InsRec* _
 #pragma unroll
         for (int u = 0; u < 16; ++u)
           if (j0 + u < m) {
-            wv[(j0 + u) * 32 + lane] = v[u];
-            wk[(j0 + u) * 32 + lane] = kk[u];
+            wv[lane * kFcWin + j0 + u] = v[u];
+            wk[lane * kFcWin + j0 + u] = kk[u];
           }
       }
       __syncwarp();
-      bool stale = false;  // this lane's staged window (op lane) saw a bucket written since
-      auto mark = [&](uint32_t b) { stale |= ((b - hb) & c.hmask) < 32u; };
-      for (int j = 0; j < m; ++j) {
+      // lane j: edit j's footprint [hb, hb + fe] (its cluster from the home bucket up to the
+      // first empty bucket) from its own window column; lng: the chain leaves the window
+      int fe = 32, at = -1;
+      if (lane < m) {
+        for (int t = 0; t < 32; ++t) {
+          const int hv = wv[t * kFcWin + lane];
+          if (hv < 0) {
+            fe = t;
+            break;
+          }
+          if (op.s < 0 && at < 0 && wk[t * kFcWin + lane] == op.d) at = t;
+        }
+      }
+      const bool lng = lane < m && fe >= 32;
+      // edits whose footprint meets (or touches) an earlier edit's, and every edit after a long
+      // one, are applied one by one after the others; the rest commute and run lane-parallel
+      bool seq = false;
+      const unsigned long_before = __ballot_sync(0xffffffffu, lng) & ((1u << lane) - 1u);
+      if (long_before || lng) seq = true;
+      for (int q = 0; q < m - 1; ++q) {
+        const uint32_t hq = __shfl_sync(0xffffffffu, hb, q);
+        const int fq = __shfl_sync(0xffffffffu, fe, q);
+        if (q < lane && (((hb - hq) & c.hmask) <= (uint32_t)fq + 1u || ((hq - hb) & c.hmask) <= (uint32_t)fe + 1u))
+          seq = true;
+      }
+      if (lane < m && !seq) {
+        if (op.s >= 0) {
+          const uint32_t b = (hb + fe) & c.hmask;
+          c.hkeys[b] = op.d;
+          c.hvals[b] = op.s;
+        } else if (at >= 0) {  // backward shift inside the cluster [at, fe)
+          int i = at;
+          for (int t = at + 1; t < fe; ++t) {
+            const uint64_t kt = wk[t * kFcWin + lane];
+            const uint32_t kh = home_bucket(kt, c.hmask);
+            const uint32_t ai = (hb + i) & c.hmask, aj = (hb + t) & c.hmask;
+            const bool stays = (ai <= aj) ? (ai < kh && kh <= aj) : (ai < kh || kh <= aj);
+            if (stays) continue;
+            c.hkeys[ai] = kt;
+            c.hvals[ai] = wv[t * kFcWin + lane];
+            i = t;
+          }
+          c.hvals[(hb + i) & c.hmask] = -1;
+        }
+      }
+      __syncwarp();
+      unsigned todo = __ballot_sync(0xffffffffu, lane < m && seq);
+      while (todo) {  // the rest in log order, warp-cooperative over fresh windows
+        const int j = __ffs(todo) - 1;
+        todo &= todo - 1u;
         const uint64_t d = __shfl_sync(0xffffffffu, op.d, j);
         const int s = __shfl_sync(0xffffffffu, op.s, j);
-        const uint32_t b0 = __shfl_sync(0xffffffffu, hb, j);
-        const bool st = __shfl_sync(0xffffffffu, (int)stale, j);
-        const uint32_t bl = (b0 + lane) & c.hmask;
-        const int hv = st ? __ldcg(c.hvals + bl) : wv[j * 32 + lane];
-        const uint64_t hk = st ? __ldcg(reinterpret_cast<const unsigned long long*>(c.hkeys) + bl) : wk[j * 32 + lane];
-        const unsigned em = __ballot_sync(0xffffffffu, hv < 0);
-        if (s >= 0) {  // insert d -> s at the first empty bucket of its chain
-          if (em) {
-            const uint32_t b = (b0 + __ffs(em) - 1) & c.hmask;
-            if (lane == 0) {
-              c.hkeys[b] = d;
-              c.hvals[b] = s;
-            }
-            mark(b);
-          } else {
-            if (lane == 0) table_insert(c, d, s);
-            stale = true;
-          }
-          __syncwarp();
-          continue;
-        }
-        // delete d: backward shift inside the window when its chain closes there
-        const unsigned mm = __ballot_sync(0xffffffffu, hv >= 0 && hk == d);
-        const int fe = em ? __ffs(em) - 1 : 32;
-        const unsigned hit = mm & (fe >= 32 ? 0xffffffffu : ((1u << fe) - 1u));
-        if (!hit) {
-          if (fe >= 32) {  // chain leaves the window
-            if (lane == 0) table_delete(c, d);
-            stale = true;
-          }
-          __syncwarp();
-          continue;
-        }
-        int i = __ffs(hit) - 1;
-        if (i + 1 >= 32 || (em >> (i + 1)) == 0u) {  // the shift may run past the window
-          if (lane == 0) table_delete(c, d);
-          stale = true;
-          __syncwarp();
-          continue;
-        }
-        const uint32_t home_l = home_bucket(hk, c.hmask);
-        for (int jj = i + 1;; ++jj) {
-          const int vj = __shfl_sync(0xffffffffu, hv, jj);
-          if (vj < 0) break;
-          const uint32_t kh = __shfl_sync(0xffffffffu, home_l, jj);
-          const uint32_t ai = (b0 + i) & c.hmask, aj = (b0 + jj) & c.hmask;
-          const bool stays = (ai <= aj) ? (ai < kh && kh <= aj) : (ai < kh || kh <= aj);
-          if (stays) continue;
-          const uint64_t kj = __shfl_sync(0xffffffffu, hk, jj);
+        if (s >= 0) {
+          uint32_t eb;
+          bool open = false;
+          window_find(c, d, lane, &eb, &open);
           if (lane == 0) {
-            c.hkeys[ai] = kj;
-            c.hvals[ai] = vj;
+            if (eb != 0xffffffffu && !open) {
+              c.hkeys[eb] = d;
+              c.hvals[eb] = s;
+            } else {
+              table_insert(c, d, s);
+            }
           }
-          mark(ai);
-          i = jj;
+          __syncwarp();
+        } else {
+          unsigned h0 = 0u, b0 = 0u;
+          window_delete(c, d, lane, 0xffffffffu, h0, 0xffffffffu, b0);
         }
-        if (lane == 0) c.hvals[(b0 + i) & c.hmask] = -1;
-        mark((b0 + i) & c.hmask);
-        __syncwarp();
       }
       k += m;
+    }
+    if (lane == 0) reinterpret_cast<unsigned long long*>(resume)[3] = globaltimer_ns();
+    return;
+  }
+
+  if (tid >= 64 && tid < 96) {  // ---- writer warp: entry metadata, ring events, outputs ----
+    int k = 0, ins = 0;
+    for (;;) {
+      const int fin = s_flag[1];
+      __threadfence_block();
+      const int avail = s_flag[2];
+      if (k >= avail) {
+        if (fin) break;
+        __nanosleep(64);
+        continue;
+      }
+      __threadfence_block();
+      while (k < avail) {  // 32 records per round, one per lane
+        const int m = min(32, avail - k);
+        WRec w{0ull, -1 - lane, 0u, -1, -2, 0, 0};
+        if (lane < m) w = wring[(k + lane) & (kFcWRing - 1)];
+        const int s = w.s;
+        const bool is_ins = w.i >= 0;
+        // a slot recurs in a round only as (eviction, then the insert that popped it): the
+        // round's last record of a slot writes its fields
+        const unsigned peers = __match_any_sync(0xffffffffu, s);
+        const bool last = (peers >> lane) == 1u;
+        const unsigned insm = __ballot_sync(0xffffffffu, is_ins);
+        const int rank = ins + __popc(insm & ((1u << lane) - 1u));
+        if (is_ins) {
+          const unsigned long long ck = (unsigned long long)(L.clock + rank + 1);
+          const long long pos = (L.ring_head + rank) & c.rmask;
+          c.ring_clock[pos] = ck;
+          c.ring_slot[pos] = s;
+          out_slot[w.i] = s;
+          out_gen[w.i] = w.g;
+          if (last) {
+            c.last_hit[s] = ck;
+            c.nbytes[s] = (long long)w.nr * w.vv * 4 + 8ll * w.nr;  // logits_cache.py:54-56
+            c.digest[s] = w.d;
+            c.pins[s] = 0;
+            c.nrows[s] = w.nr;
+            c.vocab[s] = w.vv;
+            c.gen[s] = w.g;
+            c.pages[s] = w.pg;
+            c.alive[s] = 1;
+          }
+        } else if (lane < m && last) {
+          c.gen[s] = w.g;
+          if (w.pg) c.pages[s] = -1;
+          c.alive[s] = 0;
+        }
+        ins += __popc(insm);
+        k += m;
+        __syncwarp();
+      }
+      if (lane == 0) s_flag[3] = k;
     }
     return;
   }
   if (tid != 0) return;
 
   // ---- commit thread ----
+  reinterpret_cast<unsigned long long*>(resume)[1] = globaltimer_ns();
   const long long tail0 = L.ring_tail, head0 = L.ring_head;
   const long long lim = min(head0, tail0 + mcap);
   const int nct = (int)((lim - tail0 + kFcTile - 1) / kFcTile);  // candidate tiles to walk
@@ -1305,53 +1394,95 @@ __global__ void __launch_bounds__(128) commit_kernel(CacheDev c, const InsRec* _
     mbar_wait(&bars[2], 0);
     ccnt = cnt_s[0];
   }
+  int wq = 0, wdone = 0;  // writer records queued / known done
+  long long cy_wput = 0, cy_drain = 0, cy_tile = 0, n_drain = 0;  // LCB_FC_PROF diagnostics
+  auto wput = [&](const WRec& w) {
+    if (wq - wdone >= kFcWRing) {
+      const long long c0 = clock64();
+      do {
+        wdone = s_flag[3];
+      } while (wq - wdone >= kFcWRing);
+      cy_wput += clock64() - c0;
+    }
+    wring[wq & (kFcWRing - 1)] = w;
+    ++wq;
+  };
+  auto wpublish = [&]() {
+    __threadfence_block();
+    s_flag[2] = wq;
+  };
+  auto wdrain = [&]() {  // the global entry state is current once the writer caught up
+    const long long c0 = clock64();
+    ++n_drain;
+    wpublish();
+    while (s_flag[3] < wq) {
+    }
+    __threadfence_block();
+    wdone = wq;
+    cy_drain += clock64() - c0;
+  };
   auto is_gone = [&](int s) { return (gone[s >> 5] >> (s & 31)) & 1u; };
   auto set_gone = [&](int s) { gone[s >> 5] |= 1u << (s & 31); };
+  int lo_s = 1 << 30, lo_p = 1 << 30;  // lowest mirrored stack index pushed (flushed at the end)
   auto spush = [&](int v, uint32_t g) {
     const int x = L.free_slot_top++;
-    c.free_slots[x] = v;
     const unsigned m = (unsigned)(x - bs);
     if (m < (unsigned)kFcMirror) {
       ms_val[m] = v;
       ms_gen[m] = g;
+      lo_s = min(lo_s, x);
+    } else {
+      c.free_slots[x] = v;
     }
   };
   auto ppush = [&](int v) {
     const int x = L.free_page_top++;
-    c.free_pages[x] = v;
     const unsigned m = (unsigned)(x - bp);
-    if (m < (unsigned)kFcMirror) mp_val[m] = v;
+    if (m < (unsigned)kFcMirror) {
+      mp_val[m] = v;
+      lo_p = min(lo_p, x);
+    } else {
+      c.free_pages[x] = v;
+    }
   };
   int log_n = 0;
-  int64_t stop = n;
+  int stop = (int)n;
   int pend = 0;
-  bool side_pending = L.side_count > 0;
-  if (side_pending) stop = 0;  // pinned entries wait at the LRU end: the warp policy handles them
-  for (int64_t i = 0; i < stop; ++i) {
-    const int t = (int)(i / kFcTile), k = (int)(i % kFcTile);
-    if (k == 0) {
+  // the hot control fields in registers, counters relative to the batch start
+  long long tot = L.total_bytes;
+  const long long budget = L.budget;
+  int alive = L.alive, ni = 0, ne = 0;
+  if (L.side_count > 0) stop = 0;  // pinned entries wait at the LRU end: the warp policy handles them
+  const InsRec* rt_base = rbuf;
+  int k = kFcTile - 1, t = -1;
+  for (int i = 0; i < stop; ++i) {
+    if (++k == kFcTile) {  // next record tile
+      k = 0;
+      ++t;
+      const long long c0 = clock64();
       mbar_wait(&bars[t & 1], (t >> 1) & 1);
+      cy_tile += clock64() - c0;
       rt_waited = t;
+      rt_base = rbuf + (t & 1) * kFcTile;
     }
-    const InsRec r = rbuf[(t & 1) * kFcTile + k];
+    const InsRec r = rt_base[k];
     if (k == kFcTile - 1 && t + 2 < nrt) {  // tile consumed: fetch tile t + 2 into its buffer
       rt_issued = t + 2;
       fence_proxy_async();
       mbar_expect_tx(&bars[t & 1], kRecTile);
       bulk_load(rbuf + (t & 1) * kFcTile, rec + (int64_t)(t + 2) * kFcTile, kRecTile, &bars[t & 1]);
     }
-    const int nr = r.nr, vv = r.vv;
-    if (nr < 0 || vv < 1 || vv > c.V || nr > c.page_rows) {  // config error: the warp latches it
+    if (r.nr < 0) {  // config error: the warp latches it
       stop = i;
       break;
     }
-    const int np = nr > 0 ? 1 : 0;
-    const long long bytes = (long long)nr * vv * 4 + 8ll * nr;  // logits_cache.py:54-56
+    const int np = r.nr > 0 ? 1 : 0;
     int s = -1, pg_old = -1;
     uint32_t g_old = 0;
     long long nb_old = 0;
     bool ow = false;
-    if (r.prev >= 0) {  // the key's entry is the one an earlier insert of this batch made (own writes)
+    if (r.prev >= 0) {  // the key's entry was made earlier in this batch: read it once written
+      wdrain();
       s = out_slot[r.prev];
       g_old = out_gen[r.prev];
       nb_old = c.nbytes[s];
@@ -1365,15 +1496,14 @@ __global__ void __launch_bounds__(128) commit_kernel(CacheDev c, const InsRec* _
       ow = true;
     }
     if ((!ow && L.free_slot_top == 0) || L.free_page_top + (ow && pg_old >= 0 ? 1 : 0) < np) {
-      stop = i;  // capacity: the warp latches the error / rolls back exactly as the reference shape
+      stop = i;  // capacity: the warp latches the error / rolls back as the reference shape does
       break;
     }
     uint32_t g;
     if (ow) {  // overwrite: the key keeps its slot, the entry is new
-      L.total_bytes -= nb_old;
+      tot -= nb_old;
       if (pg_old >= 0) ppush(pg_old);
       g = g_old + 1u;
-      c.gen[s] = g;
       if (r.prev < 0) set_gone(s);
     } else {
       const int x = --L.free_slot_top;
@@ -1381,13 +1511,13 @@ __global__ void __launch_bounds__(128) commit_kernel(CacheDev c, const InsRec* _
       if (m < (unsigned)kFcMirror) {
         s = ms_val[m];
         g = ms_gen[m];
-      } else {
+      } else {  // below the mirror: global, current once the writer caught up
+        wdrain();
         s = c.free_slots[x];
         g = c.gen[s];
       }
       hlog[log_n++] = HashOp{r.d, s, 0};
-      c.alive[s] = 1;
-      L.alive += 1;
+      ++alive;
     }
     int pg = -1;
     if (np) {
@@ -1395,25 +1525,10 @@ __global__ void __launch_bounds__(128) commit_kernel(CacheDev c, const InsRec* _
       const unsigned m = (unsigned)(x - bp);
       pg = m < (unsigned)kFcMirror ? mp_val[m] : c.free_pages[x];
     }
-    c.pages[s] = pg;
-    L.clock += 1;
-    c.last_hit[s] = (unsigned long long)L.clock;
-    c.pins[s] = 0;
-    c.nrows[s] = nr;
-    c.vocab[s] = vv;
-    c.nbytes[s] = bytes;
-    c.digest[s] = r.d;
-    {
-      const long long pos = L.ring_head & c.rmask;
-      c.ring_clock[pos] = (unsigned long long)L.clock;
-      c.ring_slot[pos] = s;
-      L.ring_head++;
-    }
-    L.total_bytes += bytes;
-    L.inserts += 1;
-    out_slot[i] = s;
-    out_gen[i] = g;
-    while (L.total_bytes > L.budget && L.alive > 1) {
+    wput(WRec{r.d, s, g, pg, i, r.nr, r.vv});
+    ++ni;
+    tot += r.nb;
+    while (tot > budget && alive > 1) {
       // next_victim over the start-of-batch candidates
       bool found = false;
       CandRec v;
@@ -1428,12 +1543,13 @@ __global__ void __launch_bounds__(128) commit_kernel(CacheDev c, const InsRec* _
           }
           ++ct;
           ci = 0;
+          const long long c0 = clock64();
           mbar_wait(&bars[2 + (ct & 1)], (ct >> 1) & 1);
+          cy_tile += clock64() - c0;
           ccnt = cnt_s[ct];
           continue;
         }
         v = cbuf[(ct & 1) * kFcTile + ci++];
-        L.ring_tail = tail0 + v.off + 1;
         if (is_gone(v.s)) continue;  // overwritten during the batch: its event died
         if (v.pins > 0) {            // pinned: to the side list (next_victim)
           if (L.side_count < c.side_cap) {
@@ -1449,46 +1565,66 @@ __global__ void __launch_bounds__(128) commit_kernel(CacheDev c, const InsRec* _
         break;
       }
       if (!found) {  // every scanned event consumed: the warp continues from the ring tail
-        L.ring_tail = lim;
         pend = 1;
         break;
       }
       // evict_entry
       set_gone(v.s);
       hlog[log_n++] = HashOp{v.dg, -1, 0};
-      L.total_bytes -= v.nb;
-      if (v.pg >= 0) {
-        c.pages[v.s] = -1;
-        ppush(v.pg);
-      }
+      tot -= v.nb;
+      if (v.pg >= 0) ppush(v.pg);
       spush(v.s, v.gen + 1u);
-      c.gen[v.s] = v.gen + 1u;
-      c.alive[v.s] = 0;
-      L.alive -= 1;
-      L.evictions += 1;
+      wput(WRec{0ull, v.s, v.gen + 1u, v.pg >= 0 ? 1 : 0, -1, 0, 0});
+      --alive;
+      ++ne;
     }
-    __threadfence_block();
-    s_flag[0] = log_n;
+    if ((i & 31) == 31) {  // publish every 32 inserts (the fence waits for this thread's stores)
+      __threadfence_block();
+      s_flag[0] = log_n;
+      s_flag[2] = wq;
+    }
     if (pend) {
       stop = i + 1;
       break;
     }
   }
+  // the ring tail: past the last candidate taken (every scanned event when they ran out)
+  if (pend) {
+    L.ring_tail = lim;
+  } else if (nct > 0 && ci > 0) {
+    L.ring_tail = tail0 + cbuf[(ct & 1) * kFcTile + ci - 1].off + 1;
+  } else if (nct > 0 && ct > 0) {  // (a tile boundary: the last record of the previous tile)
+    L.ring_tail = tail0 + (long long)ct * kFcTile;
+  }
+  L.total_bytes = tot;
+  L.alive = alive;
+  L.clock += ni;
+  L.ring_head += ni;
+  L.inserts += ni;
+  L.evictions += ne;
   // drain the tile loads still in flight (a CTA must not exit with bulk copies pending)
   for (int t = rt_waited + 1; t <= rt_issued; ++t) mbar_wait(&bars[t & 1], (t >> 1) & 1);
   for (int t = (nct > 0 ? ct : -1) + 1; t <= ct_issued; ++t) mbar_wait(&bars[2 + (t & 1)], (t >> 1) & 1);
+  // the mirrored stack ranges back to memory
+  for (int x = lo_s; x < min(bs + kFcMirror, L.free_slot_top); ++x) c.free_slots[x] = ms_val[x - bs];
+  for (int x = lo_p; x < min(bp + kFcMirror, L.free_page_top); ++x) c.free_pages[x] = mp_val[x - bp];
   *c.ctl = L;
   resume[0] = (int)stop;
   resume[1] = pend;
+  reinterpret_cast<unsigned long long*>(resume)[2] = globaltimer_ns();
+  reinterpret_cast<long long*>(resume)[4] = cy_wput;
+  reinterpret_cast<long long*>(resume)[5] = cy_drain;
+  reinterpret_cast<long long*>(resume)[6] = cy_tile;
+  reinterpret_cast<long long*>(resume)[7] = n_drain;
   __threadfence_block();
   s_flag[0] = log_n;
+  s_flag[2] = wq;
   s_flag[1] = 1;
 }
 
 __host__ __device__ constexpr size_t fc_smem_bytes(int ntiles, int E) {
-  return 64 + 2 * kFcTile * (sizeof(InsRec) + sizeof(CandRec)) + 32 * 32 * 12 + (size_t)kFcMirror * 12 +
-         (size_t)ntiles * 4 +
-         (size_t)((E + 31) / 32) * 4;
+  return 64 + 2 * kFcTile * (sizeof(InsRec) + sizeof(CandRec)) + kFcWRing * sizeof(WRec) + 32 * kFcWin * 12 +
+         (size_t)kFcMirror * 12 + (size_t)ntiles * 4 + (size_t)((E + 31) / 32) * 4;
 }
 
 // Copy the rows/tokens of inserts whose entry is still alive at the end of the batch.
@@ -1813,22 +1949,23 @@ static int insert_impl(lc_cache* c, const uint64_t* d_digests, const int32_t* d_
   const char* sp = getenv("LCB_SCALAR_POLICY");  // A/B hooks, read per call (tests switch them)
   const bool scalar = sp && atoi(sp) != 0;
   const char* fe = getenv("LCB_FAST_COMMIT");
-  const bool fast = !scalar && !d_keep && c->dev.maxp == 1 && n <= 65536 && c->dev.E <= (1 << 20) &&
+  long long mcap = 8 * n + 4096;
+  if (mcap > c->dev.R) mcap = c->dev.R;
+  mcap = (mcap + kFcTile - 1) / kFcTile * kFcTile;
+  const int ntiles = (int)(mcap / kFcTile);
+  const size_t smem = fc_smem_bytes(ntiles, c->dev.E);
+  const bool fast = !scalar && !d_keep && c->dev.maxp == 1 && n <= 65536 && smem <= 232448 &&
                     !(fe && atoi(fe) == 0);
   if (scalar) {
     insert_policy_scalar_kernel<<<1, 32, 0, st>>>(c->dev, d_digests, d_lengths, d_vocabs, n, d_slot, d_gen, d_keep,
                                                   d_keep_gen);
   } else if (fast) {
-    long long mcap = 8 * n + 4096;
-    if (mcap > c->dev.R) mcap = c->dev.R;
-    mcap = (mcap + kFcTile - 1) / kFcTile * kFcTile;
-    const int ntiles = (int)(mcap / kFcTile);
     const size_t nrec = (size_t)(n + kFcTile - 1) / kFcTile * kFcTile;
     const size_t o_cand = nrec * sizeof(InsRec);
     const size_t o_cnt = o_cand + (size_t)mcap * sizeof(CandRec);
     const size_t o_log = (o_cnt + (size_t)ntiles * 4 + 15) / 16 * 16;
     const size_t o_res = o_log + (size_t)(n + mcap) * sizeof(HashOp);
-    const size_t need = o_res + 16;
+    const size_t need = o_res + 64;  // resume[0..1] + commit start / commit end / log end (ns)
     if (need > c->fc_cap) {
       if (c->fc_buf) LCB_CUDA_TRY(cudaFree(c->fc_buf));
       c->fc_buf = nullptr;
@@ -1847,14 +1984,22 @@ static int insert_impl(lc_cache* c, const uint64_t* d_digests, const int32_t* d_
       LCB_CUDA_TRY(cudaFuncSetAttribute(commit_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 232448));
       smem_set = true;
     }
-    const size_t smem = fc_smem_bytes(ntiles, c->dev.E);
-    if (smem > 232448) return LC_E_CAPACITY;
     prep_keys_kernel<<<ceil_div(n * 8, 256), 256, 0, st>>>(c->dev, d_digests, d_lengths, d_vocabs, n, rec);
     prep_prev_kernel<<<ceil_div(n, 256), 256, 0, st>>>(d_digests, n, rec);
     prep_cand_kernel<<<ntiles, 256, 0, st>>>(c->dev, mcap, cand, cnt);
     commit_kernel<<<1, 128, smem, st>>>(c->dev, rec, n, cand, cnt, ntiles, mcap, hlog, d_slot, d_gen, resume);
     insert_policy_kernel<<<1, 32, 0, st>>>(c->dev, d_digests, d_lengths, d_vocabs, n, d_slot, d_gen, d_keep,
                                            d_keep_gen, resume);
+    if (getenv("LCB_FC_PROF")) {  // phase times of the fast commit (diagnostic, synchronises)
+      unsigned long long h[8];
+      LCB_CUDA_TRY(cudaMemcpyAsync(h, resume, sizeof(h), cudaMemcpyDeviceToHost, st));
+      LCB_CUDA_TRY(cudaStreamSynchronize(st));
+      fprintf(stderr,
+              "fast_commit n=%lld stop=%d pend=%d commit_us=%.1f log_us=%.1f wput_kcy=%.1f drain_kcy=%.1f (%llu) "
+              "tile_kcy=%.1f\n",
+              (long long)n, (int)(h[0] & 0xffffffffu), (int)(h[0] >> 32), (h[2] - h[1]) * 1e-3, (h[3] - h[1]) * 1e-3,
+              h[4] * 1e-3, h[5] * 1e-3, h[7], h[6] * 1e-3);
+    }
   } else {
     insert_policy_kernel<<<1, 32, 0, st>>>(c->dev, d_digests, d_lengths, d_vocabs, n, d_slot, d_gen, d_keep,
                                            d_keep_gen, nullptr);
