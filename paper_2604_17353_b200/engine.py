@@ -24,8 +24,9 @@ at once, entirely on the device:
 * every decode step is one ``lc_engine_decode_step`` launch (fold the previous
   token into the digest, produce the next row straight into the write-back
   entry's slab row -- f1: no staging buffer, no insert copy -- and emit its
-  resample task) plus one ``lc_cache_resample`` launch; the step loop can run
-  from a CUDA graph.
+  resample task) plus one ``lc_cache_resample`` launch; the step loop has no
+  host synchronisation and runs as ONE CUDA graph per wave (``LCB_ENGINE_GRAPH=0``:
+  eager launches).
 
 Semantics vs the reference's sequential calls: within a wave, all lookups happen
 before all write-backs (in request order), and the looked-up entries stay pinned
@@ -41,6 +42,7 @@ path; the pass counters follow engine.py:364-371.
 from __future__ import annotations
 
 import ctypes as C
+import os
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -313,7 +315,7 @@ class WaveEngine:
         if score_T is not None and cache is not None:  # f2 epilogue: score each new row while it is in L2
             pos_steps = (start[None, :] + torch.arange(n_steps, dtype=torch.int32, device=dev)[:, None]).contiguous()
 
-        def run():
+        def run(st):
             for s_, a in enumerate(steps):
                 _capi.check(_capi.lib.lc_engine_decode_step(cache.handle if cache else None, C.byref(a), st),
                             "lc_engine_decode_step")
@@ -329,4 +331,21 @@ class WaveEngine:
                                                               pos_steps[s_].data_ptr(), B, float(score_T), 0, st),
                                 "lc_cache_score_rows")
 
-        run()
+        if n_steps < 2 or os.environ.get("LCB_ENGINE_GRAPH", "1") == "0":
+            run(st)
+            return
+        # the step loop has no host synchronisation: capture it once and launch it as one graph, so
+        # a wave of small batches is not bound by ~2 host launches (+ memsets) per decode step
+        cur = torch.cuda.current_stream(dev)
+        cs = torch.cuda.Stream(dev)
+        cs.wait_stream(cur)
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.stream(cs):
+            g.capture_begin(capture_error_mode="thread_local")
+            try:
+                run(cs.cuda_stream)
+            finally:
+                g.capture_end()
+        cur.wait_stream(cs)
+        g.replay()
+        self._last_graph = g  # (alive until the next wave; generate_wave synchronises before returning)

@@ -39,8 +39,11 @@ def _engine(sc, **kw):
     return eng
 
 
+@pytest.mark.parametrize("graph", ["1", "0"])
 @pytest.mark.parametrize("name", [sc["name"] for sc in TRACES])
-def test_wave_engine_matches_reference_engine(name):
+def test_wave_engine_matches_reference_engine(name, graph, monkeypatch):
+    # graph "1": the decode loop runs as one CUDA graph per wave (default); "0": eager launches
+    monkeypatch.setenv("LCB_ENGINE_GRAPH", graph)
     sc = next(s for s in TRACES if s["name"] == name)
     eng = _engine(sc)
     for w, wave in enumerate(sc["waves"]):
