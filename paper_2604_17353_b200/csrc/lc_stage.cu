@@ -107,11 +107,14 @@ __device__ __forceinline__ void gbar(int g) { gbar_n<SG_GT>(g); }
 __device__ void sg_producer(const StageArgs& a, SgSmem& sm, int lane) {
   bool done = false;
   int sentinels = 0;
+  // tasks per grab: SG_PB on big batches; fewer when the batch gives each group only a few rows,
+  // so small launches (an engine decode step, a G = 8 rank's share) spread over every SM
+  const int pb = max(1, min(SG_PB, a.n_tasks / (int)(gridDim.x * SG_GROUPS * 4)));
   for (;;) {
     int nb = 0;
     if (!done) {
       int t0 = 0;
-      if (lane == 0) t0 = atomicAdd(a.next, SG_PB);
+      if (lane == 0) t0 = atomicAdd(a.next, pb);
       t0 = __shfl_sync(0xffffffffu, t0, 0);
       if (t0 >= a.n_tasks) {
         done = true;
@@ -119,7 +122,7 @@ __device__ void sg_producer(const StageArgs& a, SgSmem& sm, int lane) {
         const int t = t0 + lane;
         bool ok = false;
         TaskView tv;
-        if (lane < SG_PB && t < a.n_tasks) {
+        if (lane < pb && t < a.n_tasks) {
           const lc_task tk = a.tasks[t];
           if (tk.draw_end > tk.draw_begin) {
             const int Vt = tk.vocab > 0 ? tk.vocab : a.Vdef;

@@ -80,11 +80,14 @@ __device__ __forceinline__ void wbar(int g) { gbar_n<WG_GT>(g); }
 __device__ void wg_producer(const StageArgs& a, WgSmem& sm, int lane) {
   bool done = false;
   int sentinels = 0;
+  // tasks per grab: WG_PB on big batches; fewer when the batch gives each group only a few rows,
+  // so small launches (an engine decode step, a G = 8 rank's share) spread over every SM
+  const int pb = max(1, min(WG_PB, a.n_tasks / (int)(gridDim.x * WG_GROUPS * 4)));
   for (;;) {
     int nb = 0;
     if (!done) {
       int t0 = 0;
-      if (lane == 0) t0 = atomicAdd(a.next, WG_PB);
+      if (lane == 0) t0 = atomicAdd(a.next, pb);
       t0 = __shfl_sync(0xffffffffu, t0, 0);
       if (t0 >= a.n_tasks) {
         done = true;
@@ -92,7 +95,7 @@ __device__ void wg_producer(const StageArgs& a, WgSmem& sm, int lane) {
         const int t = t0 + lane;
         bool ok = false;
         TaskView tv;
-        if (lane < WG_PB && t < a.n_tasks) {
+        if (lane < pb && t < a.n_tasks) {
           const lc_task tk = a.tasks[t];
           if (tk.draw_end > tk.draw_begin) {
             const int Vt = tk.vocab > 0 ? tk.vocab : a.Vdef;

@@ -7,3 +7,4 @@ for gm in 1 0; do
  done
 done
 LCB_ENGINE_GRAPH=0 timeout 300 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $O/eng_launches.csv python tools/bench_engine.py --requests 256 --tokens 128 --waves 1 > $O/eng_ncu.log 2>&1
+LCB_FC_PROF=1 timeout 600 python bench.py --config c4 --no-cpu-baseline --no-check > $O/c4_fcprof.json 2> $O/c4_fcprof.err
