@@ -25,8 +25,10 @@ at once, entirely on the device:
   token into the digest, produce the next row straight into the write-back
   entry's slab row -- f1: no staging buffer, no insert copy -- and emit its
   resample task) plus one ``lc_cache_resample`` launch; the step loop has no
-  host synchronisation and runs as ONE CUDA graph per wave (``LCB_ENGINE_GRAPH=0``:
-  eager launches).
+  host synchronisation; with ``LCB_ENGINE_GRAPH=1`` it is captured once per wave
+  shape as a CUDA graph over engine-owned buffers and replayed by later waves of
+  that shape (off by default: at 256-1024 requests per wave the eager loop is as
+  fast, `profiles/r2_engine_graph_cache.jsonl`).
 
 Semantics vs the reference's sequential calls: within a wave, all lookups happen
 before all write-backs (in request order), and the looked-up entries stay pinned
@@ -124,6 +126,7 @@ class WaveEngine:
         self.cost = CostReport()
         self.agents: set[str] = set()
         self.generate_count = 0
+        self._graphs = {}  # wave shape -> (captured decode loop, its buffers, its closure)
         self.request_log: list[GenerateResult] = []
         self.hotspot_flags: list[torch.Tensor] = []  # per hotspot wave: selection flags (lc_cache_hotspots)
 
@@ -284,68 +287,102 @@ class WaveEngine:
 
     def _decode(self, B, L, n_steps, rep_h, used_h, digests, out, flags, seeds, T, K, P, wslot, wgen, staging,
                 score_T=None):
-        dev, V = self.dev, self.model.vocab_size
-        st = _dev.stream_ptr(dev)
+        dev = self.dev
+        cache = self.cache if wslot is not None else None
         start = torch.from_numpy(rep_h.astype(np.int32)).to(dev)
         u0 = torch.from_numpy(used_h.astype(np.int64)).to(dev)
+        io = dict(digests=digests, out=out, flags=flags, seeds=seeds, T=T, K=K, P=P, start=start, u0=u0)
+        if cache is not None:
+            io.update(wslot=wslot, wgen=wgen)
+        if n_steps < 2 or os.environ.get("LCB_ENGINE_GRAPH", "0") != "1":
+            self._decode_plan(B, L, n_steps, io, cache, staging, score_T)(_dev.stream_ptr(dev))
+            return
+        # The step loop has no host synchronisation: it is captured ONCE per wave shape into a CUDA
+        # graph over engine-owned buffers, and each later wave of that shape copies its inputs in,
+        # replays (one launch for fold + n_steps x (decode, resample)), and copies tokens / flags out.
+        key = (B, L, n_steps, bool(staging), score_T, cache.epoch if cache is not None else None)
+        ent = self._graphs.pop(key, None)
+        if ent is None:
+            bufs = {k: torch.empty_like(v) for k, v in io.items()}
+            cur = torch.cuda.current_stream(dev)
+            cs = torch.cuda.Stream(dev)
+            cs.wait_stream(cur)
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.stream(cs):
+                run = self._decode_plan(B, L, n_steps, bufs, cache, staging, score_T, own_workspace=True)
+                g.capture_begin(capture_error_mode="thread_local")
+                try:
+                    run(cs.cuda_stream)
+                finally:
+                    g.capture_end()
+            cur.wait_stream(cs)
+            ent = (g, bufs, run)
+            while len(self._graphs) >= 8:
+                self._graphs.pop(next(iter(self._graphs)))
+        self._graphs[key] = ent  # (most recently used last)
+        g, bufs, _ = ent
+        for k, v in io.items():
+            bufs[k].copy_(v, non_blocking=True)
+        g.replay()
+        out.copy_(bufs["out"], non_blocking=True)
+        flags.copy_(bufs["flags"], non_blocking=True)
+
+    def _decode_plan(self, B, L, n_steps, io, cache, staging, score_T, own_workspace=False):
+        """The decode loop over the device buffers ``io`` as a function of the stream: the digest
+        fold of prompt + replayed tokens, then per step one ``lc_engine_decode_step`` and one
+        resample launch (+ the hotspot score epilogue).  Its scratch lives in the returned closure."""
+        dev, V = self.dev, self.model.vocab_size
+        start, u0, out, flags = io["start"], io["u0"], io["out"], io["flags"]
         dig = [torch.empty(B, dtype=torch.int64, device=dev), torch.empty(B, dtype=torch.int64, device=dev)]
-        # digest of prompt + out[:replayed] (engine.py:337: prefill of prompt + out)
-        _capi.check(_capi.lib.lc_engine_fold(digests.data_ptr(), out.data_ptr(), L, start.data_ptr(), B,
-                                             dig[0].data_ptr(), st), "lc_engine_fold")
-        cache = self.cache if wslot is not None else None
         sdt = _capi.LC_F32 if self.dtype == "float32" else _capi.LC_BF16
         stg = None
         if staging:
             stg = torch.empty((B, V), dtype=torch.float32 if sdt == _capi.LC_F32 else torch.bfloat16, device=dev)
         tasks = torch.empty(B * _capi.TASK_DTYPE.itemsize, dtype=torch.uint8, device=dev)
-        ws = sampling._workspace(dev).get(B, V)
-        draws = _capi.LcDraws(None, seeds.data_ptr(), None, out.data_ptr(), flags.data_ptr(), None, None, None)
+        if own_workspace:  # (the shared workspace may be reallocated by later calls)
+            ws = torch.empty(int(_capi.lib.lc_resample_workspace_bytes(B, V)), dtype=torch.uint8, device=dev)
+        else:
+            ws = sampling._workspace(dev).get(B, V)
+        draws = _capi.LcDraws(None, io["seeds"].data_ptr(), None, out.data_ptr(), flags.data_ptr(), None, None, None)
+        wslot = io.get("wslot")
+        wgen = io.get("wgen")
         m = self.model
         steps = []
         for s in range(n_steps):
             a = _capi.LcDecodeStep(B, V, L, s, sdt, m.seed & mixing.MASK64, float(m.concentration),
                                    float(m.logit_range), start.data_ptr(), u0.data_ptr(), dig[s & 1].data_ptr(),
                                    dig[(s + 1) & 1].data_ptr(), out.data_ptr(),
-                                   wslot.data_ptr() if cache else None, wgen.data_ptr() if cache else None,
-                                   T.data_ptr(), K.data_ptr(), P.data_ptr(), stg.data_ptr() if stg is not None else None,
-                                   V, tasks.data_ptr())
+                                   wslot.data_ptr() if cache is not None else None,
+                                   wgen.data_ptr() if cache is not None else None,
+                                   io["T"].data_ptr(), io["K"].data_ptr(), io["P"].data_ptr(),
+                                   stg.data_ptr() if stg is not None else None, V, tasks.data_ptr())
             steps.append(a)
-
         pos_steps = None
         if score_T is not None and cache is not None:  # f2 epilogue: score each new row while it is in L2
-            pos_steps = (start[None, :] + torch.arange(n_steps, dtype=torch.int32, device=dev)[:, None]).contiguous()
+            pos_steps = torch.empty((n_steps, B), dtype=torch.int32, device=dev)
+            steps_ar = torch.arange(n_steps, dtype=torch.int32, device=dev)
+        # (``cache is not None``, never ``if cache``: LogitsCache.__len__ reads the device counters)
+        hnd = cache.handle if cache is not None else None
+        digests = io["digests"]
 
         def run(st):
+            # digest of prompt + out[:replayed] (engine.py:337: prefill of prompt + out)
+            _capi.check(_capi.lib.lc_engine_fold(digests.data_ptr(), out.data_ptr(), L, start.data_ptr(), B,
+                                                 dig[0].data_ptr(), st), "lc_engine_fold")
+            if pos_steps is not None:  # (st is the current stream, eager or capturing)
+                torch.add(start[None, :], steps_ar[:, None], out=pos_steps)
             for s_, a in enumerate(steps):
-                _capi.check(_capi.lib.lc_engine_decode_step(cache.handle if cache else None, C.byref(a), st),
-                            "lc_engine_decode_step")
+                _capi.check(_capi.lib.lc_engine_decode_step(hnd, C.byref(a), st), "lc_engine_decode_step")
                 if stg is None:
-                    rc = _capi.lib.lc_cache_resample(cache.handle, tasks.data_ptr(), B, draws, ws.data_ptr(),
-                                                     ws.numel(), None, st)
+                    rc = _capi.lib.lc_cache_resample(hnd, tasks.data_ptr(), B, draws, ws.data_ptr(), ws.numel(),
+                                                     None, st)
                 else:
                     rc = _capi.lib.lc_resample(stg.data_ptr(), sdt, V, V, tasks.data_ptr(), B, draws, ws.data_ptr(),
                                                ws.numel(), None, st)
                 _capi.check(rc, "lc_resample")
                 if pos_steps is not None:
-                    _capi.check(_capi.lib.lc_cache_score_rows(cache.handle, wslot.data_ptr(), wgen.data_ptr(),
+                    _capi.check(_capi.lib.lc_cache_score_rows(hnd, wslot.data_ptr(), wgen.data_ptr(),
                                                               pos_steps[s_].data_ptr(), B, float(score_T), 0, st),
                                 "lc_cache_score_rows")
 
-        if n_steps < 2 or os.environ.get("LCB_ENGINE_GRAPH", "1") == "0":
-            run(st)
-            return
-        # the step loop has no host synchronisation: capture it once and launch it as one graph, so
-        # a wave of small batches is not bound by ~2 host launches (+ memsets) per decode step
-        cur = torch.cuda.current_stream(dev)
-        cs = torch.cuda.Stream(dev)
-        cs.wait_stream(cur)
-        g = torch.cuda.CUDAGraph()
-        with torch.cuda.stream(cs):
-            g.capture_begin(capture_error_mode="thread_local")
-            try:
-                run(cs.cuda_stream)
-            finally:
-                g.capture_end()
-        cur.wait_stream(cs)
-        g.replay()
-        self._last_graph = g  # (alive until the next wave; generate_wave synchronises before returning)
+        return run

@@ -199,6 +199,7 @@ class LogitsCache:
         h = C.c_void_p()
         _capi.check(_capi.lib.lc_cache_create(C.byref(cfg), C.byref(h)), "lc_cache_create")
         self.handle = h
+        self.epoch = getattr(self, "epoch", 0) + 1  # (a new device cache: captured launches are stale)
         self.vocab = V
         self.page_rows = page_rows
         self.max_pages = max_pages

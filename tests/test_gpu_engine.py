@@ -162,3 +162,29 @@ def test_wave_rejects_duplicate_keys_and_mixed_policies():
         eng.generate(GenerateRequest("b", [1], c))
     with pytest.raises(lcb.ConfigError):
         eng.generate(GenerateRequest("a", [64], c))
+
+
+def test_decode_graph_reuse_equals_eager(monkeypatch):
+    """Waves of one shape replay the captured decode loop (one graph per shape) and give the
+    eager loop's tokens, outcomes and cache entries."""
+    model = ModelConfig(seed=11, vocab_size=512, concentration=2.0, logit_range=4.0)
+    prompts = [[1 + r, 2 + r % 7, 3] for r in range(48)]
+    res = {}
+    for mode in ("1", "0"):
+        monkeypatch.setenv("LCB_ENGINE_GRAPH", mode)
+        eng = WaveEngine(model, 1 << 28, max_tokens=24, device=DEV)
+        eng.register_agent("a")
+        got = []
+        for w in range(4):
+            reqs = [GenerateRequest("a", p, lcb.SamplingConfig(temperature=0.8, top_p=0.9, max_tokens=24,
+                                                               seed=1000 * w + r),
+                                    lcb.ReplayPolicy.STEP_WISE if w % 2 == 0 else lcb.ReplayPolicy.NONE,
+                                    request_id=f"{w}-{r}")
+                    for r, p in enumerate(prompts)]
+            got.append([(g.tokens, g.outcome.replayed_len, g.outcome.diverged_at, g.flags)
+                        for g in eng.generate_wave(reqs)])
+        ents = {d: (e.token_seq, np.asarray(e.logits_seq, np.float32).tobytes()) for d, e in eng.cache.entries.items()}
+        res[mode] = (got, ents, len(eng._graphs))
+    assert res["1"][0] == res["0"][0]
+    assert res["1"][1] == res["0"][1]
+    assert 1 <= res["1"][2] <= 4 and res["0"][2] == 0

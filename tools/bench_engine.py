@@ -82,7 +82,7 @@ def main():
                           "replayed_tokens": replayed, "decode_passes": decoded,
                           "position_hit_ratio": replayed / rev_tok if rev_tok else None},
         "forward_passes": {"prefill": eng.cost.prefill_passes, "decode": eng.cost.decode_passes},
-        "decode_loop": "eager launches" if os.environ.get("LCB_ENGINE_GRAPH", "1") == "0" else "one CUDA graph per wave",
+        "decode_loop": "one CUDA graph per wave" if os.environ.get("LCB_ENGINE_GRAPH", "0") == "1" else "eager launches",
         "note": "synthetic model (the reference producer), one device; timings include generate_wave's host "
                 "synchronisation and result lists (the public call)",
     }

@@ -1,5 +1,9 @@
-cd $GRAFT_REPO_ROOT
+#!/bin/bash
+# Wave engine: GPU tests (reference-engine traces, eager and graph), throughput with the decode loop
+# eager / replayed from the per-shape graph cache, and the launch list of one eager wave.
+cd "$GRAFT_REPO_ROOT"
 O=gpurun_out
+mkdir -p $O
 timeout 600 python -m pytest tests/test_gpu_engine.py -q > $O/pytest_engine.log 2>&1; echo "rc=$?" >> $O/pytest_engine.log
 for gm in 1 0; do
  for sh in "256 128" "1024 64"; do set -- $sh
@@ -7,4 +11,3 @@ for gm in 1 0; do
  done
 done
 LCB_ENGINE_GRAPH=0 timeout 300 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $O/eng_launches.csv python tools/bench_engine.py --requests 256 --tokens 128 --waves 1 > $O/eng_ncu.log 2>&1
-LCB_FC_PROF=1 timeout 600 python bench.py --config c4 --no-cpu-baseline --no-check > $O/c4_fcprof.json 2> $O/c4_fcprof.err
