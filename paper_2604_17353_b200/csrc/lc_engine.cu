@@ -27,7 +27,7 @@ __global__ void engine_fold_kernel(const uint64_t* __restrict__ din, const int32
   dout[r] = h;
 }
 
-// grid (chunks, B): block (x, r) fills ids [x*chunk, (x+1)*chunk) of request r's row; every
+// grid (ceil(V / chunk), B): the x blocks of request r fill its row together; every
 // block of a row recomputes the (one-fold) digest, block x == 0 publishes it and the task.
 template <typename OutT>
 __global__ void engine_decode_kernel(CacheDev c, bool cache_rows, lc_decode_step a, int64_t chunk) {
@@ -69,12 +69,11 @@ __global__ void engine_decode_kernel(CacheDev c, bool cache_rows, lc_decode_step
   const float boost = (float)__dmul_rn(a.concentration, a.logit_range);
   OutT* so = a.d_staging ? reinterpret_cast<OutT*>(a.d_staging) + r * a.staging_stride : nullptr;
   OutT* co = live ? reinterpret_cast<OutT*>(c.slab) + srow * (int64_t)c.V : nullptr;
-  const int64_t v1 = min((int64_t)a.vocab, (blockIdx.x + 1) * chunk);
-  for (int64_t v = blockIdx.x * chunk + threadIdx.x; v < v1; v += blockDim.x) {
-    const OutT x = producer_value<OutT>(st, v, peak, boost, a.logit_range);
-    if (so) so[v] = x;
-    if (co) co[v] = x;
-  }
+  // the row's blocks stride over it in groups of 8 ids (one 16-byte store per 8 bf16, the stream
+  // counter advanced by adds: produce_row, bit-identical to producer_value)
+  const int64_t t0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x, nt = (int64_t)gridDim.x * blockDim.x;
+  if (co) produce_row<OutT>(co, a.vocab, st, peak, boost, a.logit_range, t0, nt);
+  if (so) produce_row<OutT>(so, a.vocab, st, peak, boost, a.logit_range, t0, nt);
 }
 
 }  // namespace lcb
