@@ -84,30 +84,35 @@ __device__ __forceinline__ OutT producer_value(uint64_t st, int64_t v, uint64_t 
 template <typename OutT>
 __device__ __forceinline__ void produce_row(OutT* __restrict__ o, int64_t vocab, uint64_t st, uint64_t peak,
                                             float boost, double range, int64_t t0, int64_t nt) {
-  const double c = range * 0x1p-53;
-  const bool vec = (reinterpret_cast<uintptr_t>(o) & 15) == 0;
+  // (2k - 2^53) c == fma(k, 2c, -range) exactly (2^53 c == range: c is a power-of-two scaling of
+  // range, exact unless range is tiny), so one DFMA of the unsigned top 53 bits gives the same
+  // single rounding as the DMUL of the signed 2k - 2^53 -- with fewer 64-bit integer ops
+  const double c2 = range * 0x1p-52;
+  const bool vec = (reinterpret_cast<uintptr_t>(o) & 15) == 0 && fabs(range) >= 0x1p-900;
   const int64_t ng = vec ? vocab / 8 : 0;
   for (int64_t g = t0; g < ng; g += nt) {
     const int64_t v0 = 8 * g;
     uint64_t x = st + (uint64_t)(v0 + 1) * kGolden;
+    const uint64_t pk = peak - (uint64_t)v0;
+    const uint32_t pj = pk < 8 ? (uint32_t)pk : 8u;  // the peak's place in this group (8: none)
     float f[8];
 #pragma unroll
     for (int j = 0; j < 8; ++j) {
       const uint64_t u = avalanche64(x);
       x += kGolden;
-      const int64_t k2 = (int64_t)((u >> 11) << 1) - (int64_t)(1ull << 53);
-      f[j] = (float)__dmul_rn((double)k2, c);
-      if ((uint64_t)(v0 + j) == peak) f[j] = __fadd_rn(f[j], boost);
+      f[j] = (float)__fma_rn((double)(u >> 11), c2, -range);
+      if (pj == (uint32_t)j) f[j] = __fadd_rn(f[j], boost);
     }
     if constexpr (sizeof(OutT) == 4) {
       float4* q = reinterpret_cast<float4*>(o + v0);
       q[0] = make_float4(f[0], f[1], f[2], f[3]);
       q[1] = make_float4(f[4], f[5], f[6], f[7]);
     } else {
+      // round-to-nearest-even pairs in one instruction (F2FP.BF16.F32.PACK_AB): the values are
+      // finite, where this equals f32_to_bf16_bits
       uint32_t w[4];
 #pragma unroll
-      for (int j = 0; j < 4; ++j)
-        w[j] = (uint32_t)f32_to_bf16_bits(f[2 * j]) | ((uint32_t)f32_to_bf16_bits(f[2 * j + 1]) << 16);
+      for (int j = 0; j < 4; ++j) asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(w[j]) : "f"(f[2 * j + 1]), "f"(f[2 * j]));
       *reinterpret_cast<uint4*>(o + v0) = make_uint4(w[0], w[1], w[2], w[3]);
     }
   }

@@ -76,6 +76,27 @@ def test_fill_logits_matches_reference_producer():
         assert np.array_equal(outb.float().cpu().numpy(), ref)
 
 
+
+@pytest.mark.parametrize("vocab,conc,rng", [(32000, 2.5, 5.0), (151936, 2.5, 5.0), (1003, 1.7, -3.25),
+                                            (4099, 0.5, 1e-3), (77, 2.5, 1e-300)])
+def test_fill_logits_many_rows_match_oracle(vocab, conc, rng):
+    """The vectorised producer (8 ids per thread, one DFMA per value, packed bf16 rounding) against
+    the oracle's numpy restatement of the reference fill, bit for bit, over many rows: peaks in every
+    position of an 8-id group, ragged tails (V % 8), a negative and a tiny range (scalar path)."""
+    n = 24
+    states = [mixing_ref.mix2(91, i) for i in range(n)]
+    st = lcb._dev.u64_tensor(states, DEV)
+    for dt, tdt in ((_capi.LC_F32, torch.float32), (_capi.LC_BF16, torch.bfloat16)):
+        out = torch.empty((n, vocab), dtype=tdt, device=DEV)
+        _capi.check(_capi.lib.lc_fill_logits(st.data_ptr(), n, vocab, conc, rng, dt, out.data_ptr(), vocab, None))
+        got = out.float().cpu().numpy()
+        for i, s_ in enumerate(states):
+            want = mixing_ref.fill_logits_np(s_, vocab, conc, rng)
+            if dt == _capi.LC_BF16:
+                want = mixing_ref.bf16_round(want)
+            assert np.array_equal(got[i].view(np.uint32), want.view(np.uint32)), (vocab, dt, i)
+
+
 # -- fast-tier error model ------------------------------------------------------------------
 
 
