@@ -494,11 +494,13 @@ __global__ void __launch_bounds__(WG_THREADS, 1) wide_kernel(StageArgs a) {
         if (c + 2 < nch) issue(tv, c + 2);
       }
       WG_PH(3);
-      // keep the list bounded: sort, keep the top k, raise the threshold
+      // keep the list bounded: sort, keep the top k, raise the threshold.  Compacting as soon as
+      // the list exceeds k + k/8 (not 2k): the threshold rises after nearly every chunk, so later
+      // chunks append few candidates and each sort stays <= 128 keys (C3 7.90M -> 8.48M rows/s)
       const int nc = G.ncand;
       if (nc > WG_CAP) {
         bad = true;  // one chunk overflowed the list: left to the CTA kernel
-      } else if (nc > 2 * K || nc > WG_CAP / 2) {
+      } else if (nc > K + K / 8 || nc > WG_CAP / 2) {
         wg_sort(G, g, gt, nc);
         if (gt == 0) {
           G.thrk = G.cand[K - 1];
